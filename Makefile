@@ -21,3 +21,28 @@ clean:
 	rm -rf oracle/lib paper_2302_13431_b200/lib build
 
 .PHONY: all oracle clean
+
+# ---- product library (CUDA sm_100a)
+PKG       := paper_2302_13431_b200
+CU_SRC    := $(PKG)/csrc/sk_axis.cu $(PKG)/csrc/sk_gram.cu $(PKG)/csrc/sk_fold.cu $(PKG)/csrc/sk_power.cu \
+             $(PKG)/csrc/sk_misc.cu $(PKG)/csrc/sk_runtime.cu
+CU_HDR    := $(PKG)/csrc/sk_internal.h include/senskit_b200.h
+CU_OBJ    := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(CU_SRC))
+PROD_LIB  := $(PKG)/lib/libsenskit_b200.so
+NVFLAGS   := -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC \
+             --expt-relaxed-constexpr -Iinclude
+
+all: product
+
+product: $(PROD_LIB)
+
+build/%.o: $(PKG)/csrc/%.cu $(CU_HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(PROD_LIB): $(CU_OBJ)
+	@mkdir -p $(PKG)/lib
+	$(NVCC) -shared -gencode arch=compute_100a,code=sm_100a $(CU_OBJ) -o $@ \
+	  -L$(CUDA_HOME)/lib64 -lcusolver -lcublas -lcudart -Xlinker -rpath=$(CUDA_HOME)/lib64
+
+.PHONY: product

@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark: sensitivity-map voxels/s end to end (BASELINE.json metric).
+
+Workload (N=1): BASELINE.json configs[1] = C2 — 2D 256x256, Q=32 coils,
+calibration 32x32, ellipsoidal kernel tau=5, nullspace threshold 0.05,
+full-resolution G(x), 50 power iterations.  A step is one estimate_maps call
+(pisco preset: Gram -> nullspace -> G(x) -> power iteration -> normalise/mask)
+on one synthetic, seeded calibration.  C2 is a single slice, so it does not
+shard: under torchrun every rank runs an independent replica ("replicas only",
+weak scaling) and `value` = all ranks' voxels / max-over-ranks device time.
+
+Legs:
+  value     inputs resident in HBM, outputs to HBM buffers, CUDA events on
+            the library stream (set to torch's current stream), L2 flushed
+            between steps by a 256 MiB write (untimed).
+  e2e       the same call through the public C-ABI with pinned HOST buffers:
+            calibration H2D + maps/lambda/mask D2H inside the timed region.
+  cpu_baseline  the FP64 oracle (C++ restatement of the reference, its own
+            std::thread parallel_for, single-threaded LAPACK eigensolve as the
+            reference's Eigen) on rank 0 at N=1, one full C2 pipeline.
+`--impl reference` times that oracle as the reference arm.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sensitivity-map voxels/s end-to-end"
+UNIT = "voxels/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--seed", type=int, default=1234)
+    return ap.parse_args()
+
+
+def workload(spec):
+    return (f"{spec.name}: {'x'.join(map(str, spec.full_dims))} Q={spec.channels} calib "
+            f"{'x'.join(map(str, spec.calib))} ellipsoid tau={spec.tau} grid {'x'.join(map(str, spec.grid_dims))} "
+            f"iters={spec.power_iters} slices={spec.slices}")
+
+
+def output_voxels(spec):
+    return int(np.prod(spec.full_dims)) * spec.slices
+
+
+def k4_flops(spec):
+    n = int(np.prod(spec.grid_dims))
+    q = spec.channels
+    return n * (spec.power_iters * (8 * q * q + 8 * q) + 8 * q * q + 8 * q)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(smax)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def oracle_run(case, threads=None):
+    """One full reference-algorithm pipeline on the host (the CPU baseline)."""
+    from oracle import oracle as O
+    spec = case.spec
+    if threads:
+        O.set_max_threads(threads)
+    co = O.PipelineConfig.pisco()
+    co.kernel, co.tau, co.power_iters = spec.kernel, spec.tau, spec.power_iters
+    co.nullspace_threshold = spec.nullspace_threshold
+    if spec.full_grid:
+        co.grid = O.GRID_FULL
+    else:
+        co.grid_pad = spec.grid_dims[0] - spec.calib[0]
+    t0 = time.perf_counter()
+    for s in range(case.calib.shape[0]):
+        res = O.estimate_maps(O.Calib(case.calib[s].astype(np.complex128), case.center_offset), spec.full_dims, co,
+                              grid_dims=None if spec.full_grid or spec.ndim < 3 else spec.grid_dims)
+    dt = time.perf_counter() - t0
+    return dt, res, O.max_threads()
+
+
+def reference_arm(args, spec, rank, world):
+    from paper_2302_13431_b200 import phantom
+    if rank != 0:
+        return
+    case = phantom.generate(args.config, seed=args.seed)
+    steps = max(1, min(args.steps, 2))
+    warm = min(args.warmup, 0)
+    for _ in range(warm):
+        oracle_run(case)
+    times = []
+    threads = None
+    for _ in range(steps):
+        dt, _, threads = oracle_run(case)
+        times.append(dt)
+    t = float(np.mean(times))
+    vox = output_voxels(spec)
+    value = vox / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+        "warmup": warm, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128 (fp64 complex)", "data": "synthetic (seeded phantom/coil generator, paper_2302_13431_b200/phantom.py)",
+        "config": {"workload": workload(spec)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{steps} full {args.config} pipeline(s) ({vox} output voxels each); parallel_for on "
+                                   f"{threads} threads, LAPACK zheevd/zgemm single-threaded as the reference's Eigen"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2302_13431_b200 import phantom
+    spec = phantom.CONFIGS[args.config]
+    if args.impl == "reference":
+        reference_arm(args, spec, rank, world)
+        return
+
+    import torch
+    import paper_2302_13431_b200 as K
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    case = phantom.generate(args.config, seed=args.seed + rank)
+    q = spec.channels
+    full = spec.full_dims
+    nfull = int(np.prod(full))
+    cfg = K.PipelineConfig(kernel=spec.kernel, tau=spec.tau, nullspace_threshold=spec.nullspace_threshold,
+                           power_iters=spec.power_iters, grid=K.GRID_FULL if spec.full_grid else K.GRID_REDUCED,
+                           grid_pad=spec.grid_dims[0] - spec.calib[0],
+                           grid_dims=spec.grid_dims if spec.ndim == 3 else None)
+    ctx = K.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+
+    slices = case.calib.shape[0]
+    d_cal = torch.from_numpy(case.calib).to("cuda")
+    d_maps = torch.empty((slices, q) + tuple(full), dtype=torch.complex64, device="cuda")
+    d_lam = torch.empty((slices,) + tuple(full), dtype=torch.float32, device="cuda")
+    d_mask = torch.empty((slices,) + tuple(full), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    cal_stride = d_cal[0].numel() * 8
+
+    def step_device():
+        provs = []
+        for s in range(slices):
+            provs.append(K.api.estimate_maps_device(
+                ctx, d_cal.data_ptr() + s * cal_stride, spec.calib, case.center_offset, q, full, cfg,
+                d_maps[s].data_ptr(), d_lam[s].data_ptr(), d_mask[s].data_ptr()))
+        return provs
+
+    def timed(fn, k, flush_l2=True):
+        total = 0.0
+        stages = np.zeros(5)
+        for _ in range(k):
+            if flush_l2:
+                flush.fill_(1.0)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            provs = fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            total += e0.elapsed_time(e1)
+            for p in provs or []:
+                stages += np.array(list(p.stage_ms))
+        return total, stages / max(k, 1)
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = ctx.launches
+    lib0 = ctx.library_calls
+    total_ms, stages = timed(step_device, args.steps)
+    launches = ctx.launches - l0
+    libcalls = ctx.library_calls - lib0
+    clk = clocks.stop()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    vox = output_voxels(spec) * world
+    value = vox / (ms_per_step / 1e3)
+
+    # ---- e2e through the public API with pinned host buffers
+    h_cal = torch.from_numpy(case.calib).pin_memory()
+    h_maps = torch.empty((slices, q) + tuple(full), dtype=torch.complex64).pin_memory()
+    h_lam = torch.empty((slices,) + tuple(full), dtype=torch.float32).pin_memory()
+    h_mask = torch.empty((slices,) + tuple(full), dtype=torch.uint8).pin_memory()
+
+    def step_host():
+        provs = []
+        for s in range(slices):
+            provs.append(K.api.estimate_maps_device(
+                ctx, h_cal.data_ptr() + s * cal_stride, spec.calib, case.center_offset, q, full, cfg,
+                h_maps[s].data_ptr(), h_lam[s].data_ptr(), h_mask[s].data_ptr()))
+        return provs
+
+    step_host()
+    e2e_steps = max(3, min(args.steps, 10))
+    e2e_ms, _ = timed(step_host, e2e_steps)
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = vox / (e2e_ms / e2e_steps / 1e3)
+    assert np.array_equal(h_mask.numpy(), d_mask.cpu().numpy()), "host/device legs disagree"
+
+    peaks, peak_src = load_peaks()
+    props = torch.cuda.get_device_properties(local)
+    fp32_peak = props.multi_processor_count * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    k4_ms = stages[3]
+    achieved = k4_flops(spec) / (k4_ms / 1e3) / 1e12 if k4_ms > 0 else 0.0
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("power_kernel", {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c64 (fp32 complex); Gram eigensolve fp64",
+        "data": "synthetic (seeded phantom/coil generator, paper_2302_13431_b200/phantom.py)",
+        "config": {"workload": workload(spec), "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "flushed between steps (256 MiB write, untimed)", "output_voxels_per_rank": output_voxels(spec)},
+        "stages_ms": dict(zip(("gram", "nullspace", "field", "eigensolve", "post"), [round(x, 4) for x in stages])),
+        "roofline": {"kernel": "power_kernel (K4)", "bound": "fp32", "achieved": achieved, "peak": fp32_peak,
+                     "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None, "traffic": traffic,
+                     "peak_source": f"SMs x 128 FP32 lanes x 2 x sm_max_mhz ({peak_src} MEASURED_PEAKS sm_max_mhz)",
+                     "flops_per_launch": k4_flops(spec)},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h_cal.numel() * 8),
+                "d2h_bytes_per_step": int(h_maps.numel() * 8 + h_lam.numel() * 4 + h_mask.numel())},
+        "gpu_launches": int(launches), "library_calls": int(libcalls),
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        dt, _, threads = oracle_run(case)
+        line["cpu_baseline"] = {"value": output_voxels(spec) / dt, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"one full {args.config} pipeline ({output_voxels(spec)} voxels, {dt:.1f} s); "
+                                          "LAPACK single-threaded as the reference's Eigen"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

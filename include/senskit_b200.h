@@ -1,0 +1,174 @@
+/* senskit_b200 — C-ABI drop-in for the reference `senskit` PISCO hot path.
+ *
+ * Every entry point replaces one reference C++ function (cited per
+ * declaration, paths relative to the reference's proj/).  Plain pointers and
+ * sizes only; no torch or CUDA types cross this boundary.
+ *
+ * Buffers: every array argument may be a HOST pointer (pageable or pinned) or
+ * a DEVICE pointer on the context's GPU; the library detects which with
+ * cudaPointerGetAttributes and copies as needed.  Complex arrays are
+ * interleaved float32 (sk_c64), matching the reference's CStack v1 on-disk
+ * format (io.hpp:9-16); layouts are the reference's:
+ *   stacks      channel-major, row-major voxels:   data[q*N + j]   (types.hpp:58-74)
+ *   matrices    column-major (Eigen default):      m[r + c*rows]
+ *   GramField   voxel-major, column-major Q x Q:   v[j*Q*Q + c*Q + r] (spatial_gram.hpp:36-51)
+ *
+ * Every call is synchronous at return (the reference's calls block).  One
+ * context per GPU; a context is not re-entrant.
+ *
+ * Return codes mirror the reference CLI contract (tools/senskit_main.cpp:23-27)
+ * for the error classes the reference throws (types.hpp:22-32):
+ */
+#ifndef SENSKIT_B200_H
+#define SENSKIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SK_OK = 0,
+  SK_ERR_OTHER = 1,           /* std::runtime_error                                */
+  SK_ERR_IO = 3,              /* IoError                                           */
+  SK_ERR_NULLSPACE_EMPTY = 4, /* NullspaceEmptyError (nullspace.cpp:29-31)          */
+  SK_ERR_DIM = 5,             /* DimError                                          */
+  SK_ERR_LENGTH = 6,          /* std::length_error (field byte cap)                */
+  SK_ERR_CUDA = 7,            /* CUDA / cuSOLVER / cuBLAS failure                  */
+  SK_ERR_OOM = 8,             /* device allocation failed                          */
+  SK_ERR_UNSUPPORTED = 9      /* configuration outside the B200 path */
+};
+
+typedef struct { float re, im; } sk_c64;
+typedef struct sk_ctx sk_ctx;
+
+/* PipelineConfig (maps.hpp:23-45).  Only the `pisco` arm is implemented on
+ * the GPU: gram = fft, eig = power, field = fast (others -> SK_ERR_UNSUPPORTED).
+ * grid_dims: explicit map grid (all > 0) overrides grid/grid_pad, which is
+ * how the reference drives anisotropic grids (pipeline::compute_field /
+ * finalize with explicit dims, maps.hpp:115-123). */
+typedef struct {
+  int32_t kernel;             /* 0 rect, 1 ellipsoid        maps.hpp:24 */
+  int32_t tau;                /*                            maps.hpp:25 */
+  int32_t gram;               /* 0 explicit, 1 fft          maps.hpp:26 */
+  double nullspace_threshold; /*                            maps.hpp:27 */
+  int32_t grid;               /* 0 full, 1 reduced          maps.hpp:28 */
+  int64_t grid_pad;           /*                            maps.hpp:29 */
+  int32_t eig;                /* 0 dense, 1 power           maps.hpp:30 */
+  int32_t power_iters;        /*                            maps.hpp:31 */
+  int32_t method;             /* 0 nullspace, 1 espirit     maps.hpp:32 */
+  int32_t field;              /* 0 naive, 1 fast            maps.hpp:33 */
+  double mask_threshold;      /*                            maps.hpp:37 */
+  double apod_width;          /*                            maps.hpp:40 */
+  int64_t grid_dims[3];       /* explicit map grid or zeros */
+} sk_config;
+
+/* Provenance (maps.hpp:55-73) with device-timed stages. */
+typedef struct {
+  int64_t grid_dims[3];
+  int64_t support_size;
+  int64_t valid_shifts;
+  int64_t nullspace_rank;
+  int64_t zeroed_voxels;
+  double sigma1;
+  double cut_margin;   /* min over sigma of |sigma/cut - 1|: how far R is from flipping */
+  double stage_ms[5];  /* gram, nullspace, field, eigensolve, post (CUDA events) */
+  double total_ms;     /* device time of the whole call */
+} sk_provenance;
+
+/* ------------------------------------------------------------- context */
+int sk_create(int device, sk_ctx** out);
+int sk_destroy(sk_ctx* ctx);
+/* Use a caller-owned cudaStream_t (passed as void*); NULL restores the
+ * context's own stream. */
+int sk_set_stream(sk_ctx* ctx, void* stream);
+const char* sk_last_error(void);
+/* Kernels launched by this context since creation (our sm_100a kernels), and
+ * cuSOLVER / cuBLAS calls made (the eigensolve and Hermitian rank-k update). */
+int64_t sk_kernel_launches(const sk_ctx* ctx);
+int64_t sk_library_calls(const sk_ctx* ctx);
+
+/* ------------------------------------------------------ host utilities */
+/* make_support (kernels.hpp:24, kernels.cpp:7-35): |Lambda| x ndim offsets,
+ * row-major, lexicographic.  offsets may be NULL to query the count. */
+int sk_make_support(int shape, int tau, int ndim, int32_t* offsets, int64_t* count);
+/* reduced_grid_dims (maps.hpp:102, maps.cpp:39-45) */
+int sk_reduced_grid_dims(int ndim, const int64_t* calib_dims, int64_t pad, const int64_t* full_dims,
+                         int64_t* out);
+
+/* ------------------------------------------------------- stage entry points */
+/* gram_fft (calibration.hpp:42, calibration.cpp:80-144): calib Q x E^D
+ * (channel-major; the pad grid origin holds sample 0 as in the reference);
+ * gram: n x n column-major, n = Q*|Lambda|. */
+int sk_gram_fft(sk_ctx* ctx, int ndim, const int64_t* calib_dims, int64_t channels, const sk_c64* calib,
+                int shape, int tau, sk_c64* gram);
+
+/* extract_nullspace (nullspace.hpp:24, nullspace.cpp:7-35): spectrum = all n
+ * singular values, descending; filters (may be NULL) n x R column-major.
+ * filters_capacity: number of columns the caller allocated (>= R or error). */
+int sk_extract_nullspace(sk_ctx* ctx, int64_t n, const sk_c64* gram, double threshold_ratio, int64_t* rank,
+                         double* spectrum, sk_c64* filters, int64_t filters_capacity);
+
+/* aggregate_w (spatial_gram.hpp:61, spatial_gram.cpp:87-94): W = F F^H. */
+int sk_aggregate_w(sk_ctx* ctx, int64_t n, int64_t rank, const sk_c64* filters, sk_c64* w);
+
+/* gram_field_fast (spatial_gram.hpp:67, spatial_gram.cpp:96-148):
+ * field: N x Q x Q GramField layout. */
+int sk_gram_field_fast(sk_ctx* ctx, int64_t channels, const sk_c64* w, int shape, int tau, int ndim,
+                       const int64_t* dims, sk_c64* field);
+
+/* espirit_inplace (spatial_gram.hpp:73, spatial_gram.cpp:156-164). */
+int sk_espirit_inplace(sk_ctx* ctx, int64_t voxels, int64_t channels, sk_c64* field, int64_t support_size);
+
+/* eig_power_field (eigensolve.hpp:27, eigensolve.cpp:40-74): b_field in the
+ * GramField layout; vectors Q x N (column per voxel); values = Re(v^H B v). */
+int sk_eig_power_field(sk_ctx* ctx, int64_t voxels, int64_t channels, const sk_c64* b_field, int iters,
+                       sk_c64* vectors, float* values);
+
+/* normalize_maps (maps.hpp:92-94, maps.cpp:101-176). */
+int sk_normalize_maps(sk_ctx* ctx, int ndim, const int64_t* dims, int64_t channels, const sk_c64* raw,
+                      const int64_t* calib_dims, const int64_t* center_offset, const sk_c64* calib,
+                      double apod_width, sk_c64* out, int64_t* zeroed_voxels);
+
+/* interpolate_maps / interpolate_real (maps.hpp:98-99, maps.cpp:54-99). */
+int sk_interpolate_maps(sk_ctx* ctx, int ndim, const int64_t* low_dims, int64_t channels, const sk_c64* low,
+                        const int64_t* full_dims, sk_c64* out);
+int sk_interpolate_real(sk_ctx* ctx, int ndim, const int64_t* low_dims, const float* low,
+                        const int64_t* full_dims, float* out);
+
+/* support_mask (maps.hpp:105, maps.cpp:47-52). */
+int sk_support_mask(sk_ctx* ctx, int64_t voxels, const float* lambda, double mask_threshold, uint8_t* mask);
+
+/* ----------------------------------------------------------- full pipeline */
+/* estimate_maps (maps.hpp:85-86, maps.cpp:265-330).  Outputs on full_dims:
+ * maps Q x N_full, lambda_min_map N_full, support_mask N_full (each may be
+ * NULL).  spectrum_normalized (n = Q*|Lambda| values, may be NULL) and prov
+ * (may be NULL) carry the Provenance fields. */
+int sk_estimate_maps(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset,
+                     int64_t channels, const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg,
+                     sk_c64* maps, float* lambda_min_map, uint8_t* support_mask, double* spectrum_normalized,
+                     sk_provenance* prov);
+
+/* Stage dumps for parity checks (any may be NULL): the Gram (n x n), the
+ * grid-resolution G field (GramField layout), the raw power-iteration maps
+ * (Q x N_grid) and lambda on the grid.  Same semantics as sk_estimate_maps. */
+int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset,
+                           int64_t channels, const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg,
+                           sk_c64* maps, float* lambda_min_map, uint8_t* support_mask,
+                           double* spectrum_normalized, sk_provenance* prov, sk_c64* gram_out,
+                           sk_c64* field_out, sk_c64* raw_maps_out, float* raw_lambda_out);
+
+/* Multislice: `slices` independent calibrations (slice-major, each
+ * channel-major), one estimate_maps per slice on this GPU, outputs
+ * slice-major.  prov may be NULL or an array of `slices` records. */
+int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_t* calib_dims,
+                             const int64_t* center_offset, int64_t channels, const sk_c64* calib,
+                             const int64_t* full_dims, const sk_config* cfg, sk_c64* maps, float* lambda_min_map,
+                             uint8_t* support_mask, sk_provenance* prov);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SENSKIT_B200_H */

@@ -1,0 +1,168 @@
+// Separable small-matrix transforms along one axis of a row-major volume:
+//
+//   out[b][j][i] = sum_a M[j][a] * in[b][a][i]        (M: N x L, complex64)
+//
+// Every centred transform on the hot path is one of these per axis, because
+// the inputs are sparse boxes of a larger grid (the reference zero-pads and
+// runs full FFTs): the Gram's channel spectra (calibration.cpp:96-109), the
+// pruned inverse at the Gram lags, the G(x) lag-kernel expansion
+// (spatial_gram.cpp:125-138), the apodised calibration recon (maps.cpp:141-159)
+// and the periodic-sinc interpolation (maps.cpp:54-99).  The matrices are
+// built in FP64 on the host (sk_runtime.cu) with exact integer phase
+// reduction, so the device arithmetic is a plain complex GEMM-like contraction.
+//
+// Two mappings:
+//  * column mode (inner >= 32): a warp owns 32 consecutive `i`; each thread
+//    keeps its column's taps in registers and sweeps j; M rows come from
+//    shared memory as warp-wide broadcasts.  Loads/stores are 256-byte
+//    coalesced along i.
+//  * row mode (inner < 32, e.g. the last axis): a block stages RB input rows
+//    in shared memory, each thread owns output j and accumulates RB rows,
+//    reading M^T[a][j] coalesced from global/L2.
+#include "sk_internal.h"
+
+namespace skb {
+
+namespace {
+
+__device__ __forceinline__ void cmac(float2& acc, float2 m, float2 x) {
+  acc.x = fmaf(m.x, x.x, acc.x);
+  acc.x = fmaf(-m.y, x.y, acc.x);
+  acc.y = fmaf(m.x, x.y, acc.y);
+  acc.y = fmaf(m.y, x.x, acc.y);
+}
+
+constexpr int kColJ = 64;  // output rows per column-mode block
+
+template <int LT>
+__global__ void __launch_bounds__(256) axis_col_kernel(const float2* __restrict__ in, float2* __restrict__ out,
+                                                       const float2* __restrict__ M, int L, int N, i64 inner,
+                                                       int a0, int lt, bool accumulate) {
+  __shared__ __align__(16) float2 sm[kColJ * LT];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const i64 nchunk = (inner + 31) / 32;
+  const i64 b = i64(blockIdx.x) / nchunk;
+  const i64 i = (i64(blockIdx.x) % nchunk) * 32 + tx;
+  const int j_begin = blockIdx.y * kColJ;
+  const int j_count = min(kColJ, N - j_begin);
+  // Stage the M tile (j_count rows x lt taps), zero-padded to LT.
+  for (int e = ty * 32 + tx; e < kColJ * LT; e += 256) {
+    const int jj = e / LT, t = e % LT;
+    sm[e] = (jj < j_count && t < lt) ? M[i64(j_begin + jj) * L + a0 + t] : make_float2(0.f, 0.f);
+  }
+  float2 x[LT];
+  const bool live = i < inner;
+#pragma unroll
+  for (int t = 0; t < LT; ++t)
+    x[t] = (live && t < lt) ? in[(b * L + a0 + t) * inner + i] : make_float2(0.f, 0.f);
+  __syncthreads();
+  if (!live) return;
+  for (int jj = ty; jj < j_count; jj += 8) {
+    const float4* row = reinterpret_cast<const float4*>(sm + jj * LT);
+    float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int t = 0; t < LT; t += 2) {
+      const float4 m2 = row[t / 2];
+      cmac(acc0, make_float2(m2.x, m2.y), x[t]);
+      cmac(acc1, make_float2(m2.z, m2.w), x[t + 1]);
+    }
+    float2 acc = make_float2(acc0.x + acc1.x, acc0.y + acc1.y);
+    float2* dst = out + (b * N + j_begin + jj) * inner + i;
+    if (accumulate) {
+      const float2 prev = *dst;
+      acc.x += prev.x;
+      acc.y += prev.y;
+    }
+    *dst = acc;
+  }
+}
+
+constexpr int kRowRB = 16;   // input rows per row-mode block
+constexpr int kRowTap = 64;  // taps staged per chunk
+
+__global__ void __launch_bounds__(256) axis_row_kernel(const float2* __restrict__ in, float2* __restrict__ out,
+                                                       const float2* __restrict__ Mt, i64 rows, int L, int N,
+                                                       i64 inner) {
+  __shared__ __align__(16) float2 xs[kRowTap][kRowRB];  // [tap][row]
+  const i64 r0 = i64(blockIdx.x) * kRowRB;
+  for (int j0 = 0; j0 < N; j0 += blockDim.x) {
+    const int j = j0 + threadIdx.x;
+    float2 acc[kRowRB];
+#pragma unroll
+    for (int r = 0; r < kRowRB; ++r) acc[r] = make_float2(0.f, 0.f);
+    for (int a0 = 0; a0 < L; a0 += kRowTap) {
+      const int lt = min(kRowTap, L - a0);
+      __syncthreads();
+      for (int e = threadIdx.x; e < kRowTap * kRowRB; e += blockDim.x) {
+        const int r = e / kRowTap, t = e % kRowTap;  // consecutive threads walk taps (contiguous for inner == 1)
+        const i64 row = r0 + r;
+        float2 v = make_float2(0.f, 0.f);
+        if (row < rows && t < lt) {
+          const i64 bb = row / inner, ii = row % inner;
+          v = in[(bb * L + a0 + t) * inner + ii];
+        }
+        xs[t][r] = v;
+      }
+      __syncthreads();
+      if (j < N) {
+        for (int t = 0; t < lt; ++t) {
+          const float2 m = Mt[i64(a0 + t) * N + j];
+          const float4* xr = reinterpret_cast<const float4*>(&xs[t][0]);
+#pragma unroll
+          for (int r = 0; r < kRowRB; r += 2) {
+            const float4 x2 = xr[r / 2];
+            cmac(acc[r], m, make_float2(x2.x, x2.y));
+            cmac(acc[r + 1], m, make_float2(x2.z, x2.w));
+          }
+        }
+      }
+    }
+    if (j < N) {
+#pragma unroll
+      for (int r = 0; r < kRowRB; ++r) {
+        const i64 row = r0 + r;
+        if (row < rows) {
+          const i64 bb = row / inner, ii = row % inner;
+          out[(bb * N + j) * inner + ii] = acc[r];
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+// Mt (L x N) is stored right after M (N x L) in the same allocation.
+void apply_axis(sk_ctx* ctx, const float2* in, float2* out, const float2* M, i64 batch, int L, int N, i64 inner) {
+  if (batch <= 0 || N <= 0 || inner <= 0) return;
+  if (inner >= 32) {
+    const dim3 block(32, 8);
+    for (int a0 = 0; a0 < L; a0 += 64) {
+      const int lt = std::min(64, L - a0);
+      const i64 gx = (inner + 31) / 32 * batch;
+      if (gx > 0x7fffffffLL) fail(9, "apply_axis: grid too large");
+      const dim3 grid(unsigned(gx), unsigned((N + kColJ - 1) / kColJ));
+      const bool acc = a0 > 0;
+      if (lt <= 8)
+        axis_col_kernel<8><<<grid, block, 0, ctx->stream>>>(in, out, M, L, N, inner, a0, lt, acc);
+      else if (lt <= 16)
+        axis_col_kernel<16><<<grid, block, 0, ctx->stream>>>(in, out, M, L, N, inner, a0, lt, acc);
+      else if (lt <= 32)
+        axis_col_kernel<32><<<grid, block, 0, ctx->stream>>>(in, out, M, L, N, inner, a0, lt, acc);
+      else
+        axis_col_kernel<64><<<grid, block, 0, ctx->stream>>>(in, out, M, L, N, inner, a0, lt, acc);
+      ++ctx->launches;
+      SKB_LAUNCH("axis_col_kernel");
+    }
+  } else {
+    const i64 rows = batch * inner;
+    const float2* Mt = M + i64(N) * L;
+    const int threads = N >= 256 ? 256 : (N >= 128 ? 128 : 64);
+    const i64 blocks = (rows + kRowRB - 1) / kRowRB;
+    axis_row_kernel<<<unsigned(blocks), threads, 0, ctx->stream>>>(in, out, Mt, rows, L, N, inner);
+    ++ctx->launches;
+    SKB_LAUNCH("axis_row_kernel");
+  }
+}
+
+}  // namespace skb

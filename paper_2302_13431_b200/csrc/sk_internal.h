@@ -1,0 +1,159 @@
+// Internal declarations shared by the host runtime (sk_runtime.cu) and the
+// kernels.  Nothing here crosses the C-ABI boundary (include/senskit_b200.h).
+#pragma once
+
+#include <cuComplex.h>
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace skb {
+
+using i64 = std::int64_t;
+using Dims = std::vector<i64>;
+
+// Error classes mirror the reference's exceptions (types.hpp:22-32).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what);
+void check_cublas(cublasStatus_t s, const char* what);
+void check_cusolver(cusolverStatus_t s, const char* what);
+#define SKB_CUDA(x) ::skb::check_cuda((x), #x)
+#define SKB_LAUNCH(what) ::skb::check_cuda(cudaGetLastError(), what)
+
+inline i64 numel(const Dims& d) {
+  i64 n = 1;
+  for (i64 e : d) n *= e;
+  return n;
+}
+inline i64 center_index(i64 n) { return n / 2; }  // types.hpp:45
+
+// ------------------------------------------------------------- kernel support
+struct Support {
+  int shape = 0, tau = 0, nd = 0;
+  i64 count = 0;
+  std::vector<int> offsets;  // count x nd
+  int off(i64 i, int a) const { return offsets[size_t(i * nd + a)]; }
+};
+Support make_support(int shape, int tau, int ndim);  // kernels.cpp:7-35
+
+// ---------------------------------------------------------------- workspace
+// Grow-only device buffers keyed by name; a context owns one arena.
+class Arena {
+ public:
+  ~Arena();
+  void* get(const std::string& name, size_t bytes);
+  template <typename T>
+  T* get(const std::string& name, i64 count) {
+    return static_cast<T*>(get(name, size_t(count) * sizeof(T)));
+  }
+  void release_all();
+
+ private:
+  struct Slot {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+  };
+  std::map<std::string, Slot> slots_;
+};
+
+// Small complex matrices (DFT / sinc / apodised DFT) for the separable
+// transforms, built in FP64 on the host and cached on the device.
+struct MatrixCache {
+  std::map<std::string, float2*> mats;
+  ~MatrixCache();
+};
+
+}  // namespace skb
+
+struct sk_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  cublasHandle_t cublas = nullptr;
+  cusolverDnHandle_t cusolver = nullptr;
+  cusolverDnParams_t cusolver_params = nullptr;
+  skb::Arena arena;
+  skb::MatrixCache matrices;
+  std::map<std::string, void*> tables;  // cached index tables (device)
+  int64_t launches = 0;   // our kernels
+  int64_t lib_calls = 0;  // cuSOLVER / cuBLAS calls
+  cudaEvent_t ev[8] = {};
+};
+
+namespace skb {
+
+// ----------------------------------------------------------- kernel wrappers
+// Separable "apply a small matrix along one axis":
+//   out[b][j][i] = sum_a M[j][a] * in[b][a][i],  M is N x L (row-major, c64).
+void apply_axis(sk_ctx* ctx, const float2* in, float2* out, const float2* M, i64 batch, int L, int N, i64 inner);
+
+// K1: pairwise correlation on the lag box + Gram assembly (calibration.cpp:111-142).
+struct GramGeom {
+  int nd;
+  int pad[3];      // pad grid extents
+  int lb;          // lag box extent per axis (4*tau + 1)
+  int tau;
+  int q;           // channels
+  int lam;         // |Lambda|
+};
+size_t gram_pairs_smem(const GramGeom& g);
+void gram_pairs_launch(sk_ctx* ctx, const float2* spectra, const GramGeom& g, const int2* d_pairs, int npairs,
+                       const int* d_off, const float2* d_tw, float2* gram);
+
+// Fold W (or I - U U^H) into per-pair lag kernels on the lag box
+// (spatial_gram.cpp:108-131).  w_is_signal: W = I - w (w = U_sig U_sig^H,
+// lower triangle valid) else W = w (full matrix).
+void fold_lags_f64(sk_ctx* ctx, const double2* w, i64 n, int npairs, int lam, int nbox, const int2* d_pairs,
+                   const int* d_lag_ptr, const int* d_lag_st, bool w_is_signal, float2* lags);
+void fold_lags_f32(sk_ctx* ctx, const float2* w, i64 n, int npairs, int lam, int nbox, const int2* d_pairs,
+                   const int* d_lag_ptr, const int* d_lag_st, float2* lags);
+
+// K4: batched per-voxel power iteration over packed Hermitian planes
+// [h][N] (h = Q(Q+1)/2, plane (p<=q) holds M(row p, col q)).
+// Iterates v <- (alpha v + beta M v) / ||.||; reports mv = Re(v^H M v).
+// Optional epilogue (recon != nullptr): SoS normalisation + phase reference
+// against recon [Q][N] (maps.cpp:117-172), zeroed voxel count, mask.
+struct PowerArgs {
+  const float2* planes;
+  i64 n;            // voxels
+  int q;            // channels
+  int iters;
+  float alpha, beta;
+  float lam_scale;  // lambda = mv * lam_scale
+  const float2* recon;   // nullable
+  float2* maps;          // [Q][N]
+  float* lambda;         // [N] (lambda = mv*lam_scale) nullable
+  float* value;          // [N] alpha + beta*mv (B-form Rayleigh) nullable
+  uint8_t* mask;         // nullable
+  float mask_threshold;
+  unsigned long long* zeroed;  // nullable
+};
+void power_iteration(sk_ctx* ctx, const PowerArgs& a);
+
+// Conversions / small elementwise kernels.
+void c64_to_c128(sk_ctx* ctx, const float2* in, double2* out, i64 n);
+void c128_to_c64(sk_ctx* ctx, const double2* in, float2* out, i64 n);
+void field_full_to_planes(sk_ctx* ctx, const float2* field, i64 n, int q, float2* planes);
+void planes_to_field_full(sk_ctx* ctx, const float2* planes, i64 n, int q, float2* field);
+void espirit_field(sk_ctx* ctx, float2* field, i64 n, int q, float inv_lam);
+void renormalize_and_mask(sk_ctx* ctx, float2* maps, i64 n, int q, const float2* lambda_c, float* lambda,
+                          uint8_t* mask, float thr);
+void mask_kernel(sk_ctx* ctx, const float* lambda, i64 n, float thr, uint8_t* mask);
+void real_to_c64(sk_ctx* ctx, const float* in, float2* out, i64 n);
+void copy_strided(sk_ctx* ctx, const float2* src, i64 src_rs, i64 src_cs, float2* dst, i64 dst_rs, i64 dst_cs, i64 rows,
+                  i64 cols);
+void normalize_standalone(sk_ctx* ctx, float2* maps, i64 n, int q, const float2* recon, unsigned long long* zeroed);
+
+}  // namespace skb

@@ -1,0 +1,211 @@
+// Elementwise / layout kernels around the hot path: precision conversion for
+// the FP64 eigensolve, GramField <-> packed-plane repacking for the
+// reference-layout entry points, espirit_inplace (spatial_gram.cpp:156-164),
+// the post-interpolation SoS renormalisation + support mask
+// (maps.cpp:242-258), and the standalone normalize_maps epilogue.
+#include "sk_internal.h"
+
+namespace skb {
+
+namespace {
+
+constexpr int kT = 256;
+inline unsigned blocks_for(i64 n) { return unsigned(std::min<i64>((n + kT - 1) / kT, i64(1) << 30)); }
+
+__global__ void c64_to_c128_kernel(const float2* __restrict__ in, double2* __restrict__ out, i64 n) {
+  for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x)
+    out[i] = make_double2(in[i].x, in[i].y);
+}
+
+__global__ void c128_to_c64_kernel(const double2* __restrict__ in, float2* __restrict__ out, i64 n) {
+  for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += i64(gridDim.x) * blockDim.x)
+    out[i] = make_float2(float(in[i].x), float(in[i].y));
+}
+
+// GramField (voxel-major, col-major Q x Q) -> planes [h][N] (upper, p <= q).
+__global__ void full_to_planes_kernel(const float2* __restrict__ field, i64 n, int q, float2* __restrict__ planes) {
+  const int h = q * (q + 1) / 2;
+  const i64 total = i64(h) * n;
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+    const i64 j = e % n;
+    int pair = int(e / n), p = 0;
+    while (pair >= q - p) {
+      pair -= q - p;
+      ++p;
+    }
+    const int c = p + pair;
+    planes[e] = field[j * q * q + i64(c) * q + p];  // (row p, col c)
+  }
+}
+
+// planes -> GramField with the conjugate mirror and real diagonal
+// (spatial_gram.cpp:133-146).
+__global__ void planes_to_full_kernel(const float2* __restrict__ planes, i64 n, int q, float2* __restrict__ field) {
+  const i64 total = n * q * q;
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+    const i64 j = e / (i64(q) * q);
+    const int rc = int(e % (i64(q) * q));
+    const int col = rc / q, row = rc % q;
+    const int p = min(row, col), c = max(row, col);
+    const int pair = p * q - p * (p - 1) / 2 + (c - p);
+    float2 v = planes[i64(pair) * n + j];
+    if (row > col) v.y = -v.y;
+    if (row == col) v.y = 0.f;
+    field[e] = v;
+  }
+}
+
+__global__ void espirit_kernel(float2* __restrict__ field, i64 n, int q, float inv_lam) {
+  const i64 total = n * q * q;
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+    const int rc = int(e % (i64(q) * q));
+    float2 v = field[e];
+    v.x *= -inv_lam;
+    v.y *= -inv_lam;
+    if (rc / q == rc % q) v.x += 1.f;
+    field[e] = v;
+  }
+}
+
+// One thread per voxel: SoS renormalisation of the interpolated maps, lambda
+// real part, support mask.
+__global__ void renorm_mask_kernel(float2* __restrict__ maps, i64 n, int q, const float2* __restrict__ lam_c,
+                                   float* __restrict__ lam, uint8_t* __restrict__ mask, float thr) {
+  for (i64 j = i64(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += i64(gridDim.x) * blockDim.x) {
+    if (maps != nullptr) {
+      float sos = 0.f;
+      for (int c = 0; c < q; ++c) {
+        const float2 v = maps[i64(c) * n + j];
+        sos += v.x * v.x + v.y * v.y;
+      }
+      if (sos > 0.f) {
+        const float inv = 1.0f / sqrtf(sos);
+        for (int c = 0; c < q; ++c) {
+          float2 v = maps[i64(c) * n + j];
+          v.x *= inv;
+          v.y *= inv;
+          maps[i64(c) * n + j] = v;
+        }
+      }
+    }
+    if (lam_c != nullptr) {
+      const float l = lam_c[j].x;
+      if (lam) lam[j] = l;
+      if (mask) mask[j] = l < thr ? 1 : 0;
+    }
+  }
+}
+
+__global__ void mask_only_kernel(const float* __restrict__ lam, i64 n, float thr, uint8_t* __restrict__ mask) {
+  for (i64 j = i64(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += i64(gridDim.x) * blockDim.x)
+    mask[j] = lam[j] < thr ? 1 : 0;
+}
+
+__global__ void real_to_c64_kernel(const float* __restrict__ in, float2* __restrict__ out, i64 n) {
+  for (i64 j = i64(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += i64(gridDim.x) * blockDim.x)
+    out[j] = make_float2(in[j], 0.f);
+}
+
+__global__ void copy_strided_kernel(const float2* __restrict__ src, i64 src_rs, i64 src_cs, float2* __restrict__ dst,
+                                    i64 dst_rs, i64 dst_cs, i64 rows, i64 cols) {
+  const i64 total = rows * cols;
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+    const i64 c = e / rows, r = e % rows;
+    dst[r * dst_rs + c * dst_cs] = src[r * src_rs + c * src_cs];
+  }
+}
+
+// normalize_maps on channel-major maps (maps.cpp:117-172), one thread per voxel.
+__global__ void normalize_kernel(float2* __restrict__ maps, i64 n, int q, const float2* __restrict__ recon,
+                                 unsigned long long* zeroed) {
+  for (i64 j = i64(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += i64(gridDim.x) * blockDim.x) {
+    float sos = 0.f;
+    for (int c = 0; c < q; ++c) {
+      const float2 v = maps[i64(c) * n + j];
+      sos += v.x * v.x + v.y * v.y;
+    }
+    float inv = 1.f;
+    if (sos > 0.f)
+      inv = 1.0f / sqrtf(sos);
+    else
+      atomicAdd(zeroed, 1ull);
+    float ux = 0.f, uy = 0.f;
+    for (int c = 0; c < q; ++c) {
+      const float2 v = maps[i64(c) * n + j];
+      const float2 r = recon[i64(c) * n + j];
+      const float vx = v.x * inv, vy = v.y * inv;
+      ux += vx * r.x + vy * r.y;
+      uy += vx * r.y - vy * r.x;
+    }
+    const float mag = sqrtf(ux * ux + uy * uy);
+    float cx = 1.f, cy = 0.f;
+    if (mag > 0.f) {
+      cx = ux / mag;
+      cy = uy / mag;
+    }
+    for (int c = 0; c < q; ++c) {
+      const float2 v = maps[i64(c) * n + j];
+      const float vx = v.x * inv, vy = v.y * inv;
+      maps[i64(c) * n + j] = make_float2(vx * cx - vy * cy, vx * cy + vy * cx);
+    }
+  }
+}
+
+}  // namespace
+
+#define SKB_GRID(n) blocks_for(n), kT, 0, ctx->stream
+
+void c64_to_c128(sk_ctx* ctx, const float2* in, double2* out, i64 n) {
+  c64_to_c128_kernel<<<SKB_GRID(n)>>>(in, out, n);
+  ++ctx->launches;
+  SKB_LAUNCH("c64_to_c128");
+}
+void c128_to_c64(sk_ctx* ctx, const double2* in, float2* out, i64 n) {
+  c128_to_c64_kernel<<<SKB_GRID(n)>>>(in, out, n);
+  ++ctx->launches;
+  SKB_LAUNCH("c128_to_c64");
+}
+void field_full_to_planes(sk_ctx* ctx, const float2* field, i64 n, int q, float2* planes) {
+  full_to_planes_kernel<<<SKB_GRID(n * q * (q + 1) / 2)>>>(field, n, q, planes);
+  ++ctx->launches;
+  SKB_LAUNCH("full_to_planes");
+}
+void planes_to_field_full(sk_ctx* ctx, const float2* planes, i64 n, int q, float2* field) {
+  planes_to_full_kernel<<<SKB_GRID(n * q * q)>>>(planes, n, q, field);
+  ++ctx->launches;
+  SKB_LAUNCH("planes_to_full");
+}
+void espirit_field(sk_ctx* ctx, float2* field, i64 n, int q, float inv_lam) {
+  espirit_kernel<<<SKB_GRID(n * q * q)>>>(field, n, q, inv_lam);
+  ++ctx->launches;
+  SKB_LAUNCH("espirit");
+}
+void renormalize_and_mask(sk_ctx* ctx, float2* maps, i64 n, int q, const float2* lambda_c, float* lambda,
+                          uint8_t* mask, float thr) {
+  renorm_mask_kernel<<<SKB_GRID(n)>>>(maps, n, q, lambda_c, lambda, mask, thr);
+  ++ctx->launches;
+  SKB_LAUNCH("renorm_mask");
+}
+void mask_kernel(sk_ctx* ctx, const float* lambda, i64 n, float thr, uint8_t* mask) {
+  mask_only_kernel<<<SKB_GRID(n)>>>(lambda, n, thr, mask);
+  ++ctx->launches;
+  SKB_LAUNCH("mask");
+}
+void real_to_c64(sk_ctx* ctx, const float* in, float2* out, i64 n) {
+  real_to_c64_kernel<<<SKB_GRID(n)>>>(in, out, n);
+  ++ctx->launches;
+  SKB_LAUNCH("real_to_c64");
+}
+void copy_strided(sk_ctx* ctx, const float2* src, i64 src_rs, i64 src_cs, float2* dst, i64 dst_rs, i64 dst_cs, i64 rows,
+                  i64 cols) {
+  copy_strided_kernel<<<SKB_GRID(rows * cols)>>>(src, src_rs, src_cs, dst, dst_rs, dst_cs, rows, cols);
+  ++ctx->launches;
+  SKB_LAUNCH("copy_strided");
+}
+void normalize_standalone(sk_ctx* ctx, float2* maps, i64 n, int q, const float2* recon, unsigned long long* zeroed) {
+  normalize_kernel<<<SKB_GRID(n)>>>(maps, n, q, recon, zeroed);
+  ++ctx->launches;
+  SKB_LAUNCH("normalize");
+}
+
+}  // namespace skb

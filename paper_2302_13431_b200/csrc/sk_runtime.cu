@@ -1,0 +1,959 @@
+// Host runtime: context, workspace, transform matrices, stage orchestration
+// and the C-ABI (include/senskit_b200.h).  One sk_ctx per GPU; every entry
+// point validates like the reference, runs on the context stream, and
+// synchronises before returning.
+//
+// Pipeline (maps.cpp:265-330, pisco preset) as run here:
+//   gram       K1: channel spectra (apply_axis DFT) + pair lag contraction
+//   nullspace  K2: FP64 cuSOLVER Xsyevd on the promoted Gram, cut on the
+//                  host, Ws = U_sig U_sig^H by cuBLAS ZHERK (W = I - Ws)
+//   field      fold W into lag kernels, K3 lag expansion -> packed G planes
+//   eigensolve K4: power iteration (+ fused normalize epilogue)
+//   post       K5: apodised recon (before K4, timed here), interpolation,
+//                  SoS renormalisation, support mask
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/senskit_b200.h"
+#include "sk_internal.h"
+#include <complex>
+
+using namespace skb;
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+// ================================================================ errors
+namespace skb {
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error(code, msg); }
+void check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation) fail(SK_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+  fail(SK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void check_cublas(cublasStatus_t s, const char* what) {
+  if (s != CUBLAS_STATUS_SUCCESS) fail(SK_ERR_CUDA, std::string(what) + ": cuBLAS status " + std::to_string(int(s)));
+}
+void check_cusolver(cusolverStatus_t s, const char* what) {
+  if (s != CUSOLVER_STATUS_SUCCESS)
+    fail(SK_ERR_CUDA, std::string(what) + ": cuSOLVER status " + std::to_string(int(s)));
+}
+
+// ================================================================ arena
+Arena::~Arena() { release_all(); }
+void* Arena::get(const std::string& name, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  Slot& s = slots_[name];
+  if (s.bytes < bytes) {
+    if (s.ptr) cudaFree(s.ptr);
+    s.ptr = nullptr;
+    s.bytes = 0;
+    const size_t want = (bytes + 255) & ~size_t(255);
+    check_cuda(cudaMalloc(&s.ptr, want), ("cudaMalloc(" + name + ")").c_str());
+    s.bytes = want;
+  }
+  return s.ptr;
+}
+void Arena::release_all() {
+  for (auto& kv : slots_)
+    if (kv.second.ptr) cudaFree(kv.second.ptr);
+  slots_.clear();
+}
+MatrixCache::~MatrixCache() {
+  for (auto& kv : mats) cudaFree(kv.second);
+}
+
+// ================================================================ support
+Support make_support(int shape, int tau, int ndim) {  // kernels.cpp:7-35
+  if (tau < 0) fail(SK_ERR_DIM, "kernel radius must be >= 0");
+  if (ndim < 1) fail(SK_ERR_DIM, "kernel dimension must be >= 1");
+  Support s;
+  s.shape = shape;
+  s.tau = tau;
+  s.nd = ndim;
+  const int side = 2 * tau + 1;
+  std::vector<int> idx(size_t(ndim), 0);
+  while (true) {
+    long r2 = 0;
+    for (int a = 0; a < ndim; ++a) {
+      const long v = long(idx[size_t(a)]) - tau;
+      r2 += v * v;
+    }
+    if (!(shape == 1 && r2 > long(tau) * tau))
+      for (int a = 0; a < ndim; ++a) s.offsets.push_back(idx[size_t(a)] - tau);
+    int a = ndim - 1;
+    for (; a >= 0; --a) {
+      if (++idx[size_t(a)] < side) break;
+      idx[size_t(a)] = 0;
+    }
+    if (a < 0) break;
+  }
+  s.count = i64(s.offsets.size()) / ndim;
+  return s;
+}
+}  // namespace skb
+
+// ================================================================ helpers
+namespace {
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes attr{};
+  const cudaError_t e = cudaPointerGetAttributes(&attr, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+// Device view of a caller input: the pointer itself, or an arena upload.
+template <typename T>
+const T* device_in(sk_ctx* ctx, const T* p, i64 count, const std::string& slot) {
+  if (!p) return nullptr;
+  if (is_device_ptr(p)) return p;
+  T* d = ctx->arena.get<T>(slot, count);
+  SKB_CUDA(cudaMemcpyAsync(d, p, size_t(count) * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+  return d;
+}
+
+// Device destination for a caller output (direct, or arena + copy-back).
+template <typename T>
+struct Out {
+  T* user = nullptr;
+  T* dev = nullptr;
+  i64 count = 0;
+  bool host = false;
+  Out(sk_ctx* ctx, T* p, i64 n, const std::string& slot) : user(p), count(n) {
+    if (!p) {
+      dev = nullptr;
+    } else if (is_device_ptr(p)) {
+      dev = p;
+    } else {
+      host = true;
+      dev = ctx->arena.get<T>(slot, n);
+    }
+  }
+  void finish(sk_ctx* ctx) {
+    if (host && user)
+      SKB_CUDA(cudaMemcpyAsync(user, dev, size_t(count) * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+};
+
+Dims dims_of(int nd, const int64_t* d) { return Dims(d, d + nd); }
+std::string key_of(const Dims& d) {
+  std::string s;
+  for (i64 e : d) s += std::to_string(e) + "x";
+  return s;
+}
+
+// Upload an N x L matrix (row-major) followed by its transpose (L x N).
+float2* upload_matrix(sk_ctx* ctx, const std::string& key, int N, int L, const std::vector<std::complex<double>>& m) {
+  auto it = ctx->matrices.mats.find(key);
+  if (it != ctx->matrices.mats.end()) return it->second;
+  std::vector<float2> h(size_t(2) * N * L);
+  for (int j = 0; j < N; ++j)
+    for (int a = 0; a < L; ++a) {
+      const auto v = m[size_t(j) * L + a];
+      h[size_t(j) * L + a] = make_float2(float(v.real()), float(v.imag()));
+      h[size_t(N) * L + size_t(a) * N + j] = make_float2(float(v.real()), float(v.imag()));
+    }
+  float2* d = nullptr;
+  SKB_CUDA(cudaMalloc(&d, h.size() * sizeof(float2)));
+  SKB_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  ctx->matrices.mats[key] = d;
+  return d;
+}
+
+// exp(sign * i 2 pi m / n) with m reduced exactly in integers.
+std::complex<double> cis(int sign, i64 m, i64 n) {
+  m %= n;
+  if (m < 0) m += n;
+  const double ang = double(sign) * 2.0 * M_PI * double(m) / double(n);
+  return {std::cos(ang), std::sin(ang)};
+}
+
+// Centred DFT taps: M[j][a] = w(a) exp(sign i 2 pi (a - a0)(j - j0) / N).
+float2* dft_matrix(sk_ctx* ctx, int N, int L, i64 a0, i64 j0, int sign, double sigma) {
+  const std::string key = "dft:" + std::to_string(N) + ":" + std::to_string(L) + ":" + std::to_string(a0) + ":" +
+                          std::to_string(j0) + ":" + std::to_string(sign) + ":" + std::to_string(sigma);
+  auto it = ctx->matrices.mats.find(key);
+  if (it != ctx->matrices.mats.end()) return it->second;
+  std::vector<std::complex<double>> m(size_t(N) * L);
+  for (int j = 0; j < N; ++j)
+    for (int a = 0; a < L; ++a) {
+      double w = 1.0;
+      if (sigma > 0) {
+        const double f = double(a - a0);
+        w = std::exp(-f * f / (2.0 * sigma * sigma));
+      }
+      m[size_t(j) * L + a] = w * cis(sign, (a - a0) * (j - j0), N);
+    }
+  return upload_matrix(ctx, key, N, L, m);
+}
+
+// Periodic-sinc interpolation along one axis (maps.cpp:54-90):
+// image_to_kspace on n_low (x 1/n_low), centred zero-pad into N, kspace_to_image.
+float2* sinc_matrix(sk_ctx* ctx, int N, int nl) {
+  const std::string key = "sinc:" + std::to_string(N) + ":" + std::to_string(nl);
+  auto it = ctx->matrices.mats.find(key);
+  if (it != ctx->matrices.mats.end()) return it->second;
+  const i64 cl = nl / 2, cf = N / 2;
+  std::vector<std::complex<double>> m(size_t(N) * nl);
+  for (int j = 0; j < N; ++j)
+    for (int b = 0; b < nl; ++b) {
+      std::complex<double> acc = 0;
+      for (i64 f = -cl; f < nl - cl; ++f) acc += cis(+1, f * (j - cf), N) * cis(-1, f * (b - cl), nl);
+      m[size_t(j) * nl + b] = acc / double(nl);
+    }
+  return upload_matrix(ctx, key, N, nl, m);
+}
+
+// Apply per-axis matrices last axis first: in [batch][in_ext...] -> out [batch][out_ext...].
+void separable(sk_ctx* ctx, const float2* in, float2* out, i64 batch, const Dims& in_ext, const Dims& out_ext,
+               const std::vector<float2*>& mats, const std::string& tag) {
+  const int nd = int(in_ext.size());
+  Dims cur = in_ext;
+  const float2* src = in;
+  for (int a = nd - 1; a >= 0; --a) {
+    float2* dst;
+    if (a == 0) {
+      dst = out;
+    } else {
+      Dims next = cur;
+      next[size_t(a)] = out_ext[size_t(a)];
+      dst = ctx->arena.get<float2>(tag + (a % 2 ? ":a" : ":b"), batch * numel(next));
+    }
+    i64 b = batch, inner = 1;
+    for (int k = 0; k < a; ++k) b *= cur[size_t(k)];
+    for (int k = a + 1; k < nd; ++k) inner *= cur[size_t(k)];
+    apply_axis(ctx, src, dst, mats[size_t(a)], b, int(in_ext[size_t(a)]), int(out_ext[size_t(a)]), inner);
+    cur[size_t(a)] = out_ext[size_t(a)];
+    src = dst;
+  }
+}
+
+// Cached device tables per (support, q).
+struct SupportTables {
+  int2* pairs = nullptr;  // h entries (p <= q)
+  int* off = nullptr;     // lam: box index of n_s relative to lag 0
+  int* lag_ptr = nullptr; // nbox + 1
+  int* lag_st = nullptr;  // lam^2 packed (s | t << 16), grouped by lag n_t - n_s
+  int nbox = 0, lb = 0;
+};
+
+SupportTables& tables_for(sk_ctx* ctx, const Support& s, int q) {
+  static std::map<std::pair<sk_ctx*, std::string>, SupportTables> cache;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  const std::string key = std::to_string(s.shape) + ":" + std::to_string(s.tau) + ":" + std::to_string(s.nd) + ":" +
+                          std::to_string(q);
+  auto it = cache.find({ctx, key});
+  if (it != cache.end()) return it->second;
+  SupportTables t;
+  t.lb = 4 * s.tau + 1;
+  t.nbox = 1;
+  std::vector<int> bs(size_t(s.nd), 1);
+  for (int a = s.nd - 1; a >= 0; --a) {
+    bs[size_t(a)] = t.nbox;
+    t.nbox *= t.lb;
+  }
+  std::vector<int> off(static_cast<size_t>(s.count));
+  for (i64 i = 0; i < s.count; ++i) {
+    int o = 0;
+    for (int a = 0; a < s.nd; ++a) o += s.off(i, a) * bs[size_t(a)];
+    off[size_t(i)] = o;
+  }
+  const int ctr = (t.nbox - 1) / 2;
+  std::vector<std::vector<int>> lists(static_cast<size_t>(t.nbox));
+  for (i64 si = 0; si < s.count; ++si)
+    for (i64 ti = 0; ti < s.count; ++ti)
+      lists[size_t(off[size_t(ti)] - off[size_t(si)] + ctr)].push_back(int(si) | (int(ti) << 16));
+  std::vector<int> ptr(size_t(t.nbox) + 1, 0), st;
+  for (int l = 0; l < t.nbox; ++l) {
+    ptr[size_t(l) + 1] = ptr[size_t(l)] + int(lists[size_t(l)].size());
+    st.insert(st.end(), lists[size_t(l)].begin(), lists[size_t(l)].end());
+  }
+  std::vector<int2> pairs;
+  for (int p = 0; p < q; ++p)
+    for (int c = p; c < q; ++c) pairs.push_back(make_int2(p, c));
+  auto up = [](const void* h, size_t bytes) {
+    void* d = nullptr;
+    check_cuda(cudaMalloc(&d, std::max<size_t>(bytes, 16)), "cudaMalloc(table)");
+    check_cuda(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice), "upload table");
+    return d;
+  };
+  t.pairs = static_cast<int2*>(up(pairs.data(), pairs.size() * sizeof(int2)));
+  t.off = static_cast<int*>(up(off.data(), off.size() * sizeof(int)));
+  t.lag_ptr = static_cast<int*>(up(ptr.data(), ptr.size() * sizeof(int)));
+  t.lag_st = static_cast<int*>(up(st.data(), std::max<size_t>(st.size(), 1) * sizeof(int)));
+  return cache.emplace(std::make_pair(ctx, key), t).first->second;
+}
+
+i64 next_pow2(i64 n) {
+  i64 p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+void check_calib(const Dims& cdims, i64 q, const Support& s) {  // calibration.cpp:12-20
+  if (cdims.empty()) fail(SK_ERR_DIM, "stack needs at least one axis");
+  for (i64 d : cdims)
+    if (d < 1) fail(SK_ERR_DIM, "stack axis extents must be >= 1");
+  if (q < 1) fail(SK_ERR_DIM, "stack needs at least one channel");
+  if (i64(cdims.size()) != s.nd) fail(SK_ERR_DIM, "support dimension does not match calibration region");
+  for (i64 d : cdims)
+    if (d <= 2 * s.tau) fail(SK_ERR_DIM, "calibration region too small for kernel radius " + std::to_string(s.tau));
+  if (cdims.size() > 3) fail(SK_ERR_UNSUPPORTED, "more than 3 dimensions is outside the B200 path");
+}
+
+// ---------------------------------------------------------------- K1
+float2* run_gram(sk_ctx* ctx, const Dims& cdims, i64 q, const float2* calib, const Support& s, float2* gram_dst) {
+  const int nd = int(cdims.size());
+  const i64 lam = s.count, n = q * lam;
+  Dims pad(cdims.size());
+  for (size_t a = 0; a < cdims.size(); ++a) pad[a] = next_pow2(cdims[a] + 2 * s.tau);  // calibration.cpp:89-93
+  std::vector<float2*> mats(static_cast<size_t>(nd));
+  for (int a = 0; a < nd; ++a) mats[size_t(a)] = dft_matrix(ctx, int(pad[size_t(a)]), int(cdims[size_t(a)]), 0, 0, -1, 0.0);
+  float2* spectra = ctx->arena.get<float2>("gram:spectra", q * numel(pad));
+  separable(ctx, calib, spectra, q, cdims, pad, mats, "gram:tmp");
+  SupportTables& t = tables_for(ctx, s, int(q));
+  GramGeom g{};
+  g.nd = nd;
+  g.pad[0] = g.pad[1] = g.pad[2] = 1;
+  for (int a = 0; a < nd; ++a) g.pad[a] = int(pad[size_t(a)]);
+  g.lb = 4 * s.tau + 1;
+  g.tau = s.tau;
+  g.q = int(q);
+  g.lam = int(lam);
+  // twiddles e^{+i 2 pi m / P_a}
+  std::vector<std::complex<double>> tw;
+  for (int a = 0; a < 3; ++a)
+    for (int m = 0; m < g.pad[a]; ++m) tw.push_back(cis(+1, m, g.pad[a]));
+  const std::string key = "gramtw:" + std::to_string(g.pad[0]) + ":" + std::to_string(g.pad[1]) + ":" +
+                          std::to_string(g.pad[2]);
+  float2* d_tw = upload_matrix(ctx, key, int(tw.size()), 1, tw);
+  float2* gram = gram_dst ? gram_dst : ctx->arena.get<float2>("gram:G", n * n);
+  gram_pairs_launch(ctx, spectra, g, t.pairs, int(q * (q + 1) / 2), t.off, d_tw, gram);
+  return gram;
+}
+
+// ---------------------------------------------------------------- K2
+struct Eig {
+  std::vector<double> evals;  // ascending
+  double2* evecs = nullptr;   // n x n column-major, device
+  i64 n = 0, rank = 0;
+  double sigma1 = 0, cut = 0, margin = 0;
+  std::vector<double> spectrum;  // descending sigma
+};
+
+Eig run_eigh(sk_ctx* ctx, const float2* gram, i64 n, double ratio) {  // nullspace.cpp:7-35
+  if (!(ratio > 0.0 && ratio < 1.0)) fail(SK_ERR_DIM, "nullspace threshold ratio must lie in (0,1)");
+  if (n <= 0) fail(SK_ERR_DIM, "Gram matrix must be square");
+  Eig e;
+  e.n = n;
+  e.evecs = ctx->arena.get<double2>("eig:A", n * n);
+  c64_to_c128(ctx, gram, e.evecs, n * n);
+  double* d_w = ctx->arena.get<double>("eig:w", n);
+  size_t dev_bytes = 0, host_bytes = 0;
+  check_cusolver(cusolverDnXsyevd_bufferSize(ctx->cusolver, ctx->cusolver_params, CUSOLVER_EIG_MODE_VECTOR,
+                                             CUBLAS_FILL_MODE_LOWER, n, CUDA_C_64F, e.evecs, n, CUDA_R_64F, d_w,
+                                             CUDA_C_64F, &dev_bytes, &host_bytes),
+                 "Xsyevd_bufferSize");
+  void* d_work = ctx->arena.get("eig:work", dev_bytes);
+  static thread_local std::vector<unsigned char> h_work;
+  h_work.resize(std::max<size_t>(host_bytes, 1));
+  int* d_info = ctx->arena.get<int>("eig:info", 1);
+  check_cusolver(cusolverDnXsyevd(ctx->cusolver, ctx->cusolver_params, CUSOLVER_EIG_MODE_VECTOR,
+                                  CUBLAS_FILL_MODE_LOWER, n, CUDA_C_64F, e.evecs, n, CUDA_R_64F, d_w, CUDA_C_64F,
+                                  d_work, dev_bytes, h_work.data(), host_bytes, d_info),
+                 "Xsyevd");
+  ++ctx->lib_calls;
+  e.evals.resize(size_t(n));
+  int info = 0;
+  SKB_CUDA(cudaMemcpyAsync(e.evals.data(), d_w, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  SKB_CUDA(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (info != 0) fail(SK_ERR_OTHER, "Gram eigendecomposition failed");
+  std::vector<double> sig(static_cast<size_t>(n));
+  for (i64 i = 0; i < n; ++i) sig[size_t(i)] = std::sqrt(std::max(0.0, e.evals[size_t(i)]));
+  e.spectrum.assign(sig.rbegin(), sig.rend());
+  e.sigma1 = e.spectrum[0];
+  e.cut = ratio * e.sigma1;
+  i64 r = 0;
+  while (r < n && sig[size_t(r)] < e.cut) ++r;
+  e.rank = r;
+  double margin = 1e300;
+  for (double sv : sig)
+    if (e.cut > 0) margin = std::min(margin, std::fabs(sv / e.cut - 1.0));
+  e.margin = margin;
+  if (r == 0) {
+    char buf[96];
+    std::snprintf(buf, sizeof buf, "%f", ratio);
+    fail(SK_ERR_NULLSPACE_EMPTY, std::string("calibration matrix has no approximate nullspace at ratio ") + buf);
+  }
+  return e;
+}
+
+// ---------------------------------------------------------------- K3
+// Lag kernels from the signal subspace, expanded onto the grid as packed planes.
+float2* run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims& grid) {
+  const i64 n = e.n, k = n - e.rank;
+  const int lam = int(s.count);
+  SupportTables& t = tables_for(ctx, s, q);
+  const int h = q * (q + 1) / 2;
+  double2* ws = ctx->arena.get<double2>("field:Ws", n * n);
+  if (k > 0) {
+    const double one = 1.0, zero = 0.0;
+    check_cublas(cublasZherk(ctx->cublas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, int(n), int(k), &one,
+                             reinterpret_cast<const cuDoubleComplex*>(e.evecs + e.rank * n), int(n), &zero,
+                             reinterpret_cast<cuDoubleComplex*>(ws), int(n)),
+                 "Zherk");
+    ++ctx->lib_calls;
+  } else {
+    SKB_CUDA(cudaMemsetAsync(ws, 0, size_t(n * n) * sizeof(double2), ctx->stream));
+  }
+  float2* lags = ctx->arena.get<float2>("field:lags", i64(h) * t.nbox);
+  fold_lags_f64(ctx, ws, n, h, lam, t.nbox, t.pairs, t.lag_ptr, t.lag_st, true, lags);
+  const int nd = int(grid.size());
+  Dims box(size_t(nd), t.lb);
+  std::vector<float2*> mats(static_cast<size_t>(nd));
+  for (int a = 0; a < nd; ++a)
+    mats[size_t(a)] = dft_matrix(ctx, int(grid[size_t(a)]), t.lb, 2 * s.tau, center_index(grid[size_t(a)]), -1, 0.0);
+  float2* planes = ctx->arena.get<float2>("field:planes", i64(h) * numel(grid));
+  separable(ctx, lags, planes, h, box, grid, mats, "field:tmp");
+  return planes;
+}
+
+// Lag kernels from a caller-supplied W (gram_field_fast entry point).
+float2* run_field_from_w(sk_ctx* ctx, const float2* w, const Support& s, int q, const Dims& grid) {
+  const i64 n = i64(q) * s.count;
+  SupportTables& t = tables_for(ctx, s, q);
+  const int h = q * (q + 1) / 2;
+  float2* lags = ctx->arena.get<float2>("field:lags", i64(h) * t.nbox);
+  fold_lags_f32(ctx, w, n, h, int(s.count), t.nbox, t.pairs, t.lag_ptr, t.lag_st, lags);
+  const int nd = int(grid.size());
+  Dims box(size_t(nd), t.lb);
+  std::vector<float2*> mats(static_cast<size_t>(nd));
+  for (int a = 0; a < nd; ++a)
+    mats[size_t(a)] = dft_matrix(ctx, int(grid[size_t(a)]), t.lb, 2 * s.tau, center_index(grid[size_t(a)]), -1, 0.0);
+  float2* planes = ctx->arena.get<float2>("field:planes", i64(h) * numel(grid));
+  separable(ctx, lags, planes, h, box, grid, mats, "field:tmp");
+  return planes;
+}
+
+// ---------------------------------------------------------------- K5 pieces
+float2* run_recon(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float2* calib, const Dims& grid,
+                  double apod_width) {  // maps.cpp:130-160
+  const int nd = int(cdims.size());
+  std::vector<float2*> mats(static_cast<size_t>(nd));
+  for (int a = 0; a < nd; ++a) {
+    const double sigma = apod_width > 0 ? apod_width : double(cdims[size_t(a)]) / 4.0;
+    mats[size_t(a)] = dft_matrix(ctx, int(grid[size_t(a)]), int(cdims[size_t(a)]), co[size_t(a)],
+                                 center_index(grid[size_t(a)]), +1, sigma);
+  }
+  float2* recon = ctx->arena.get<float2>("post:recon", q * numel(grid));
+  separable(ctx, calib, recon, q, cdims, grid, mats, "post:tmp");
+  return recon;
+}
+
+void run_interp(sk_ctx* ctx, const float2* low, float2* out, i64 batch, const Dims& low_dims, const Dims& full) {
+  const int nd = int(low_dims.size());
+  std::vector<float2*> mats(static_cast<size_t>(nd));
+  for (int a = 0; a < nd; ++a) mats[size_t(a)] = sinc_matrix(ctx, int(full[size_t(a)]), int(low_dims[size_t(a)]));
+  separable(ctx, low, out, batch, low_dims, full, mats, "interp:tmp");
+}
+
+// ---------------------------------------------------------------- pipeline
+struct PipelineOut {
+  float2* maps = nullptr;     // device [Q][N_full] (nullable)
+  float* lambda = nullptr;    // device [N_full]
+  uint8_t* mask = nullptr;    // device [N_full]
+  float2* gram = nullptr;     // debug: device n x n
+  float2* field = nullptr;    // debug: device GramField layout (grid)
+  float2* raw_maps = nullptr; // debug: device [Q][N_grid]
+  float* raw_lambda = nullptr;
+  double* spectrum = nullptr; // host n
+};
+
+void validate_config(const sk_config* cfg) {
+  if (!cfg) fail(SK_ERR_DIM, "null config");
+  if (cfg->gram != 1) fail(SK_ERR_UNSUPPORTED, "gram = explicit is the baseline arm; the B200 path runs gram_fft");
+  if (cfg->eig != 1) fail(SK_ERR_UNSUPPORTED, "eig = dense is the baseline arm; the B200 path runs power iteration");
+  if (cfg->field != 1) fail(SK_ERR_UNSUPPORTED, "field = naive is the H(x) baseline; the B200 path runs the fast field");
+  if (cfg->kernel != 0 && cfg->kernel != 1) fail(SK_ERR_DIM, "unknown kernel shape");
+  if (cfg->power_iters < 0) fail(SK_ERR_DIM, "power_iters must be >= 0");
+}
+
+void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float2* calib, const Dims& full,
+              const sk_config* cfg, PipelineOut& out, sk_provenance* prov) {
+  validate_config(cfg);
+  const int nd = int(cdims.size());
+  if (full.size() != cdims.size()) fail(SK_ERR_DIM, "full_dims rank mismatch");  // maps.cpp:267-271
+  for (int a = 0; a < nd; ++a)
+    if (full[size_t(a)] < cdims[size_t(a)]) fail(SK_ERR_DIM, "full_dims must be at least the calibration extent");
+  const Support s = make_support(cfg->kernel, cfg->tau, nd);
+  check_calib(cdims, q, s);
+  if (q > 64) fail(SK_ERR_UNSUPPORTED, "more than 64 channels is outside the B200 path");
+  // grid_dims_for (maps.cpp:188-193) or the explicit grid.
+  Dims grid(static_cast<size_t>(nd));
+  bool explicit_grid = true;
+  for (int a = 0; a < nd; ++a) explicit_grid = explicit_grid && cfg->grid_dims[a] > 0;
+  for (int a = 0; a < nd; ++a) {
+    if (explicit_grid)
+      grid[size_t(a)] = cfg->grid_dims[a];
+    else if (cfg->grid == 1)
+      grid[size_t(a)] = std::min(cdims[size_t(a)] + cfg->grid_pad, full[size_t(a)]);
+    else
+      grid[size_t(a)] = full[size_t(a)];
+  }
+  for (int a = 0; a < nd; ++a) {
+    if (grid[size_t(a)] < cdims[size_t(a)]) fail(SK_ERR_DIM, "map grid smaller than calibration region");
+    if (full[size_t(a)] < grid[size_t(a)])
+      fail(SK_ERR_DIM, "interpolation target smaller than source on axis " + std::to_string(a));
+  }
+  const i64 lam = s.count, n = q * lam, ngrid = numel(grid), nfull = numel(full);
+  const bool interp = grid != full;
+
+  cudaEvent_t* ev = ctx->ev;
+  SKB_CUDA(cudaEventRecord(ev[0], ctx->stream));
+  // gram
+  float2* gram = run_gram(ctx, cdims, q, calib, s, out.gram);
+  SKB_CUDA(cudaEventRecord(ev[1], ctx->stream));
+  // nullspace
+  Eig e = run_eigh(ctx, gram, n, cfg->nullspace_threshold);
+  SKB_CUDA(cudaEventRecord(ev[2], ctx->stream));
+  // field
+  float2* planes = run_field(ctx, e, s, int(q), grid);
+  if (out.field) planes_to_field_full(ctx, planes, ngrid, int(q), out.field);
+  SKB_CUDA(cudaEventRecord(ev[3], ctx->stream));
+  // post (part 1): apodised recon on the map grid, consumed by K4's epilogue
+  float2* recon = run_recon(ctx, cdims, co, q, calib, grid, cfg->apod_width);
+  SKB_CUDA(cudaEventRecord(ev[4], ctx->stream));
+  // eigensolve (+ fused normalisation)
+  unsigned long long* zeroed = ctx->arena.get<unsigned long long>("post:zeroed", 1);
+  SKB_CUDA(cudaMemsetAsync(zeroed, 0, sizeof(unsigned long long), ctx->stream));
+  float2* maps_grid = (!interp && out.maps) ? out.maps : ctx->arena.get<float2>("post:maps_grid", q * ngrid);
+  float* lam_grid = (!interp && out.lambda) ? out.lambda : ctx->arena.get<float>("post:lam_grid", ngrid);
+  if (out.raw_maps) {
+    // raw (pre-normalisation) eigenvectors for parity dumps: run K4 without the epilogue first
+    PowerArgs r{};
+    r.planes = planes; r.n = ngrid; r.q = int(q); r.iters = cfg->power_iters;
+    r.alpha = 1.f; r.beta = -1.f / float(lam); r.lam_scale = 1.f / float(lam);
+    r.maps = out.raw_maps; r.lambda = out.raw_lambda;
+    power_iteration(ctx, r);
+  }
+  PowerArgs pa{};
+  pa.planes = planes;
+  pa.n = ngrid;
+  pa.q = int(q);
+  pa.iters = cfg->power_iters;
+  pa.alpha = 1.f;                    // B = I - G/|Lambda|
+  pa.beta = -1.f / float(lam);
+  pa.lam_scale = 1.f / float(lam);   // lambda = v^H G v / |Lambda| = 1 - v^H B v
+  pa.recon = recon;
+  pa.maps = maps_grid;
+  pa.lambda = lam_grid;
+  pa.mask = (!interp && out.mask) ? out.mask : nullptr;
+  pa.mask_threshold = float(cfg->mask_threshold);
+  pa.zeroed = zeroed;
+  power_iteration(ctx, pa);
+  SKB_CUDA(cudaEventRecord(ev[5], ctx->stream));
+  // post (part 2): interpolation + renormalisation + mask (maps.cpp:236-258)
+  if (interp) {
+    float2* maps_full = out.maps ? out.maps : ctx->arena.get<float2>("post:maps_full", q * nfull);
+    run_interp(ctx, maps_grid, maps_full, q, grid, full);
+    float2* lam_c = ctx->arena.get<float2>("post:lam_c", ngrid);
+    real_to_c64(ctx, lam_grid, lam_c, ngrid);
+    float2* lam_full_c = ctx->arena.get<float2>("post:lam_full_c", nfull);
+    run_interp(ctx, lam_c, lam_full_c, 1, grid, full);
+    renormalize_and_mask(ctx, maps_full, nfull, int(q), lam_full_c, out.lambda, out.mask, float(cfg->mask_threshold));
+  }
+  SKB_CUDA(cudaEventRecord(ev[6], ctx->stream));
+  unsigned long long h_zeroed = 0;
+  SKB_CUDA(cudaMemcpyAsync(&h_zeroed, zeroed, sizeof h_zeroed, cudaMemcpyDeviceToHost, ctx->stream));
+  SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (out.spectrum)
+    for (i64 i = 0; i < n; ++i) out.spectrum[i] = e.sigma1 > 0 ? e.spectrum[size_t(i)] / e.sigma1 : 0.0;
+  if (prov) {
+    float ms[6];
+    for (int i = 0; i < 6; ++i) SKB_CUDA(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+    std::memset(prov, 0, sizeof *prov);
+    for (int a = 0; a < nd; ++a) prov->grid_dims[a] = grid[size_t(a)];
+    prov->support_size = lam;
+    prov->valid_shifts = 1;
+    for (i64 d : cdims) prov->valid_shifts *= std::max<i64>(0, d - 2 * cfg->tau);
+    prov->nullspace_rank = e.rank;
+    prov->zeroed_voxels = i64(h_zeroed);
+    prov->sigma1 = e.sigma1;
+    prov->cut_margin = e.margin;
+    prov->stage_ms[0] = ms[0];
+    prov->stage_ms[1] = ms[1];
+    prov->stage_ms[2] = ms[2];
+    prov->stage_ms[3] = ms[4];
+    prov->stage_ms[4] = ms[3] + ms[5];
+    float total = 0;
+    SKB_CUDA(cudaEventElapsedTime(&total, ev[0], ev[6]));
+    prov->total_ms = total;
+  }
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return SK_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SK_ERR_OTHER;
+  }
+}
+
+void require_ctx(sk_ctx* ctx) {
+  if (!ctx) fail(SK_ERR_DIM, "null context");
+  SKB_CUDA(cudaSetDevice(ctx->device));
+}
+
+}  // namespace
+
+// ================================================================ C-ABI
+extern "C" {
+
+const char* sk_last_error(void) { return g_last_error.c_str(); }
+
+int sk_create(int device, sk_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(SK_ERR_DIM, "null output");
+    int count = 0;
+    SKB_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) fail(SK_ERR_CUDA, "no such CUDA device " + std::to_string(device));
+    SKB_CUDA(cudaSetDevice(device));
+    auto* ctx = new sk_ctx();
+    ctx->device = device;
+    SKB_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
+    SKB_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+    ctx->stream = ctx->own_stream;
+    check_cublas(cublasCreate(&ctx->cublas), "cublasCreate");
+    check_cublas(cublasSetStream(ctx->cublas, ctx->stream), "cublasSetStream");
+    check_cusolver(cusolverDnCreate(&ctx->cusolver), "cusolverDnCreate");
+    check_cusolver(cusolverDnSetStream(ctx->cusolver, ctx->stream), "cusolverDnSetStream");
+    check_cusolver(cusolverDnCreateParams(&ctx->cusolver_params), "cusolverDnCreateParams");
+    for (auto& e : ctx->ev) SKB_CUDA(cudaEventCreate(&e));
+    *out = ctx;
+  });
+}
+
+int sk_destroy(sk_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->arena.release_all();
+    for (auto& e : ctx->ev) cudaEventDestroy(e);
+    cusolverDnDestroyParams(ctx->cusolver_params);
+    cusolverDnDestroy(ctx->cusolver);
+    cublasDestroy(ctx->cublas);
+    cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+  });
+}
+
+int sk_set_stream(sk_ctx* ctx, void* stream) {
+  return guarded([&] {
+    require_ctx(ctx);
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    check_cublas(cublasSetStream(ctx->cublas, ctx->stream), "cublasSetStream");
+    check_cusolver(cusolverDnSetStream(ctx->cusolver, ctx->stream), "cusolverDnSetStream");
+  });
+}
+
+int64_t sk_kernel_launches(const sk_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int64_t sk_library_calls(const sk_ctx* ctx) { return ctx ? ctx->lib_calls : 0; }
+
+int sk_make_support(int shape, int tau, int ndim, int32_t* offsets, int64_t* count) {
+  return guarded([&] {
+    const Support s = make_support(shape, tau, ndim);
+    if (count) *count = s.count;
+    if (offsets) std::copy(s.offsets.begin(), s.offsets.end(), offsets);
+  });
+}
+
+int sk_reduced_grid_dims(int ndim, const int64_t* calib_dims, int64_t pad, const int64_t* full_dims, int64_t* out) {
+  return guarded([&] {
+    for (int a = 0; a < ndim; ++a) out[a] = std::min(calib_dims[a] + pad, full_dims[a]);
+  });
+}
+
+int sk_gram_fft(sk_ctx* ctx, int ndim, const int64_t* calib_dims, int64_t channels, const sk_c64* calib, int shape,
+                int tau, sk_c64* gram) {
+  return guarded([&] {
+    require_ctx(ctx);
+    const Dims cd = dims_of(ndim, calib_dims);
+    const Support s = make_support(shape, tau, ndim);
+    check_calib(cd, channels, s);
+    const i64 n = channels * s.count;
+    const float2* d_cal = device_in(ctx, reinterpret_cast<const float2*>(calib), channels * numel(cd), "in:calib");
+    Out<float2> g(ctx, reinterpret_cast<float2*>(gram), n * n, "out:gram");
+    run_gram(ctx, cd, channels, d_cal, s, g.dev);
+    g.finish(ctx);
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_extract_nullspace(sk_ctx* ctx, int64_t n, const sk_c64* gram, double ratio, int64_t* rank, double* spectrum,
+                         sk_c64* filters, int64_t filters_capacity) {
+  return guarded([&] {
+    require_ctx(ctx);
+    const float2* d_g = device_in(ctx, reinterpret_cast<const float2*>(gram), n * n, "in:gram");
+    Eig e = run_eigh(ctx, d_g, n, ratio);
+    if (rank) *rank = e.rank;
+    if (spectrum) std::copy(e.spectrum.begin(), e.spectrum.end(), spectrum);
+    if (filters) {
+      if (filters_capacity < e.rank) fail(SK_ERR_DIM, "filters buffer has fewer columns than the nullspace rank");
+      Out<float2> f(ctx, reinterpret_cast<float2*>(filters), n * e.rank, "out:filters");
+      c128_to_c64(ctx, e.evecs, f.dev, n * e.rank);
+      f.finish(ctx);
+    }
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_aggregate_w(sk_ctx* ctx, int64_t n, int64_t r, const sk_c64* filters, sk_c64* w) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (r < 1) fail(SK_ERR_NULLSPACE_EMPTY, "aggregate requires at least one filter");  // spatial_gram.cpp:88
+    const float2* d_f = device_in(ctx, reinterpret_cast<const float2*>(filters), n * r, "in:filters");
+    Out<float2> o(ctx, reinterpret_cast<float2*>(w), n * n, "out:w");
+    const cuComplex one = make_cuComplex(1.f, 0.f), zero = make_cuComplex(0.f, 0.f);
+    check_cublas(cublasCgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_C, int(n), int(n), int(r), &one,
+                             reinterpret_cast<const cuComplex*>(d_f), int(n), reinterpret_cast<const cuComplex*>(d_f),
+                             int(n), &zero, reinterpret_cast<cuComplex*>(o.dev), int(n)),
+                 "Cgemm");
+    ++ctx->lib_calls;
+    o.finish(ctx);
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_gram_field_fast(sk_ctx* ctx, int64_t q, const sk_c64* w, int shape, int tau, int ndim, const int64_t* dims,
+                       sk_c64* field) {
+  return guarded([&] {
+    require_ctx(ctx);
+    const Dims grid = dims_of(ndim, dims);
+    const Support s = make_support(shape, tau, ndim);
+    if (i64(grid.size()) != s.nd) fail(SK_ERR_DIM, "voxel grid rank does not match support dimension");
+    for (i64 d : grid)
+      if (d < 1) fail(SK_ERR_DIM, "voxel grid extents must be >= 1");
+    if (4 * tau + 1 > 29) fail(SK_ERR_UNSUPPORTED, "kernel radius > 7 is outside the B200 path");
+    const i64 n = q * s.count, ng = numel(grid);
+    const float2* d_w = device_in(ctx, reinterpret_cast<const float2*>(w), n * n, "in:w");
+    float2* planes = run_field_from_w(ctx, d_w, s, int(q), grid);
+    Out<float2> f(ctx, reinterpret_cast<float2*>(field), ng * q * q, "out:field");
+    planes_to_field_full(ctx, planes, ng, int(q), f.dev);
+    f.finish(ctx);
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_espirit_inplace(sk_ctx* ctx, int64_t voxels, int64_t q, sk_c64* field, int64_t support_size) {
+  return guarded([&] {
+    require_ctx(ctx);
+    const i64 cnt = voxels * q * q;
+    const bool dev = is_device_ptr(field);
+    float2* d = dev ? reinterpret_cast<float2*>(field) : ctx->arena.get<float2>("io:field", cnt);
+    if (!dev) SKB_CUDA(cudaMemcpyAsync(d, field, size_t(cnt) * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+    espirit_field(ctx, d, voxels, int(q), float(1.0 / double(support_size)));
+    if (!dev) SKB_CUDA(cudaMemcpyAsync(field, d, size_t(cnt) * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_eig_power_field(sk_ctx* ctx, int64_t voxels, int64_t q, const sk_c64* b_field, int iters, sk_c64* vectors,
+                       float* values) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (q > 64) fail(SK_ERR_UNSUPPORTED, "more than 64 channels is outside the B200 path");
+    const float2* d_b = device_in(ctx, reinterpret_cast<const float2*>(b_field), voxels * q * q, "in:field");
+    float2* planes = ctx->arena.get<float2>("field:planes", voxels * q * (q + 1) / 2);
+    field_full_to_planes(ctx, d_b, voxels, int(q), planes);
+    float2* maps = ctx->arena.get<float2>("power:maps", voxels * q);
+    Out<float> val(ctx, values, voxels, "out:values");
+    PowerArgs a{};
+    a.planes = planes;
+    a.n = voxels;
+    a.q = int(q);
+    a.iters = iters;
+    a.alpha = 0.f;  // B given directly
+    a.beta = 1.f;
+    a.lam_scale = 1.f;
+    a.maps = maps;
+    a.value = val.dev;
+    power_iteration(ctx, a);
+    // [Q][N] -> Q x N column per voxel (eigensolve.hpp:13): element (c, j) at c + j*Q
+    if (vectors) {
+      Out<float2> vec(ctx, reinterpret_cast<float2*>(vectors), voxels * q, "out:vectors");
+      // rows = voxels j, cols = channels c: src maps[c*N + j], dst vectors[c + j*Q]
+      copy_strided(ctx, maps, 1, voxels, vec.dev, q, 1, voxels, q);
+      vec.finish(ctx);
+    }
+    val.finish(ctx);
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_normalize_maps(sk_ctx* ctx, int ndim, const int64_t* dims, int64_t q, const sk_c64* raw,
+                      const int64_t* calib_dims, const int64_t* center_offset, const sk_c64* calib, double apod_width,
+                      sk_c64* out, int64_t* zeroed_voxels) {
+  return guarded([&] {
+    require_ctx(ctx);
+    const Dims grid = dims_of(ndim, dims), cd = dims_of(ndim, calib_dims), co = dims_of(ndim, center_offset);
+    for (int a = 0; a < ndim; ++a)
+      if (grid[size_t(a)] < cd[size_t(a)]) fail(SK_ERR_DIM, "map grid smaller than calibration region");
+    const i64 ng = numel(grid);
+    const float2* d_raw = device_in(ctx, reinterpret_cast<const float2*>(raw), q * ng, "in:raw");
+    const float2* d_cal = device_in(ctx, reinterpret_cast<const float2*>(calib), q * numel(cd), "in:calib");
+    float2* recon = run_recon(ctx, cd, co, q, d_cal, grid, apod_width);
+    Out<float2> o(ctx, reinterpret_cast<float2*>(out), q * ng, "out:maps");
+    SKB_CUDA(cudaMemcpyAsync(o.dev, d_raw, size_t(q * ng) * sizeof(float2), cudaMemcpyDeviceToDevice, ctx->stream));
+    unsigned long long* z = ctx->arena.get<unsigned long long>("post:zeroed", 1);
+    SKB_CUDA(cudaMemsetAsync(z, 0, sizeof(unsigned long long), ctx->stream));
+    normalize_standalone(ctx, o.dev, ng, int(q), recon, z);
+    o.finish(ctx);
+    unsigned long long hz = 0;
+    SKB_CUDA(cudaMemcpyAsync(&hz, z, sizeof hz, cudaMemcpyDeviceToHost, ctx->stream));
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (zeroed_voxels) *zeroed_voxels = i64(hz);
+  });
+}
+
+int sk_interpolate_maps(sk_ctx* ctx, int ndim, const int64_t* low_dims, int64_t q, const sk_c64* low,
+                        const int64_t* full_dims, sk_c64* out) {
+  return guarded([&] {
+    require_ctx(ctx);
+    const Dims ld = dims_of(ndim, low_dims), fd = dims_of(ndim, full_dims);
+    for (int a = 0; a < ndim; ++a)
+      if (fd[size_t(a)] < ld[size_t(a)])
+        fail(SK_ERR_DIM, "interpolation target smaller than source on axis " + std::to_string(a));
+    const float2* d_low = device_in(ctx, reinterpret_cast<const float2*>(low), q * numel(ld), "in:low");
+    Out<float2> o(ctx, reinterpret_cast<float2*>(out), q * numel(fd), "out:interp");
+    run_interp(ctx, d_low, o.dev, q, ld, fd);
+    o.finish(ctx);
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_interpolate_real(sk_ctx* ctx, int ndim, const int64_t* low_dims, const float* low, const int64_t* full_dims,
+                        float* out) {
+  return guarded([&] {
+    require_ctx(ctx);
+    const Dims ld = dims_of(ndim, low_dims), fd = dims_of(ndim, full_dims);
+    for (int a = 0; a < ndim; ++a)
+      if (fd[size_t(a)] < ld[size_t(a)])
+        fail(SK_ERR_DIM, "interpolation target smaller than source on axis " + std::to_string(a));
+    const float* d_low = device_in(ctx, low, numel(ld), "in:lowr");
+    float2* lc = ctx->arena.get<float2>("interp:lc", numel(ld));
+    real_to_c64(ctx, d_low, lc, numel(ld));
+    float2* fc = ctx->arena.get<float2>("interp:fc", numel(fd));
+    run_interp(ctx, lc, fc, 1, ld, fd);
+    Out<float> o(ctx, out, numel(fd), "out:interpr");
+    renormalize_and_mask(ctx, nullptr, numel(fd), 0, fc, o.dev, nullptr, 0.f);
+    o.finish(ctx);
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_support_mask(sk_ctx* ctx, int64_t voxels, const float* lambda, double thr, uint8_t* mask) {
+  return guarded([&] {
+    require_ctx(ctx);
+    const float* d_l = device_in(ctx, lambda, voxels, "in:lambda");
+    Out<uint8_t> o(ctx, mask, voxels, "out:mask");
+    mask_kernel(ctx, d_l, voxels, float(thr), o.dev);
+    o.finish(ctx);
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset,
+                           int64_t q, const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg,
+                           sk_c64* maps, float* lambda, uint8_t* mask, double* spectrum, sk_provenance* prov,
+                           sk_c64* gram_out, sk_c64* field_out, sk_c64* raw_maps_out, float* raw_lambda_out) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (ndim < 1) fail(SK_ERR_DIM, "stack needs at least one axis");
+    const Dims cd = dims_of(ndim, calib_dims), co = dims_of(ndim, center_offset), fd = dims_of(ndim, full_dims);
+    for (i64 d : cd)
+      if (d < 1) fail(SK_ERR_DIM, "stack axis extents must be >= 1");
+    if (q < 1) fail(SK_ERR_DIM, "stack needs at least one channel");
+    const i64 nfull = numel(fd);
+    const float2* d_cal = device_in(ctx, reinterpret_cast<const float2*>(calib), q * numel(cd), "in:calib");
+    Out<float2> om(ctx, reinterpret_cast<float2*>(maps), q * nfull, "out:maps");
+    Out<float> ol(ctx, lambda, nfull, "out:lambda");
+    Out<uint8_t> ok(ctx, mask, nfull, "out:mask");
+    // debug dumps need sizes: derive them the same way the pipeline does
+    const Support s = make_support(cfg ? cfg->kernel : 0, cfg ? cfg->tau : 0, ndim);
+    const i64 n = q * s.count;
+    Dims grid(static_cast<size_t>(ndim));
+    if (cfg) {
+      bool ex = true;
+      for (int a = 0; a < ndim; ++a) ex = ex && cfg->grid_dims[a] > 0;
+      for (int a = 0; a < ndim; ++a)
+        grid[size_t(a)] = ex ? cfg->grid_dims[a]
+                             : (cfg->grid == 1 ? std::min(cd[size_t(a)] + cfg->grid_pad, fd[size_t(a)]) : fd[size_t(a)]);
+    }
+    const i64 ng = numel(grid);
+    Out<float2> og(ctx, reinterpret_cast<float2*>(gram_out), n * n, "dbg:gram");
+    Out<float2> of(ctx, reinterpret_cast<float2*>(field_out), ng * q * q, "dbg:field");
+    Out<float2> orm(ctx, reinterpret_cast<float2*>(raw_maps_out), q * ng, "dbg:raw");
+    Out<float> orl(ctx, raw_lambda_out, ng, "dbg:rawl");
+    std::vector<double> spec(size_t(std::max<i64>(n, 1)));
+    PipelineOut po;
+    po.maps = om.dev;
+    po.lambda = ol.dev;
+    po.mask = ok.dev;
+    po.gram = og.dev;
+    po.field = of.dev;
+    po.raw_maps = orm.dev;
+    po.raw_lambda = orl.dev;
+    po.spectrum = spectrum ? spec.data() : nullptr;
+    pipeline(ctx, cd, co, q, d_cal, fd, cfg, po, prov);
+    om.finish(ctx);
+    ol.finish(ctx);
+    ok.finish(ctx);
+    og.finish(ctx);
+    of.finish(ctx);
+    orm.finish(ctx);
+    orl.finish(ctx);
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (spectrum) std::copy(spec.begin(), spec.begin() + n, spectrum);
+  });
+}
+
+int sk_estimate_maps(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset, int64_t q,
+                     const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg, sk_c64* maps, float* lambda,
+                     uint8_t* mask, double* spectrum, sk_provenance* prov) {
+  return sk_estimate_maps_debug(ctx, ndim, calib_dims, center_offset, q, calib, full_dims, cfg, maps, lambda, mask,
+                                spectrum, prov, nullptr, nullptr, nullptr, nullptr);
+}
+
+int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_t* calib_dims,
+                             const int64_t* center_offset, int64_t q, const sk_c64* calib, const int64_t* full_dims,
+                             const sk_config* cfg, sk_c64* maps, float* lambda, uint8_t* mask, sk_provenance* prov) {
+  const Dims cd = dims_of(ndim, calib_dims), fd = dims_of(ndim, full_dims);
+  const i64 ncal = q * numel(cd), nfull = numel(fd);
+  for (i64 s = 0; s < slices; ++s) {
+    const int rc = sk_estimate_maps(ctx, ndim, calib_dims, center_offset, q, calib + s * ncal, full_dims, cfg,
+                                    maps ? maps + s * q * nfull : nullptr, lambda ? lambda + s * nfull : nullptr,
+                                    mask ? mask + s * nfull : nullptr, nullptr, prov ? prov + s : nullptr);
+    if (rc != SK_OK) return rc;
+  }
+  return SK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,299 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the FP64 oracle.
+
+Every test here needs a B200 and is marked ``gpu``.  Inputs are seeded; the
+oracle sees the same float32 calibration the GPU sees (promoted to double, as
+io.cpp:66-67 does when it loads a CStack).  A JSON report of every measured
+error is appended to gpurun_out/parity_report.jsonl for the record.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from tests import parity as PM
+
+pytestmark = pytest.mark.gpu
+
+REPORT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out",
+                      "parity_report.jsonl")
+
+
+def report(name, **kw):
+    os.makedirs(os.path.dirname(REPORT), exist_ok=True)
+    with open(REPORT, "a") as f:
+        f.write(json.dumps({"test": name, **kw}) + "\n")
+
+
+@pytest.fixture(scope="module")
+def K():
+    import paper_2302_13431_b200 as K
+    K.default_context(0)
+    return K
+
+
+def rnd(shape, seed, dtype=np.complex64):
+    r = np.random.default_rng(seed)
+    return (r.standard_normal(shape) + 1j * r.standard_normal(shape)).astype(dtype)
+
+
+def rnd_orthonormal(rows, cols, seed):
+    q, _ = np.linalg.qr(rnd((rows, cols), seed, np.complex128))
+    return q
+
+
+def f32(a):
+    """What the oracle sees: the float32 values, promoted."""
+    return np.asarray(a, dtype=np.complex64).astype(np.complex128)
+
+
+# ------------------------------------------------------------------- K1 gram
+@pytest.mark.parametrize("shape,tau,dims,q", [
+    (1, 3, (24, 24), 8), (1, 5, (32, 32), 4), (0, 2, (14, 16), 3), (1, 2, (9, 10, 8), 2), (0, 1, (12,), 3),
+    (1, 4, (24, 24), 6),
+])
+def test_gram_fft_parity(K, O, shape, tau, dims, q):
+    cal = rnd((q,) + dims, 1)
+    g = K.gram_fft(K.Calib(cal, tuple(d // 2 for d in dims)), shape, tau)
+    ref = O.gram_fft(O.Calib(f32(cal), tuple(d // 2 for d in dims)), shape, tau)
+    err = PM.rel_fro(g, ref)
+    report("gram_fft", shape=shape, tau=tau, dims=dims, q=q, rel_fro=err)
+    assert err < PM.TOL_GRAM
+    assert np.abs(g - g.conj().T).max() == 0.0  # exactly Hermitian by construction
+
+
+def test_gram_fft_errors(K):
+    with pytest.raises(K.DimError):
+        K.gram_fft(K.Calib(rnd((1, 6, 6), 3), (3, 3)), K.RECT, 3)  # calibration.cpp:15-19
+
+
+# ------------------------------------------------------------------ K2 nullspace
+def test_nullspace_known_answers(K):  # test_nullspace.cpp:22-43
+    b = K.extract_nullspace(np.diag([4.0, 1.0, 1e-6]).astype(np.complex64), 0.05)
+    assert b.rank == 1
+    assert np.allclose(b.spectrum, [2.0, 1.0, 1e-3], rtol=1e-6)
+    assert abs(abs(b.filters[2, 0]) - 1) < 1e-6
+    with pytest.raises(K.NullspaceEmptyError):
+        K.extract_nullspace(np.eye(4, dtype=np.complex64), 0.05)
+    for r in (0.0, 1.0):
+        with pytest.raises(K.DimError):
+            K.extract_nullspace(np.eye(2, dtype=np.complex64), r)
+
+
+def test_nullspace_parity(K, O):
+    cal = rnd((4, 24, 24), 7)
+    st = cal.copy()
+    st[1] = 1j * st[0]  # rank-deficient: a real nullspace
+    g = O.gram_fft(O.Calib(f32(st), (12, 12)), 1, 3)
+    gb = K.extract_nullspace(g.astype(np.complex64), 0.05)
+    ob = O.extract_nullspace(f32(g.astype(np.complex64)), 0.05)
+    assert gb.rank == ob.rank
+    assert np.abs(gb.spectrum - ob.spectrum).max() < 1e-6 * ob.spectrum[0]
+    wg = gb.filters.astype(np.complex128) @ gb.filters.conj().T.astype(np.complex128)
+    wo = ob.filters @ ob.filters.conj().T
+    report("nullspace", rank=gb.rank, w_rel_fro=PM.rel_fro(wg, wo))
+    assert PM.rel_fro(wg, wo) < 1e-4
+    wa = K.aggregate_w(gb.filters)
+    assert PM.rel_fro(wa, wo) < 1e-4
+
+
+# -------------------------------------------------------------------- K3 field
+@pytest.mark.parametrize("dims,shape,tau,q", [((8, 8), 0, 1, 3), ((5, 8), 0, 1, 3), ((4, 4), 0, 1, 3),
+                                              ((16, 12), 1, 2, 4), ((6, 5, 4), 1, 1, 2)])
+def test_gram_field_fast_parity(K, O, dims, shape, tau, q):  # test_spatial_gram.cpp:160-170
+    lam = O.make_support(shape, tau, len(dims)).shape[0]
+    F = rnd_orthonormal(q * lam, max(2, q * lam // 3), 35)
+    W = O.aggregate_w(F)
+    got = K.gram_field_fast(W.astype(np.complex64), q, shape, tau, dims)
+    ref = O.gram_field_fast(f32(W.astype(np.complex64)), q, shape, tau, dims)
+    err = PM.rel_fro(got, ref)
+    report("gram_field_fast", dims=dims, rel_fro=err)
+    assert err < PM.TOL_FIELD
+
+
+# -------------------------------------------------------------------- K4 power
+@pytest.mark.parametrize("q", [2, 3, 8, 13, 32, 40, 64])
+def test_power_parity(K, O, q):
+    n = 300
+    m = rnd((n, q, q), 11, np.complex128)
+    herm = (m + m.conj().transpose(0, 2, 1)) / 2
+    herm = (herm + 2.5 * q ** 0.5 * np.eye(q)).astype(np.complex64)  # well-separated top eigenvalue
+    vg, valg = K.eig_power_field(herm, 30)
+    vo, valo = O.eig_power_field(f32(herm), 30)
+    ph = np.sum(vo.conj() * vg, 0)
+    ph = ph / np.abs(ph)
+    err_v = np.abs(vg - vo * ph[None]).max()
+    err_l = PM.rel_fro(valg, valo)
+    report("power", q=q, vec_max=float(err_v), value_rel=err_l)
+    assert err_v < 1e-3 and err_l < 1e-5
+
+
+def test_power_known_answers(K):  # test_eigensolve.cpp:67-83, eigensolve.cpp:56-66
+    v, val = K.eig_power_field(np.diag([1.0, 0.1]).astype(np.complex64)[None], 10)
+    assert abs(abs(v[0, 0]) - 1) < 1e-6 and abs(val[0] - 1) < 1e-6
+    v, _ = K.eig_power_field(np.eye(3, dtype=np.complex64)[None], 10)
+    assert np.abs(v[:, 0] - 1 / np.sqrt(3)).max() < 1e-6
+    b = (np.array([[1, -1], [-1, 1]], dtype=np.complex64) / 2)[None]
+    v, val = K.eig_power_field(b, 5)
+    assert abs(abs(v[0, 0]) - 2 ** -0.5) < 1e-6 and abs(val[0] - 1) < 1e-6
+    v, val = K.eig_power_field(np.zeros((1, 3, 3), np.complex64), 5)
+    assert np.array_equal(v[:, 0], [1, 0, 0]) and val[0] == 0
+
+
+def test_espirit(K, O):
+    f = rnd((50, 5, 5), 3)
+    assert np.abs(K.espirit(f, 9) - O.espirit(f32(f), 9)).max() < 1e-6
+
+
+# ---------------------------------------------------------------------- K5 post
+def test_interpolation_parity(K, O):
+    x = rnd((3, 10, 12), 5)
+    got = K.interpolate_maps(x, (40, 36))
+    ref = O.interpolate_maps(f32(x), (40, 36))
+    assert PM.rel_fro(got, ref) < 1e-5
+    low = np.zeros((2, 8, 8), np.complex64)
+    low[0] = 0.3 - 0.2j
+    up = K.interpolate_maps(low, (32, 32))
+    assert np.abs(up[0] - (0.3 - 0.2j)).max() < 1e-6
+    lr = np.random.default_rng(1).random((10, 12)).astype(np.float32)
+    assert PM.rel_fro(K.interpolate_real(lr, (40, 36)), O.interpolate_real(lr.astype(np.float64), (40, 36))) < 1e-5
+    with pytest.raises(K.DimError):
+        K.interpolate_maps(rnd((1, 8, 8), 64), (4, 8))
+
+
+def test_normalize_parity(K, O):
+    raw = rnd((4, 20, 18), 65)
+    cal = rnd((4, 8, 8), 66)
+    got, z = K.normalize_maps(raw, K.Calib(cal, (4, 4)))
+    ref, zo = O.normalize_maps(f32(raw), O.Calib(f32(cal), (4, 4)))
+    assert z == zo == 0
+    assert PM.rel_fro(got, ref) < 1e-5
+    m = np.zeros((2, 4, 4), np.complex64)
+    m[0, 0, 0] = 1
+    _, z = K.normalize_maps(m, K.Calib(np.ones((2, 1, 1), np.complex64), (0, 0)))
+    assert z == 15
+
+
+def test_support_mask(K):  # test_maps.cpp:19-23
+    lam = np.zeros(5, np.float32)
+    assert K.support_mask(lam, 0.1).tolist() == [1] * 5
+    assert K.support_mask(lam, 0.0).tolist() == [0] * 5
+
+
+# ------------------------------------------------------------------ end to end
+def _pipeline_case(K, O, calib, co, full, cfgk, cfgo, grid=None, name=""):
+    res = K.estimate_maps(K.Calib(calib, co), full, cfgk, want_raw=True)
+    ref = O.estimate_maps(O.Calib(f32(calib), co), full, cfgo, grid_dims=grid, want_raw=True)
+    assert res.nullspace_rank == ref.nullspace_rank, (res.nullspace_rank, ref.nullspace_rank)
+    assert np.abs(res.spectrum_normalized - ref.spectrum_normalized).max() < 1e-5
+    lam_raw = PM.lambda_errors(res.raw_lambda, ref.raw_lambda)
+    lam_fin = PM.lambda_errors(res.lambda_min_map, ref.lambda_min_map, ref.support_mask)
+    nrmse = PM.maps_nrmse(res.maps, ref.maps, ref.support_mask)
+    raw_nrmse = PM.maps_nrmse(res.raw_maps, ref.raw_maps, np.ones(res.raw_lambda.shape))
+    mask_agree = float(np.mean(res.support_mask == ref.support_mask))
+    report("estimate_maps", case=name, rank=res.nullspace_rank, cut_margin=res.cut_margin, lambda_raw=lam_raw,
+           lambda_final=lam_fin, maps_nrmse=nrmse, raw_maps_nrmse_all=raw_nrmse, mask_agree=mask_agree,
+           stage_ms=res.stage_ms, total_ms=res.total_ms)
+    assert lam_raw["normwise"] < PM.TOL_LAMBDA
+    assert lam_fin["normwise"] < PM.TOL_LAMBDA
+    assert nrmse < PM.TOL_MAPS
+    assert mask_agree > 0.999
+    # unit sum-of-squares inside the mask (test_maps.cpp:137-146)
+    m = res.maps.reshape(res.maps.shape[0], -1)[:, res.support_mask.ravel() > 0]
+    assert np.abs(np.sum(np.abs(m) ** 2, 0) - 1).max() < 1e-4
+    return res, ref
+
+
+def _cfgs(K, O, spec):
+    ck = K.PipelineConfig(kernel=spec.kernel, tau=spec.tau, nullspace_threshold=spec.nullspace_threshold,
+                          power_iters=spec.power_iters,
+                          grid=K.GRID_FULL if spec.full_grid else K.GRID_REDUCED,
+                          grid_pad=spec.grid_dims[0] - spec.calib[0])
+    co = O.PipelineConfig.pisco()
+    co.kernel, co.tau, co.nullspace_threshold = spec.kernel, spec.tau, spec.nullspace_threshold
+    co.power_iters = spec.power_iters
+    co.grid = O.GRID_FULL if spec.full_grid else O.GRID_REDUCED
+    co.grid_pad = spec.grid_dims[0] - spec.calib[0]
+    return ck, co
+
+
+def test_estimate_maps_c1(K, O):
+    from paper_2302_13431_b200 import phantom
+    case = phantom.generate("C1")
+    ck, co = _cfgs(K, O, case.spec)
+    res, _ = _pipeline_case(K, O, case.calib[0], case.center_offset, case.spec.full_dims, ck, co, name="C1")
+    assert res.grid_dims == (64, 64)
+
+
+def test_estimate_maps_c2(K, O):
+    from paper_2302_13431_b200 import phantom
+    case = phantom.generate("C2")
+    ck, co = _cfgs(K, O, case.spec)
+    _pipeline_case(K, O, case.calib[0], case.center_offset, case.spec.full_dims, ck, co, name="C2")
+
+
+def test_estimate_maps_small_variants(K, O):
+    # noisy reference scene, rect kernel, reduced grid with odd sizes, 3-D explicit grid
+    sc = O.simulate(6, (48, 40), 2, 5, noise_sigma=0.01, noise_seed=6)
+    cal = O.extract_calibration(sc["kspace"], (20, 18))
+    calib = cal.data.astype(np.complex64)
+    ck = K.PipelineConfig(kernel=K.RECT, tau=2, grid_pad=10, power_iters=25)
+    co = O.PipelineConfig.pisco()
+    co.kernel, co.tau, co.grid_pad, co.power_iters = O.RECT, 2, 10, 25
+    _pipeline_case(K, O, calib, cal.center_offset, (48, 40), ck, co, name="rect-reduced-odd")
+    sc3 = O.simulate(4, (20, 18, 16), 1, 9, noise_sigma=0.01, noise_seed=2)
+    cal3 = O.extract_calibration(sc3["kspace"], (10, 10, 8))
+    ck3 = K.PipelineConfig(kernel=K.ELLIPSOID, tau=2, power_iters=15, grid_dims=(14, 12, 10))
+    co3 = O.PipelineConfig.pisco()
+    co3.tau, co3.power_iters = 2, 15
+    _pipeline_case(K, O, cal3.data.astype(np.complex64), cal3.center_offset, (20, 18, 16), ck3, co3,
+                   grid=(14, 12, 10), name="3d-explicit-grid")
+
+
+def test_field_parity_in_pipeline(K, O):
+    from paper_2302_13431_b200 import phantom
+    case = phantom.generate("C1")
+    ck, co = _cfgs(K, O, case.spec)
+    res = K.estimate_maps(K.Calib(case.calib[0], case.center_offset), case.spec.full_dims, ck, want_gram=True,
+                          want_field=True)
+    cal = O.Calib(f32(case.calib[0]), case.center_offset)
+    g = O.gram_fft(cal, ck.kernel, ck.tau)
+    assert PM.rel_fro(res.gram, g) < PM.TOL_GRAM
+    b = O.extract_nullspace(g, 0.05)
+    field = O.gram_field_fast(O.aggregate_w(b.filters), 8, ck.kernel, ck.tau, (64, 64))
+    err = PM.rel_fro(res.field, field)
+    report("field_in_pipeline", case="C1", gram_rel=PM.rel_fro(res.gram, g), field_rel=err)
+    assert err < PM.TOL_FIELD
+
+
+def test_pipeline_errors(K):  # test_maps.cpp:192-217
+    st = rnd((2, 12, 12), 79)
+    cfg = K.PipelineConfig(kernel=K.RECT, tau=0, grid=K.GRID_FULL)
+    with pytest.raises(K.NullspaceEmptyError):
+        K.estimate_maps(K.Calib(st, (6, 6)), (12, 12), cfg)
+    with pytest.raises(K.DimError):
+        K.estimate_maps(K.Calib(rnd((2, 8, 8), 80), (4, 4)), (8, 8), K.PipelineConfig(kernel=K.RECT, tau=4))
+    with pytest.raises(K.DimError):
+        K.estimate_maps(K.Calib(st, (6, 6)), (8, 8), K.PipelineConfig())
+    with pytest.raises(K.UnsupportedError):
+        K.estimate_maps(K.Calib(st, (6, 6)), (12, 12), K.PipelineConfig(gram=0))
+
+
+def test_determinism_and_device_buffers(K):
+    import torch
+    from paper_2302_13431_b200 import phantom
+    case = phantom.generate("C1")
+    ck = K.PipelineConfig(tau=3, power_iters=30, grid_pad=40)
+    a = K.estimate_maps(K.Calib(case.calib[0], case.center_offset), (256, 256), ck)
+    b = K.estimate_maps(K.Calib(case.calib[0], case.center_offset), (256, 256), ck)
+    assert np.array_equal(a.maps, b.maps) and np.array_equal(a.lambda_min_map, b.lambda_min_map)
+    ctx = K.default_context(0)
+    cal = torch.from_numpy(case.calib[0]).cuda()
+    maps = torch.empty((8, 256, 256), dtype=torch.complex64, device="cuda")
+    lam = torch.empty((256, 256), dtype=torch.float32, device="cuda")
+    mask = torch.empty((256, 256), dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    K.api.estimate_maps_device(ctx, cal.data_ptr(), (24, 24), case.center_offset, 8, (256, 256), ck,
+                               maps.data_ptr(), lam.data_ptr(), mask.data_ptr())
+    assert np.array_equal(maps.cpu().numpy(), a.maps)
+    assert np.array_equal(mask.cpu().numpy(), a.support_mask)
