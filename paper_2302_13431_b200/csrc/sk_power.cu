@@ -131,11 +131,18 @@ __global__ void __launch_bounds__(256) power_kernel(PowerArgs a) {
     matvec(mv);
     float2 w = make_float2(a.alpha * vp.x + a.beta * mv.x, a.alpha * vp.y + a.beta * mv.y);
     float nrm = sqrtf(group_sum<QP>(w.x * w.x + w.y * w.y, red, vox, half));
-    if (it == 0 && nrm < 1e-14f) {
+    if (it == 0) {
       // All-ones start annihilated: restart from e_0 (eigensolve.cpp:58-63).
-      vp = (p == 0) ? make_float2(1.f, 0.f) : make_float2(0.f, 0.f);
-      w = make_float2(a.alpha * vp.x + a.beta * m[0].x, a.alpha * vp.y + a.beta * m[0].y);
-      nrm = sqrtf(group_sum<QP>(w.x * w.x + w.y * w.y, red, vox, half));
+      // The e_0 candidate is formed by every thread (the reductions must stay
+      // warp/block-uniform) and selected per voxel.
+      const float2 v0 = (p == 0) ? make_float2(1.f, 0.f) : make_float2(0.f, 0.f);
+      const float2 w0 = make_float2(a.alpha * v0.x + a.beta * m[0].x, a.alpha * v0.y + a.beta * m[0].y);
+      const float nrm0 = sqrtf(group_sum<QP>(w0.x * w0.x + w0.y * w0.y, red, vox, half));
+      if (nrm < 1e-14f) {
+        vp = v0;
+        w = w0;
+        nrm = nrm0;
+      }
     }
     if (nrm < 1e-14f) done = true;  // B ~ 0 here: keep the current v
     if (!done) {
