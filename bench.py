@@ -65,6 +65,24 @@ def k4_flops(spec):
     return n * (spec.power_iters * (8 * q * q + 8 * q) + 8 * q * q + 8 * q)
 
 
+def stage_work(spec, lam_box, support_size):
+    """SURVEY.md §8(d) algorithmic bytes / flops per stage for one slice."""
+    q = spec.channels
+    h = q * (q + 1) // 2
+    e = int(np.prod(spec.calib))
+    n_grid = int(np.prod(spec.grid_dims))
+    n_full = int(np.prod(spec.full_dims))
+    n = q * support_size
+    interp = tuple(spec.grid_dims) != tuple(spec.full_dims)
+    post = 8 * n_grid * q + 8 * q * e + ((8 * n_full * q + 5 * n_full + 4 * n_grid) if interp else (8 * n_grid * q + 5 * n_grid))
+    return {
+        "gram": ("hbm", 8 * q * e + 8 * n * n),
+        "field": ("hbm", 8 * n_grid * h + 8 * h * lam_box),
+        "eigensolve": ("fp32", k4_flops(spec)),
+        "post": ("hbm", post),
+    }
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -306,6 +324,26 @@ def main():
         except Exception:
             traffic = None
 
+    # per-stage roofline fractions (stage device time from the library's CUDA events)
+    sup = K.make_support(spec.kernel, spec.tau, spec.ndim).shape[0]
+    lam_box = (4 * spec.tau + 1) ** spec.ndim
+    hbm_peak = peaks.get("hbm_gbs", 6552.6)
+    stage_roof = {}
+    for name, (bound, work) in stage_work(spec, lam_box, sup).items():
+        ms = float(dict(zip(("gram", "nullspace", "field", "eigensolve", "post"), stages))[name])
+        if ms <= 0:
+            continue
+        if bound == "hbm":
+            ach = work / (ms / 1e3) / 1e9
+            stage_roof[name] = {"bound": "hbm", "achieved_GBps": round(ach, 1), "frac": round(ach / hbm_peak, 4),
+                                "algorithmic_bytes": int(work)}
+        else:
+            ach = work / (ms / 1e3) / 1e12
+            stage_roof[name] = {"bound": "fp32", "achieved_TFLOPs": round(ach, 2), "frac": round(ach / fp32_peak, 4),
+                                "algorithmic_flops": int(work)}
+    stage_roof["nullspace"] = {"bound": "latency (FP64 subspace eigensolve, cuSOLVER/cuBLAS + own kernels)",
+                               "ms": round(float(stages[1]), 3)}
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -314,6 +352,7 @@ def main():
         "config": {"workload": workload(spec), "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                    "l2": "flushed between steps (256 MiB write, untimed)", "output_voxels_per_rank": output_voxels(spec)},
         "stages_ms": dict(zip(("gram", "nullspace", "field", "eigensolve", "post"), [round(x, 4) for x in stages])),
+        "stages_roofline": stage_roof,
         "roofline": {"kernel": "power_kernel (K4)", "bound": "fp32", "achieved": achieved, "peak": fp32_peak,
                      "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None, "traffic": traffic,
                      "peak_source": f"SMs x 128 FP32 lanes x 2 x sm_max_mhz ({peak_src} MEASURED_PEAKS sm_max_mhz)",

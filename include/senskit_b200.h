@@ -62,6 +62,15 @@ typedef struct {
   double mask_threshold;      /*                            maps.hpp:37 */
   double apod_width;          /*                            maps.hpp:40 */
   int64_t grid_dims[3];       /* explicit map grid or zeros */
+  /* B200 extensions (zero = default):
+   * eig_solver  nullspace eigensolve: 0 auto (block subspace iteration on the
+   *             signal subspace unless spectrum_normalized is requested or
+   *             n <= 512), 1 full cuSOLVER Xsyevd, 2 subspace.
+   * certify     subspace solver only: prove R exact with one Cholesky of
+   *             cut^2 I - G + 2 sigma_1^2 U U^H (falls back to the full solver
+   *             if it fails). */
+  int32_t eig_solver;
+  int32_t certify;
 } sk_config;
 
 /* Provenance (maps.hpp:55-73) with device-timed stages. */
@@ -73,6 +82,10 @@ typedef struct {
   int64_t zeroed_voxels;
   double sigma1;
   double cut_margin;   /* min over sigma of |sigma/cut - 1|: how far R is from flipping */
+  int32_t eig_solver_used; /* 1 full, 2 subspace */
+  int32_t certified;       /* subspace: R proven exact by the Cholesky test */
+  int32_t subspace_iterations;
+  int32_t subspace_block;
   double stage_ms[5];  /* gram, nullspace, field, eigensolve, post (CUDA events) */
   double total_ms;     /* device time of the whole call */
 } sk_provenance;

@@ -64,7 +64,7 @@ class sk_config(C.Structure):
         ("kernel", C.c_int32), ("tau", C.c_int32), ("gram", C.c_int32), ("nullspace_threshold", C.c_double),
         ("grid", C.c_int32), ("grid_pad", C.c_int64), ("eig", C.c_int32), ("power_iters", C.c_int32),
         ("method", C.c_int32), ("field", C.c_int32), ("mask_threshold", C.c_double), ("apod_width", C.c_double),
-        ("grid_dims", C.c_int64 * 3),
+        ("grid_dims", C.c_int64 * 3), ("eig_solver", C.c_int32), ("certify", C.c_int32),
     ]
 
 
@@ -72,7 +72,9 @@ class sk_provenance(C.Structure):
     _fields_ = [
         ("grid_dims", C.c_int64 * 3), ("support_size", C.c_int64), ("valid_shifts", C.c_int64),
         ("nullspace_rank", C.c_int64), ("zeroed_voxels", C.c_int64), ("sigma1", C.c_double),
-        ("cut_margin", C.c_double), ("stage_ms", C.c_double * 5), ("total_ms", C.c_double),
+        ("cut_margin", C.c_double), ("eig_solver_used", C.c_int32), ("certified", C.c_int32),
+        ("subspace_iterations", C.c_int32), ("subspace_block", C.c_int32),
+        ("stage_ms", C.c_double * 5), ("total_ms", C.c_double),
     ]
 
 
@@ -92,6 +94,8 @@ class PipelineConfig:
     mask_threshold: float = 0.01
     apod_width: float = -1.0
     grid_dims: tuple | None = None   # explicit map grid (maps.hpp:115-123)
+    eig_solver: int = 0      # B200 extension: 0 auto, 1 full cuSOLVER, 2 subspace
+    certify: int = 0         # B200 extension: prove R with one Cholesky (subspace solver)
 
     @staticmethod
     def pisco() -> "PipelineConfig":   # maps.cpp:21-28
@@ -101,7 +105,7 @@ class PipelineConfig:
         gd = (C.c_int64 * 3)(*(list(self.grid_dims or ()) + [0, 0, 0])[:3])
         return sk_config(self.kernel, self.tau, self.gram, self.nullspace_threshold, self.grid, self.grid_pad,
                          self.eig, self.power_iters, self.method, self.field, self.mask_threshold,
-                         self.apod_width, gd)
+                         self.apod_width, gd, self.eig_solver, self.certify)
 
 
 @dataclass
@@ -437,7 +441,9 @@ def estimate_maps(calib: Calib, full_dims, cfg: PipelineConfig, ctx: Context | N
         tuple(int(prov.grid_dims[a]) for a in range(nd)), int(prov.support_size), int(prov.nullspace_rank),
         float(prov.sigma1), float(prov.cut_margin), spec, dict(zip(STAGES, list(prov.stage_ms))),
         float(prov.total_ms), int(prov.zeroed_voxels), gram,
-        fieldb.reshape(ngrid, q, q).transpose(0, 2, 1) if want_field else None, raw, raw_l)
+        fieldb.reshape(ngrid, q, q).transpose(0, 2, 1) if want_field else None, raw, raw_l,
+        extra={"eig_solver": "full" if prov.eig_solver_used == 1 else "subspace", "certified": bool(prov.certified),
+               "subspace_iterations": int(prov.subspace_iterations), "subspace_block": int(prov.subspace_block)})
 
 
 def estimate_maps_device(ctx: Context, calib_ptr: int, calib_dims, center_offset, q: int, full_dims,

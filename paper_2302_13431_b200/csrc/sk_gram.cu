@@ -34,12 +34,10 @@ __device__ __forceinline__ void cmac(float2& acc, float2 a, float2 b) {
   acc.y = fmaf(a.y, b.x, acc.y);
 }
 
-// e^{+i 2 pi m / P} for m in [0, P): twiddle tables for the three axes.
-__device__ __forceinline__ float2 twiddle(const float2* tw, int k, int lag, int P) {
-  int m = (k * lag) % P;
-  if (m < 0) m += P;
-  return tw[m];
-}
+// e^{+i 2 pi m / P} for m in [0, P): twiddle tables for the three axes.  The
+// pad extents are powers of two (calibration.cpp:89-93), so the phase index
+// reduces with a mask (two's complement handles negative lags).
+__device__ __forceinline__ float2 twiddle(const float2* tw, int k, int lag, int P) { return tw[(k * lag) & (P - 1)]; }
 
 __global__ void __launch_bounds__(256) gram_pairs_kernel(const float2* __restrict__ spectra, GramGeom g,
                                                          const int2* __restrict__ pairs,
@@ -71,7 +69,25 @@ __global__ void __launch_bounds__(256) gram_pairs_kernel(const float2* __restric
 
   // Stage A: contract axis 0 of conj(S_p) S_q onto the lb lags.
   float2* stageA_out = (g.nd == 1) ? box : A;
-  for (int r = threadIdx.x; r < rest; r += blockDim.x) {
+  float2* prod = reinterpret_cast<float2*>(off + ((g.lam + 3) & ~3));
+  if (g.stage_prod) {
+    // Small pad grid: stage the pair product once, then spread (lag, column)
+    // items over all threads (a warp shares one lag -> broadcast twiddles).
+    for (int e = threadIdx.x; e < npad; e += blockDim.x) prod[e] = cconj_mul(Sp[e], Sq[e]);
+    __syncthreads();
+    for (int item = threadIdx.x; item < lb * rest; item += blockDim.x) {
+      const int l = item / rest, r = item % rest;
+      float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+      int k0 = 0;
+      for (; k0 + 1 < P0; k0 += 2) {
+        cmac(acc0, prod[k0 * rest + r], twiddle(tw0, k0, l - t2, P0));
+        cmac(acc1, prod[(k0 + 1) * rest + r], twiddle(tw0, k0 + 1, l - t2, P0));
+      }
+      if (k0 < P0) cmac(acc0, prod[k0 * rest + r], twiddle(tw0, k0, l - t2, P0));
+      stageA_out[i64(l) * rest + r] = make_float2(acc0.x + acc1.x, acc0.y + acc1.y);
+    }
+  }
+  for (int r = threadIdx.x; !g.stage_prod && r < rest; r += blockDim.x) {
     float2 acc[kMaxLb];
 #pragma unroll
     for (int l = 0; l < kMaxLb; ++l) acc[l] = make_float2(0.f, 0.f);
@@ -149,12 +165,23 @@ size_t gram_pairs_smem(const GramGeom& g) {
   const int P0 = g.pad[0], P1 = g.pad[1], P2 = g.pad[2];
   const size_t lb = size_t(g.lb);
   const size_t nbox = g.nd == 1 ? lb : (g.nd == 2 ? lb * lb : lb * lb * lb);
-  return (size_t(P0 + P1 + P2) + lb * P1 * P2 + lb * lb * P2 + nbox) * sizeof(float2) + size_t(g.lam) * sizeof(int);
+  const size_t prod = g.stage_prod ? size_t(P0) * P1 * P2 : 0;
+  return (size_t(P0 + P1 + P2) + lb * P1 * P2 + lb * lb * P2 + nbox + prod) * sizeof(float2) +
+         size_t((g.lam + 3) & ~3) * sizeof(int);
 }
 
-void gram_pairs_launch(sk_ctx* ctx, const float2* spectra, const GramGeom& g, const int2* d_pairs, int npairs,
+void gram_pairs_launch(sk_ctx* ctx, const float2* spectra, const GramGeom& g_in, const int2* d_pairs, int npairs,
                        const int* d_off, const float2* d_tw, float2* gram) {
+  GramGeom g = g_in;
   if (g.lb > kMaxLb) fail(9, "gram_fft: kernel radius > 7 is outside the B200 path");
+  for (int a = 0; a < 3; ++a)
+    if (g.pad[a] & (g.pad[a] - 1)) fail(9, "gram_fft: pad extents must be powers of two");
+  g.stage_prod = 0;
+  {
+    GramGeom t = g;
+    t.stage_prod = 1;
+    if (gram_pairs_smem(t) <= 160 * 1024) g.stage_prod = 1;
+  }
   const size_t smem = gram_pairs_smem(g);
   if (smem > 227 * 1024) fail(9, "gram_fft: padded calibration too large for the on-chip lag contraction");
   SKB_CUDA(cudaFuncSetAttribute(gram_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

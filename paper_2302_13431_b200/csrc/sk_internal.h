@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include "../../include/senskit_b200.h"
+
 namespace skb {
 
 using i64 = std::int64_t;
@@ -107,6 +109,7 @@ struct GramGeom {
   int tau;
   int q;           // channels
   int lam;         // |Lambda|
+  int stage_prod;  // set by the launcher: stage conj(S_p) S_q in shared memory
 };
 size_t gram_pairs_smem(const GramGeom& g);
 void gram_pairs_launch(sk_ctx* ctx, const float2* spectra, const GramGeom& g, const int2* d_pairs, int npairs,
@@ -155,5 +158,14 @@ void real_to_c64(sk_ctx* ctx, const float* in, float2* out, i64 n);
 void copy_strided(sk_ctx* ctx, const float2* src, i64 src_rs, i64 src_cs, float2* dst, i64 dst_rs, i64 dst_cs, i64 rows,
                   i64 cols);
 void normalize_standalone(sk_ctx* ctx, float2* maps, i64 n, int q, const float2* recon, unsigned long long* zeroed);
+
+// Subspace eigensolver helpers (FP64).
+void random_block(sk_ctx* ctx, double2* v, i64 n, i64 cols, i64 col0, unsigned int seed);
+void ritz_residuals(sk_ctx* ctx, const double2* y, const double2* v, const double* theta, i64 n, i64 cols,
+                    double* res);
+void shift_negate(sk_ctx* ctx, const double2* a, double2* m, i64 n, double shift);
+void cross_gram(sk_ctx* ctx, const double2* x, const double2* y, i64 n, int b, double2* out);
+void chol_inv(sk_ctx* ctx, const double2* s, int b, double2* minv, int* flag);
+void cholesky_small(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag);
 
 }  // namespace skb

@@ -151,9 +151,85 @@ __global__ void normalize_kernel(float2* __restrict__ maps, i64 n, int q, const 
   }
 }
 
+// Deterministic Gaussian-ish start block for the subspace eigensolver
+// (hash-based, reproducible across runs and GPUs).
+__device__ __forceinline__ unsigned int mix32(unsigned int x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+__global__ void random_block_kernel(double2* __restrict__ v, i64 n, i64 cols, i64 col0, unsigned int seed) {
+  const i64 total = n * cols;
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+    const i64 c = e / n + col0, r = e % n;
+    const unsigned int h1 = mix32(unsigned(r) * 2654435761u ^ mix32(unsigned(c) + seed));
+    const unsigned int h2 = mix32(h1 ^ 0x9e3779b9u);
+    // sum of uniforms: cheap, symmetric, full-rank with probability 1
+    const double u1 = (double(h1) + 0.5) / 4294967296.0 - 0.5;
+    const double u2 = (double(h2) + 0.5) / 4294967296.0 - 0.5;
+    v[r + c * n] = make_double2(u1, u2);
+  }
+}
+
+// res[c] = || Y[:,c] - theta[c] V[:,c] ||^2  (one block per column)
+__global__ void ritz_residual_kernel(const double2* __restrict__ y, const double2* __restrict__ v,
+                                     const double* __restrict__ theta, i64 n, double* __restrict__ res) {
+  const i64 c = blockIdx.x;
+  const double t = theta[c];
+  double acc = 0.0;
+  for (i64 r = threadIdx.x; r < n; r += blockDim.x) {
+    const double2 a = y[r + c * n], b = v[r + c * n];
+    const double dx = a.x - t * b.x, dy = a.y - t * b.y;
+    acc += dx * dx + dy * dy;
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (int(threadIdx.x) < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) res[c] = red[0];
+}
+
+// M = shift*I - A + alpha * U U^H is formed by the caller with ZHERK; this adds
+// the diagonal shift and negates A in one pass (lower triangle only).
+__global__ void shift_negate_kernel(const double2* __restrict__ a, double2* __restrict__ m, i64 n, double shift) {
+  const i64 total = n * n;
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+    const i64 c = e / n, r = e % n;
+    if (r < c) continue;
+    double2 v = a[e];
+    v.x = -v.x;
+    v.y = -v.y;
+    if (r == c) v.x += shift;
+    m[e] = v;
+  }
+}
+
 }  // namespace
 
 #define SKB_GRID(n) blocks_for(n), kT, 0, ctx->stream
+
+void random_block(sk_ctx* ctx, double2* v, i64 n, i64 cols, i64 col0, unsigned int seed) {
+  random_block_kernel<<<SKB_GRID(n * cols)>>>(v, n, cols, col0, seed);
+  ++ctx->launches;
+  SKB_LAUNCH("random_block");
+}
+void ritz_residuals(sk_ctx* ctx, const double2* y, const double2* v, const double* theta, i64 n, i64 cols,
+                    double* res) {
+  ritz_residual_kernel<<<unsigned(cols), 256, 0, ctx->stream>>>(y, v, theta, n, res);
+  ++ctx->launches;
+  SKB_LAUNCH("ritz_residual");
+}
+void shift_negate(sk_ctx* ctx, const double2* a, double2* m, i64 n, double shift) {
+  shift_negate_kernel<<<SKB_GRID(n * n)>>>(a, m, n, shift);
+  ++ctx->launches;
+  SKB_LAUNCH("shift_negate");
+}
 
 void c64_to_c128(sk_ctx* ctx, const float2* in, double2* out, i64 n) {
   c64_to_c128_kernel<<<SKB_GRID(n)>>>(in, out, n);

@@ -31,6 +31,16 @@ __device__ __forceinline__ void cmac(float2& acc, float2 m, float2 x) {
   acc.y = fmaf(m.y, x.x, acc.y);
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 template <int QP>
 struct Group {
   static constexpr int kThreads = 256;
@@ -66,29 +76,50 @@ __device__ __forceinline__ void group_sync() {
 }
 
 template <int QP>
-__global__ void __launch_bounds__(256) power_kernel(PowerArgs a) {
+__global__ void __launch_bounds__(256, (QP <= 32 ? 2 : 1)) power_kernel(PowerArgs a) {
   using G = Group<QP>;
   constexpr int VPB = G::kVPB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int Q = a.q;
   const int h = Q * (Q + 1) / 2;
-  float2* gs = reinterpret_cast<float2*>(smem_raw);       // [h][VPB]
-  float2* vs = gs + i64(h) * VPB;                          // [VPB][kStride]
-  float* red = reinterpret_cast<float*>(vs + VPB * G::kStride);  // [VPB][2]
+  // Persistent: the block walks voxel tiles with a double-buffered cp.async
+  // prefetch of the next tile's h x VPB plane slab (VPB-wide coalesced rows).
+  const int tile_elems = (h > QP ? h : QP) * VPB;
+  float2* gbuf = reinterpret_cast<float2*>(smem_raw);             // [2][tile_elems]
+  float2* vs = gbuf + 2 * tile_elems;                             // [VPB][kStride]
+  float* red = reinterpret_cast<float*>(vs + VPB * G::kStride);   // [VPB][2]
 
   const int vox = threadIdx.x / QP;
   const int p = threadIdx.x % QP;
   const int half = (threadIdx.x / 32) & 1;
-  const i64 j0 = i64(blockIdx.x) * VPB;
-  const i64 j = j0 + vox;
-  const bool live = j < a.n;
+  const i64 tiles = (a.n + VPB - 1) / VPB;
 
-  // Stage the block's tile of packed planes (VPB-wide coalesced rows).
-  for (int e = threadIdx.x; e < h * VPB; e += blockDim.x) {
-    const int pair = e / VPB, v = e % VPB;
-    gs[e] = (j0 + v < a.n) ? a.planes[i64(pair) * a.n + j0 + v] : make_float2(0.f, 0.f);
+  auto load_tile = [&](i64 t, float2* dst) {
+    const i64 jj0 = t * VPB;
+    for (int e = threadIdx.x; e < h * VPB; e += blockDim.x) {
+      const int pair = e / VPB, v = e % VPB;
+      const bool ok = jj0 + v < a.n;
+      cp_async8(dst + e, a.planes + (ok ? i64(pair) * a.n + jj0 + v : 0), ok ? 8 : 0);
+    }
+    cp_async_commit();
+  };
+
+  i64 tile = blockIdx.x;
+  int buf = 0;
+  if (tile < tiles) load_tile(tile, gbuf);
+  for (; tile < tiles; tile += gridDim.x, buf ^= 1) {
+  const i64 next = tile + gridDim.x;
+  if (next < tiles) {
+    load_tile(next, gbuf + (buf ^ 1) * tile_elems);
+    cp_async_wait<1>();
+  } else {
+    cp_async_wait<0>();
   }
   __syncthreads();
+  float2* gs = gbuf + buf * tile_elems;
+  const i64 j0 = tile * VPB;
+  const i64 j = j0 + vox;
+  const bool live = j < a.n;
 
   // Unpack this thread's matrix row.
   float2 m[QP];
@@ -114,40 +145,90 @@ __global__ void __launch_bounds__(256) power_kernel(PowerArgs a) {
   bool done = false;
   group_sync<QP>();
 
+  // M v with v broadcast from shared memory: v is staged into registers in
+  // chunks of 8 complex values (4 LDS.128 in flight) feeding 4 independent
+  // accumulator pairs, so the FMA pipe is not serialised on LDS latency.
   auto matvec = [&](float2& out) {
     const float4* v4 = reinterpret_cast<const float4*>(myv);
-    float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+    float2 acc[4];
 #pragma unroll
-    for (int c = 0; c < QP; c += 2) {
-      const float4 vv = v4[c / 2];
-      cmac(acc0, m[c], make_float2(vv.x, vv.y));
-      cmac(acc1, m[c + 1], make_float2(vv.z, vv.w));
+    for (int k = 0; k < 4; ++k) acc[k] = make_float2(0.f, 0.f);
+    constexpr int kChunk = QP < 8 ? QP : 8;
+#pragma unroll
+    for (int c0 = 0; c0 < QP; c0 += kChunk) {
+      float4 vv[kChunk / 2];
+#pragma unroll
+      for (int t = 0; t < kChunk / 2; ++t) vv[t] = v4[c0 / 2 + t];
+#pragma unroll
+      for (int t = 0; t < kChunk / 2; ++t) {
+        cmac(acc[(2 * t) & 3], m[c0 + 2 * t], make_float2(vv[t].x, vv[t].y));
+        cmac(acc[(2 * t + 1) & 3], m[c0 + 2 * t + 1], make_float2(vv[t].z, vv[t].w));
+      }
     }
-    out = make_float2(acc0.x + acc1.x, acc0.y + acc1.y);
+    out = make_float2((acc[0].x + acc[1].x) + (acc[2].x + acc[3].x), (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y));
   };
 
-  for (int it = 0; it < a.iters; ++it) {
+  // Iteration 0, peeled: an annihilated all-ones start restarts from e_0
+  // (eigensolve.cpp:56-63).  The e_0 candidate is formed by every thread (the
+  // reductions stay warp/block-uniform) and selected per voxel.
+  if (a.iters > 0) {
     float2 mv;
     matvec(mv);
     float2 w = make_float2(a.alpha * vp.x + a.beta * mv.x, a.alpha * vp.y + a.beta * mv.y);
-    float nrm = sqrtf(group_sum<QP>(w.x * w.x + w.y * w.y, red, vox, half));
-    if (it == 0) {
-      // All-ones start annihilated: restart from e_0 (eigensolve.cpp:58-63).
-      // The e_0 candidate is formed by every thread (the reductions must stay
-      // warp/block-uniform) and selected per voxel.
-      const float2 v0 = (p == 0) ? make_float2(1.f, 0.f) : make_float2(0.f, 0.f);
-      const float2 w0 = make_float2(a.alpha * v0.x + a.beta * m[0].x, a.alpha * v0.y + a.beta * m[0].y);
-      const float nrm0 = sqrtf(group_sum<QP>(w0.x * w0.x + w0.y * w0.y, red, vox, half));
-      if (nrm < 1e-14f) {
-        vp = v0;
-        w = w0;
-        nrm = nrm0;
-      }
+    float n2 = group_sum<QP>(w.x * w.x + w.y * w.y, red, vox, half);
+    const float2 v0 = (p == 0) ? make_float2(1.f, 0.f) : make_float2(0.f, 0.f);
+    const float2 w0 = make_float2(a.alpha * v0.x + a.beta * m[0].x, a.alpha * v0.y + a.beta * m[0].y);
+    const float n20 = group_sum<QP>(w0.x * w0.x + w0.y * w0.y, red, vox, half);
+    if (n2 < 1e-28f) {  // ||B v|| < 1e-14
+      vp = v0;
+      w = w0;
+      n2 = n20;
     }
-    if (nrm < 1e-14f) done = true;  // B ~ 0 here: keep the current v
+    if (n2 < 1e-28f) done = true;  // B ~ 0 here: keep the current v
     if (!done) {
-      const float inv = 1.0f / nrm;
+      const float inv = rsqrtf(n2);
       vp = make_float2(w.x * inv, w.y * inv);
+    }
+    group_sync<QP>();
+    myv[p] = vp;
+    group_sync<QP>();
+  }
+  // Iterations 1..iters-1, software-pipelined: the shared vector holds the
+  // UNNORMALISED iterate u_k (u_1 = v_1).  The reduction ||u_k||^2 runs
+  // alongside the mat-vec M u_k (independent instructions), and the scale is
+  // applied afterwards: w = B (u_k / ||u_k||) = B v_k, exactly the reference
+  // step.  ||B v_k|| is only known one iteration later, so the break test of
+  // iteration k (||B v_k|| < 1e-14 -> keep v_k) is evaluated then, with v_k
+  // kept in `vprev`.
+  float2 up = vp;          // u_k
+  float2 vprev = vp;       // v_k (normalised)
+  for (int it = 1; it < a.iters; ++it) {
+    const float n2 = group_sum<QP>(up.x * up.x + up.y * up.y, red, vox, half);  // ||u_k||^2 = ||B v_{k-1}||^2
+    float2 mv;
+    matvec(mv);                                                                 // M u_k
+    if (it > 1 && n2 < 1e-28f && !done) {  // iteration it-1 should have stopped: keep v_{it-1}
+      done = true;
+    }
+    const float inv = rsqrtf(n2);
+    if (!done) {
+      vprev = make_float2(up.x * inv, up.y * inv);  // v_k
+      up = make_float2((a.alpha * up.x + a.beta * mv.x) * inv, (a.alpha * up.y + a.beta * mv.y) * inv);
+    }
+    group_sync<QP>();
+    myv[p] = up;
+    group_sync<QP>();
+  }
+  if (a.iters > 1) {
+    const float n2 = group_sum<QP>(up.x * up.x + up.y * up.y, red, vox, half);  // ||B v_{iters-1}||^2
+    if (!done) {
+      if (n2 < 1e-28f) {
+        vp = vprev;
+      } else {
+        const float inv = rsqrtf(n2);
+        vp = make_float2(up.x * inv, up.y * inv);
+      }
+    } else {
+      vp = vprev;
     }
     group_sync<QP>();
     myv[p] = vp;
@@ -196,17 +277,21 @@ __global__ void __launch_bounds__(256) power_kernel(PowerArgs a) {
     if (a.value) a.value[j] = a.alpha * vn2 + a.beta * mv;
     if (a.mask) a.mask[j] = lam < a.mask_threshold ? 1 : 0;
   }
+  __syncthreads();  // the staging buffer is the prefetch target two tiles on
+  }
 }
 
 template <int QP>
 void launch(sk_ctx* ctx, const PowerArgs& a) {
   using G = Group<QP>;
   const int h = a.q * (a.q + 1) / 2;
-  const size_t tile = size_t(h) * G::kVPB * sizeof(float2);
-  const size_t smem = std::max(tile, size_t(QP) * G::kVPB * sizeof(float2)) +
-                      size_t(G::kVPB) * G::kStride * sizeof(float2) + size_t(G::kVPB) * 2 * sizeof(float);
+  const size_t tile = size_t(std::max(h, QP)) * G::kVPB * sizeof(float2);
+  const size_t smem = 2 * tile + size_t(G::kVPB) * G::kStride * sizeof(float2) + size_t(G::kVPB) * 2 * sizeof(float);
   SKB_CUDA(cudaFuncSetAttribute(power_kernel<QP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  const i64 blocks = (a.n + G::kVPB - 1) / G::kVPB;
+  int per_sm = 0;
+  SKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_kernel<QP>, G::kThreads, smem));
+  const i64 tiles = (a.n + G::kVPB - 1) / G::kVPB;
+  const i64 blocks = std::min<i64>(tiles, i64(std::max(per_sm, 1)) * ctx->sm_count);
   power_kernel<QP><<<unsigned(blocks), G::kThreads, smem, ctx->stream>>>(a);
   ++ctx->launches;
   SKB_LAUNCH("power_kernel");

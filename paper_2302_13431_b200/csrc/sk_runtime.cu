@@ -345,10 +345,13 @@ float2* run_gram(sk_ctx* ctx, const Dims& cdims, i64 q, const float2* calib, con
 // ---------------------------------------------------------------- K2
 struct Eig {
   std::vector<double> evals;  // ascending
-  double2* evecs = nullptr;   // n x n column-major, device
-  i64 n = 0, rank = 0;
+  double2* evecs = nullptr;   // n x n column-major, device (full solver only)
+  const double2* usig = nullptr;  // n x k signal eigenvectors (lambda >= cut^2), device
+  i64 n = 0, rank = 0, k = 0;
   double sigma1 = 0, cut = 0, margin = 0;
-  std::vector<double> spectrum;  // descending sigma
+  std::vector<double> spectrum;  // descending sigma (subspace solver: top block only, rest 0)
+  bool full = true, certified = false;
+  int iterations = 0, block = 0;
 };
 
 Eig run_eigh(sk_ctx* ctx, const float2* gram, i64 n, double ratio) {  // nullspace.cpp:7-35
@@ -396,13 +399,341 @@ Eig run_eigh(sk_ctx* ctx, const float2* gram, i64 n, double ratio) {  // nullspa
     std::snprintf(buf, sizeof buf, "%f", ratio);
     fail(SK_ERR_NULLSPACE_EMPTY, std::string("calibration matrix has no approximate nullspace at ratio ") + buf);
   }
+  e.k = n - r;
+  e.usig = e.evecs + r * n;
+  e.full = true;
   return e;
+}
+
+// ---------------------------------------------------------------- K2 (subspace)
+// The pipeline needs only the signal subspace {lambda >= (ratio*sigma_1)^2}
+// (k = n - R ~ 20-50 vectors) and the count R.  Block subspace
+// iteration with Rayleigh-Ritz on the FP64-promoted Gram (cuBLAS ZGEMM for
+// A*V, CholQR2 orthonormalisation, cuSOLVER on the b x b projection) returns
+// exactly that.  Convergence: every Ritz pair with theta >= cut^2/2 has
+// ||A v - theta v|| <= tol*theta_max, and the block extends below cut^2/2 so
+// no eigenvalue above the cut can hide outside it.  Optional certification:
+// Cholesky of cut^2*I - A + 2 theta_max U U^H succeeds iff lambda_{k+1} < cut^2
+// (with U the k Ritz vectors above the cut), i.e. R is exact.  Any failure
+// falls back to the full eigensolver.
+struct SubspaceStatus {
+  bool ok = false;
+};
+
+void zgemm(sk_ctx* ctx, cublasOperation_t ta, cublasOperation_t tb, i64 m, i64 n, i64 k, const double2* a, i64 lda,
+           const double2* b, i64 ldb, double2* c, i64 ldc) {
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+  check_cublas(cublasZgemm(ctx->cublas, ta, tb, int(m), int(n), int(k), &one,
+                           reinterpret_cast<const cuDoubleComplex*>(a), int(lda),
+                           reinterpret_cast<const cuDoubleComplex*>(b), int(ldb), &zero,
+                           reinterpret_cast<cuDoubleComplex*>(c), int(ldc)),
+               "Zgemm");
+  ++ctx->lib_calls;
+}
+
+// In-place Cholesky-QR of X (n x b).  Returns false if X is numerically rank deficient.
+bool cholqr(sk_ctx* ctx, double2* x, i64 n, i64 b) {
+  double2* s = ctx->arena.get<double2>("ss:S", b * b);
+  const double one = 1.0, zero = 0.0;
+  check_cublas(cublasZherk(ctx->cublas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C, int(b), int(n), &one,
+                           reinterpret_cast<const cuDoubleComplex*>(x), int(n), &zero,
+                           reinterpret_cast<cuDoubleComplex*>(s), int(b)),
+               "Zherk(cholqr)");
+  size_t dbytes = 0, hbytes = 0;
+  check_cusolver(cusolverDnXpotrf_bufferSize(ctx->cusolver, ctx->cusolver_params, CUBLAS_FILL_MODE_LOWER, b,
+                                             CUDA_C_64F, s, b, CUDA_C_64F, &dbytes, &hbytes),
+                 "Xpotrf_bufferSize");
+  void* dwork = ctx->arena.get("ss:potrf_work", dbytes);
+  static thread_local std::vector<unsigned char> hwork;
+  hwork.resize(std::max<size_t>(hbytes, 1));
+  int* info = ctx->arena.get<int>("ss:info", 1);
+  check_cusolver(cusolverDnXpotrf(ctx->cusolver, ctx->cusolver_params, CUBLAS_FILL_MODE_LOWER, b, CUDA_C_64F, s, b,
+                                  CUDA_C_64F, dwork, dbytes, hwork.data(), hbytes, info),
+                 "Xpotrf");
+  const cuDoubleComplex onec = make_cuDoubleComplex(1.0, 0.0);
+  check_cublas(cublasZtrsm(ctx->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT,
+                           int(n), int(b), &onec, reinterpret_cast<const cuDoubleComplex*>(s), int(b),
+                           reinterpret_cast<cuDoubleComplex*>(x), int(n)),
+               "Ztrsm");
+  ctx->lib_calls += 3;
+  int h_info = 0;
+  SKB_CUDA(cudaMemcpyAsync(&h_info, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return h_info == 0;
+}
+
+constexpr i64 kSmallBlockMax = 112;  // custom one-CTA Cholesky limit (shared memory)
+
+// Eigendecomposition of the b x b Rayleigh-Ritz matrix (lower triangle used),
+// eigenvalues ascending into w, eigenvectors overwrite H.  Default: cuSOLVER
+// Jacobi (ZHEEVJ, tol 1e-14); SKB_SMALL_EIG=dc / batched select
+// divide-and-conquer (Xsyevd) / XsyevBatched for comparison.
+void small_heev(sk_ctx* ctx, double2* H, i64 b, double* w, int* d_info) {
+  static const int mode = [] {
+    const char* v = std::getenv("SKB_SMALL_EIG");
+    if (!v) return 1;  // default: cuSOLVER Jacobi (fastest measured at b ~ 96)
+    if (std::string(v) == "dc") return 0;
+    if (std::string(v) == "batched") return 2;
+    return 1;
+  }();
+  const bool jacobi = mode == 1;
+  if (mode == 2) {
+    size_t dbytes = 0, hbytes = 0;
+    check_cusolver(cusolverDnXsyevBatched_bufferSize(ctx->cusolver, ctx->cusolver_params, CUSOLVER_EIG_MODE_VECTOR,
+                                                     CUBLAS_FILL_MODE_LOWER, b, CUDA_C_64F, H, b, CUDA_R_64F, w,
+                                                     CUDA_C_64F, &dbytes, &hbytes, 1),
+                   "XsyevBatched_bufferSize");
+    void* dwork = ctx->arena.get("ss:syevb_work", dbytes);
+    static thread_local std::vector<unsigned char> hwork;
+    hwork.resize(std::max<size_t>(hbytes, 1));
+    check_cusolver(cusolverDnXsyevBatched(ctx->cusolver, ctx->cusolver_params, CUSOLVER_EIG_MODE_VECTOR,
+                                          CUBLAS_FILL_MODE_LOWER, b, CUDA_C_64F, H, b, CUDA_R_64F, w, CUDA_C_64F,
+                                          dwork, dbytes, hwork.data(), hbytes, d_info, 1),
+                   "XsyevBatched");
+  } else if (jacobi) {
+    static syevjInfo_t params = nullptr;
+    if (!params) {
+      check_cusolver(cusolverDnCreateSyevjInfo(&params), "CreateSyevjInfo");
+      check_cusolver(cusolverDnXsyevjSetTolerance(params, 1e-14), "syevjSetTolerance");
+      check_cusolver(cusolverDnXsyevjSetMaxSweeps(params, 30), "syevjSetMaxSweeps");
+    }
+    int lwork = 0;
+    check_cusolver(cusolverDnZheevj_bufferSize(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                               int(b), reinterpret_cast<cuDoubleComplex*>(H), int(b), w, &lwork,
+                                               params),
+                   "Zheevj_bufferSize");
+    auto* work = ctx->arena.get<cuDoubleComplex>("ss:syevj_work", std::max(lwork, 1));
+    check_cusolver(cusolverDnZheevj(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, int(b),
+                                    reinterpret_cast<cuDoubleComplex*>(H), int(b), w, work, lwork, d_info, params),
+                   "Zheevj");
+  } else {
+    size_t dbytes = 0, hbytes = 0;
+    check_cusolver(cusolverDnXsyevd_bufferSize(ctx->cusolver, ctx->cusolver_params, CUSOLVER_EIG_MODE_VECTOR,
+                                               CUBLAS_FILL_MODE_LOWER, b, CUDA_C_64F, H, b, CUDA_R_64F, w,
+                                               CUDA_C_64F, &dbytes, &hbytes),
+                   "Xsyevd_bufferSize(ritz)");
+    void* dwork = ctx->arena.get("ss:syevd_work", dbytes);
+    static thread_local std::vector<unsigned char> hwork;
+    hwork.resize(std::max<size_t>(hbytes, 1));
+    check_cusolver(cusolverDnXsyevd(ctx->cusolver, ctx->cusolver_params, CUSOLVER_EIG_MODE_VECTOR,
+                                    CUBLAS_FILL_MODE_LOWER, b, CUDA_C_64F, H, b, CUDA_R_64F, w, CUDA_C_64F, dwork,
+                                    dbytes, hwork.data(), hbytes, d_info),
+                   "Xsyevd(ritz)");
+  }
+  ++ctx->lib_calls;
+}
+
+// Orthonormalise X (n x b) in place by CholQR2.  b <= kSmallBlockMax uses the
+// custom no-sync kernels (cross_gram, chol_inv) + ZGEMM; larger blocks use
+// cuBLAS HERK/TRSM + cuSOLVER POTRF.  Returns false only on a detected
+// (synchronous path) failure; the fast path raises `flag` instead.
+bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int passes = 2) {
+  (void)tmp;
+  if (b > kSmallBlockMax) {
+    for (int p = 0; p < passes; ++p)
+      if (!cholqr(ctx, x, n, b)) return false;
+    return true;
+  }
+  double2* S = ctx->arena.get<double2>("ss:S", b * b);
+  double2* L = ctx->arena.get<double2>("ss:L", b * b);
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+  static const bool lib_chol = [] {
+    const char* v = std::getenv("SKB_SMALL_CHOL");
+    return !(v && std::string(v) == "custom");  // default: cuSOLVER POTRF (no host sync)
+  }();
+  for (int pass = 0; pass < passes; ++pass) {
+    cross_gram(ctx, x, x, n, int(b), S);        // S = X^H X
+    if (lib_chol) {
+      size_t dbytes = 0, hbytes = 0;
+      check_cusolver(cusolverDnXpotrf_bufferSize(ctx->cusolver, ctx->cusolver_params, CUBLAS_FILL_MODE_LOWER, b,
+                                                 CUDA_C_64F, S, b, CUDA_C_64F, &dbytes, &hbytes),
+                     "Xpotrf_bufferSize");
+      void* dwork = ctx->arena.get("ss:potrf_work", dbytes);
+      static thread_local std::vector<unsigned char> hwork;
+      hwork.resize(std::max<size_t>(hbytes, 1));
+      check_cusolver(cusolverDnXpotrf(ctx->cusolver, ctx->cusolver_params, CUBLAS_FILL_MODE_LOWER, b, CUDA_C_64F, S, b,
+                                      CUDA_C_64F, dwork, dbytes, hwork.data(), hbytes, flag + 1),
+                     "Xpotrf");
+      ++ctx->lib_calls;
+      L = S;
+    } else {
+      cholesky_small(ctx, S, int(b), L, flag);  // S = L L^H
+    }
+    check_cublas(cublasZtrsm(ctx->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C,
+                             CUBLAS_DIAG_NON_UNIT, int(n), int(b), &one, reinterpret_cast<const cuDoubleComplex*>(L),
+                             int(b), reinterpret_cast<cuDoubleComplex*>(x), int(n)),
+                 "Ztrsm(orth)");                 // X <- X L^{-H}
+    ++ctx->lib_calls;
+  }
+  return true;
+}
+
+bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, bool certify, Eig& e) {
+  e = Eig();
+  e.n = n;
+  e.full = false;
+  double2* A = ctx->arena.get<double2>("eig:A", n * n);
+  c64_to_c128(ctx, gram, A, n * n);
+  // Per-size hints from the previous call: block size and the number of
+  // orthogonalised iterations before the (single) Rayleigh-Ritz check.
+  static std::map<std::pair<sk_ctx*, i64>, std::pair<i64, int>> hint;
+  i64 b = 96;
+  int q_plan = 3;
+  auto it_h = hint.find({ctx, n});
+  if (it_h != hint.end()) {
+    b = std::max<i64>(64, ((it_h->second.first + 40 + 31) / 32) * 32);
+    q_plan = it_h->second.second;
+  }
+  b = std::min(b, n);
+  const i64 bcap = std::min(n, std::max<i64>(4 * b, 256));
+  double2* V = ctx->arena.get<double2>("ss:V", n * bcap);
+  double2* Y = ctx->arena.get<double2>("ss:Y", n * bcap);
+  double2* T = ctx->arena.get<double2>("ss:T", n * bcap);
+  double2* H = ctx->arena.get<double2>("ss:H", bcap * bcap);
+  double* w = ctx->arena.get<double>("ss:w", bcap);
+  double* res = ctx->arena.get<double>("ss:res", bcap);
+  int* d_info = ctx->arena.get<int>("ss:einfo", 3);
+  int* flag = d_info + 1;
+  SKB_CUDA(cudaMemsetAsync(d_info, 0, 3 * sizeof(int), ctx->stream));
+  random_block(ctx, V, n, b, 0, 0x5eed5u);
+  if (!orth(ctx, V, T, n, b, flag)) return false;
+  const double tol = 3e-10;
+  const int maxit = 80;
+  const i64 guard = 8;
+  std::vector<double> hw(static_cast<size_t>(bcap)), hres(static_cast<size_t>(bcap));
+  bool converged = false;
+  int iters = 0;
+  i64 m = 0;
+  double theta_max = 0.0, c = 0.0;
+  while (iters < maxit) {
+    for (int i = 0; i < q_plan; ++i, ++iters) {
+      zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);  // Y = A V
+      std::swap(V, Y);
+      // Only the span matters between Rayleigh-Ritz steps: one CholQR pass
+      // (orthogonality ~ kappa^2 eps) except before the projection.
+      if (!orth(ctx, V, T, n, b, flag, i + 1 == q_plan ? 2 : 1)) return false;
+    }
+    zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);
+    ++iters;
+    // Rayleigh-Ritz on span(V): H = V^H A V = S diag(w) S^H.
+    if (b <= kSmallBlockMax) {
+      cross_gram(ctx, V, Y, n, int(b), H);
+    } else {
+      zgemm(ctx, CUBLAS_OP_C, CUBLAS_OP_N, b, b, n, V, n, Y, n, H, b);
+    }
+    small_heev(ctx, H, b, w, d_info);
+    zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, b, V, n, H, b, T, n);  // V <- V S
+    std::swap(V, T);
+    zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, b, Y, n, H, b, T, n);  // Y <- Y S
+    std::swap(Y, T);
+    ritz_residuals(ctx, Y, V, w, n, b, res);
+    int hinfo[3] = {0, 0, 0};
+    SKB_CUDA(cudaMemcpyAsync(hw.data(), w, size_t(b) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    SKB_CUDA(cudaMemcpyAsync(hres.data(), res, size_t(b) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    SKB_CUDA(cudaMemcpyAsync(hinfo, d_info, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hinfo[0] != 0 || hinfo[1] != 0 || hinfo[2] != 0) return false;  // syevd failure / rank-deficient block
+    theta_max = hw[size_t(b - 1)];
+    if (!(theta_max > 0.0)) return false;
+    c = ratio * ratio * theta_max;
+    m = 0;
+    for (i64 i = 0; i < b; ++i) m += hw[size_t(i)] >= c ? 1 : 0;
+    if (m > b - guard && b < n) {
+      const i64 nb = std::min(n, std::min(bcap, 2 * b));
+      if (nb <= b) return false;
+      random_block(ctx, V, n, nb - b, b, 0x5eed5u + unsigned(iters));
+      b = nb;
+      if (!orth(ctx, V, T, n, b, flag)) return false;
+      q_plan = 3;
+      continue;
+    }
+    // Converged when every Ritz pair at or above cut^2/2 has a small residual and
+    // the block reaches below cut^2/2.
+    double worst = 0.0, rate = 0.0;
+    bool reaches = hw[0] < 0.5 * c || b == n;
+    for (i64 i = 0; i < b; ++i) {
+      if (hw[size_t(i)] < 0.5 * c) continue;
+      const double r = std::sqrt(std::max(hres[size_t(i)], 0.0)) / theta_max;
+      worst = std::max(worst, r);
+      rate = std::max(rate, std::max(hw[0], 0.0) / hw[size_t(i)]);
+    }
+    if (reaches && worst <= tol) {
+      converged = true;
+      break;
+    }
+    // Predict the remaining iterations from the observed Ritz-value ratios.
+    int extra = 1;
+    if (reaches && rate > 0.0 && rate < 1.0 && worst > 0.0)
+      extra = int(std::ceil(std::log(tol / worst) / std::log(rate)));
+    q_plan = std::max(1, std::min(extra, 20));
+  }
+  if (!converged) return false;
+  if (m == 0 || m == n) {
+    char buf[96];
+    std::snprintf(buf, sizeof buf, "%f", ratio);
+    fail(SK_ERR_NULLSPACE_EMPTY, std::string("calibration matrix has no approximate nullspace at ratio ") + buf);
+  }
+  double2* U = V + (b - m) * n;  // the last m Ritz columns (ascending theta)
+  if (certify) {
+    double2* M = ctx->arena.get<double2>("ss:M", n * n);
+    shift_negate(ctx, A, M, n, c);
+    const double alpha = 2.0 * theta_max, one = 1.0;
+    check_cublas(cublasZherk(ctx->cublas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, int(n), int(m), &alpha,
+                             reinterpret_cast<const cuDoubleComplex*>(U), int(n), &one,
+                             reinterpret_cast<cuDoubleComplex*>(M), int(n)),
+                 "Zherk(certify)");
+    size_t dbytes = 0, hbytes = 0;
+    check_cusolver(cusolverDnXpotrf_bufferSize(ctx->cusolver, ctx->cusolver_params, CUBLAS_FILL_MODE_LOWER, n,
+                                               CUDA_C_64F, M, n, CUDA_C_64F, &dbytes, &hbytes),
+                   "Xpotrf_bufferSize(certify)");
+    void* dwork = ctx->arena.get("ss:cert_work", dbytes);
+    static thread_local std::vector<unsigned char> hwork2;
+    hwork2.resize(std::max<size_t>(hbytes, 1));
+    check_cusolver(cusolverDnXpotrf(ctx->cusolver, ctx->cusolver_params, CUBLAS_FILL_MODE_LOWER, n, CUDA_C_64F, M, n,
+                                    CUDA_C_64F, dwork, dbytes, hwork2.data(), hbytes, d_info),
+                   "Xpotrf(certify)");
+    ctx->lib_calls += 2;
+    int h_info = 0;
+    SKB_CUDA(cudaMemcpyAsync(&h_info, d_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h_info != 0) return false;  // an eigenvalue >= cut^2 outside the Ritz set: use the full solver
+    e.certified = true;
+  }
+  double2* keep = ctx->arena.get<double2>("ss:U", n * m);
+  SKB_CUDA(cudaMemcpyAsync(keep, U, size_t(n * m) * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+  e.usig = keep;
+  e.k = m;
+  e.rank = n - m;
+  e.sigma1 = std::sqrt(theta_max);
+  e.cut = ratio * e.sigma1;
+  e.spectrum.assign(size_t(n), 0.0);
+  for (i64 i = 0; i < b; ++i) e.spectrum[size_t(i)] = std::sqrt(std::max(0.0, hw[size_t(b - 1 - i)]));
+  double margin = 1e300;
+  for (i64 i = 0; i < b; ++i) margin = std::min(margin, std::fabs(e.spectrum[size_t(i)] / e.cut - 1.0));
+  e.margin = margin;
+  e.iterations = iters;
+  e.block = int(b);
+  hint[{ctx, n}] = {m, std::max(1, iters - 1)};
+  return true;
+}
+
+// Nullspace stage dispatcher: solver 0 = auto (subspace unless the full
+// spectrum is requested or n is small), 1 = full cuSOLVER, 2 = subspace.
+Eig run_nullspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, int solver, bool need_spectrum,
+                  bool certify) {
+  if (!(ratio > 0.0 && ratio < 1.0)) fail(SK_ERR_DIM, "nullspace threshold ratio must lie in (0,1)");
+  const bool subspace = solver == 2 || (solver == 0 && !need_spectrum && n > 512);
+  if (subspace) {
+    Eig e;
+    if (run_eigh_subspace(ctx, gram, n, ratio, certify, e)) return e;
+  }
+  return run_eigh(ctx, gram, n, ratio);
 }
 
 // ---------------------------------------------------------------- K3
 // Lag kernels from the signal subspace, expanded onto the grid as packed planes.
 float2* run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims& grid) {
-  const i64 n = e.n, k = n - e.rank;
+  const i64 n = e.n, k = e.k;
   const int lam = int(s.count);
   SupportTables& t = tables_for(ctx, s, q);
   const int h = q * (q + 1) / 2;
@@ -410,7 +741,7 @@ float2* run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims
   if (k > 0) {
     const double one = 1.0, zero = 0.0;
     check_cublas(cublasZherk(ctx->cublas, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, int(n), int(k), &one,
-                             reinterpret_cast<const cuDoubleComplex*>(e.evecs + e.rank * n), int(n), &zero,
+                             reinterpret_cast<const cuDoubleComplex*>(e.usig), int(n), &zero,
                              reinterpret_cast<cuDoubleComplex*>(ws), int(n)),
                  "Zherk");
     ++ctx->lib_calls;
@@ -525,7 +856,8 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   float2* gram = run_gram(ctx, cdims, q, calib, s, out.gram);
   SKB_CUDA(cudaEventRecord(ev[1], ctx->stream));
   // nullspace
-  Eig e = run_eigh(ctx, gram, n, cfg->nullspace_threshold);
+  Eig e = run_nullspace(ctx, gram, n, cfg->nullspace_threshold, cfg->eig_solver, out.spectrum != nullptr,
+                        cfg->certify != 0);
   SKB_CUDA(cudaEventRecord(ev[2], ctx->stream));
   // field
   float2* planes = run_field(ctx, e, s, int(q), grid);
@@ -591,6 +923,10 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
     prov->zeroed_voxels = i64(h_zeroed);
     prov->sigma1 = e.sigma1;
     prov->cut_margin = e.margin;
+    prov->eig_solver_used = e.full ? 1 : 2;
+    prov->certified = e.certified ? 1 : 0;
+    prov->subspace_iterations = e.iterations;
+    prov->subspace_block = e.block;
     prov->stage_ms[0] = ms[0];
     prov->stage_ms[1] = ms[1];
     prov->stage_ms[2] = ms[2];

@@ -1,0 +1,282 @@
+// Small dense FP64 kernels for the subspace nullspace solver (K2):
+//
+//  * cross_gram:  H = X^H Y for tall-skinny X, Y (n x b, b <= 128), as a
+//    deterministic two-phase reduction (row-chunk partials, then a fixed-order
+//    sum).  Used for CholQR's X^H X and for the Rayleigh-Ritz projection.
+//  * chol_inv:    one CTA: S = L L^H (Cholesky, lower) and M = L^{-1}, both
+//    packed in shared memory; writes M as a full column-major b x b matrix so
+//    that V = Y M^H is one ZGEMM.  A non-positive pivot raises a device flag
+//    (read at the next host synchronisation) instead of stopping the stream.
+//
+// These replace per-iteration cuBLAS HERK/TRSM + cuSOLVER POTRF calls whose
+// launch and host-sync overhead dominated the stage at b ~ 96.
+#include "sk_internal.h"
+
+namespace skb {
+
+namespace {
+
+__device__ __forceinline__ double2 cfma_conj(double2 acc, double2 a, double2 b) {  // acc + conj(a) * b
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+  return acc;
+}
+__device__ __forceinline__ double2 cfma(double2 acc, double2 a, double2 b) {  // acc + a * b
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+  return acc;
+}
+
+constexpr int kTile = 32;
+constexpr int kRows = 32;  // rows staged per step
+
+// partial[chunk][j][i] (col-major b x b) = sum_{r in chunk} conj(X[r,i]) * Y[r,j]
+__global__ void __launch_bounds__(256) cross_gram_partial_kernel(const double2* __restrict__ x, const double2* __restrict__ y,
+                                                                 i64 n, int b, i64 rows_per_chunk,
+                                                                 double2* __restrict__ partial) {
+  __shared__ double2 xs[kRows][kTile + 1];
+  __shared__ double2 ys[kRows][kTile + 1];
+  const int tiles = (b + kTile - 1) / kTile;
+  const int ti = blockIdx.x % tiles, tj = blockIdx.x / tiles;
+  const i64 chunk = blockIdx.y;
+  const i64 r0 = chunk * rows_per_chunk, r1 = min(n, r0 + rows_per_chunk);
+  const int tx = threadIdx.x % kTile, ty = threadIdx.x / kTile;  // 32 x 8
+  double2 acc[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) acc[k] = make_double2(0.0, 0.0);
+  for (i64 rs = r0; rs < r1; rs += kRows) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < kRows * kTile; e += blockDim.x) {
+      const int rr = e / kTile, cc = e % kTile;
+      const i64 r = rs + rr;
+      const int ci = ti * kTile + cc, cj = tj * kTile + cc;
+      xs[rr][cc] = (r < r1 && ci < b) ? x[r + i64(ci) * n] : make_double2(0.0, 0.0);
+      ys[rr][cc] = (r < r1 && cj < b) ? y[r + i64(cj) * n] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < kRows; ++rr) {
+      const double2 xv = xs[rr][tx];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k] = cfma_conj(acc[k], xv, ys[rr][ty + 8 * k]);
+    }
+  }
+  const int i = ti * kTile + tx;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int j = tj * kTile + ty + 8 * k;
+    if (i < b && j < b) partial[chunk * b * b + i64(j) * b + i] = acc[k];
+  }
+}
+
+__global__ void reduce_partials_kernel(const double2* __restrict__ partial, int chunks, int bb,
+                                       double2* __restrict__ out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bb; e += gridDim.x * blockDim.x) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int c = 0; c < chunks; ++c) {
+      const double2 v = partial[i64(c) * bb + e];
+      s.x += v.x;
+      s.y += v.y;
+    }
+    out[e] = s;
+  }
+}
+
+__device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }  // packed lower, i >= j
+
+// One CTA.  S (b x b col-major, Hermitian; lower used) -> Minv (b x b col-major,
+// lower = L^{-1}, upper zero).  *flag |= 1 on a non-positive pivot.
+__global__ void __launch_bounds__(256) chol_inv_kernel(const double2* __restrict__ s, int b,
+                                                       double2* __restrict__ minv, int* __restrict__ flag) {
+  extern __shared__ double2 sm[];
+  double2* L = sm;                    // packed lower b(b+1)/2
+  double2* M = sm + b * (b + 1) / 2;  // packed lower b(b+1)/2
+  __shared__ double pivot;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < b * (b + 1) / 2; e += blockDim.x) {
+    int i = int((sqrt(8.0 * e + 1.0) - 1.0) / 2.0);
+    while (pk(i, 0) > e) --i;
+    while (pk(i + 1, 0) <= e) ++i;
+    const int j = e - pk(i, 0);
+    L[e] = s[i + i64(j) * b];
+  }
+  __syncthreads();
+  // Right-looking Cholesky.
+  for (int j = 0; j < b; ++j) {
+    if (tid == 0) {
+      double d = L[pk(j, j)].x;
+      if (!(d > 0.0)) {
+        atomicOr(flag, 1);
+        d = 1.0;
+      }
+      pivot = sqrt(d);
+      L[pk(j, j)] = make_double2(pivot, 0.0);
+    }
+    __syncthreads();
+    const double inv = 1.0 / pivot;
+    for (int i = j + 1 + tid; i < b; i += blockDim.x) {
+      double2 v = L[pk(i, j)];
+      L[pk(i, j)] = make_double2(v.x * inv, v.y * inv);
+    }
+    __syncthreads();
+    // trailing update: A[i][k] -= L[i][j] * conj(L[k][j]) for j < k <= i
+    const int m = b - j - 1;
+    const int cnt = m * (m + 1) / 2;
+    for (int e = tid; e < cnt; e += blockDim.x) {
+      int ii = int((sqrt(8.0 * e + 1.0) - 1.0) / 2.0);
+      while (ii * (ii + 1) / 2 > e) --ii;
+      while ((ii + 1) * (ii + 2) / 2 <= e) ++ii;
+      const int kk = e - ii * (ii + 1) / 2;
+      const int i = j + 1 + ii, k = j + 1 + kk;
+      const double2 lij = L[pk(i, j)], lkj = L[pk(k, j)];
+      double2 a = L[pk(i, k)];
+      // a -= lij * conj(lkj)
+      a.x -= lij.x * lkj.x + lij.y * lkj.y;
+      a.y -= lij.y * lkj.x - lij.x * lkj.y;
+      L[pk(i, k)] = a;
+    }
+    __syncthreads();
+  }
+  // M = L^{-1}: columns are independent forward substitutions.
+  for (int j = tid; j < b; j += blockDim.x) {
+    M[pk(j, j)] = make_double2(1.0 / L[pk(j, j)].x, 0.0);
+    for (int i = j + 1; i < b; ++i) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int k = j; k < i; ++k) acc = cfma(acc, L[pk(i, k)], M[pk(k, j)]);
+      const double inv = 1.0 / L[pk(i, i)].x;
+      M[pk(i, j)] = make_double2(-acc.x * inv, -acc.y * inv);
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < b * b; e += blockDim.x) {
+    const int j = e / b, i = e % b;
+    minv[e] = i >= j ? M[pk(i, j)] : make_double2(0.0, 0.0);
+  }
+}
+
+// One CTA of 32 x 32 threads: in-place right-looking Cholesky S = L L^H of a
+// b x b Hermitian matrix held whole in shared memory (b <= 112).  Writes L
+// (lower, column-major, leading dimension b) for a following TRSM.
+__global__ void __launch_bounds__(1024) chol_kernel(const double2* __restrict__ s, int b, double2* __restrict__ l,
+                                                    int* __restrict__ flag) {
+  extern __shared__ double2 sm[];
+  const int ld = b + 1;  // row-major A[i][k] at i*ld + k
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  __shared__ double piv;
+  for (int e = tid; e < b * b; e += 1024) {
+    const int k = e / b, i = e % b;  // coalesced read of column-major S(i,k)
+    sm[i * ld + k] = s[e];
+  }
+  __syncthreads();
+  (void)piv;
+  constexpr int NB = 16;  // blocked right-looking: 16-wide panels
+  for (int kb = 0; kb < b; kb += NB) {
+    const int ke = min(b, kb + NB);
+    // 1. unblocked factor of the diagonal block by warp 0
+    if (tid < 32) {
+      for (int j = kb; j < ke; ++j) {
+        double d = sm[j * ld + j].x;
+        if (!(d > 0.0)) {
+          if (tid == 0) atomicOr(flag, 1);
+          d = 1.0;
+        }
+        const double p = sqrt(d), inv = 1.0 / p;
+        __syncwarp();
+        if (tid == 0) sm[j * ld + j] = make_double2(p, 0.0);
+        const int i = j + 1 + tid;
+        if (i < ke) {
+          const double2 v = sm[i * ld + j];
+          sm[i * ld + j] = make_double2(v.x * inv, v.y * inv);
+        }
+        __syncwarp();
+        if (i < ke) {
+          const double2 lij = sm[i * ld + j];
+          for (int k = j + 1; k <= i; ++k) {
+            const double2 lkj = sm[k * ld + j];
+            double2 a = sm[i * ld + k];
+            a.x -= lij.x * lkj.x + lij.y * lkj.y;
+            a.y -= lij.y * lkj.x - lij.x * lkj.y;
+            sm[i * ld + k] = a;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // 2. panel: rows below solve x L_blk^H = a (forward substitution per row)
+    for (int i = ke + tid; i < b; i += 1024) {
+      for (int j = kb; j < ke; ++j) {
+        double2 a = sm[i * ld + j];
+        for (int t = kb; t < j; ++t) {
+          const double2 x = sm[i * ld + t], l = sm[j * ld + t];
+          a.x -= x.x * l.x + x.y * l.y;  // a -= x * conj(l)
+          a.y -= x.y * l.x - x.x * l.y;
+        }
+        const double inv = 1.0 / sm[j * ld + j].x;
+        sm[i * ld + j] = make_double2(a.x * inv, a.y * inv);
+      }
+    }
+    __syncthreads();
+    // 3. trailing update A[i][k] -= sum_t L[i][t] conj(L[k][t]), ke <= k <= i
+    for (int i = ke + ty; i < b; i += 32) {
+      for (int k = ke + tx; k <= i; k += 32) {
+        double2 a = sm[i * ld + k];
+#pragma unroll 4
+        for (int t = kb; t < ke; ++t) {
+          const double2 x = sm[i * ld + t], y = sm[k * ld + t];
+          a.x -= x.x * y.x + x.y * y.y;
+          a.y -= x.y * y.x - x.x * y.y;
+        }
+        sm[i * ld + k] = a;
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < b * b; e += 1024) {
+    const int k = e / b, i = e % b;
+    l[e] = i >= k ? sm[i * ld + k] : make_double2(0.0, 0.0);
+  }
+}
+
+}  // namespace
+
+void cholesky_small(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag) {
+  const size_t smem = size_t(b) * (b + 1) * sizeof(double2);
+  if (smem > 227 * 1024) fail(SK_ERR_UNSUPPORTED, "cholesky_small: block too large");
+  SKB_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  chol_kernel<<<1, dim3(32, 32), smem, ctx->stream>>>(s, b, l, flag);
+  ++ctx->launches;
+  SKB_LAUNCH("chol_kernel");
+}
+
+void cross_gram(sk_ctx* ctx, const double2* x, const double2* y, i64 n, int b, double2* out) {
+  const int tiles = (b + kTile - 1) / kTile;
+  // ~2 waves of CTAs over the SMs
+  i64 chunks = std::max<i64>(1, (2 * i64(ctx->sm_count)) / (tiles * tiles));
+  i64 rows = (n + chunks - 1) / chunks;
+  rows = ((rows + kRows - 1) / kRows) * kRows;
+  chunks = (n + rows - 1) / rows;
+  double2* partial = ctx->arena.get<double2>("ss:partial", chunks * b * b);
+  cross_gram_partial_kernel<<<dim3(unsigned(tiles * tiles), unsigned(chunks)), 256, 0, ctx->stream>>>(x, y, n, b, rows,
+                                                                                                       partial);
+  ++ctx->launches;
+  SKB_LAUNCH("cross_gram_partial");
+  reduce_partials_kernel<<<unsigned((b * b + 255) / 256), 256, 0, ctx->stream>>>(partial, int(chunks), b * b, out);
+  ++ctx->launches;
+  SKB_LAUNCH("reduce_partials");
+}
+
+void chol_inv(sk_ctx* ctx, const double2* s, int b, double2* minv, int* flag) {
+  const size_t smem = size_t(b) * (b + 1) * sizeof(double2);
+  if (smem > 227 * 1024) fail(SK_ERR_UNSUPPORTED, "chol_inv: block too large");
+  SKB_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  chol_inv_kernel<<<1, 256, smem, ctx->stream>>>(s, b, minv, flag);
+  ++ctx->launches;
+  SKB_LAUNCH("chol_inv");
+}
+
+}  // namespace skb

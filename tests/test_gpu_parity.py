@@ -182,10 +182,23 @@ def test_support_mask(K):  # test_maps.cpp:19-23
 
 # ------------------------------------------------------------------ end to end
 def _pipeline_case(K, O, calib, co, full, cfgk, cfgo, grid=None, name=""):
-    res = K.estimate_maps(K.Calib(calib, co), full, cfgk, want_raw=True)
+    import dataclasses
     ref = O.estimate_maps(O.Calib(f32(calib), co), full, cfgo, grid_dims=grid, want_raw=True)
+    out = None
+    # full cuSOLVER spectrum path, then the subspace solver (certified) that the bench runs
+    for solver, spectrum in ((1, True), (2, False)):
+        ck = dataclasses.replace(cfgk, eig_solver=solver, certify=1)
+        res = _pipeline_check(K, O, calib, co, full, ck, ref, spectrum, f"{name}/{'full' if solver == 1 else 'subspace'}")
+        out = out or res
+    return out, ref
+
+
+def _pipeline_check(K, O, calib, co, full, cfgk, ref, want_spectrum, name):
+    res = K.estimate_maps(K.Calib(calib, co), full, cfgk, want_raw=True, want_spectrum=want_spectrum)
     assert res.nullspace_rank == ref.nullspace_rank, (res.nullspace_rank, ref.nullspace_rank)
-    if res.spectrum_normalized is not None and res.spectrum_normalized.any():
+    if cfgk.eig_solver == 2:
+        assert res.extra["eig_solver"] == "subspace" and res.extra["certified"], res.extra
+    if want_spectrum:
         # eigenvalues sigma^2 of the fp32 Gram: absolute error ~ eps*||G|| (tiny sigmas are noise-level)
         assert np.abs(res.spectrum_normalized ** 2 - ref.spectrum_normalized ** 2).max() < 1e-5
     lam_raw = PM.lambda_errors(res.raw_lambda, ref.raw_lambda)
@@ -195,7 +208,7 @@ def _pipeline_case(K, O, calib, co, full, cfgk, cfgo, grid=None, name=""):
     mask_agree = float(np.mean(res.support_mask == ref.support_mask))
     report("estimate_maps", case=name, rank=res.nullspace_rank, cut_margin=res.cut_margin, lambda_raw=lam_raw,
            lambda_final=lam_fin, maps_nrmse=nrmse, raw_maps_nrmse_all=raw_nrmse, mask_agree=mask_agree,
-           stage_ms=res.stage_ms, total_ms=res.total_ms)
+           stage_ms=res.stage_ms, total_ms=res.total_ms, solver=res.extra)
     assert lam_raw["normwise"] < PM.TOL_LAMBDA
     assert lam_fin["normwise"] < PM.TOL_LAMBDA
     assert nrmse < PM.TOL_MAPS
@@ -203,7 +216,7 @@ def _pipeline_case(K, O, calib, co, full, cfgk, cfgo, grid=None, name=""):
     # unit sum-of-squares inside the mask (test_maps.cpp:137-146)
     m = res.maps.reshape(res.maps.shape[0], -1)[:, res.support_mask.ravel() > 0]
     assert np.abs(np.sum(np.abs(m) ** 2, 0) - 1).max() < 1e-4
-    return res, ref
+    return res
 
 
 def _cfgs(K, O, spec):
