@@ -130,7 +130,108 @@ __global__ void __launch_bounds__(256) axis_row_kernel(const float2* __restrict_
   }
 }
 
+// Symmetric-tap centred DFT along an axis (the G(x) lag expansion,
+// spatial_gram.cpp:125-138): taps a = 0..2H hold lags l = a - H, and
+//   out[b][j][i] = x_0 + sum_{l=1..H} [ c_jl (x_l + x_-l) + i s_jl (x_l - x_-l) ]
+// with (c, s) = (cos, sign*sin)(2 pi l (j - j0) / N).  Pairing l with -l
+// halves the FMAs of the generic contraction.  A thread owns one (b, i)
+// column: it forms S_l = x_l + x_-l and D_l = x_l - x_-l once in registers,
+// then sweeps its block's j range with the (c, s) table broadcast from
+// shared memory; stores are 256-byte coalesced along i.
+template <int H>
+__global__ void __launch_bounds__(256) axis_symdft_kernel(const float2* __restrict__ in, float2* __restrict__ out,
+                                                          const float2* __restrict__ cs, int N, i64 inner) {
+  // Each thread owns TWO columns (i, i + 32): every table entry read from
+  // shared memory feeds 8 FMAs.
+  __shared__ __align__(16) float2 tab[kColJ * H];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const i64 nchunk = (inner + 63) / 64;
+  const i64 b = i64(blockIdx.x) / nchunk;
+  const i64 i0 = (i64(blockIdx.x) % nchunk) * 64 + tx;
+  constexpr int L = 2 * H + 1;
+  float2 S[2][H], D[2][H], x0[2];
+  bool live[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const i64 i = i0 + 32 * u;
+    live[u] = i < inner;
+    x0[u] = live[u] ? in[(b * L + H) * inner + i] : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int l = 0; l < H; ++l) {
+      float2 xp = make_float2(0.f, 0.f), xm = make_float2(0.f, 0.f);
+      if (live[u]) {
+        xp = in[(b * L + H + 1 + l) * inner + i];
+        xm = in[(b * L + H - 1 - l) * inner + i];
+      }
+      S[u][l] = make_float2(xp.x + xm.x, xp.y + xm.y);
+      D[u][l] = make_float2(xp.x - xm.x, xp.y - xm.y);
+    }
+  }
+  float2* dst = out + b * N * inner + i0;
+  // The block sweeps every output row; the (c, s) table streams through
+  // shared memory in kColJ-row chunks.
+  for (int j_begin = 0; j_begin < N; j_begin += kColJ) {
+    const int j_count = min(kColJ, N - j_begin);
+    __syncthreads();
+    for (int e = ty * 32 + tx; e < kColJ * H; e += 256) {
+      const int jj = e / H, l = e % H;
+      tab[e] = jj < j_count ? cs[i64(j_begin + jj) * H + l] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    for (int jj = ty; jj < j_count; jj += 8) {
+      const float4* row = reinterpret_cast<const float4*>(tab + jj * H);
+      float ax[2], ay[2], bx[2], by[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        ax[u] = x0[u].x;
+        ay[u] = x0[u].y;
+        bx[u] = 0.f;
+        by[u] = 0.f;
+      }
+#pragma unroll
+      for (int l = 0; l < H; l += 2) {
+        const float4 t = row[l / 2];  // (c_l, s_l, c_l+1, s_l+1)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          ax[u] = fmaf(t.x, S[u][l].x, ax[u]);
+          ax[u] = fmaf(-t.y, D[u][l].y, ax[u]);
+          ay[u] = fmaf(t.x, S[u][l].y, ay[u]);
+          ay[u] = fmaf(t.y, D[u][l].x, ay[u]);
+          bx[u] = fmaf(t.z, S[u][l + 1].x, bx[u]);
+          bx[u] = fmaf(-t.w, D[u][l + 1].y, bx[u]);
+          by[u] = fmaf(t.z, S[u][l + 1].y, by[u]);
+          by[u] = fmaf(t.w, D[u][l + 1].x, by[u]);
+        }
+      }
+      float2* d = dst + i64(j_begin + jj) * inner;
+      if (live[0]) d[0] = make_float2(ax[0] + bx[0], ay[0] + by[0]);
+      if (live[1]) d[32] = make_float2(ax[1] + bx[1], ay[1] + by[1]);
+    }
+  }
+}
+
 }  // namespace
+
+void apply_axis_symdft(sk_ctx* ctx, const float2* in, float2* out, const float2* cs, i64 batch, int H, int N,
+                       i64 inner) {
+  if (batch <= 0 || N <= 0 || inner <= 0) return;
+  if (inner < 32 || H > 16 || (H & 1)) fail(9, "apply_axis_symdft: needs inner >= 32 and even H <= 16");
+  const i64 gx = (inner + 63) / 64 * batch;
+  if (gx > 0x7fffffffLL) fail(9, "apply_axis_symdft: grid too large");
+  const dim3 grid{unsigned(gx)}, block{32, 8};
+  switch (H) {
+    case 2: axis_symdft_kernel<2><<<grid, block, 0, ctx->stream>>>(in, out, cs, N, inner); break;
+    case 4: axis_symdft_kernel<4><<<grid, block, 0, ctx->stream>>>(in, out, cs, N, inner); break;
+    case 6: axis_symdft_kernel<6><<<grid, block, 0, ctx->stream>>>(in, out, cs, N, inner); break;
+    case 8: axis_symdft_kernel<8><<<grid, block, 0, ctx->stream>>>(in, out, cs, N, inner); break;
+    case 10: axis_symdft_kernel<10><<<grid, block, 0, ctx->stream>>>(in, out, cs, N, inner); break;
+    case 12: axis_symdft_kernel<12><<<grid, block, 0, ctx->stream>>>(in, out, cs, N, inner); break;
+    case 14: axis_symdft_kernel<14><<<grid, block, 0, ctx->stream>>>(in, out, cs, N, inner); break;
+    default: axis_symdft_kernel<16><<<grid, block, 0, ctx->stream>>>(in, out, cs, N, inner); break;
+  }
+  ++ctx->launches;
+  SKB_LAUNCH("axis_symdft_kernel");
+}
 
 // Mt (L x N) is stored right after M (N x L) in the same allocation.
 void apply_axis(sk_ctx* ctx, const float2* in, float2* out, const float2* M, i64 batch, int L, int N, i64 inner) {

@@ -100,6 +100,9 @@ namespace skb {
 // Separable "apply a small matrix along one axis":
 //   out[b][j][i] = sum_a M[j][a] * in[b][a][i],  M is N x L (row-major, c64).
 void apply_axis(sk_ctx* ctx, const float2* in, float2* out, const float2* M, i64 batch, int L, int N, i64 inner);
+// Symmetric-tap centred DFT (taps l = -H..H): cs[j][l-1] = (cos, sign*sin)(2 pi l (j - j0)/N).
+void apply_axis_symdft(sk_ctx* ctx, const float2* in, float2* out, const float2* cs, i64 batch, int H, int N,
+                       i64 inner);
 
 // K1: pairwise correlation on the lag box + Gram assembly (calibration.cpp:111-142).
 struct GramGeom {

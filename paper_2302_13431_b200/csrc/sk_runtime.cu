@@ -237,6 +237,55 @@ void separable(sk_ctx* ctx, const float2* in, float2* out, i64 batch, const Dims
   }
 }
 
+// (cos, sign*sin)(2 pi l (j - j0) / N) for j < N, l = 1..H (row-major [j][l-1]).
+float2* symdft_table(sk_ctx* ctx, int N, int H, i64 j0, int sign) {
+  const std::string key = "symcs:" + std::to_string(N) + ":" + std::to_string(H) + ":" + std::to_string(j0) + ":" +
+                          std::to_string(sign);
+  auto it = ctx->matrices.mats.find(key);
+  if (it != ctx->matrices.mats.end()) return it->second;
+  std::vector<float2> h(size_t(N) * H);
+  for (int j = 0; j < N; ++j)
+    for (int l = 1; l <= H; ++l) {
+      const std::complex<double> z = cis(+1, i64(l) * (j - j0), N);
+      h[size_t(j) * H + (l - 1)] = make_float2(float(z.real()), float(sign * z.imag()));
+    }
+  float2* d = nullptr;
+  SKB_CUDA(cudaMalloc(&d, h.size() * sizeof(float2)));
+  SKB_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  ctx->matrices.mats[key] = d;
+  return d;
+}
+
+// G(x) lag expansion (spatial_gram.cpp:125-138): lag box [h][lb]^D -> planes
+// [h][grid].  Axes are transformed last to first; stages whose inner extent
+// is >= 32 use the symmetric-tap kernel, the innermost axis the generic one.
+void expand_lags(sk_ctx* ctx, const float2* lags, float2* planes, i64 h, int tau, const Dims& grid) {
+  const int nd = int(grid.size()), lb = 4 * tau + 1, H = 2 * tau;
+  Dims cur(static_cast<size_t>(nd), lb);
+  const float2* src = lags;
+  for (int a = nd - 1; a >= 0; --a) {
+    float2* dst;
+    if (a == 0) {
+      dst = planes;
+    } else {
+      Dims next = cur;
+      next[size_t(a)] = grid[size_t(a)];
+      dst = ctx->arena.get<float2>(std::string("field:tmp") + (a % 2 ? ":a" : ":b"), h * numel(next));
+    }
+    i64 b = h, inner = 1;
+    for (int k = 0; k < a; ++k) b *= cur[size_t(k)];
+    for (int k = a + 1; k < nd; ++k) inner *= cur[size_t(k)];
+    const int N = int(grid[size_t(a)]);
+    if (inner >= 32 && H <= 16) {
+      apply_axis_symdft(ctx, src, dst, symdft_table(ctx, N, H, center_index(N), -1), b, H, N, inner);
+    } else {
+      apply_axis(ctx, src, dst, dft_matrix(ctx, N, lb, 2 * tau, center_index(N), -1, 0.0), b, lb, N, inner);
+    }
+    cur[size_t(a)] = grid[size_t(a)];
+    src = dst;
+  }
+}
+
 // Cached device tables per (support, q).
 struct SupportTables {
   int2* pairs = nullptr;  // h entries (p <= q)
@@ -750,13 +799,8 @@ float2* run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims
   }
   float2* lags = ctx->arena.get<float2>("field:lags", i64(h) * t.nbox);
   fold_lags_f64(ctx, ws, n, h, lam, t.nbox, t.pairs, t.lag_ptr, t.lag_st, true, lags);
-  const int nd = int(grid.size());
-  Dims box(size_t(nd), t.lb);
-  std::vector<float2*> mats(static_cast<size_t>(nd));
-  for (int a = 0; a < nd; ++a)
-    mats[size_t(a)] = dft_matrix(ctx, int(grid[size_t(a)]), t.lb, 2 * s.tau, center_index(grid[size_t(a)]), -1, 0.0);
   float2* planes = ctx->arena.get<float2>("field:planes", i64(h) * numel(grid));
-  separable(ctx, lags, planes, h, box, grid, mats, "field:tmp");
+  expand_lags(ctx, lags, planes, h, s.tau, grid);
   return planes;
 }
 
@@ -767,13 +811,8 @@ float2* run_field_from_w(sk_ctx* ctx, const float2* w, const Support& s, int q, 
   const int h = q * (q + 1) / 2;
   float2* lags = ctx->arena.get<float2>("field:lags", i64(h) * t.nbox);
   fold_lags_f32(ctx, w, n, h, int(s.count), t.nbox, t.pairs, t.lag_ptr, t.lag_st, lags);
-  const int nd = int(grid.size());
-  Dims box(size_t(nd), t.lb);
-  std::vector<float2*> mats(static_cast<size_t>(nd));
-  for (int a = 0; a < nd; ++a)
-    mats[size_t(a)] = dft_matrix(ctx, int(grid[size_t(a)]), t.lb, 2 * s.tau, center_index(grid[size_t(a)]), -1, 0.0);
   float2* planes = ctx->arena.get<float2>("field:planes", i64(h) * numel(grid));
-  separable(ctx, lags, planes, h, box, grid, mats, "field:tmp");
+  expand_lags(ctx, lags, planes, h, s.tau, grid);
   return planes;
 }
 
