@@ -578,7 +578,11 @@ void small_heev(sk_ctx* ctx, double2* H, i64 b, double* w, int* d_info) {
 // (synchronous path) failure; the fast path raises `flag` instead.
 bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int passes = 2) {
   (void)tmp;
-  if (b > kSmallBlockMax) {
+  static const bool lib_chol = [] {
+    const char* v = std::getenv("SKB_SMALL_CHOL");
+    return !(v && std::string(v) == "custom");  // default: cuSOLVER POTRF (no host sync)
+  }();
+  if (b > 256 || (!lib_chol && b > kSmallBlockMax)) {
     for (int p = 0; p < passes; ++p)
       if (!cholqr(ctx, x, n, b)) return false;
     return true;
@@ -586,10 +590,6 @@ bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int 
   double2* S = ctx->arena.get<double2>("ss:S", b * b);
   double2* L = ctx->arena.get<double2>("ss:L", b * b);
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
-  static const bool lib_chol = [] {
-    const char* v = std::getenv("SKB_SMALL_CHOL");
-    return !(v && std::string(v) == "custom");  // default: cuSOLVER POTRF (no host sync)
-  }();
   for (int pass = 0; pass < passes; ++pass) {
     cross_gram(ctx, x, x, n, int(b), S);        // S = X^H X
     if (lib_chol) {
@@ -665,7 +665,7 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
     zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);
     ++iters;
     // Rayleigh-Ritz on span(V): H = V^H A V = S diag(w) S^H.
-    if (b <= kSmallBlockMax) {
+    if (b <= 256) {
       cross_gram(ctx, V, Y, n, int(b), H);
     } else {
       zgemm(ctx, CUBLAS_OP_C, CUBLAS_OP_N, b, b, n, V, n, Y, n, H, b);
@@ -771,7 +771,7 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
 Eig run_nullspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, int solver, bool need_spectrum,
                   bool certify) {
   if (!(ratio > 0.0 && ratio < 1.0)) fail(SK_ERR_DIM, "nullspace threshold ratio must lie in (0,1)");
-  const bool subspace = solver == 2 || (solver == 0 && !need_spectrum && n > 512);
+  const bool subspace = solver == 2 || (solver == 0 && !need_spectrum && n > 128);
   if (subspace) {
     Eig e;
     if (run_eigh_subspace(ctx, gram, n, ratio, certify, e)) return e;
