@@ -1,0 +1,175 @@
+// K3 — G(x) lag expansion (spatial_gram.cpp:125-138) in FP64.
+//
+// G_pq(x) = sum_l k_pq[l] exp(-i 2 pi l . x) over the (4 tau + 1)^D lag box,
+// evaluated separably axis by axis (last axis first).  Lags are symmetric
+// (l in [-H, H], H = 2 tau), so each output is
+//   x_0 + sum_{l=1..H} [ c_l (x_l + x_-l) + i s_l (x_l - x_-l) ],
+// (c, s) = (cos, -sin)(2 pi l (j - j0) / N): half the MACs of a plain DFT.
+//
+// Arithmetic is FP64 and the final stage writes G as an fp32 pair
+// (hi = fl32(G), lo = fl32(G - hi)): K4 iterates on hi alone (FP32, registers)
+// and evaluates the Rayleigh quotient on hi + lo, so per-voxel eigenvalues
+// keep ~FP64 accuracy even where lambda ~ 1e-4.
+//
+//  * expand_row: stage along an axis with small inner extent (always the last
+//    axis): a block stages RB rows' (S, D) in shared memory and each thread
+//    owns one output index j with its (c, s) row in registers.
+//  * expand_col: inner >= 32: a warp owns 32 consecutive inner indices, each
+//    thread keeps its column's (S, D) in registers and sweeps all output rows
+//    with the (c, s) table broadcast from shared memory (256-byte stores).
+#include "sk_internal.h"
+
+namespace skb {
+
+namespace {
+
+constexpr int kRB = 8;       // rows per expand_row block
+constexpr int kColRows = 32; // table rows staged per chunk in expand_col
+
+__device__ __forceinline__ void store_out(double2 v, double2* out64, float2* hi, float2* lo, i64 idx) {
+  if (out64) {
+    out64[idx] = v;
+  } else {
+    const float hx = float(v.x), hy = float(v.y);
+    hi[idx] = make_float2(hx, hy);
+    lo[idx] = make_float2(float(v.x - double(hx)), float(v.y - double(hy)));
+  }
+}
+
+template <int H>
+__global__ void __launch_bounds__(256) expand_row_kernel(const double2* __restrict__ in, i64 rows, i64 inner, int N,
+                                                         const double2* __restrict__ cs, double2* out64, float2* hi,
+                                                         float2* lo) {
+  constexpr int L = 2 * H + 1;
+  __shared__ double2 sS[kRB][H + 1], sD[kRB][H + 1];  // [row][0] of sS holds x_0
+  const i64 r0 = i64(blockIdx.x) * kRB;
+  for (int e = threadIdx.x; e < kRB * (H + 1); e += blockDim.x) {
+    const int r = e / (H + 1), l = e % (H + 1);
+    const i64 row = r0 + r;
+    double2 s = make_double2(0.0, 0.0), d = make_double2(0.0, 0.0);
+    if (row < rows) {
+      const i64 b = row / inner, i = row % inner;
+      if (l == 0) {
+        s = in[(b * L + H) * inner + i];
+      } else {
+        const double2 xp = in[(b * L + H + l) * inner + i], xm = in[(b * L + H - l) * inner + i];
+        s = make_double2(xp.x + xm.x, xp.y + xm.y);
+        d = make_double2(xp.x - xm.x, xp.y - xm.y);
+      }
+    }
+    sS[r][l] = s;
+    sD[r][l] = d;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    double2 t[H > 0 ? H : 1];
+#pragma unroll
+    for (int l = 0; l < H; ++l) t[l] = cs[i64(j) * H + l];
+    for (int r = 0; r < kRB; ++r) {
+      const i64 row = r0 + r;
+      if (row >= rows) break;
+      double ax = 0.0, ay = 0.0;
+#pragma unroll
+      for (int l = 0; l < H; ++l) {
+        const double2 S = sS[r][l + 1], D = sD[r][l + 1];
+        ax = fma(t[l].x, S.x, ax);
+        ax = fma(-t[l].y, D.y, ax);
+        ay = fma(t[l].x, S.y, ay);
+        ay = fma(t[l].y, D.x, ay);
+      }
+      const double2 x0 = sS[r][0];
+      const i64 b = row / inner, i = row % inner;
+      store_out(make_double2(x0.x + ax, x0.y + ay), out64, hi, lo, (b * N + j) * inner + i);
+    }
+  }
+}
+
+template <int H>
+__global__ void __launch_bounds__(256) expand_col_kernel(const double2* __restrict__ in, i64 inner, int N,
+                                                         const double2* __restrict__ cs, double2* out64, float2* hi,
+                                                         float2* lo) {
+  constexpr int L = 2 * H + 1;
+  __shared__ __align__(16) double2 tab[kColRows * (H > 0 ? H : 1)];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const i64 nchunk = (inner + 31) / 32;
+  const i64 b = i64(blockIdx.x) / nchunk;
+  const i64 i = (i64(blockIdx.x) % nchunk) * 32 + tx;
+  const bool live = i < inner;
+  double2 S[H > 0 ? H : 1], D[H > 0 ? H : 1], x0 = make_double2(0.0, 0.0);
+  if (live) x0 = in[(b * L + H) * inner + i];
+#pragma unroll
+  for (int l = 0; l < H; ++l) {
+    double2 xp = make_double2(0.0, 0.0), xm = make_double2(0.0, 0.0);
+    if (live) {
+      xp = in[(b * L + H + 1 + l) * inner + i];
+      xm = in[(b * L + H - 1 - l) * inner + i];
+    }
+    S[l] = make_double2(xp.x + xm.x, xp.y + xm.y);
+    D[l] = make_double2(xp.x - xm.x, xp.y - xm.y);
+  }
+  for (int j_begin = 0; j_begin < N; j_begin += kColRows) {
+    const int j_count = min(kColRows, N - j_begin);
+    __syncthreads();
+    for (int e = ty * 32 + tx; e < kColRows * H; e += 256) {
+      const int jj = e / H, l = e % H;
+      tab[e] = jj < j_count ? cs[i64(j_begin + jj) * H + l] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    if (!live) continue;
+    for (int jj = ty; jj < j_count; jj += 8) {
+      const double2* row = tab + jj * H;
+      double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
+#pragma unroll
+      for (int l = 0; l < H; l += 2) {
+        const double2 t0 = row[l], t1 = row[l + 1];
+        ax = fma(t0.x, S[l].x, ax);
+        ax = fma(-t0.y, D[l].y, ax);
+        ay = fma(t0.x, S[l].y, ay);
+        ay = fma(t0.y, D[l].x, ay);
+        bx = fma(t1.x, S[l + 1].x, bx);
+        bx = fma(-t1.y, D[l + 1].y, bx);
+        by = fma(t1.x, S[l + 1].y, by);
+        by = fma(t1.y, D[l + 1].x, by);
+      }
+      store_out(make_double2(x0.x + (ax + bx), x0.y + (ay + by)), out64, hi, lo,
+                (b * N + j_begin + jj) * inner + i);
+    }
+  }
+}
+
+template <int H>
+void launch_stage(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int N, const double2* cs, double2* out64,
+                  float2* hi, float2* lo) {
+  if (inner >= 32) {
+    const i64 gx = (inner + 31) / 32 * batch;
+    if (gx > 0x7fffffffLL) fail(SK_ERR_UNSUPPORTED, "expand: grid too large");
+    expand_col_kernel<H><<<dim3{unsigned(gx)}, dim3{32, 8}, 0, ctx->stream>>>(in, inner, N, cs, out64, hi, lo);
+  } else {
+    const i64 rows = batch * inner;
+    const int threads = N >= 256 ? 256 : (N >= 128 ? 128 : 64);
+    expand_row_kernel<H><<<unsigned((rows + kRB - 1) / kRB), threads, 0, ctx->stream>>>(in, rows, inner, N, cs, out64,
+                                                                                          hi, lo);
+  }
+  ++ctx->launches;
+  SKB_LAUNCH("expand stage");
+}
+
+}  // namespace
+
+void expand_stage_f64(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int H, int N, const double2* cs,
+                      double2* out64, float2* hi, float2* lo) {
+  if (batch <= 0 || N <= 0 || inner <= 0) return;
+  switch (H) {
+    case 0: launch_stage<0>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
+    case 2: launch_stage<2>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
+    case 4: launch_stage<4>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
+    case 6: launch_stage<6>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
+    case 8: launch_stage<8>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
+    case 10: launch_stage<10>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
+    case 12: launch_stage<12>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
+    case 14: launch_stage<14>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
+    default: fail(SK_ERR_UNSUPPORTED, "G(x) expansion: kernel radius > 7 is outside the B200 path");
+  }
+}
+
+}  // namespace skb

@@ -4,7 +4,9 @@
 //   k_pq[l] = sum_{(s,t): n_t - n_s = l} W[q|L| + s, p|L| + t]      (p <= q)
 //
 // The (s,t) lists per lag are a CSR table built once per support on the host,
-// so every output is a fixed-order sum (deterministic, no atomics).
+// so every output is a fixed-order sum (deterministic, no atomics).  Lag
+// kernels are kept in FP64: the G(x) expansion that follows runs in FP64 and
+// only its output is rounded (to an fp32 hi/lo pair).
 //
 // On the pipeline path W is never formed from the R ~ n nullspace filters:
 // with a complete orthonormal eigenbasis W = F F^H = I - U_sig U_sig^H, where
@@ -20,11 +22,10 @@ namespace {
 template <bool kSignal>
 __global__ void __launch_bounds__(256) fold_f64_kernel(const double2* __restrict__ w, i64 n, int lam, int nbox,
                                                        const int2* __restrict__ pairs, const int* __restrict__ ptr,
-                                                       const int* __restrict__ st, float2* __restrict__ lags) {
+                                                       const int* __restrict__ st, double2* __restrict__ lags) {
   const int2 pq = pairs[blockIdx.x];
   const int p = pq.x, q = pq.y;
   const i64 row0 = i64(q) * lam, col0 = i64(p) * lam;
-  const int ctr = (nbox - 1) / 2;
   for (int l = threadIdx.x; l < nbox; l += blockDim.x) {
     double re = 0.0, im = 0.0;
     for (int e = ptr[l]; e < ptr[l + 1]; ++e) {
@@ -47,32 +48,31 @@ __global__ void __launch_bounds__(256) fold_f64_kernel(const double2* __restrict
       re += v.x;
       im += v.y;
     }
-    (void)ctr;
-    lags[i64(blockIdx.x) * nbox + l] = make_float2(float(re), float(im));
+    lags[i64(blockIdx.x) * nbox + l] = make_double2(re, im);
   }
 }
 
 __global__ void __launch_bounds__(256) fold_f32_kernel(const float2* __restrict__ w, i64 n, int lam, int nbox,
                                                        const int2* __restrict__ pairs, const int* __restrict__ ptr,
-                                                       const int* __restrict__ st, float2* __restrict__ lags) {
+                                                       const int* __restrict__ st, double2* __restrict__ lags) {
   const int2 pq = pairs[blockIdx.x];
   const i64 row0 = i64(pq.y) * lam, col0 = i64(pq.x) * lam;
   for (int l = threadIdx.x; l < nbox; l += blockDim.x) {
-    float re = 0.f, im = 0.f;
+    double re = 0.0, im = 0.0;
     for (int e = ptr[l]; e < ptr[l + 1]; ++e) {
       const int s = st[e] & 0xffff, t = st[e] >> 16;
       const float2 v = w[(row0 + s) + (col0 + t) * n];
       re += v.x;
       im += v.y;
     }
-    lags[i64(blockIdx.x) * nbox + l] = make_float2(re, im);
+    lags[i64(blockIdx.x) * nbox + l] = make_double2(re, im);
   }
 }
 
 }  // namespace
 
 void fold_lags_f64(sk_ctx* ctx, const double2* w, i64 n, int npairs, int lam, int nbox, const int2* d_pairs,
-                   const int* d_lag_ptr, const int* d_lag_st, bool w_is_signal, float2* lags) {
+                   const int* d_lag_ptr, const int* d_lag_st, bool w_is_signal, double2* lags) {
   if (w_is_signal)
     fold_f64_kernel<true><<<npairs, 256, 0, ctx->stream>>>(w, n, lam, nbox, d_pairs, d_lag_ptr, d_lag_st, lags);
   else
@@ -82,7 +82,7 @@ void fold_lags_f64(sk_ctx* ctx, const double2* w, i64 n, int npairs, int lam, in
 }
 
 void fold_lags_f32(sk_ctx* ctx, const float2* w, i64 n, int npairs, int lam, int nbox, const int2* d_pairs,
-                   const int* d_lag_ptr, const int* d_lag_st, float2* lags) {
+                   const int* d_lag_ptr, const int* d_lag_st, double2* lags) {
   fold_f32_kernel<<<npairs, 256, 0, ctx->stream>>>(w, n, lam, nbox, d_pairs, d_lag_ptr, d_lag_st, lags);
   ++ctx->launches;
   SKB_LAUNCH("fold_f32_kernel");

@@ -122,9 +122,13 @@ void gram_pairs_launch(sk_ctx* ctx, const float2* spectra, const GramGeom& g, co
 // (spatial_gram.cpp:108-131).  w_is_signal: W = I - w (w = U_sig U_sig^H,
 // lower triangle valid) else W = w (full matrix).
 void fold_lags_f64(sk_ctx* ctx, const double2* w, i64 n, int npairs, int lam, int nbox, const int2* d_pairs,
-                   const int* d_lag_ptr, const int* d_lag_st, bool w_is_signal, float2* lags);
+                   const int* d_lag_ptr, const int* d_lag_st, bool w_is_signal, double2* lags);
 void fold_lags_f32(sk_ctx* ctx, const float2* w, i64 n, int npairs, int lam, int nbox, const int2* d_pairs,
-                   const int* d_lag_ptr, const int* d_lag_st, float2* lags);
+                   const int* d_lag_ptr, const int* d_lag_st, double2* lags);
+// One FP64 stage of the G(x) lag expansion (sk_expand.cu): in [batch][2H+1][inner]
+// -> out [batch][N][inner]; final stage writes the fp32 hi/lo pair (out64 == nullptr).
+void expand_stage_f64(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int H, int N, const double2* cs,
+                      double2* out64, float2* hi, float2* lo);
 
 // K4: batched per-voxel power iteration over packed Hermitian planes
 // [h][N] (h = Q(Q+1)/2, plane (p<=q) holds M(row p, col q)).
@@ -133,6 +137,7 @@ void fold_lags_f32(sk_ctx* ctx, const float2* w, i64 n, int npairs, int lam, int
 // against recon [Q][N] (maps.cpp:117-172), zeroed voxel count, mask.
 struct PowerArgs {
   const float2* planes;
+  const float2* planes_lo;  // nullable: fp32 residual G - hi, used only in the final Rayleigh quotient
   i64 n;            // voxels
   int q;            // channels
   int iters;
@@ -152,7 +157,7 @@ void power_iteration(sk_ctx* ctx, const PowerArgs& a);
 void c64_to_c128(sk_ctx* ctx, const float2* in, double2* out, i64 n);
 void c128_to_c64(sk_ctx* ctx, const double2* in, float2* out, i64 n);
 void field_full_to_planes(sk_ctx* ctx, const float2* field, i64 n, int q, float2* planes);
-void planes_to_field_full(sk_ctx* ctx, const float2* planes, i64 n, int q, float2* field);
+void planes_to_field_full(sk_ctx* ctx, const float2* planes, const float2* planes_lo, i64 n, int q, float2* field);
 void espirit_field(sk_ctx* ctx, float2* field, i64 n, int q, float inv_lam);
 void renormalize_and_mask(sk_ctx* ctx, float2* maps, i64 n, int q, const float2* lambda_c, float* lambda,
                           uint8_t* mask, float thr);

@@ -40,7 +40,8 @@ __global__ void full_to_planes_kernel(const float2* __restrict__ field, i64 n, i
 
 // planes -> GramField with the conjugate mirror and real diagonal
 // (spatial_gram.cpp:133-146).
-__global__ void planes_to_full_kernel(const float2* __restrict__ planes, i64 n, int q, float2* __restrict__ field) {
+__global__ void planes_to_full_kernel(const float2* __restrict__ planes, const float2* __restrict__ planes_lo, i64 n,
+                                      int q, float2* __restrict__ field) {
   const i64 total = n * q * q;
   for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
     const i64 j = e / (i64(q) * q);
@@ -49,6 +50,10 @@ __global__ void planes_to_full_kernel(const float2* __restrict__ planes, i64 n, 
     const int p = min(row, col), c = max(row, col);
     const int pair = p * q - p * (p - 1) / 2 + (c - p);
     float2 v = planes[i64(pair) * n + j];
+    if (planes_lo) {
+      const float2 l = planes_lo[i64(pair) * n + j];
+      v = make_float2(float(double(v.x) + double(l.x)), float(double(v.y) + double(l.y)));
+    }
     if (row > col) v.y = -v.y;
     if (row == col) v.y = 0.f;
     field[e] = v;
@@ -246,8 +251,8 @@ void field_full_to_planes(sk_ctx* ctx, const float2* field, i64 n, int q, float2
   ++ctx->launches;
   SKB_LAUNCH("full_to_planes");
 }
-void planes_to_field_full(sk_ctx* ctx, const float2* planes, i64 n, int q, float2* field) {
-  planes_to_full_kernel<<<SKB_GRID(n * q * q)>>>(planes, n, q, field);
+void planes_to_field_full(sk_ctx* ctx, const float2* planes, const float2* planes_lo, i64 n, int q, float2* field) {
+  planes_to_full_kernel<<<SKB_GRID(n * q * q)>>>(planes, planes_lo, n, q, field);
   ++ctx->launches;
   SKB_LAUNCH("planes_to_full");
 }

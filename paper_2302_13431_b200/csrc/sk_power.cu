@@ -68,6 +68,22 @@ __device__ __forceinline__ float group_sum(float x, float* red, int vox, int hal
 }
 
 template <int QP>
+__device__ __forceinline__ double group_sum_d(double x, double* red, int vox, int half) {
+  if constexpr (QP <= 32) {
+#pragma unroll
+    for (int o = QP / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+  } else {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[vox * 2 + half] = x;
+    __syncthreads();
+    return red[vox * 2] + red[vox * 2 + 1];
+  }
+}
+
+template <int QP>
 __device__ __forceinline__ void group_sync() {
   if constexpr (QP <= 32)
     __syncwarp();
@@ -87,7 +103,8 @@ __global__ void __launch_bounds__(256, (QP <= 32 ? 2 : 1)) power_kernel(PowerArg
   const int tile_elems = (h > QP ? h : QP) * VPB;
   float2* gbuf = reinterpret_cast<float2*>(smem_raw);             // [2][tile_elems]
   float2* vs = gbuf + 2 * tile_elems;                             // [VPB][kStride]
-  float* red = reinterpret_cast<float*>(vs + VPB * G::kStride);   // [VPB][2]
+  double* redd = reinterpret_cast<double*>(vs + VPB * G::kStride);  // [VPB][2]
+  float* red = reinterpret_cast<float*>(redd + VPB * 2);           // [VPB][2]
 
   const int vox = threadIdx.x / QP;
   const int p = threadIdx.x % QP;
@@ -136,6 +153,17 @@ __global__ void __launch_bounds__(256, (QP <= 32 ? 2 : 1)) power_kernel(PowerArg
       if (p == c) val.y = 0.f;  // spatial_gram.cpp:140-146
     }
     m[c] = val;
+  }
+  // The tile buffer is free once every row is in registers: stream the lo
+  // residual planes into it while the iterations run (hi/lo split, sk_expand.cu).
+  if (a.planes_lo != nullptr) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < h * VPB; e += blockDim.x) {
+      const int pair = e / VPB, v = e % VPB;
+      const bool ok = j0 + v < a.n;
+      cp_async8(gs + e, a.planes_lo + (ok ? i64(pair) * a.n + j0 + v : 0), ok ? 8 : 0);
+    }
+    cp_async_commit();
   }
 
   float2* myv = vs + vox * G::kStride;
@@ -235,10 +263,37 @@ __global__ void __launch_bounds__(256, (QP <= 32 ? 2 : 1)) power_kernel(PowerArg
     group_sync<QP>();
   }
 
-  // Rayleigh quotient: mv = Re(v^H M v); value = Re(v^H B v).
-  float2 mvv;
-  matvec(mvv);
-  const float mv = group_sum<QP>(vp.x * mvv.x + vp.y * mvv.y, red, vox, half);
+  // Rayleigh quotient in FP64 on M = hi + lo: mv = Re(v^H M v) (the FP32
+  // iterate v enters only to second order); value = Re(v^H B v).
+  double mrx = 0.0, mry = 0.0;
+#pragma unroll
+  for (int c = 0; c < QP; ++c) {
+    const float2 vc = myv[c];
+    mrx = fma(double(m[c].x), double(vc.x), mrx);
+    mrx = fma(-double(m[c].y), double(vc.y), mrx);
+    mry = fma(double(m[c].x), double(vc.y), mry);
+    mry = fma(double(m[c].y), double(vc.x), mry);
+  }
+  if (a.planes_lo != nullptr) {
+    cp_async_wait<0>();
+    __syncthreads();
+    if (p < Q) {
+      for (int c = 0; c < Q; ++c) {
+        float2 lv;
+        if (p <= c) {
+          lv = gs[(p * Q - p * (p - 1) / 2 + (c - p)) * VPB + vox];
+        } else {
+          const float2 t = gs[(c * Q - c * (c - 1) / 2 + (p - c)) * VPB + vox];
+          lv = make_float2(t.x, -t.y);
+        }
+        if (p == c) lv.y = 0.f;
+        const float2 vc = myv[c];
+        mrx += double(lv.x) * vc.x - double(lv.y) * vc.y;
+        mry += double(lv.x) * vc.y + double(lv.y) * vc.x;
+      }
+    }
+  }
+  const double mv = group_sum_d<QP>(double(vp.x) * mrx + double(vp.y) * mry, redd, vox, half);
   const float vn2 = group_sum<QP>(vp.x * vp.x + vp.y * vp.y, red, vox, half);
 
   if (a.recon != nullptr) {
@@ -272,9 +327,9 @@ __global__ void __launch_bounds__(256, (QP <= 32 ? 2 : 1)) power_kernel(PowerArg
     if (j0 + v < a.n) a.maps[i64(c) * a.n + j0 + v] = ms[c * VPB + v];
   }
   if (p == 0 && live) {
-    const float lam = mv * a.lam_scale;
+    const float lam = float(mv * double(a.lam_scale));
     if (a.lambda) a.lambda[j] = lam;
-    if (a.value) a.value[j] = a.alpha * vn2 + a.beta * mv;
+    if (a.value) a.value[j] = float(double(a.alpha) * vn2 + double(a.beta) * mv);
     if (a.mask) a.mask[j] = lam < a.mask_threshold ? 1 : 0;
   }
   __syncthreads();  // the staging buffer is the prefetch target two tiles on
@@ -286,7 +341,8 @@ void launch(sk_ctx* ctx, const PowerArgs& a) {
   using G = Group<QP>;
   const int h = a.q * (a.q + 1) / 2;
   const size_t tile = size_t(std::max(h, QP)) * G::kVPB * sizeof(float2);
-  const size_t smem = 2 * tile + size_t(G::kVPB) * G::kStride * sizeof(float2) + size_t(G::kVPB) * 2 * sizeof(float);
+  const size_t smem = 2 * tile + size_t(G::kVPB) * G::kStride * sizeof(float2) +
+                      size_t(G::kVPB) * 2 * (sizeof(double) + sizeof(float));
   SKB_CUDA(cudaFuncSetAttribute(power_kernel<QP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int per_sm = 0;
   SKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_kernel<QP>, G::kThreads, smem));

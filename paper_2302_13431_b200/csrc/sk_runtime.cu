@@ -256,35 +256,54 @@ float2* symdft_table(sk_ctx* ctx, int N, int H, i64 j0, int sign) {
   return d;
 }
 
-// G(x) lag expansion (spatial_gram.cpp:125-138): lag box [h][lb]^D -> planes
-// [h][grid].  Axes are transformed last to first; stages whose inner extent
-// is >= 32 use the symmetric-tap kernel, the innermost axis the generic one.
-void expand_lags(sk_ctx* ctx, const float2* lags, float2* planes, i64 h, int tau, const Dims& grid) {
+// FP64 (cos, sign*sin)(2 pi l (j - j0) / N) for j < N, l = 1..H ([j][l-1]).
+double2* symdft_table64(sk_ctx* ctx, int N, int H, i64 j0, int sign) {
+  const std::string key = "symcs64:" + std::to_string(N) + ":" + std::to_string(H) + ":" + std::to_string(j0) + ":" +
+                          std::to_string(sign);
+  auto it = ctx->matrices.mats.find(key);
+  if (it != ctx->matrices.mats.end()) return reinterpret_cast<double2*>(it->second);
+  std::vector<double2> h(size_t(N) * std::max(H, 1));
+  for (int j = 0; j < N; ++j)
+    for (int l = 1; l <= H; ++l) {
+      const std::complex<double> z = cis(+1, i64(l) * (j - j0), N);
+      h[size_t(j) * H + (l - 1)] = make_double2(z.real(), sign * z.imag());
+    }
+  double2* d = nullptr;
+  SKB_CUDA(cudaMalloc(&d, h.size() * sizeof(double2)));
+  SKB_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  ctx->matrices.mats[key] = reinterpret_cast<float2*>(d);
+  return d;
+}
+
+// G(x) lag expansion (spatial_gram.cpp:125-138): FP64 lag box [h][lb]^D ->
+// fp32 hi/lo planes [h][grid] (sk_expand.cu).  Axes are transformed last to
+// first; intermediates stay FP64.
+void expand_lags(sk_ctx* ctx, const double2* lags, float2* hi, float2* lo, i64 h, int tau, const Dims& grid) {
   const int nd = int(grid.size()), lb = 4 * tau + 1, H = 2 * tau;
   Dims cur(static_cast<size_t>(nd), lb);
-  const float2* src = lags;
+  const double2* src = lags;
   for (int a = nd - 1; a >= 0; --a) {
-    float2* dst;
-    if (a == 0) {
-      dst = planes;
-    } else {
+    double2* dst = nullptr;
+    if (a > 0) {
       Dims next = cur;
       next[size_t(a)] = grid[size_t(a)];
-      dst = ctx->arena.get<float2>(std::string("field:tmp") + (a % 2 ? ":a" : ":b"), h * numel(next));
+      dst = ctx->arena.get<double2>(std::string("field:tmp64") + (a % 2 ? ":a" : ":b"), h * numel(next));
     }
     i64 b = h, inner = 1;
     for (int k = 0; k < a; ++k) b *= cur[size_t(k)];
     for (int k = a + 1; k < nd; ++k) inner *= cur[size_t(k)];
     const int N = int(grid[size_t(a)]);
-    if (inner >= 32 && H <= 16) {
-      apply_axis_symdft(ctx, src, dst, symdft_table(ctx, N, H, center_index(N), -1), b, H, N, inner);
-    } else {
-      apply_axis(ctx, src, dst, dft_matrix(ctx, N, lb, 2 * tau, center_index(N), -1, 0.0), b, lb, N, inner);
-    }
+    expand_stage_f64(ctx, src, b, inner, H, N, symdft_table64(ctx, N, H, center_index(N), -1), dst,
+                     a == 0 ? hi : nullptr, a == 0 ? lo : nullptr);
     cur[size_t(a)] = grid[size_t(a)];
     src = dst;
   }
 }
+
+struct Planes {
+  float2* hi = nullptr;
+  float2* lo = nullptr;
+};
 
 // Cached device tables per (support, q).
 struct SupportTables {
@@ -781,7 +800,7 @@ Eig run_nullspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, int solv
 
 // ---------------------------------------------------------------- K3
 // Lag kernels from the signal subspace, expanded onto the grid as packed planes.
-float2* run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims& grid) {
+Planes run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims& grid) {
   const i64 n = e.n, k = e.k;
   const int lam = int(s.count);
   SupportTables& t = tables_for(ctx, s, q);
@@ -797,23 +816,27 @@ float2* run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims
   } else {
     SKB_CUDA(cudaMemsetAsync(ws, 0, size_t(n * n) * sizeof(double2), ctx->stream));
   }
-  float2* lags = ctx->arena.get<float2>("field:lags", i64(h) * t.nbox);
+  double2* lags = ctx->arena.get<double2>("field:lags64", i64(h) * t.nbox);
   fold_lags_f64(ctx, ws, n, h, lam, t.nbox, t.pairs, t.lag_ptr, t.lag_st, true, lags);
-  float2* planes = ctx->arena.get<float2>("field:planes", i64(h) * numel(grid));
-  expand_lags(ctx, lags, planes, h, s.tau, grid);
-  return planes;
+  Planes p;
+  p.hi = ctx->arena.get<float2>("field:planes", i64(h) * numel(grid));
+  p.lo = ctx->arena.get<float2>("field:planes_lo", i64(h) * numel(grid));
+  expand_lags(ctx, lags, p.hi, p.lo, h, s.tau, grid);
+  return p;
 }
 
 // Lag kernels from a caller-supplied W (gram_field_fast entry point).
-float2* run_field_from_w(sk_ctx* ctx, const float2* w, const Support& s, int q, const Dims& grid) {
+Planes run_field_from_w(sk_ctx* ctx, const float2* w, const Support& s, int q, const Dims& grid) {
   const i64 n = i64(q) * s.count;
   SupportTables& t = tables_for(ctx, s, q);
   const int h = q * (q + 1) / 2;
-  float2* lags = ctx->arena.get<float2>("field:lags", i64(h) * t.nbox);
+  double2* lags = ctx->arena.get<double2>("field:lags64", i64(h) * t.nbox);
   fold_lags_f32(ctx, w, n, h, int(s.count), t.nbox, t.pairs, t.lag_ptr, t.lag_st, lags);
-  float2* planes = ctx->arena.get<float2>("field:planes", i64(h) * numel(grid));
-  expand_lags(ctx, lags, planes, h, s.tau, grid);
-  return planes;
+  Planes p;
+  p.hi = ctx->arena.get<float2>("field:planes", i64(h) * numel(grid));
+  p.lo = ctx->arena.get<float2>("field:planes_lo", i64(h) * numel(grid));
+  expand_lags(ctx, lags, p.hi, p.lo, h, s.tau, grid);
+  return p;
 }
 
 // ---------------------------------------------------------------- K5 pieces
@@ -899,8 +922,9 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
                         cfg->certify != 0);
   SKB_CUDA(cudaEventRecord(ev[2], ctx->stream));
   // field
-  float2* planes = run_field(ctx, e, s, int(q), grid);
-  if (out.field) planes_to_field_full(ctx, planes, ngrid, int(q), out.field);
+  const Planes pl = run_field(ctx, e, s, int(q), grid);
+  float2* planes = pl.hi;
+  if (out.field) planes_to_field_full(ctx, pl.hi, pl.lo, ngrid, int(q), out.field);
   SKB_CUDA(cudaEventRecord(ev[3], ctx->stream));
   // post (part 1): apodised recon on the map grid, consumed by K4's epilogue
   float2* recon = run_recon(ctx, cdims, co, q, calib, grid, cfg->apod_width);
@@ -913,13 +937,14 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   if (out.raw_maps) {
     // raw (pre-normalisation) eigenvectors for parity dumps: run K4 without the epilogue first
     PowerArgs r{};
-    r.planes = planes; r.n = ngrid; r.q = int(q); r.iters = cfg->power_iters;
+    r.planes = planes; r.planes_lo = pl.lo; r.n = ngrid; r.q = int(q); r.iters = cfg->power_iters;
     r.alpha = 1.f; r.beta = -1.f / float(lam); r.lam_scale = 1.f / float(lam);
     r.maps = out.raw_maps; r.lambda = out.raw_lambda;
     power_iteration(ctx, r);
   }
   PowerArgs pa{};
   pa.planes = planes;
+  pa.planes_lo = pl.lo;
   pa.n = ngrid;
   pa.q = int(q);
   pa.iters = cfg->power_iters;
@@ -1129,9 +1154,9 @@ int sk_gram_field_fast(sk_ctx* ctx, int64_t q, const sk_c64* w, int shape, int t
     if (4 * tau + 1 > 29) fail(SK_ERR_UNSUPPORTED, "kernel radius > 7 is outside the B200 path");
     const i64 n = q * s.count, ng = numel(grid);
     const float2* d_w = device_in(ctx, reinterpret_cast<const float2*>(w), n * n, "in:w");
-    float2* planes = run_field_from_w(ctx, d_w, s, int(q), grid);
+    const Planes pl = run_field_from_w(ctx, d_w, s, int(q), grid);
     Out<float2> f(ctx, reinterpret_cast<float2*>(field), ng * q * q, "out:field");
-    planes_to_field_full(ctx, planes, ng, int(q), f.dev);
+    planes_to_field_full(ctx, pl.hi, pl.lo, ng, int(q), f.dev);
     f.finish(ctx);
     SKB_CUDA(cudaStreamSynchronize(ctx->stream));
   });

@@ -211,6 +211,9 @@ def _pipeline_check(K, O, calib, co, full, cfgk, ref, want_spectrum, name):
            stage_ms=res.stage_ms, total_ms=res.total_ms, solver=res.extra)
     assert lam_raw["normwise"] < PM.TOL_LAMBDA
     assert lam_fin["normwise"] < PM.TOL_LAMBDA
+    # per-voxel: every eigenvalue within 1e-4 relative (hi/lo G + FP64 Rayleigh quotient)
+    assert lam_raw["pointwise_max"] < PM.TOL_LAMBDA
+    assert lam_fin["pointwise_max"] < PM.TOL_LAMBDA
     assert nrmse < PM.TOL_MAPS
     assert mask_agree > 0.999
     # unit sum-of-squares inside the mask (test_maps.cpp:137-146)
@@ -298,7 +301,7 @@ def test_determinism_and_device_buffers(K):
     import torch
     from paper_2302_13431_b200 import phantom
     case = phantom.generate("C1")
-    ck = K.PipelineConfig(tau=3, power_iters=30, grid_pad=40)
+    ck = K.PipelineConfig(tau=3, power_iters=30, grid_pad=40, eig_solver=2)  # same solver on both paths
     a = K.estimate_maps(K.Calib(case.calib[0], case.center_offset), (256, 256), ck)
     b = K.estimate_maps(K.Calib(case.calib[0], case.center_offset), (256, 256), ck)
     assert np.array_equal(a.maps, b.maps) and np.array_equal(a.lambda_min_map, b.lambda_min_map)
