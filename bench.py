@@ -171,7 +171,9 @@ def reference_arm(args, spec, rank, world):
     from paper_2302_13431_b200 import phantom
     if rank != 0:
         return
-    case = phantom.generate(args.config, seed=args.seed)
+    # bounded sample: one full pipeline per step (one slice for multislice
+    # configs, voxels/s extrapolated); at most 2 steps so the arm ends in minutes
+    case = phantom.generate(args.config, seed=args.seed, slices=1 if spec.slices > 1 else None)
     steps = max(1, min(args.steps, 2))
     warm = min(args.warmup, 0)
     for _ in range(warm):
@@ -182,7 +184,7 @@ def reference_arm(args, spec, rank, world):
         dt, _, threads = oracle_run(case)
         times.append(dt)
     t = float(np.mean(times))
-    vox = output_voxels(spec)
+    vox = output_voxels(spec) // spec.slices
     value = vox / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
@@ -217,7 +219,15 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    case = phantom.generate(args.config, seed=args.seed + rank)
+    from paper_2302_13431_b200 import shard
+    sharded = spec.slices > 1
+    if sharded:
+        # multislice: contiguous slice blocks per rank, strong scaling
+        block = shard.partition(spec.slices, world, rank)
+        case = phantom.generate(args.config, seed=args.seed, slice_range=block)
+    else:
+        # single slice: independent replicas, weak scaling
+        case = phantom.generate(args.config, seed=args.seed + rank)
     q = spec.channels
     full = spec.full_dims
     nfull = int(np.prod(full))
@@ -238,6 +248,10 @@ def main():
     cal_stride = d_cal[0].numel() * 8
 
     def step_device():
+        if sharded:  # all local slices in one call (concurrent lanes inside the library)
+            return K.api.estimate_maps_batched_device(ctx, d_cal.data_ptr(), slices, spec.calib, case.center_offset,
+                                                      q, full, cfg, d_maps.data_ptr(), d_lam.data_ptr(),
+                                                      d_mask.data_ptr())
         provs = []
         for s in range(slices):
             provs.append(K.api.estimate_maps_device(
@@ -284,43 +298,51 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    vox = output_voxels(spec) * world
+    # all ranks' output voxels: sharded -> the whole volume once; replicas -> one volume per rank
+    vox = output_voxels(spec) if sharded else output_voxels(spec) * world
     value = vox / (ms_per_step / 1e3)
 
-    # ---- e2e through the public API with pinned host buffers
+    # ---- e2e through the public API with pinned host buffers (one slice-sized
+    # output buffer reused per slice; every slice's result is read back)
     h_cal = torch.from_numpy(case.calib).pin_memory()
-    h_maps = torch.empty((slices, q) + tuple(full), dtype=torch.complex64).pin_memory()
-    h_lam = torch.empty((slices,) + tuple(full), dtype=torch.float32).pin_memory()
-    h_mask = torch.empty((slices,) + tuple(full), dtype=torch.uint8).pin_memory()
+    hs = slices if sharded else 1
+    h_maps = torch.empty((hs, q) + tuple(full), dtype=torch.complex64).pin_memory()
+    h_lam = torch.empty((hs,) + tuple(full), dtype=torch.float32).pin_memory()
+    h_mask = torch.empty((hs,) + tuple(full), dtype=torch.uint8).pin_memory()
 
     def step_host():
+        if sharded:
+            return K.api.estimate_maps_batched_device(ctx, h_cal.data_ptr(), slices, spec.calib, case.center_offset,
+                                                      q, full, cfg, h_maps.data_ptr(), h_lam.data_ptr(),
+                                                      h_mask.data_ptr())
         provs = []
         for s in range(slices):
             provs.append(K.api.estimate_maps_device(
                 ctx, h_cal.data_ptr() + s * cal_stride, spec.calib, case.center_offset, q, full, cfg,
-                h_maps[s].data_ptr(), h_lam[s].data_ptr(), h_mask[s].data_ptr()))
+                h_maps.data_ptr(), h_lam.data_ptr(), h_mask.data_ptr()))
         return provs
 
     step_host()
-    e2e_steps = max(3, min(args.steps, 10))
+    e2e_steps = max(3, min(args.steps, 10)) if not sharded else max(1, min(args.steps, 3))
     e2e_ms, _ = timed(step_host, e2e_steps)
     if dist:
         t = torch.tensor([e2e_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_value = vox / (e2e_ms / e2e_steps / 1e3)
-    assert np.array_equal(h_mask.numpy(), d_mask.cpu().numpy()), "host/device legs disagree"
+    assert np.array_equal(h_mask[hs - 1].numpy(), d_mask[slices - 1].cpu().numpy()), "host/device legs disagree"
 
     peaks, peak_src = load_peaks()
     props = torch.cuda.get_device_properties(local)
     fp32_peak = props.multi_processor_count * 128 * 2 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
     k4_ms = stages[3]
-    achieved = k4_flops(spec) / (k4_ms / 1e3) / 1e12 if k4_ms > 0 else 0.0
+    k4_work = k4_flops(spec) * slices
+    achieved = k4_work / (k4_ms / 1e3) / 1e12 if k4_ms > 0 else 0.0
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("power_kernel", {}).get("dram_bytes_per_launch")
+            traffic = json.load(open(prof)).get("power_kernel", {}).get(args.config, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -330,6 +352,7 @@ def main():
     hbm_peak = peaks.get("hbm_gbs", 6552.6)
     stage_roof = {}
     for name, (bound, work) in stage_work(spec, lam_box, sup).items():
+        work = work * slices
         ms = float(dict(zip(("gram", "nullspace", "field", "eigensolve", "post"), stages))[name])
         if ms <= 0:
             continue
@@ -346,11 +369,15 @@ def main():
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "c64 (fp32 complex); Gram eigensolve fp64",
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None,
+        "dtype": "c64 (fp32 complex); Gram eigensolve, lag expansion and final Rayleigh quotient fp64",
         "data": "synthetic (seeded phantom/coil generator, paper_2302_13431_b200/phantom.py)",
-        "config": {"workload": workload(spec), "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "l2": "flushed between steps (256 MiB write, untimed)", "output_voxels_per_rank": output_voxels(spec)},
+        "config": {"workload": workload(spec),
+                   "parallelism": (f"slice-sharded x{world}" if sharded else f"replicas x{world}") if world > 1
+                   else "single GPU",
+                   "l2": "flushed between steps (256 MiB write, untimed)",
+                   "output_voxels_per_rank": output_voxels(spec) // spec.slices * slices},
         "stages_ms": dict(zip(("gram", "nullspace", "field", "eigensolve", "post"), [round(x, 4) for x in stages])),
         "stages_roofline": stage_roof,
         "roofline": {"kernel": "power_kernel (K4)", "bound": "fp32", "achieved": achieved, "peak": fp32_peak,
@@ -358,15 +385,18 @@ def main():
                      "peak_source": f"SMs x 128 FP32 lanes x 2 x sm_max_mhz ({peak_src} MEASURED_PEAKS sm_max_mhz)",
                      "flops_per_launch": k4_flops(spec)},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h_cal.numel() * 8),
-                "d2h_bytes_per_step": int(h_maps.numel() * 8 + h_lam.numel() * 4 + h_mask.numel())},
+                "d2h_bytes_per_step": int((h_maps.numel() * 8 + h_lam.numel() * 4 + h_mask.numel()) * slices // hs)},
         "gpu_launches": int(launches), "library_calls": int(libcalls),
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        dt, _, threads = oracle_run(case)
-        line["cpu_baseline"] = {"value": output_voxels(spec) / dt, "unit": UNIT, "cores": threads, "kind": "port",
-                                "sample": f"one full {args.config} pipeline ({output_voxels(spec)} voxels, {dt:.1f} s); "
-                                          "LAPACK single-threaded as the reference's Eigen"}
+        one = phantom.Case(spec, case.calib[:1], case.center_offset) if sharded else case
+        dt, _, threads = oracle_run(one)
+        per = output_voxels(spec) // spec.slices
+        line["cpu_baseline"] = {"value": per / dt, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": (f"one full {args.config} slice pipeline ({per} voxels, {dt:.1f} s)"
+                                           + (f"; voxels/s extrapolated to {spec.slices} slices" if sharded else "")
+                                           + "; LAPACK single-threaded as the reference's Eigen")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

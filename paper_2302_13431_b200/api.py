@@ -457,6 +457,18 @@ def estimate_maps_device(ctx: Context, calib_ptr: int, calib_dims, center_offset
     return prov
 
 
+def estimate_maps_batched_device(ctx: Context, calib_ptr: int, slices: int, calib_dims, center_offset, q: int,
+                                 full_dims, cfg: PipelineConfig, maps_ptr: int, lambda_ptr: int, mask_ptr: int):
+    """Multislice on device (or pinned host) buffers, slice-major; returns per-slice provenance."""
+    prov = (sk_provenance * max(int(slices), 1))()
+    cfgc = cfg.to_c()
+    _check(lib().sk_estimate_maps_batched(ctx.handle, int(slices), len(calib_dims), _p(_i64(calib_dims)),
+                                          _p(_i64(center_offset)), q, C.c_void_p(calib_ptr), _p(_i64(full_dims)),
+                                          C.byref(cfgc), C.c_void_p(maps_ptr), C.c_void_p(lambda_ptr),
+                                          C.c_void_p(mask_ptr), C.cast(prov, C.c_void_p)))
+    return list(prov)[: int(slices)]
+
+
 def estimate_maps_batched(calibs: np.ndarray, center_offset, full_dims, cfg: PipelineConfig,
                           ctx: Context | None = None):
     """Multislice: calibs (S, Q, *E) -> maps (S, Q, *full), lambda (S, *full), mask (S, *full)."""

@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <thread>
 
 #include "../../include/senskit_b200.h"
 #include "sk_internal.h"
@@ -559,12 +560,12 @@ void small_heev(sk_ctx* ctx, double2* H, i64 b, double* w, int* d_info) {
                                           dwork, dbytes, hwork.data(), hbytes, d_info, 1),
                    "XsyevBatched");
   } else if (jacobi) {
-    static syevjInfo_t params = nullptr;
-    if (!params) {
-      check_cusolver(cusolverDnCreateSyevjInfo(&params), "CreateSyevjInfo");
-      check_cusolver(cusolverDnXsyevjSetTolerance(params, 1e-14), "syevjSetTolerance");
-      check_cusolver(cusolverDnXsyevjSetMaxSweeps(params, 30), "syevjSetMaxSweeps");
+    if (!ctx->syevj) {
+      check_cusolver(cusolverDnCreateSyevjInfo(&ctx->syevj), "CreateSyevjInfo");
+      check_cusolver(cusolverDnXsyevjSetTolerance(ctx->syevj, 1e-14), "syevjSetTolerance");
+      check_cusolver(cusolverDnXsyevjSetMaxSweeps(ctx->syevj, 30), "syevjSetMaxSweeps");
     }
+    syevjInfo_t params = ctx->syevj;
     int lwork = 0;
     check_cusolver(cusolverDnZheevj_bufferSize(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
                                                int(b), reinterpret_cast<cuDoubleComplex*>(H), int(b), w, &lwork,
@@ -644,10 +645,10 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   c64_to_c128(ctx, gram, A, n * n);
   // Per-size hints from the previous call: block size and the number of
   // orthogonalised iterations before the (single) Rayleigh-Ritz check.
-  static std::map<std::pair<sk_ctx*, i64>, std::pair<i64, int>> hint;
+  auto& hint = ctx->subspace_hint;
   i64 b = 96;
   int q_plan = 3;
-  auto it_h = hint.find({ctx, n});
+  auto it_h = hint.find(n);
   if (it_h != hint.end()) {
     b = std::max<i64>(64, ((it_h->second.first + 40 + 31) / 32) * 32);
     q_plan = it_h->second.second;
@@ -781,7 +782,7 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   e.margin = margin;
   e.iterations = iters;
   e.block = int(b);
-  hint[{ctx, n}] = {m, std::max(1, iters - 1)};
+  hint[n] = {m, std::max(1, iters - 1)};
   return true;
 }
 
@@ -1053,8 +1054,11 @@ int sk_create(int device, sk_ctx** out) {
 int sk_destroy(sk_ctx* ctx) {
   return guarded([&] {
     if (!ctx) return;
+    for (sk_ctx* sub : ctx->lanes) sk_destroy(sub);
+    ctx->lanes.clear();
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    if (ctx->syevj) cusolverDnDestroySyevjInfo(ctx->syevj);
     ctx->arena.release_all();
     for (auto& e : ctx->ev) cudaEventDestroy(e);
     cusolverDnDestroyParams(ctx->cusolver_params);
@@ -1345,14 +1349,57 @@ int sk_estimate_maps(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int
 int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_t* calib_dims,
                              const int64_t* center_offset, int64_t q, const sk_c64* calib, const int64_t* full_dims,
                              const sk_config* cfg, sk_c64* maps, float* lambda, uint8_t* mask, sk_provenance* prov) {
+  if (!ctx || slices < 0 || ndim < 1) {
+    g_last_error = "bad arguments";
+    return SK_ERR_DIM;
+  }
   const Dims cd = dims_of(ndim, calib_dims), fd = dims_of(ndim, full_dims);
   const i64 ncal = q * numel(cd), nfull = numel(fd);
-  for (i64 s = 0; s < slices; ++s) {
-    const int rc = sk_estimate_maps(ctx, ndim, calib_dims, center_offset, q, calib + s * ncal, full_dims, cfg,
-                                    maps ? maps + s * q * nfull : nullptr, lambda ? lambda + s * nfull : nullptr,
-                                    mask ? mask + s * nfull : nullptr, nullptr, prov ? prov + s : nullptr);
-    if (rc != SK_OK) return rc;
+  // Slices are independent pipelines whose small dense stages are latency
+  // bound: run them on `lanes` sub-contexts (own stream, cuBLAS/cuSOLVER
+  // handles and workspace) driven by host threads, so the GPU overlaps them.
+  int lanes = 8;
+  if (const char* v = std::getenv("SKB_LANES")) lanes = std::max(1, std::atoi(v));
+  lanes = int(std::min<i64>(lanes, std::max<i64>(slices, 1)));
+  int rc0 = guarded([&] {
+    require_ctx(ctx);
+    while (int(ctx->lanes.size()) < lanes) {
+      sk_ctx* sub = nullptr;
+      const int rc = sk_create(ctx->device, &sub);
+      if (rc != SK_OK) fail(rc, g_last_error);
+      ctx->lanes.push_back(sub);
+    }
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));  // inputs written on the caller's stream are visible
+  });
+  if (rc0 != SK_OK) return rc0;
+  std::vector<int> rcs(size_t(lanes), SK_OK);
+  std::vector<std::string> errs(static_cast<size_t>(lanes));
+  auto work = [&](int lane) {
+    sk_ctx* sub = lanes == 1 ? ctx : ctx->lanes[size_t(lane)];
+    cudaSetDevice(ctx->device);
+    for (i64 s = lane; s < slices; s += lanes) {
+      const int rc = sk_estimate_maps(sub, ndim, calib_dims, center_offset, q, calib + s * ncal, full_dims, cfg,
+                                      maps ? maps + s * q * nfull : nullptr, lambda ? lambda + s * nfull : nullptr,
+                                      mask ? mask + s * nfull : nullptr, nullptr, prov ? prov + s : nullptr);
+      if (rc != SK_OK) {
+        rcs[size_t(lane)] = rc;
+        errs[size_t(lane)] = sk_last_error();
+        return;
+      }
+    }
+  };
+  if (lanes == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int l = 0; l < lanes; ++l) pool.emplace_back(work, l);
+    for (auto& t : pool) t.join();
   }
+  for (int l = 0; l < lanes; ++l)
+    if (rcs[size_t(l)] != SK_OK) {
+      g_last_error = errs[size_t(l)];
+      return rcs[size_t(l)];
+    }
   return SK_OK;
 }
 

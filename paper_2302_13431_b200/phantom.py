@@ -180,17 +180,24 @@ class Case:
 
 
 def generate(name: str, seed: int = 1234, with_kspace: bool = False, slices: int | None = None,
-             full_dims=None, channels: int | None = None) -> Case:
-    """Seeded case for config `name` (C1..C5).  `slices` limits C3's slice count."""
+             full_dims=None, channels: int | None = None, slice_range=None) -> Case:
+    """Seeded case for config `name` (C1..C5).
+
+    `slices` limits C3's slice count (first `slices` slices); `slice_range`
+    = (start, stop) generates only that block.  Every slice has its own RNG
+    stream (seed, slice index), so a shard's data does not depend on how the
+    slices are partitioned across ranks.
+    """
     spec = CONFIGS[name]
     if full_dims is not None or channels is not None:
         spec = ConfigSpec(**{**spec.__dict__, **({"full_dims": tuple(full_dims)} if full_dims else {}),
                              **({"channels": channels} if channels else {})})
     dims = spec.full_dims
     ns = spec.slices if slices is None else slices
-    rng = np.random.Generator(np.random.PCG64(seed))
+    start, stop = slice_range if slice_range is not None else (0, ns)
     calibs, kss, tms = [], [], []
-    for s in range(ns):
+    for s in range(start, stop):
+        rng = np.random.Generator(np.random.PCG64([seed, s]))
         z = (s - spec.slices // 2) / spec.slices if spec.slices > 1 else 0.0
         maps = coil_maps(spec, dims, z_slice=z)
         rho = phantom(dims, rng)
