@@ -168,6 +168,13 @@ void renormalize_and_mask(sk_ctx* ctx, float2* maps, i64 n, int q, const float2*
                           uint8_t* mask, float thr);
 void mask_kernel(sk_ctx* ctx, const float* lambda, i64 n, float thr, uint8_t* mask);
 void real_to_c64(sk_ctx* ctx, const float* in, float2* out, i64 n);
+void real_to_c128(sk_ctx* ctx, const float* in, double2* out, i64 n);
+void lam64_to_f32_mask(sk_ctx* ctx, const double2* lam_c, i64 n, float* lam, uint8_t* mask, float thr);
+// Periodic-sinc interpolation along one axis by shared-memory radix-2 FFTs
+// (sk_interp.cu): in [batch][n][inner] -> out [batch][N][inner], float2 or
+// double2 elements.  Returns false (nothing launched) unless n, N are powers
+// of two with 2 <= n <= N <= 1024.
+bool interp_axis_fft(sk_ctx* ctx, const void* in, void* out, i64 batch, int n, int N, i64 inner, bool fp64);
 void copy_strided(sk_ctx* ctx, const float2* src, i64 src_rs, i64 src_cs, float2* dst, i64 dst_rs, i64 dst_cs, i64 rows,
                   i64 cols);
 void normalize_standalone(sk_ctx* ctx, float2* maps, i64 n, int q, const float2* recon, unsigned long long* zeroed);

@@ -106,6 +106,20 @@ __global__ void mask_only_kernel(const float* __restrict__ lam, i64 n, float thr
     mask[j] = lam[j] < thr ? 1 : 0;
 }
 
+__global__ void real_to_c128_kernel(const float* __restrict__ in, double2* __restrict__ out, i64 n) {
+  for (i64 j = i64(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += i64(gridDim.x) * blockDim.x)
+    out[j] = make_double2(double(in[j]), 0.0);
+}
+
+__global__ void lam64_mask_kernel(const double2* __restrict__ lam_c, i64 n, float* __restrict__ lam,
+                                  uint8_t* __restrict__ mask, float thr) {
+  for (i64 j = i64(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += i64(gridDim.x) * blockDim.x) {
+    const double l = lam_c[j].x;  // interpolate_real keeps the real part (maps.cpp:92-99)
+    if (lam) lam[j] = float(l);
+    if (mask) mask[j] = l < double(thr) ? 1 : 0;
+  }
+}
+
 __global__ void real_to_c64_kernel(const float* __restrict__ in, float2* __restrict__ out, i64 n) {
   for (i64 j = i64(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += i64(gridDim.x) * blockDim.x)
     out[j] = make_float2(in[j], 0.f);
@@ -271,6 +285,16 @@ void mask_kernel(sk_ctx* ctx, const float* lambda, i64 n, float thr, uint8_t* ma
   mask_only_kernel<<<SKB_GRID(n)>>>(lambda, n, thr, mask);
   ++ctx->launches;
   SKB_LAUNCH("mask");
+}
+void real_to_c128(sk_ctx* ctx, const float* in, double2* out, i64 n) {
+  real_to_c128_kernel<<<SKB_GRID(n)>>>(in, out, n);
+  ++ctx->launches;
+  SKB_LAUNCH("real_to_c128");
+}
+void lam64_to_f32_mask(sk_ctx* ctx, const double2* lam_c, i64 n, float* lam, uint8_t* mask, float thr) {
+  lam64_mask_kernel<<<SKB_GRID(n)>>>(lam_c, n, lam, mask, thr);
+  ++ctx->launches;
+  SKB_LAUNCH("lam64_mask");
 }
 void real_to_c64(sk_ctx* ctx, const float* in, float2* out, i64 n) {
   real_to_c64_kernel<<<SKB_GRID(n)>>>(in, out, n);

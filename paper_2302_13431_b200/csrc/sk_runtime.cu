@@ -855,11 +855,72 @@ float2* run_recon(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const f
   return recon;
 }
 
+// Interpolation, one axis at a time (last first): radix-2 FFT kernel for
+// power-of-two extents (sk_interp.cu), the exact per-axis sinc matrix
+// otherwise.  fp64 selects double2 elements (FFT path only).
+bool interp_fft_ok(const Dims& low, const Dims& full) {
+  for (size_t a = 0; a < low.size(); ++a) {
+    const i64 n = low[a], N = full[a];
+    if (n < 2 || N > 1024 || (n & (n - 1)) || (N & (N - 1)) || n > N) return false;
+  }
+  return true;
+}
+
 void run_interp(sk_ctx* ctx, const float2* low, float2* out, i64 batch, const Dims& low_dims, const Dims& full) {
   const int nd = int(low_dims.size());
+  if (interp_fft_ok(low_dims, full)) {
+    Dims cur = low_dims;
+    const float2* src = low;
+    for (int a = nd - 1; a >= 0; --a) {
+      float2* dst = out;
+      if (a > 0) {
+        Dims next = cur;
+        next[size_t(a)] = full[size_t(a)];
+        dst = ctx->arena.get<float2>(std::string("interp:fft") + (a % 2 ? ":a" : ":b"), batch * numel(next));
+      }
+      i64 b = batch, inner = 1;
+      for (int k = 0; k < a; ++k) b *= cur[size_t(k)];
+      for (int k = a + 1; k < nd; ++k) inner *= cur[size_t(k)];
+      interp_axis_fft(ctx, src, dst, b, int(low_dims[size_t(a)]), int(full[size_t(a)]), inner, false);
+      cur[size_t(a)] = full[size_t(a)];
+      src = dst;
+    }
+    return;
+  }
   std::vector<float2*> mats(static_cast<size_t>(nd));
   for (int a = 0; a < nd; ++a) mats[size_t(a)] = sinc_matrix(ctx, int(full[size_t(a)]), int(low_dims[size_t(a)]));
   separable(ctx, low, out, batch, low_dims, full, mats, "interp:tmp");
+}
+
+// interpolate_real (maps.cpp:92-99) + support mask (maps.cpp:47-52): FP64
+// FFT path for power-of-two extents, the FP32 sinc-matrix path otherwise.
+void run_interp_lambda(sk_ctx* ctx, const float* low, const Dims& low_dims, const Dims& full, float* lam_out,
+                       uint8_t* mask, float thr) {
+  const int nd = int(low_dims.size());
+  const i64 nlow = numel(low_dims), nfull = numel(full);
+  if (interp_fft_ok(low_dims, full)) {
+    double2* src = ctx->arena.get<double2>("interp:lam64", nlow);
+    real_to_c128(ctx, low, src, nlow);
+    Dims cur = low_dims;
+    for (int a = nd - 1; a >= 0; --a) {
+      Dims next = cur;
+      next[size_t(a)] = full[size_t(a)];
+      double2* dst = ctx->arena.get<double2>(std::string("interp:lam64") + (a % 2 ? ":a" : ":b"), numel(next));
+      i64 b = 1, inner = 1;
+      for (int k = 0; k < a; ++k) b *= cur[size_t(k)];
+      for (int k = a + 1; k < nd; ++k) inner *= cur[size_t(k)];
+      interp_axis_fft(ctx, src, dst, b, int(low_dims[size_t(a)]), int(full[size_t(a)]), inner, true);
+      cur = next;
+      src = dst;
+    }
+    lam64_to_f32_mask(ctx, src, nfull, lam_out, mask, thr);
+    return;
+  }
+  float2* lam_c = ctx->arena.get<float2>("post:lam_c", nlow);
+  real_to_c64(ctx, low, lam_c, nlow);
+  float2* lam_full_c = ctx->arena.get<float2>("post:lam_full_c", nfull);
+  run_interp(ctx, lam_c, lam_full_c, 1, low_dims, full);
+  renormalize_and_mask(ctx, nullptr, nfull, 0, lam_full_c, lam_out, mask, thr);
 }
 
 // ---------------------------------------------------------------- pipeline
@@ -964,11 +1025,8 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   if (interp) {
     float2* maps_full = out.maps ? out.maps : ctx->arena.get<float2>("post:maps_full", q * nfull);
     run_interp(ctx, maps_grid, maps_full, q, grid, full);
-    float2* lam_c = ctx->arena.get<float2>("post:lam_c", ngrid);
-    real_to_c64(ctx, lam_grid, lam_c, ngrid);
-    float2* lam_full_c = ctx->arena.get<float2>("post:lam_full_c", nfull);
-    run_interp(ctx, lam_c, lam_full_c, 1, grid, full);
-    renormalize_and_mask(ctx, maps_full, nfull, int(q), lam_full_c, out.lambda, out.mask, float(cfg->mask_threshold));
+    run_interp_lambda(ctx, lam_grid, grid, full, out.lambda, out.mask, float(cfg->mask_threshold));
+    renormalize_and_mask(ctx, maps_full, nfull, int(q), nullptr, nullptr, nullptr, 0.f);
   }
   SKB_CUDA(cudaEventRecord(ev[6], ctx->stream));
   unsigned long long h_zeroed = 0;
@@ -1262,12 +1320,8 @@ int sk_interpolate_real(sk_ctx* ctx, int ndim, const int64_t* low_dims, const fl
       if (fd[size_t(a)] < ld[size_t(a)])
         fail(SK_ERR_DIM, "interpolation target smaller than source on axis " + std::to_string(a));
     const float* d_low = device_in(ctx, low, numel(ld), "in:lowr");
-    float2* lc = ctx->arena.get<float2>("interp:lc", numel(ld));
-    real_to_c64(ctx, d_low, lc, numel(ld));
-    float2* fc = ctx->arena.get<float2>("interp:fc", numel(fd));
-    run_interp(ctx, lc, fc, 1, ld, fd);
     Out<float> o(ctx, out, numel(fd), "out:interpr");
-    renormalize_and_mask(ctx, nullptr, numel(fd), 0, fc, o.dev, nullptr, 0.f);
+    run_interp_lambda(ctx, d_low, ld, fd, o.dev, nullptr, 0.f);
     o.finish(ctx);
     SKB_CUDA(cudaStreamSynchronize(ctx->stream));
   });
