@@ -187,5 +187,8 @@ void shift_negate(sk_ctx* ctx, const double2* a, double2* m, i64 n, double shift
 void cross_gram(sk_ctx* ctx, const double2* x, const double2* y, i64 n, int b, double2* out);
 void chol_inv(sk_ctx* ctx, const double2* s, int b, double2* minv, int* flag);
 void cholesky_small(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag);
+// One CholQR pass on X (n x b, b <= 118): cross_gram + one-CTA lazy Cholesky +
+// warp-per-row triangular solve; no host synchronisation (flag raised on failure).
+void cholqr_fast(sk_ctx* ctx, double2* x, i64 n, int b, double2* s, double2* l, int* flag);
 
 }  // namespace skb

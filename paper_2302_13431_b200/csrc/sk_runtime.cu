@@ -598,17 +598,27 @@ void small_heev(sk_ctx* ctx, double2* H, i64 b, double* w, int* d_info) {
 // (synchronous path) failure; the fast path raises `flag` instead.
 bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int passes = 2) {
   (void)tmp;
-  static const bool lib_chol = [] {
+  // default: cuSOLVER POTRF + cuBLAS TRSM (measured fastest at b = 64..96);
+  // SKB_SMALL_CHOL=fast selects the own lazy Cholesky + row TRSM (b <= 112),
+  // =custom the own blocked Cholesky + cuBLAS TRSM.
+  static const int chol_mode = [] {
     const char* v = std::getenv("SKB_SMALL_CHOL");
-    return !(v && std::string(v) == "custom");  // default: cuSOLVER POTRF (no host sync)
+    if (v && std::string(v) == "fast") return 0;
+    if (v && std::string(v) == "custom") return 2;
+    return 1;
   }();
-  if (b > 256 || (!lib_chol && b > kSmallBlockMax)) {
+  const bool lib_chol = chol_mode == 1 || b > kSmallBlockMax;
+  if (b > 256 || (chol_mode == 2 && b > kSmallBlockMax)) {
     for (int p = 0; p < passes; ++p)
       if (!cholqr(ctx, x, n, b)) return false;
     return true;
   }
   double2* S = ctx->arena.get<double2>("ss:S", b * b);
   double2* L = ctx->arena.get<double2>("ss:L", b * b);
+  if (chol_mode == 0 && b <= kSmallBlockMax) {
+    for (int pass = 0; pass < passes; ++pass) cholqr_fast(ctx, x, n, int(b), S, L, flag);
+    return true;
+  }
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
   for (int pass = 0; pass < passes; ++pass) {
     cross_gram(ctx, x, x, n, int(b), S);        // S = X^H X
@@ -646,12 +656,23 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   // Per-size hints from the previous call: block size and the number of
   // orthogonalised iterations before the (single) Rayleigh-Ritz check.
   auto& hint = ctx->subspace_hint;
-  i64 b = 96;
+  // Block size: small-matrix latency dominates up to n ~ 4k (b = 64 measured
+  // best for C2/C3/C4), the n^2 b GEMM beyond (b = 128 best for C5).
+  const bool big = n > 4096;
+  i64 b = big ? 128 : 64;
   int q_plan = 3;
   auto it_h = hint.find(n);
   if (it_h != hint.end()) {
-    b = std::max<i64>(64, ((it_h->second.first + 40 + 31) / 32) * 32);
+    const i64 k_prev = it_h->second.first;
+    b = big ? std::max<i64>(128, ((k_prev + 48 + 31) / 32) * 32) : std::max<i64>(64, ((k_prev + 16 + 15) / 16) * 16);
     q_plan = it_h->second.second;
+  }
+  if (const char* v = std::getenv("SKB_BLOCK")) {  // experiment override
+    const i64 fixed = std::atoll(v);
+    if (fixed > 0) {
+      if (it_h == hint.end() || it_h->second.first + 8 > fixed) q_plan = 3;
+      b = fixed;
+    }
   }
   b = std::min(b, n);
   const i64 bcap = std::min(n, std::max<i64>(4 * b, 256));
@@ -676,7 +697,24 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   double theta_max = 0.0, c = 0.0;
   while (iters < maxit) {
     for (int i = 0; i < q_plan; ++i, ++iters) {
-      zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);  // Y = A V
+      if (i + 2 < q_plan) {
+        // Early iterations only steer the span: FP32 CGEMM on the fp32 Gram
+        // (its rounding ~1e-7 is removed by the FP64 iterations that follow);
+        // orthonormalisation stays FP64 (kappa(A V)^2 exceeds 1/eps_fp32).
+        float2* V32 = ctx->arena.get<float2>("ss:V32", n * bcap);
+        float2* Y32 = ctx->arena.get<float2>("ss:Y32", n * bcap);
+        c128_to_c64(ctx, V, V32, n * b);
+        const cuComplex one = make_cuComplex(1.f, 0.f), zero = make_cuComplex(0.f, 0.f);
+        check_cublas(cublasCgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(n), int(b), int(n), &one,
+                                 reinterpret_cast<const cuComplex*>(gram), int(n),
+                                 reinterpret_cast<const cuComplex*>(V32), int(n), &zero,
+                                 reinterpret_cast<cuComplex*>(Y32), int(n)),
+                     "Cgemm(subspace)");
+        ++ctx->lib_calls;
+        c64_to_c128(ctx, Y32, Y, n * b);
+      } else {
+        zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);  // Y = A V
+      }
       std::swap(V, Y);
       // Only the span matters between Rayleigh-Ritz steps: one CholQR pass
       // (orthogonality ~ kappa^2 eps) except before the projection.

@@ -242,7 +242,126 @@ __global__ void __launch_bounds__(1024) chol_kernel(const double2* __restrict__ 
   }
 }
 
+// One CTA, 128 threads, one barrier per step: "lazy" right-looking Cholesky
+// of the b x b Hermitian S (b <= 118) held in shared memory.  Column j is
+// left unscaled during the sweep (updates use A_ij conj(A_kj) / d_j); the
+// final pass writes L (column-major, leading dimension b, zero upper part).
+__global__ void __launch_bounds__(128) chol_lazy_kernel(const double2* __restrict__ s, int b,
+                                                        double2* __restrict__ l, int* __restrict__ flag) {
+  extern __shared__ double2 sm[];
+  const int ld = b + 1;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < b * b; e += blockDim.x) {
+    const int k = e / b, i = e % b;
+    sm[i * ld + k] = s[e];
+  }
+  for (int j = 0; j < b; ++j) {
+    __syncthreads();
+    double d = sm[j * ld + j].x;
+    if (!(d > 0.0)) {
+      if (tid == 0) {
+        atomicOr(flag, 1);
+        sm[j * ld + j].x = 1.0;
+      }
+      d = 1.0;
+    }
+    const double inv_d = 1.0 / d;
+    // trailing update, two threads per row (even/odd columns)
+    for (int r = tid >> 1; j + 1 + r < b; r += (blockDim.x >> 1)) {
+      const int i = j + 1 + r;
+      const double2 aij = sm[i * ld + j];
+      const double2 sij = make_double2(aij.x * inv_d, aij.y * inv_d);
+      for (int k = j + 1 + (tid & 1); k <= i; k += 2) {
+        const double2 akj = sm[k * ld + j];
+        double2 a = sm[i * ld + k];
+        a.x -= sij.x * akj.x + sij.y * akj.y;  // a -= (A_ij / d) conj(A_kj)
+        a.y -= sij.y * akj.x - sij.x * akj.y;
+        sm[i * ld + k] = a;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < b * b; e += blockDim.x) {
+    const int k = e / b, i = e % b;
+    double2 v = make_double2(0.0, 0.0);
+    if (i >= k) {
+      const double p = sqrt(sm[k * ld + k].x);
+      v = sm[i * ld + k];
+      if (i == k) {
+        v = make_double2(p, 0.0);
+      } else {
+        v.x /= p;
+        v.y /= p;
+      }
+    }
+    l[e] = v;
+  }
+}
+
+// V = X L^{-H} row by row (X, V: n x b column-major; L lower, column-major):
+// v_c = (x_c - sum_{t<c} v_t conj(L_ct)) / L_cc.  A warp owns a row; lanes
+// hold v_t for t = lane + 32u; L is staged once per CTA in shared memory.
+__global__ void __launch_bounds__(256) trsm_rows_kernel(double2* __restrict__ x, i64 n, int b,
+                                                        const double2* __restrict__ l) {
+  extern __shared__ double2 sl[];  // L row-major [c][t], ld = b
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) {
+    const int t = e / b, c = e % b;  // coalesced read of column-major L(c, t)
+    sl[c * b + t] = l[e];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  constexpr int kU = 4;  // b <= 128
+  for (i64 r = i64(blockIdx.x) * nw + warp; r < n; r += i64(gridDim.x) * nw) {
+    double2 v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) v[u] = make_double2(0.0, 0.0);
+    for (int c = 0; c < b; ++c) {
+      double sx = 0.0, sy = 0.0;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int t = lane + 32 * u;
+        if (t < c) {
+          const double2 lct = sl[c * b + t];
+          sx += v[u].x * lct.x + v[u].y * lct.y;  // v_t * conj(L_ct)
+          sy += v[u].y * lct.x - v[u].x * lct.y;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o);
+      }
+      if (lane == (c & 31)) {
+        const double2 xc = x[r + i64(c) * n];
+        const double inv = 1.0 / sl[c * b + c].x;
+        v[c >> 5] = make_double2((xc.x - sx) * inv, (xc.y - sy) * inv);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int t = lane + 32 * u;
+      if (t < b) x[r + i64(t) * n] = v[u];
+    }
+  }
+}
+
 }  // namespace
+
+void cholqr_fast(sk_ctx* ctx, double2* x, i64 n, int b, double2* s, double2* l, int* flag) {
+  if (b > 118) fail(SK_ERR_UNSUPPORTED, "cholqr_fast: block too large");
+  cross_gram(ctx, x, x, n, b, s);
+  const size_t smem = size_t(b) * (b + 1) * sizeof(double2);
+  SKB_CUDA(cudaFuncSetAttribute(chol_lazy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  chol_lazy_kernel<<<1, 128, smem, ctx->stream>>>(s, b, l, flag);
+  ++ctx->launches;
+  SKB_LAUNCH("chol_lazy_kernel");
+  const size_t smem2 = size_t(b) * b * sizeof(double2);
+  SKB_CUDA(cudaFuncSetAttribute(trsm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+  const i64 blocks = std::min<i64>((n + 7) / 8, ctx->sm_count);
+  trsm_rows_kernel<<<unsigned(blocks), 256, smem2, ctx->stream>>>(x, n, b, l);
+  ++ctx->launches;
+  SKB_LAUNCH("trsm_rows_kernel");
+}
 
 void cholesky_small(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag) {
   const size_t smem = size_t(b) * (b + 1) * sizeof(double2);
