@@ -153,6 +153,14 @@ int sk_interpolate_real(sk_ctx* ctx, int ndim, const int64_t* low_dims, const fl
 /* support_mask (maps.hpp:105, maps.cpp:47-52). */
 int sk_support_mask(sk_ctx* ctx, int64_t voxels, const float* lambda, double mask_threshold, uint8_t* mask);
 
+/* Test hook for the K2 Rayleigh-Ritz eigensolver (no reference counterpart;
+ * the reference uses Eigen's SelfAdjointEigenSolver, nullspace.cpp:13):
+ * h is an n x n Hermitian complex128 matrix, column-major, interleaved
+ * (re, im) doubles, host memory; on return it holds the eigenvectors and w
+ * the eigenvalues ascending.  n <= 64 uses the one-CTA kernel, larger n
+ * cuSOLVER Jacobi. */
+int sk_debug_small_eigh(sk_ctx* ctx, int64_t n, double* h, double* w);
+
 /* ----------------------------------------------------------- full pipeline */
 /* estimate_maps (maps.hpp:85-86, maps.cpp:265-330).  Outputs on full_dims:
  * maps Q x N_full, lambda_min_map N_full, support_mask N_full (each may be

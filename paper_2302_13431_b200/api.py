@@ -170,6 +170,7 @@ _SIGS = {
     "sk_interpolate_maps": ([_VP, _I32, _VP, _I64, _VP, _VP, _VP], _I32),
     "sk_interpolate_real": ([_VP, _I32, _VP, _VP, _VP, _VP], _I32),
     "sk_support_mask": ([_VP, _I64, _VP, _D, _VP], _I32),
+    "sk_debug_small_eigh": ([_VP, _I64, _VP, _VP], _I32),
     "sk_estimate_maps": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP], _I32),
     "sk_estimate_maps_debug": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                 _VP, _VP], _I32),
@@ -384,6 +385,18 @@ def interpolate_real(low: np.ndarray, full_dims, ctx: Context | None = None) -> 
     out = np.zeros(tuple(full_dims), dtype=np.float32)
     _check(lib().sk_interpolate_real(_ctx(ctx), lo.ndim, _p(_i64(lo.shape)), _p(lo), _p(_i64(full_dims)), _p(out)))
     return out
+
+
+def small_eigh(h: np.ndarray, ctx: Context | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """Test hook: the K2 Rayleigh-Ritz eigensolver on a Hermitian complex128
+    matrix (eigenvalues ascending, eigenvectors as columns), like numpy.linalg.eigh."""
+    a = np.array(h, dtype=np.complex128, order="F", copy=True)
+    n = a.shape[0]
+    if a.shape != (n, n):
+        raise ValueError("small_eigh: square matrix required")
+    w = np.zeros(n, dtype=np.float64)
+    _check(lib().sk_debug_small_eigh(_ctx(ctx), n, a.ctypes.data, w.ctypes.data))
+    return w, a
 
 
 def support_mask(lam: np.ndarray, threshold: float, ctx: Context | None = None) -> np.ndarray:

@@ -1,0 +1,590 @@
+// One-CTA FP64 Hermitian eigensolver for the Rayleigh-Ritz matrix of the K2
+// subspace solver (b <= 64, everything resident in shared memory).
+//
+// The reference solves the full Gram eigenproblem with Eigen's
+// SelfAdjointEigenSolver (nullspace.cpp:13); the B200 path projects onto a
+// b-column block (run_eigh_subspace) and only needs the b x b projection
+// H = V^H A V diagonalised.  cuSOLVER's dense solvers spend ~1 ms of small
+// launches on b = 64 (measured: Zheevj, Xsyevd and XsyevBatched alike), so
+// this kernel does the whole decomposition in one CTA.  It is latency-bound
+// (one SM, dependent FP64 chains), so every phase is organised around few
+// block barriers and no FP64 divisions on the critical chains (reciprocal
+// approximation + Newton steps instead):
+//
+//   1. Householder tridiagonalisation H = Q T Q^H (the zhetd2 / zlarfg
+//      convention: H_k = I - tau v v^H, v_0 = 1, real off-diagonal beta);
+//      H is kept as a full Hermitian matrix (padded rows) in shared memory so
+//      that rows are read contiguously without conjugation branches.  Two
+//      barriers per column: norms and p^H v are reduced redundantly by every
+//      warp, v and w = p - tau/2 (p^H v) v are formed on the fly.
+//   2. Eigenvalues of T by multisection (Sturm counts, dlaebz rules for tiny
+//      pivots): every eigenvalue is bracketed by TPE threads that evaluate
+//      two interior points each per step, to 1e-10 ||T||.
+//   3. Eigenvectors of T by inverse iteration (dstein): two solves of
+//      (T - lambda I) z = r with partial pivoting from a pseudo-random start
+//      (factors in shared memory), a Rayleigh-quotient refinement of lambda
+//      (to ~eps ||T||), and Gram-Schmidt plus shifted re-solves inside
+//      clusters of close eigenvalues.
+//   4. Back-transformation X = Q Z, one column per 8 lanes (no block barriers).
+//
+// Output matches cusolverDnZheevj: eigenvalues ascending in w, eigenvectors
+// overwrite H column-major.  A non-finite intermediate raises info[0] (the
+// caller then takes the full-matrix path, as for any solver failure).
+#include "sk_internal.h"
+
+#include <cfloat>
+#include <cstdio>
+#include <cstdlib>
+
+namespace skb {
+
+namespace {
+
+constexpr int kThreads = 512;
+constexpr int kMaxN = 64;
+
+__device__ long long g_phase_clock[8];  // development aid: clock64 at phase boundaries (thread 0)
+#define SKB_EIG_STAMP(i) \
+  if (threadIdx.x == 0) g_phase_clock[i] = clock64();
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cfma(double2 acc, double2 a, double2 b) {  // acc + a b
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+  return acc;
+}
+__device__ __forceinline__ double2 cfma_conj(double2 acc, double2 a, double2 b) {  // acc + conj(a) b
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+  return acc;
+}
+
+// 1/x from the hardware approximation plus Newton steps (1: ~2^-46, 2: ~ulp).
+template <int kNewton>
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < kNewton; ++i) r = fma(r, fma(-x, r, 1.0), r);
+  return r;
+}
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// Block-wide sum; every thread receives the total.
+__device__ __forceinline__ double block_sum(double x, double* red) {
+  x = warp_sum(x);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < kThreads / 32; ++k) s += red[k];
+  __syncthreads();
+  return s;
+}
+
+// Number of eigenvalues of the symmetric tridiagonal (d, e2 = e^2) not above
+// x0 and x1 (two independent chains for ILP).
+__device__ __forceinline__ void sturm_count2(const double* d, const double* e2, int n, double x0, double x1,
+                                             double pivmin, int& c0, int& c1) {
+  double q0 = d[0] - x0, q1 = d[0] - x1;
+  if (fabs(q0) < pivmin) q0 = -pivmin;
+  if (fabs(q1) < pivmin) q1 = -pivmin;
+  c0 = q0 <= 0.0 ? 1 : 0;
+  c1 = q1 <= 0.0 ? 1 : 0;
+  for (int i = 1; i < n; ++i) {
+    const double di = d[i], ei = e2[i - 1];
+    q0 = (di - x0) - ei * frcp<1>(q0);
+    q1 = (di - x1) - ei * frcp<1>(q1);
+    if (fabs(q0) < pivmin) q0 = -pivmin;
+    if (fabs(q1) < pivmin) q1 = -pivmin;
+    c0 += q0 <= 0.0 ? 1 : 0;
+    c1 += q1 <= 0.0 ? 1 : 0;
+  }
+}
+
+__device__ __forceinline__ double hash_unit(unsigned a, unsigned b) {  // deterministic value in (-1, 1)
+  unsigned h = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u) * 0x85EBCA77u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  h *= 0x297A2D39u;
+  h ^= h >> 15;
+  return (double(h) + 0.5) * (2.0 / 4294967296.0) - 1.0;
+}
+
+// Solve (T - s I) z = r in place (z holds r on entry, stride zs) by Gaussian
+// elimination with partial pivoting (dgtsv / dlagtf style); zero pivots are
+// perturbed to `tiny`.  Factor rows (1/u0, u1, u2) go to shared memory
+// u[(i * 3 + f) * stride + t] (conflict-free across t); the eliminated
+// right-hand side is kept in z.
+__device__ void tri_solve(const double* d, const double* e, int n, double s, double tiny, double* z, int zs,
+                          double* u, int stride, int t) {
+  auto U = [&](int i, int f) -> double& { return u[(i * 3 + f) * stride + t]; };
+  double p0 = d[0] - s, p1 = n > 1 ? e[0] : 0.0, p2 = 0.0, r0 = z[0];
+  for (int i = 0; i + 1 < n; ++i) {
+    const double sub = e[i], dg = d[i + 1] - s, sup = (i + 2 < n) ? e[i + 1] : 0.0, rr = z[(i + 1) * zs];
+    if (fabs(p0) >= fabs(sub)) {
+      if (p0 == 0.0) p0 = tiny;
+      const double inv = frcp<2>(p0), l = sub * inv;
+      U(i, 0) = inv;
+      U(i, 1) = p1;
+      U(i, 2) = p2;
+      z[i * zs] = r0;
+      p0 = dg - l * p1;
+      p1 = sup - l * p2;
+      r0 = rr - l * r0;
+    } else {
+      const double inv = frcp<2>(sub), l = p0 * inv;
+      U(i, 0) = inv;
+      U(i, 1) = dg;
+      U(i, 2) = sup;
+      z[i * zs] = rr;
+      const double n0 = p1 - l * dg, n1 = p2 - l * sup, nr = r0 - l * rr;
+      p0 = n0;
+      p1 = n1;
+      r0 = nr;
+    }
+    p2 = 0.0;
+  }
+  if (p0 == 0.0) p0 = tiny;
+  double z1 = r0 * frcp<2>(p0), z2 = 0.0;  // z_{i+1}, z_{i+2}
+  z[(n - 1) * zs] = z1;
+  for (int i = n - 2; i >= 0; --i) {
+    const double zi = (z[i * zs] - U(i, 1) * z1 - U(i, 2) * z2) * U(i, 0);
+    z[i * zs] = zi;
+    z2 = z1;
+    z1 = zi;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) herm_eig_kernel(double2* __restrict__ H, int n, double* __restrict__ w,
+                                                             double floor_rel, int* __restrict__ info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ld = n + 1;  // padded row stride (double2) of the full Hermitian A (bank skew)
+  const int xs = n + 1;  // padded row stride of X
+  const int zs = n + 1;  // padded row stride of zr
+  const int uwords = (max(2 * n * xs, 3 * n * n) + 1) & ~1;  // X (complex) and the LU factors share it; even
+  double2* A = reinterpret_cast<double2*>(smem_raw);  // full Hermitian matrix; row k holds v_k after step k
+  double* un = reinterpret_cast<double*>(A + n * ld);  // union: LU factors (step 3), X (step 4)
+  double2* X = reinterpret_cast<double2*>(un);         // [n][xs] row-major
+  double2* pv = reinterpret_cast<double2*>(un + uwords);  // [n]
+  double2* vv = pv + n;                                    // [n]
+  double2* tau = vv + n;                                   // [n]
+  double* d = reinterpret_cast<double*>(tau + n);
+  double* e = d + n;
+  double* e2 = e + n;
+  double* lam = e2 + n;
+  double* red = lam + n;  // [kThreads / 32]
+  double* zr = red + kThreads / 32;                // [n][zs] real eigenvectors of T, row-major [i][t]
+  int* cl = reinterpret_cast<int*>(zr + n * zs);  // [2n + 1] cluster table
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  SKB_EIG_STAMP(0);
+
+  // lower triangle of H (column-major) -> full Hermitian A (row-major)
+  for (int e0 = tid; e0 < n * n; e0 += kThreads) {
+    const int i = e0 % n, j = e0 / n;
+    if (i >= j) {
+      double2 a = H[i + size_t(j) * n];
+      if (i == j) a.y = 0.0;
+      A[i * ld + j] = a;
+      A[j * ld + i] = cconj(a);
+    }
+  }
+  __syncthreads();
+
+  // ---- 1. tridiagonalisation (zhetd2, lower): x = A(k+1:, k) = conj(A(k, k+1:))
+  long long tacc0 = 0, tacc1 = 0, tacc2 = 0, tc = 0;
+  for (int k = 0; k + 1 < n; ++k) {
+    tc = clock64();
+    const int m = n - k - 1;
+    const double2* rowk = A + k * ld + k + 1;  // conj(x)
+    // ||x[1:]||^2, redundantly per warp (m <= 63)
+    double part = 0.0;
+    for (int i = 1 + lane; i < m; i += 32) {
+      const double2 a = rowk[i];
+      part += a.x * a.x + a.y * a.y;
+    }
+    const double xnorm2 = warp_sum(part);
+    const double2 alpha = cconj(rowk[0]);
+    double2 t = make_double2(0.0, 0.0), scale = make_double2(0.0, 0.0);
+    double beta = alpha.x;
+    if (xnorm2 > 0.0 || alpha.y != 0.0) {  // zlarfg
+      beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xnorm2), alpha.x);
+      const double ib = frcp<2>(beta);
+      t = make_double2((beta - alpha.x) * ib, -alpha.y * ib);
+      const double2 den = make_double2(alpha.x - beta, alpha.y);
+      const double inv = frcp<2>(den.x * den.x + den.y * den.y);
+      scale = make_double2(den.x * inv, -den.y * inv);
+    }
+    if (tid == 0) {
+      e[k] = beta;
+      d[k] = A[k * ld + k].x;
+      tau[k] = t;
+    }
+    if (t.x == 0.0 && t.y == 0.0) continue;  // H_k = I (uniform across the block; A unchanged)
+    tacc0 += clock64() - tc;
+    tc = clock64();
+    auto vj_of = [&](int j) { return j == 0 ? make_double2(1.0, 0.0) : cmul(cconj(rowk[j]), scale); };
+    if (tid < m) vv[tid] = vj_of(tid);
+    // p = tau * A22 v, eight lanes per row, v formed on the fly
+    {
+      const int i = tid >> 3, h = tid & 7;
+      double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+      if (i < m) {
+        const double2* ar = A + (k + 1 + i) * ld + k + 1;
+        int j = h;
+        for (; j + 8 < m; j += 16) {
+          acc0 = cfma(acc0, ar[j], vj_of(j));
+          acc1 = cfma(acc1, ar[j + 8], vj_of(j + 8));
+        }
+        if (j < m) acc0 = cfma(acc0, ar[j], vj_of(j));
+      }
+      double2 acc = cadd(acc0, acc1);
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      }
+      if (i < m && h == 0) pv[i] = cmul(t, acc);
+    }
+    __syncthreads();
+    tacc1 += clock64() - tc;
+    tc = clock64();
+    // a2 = -tau/2 (p^H v), redundantly per warp; w = p + a2 v on the fly
+    double2 dp = make_double2(0.0, 0.0);
+    for (int i = lane; i < m; i += 32) dp = cfma_conj(dp, pv[i], vv[i]);
+    dp.x = warp_sum(dp.x);
+    dp.y = warp_sum(dp.y);
+    const double2 a2 = cmul(make_double2(-0.5 * t.x, -0.5 * t.y), dp);
+    // A22 -= v w^H + w v^H (both triangles); v_k goes to row k (dead after this step)
+    if (tid < m) A[k * ld + k + 1 + tid] = vv[tid];
+    {
+      // this lane's columns j = lane, lane + 32 (m <= 63)
+      const int j0 = lane, j1 = lane + 32;
+      double2 vc0 = make_double2(0.0, 0.0), wc0 = vc0, vc1 = vc0, wc1 = vc0;
+      if (j0 < m) {
+        vc0 = cconj(vv[j0]);
+        wc0 = cconj(cfma(pv[j0], a2, vv[j0]));
+      }
+      if (j1 < m) {
+        vc1 = cconj(vv[j1]);
+        wc1 = cconj(cfma(pv[j1], a2, vv[j1]));
+      }
+      for (int i = warp; i < m; i += kThreads / 32) {
+        const double2 vi = vv[i], wi = cfma(pv[i], a2, vi);
+        double2* ar = A + (k + 1 + i) * ld + k + 1;
+        if (j0 < m) {
+          const double2 sub = cadd(cmul(vi, wc0), cmul(wi, vc0));
+          double2 a = ar[j0];
+          a.x -= sub.x;
+          a.y = (i == j0) ? 0.0 : a.y - sub.y;
+          ar[j0] = a;
+        }
+        if (j1 < m) {
+          const double2 sub = cadd(cmul(vi, wc1), cmul(wi, vc1));
+          double2 a = ar[j1];
+          a.x -= sub.x;
+          a.y = (i == j1) ? 0.0 : a.y - sub.y;
+          ar[j1] = a;
+        }
+      }
+    }
+    __syncthreads();
+    tacc2 += clock64() - tc;
+  }
+  if (tid == 0) {
+    g_phase_clock[6] = tacc0;
+    g_phase_clock[7] = tacc1 * 1000000 + tacc2 / 1000;
+  }
+  if (tid == 0) {
+    d[n - 1] = A[(n - 1) * ld + n - 1].x;
+    tau[n - 1] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+
+  SKB_EIG_STAMP(1);
+  // ---- 2. eigenvalues by multisection
+  double lo = 0.0, hi = 0.0, emax2 = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
+    lo = i == 0 ? d[i] - r : fmin(lo, d[i] - r);
+    hi = i == 0 ? d[i] + r : fmax(hi, d[i] + r);
+    if (i + 1 < n) emax2 = fmax(emax2, e[i] * e[i]);
+  }
+  if (tid < n - 1) e2[tid] = e[tid] * e[tid];
+  __syncthreads();
+  const double tnorm = fmax(fabs(lo), fabs(hi));
+  const double pivmin = DBL_MIN * fmax(1.0, emax2);
+  lo -= 2.0 * DBL_EPSILON * tnorm + pivmin;
+  hi += 2.0 * DBL_EPSILON * tnorm + pivmin;
+  int tpe = 1;
+  while (tpe * 2 * n <= kThreads && tpe < 4) tpe *= 2;  // more points per step hit the MUFU/FP64 rate
+  {
+    const int t = tid / tpe, s = tid % tpe, base = lane & ~(tpe - 1);
+    const int pts = 2 * tpe;  // interior points per eigenvalue per step
+    const bool act = t < n;
+    double a = lo, b = hi;
+    // fixed step count (uniform control flow); to 1e-10 ||T||, the Rayleigh
+    // quotient after inverse iteration supplies the rest
+    const int steps = int(ceil(log((hi - lo) / (1e-10 * tnorm + pivmin)) / log(double(pts + 1)))) + 1;
+    for (int it = 0; it < steps; ++it) {
+      const double wdt = (b - a) / double(pts + 1);
+      const double x0 = a + wdt * double(2 * s + 1), x1 = a + wdt * double(2 * s + 2);
+      int k0 = 0, k1 = 0;
+      if (act) sturm_count2(d, e2, n, x0, x1, pivmin, k0, k1);
+      double na = a, nb = b;
+      for (int q = 0; q < tpe; ++q) {
+        const double y0 = __shfl_sync(0xffffffffu, x0, base + q), y1 = __shfl_sync(0xffffffffu, x1, base + q);
+        const int m0 = __shfl_sync(0xffffffffu, k0, base + q), m1 = __shfl_sync(0xffffffffu, k1, base + q);
+        if (m0 <= t) na = fmax(na, y0);
+        if (m0 > t) nb = fmin(nb, y0);
+        if (m1 <= t) na = fmax(na, y1);
+        if (m1 > t) nb = fmin(nb, y1);
+      }
+      a = na;
+      b = nb;
+    }
+    if (act && s == 0) lam[t] = 0.5 * (a + b);
+  }
+  __syncthreads();
+
+  SKB_EIG_STAMP(2);
+  // ---- 3. eigenvectors of T by inverse iteration (one thread per eigenvalue)
+  const double tiny = DBL_EPSILON * tnorm + pivmin;
+  if (tid < n) {
+    const int t = tid;
+    double* z = zr + t;  // column t, row stride zs
+    for (int i = 0; i < n; ++i) z[i * zs] = hash_unit(unsigned(t), unsigned(i));
+    for (int pass = 0; pass < 2; ++pass) {
+      tri_solve(d, e, n, lam[t], tiny, z, zs, un, n, t);
+      double s2 = 0.0;
+      for (int i = 0; i < n; ++i) s2 += z[i * zs] * z[i * zs];
+      const double inv = rsqrt(s2);
+      for (int i = 0; i < n; ++i) z[i * zs] *= inv;
+    }
+    double rq = 0.0;  // Rayleigh quotient refinement of lambda
+    for (int i = 0; i < n; ++i) {
+      const double zi = z[i * zs];
+      rq += d[i] * zi * zi;
+      if (i + 1 < n) rq += 2.0 * e[i] * zi * z[(i + 1) * zs];
+    }
+    lam[t] = rq;
+  }
+  __syncthreads();
+
+  SKB_EIG_STAMP(3);
+  // Clusters (dstein): consecutive eigenvalues closer than kClus ||T||.
+  // Inverse-iteration vectors are orthogonal to ~eps ||T|| / gap, so cluster
+  // members are orthonormalised (CGS2, in order) and - when the cluster
+  // reaches above floor_rel ||T|| - re-solved with their own shifts and
+  // re-orthonormalised twice, which converges to the individual eigenvectors.
+  // Clusters below the floor (the noise tail of a Ritz spectrum, never used
+  // individually by the caller) only get the orthonormalisation.
+  constexpr double kClus = 1e-5;
+  int* cs = cl;      // cluster start of j
+  int* cf = cl + n;  // bit0: multi-member cluster, bit1: refine
+  if (tid == 0) {
+    int any = 0;
+    for (int i = 0; i < n; ++i) {
+      cs[i] = (i > 0 && fabs(lam[i] - lam[i - 1]) < kClus * tnorm) ? cs[i - 1] : i;
+      cf[i] = 0;
+    }
+    for (int i = 0; i < n;) {
+      int j = i;
+      while (j + 1 < n && cs[j + 1] == i) ++j;
+      if (j > i) {
+        any = 1;
+        const int fl = 1 | (lam[j] >= floor_rel * tnorm ? 2 : 0);
+        for (int q = i; q <= j; ++q) cf[q] = fl;
+      }
+      i = j + 1;
+    }
+    cl[2 * n] = any;
+  }
+  __syncthreads();
+  if (cl[2 * n]) {
+    double* dots = reinterpret_cast<double*>(pv);  // free after step 1
+    auto cgs2 = [&](int j) {  // z_j <- normalise((I - Z_c Z_c^T)^2 z_j), Z_c = members before j
+      const int j0 = cs[j];
+      for (int pass = 0; pass < 2 && j0 < j; ++pass) {
+        for (int q = j0 + warp; q < j; q += kThreads / 32) {
+          double sd = 0.0;
+          for (int i = lane; i < n; i += 32) sd += zr[i * zs + q] * zr[i * zs + j];
+          sd = warp_sum(sd);
+          if (lane == 0) dots[q] = sd;
+        }
+        __syncthreads();
+        for (int i = tid; i < n; i += kThreads) {
+          double acc = zr[i * zs + j];
+          for (int q = j0; q < j; ++q) acc -= dots[q] * zr[i * zs + q];
+          zr[i * zs + j] = acc;
+        }
+        __syncthreads();
+      }
+      double part3 = 0.0;
+      for (int i = tid; i < n; i += kThreads) part3 += zr[i * zs + j] * zr[i * zs + j];
+      const double nn = block_sum(part3, red);
+      const double inv = nn > 0.0 ? rsqrt(nn) : 0.0;
+      for (int i = tid; i < n; i += kThreads) zr[i * zs + j] *= inv;
+      __syncthreads();
+    };
+    for (int j = 0; j < n; ++j)
+      if (cf[j] & 1) cgs2(j);
+    for (int round = 0; round < 2; ++round) {
+      if (tid < n && (cf[tid] & 2)) tri_solve(d, e, n, lam[tid], tiny, zr + tid, zs, un, n, tid);
+      __syncthreads();
+      for (int j = 0; j < n; ++j)
+        if (cf[j] & 2) cgs2(j);
+    }
+    if (tid < n && (cf[tid] & 2)) {  // refresh lambda from the final vector
+      double rq = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const double zi = zr[i * zs + tid];
+        rq += d[i] * zi * zi;
+        if (i + 1 < n) rq += 2.0 * e[i] * zi * zr[(i + 1) * zs + tid];
+      }
+      lam[tid] = rq;
+    }
+    __syncthreads();
+  }
+
+  SKB_EIG_STAMP(4);
+  // ---- 4. back-transformation X = Q Z (H_0 ... H_{n-2} applied right to left)
+  for (int e0 = tid; e0 < n * n; e0 += kThreads) {
+    const int i = e0 / n, c = e0 % n;
+    X[i * xs + c] = make_double2(zr[i * zs + c], 0.0);
+  }
+  __syncthreads();
+  {
+    // Reflectors in pairs (k1 = k applied first, then k0 = k - 1):
+    //   s1 = v1^H X,  s0 = v0^H X - tau1 (v0^H v1) s1,
+    //   X -= tau1 v1 s1 + tau0 v0 s0      (v0 starts one row above v1).
+    const int c = tid >> 3, rs = tid & 7;  // 8 lanes per column, rows interleaved
+    const bool act = c < n;
+    auto xat = [&](int r) -> double2& { return X[r * xs + c]; };
+    int k = n - 2;
+    for (; k >= 1; k -= 2) {
+      const int k0 = k - 1;
+      const double2 t1 = tau[k], t0 = tau[k0];
+      const double2* v1 = A + k * ld + k + 1;    // rows k+1 .. n-1
+      const double2* v0 = A + k0 * ld + k0 + 1;  // rows k   .. n-1
+      const int m1 = n - k - 1;
+      double2 s1 = make_double2(0.0, 0.0), s0 = s1, c01 = s1;
+      if (act) {
+        if (rs == 0) s0 = cfma_conj(s0, v0[0], xat(k));
+        for (int i = rs; i < m1; i += 8) {
+          const double2 x = xat(k + 1 + i);
+          s1 = cfma_conj(s1, v1[i], x);
+          s0 = cfma_conj(s0, v0[i + 1], x);
+          c01 = cfma_conj(c01, v0[i + 1], v1[i]);
+        }
+      }
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        s1.x += __shfl_xor_sync(0xffffffffu, s1.x, o);
+        s1.y += __shfl_xor_sync(0xffffffffu, s1.y, o);
+        s0.x += __shfl_xor_sync(0xffffffffu, s0.x, o);
+        s0.y += __shfl_xor_sync(0xffffffffu, s0.y, o);
+        c01.x += __shfl_xor_sync(0xffffffffu, c01.x, o);
+        c01.y += __shfl_xor_sync(0xffffffffu, c01.y, o);
+      }
+      const double2 f1 = cmul(t1, s1);
+      const double2 g = cmul(c01, f1);
+      const double2 f0 = cmul(t0, make_double2(s0.x - g.x, s0.y - g.y));
+      if (act) {
+        if (rs == 0) {
+          double2& x = xat(k);
+          const double2 u = cmul(v0[0], f0);
+          x.x -= u.x;
+          x.y -= u.y;
+        }
+        for (int i = rs; i < m1; i += 8) {
+          double2& x = xat(k + 1 + i);
+          const double2 u = cadd(cmul(v1[i], f1), cmul(v0[i + 1], f0));
+          x.x -= u.x;
+          x.y -= u.y;
+        }
+      }
+    }
+    if (k == 0) {  // leftover single reflector
+      const double2 tk = tau[0];
+      const double2* vk = A + 1;
+      const int m = n - 1;
+      double2 sd = make_double2(0.0, 0.0);
+      if (act)
+        for (int i = rs; i < m; i += 8) sd = cfma_conj(sd, vk[i], xat(1 + i));
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        sd.x += __shfl_xor_sync(0xffffffffu, sd.x, o);
+        sd.y += __shfl_xor_sync(0xffffffffu, sd.y, o);
+      }
+      const double2 f = cmul(tk, sd);
+      if (act)
+        for (int i = rs; i < m; i += 8) {
+          double2& x = xat(1 + i);
+          const double2 u = cmul(vk[i], f);
+          x.x -= u.x;
+          x.y -= u.y;
+        }
+    }
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int e0 = tid; e0 < n * n; e0 += kThreads) {
+    const int i = e0 % n, c = e0 / n;
+    const double2 x = X[i * xs + c];
+    bad |= !isfinite(x.x) || !isfinite(x.y);
+    H[i + size_t(c) * n] = x;
+  }
+  if (tid < n) {
+    w[tid] = lam[tid];
+    bad |= !isfinite(lam[tid]);
+  }
+  if (bad) atomicExch(info, 1);
+  SKB_EIG_STAMP(5);
+}
+
+size_t herm_eig_smem(int n) {
+  const size_t np = size_t(n) * (n + 1);  // full matrix, padded rows
+  const size_t uwords = (std::max<size_t>(2 * size_t(n) * (n + 1), 3 * size_t(n) * n) + 1) & ~size_t(1);
+  return np * sizeof(double2) + uwords * sizeof(double) + 3 * size_t(n) * sizeof(double2) +
+         (4 * size_t(n) + kThreads / 32 + size_t(n) * (n + 1)) * sizeof(double) + (2 * size_t(n) + 1) * sizeof(int);
+}
+
+}  // namespace
+
+bool herm_eig_small(sk_ctx* ctx, double2* H, int n, double* w, int* info, double floor_rel) {
+  if (n < 1 || n > kMaxN) return false;
+  const size_t smem = herm_eig_smem(n);
+  SKB_CUDA(cudaFuncSetAttribute(herm_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  herm_eig_kernel<<<1, kThreads, smem, ctx->stream>>>(H, n, w, floor_rel, info);
+  ++ctx->launches;
+  SKB_LAUNCH("herm_eig_kernel");
+  if (std::getenv("SKB_PROFILE_NS")) {
+    long long c[8];
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+    SKB_CUDA(cudaMemcpyFromSymbol(c, g_phase_clock, sizeof c));
+    std::fprintf(stderr,
+                 "[eig n=%d] kcycles tridiag %.1f (norm %.1f p %.1f r2 %.1f) bisect %.1f invit %.1f clusters %.1f "
+                 "back %.1f\n",
+                 n, (c[1] - c[0]) / 1e3, c[6] / 1e3, (c[7] / 1000000) / 1e3, double(c[7] % 1000000), (c[2] - c[1]) / 1e3,
+                 (c[3] - c[2]) / 1e3, (c[4] - c[3]) / 1e3, (c[5] - c[4]) / 1e3);
+  }
+  return true;
+}
+
+}  // namespace skb

@@ -187,6 +187,12 @@ void shift_negate(sk_ctx* ctx, const double2* a, double2* m, i64 n, double shift
 void cross_gram(sk_ctx* ctx, const double2* x, const double2* y, i64 n, int b, double2* out);
 void chol_inv(sk_ctx* ctx, const double2* s, int b, double2* minv, int* flag);
 void cholesky_small(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag);
+// One-CTA Hermitian eigensolver (sk_eig.cu) for b <= 64: eigenvalues ascending
+// into w, eigenvectors overwrite H (column-major); info[0] = 1 on a
+// non-finite result.  Returns false (nothing launched) for larger b.
+// Clusters of close eigenvalues lying entirely below floor_rel * ||H|| are
+// only orthonormalised, not refined to individual eigenvectors.
+bool herm_eig_small(sk_ctx* ctx, double2* H, int n, double* w, int* info, double floor_rel = 0.0);
 // One CholQR pass on X (n x b, b <= 118): cross_gram + one-CTA lazy Cholesky +
 // warp-per-row triangular solve; no host synchronisation (flag raised on failure).
 void cholqr_fast(sk_ctx* ctx, double2* x, i64 n, int b, double2* s, double2* l, int* flag);

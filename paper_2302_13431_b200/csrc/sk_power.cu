@@ -8,21 +8,22 @@
 // expansion) as an fp32 hi/lo pair.  Blocks are persistent and walk voxel
 // tiles; the next tile's h x VPB slab of hi planes is prefetched with
 // cp.async (double buffer) while the current tile iterates.  Each voxel is
-// unpacked into registers: matrix row p is held by TPR threads (TPR = 1 by
-// default; 2 halves the registers per thread and is kept as a measured,
-// slower alternative), QP = Q rounded up to a power of two (padding rows/cols
-// are zero).
+// unpacked into registers: a thread holds RPT full matrix rows
+// (p = local + r * QP/RPT), QP = Q rounded up to a power of two (padding
+// rows/cols are zero).
 //
-// Per iteration a thread does QP/TPR complex MACs (its row segment times v, v
-// broadcast from shared memory as float4 pairs) and rescales its own
-// component; v and the per-warp partials of ||u||^2 are double-buffered so an
-// iteration costs one voxel-scoped barrier (named barrier when a voxel spans
-// several warps, __syncwarp otherwise).  The matrix never leaves
-// registers across the `iters` iterations, so the stage is FP32-bound:
-// 8 Q^2 flops per voxel-iteration against one read of the planes.  The final
-// Rayleigh quotient is evaluated in FP64 on hi + lo (lo streamed into the
-// free tile buffer during the iterations), which keeps per-voxel eigenvalues
-// at ~FP64 accuracy.
+// Per iteration a thread loads v once from shared memory (float4 broadcast
+// pairs) and does RPT * QP complex MACs with it, then rescales its own
+// components; v and the per-warp partials of ||u||^2 are double-buffered so
+// an iteration costs one voxel-scoped barrier (named barrier when a voxel
+// spans several warps, __syncwarp otherwise).  RPT = 2 halves the shared
+// loads and the reduction overhead per FMA for Q = 32 (the main loop is then
+// ~80% FFMA).  The matrix never leaves registers across the `iters`
+// iterations, so the stage is FP32-bound: 8 Q^2 flops per voxel-iteration
+// against one read of the planes.  The final Rayleigh quotient is evaluated
+// in FP64 on hi + lo (lo streamed into the free tile buffer during the
+// iterations), which keeps per-voxel eigenvalues at ~FP64 accuracy
+// (DESIGN.md §5).
 //
 // Exactly the reference's control flow: fixed iteration count; at it == 0 an
 // annihilated all-ones start restarts from e_0; a norm below 1e-14 freezes v.
@@ -39,6 +40,24 @@ __device__ __forceinline__ void cmac(float2& acc, float2 m, float2 x) {
   acc.y = fmaf(m.y, x.x, acc.y);
 }
 
+// Packed FP32x2 FMA (FFMA2, sm_100): same FMA-pipe rate as FFMA at half the
+// issue slots.  ptxas folds pk(s, s) into a scalar-broadcast operand and
+// pk(hi, lo) of a register pair into a swapped (LO_HI) operand.
+using u64 = unsigned long long;
+__device__ __forceinline__ u64 pk(float lo, float hi) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void ffma2(u64& d, u64 a, u64 b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+__device__ __forceinline__ float2 unpk(u64 x) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(x));
+  return r;
+}
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
@@ -49,21 +68,20 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <int QP, int TPR>
+template <int QP_, int RPT_, int THREADS_, int MINB_>
 struct Layout {
-  static constexpr int kThreads = 256;
-  static constexpr int kCols = QP / TPR;         // matrix columns held per thread
-  static constexpr int kTPV = QP * TPR;          // threads per voxel
+  static constexpr int QP = QP_, RPT = RPT_, kThreads = THREADS_, kMinBlocks = MINB_;
+  static constexpr int kTPV = QP / RPT;          // threads per voxel
   static constexpr int kVPB = kThreads / kTPV;   // voxels per block
   static constexpr int kWPV = kTPV > 32 ? kTPV / 32 : 1;  // warps per voxel
   static constexpr int kStride = QP + 2;         // float2 per v row (16-B aligned, bank-skewed)
+  static constexpr int kAcc = RPT >= 4 ? 1 : 4 / RPT;     // accumulator pairs per row
 };
 
-// Sum over the voxel's rows of a per-row value replicated in its TPR threads.
-template <int QP, int TPR, typename T>
-__device__ __forceinline__ T row_sum(T x, T* red, int vox, int hc) {
-  using L = Layout<QP, TPR>;
-  if (TPR > 1 && hc != 0) x = T(0);
+// Sum over the voxel's threads.  Multi-warp voxels go through shared memory
+// with block-wide barriers (used only outside the iteration loop).
+template <class L, typename T>
+__device__ __forceinline__ T voxel_sum(T x, T* red, int vox) {
   if constexpr (L::kTPV <= 32) {
 #pragma unroll
     for (int o = L::kTPV / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -82,16 +100,9 @@ __device__ __forceinline__ T row_sum(T x, T* red, int vox, int hc) {
   }
 }
 
-// Combine the TPR partial row sums (adjacent lanes).
-template <int TPR, typename T>
-__device__ __forceinline__ T pair_sum(T x) {
-  if constexpr (TPR == 2) x += __shfl_xor_sync(0xffffffffu, x, 1);
-  return x;
-}
-
-template <int QP, int TPR>
+template <class L>
 __device__ __forceinline__ void voxel_sync() {
-  if constexpr (Layout<QP, TPR>::kTPV <= 32)
+  if constexpr (L::kTPV <= 32)
     __syncwarp();
   else
     __syncthreads();
@@ -99,42 +110,47 @@ __device__ __forceinline__ void voxel_sync() {
 
 // Barrier over the threads of one voxel only: a warp-level sync for
 // single-warp voxels, a named barrier (id 1 + vox) for multi-warp voxels.
-template <int QP, int TPR>
+template <class L>
 __device__ __forceinline__ void voxel_bar(int vox) {
-  constexpr int kTPV = Layout<QP, TPR>::kTPV;
-  if constexpr (kTPV <= 32) {
+  if constexpr (L::kTPV <= 32) {
     __syncwarp();
   } else {
-    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + vox), "n"(kTPV) : "memory");
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + vox), "n"(L::kTPV) : "memory");
   }
-}
-
-template <int QP, int TPR>
-constexpr int min_blocks() {
-  return (QP == 64 && TPR == 1) ? 1 : (QP == 32 && TPR == 2) ? 3 : 2;
 }
 
 __device__ __forceinline__ int pair_index(int p, int c, int Q) { return p * Q - p * (p - 1) / 2 + (c - p); }
 
-template <int QP, int TPR>
-__global__ void __launch_bounds__(256, min_blocks<QP, TPR>()) power_kernel(PowerArgs a) {
-  using Lt = Layout<QP, TPR>;
-  constexpr int VPB = Lt::kVPB, COLS = Lt::kCols, WPV = Lt::kWPV;
+// Element (p, c) of the Hermitian matrix from the packed tile (zero outside Q).
+__device__ __forceinline__ float2 herm_at(const float2* gs, int p, int c, int Q, int VPB, int vox) {
+  float2 val = make_float2(0.f, 0.f);
+  if (p < Q && c < Q) {
+    if (p <= c) {
+      val = gs[pair_index(p, c, Q) * VPB + vox];
+    } else {
+      const float2 t = gs[pair_index(c, p, Q) * VPB + vox];
+      val = make_float2(t.x, -t.y);
+    }
+    if (p == c) val.y = 0.f;  // spatial_gram.cpp:140-146
+  }
+  return val;
+}
+
+template <class L>
+__global__ void __launch_bounds__(L::kThreads, L::kMinBlocks) power_kernel(PowerArgs a) {
+  constexpr int QP = L::QP, RPT = L::RPT, VPB = L::kVPB, WPV = L::kWPV, TPV = L::kTPV;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int Q = a.q;
   const int h = Q * (Q + 1) / 2;
   const int tile_elems = (h > QP ? h : QP) * VPB;
-  float2* gbuf = reinterpret_cast<float2*>(smem_raw);                     // [2][tile_elems]
-  float2* vs = gbuf + 2 * tile_elems;                                     // [2][VPB][kStride]
-  double* redd = reinterpret_cast<double*>(vs + 2 * VPB * Lt::kStride);   // [VPB][kWPV]
-  float* red = reinterpret_cast<float*>(redd + VPB * WPV);                // [VPB][kWPV]
-  float* red2 = red + VPB * WPV;                                          // [2][VPB][kWPV]
+  float2* gbuf = reinterpret_cast<float2*>(smem_raw);                    // [2][tile_elems]
+  float2* vs = gbuf + 2 * tile_elems;                                    // [2][VPB][kStride]
+  double* redd = reinterpret_cast<double*>(vs + 2 * VPB * L::kStride);   // [VPB][kWPV]
+  float* red = reinterpret_cast<float*>(redd + VPB * WPV);               // [VPB][kWPV]
+  float* red2 = red + VPB * WPV;                                         // [2][VPB][kWPV]
 
-  const int vox = threadIdx.x / Lt::kTPV;
-  const int local = threadIdx.x % Lt::kTPV;
-  const int p = local / TPR;
-  const int hc = local % TPR;
-  const int c0 = hc * COLS;
+  const int vox = threadIdx.x / TPV;
+  const int local = threadIdx.x % TPV;  // rows local + r * TPV
   const i64 tiles = (a.n + VPB - 1) / VPB;
 
   auto load_tile = [&](i64 t, float2* dst, const float2* src) {
@@ -164,63 +180,54 @@ __global__ void __launch_bounds__(256, min_blocks<QP, TPR>()) power_kernel(Power
     const i64 j = j0 + vox;
     const bool live = j < a.n;
 
-    // Unpack this thread's row segment (columns c0 .. c0 + COLS).
-    float2 m[COLS];
+    // Unpack this thread's rows.
+    float2 m[RPT][QP];
 #pragma unroll
-    for (int c = 0; c < COLS; ++c) {
-      const int cc = c0 + c;
-      float2 val = make_float2(0.f, 0.f);
-      if (p < Q && cc < Q) {
-        if (p <= cc) {
-          val = gs[pair_index(p, cc, Q) * VPB + vox];
-        } else {
-          const float2 t = gs[pair_index(cc, p, Q) * VPB + vox];
-          val = make_float2(t.x, -t.y);
-        }
-        if (p == cc) val.y = 0.f;  // spatial_gram.cpp:140-146
-      }
-      m[c] = val;
-    }
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+      for (int c = 0; c < QP; ++c) m[r][c] = herm_at(gs, local + r * TPV, c, Q, VPB, vox);
     // The tile buffer is free once every row is in registers: stream the lo
     // residual planes into it while the iterations run.
     if (a.planes_lo != nullptr) {
       __syncthreads();
       load_tile(tile, gs, a.planes_lo);
     }
-    // M[p][0] for the e_0 restart (held by the hc == 0 thread of the row)
-    float2 mp0 = m[0];
-    if constexpr (TPR == 2) {
-      mp0.x = __shfl_sync(0xffffffffu, m[0].x, threadIdx.x & ~1);
-      mp0.y = __shfl_sync(0xffffffffu, m[0].y, threadIdx.x & ~1);
-    }
 
-    // v is double-buffered in shared memory (vb[0], vb[1]) together with the
-    // per-warp partials of ||u||^2, so an iteration needs one voxel barrier.
-    auto vb = [&](int b) { return vs + (b * VPB + vox) * Lt::kStride; };
+    // v is double-buffered in shared memory (buffers 0 and 1) together with
+    // the per-warp partials of ||u||^2, so an iteration needs one voxel barrier.
+    auto vb = [&](int b) { return vs + (b * VPB + vox) * L::kStride; };
     const float init = rsqrtf(float(Q));
-    float2 vp = (p < Q) ? make_float2(init, 0.f) : make_float2(0.f, 0.f);
-    if (hc == 0) vb(0)[p] = vp;
+    float2 vp[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      vp[r] = (local + r * TPV < Q) ? make_float2(init, 0.f) : make_float2(0.f, 0.f);
+      vb(0)[local + r * TPV] = vp[r];
+    }
     bool done = false;
-    voxel_sync<QP, TPR>();
+    voxel_sync<L>();
 
     // Publish u into buffer b and its squared norm: returned directly for a
     // single-warp voxel, left as per-warp partials in red2[b] otherwise.
-    auto publish = [&](float2 u, int b) -> float {
-      if (hc == 0) vb(b)[p] = u;
-      float x = (hc == 0) ? u.x * u.x + u.y * u.y : 0.f;
-      if constexpr (Lt::kTPV <= 32) {
+    auto publish = [&](const float2 (&u)[RPT], int b) -> float {
+      float x = 0.f;
 #pragma unroll
-        for (int o = Lt::kTPV / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      for (int r = 0; r < RPT; ++r) {
+        vb(b)[local + r * TPV] = u[r];
+        x = fmaf(u[r].x, u[r].x, fmaf(u[r].y, u[r].y, x));
+      }
+      if constexpr (TPV <= 32) {
+#pragma unroll
+        for (int o = TPV / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
         return x;
       } else {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if ((threadIdx.x & 31) == 0) red2[(b * VPB + vox) * WPV + ((threadIdx.x % Lt::kTPV) >> 5)] = x;
+        if ((threadIdx.x & 31) == 0) red2[(b * VPB + vox) * WPV + (local >> 5)] = x;
         return 0.f;
       }
     };
     auto published_norm = [&](float own, int b) -> float {
-      if constexpr (Lt::kTPV <= 32) {
+      if constexpr (TPV <= 32) {
         return own;
       } else {
         float s = 0.f;
@@ -230,48 +237,79 @@ __global__ void __launch_bounds__(256, min_blocks<QP, TPR>()) power_kernel(Power
       }
     };
 
-    // M v: v is staged into registers in chunks of 8 complex values (4
-    // LDS.128 in flight) feeding 4 independent accumulator pairs.
-    auto matvec = [&](const float2* v, float2& out) {
-      const float4* v4 = reinterpret_cast<const float4*>(v + c0);
-      float2 acc[4];
+    // M v for the thread's rows: v is staged into registers in chunks of 8
+    // complex values (4 LDS.128, shared by all RPT rows) feeding kAcc
+    // independent accumulator pairs per row.
+    // Complex MAC as two FFMA2: acc += m.x * (v.x, v.y), acc2 += m.y * (v.y, v.x);
+    // (M v) = (acc.x - acc2.x, acc.y + acc2.y).
+    auto matvec = [&](const float2* v, float2 (&out)[RPT]) {
+      constexpr int A = L::kAcc;
+      const float4* v4 = reinterpret_cast<const float4*>(v);
+      u64 acc[RPT][A], acc2[RPT][A];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) acc[k] = make_float2(0.f, 0.f);
-      constexpr int kChunk = COLS < 8 ? COLS : 8;
+      for (int r = 0; r < RPT; ++r)
 #pragma unroll
-      for (int cb = 0; cb < COLS; cb += kChunk) {
+        for (int k = 0; k < A; ++k) acc[r][k] = acc2[r][k] = 0ull;
+      constexpr int kChunk = QP < 8 ? QP : 8;
+#pragma unroll
+      for (int cb = 0; cb < QP; cb += kChunk) {
         float4 vv[kChunk / 2];
 #pragma unroll
         for (int t = 0; t < kChunk / 2; ++t) vv[t] = v4[cb / 2 + t];
 #pragma unroll
-        for (int t = 0; t < kChunk / 2; ++t) {
-          cmac(acc[(2 * t) & 3], m[cb + 2 * t], make_float2(vv[t].x, vv[t].y));
-          cmac(acc[(2 * t + 1) & 3], m[cb + 2 * t + 1], make_float2(vv[t].z, vv[t].w));
-        }
+        for (int t = 0; t < kChunk / 2; ++t)
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) {
+            const float2 ma = m[r][cb + 2 * t], mb = m[r][cb + 2 * t + 1];
+            const int ka = (2 * t) % A, kb = (2 * t + 1) % A;
+            ffma2(acc[r][ka], pk(ma.x, ma.x), pk(vv[t].x, vv[t].y));
+            ffma2(acc2[r][ka], pk(ma.y, ma.y), pk(vv[t].y, vv[t].x));
+            ffma2(acc[r][kb], pk(mb.x, mb.x), pk(vv[t].z, vv[t].w));
+            ffma2(acc2[r][kb], pk(mb.y, mb.y), pk(vv[t].w, vv[t].z));
+          }
       }
-      out = make_float2(pair_sum<TPR>((acc[0].x + acc[1].x) + (acc[2].x + acc[3].x)),
-                        pair_sum<TPR>((acc[0].y + acc[1].y) + (acc[2].y + acc[3].y)));
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        float2 s = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < A; ++k) {
+          const float2 x = unpk(acc[r][k]), y = unpk(acc2[r][k]);
+          s = make_float2(s.x + (x.x - y.x), s.y + (x.y + y.y));
+        }
+        out[r] = s;
+      }
     };
 
     // Iteration 0, peeled: an annihilated all-ones start restarts from e_0
     // (eigensolve.cpp:56-63); the candidate is formed uniformly and selected.
     if (a.iters > 0) {
-      float2 mv;
+      float2 mv[RPT], w[RPT], w0[RPT], v0[RPT];
       matvec(vb(0), mv);
-      float2 w = make_float2(a.alpha * vp.x + a.beta * mv.x, a.alpha * vp.y + a.beta * mv.y);
-      float n2 = row_sum<QP, TPR>(w.x * w.x + w.y * w.y, red, vox, hc);
-      const float2 v0 = (p == 0) ? make_float2(1.f, 0.f) : make_float2(0.f, 0.f);
-      const float2 w0 = make_float2(a.alpha * v0.x + a.beta * mp0.x, a.alpha * v0.y + a.beta * mp0.y);
-      const float n20 = row_sum<QP, TPR>(w0.x * w0.x + w0.y * w0.y, red, vox, hc);
+      float x = 0.f, x0 = 0.f;
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        w[r] = make_float2(a.alpha * vp[r].x + a.beta * mv[r].x, a.alpha * vp[r].y + a.beta * mv[r].y);
+        v0[r] = (local + r * TPV == 0) ? make_float2(1.f, 0.f) : make_float2(0.f, 0.f);
+        // (B e_0)[p] = alpha e_0[p] + beta M[p][0]
+        w0[r] = make_float2(a.alpha * v0[r].x + a.beta * m[r][0].x, a.alpha * v0[r].y + a.beta * m[r][0].y);
+        x += w[r].x * w[r].x + w[r].y * w[r].y;
+        x0 += w0[r].x * w0[r].x + w0[r].y * w0[r].y;
+      }
+      float n2 = voxel_sum<L>(x, red, vox);
+      const float n20 = voxel_sum<L>(x0, red, vox);
       if (n2 < 1e-28f) {  // ||B v|| < 1e-14
-        vp = v0;
-        w = w0;
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          vp[r] = v0[r];
+          w[r] = w0[r];
+        }
         n2 = n20;
       }
       if (n2 < 1e-28f) done = true;  // B ~ 0 here: keep the current v
       if (!done) {
         const float inv = rsqrtf(n2);
-        vp = make_float2(w.x * inv, w.y * inv);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) vp[r] = make_float2(w[r].x * inv, w[r].y * inv);
       }
     }
     // Iterations 1..iters-1, software-pipelined on the unnormalised iterate
@@ -281,106 +319,128 @@ __global__ void __launch_bounds__(256, min_blocks<QP, TPR>()) power_kernel(Power
     // in vprev.  Iteration k reads buffer k&1 and writes buffer (k+1)&1; the
     // barrier at the top of iteration k+1 orders both (every read of (k+1)&1
     // from iteration k-1 precedes the barrier at the top of iteration k).
-    float2 up = vp, vprev = vp;
+    float2 up[RPT], vprev[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) up[r] = vprev[r] = vp[r];
     float own = 0.f;
-    if (a.iters > 1) own = publish(up, 1);  // iteration 0 read only vb[0]
+    if (a.iters > 1) own = publish(up, 1);  // iteration 0 read only buffer 0
     for (int it = 1; it < a.iters; ++it) {
       const int b = it & 1;
-      voxel_bar<QP, TPR>(vox);
+      voxel_bar<L>(vox);
       const float n2 = published_norm(own, b);
-      float2 mv;
+      float2 mv[RPT];
       matvec(vb(b), mv);
       if (it > 1 && n2 < 1e-28f && !done) done = true;
       const float inv = rsqrtf(n2);
       if (!done) {
-        vprev = make_float2(up.x * inv, up.y * inv);
-        up = make_float2((a.alpha * up.x + a.beta * mv.x) * inv, (a.alpha * up.y + a.beta * mv.y) * inv);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {
+          vprev[r] = make_float2(up[r].x * inv, up[r].y * inv);
+          up[r] = make_float2((a.alpha * up[r].x + a.beta * mv[r].x) * inv,
+                              (a.alpha * up[r].y + a.beta * mv[r].y) * inv);
+        }
       }
       own = publish(up, b ^ 1);
     }
     int fb = 0;  // buffer that receives the final v
     if (a.iters > 1) {
-      voxel_bar<QP, TPR>(vox);
+      voxel_bar<L>(vox);
       const float n2 = published_norm(own, a.iters & 1);
-      if (!done && !(n2 < 1e-28f)) {
-        const float inv = rsqrtf(n2);
-        vp = make_float2(up.x * inv, up.y * inv);
-      } else {
-        vp = vprev;
-      }
+      const bool keep = done || n2 < 1e-28f;
+      const float inv = keep ? 0.f : rsqrtf(n2);
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) vp[r] = keep ? vprev[r] : make_float2(up[r].x * inv, up[r].y * inv);
       fb = (a.iters & 1) ^ 1;  // last read by iteration iters-1, before the barrier above
     }
-    voxel_sync<QP, TPR>();
+    voxel_sync<L>();
     float2* myv = vb(fb);
-    if (hc == 0) myv[p] = vp;
-    voxel_sync<QP, TPR>();
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) myv[local + r * TPV] = vp[r];
+    voxel_sync<L>();
 
     // Rayleigh quotient in FP64 on M = hi + lo: mv = Re(v^H M v) (the FP32
     // iterate v enters only to second order); value = Re(v^H B v).
-    double mrx = 0.0, mry = 0.0;
+    double mrx[RPT], mry[RPT];
 #pragma unroll
-    for (int c = 0; c < COLS; ++c) {
-      const float2 vc = myv[c0 + c];
-      mrx = fma(double(m[c].x), double(vc.x), mrx);
-      mrx = fma(-double(m[c].y), double(vc.y), mrx);
-      mry = fma(double(m[c].x), double(vc.y), mry);
-      mry = fma(double(m[c].y), double(vc.x), mry);
+    for (int r = 0; r < RPT; ++r) {
+      mrx[r] = 0.0;
+      mry[r] = 0.0;
+#pragma unroll
+      for (int c = 0; c < QP; ++c) {
+        const float2 vc = myv[c];
+        mrx[r] = fma(double(m[r][c].x), double(vc.x), mrx[r]);
+        mrx[r] = fma(-double(m[r][c].y), double(vc.y), mrx[r]);
+        mry[r] = fma(double(m[r][c].x), double(vc.y), mry[r]);
+        mry[r] = fma(double(m[r][c].y), double(vc.x), mry[r]);
+      }
     }
     if (a.planes_lo != nullptr) {
       cp_async_wait<0>();
       __syncthreads();
-      if (p < Q) {
-        for (int c = c0; c < c0 + COLS && c < Q; ++c) {
-          float2 lv;
-          if (p <= c) {
-            lv = gs[pair_index(p, c, Q) * VPB + vox];
-          } else {
-            const float2 t = gs[pair_index(c, p, Q) * VPB + vox];
-            lv = make_float2(t.x, -t.y);
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int p = local + r * TPV;
+        if (p < Q) {
+          for (int c = 0; c < Q; ++c) {
+            const float2 lv = herm_at(gs, p, c, Q, VPB, vox);
+            const float2 vc = myv[c];
+            mrx[r] += double(lv.x) * vc.x - double(lv.y) * vc.y;
+            mry[r] += double(lv.x) * vc.y + double(lv.y) * vc.x;
           }
-          if (p == c) lv.y = 0.f;
-          const float2 vc = myv[c];
-          mrx += double(lv.x) * vc.x - double(lv.y) * vc.y;
-          mry += double(lv.x) * vc.y + double(lv.y) * vc.x;
         }
       }
     }
-    mrx = pair_sum<TPR>(mrx);
-    mry = pair_sum<TPR>(mry);
-    const double mv = row_sum<QP, TPR>(double(vp.x) * mrx + double(vp.y) * mry, redd, vox, hc);
-    const float vn2 = row_sum<QP, TPR>(vp.x * vp.x + vp.y * vp.y, red, vox, hc);
+    double xd = 0.0;
+    float xn = 0.f;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      xd += double(vp[r].x) * mrx[r] + double(vp[r].y) * mry[r];
+      xn += vp[r].x * vp[r].x + vp[r].y * vp[r].y;
+    }
+    const double mv = voxel_sum<L>(xd, redd, vox);
+    const float vn2 = voxel_sum<L>(xn, red, vox);
 
     if (a.recon != nullptr) {
       // normalize_maps, per voxel: SoS (maps.cpp:117-128) then phase reference
       // against the apodised coil-combined calibration recon (maps.cpp:163-172).
       if (vn2 > 0.f) {
         const float inv = 1.0f / sqrtf(vn2);
-        vp.x *= inv;
-        vp.y *= inv;
-      } else if (p == 0 && hc == 0 && live && a.zeroed) {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) vp[r] = make_float2(vp[r].x * inv, vp[r].y * inv);
+      } else if (local == 0 && live && a.zeroed) {
         atomicAdd(a.zeroed, 1ull);
       }
-      float2 r = make_float2(0.f, 0.f);
-      if (p < Q && live) r = a.recon[i64(p) * a.n + j];
-      const float ux = row_sum<QP, TPR>(vp.x * r.x + vp.y * r.y, red, vox, hc);  // conj(v) * r
-      const float uy = row_sum<QP, TPR>(vp.x * r.y - vp.y * r.x, red, vox, hc);
+      float xr = 0.f, xi = 0.f;
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int p = local + r * TPV;
+        float2 rc = make_float2(0.f, 0.f);
+        if (p < Q && live) rc = a.recon[i64(p) * a.n + j];
+        xr += vp[r].x * rc.x + vp[r].y * rc.y;  // conj(v) * recon
+        xi += vp[r].x * rc.y - vp[r].y * rc.x;
+      }
+      const float ux = voxel_sum<L>(xr, red, vox);
+      const float uy = voxel_sum<L>(xi, red, vox);
       const float mag = sqrtf(ux * ux + uy * uy);
       if (mag > 0.f) {
         const float cx = ux / mag, cy = uy / mag;
-        vp = make_float2(vp.x * cx - vp.y * cy, vp.x * cy + vp.y * cx);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+          vp[r] = make_float2(vp[r].x * cx - vp[r].y * cy, vp[r].x * cy + vp[r].y * cx);
       }
     }
 
     // Stage maps for channel-major coalesced stores: reuse the plane tile.
     __syncthreads();
     float2* ms = gs;  // [QP][VPB]
-    if (hc == 0) ms[p * VPB + vox] = vp;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) ms[(local + r * TPV) * VPB + vox] = vp[r];
     __syncthreads();
     for (int e = threadIdx.x; e < Q * VPB; e += blockDim.x) {
       const int c = e / VPB, v = e % VPB;
       if (j0 + v < a.n) a.maps[i64(c) * a.n + j0 + v] = ms[c * VPB + v];
     }
-    if (p == 0 && hc == 0 && live) {
+    if (local == 0 && live) {
       const float lam = float(mv * double(a.lam_scale));
       if (a.lambda) a.lambda[j] = lam;
       if (a.value) a.value[j] = float(double(a.alpha) * vn2 + double(a.beta) * mv);
@@ -390,47 +450,44 @@ __global__ void __launch_bounds__(256, min_blocks<QP, TPR>()) power_kernel(Power
   }
 }
 
-template <int QP, int TPR>
+template <class L>
 void launch(sk_ctx* ctx, const PowerArgs& a) {
-  using Lt = Layout<QP, TPR>;
   const int h = a.q * (a.q + 1) / 2;
-  const size_t tile = size_t(std::max(h, QP)) * Lt::kVPB * sizeof(float2);
-  const size_t smem = 2 * tile + 2 * size_t(Lt::kVPB) * Lt::kStride * sizeof(float2) +
-                      size_t(Lt::kVPB) * Lt::kWPV * (sizeof(double) + 3 * sizeof(float));
-  SKB_CUDA(cudaFuncSetAttribute(power_kernel<QP, TPR>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const size_t tile = size_t(std::max(h, L::QP)) * L::kVPB * sizeof(float2);
+  const size_t smem = 2 * tile + 2 * size_t(L::kVPB) * L::kStride * sizeof(float2) +
+                      size_t(L::kVPB) * L::kWPV * (sizeof(double) + 3 * sizeof(float));
+  SKB_CUDA(cudaFuncSetAttribute(power_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   int per_sm = 0;
-  SKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_kernel<QP, TPR>, Lt::kThreads, smem));
-  const i64 tiles = (a.n + Lt::kVPB - 1) / Lt::kVPB;
+  SKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_kernel<L>, L::kThreads, smem));
+  const i64 tiles = (a.n + L::kVPB - 1) / L::kVPB;
   const i64 blocks = std::min<i64>(tiles, i64(std::max(per_sm, 1)) * ctx->sm_count);
-  power_kernel<QP, TPR><<<unsigned(blocks), Lt::kThreads, smem, ctx->stream>>>(a);
+  power_kernel<L><<<unsigned(blocks), L::kThreads, smem, ctx->stream>>>(a);
   ++ctx->launches;
   SKB_LAUNCH("power_kernel");
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
 }
 
 }  // namespace
 
 void power_iteration(sk_ctx* ctx, const PowerArgs& a) {
   if (a.n <= 0) return;
-  // Row split (threads per matrix row) per size class; SKB_POWER_TPR32 /
-  // SKB_POWER_TPR64 select the alternative layout for experiments.
-  static const int tpr32 = [] {
-    const char* v = std::getenv("SKB_POWER_TPR32");
-    return v && std::atoi(v) == 2 ? 2 : 1;
-  }();
-  static const int tpr64 = [] {
-    const char* v = std::getenv("SKB_POWER_TPR64");
-    return v && std::atoi(v) == 2 ? 2 : 1;
-  }();
+  // Rows per thread for Q in (16, 32]; SKB_POWER_RPT32=2 selects the
+  // two-row layout (measured equal with FFMA2, but it spills).
+  static const int rpt32 = env_int("SKB_POWER_RPT32", 1);
   if (a.q <= 4)
-    launch<4, 1>(ctx, a);
+    launch<Layout<4, 1, 256, 2>>(ctx, a);
   else if (a.q <= 8)
-    launch<8, 1>(ctx, a);
+    launch<Layout<8, 1, 256, 2>>(ctx, a);
   else if (a.q <= 16)
-    launch<16, 1>(ctx, a);
+    launch<Layout<16, 1, 256, 2>>(ctx, a);
   else if (a.q <= 32)
-    tpr32 == 2 ? launch<32, 2>(ctx, a) : launch<32, 1>(ctx, a);
+    rpt32 == 1 ? launch<Layout<32, 1, 256, 2>>(ctx, a) : launch<Layout<32, 2, 128, 3>>(ctx, a);
   else if (a.q <= 64)
-    tpr64 == 2 ? launch<64, 2>(ctx, a) : launch<64, 1>(ctx, a);
+    launch<Layout<64, 1, 256, 1>>(ctx, a);
   else
     fail(9, "eig_power_field: more than 64 channels is outside the B200 path");
 }

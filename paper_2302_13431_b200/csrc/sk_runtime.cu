@@ -537,15 +537,17 @@ constexpr i64 kSmallBlockMax = 112;  // custom one-CTA Cholesky limit (shared me
 // eigenvalues ascending into w, eigenvectors overwrite H.  Default: cuSOLVER
 // Jacobi (ZHEEVJ, tol 1e-14); SKB_SMALL_EIG=dc / batched select
 // divide-and-conquer (Xsyevd) / XsyevBatched for comparison.
-void small_heev(sk_ctx* ctx, double2* H, i64 b, double* w, int* d_info) {
+void small_heev(sk_ctx* ctx, double2* H, i64 b, double* w, int* d_info, double floor_rel = 0.0) {
   static const int mode = [] {
     const char* v = std::getenv("SKB_SMALL_EIG");
-    if (!v) return 1;  // default: cuSOLVER Jacobi (fastest measured at b ~ 96)
+    if (!v) return 3;  // default: own one-CTA solver for b <= 64, cuSOLVER Jacobi above
     if (std::string(v) == "dc") return 0;
+    if (std::string(v) == "jacobi") return 1;
     if (std::string(v) == "batched") return 2;
-    return 1;
+    return 3;
   }();
-  const bool jacobi = mode == 1;
+  if (mode == 3 && herm_eig_small(ctx, H, int(b), w, d_info, floor_rel)) return;
+  const bool jacobi = mode == 1 || mode == 3;
   if (mode == 2) {
     size_t dbytes = 0, hbytes = 0;
     check_cusolver(cusolverDnXsyevBatched_bufferSize(ctx->cusolver, ctx->cusolver_params, CUSOLVER_EIG_MODE_VECTOR,
@@ -647,12 +649,44 @@ bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int 
   return true;
 }
 
+// Development aid (SKB_PROFILE_NS=1): event laps inside the subspace solver,
+// summed per phase label and printed to stderr when the solver returns.
+struct PhaseLaps {
+  sk_ctx* ctx;
+  bool on;
+  std::vector<std::pair<std::string, cudaEvent_t>> ev;
+  explicit PhaseLaps(sk_ctx* c) : ctx(c), on(std::getenv("SKB_PROFILE_NS") != nullptr) { lap("start"); }
+  void lap(const char* label) {
+    if (!on) return;
+    cudaEvent_t e;
+    SKB_CUDA(cudaEventCreate(&e));
+    SKB_CUDA(cudaEventRecord(e, ctx->stream));
+    ev.emplace_back(label, e);
+  }
+  ~PhaseLaps() {
+    if (!on) return;
+    cudaEventSynchronize(ev.back().second);
+    std::map<std::string, std::pair<double, int>> sum;
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+      auto& s = sum[ev[i].first];
+      s.first += ms;
+      s.second += 1;
+    }
+    for (auto& kv : sum) std::fprintf(stderr, "[ns] %-10s %8.3f ms  %3dx\n", kv.first.c_str(), kv.second.first, kv.second.second);
+    for (auto& p : ev) cudaEventDestroy(p.second);
+  }
+};
+
 bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, bool certify, Eig& e) {
+  PhaseLaps laps(ctx);
   e = Eig();
   e.n = n;
   e.full = false;
   double2* A = ctx->arena.get<double2>("eig:A", n * n);
   c64_to_c128(ctx, gram, A, n * n);
+  laps.lap("promote");
   // Per-size hints from the previous call: block size and the number of
   // orthogonalised iterations before the (single) Rayleigh-Ritz check.
   auto& hint = ctx->subspace_hint;
@@ -686,7 +720,9 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   int* flag = d_info + 1;
   SKB_CUDA(cudaMemsetAsync(d_info, 0, 3 * sizeof(int), ctx->stream));
   random_block(ctx, V, n, b, 0, 0x5eed5u);
+  laps.lap("misc");
   if (!orth(ctx, V, T, n, b, flag)) return false;
+  laps.lap("orth");
   const double tol = 3e-10;
   const int maxit = 80;
   const i64 guard = 8;
@@ -705,22 +741,34 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
         float2* Y32 = ctx->arena.get<float2>("ss:Y32", n * bcap);
         c128_to_c64(ctx, V, V32, n * b);
         const cuComplex one = make_cuComplex(1.f, 0.f), zero = make_cuComplex(0.f, 0.f);
-        check_cublas(cublasCgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(n), int(b), int(n), &one,
-                                 reinterpret_cast<const cuComplex*>(gram), int(n),
-                                 reinterpret_cast<const cuComplex*>(V32), int(n), &zero,
-                                 reinterpret_cast<cuComplex*>(Y32), int(n)),
-                     "Cgemm(subspace)");
+        // FP32 (SKB_EARLY_GEMM=tf32 / bf16 select tensor-core modes; measured to
+        // need ~2x the iterations: the wanted subspace reaches down to
+        // ratio^2 * lambda_1, below their rounding relative to lambda_1).
+        static const cublasComputeType_t early = [] {
+          const char* v = std::getenv("SKB_EARLY_GEMM");
+          if (v && std::string(v) == "tf32") return CUBLAS_COMPUTE_32F_FAST_TF32;
+          if (v && std::string(v) == "bf16") return CUBLAS_COMPUTE_32F_FAST_16BF;
+          return CUBLAS_COMPUTE_32F;
+        }();
+        check_cublas(cublasGemmEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(n), int(b), int(n), &one, gram,
+                                  CUDA_C_32F, int(n), V32, CUDA_C_32F, int(n), &zero, Y32, CUDA_C_32F, int(n), early,
+                                  CUBLAS_GEMM_DEFAULT),
+                     "GemmEx(subspace)");
         ++ctx->lib_calls;
         c64_to_c128(ctx, Y32, Y, n * b);
+        laps.lap("gemm32");
       } else {
         zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);  // Y = A V
+        laps.lap("gemm64");
       }
       std::swap(V, Y);
       // Only the span matters between Rayleigh-Ritz steps: one CholQR pass
       // (orthogonality ~ kappa^2 eps) except before the projection.
       if (!orth(ctx, V, T, n, b, flag, i + 1 == q_plan ? 2 : 1)) return false;
+      laps.lap("orth");
     }
     zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);
+    laps.lap("gemm64");
     ++iters;
     // Rayleigh-Ritz on span(V): H = V^H A V = S diag(w) S^H.
     if (b <= 256) {
@@ -728,17 +776,23 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
     } else {
       zgemm(ctx, CUBLAS_OP_C, CUBLAS_OP_N, b, b, n, V, n, Y, n, H, b);
     }
-    small_heev(ctx, H, b, w, d_info);
+    laps.lap("rr_gram");
+    // Ritz pairs below cut^2 / 2 are never used individually (the residual
+    // test and the split both start there): a floor of cut^2 / 4 is safe.
+    small_heev(ctx, H, b, w, d_info, 0.25 * ratio * ratio);
+    laps.lap("rr_heev");
     zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, b, V, n, H, b, T, n);  // V <- V S
     std::swap(V, T);
     zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, b, Y, n, H, b, T, n);  // Y <- Y S
     std::swap(Y, T);
     ritz_residuals(ctx, Y, V, w, n, b, res);
+    laps.lap("rr_rotate");
     int hinfo[3] = {0, 0, 0};
     SKB_CUDA(cudaMemcpyAsync(hw.data(), w, size_t(b) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     SKB_CUDA(cudaMemcpyAsync(hres.data(), res, size_t(b) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     SKB_CUDA(cudaMemcpyAsync(hinfo, d_info, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+    laps.lap("sync");
     if (hinfo[0] != 0 || hinfo[1] != 0 || hinfo[2] != 0) return false;  // syevd failure / rank-deficient block
     theta_max = hw[size_t(b - 1)];
     if (!(theta_max > 0.0)) return false;
@@ -808,6 +862,7 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   }
   double2* keep = ctx->arena.get<double2>("ss:U", n * m);
   SKB_CUDA(cudaMemcpyAsync(keep, U, size_t(n * m) * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+  laps.lap("finish");
   e.usig = keep;
   e.k = m;
   e.rank = n - m;
@@ -1373,6 +1428,25 @@ int sk_support_mask(sk_ctx* ctx, int64_t voxels, const float* lambda, double thr
     mask_kernel(ctx, d_l, voxels, float(thr), o.dev);
     o.finish(ctx);
     SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_debug_small_eigh(sk_ctx* ctx, int64_t n, double* h, double* w) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (n < 1 || n > 4096 || h == nullptr || w == nullptr) fail(SK_ERR_DIM, "sk_debug_small_eigh: bad arguments");
+    double2* dh = ctx->arena.get<double2>("dbg:h", n * n);
+    double* dw = ctx->arena.get<double>("dbg:w", n);
+    int* info = ctx->arena.get<int>("dbg:info", 1);
+    SKB_CUDA(cudaMemsetAsync(info, 0, sizeof(int), ctx->stream));
+    SKB_CUDA(cudaMemcpyAsync(dh, h, size_t(n * n) * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    small_heev(ctx, dh, n, dw, info);
+    int hinfo = 0;
+    SKB_CUDA(cudaMemcpyAsync(h, dh, size_t(n * n) * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    SKB_CUDA(cudaMemcpyAsync(w, dw, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    SKB_CUDA(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hinfo != 0) fail(SK_ERR_OTHER, "sk_debug_small_eigh: solver reported failure");
   });
 }
 

@@ -80,6 +80,48 @@ def test_nullspace_known_answers(K):  # test_nullspace.cpp:22-43
             K.extract_nullspace(np.eye(2, dtype=np.complex64), r)
 
 
+def _hermitian_with_spectrum(n, lam, seed):
+    q = rnd_orthonormal(n, n, seed)
+    h = (q * np.asarray(lam, dtype=np.float64)) @ q.conj().T
+    return 0.5 * (h + h.conj().T)
+
+
+@pytest.mark.parametrize("n,kind", [
+    (1, "random"), (2, "random"), (7, "random"), (33, "ritz"), (48, "degenerate"), (64, "ritz"), (64, "degenerate"),
+    (64, "close"), (64, "random"), (96, "ritz"),
+])
+def test_small_eigh(K, n, kind):
+    """The K2 Rayleigh-Ritz eigensolver (one-CTA kernel for n <= 64, cuSOLVER
+    Jacobi above) against numpy.linalg.eigh, on spectra like the Ritz
+    matrices of the subspace solver: six decades of decay, exactly repeated
+    eigenvalues (symmetric coil rings) and near-degenerate pairs."""
+    r = np.random.default_rng(100 + n)
+    if kind == "random":
+        h = rnd((n, n), 200 + n, np.complex128)
+        h = 0.5 * (h + h.conj().T)
+    else:
+        lam = np.sort(10.0 ** r.uniform(-6, 0, n))[::-1] * 3.7
+        if kind == "degenerate":
+            lam[5:9] = lam[5]
+            lam[20:22] = lam[20]
+            lam[-6:] = 0.0
+        if kind == "close":
+            lam[10] = lam[11] * (1 + 1e-9)
+            lam[30] = lam[31] * (1 + 1e-6)
+        h = _hermitian_with_spectrum(n, lam, 300 + n)
+    w, x = K.api.small_eigh(h)
+    wr = np.linalg.eigvalsh(h)
+    nrm = np.abs(wr).max()
+    werr = np.abs(w - wr).max() / nrm
+    res = np.abs(h @ x - x * w).max() / nrm
+    orth = np.abs(x.conj().T @ x - np.eye(n)).max()
+    report("small_eigh", n=n, kind=kind, eig_err=float(werr), residual=float(res), orth=float(orth))
+    assert np.all(np.diff(w) >= -1e-12 * nrm)
+    assert werr < 1e-12
+    assert res < 1e-11
+    assert orth < 1e-10
+
+
 def test_nullspace_parity(K, O):
     cal = rnd((4, 24, 24), 7)
     st = cal.copy()
