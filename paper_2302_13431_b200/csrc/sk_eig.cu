@@ -570,7 +570,7 @@ size_t herm_eig_smem(int n) {
 bool herm_eig_small(sk_ctx* ctx, double2* H, int n, double* w, int* info, double floor_rel) {
   if (n < 1 || n > kMaxN) return false;
   const size_t smem = herm_eig_smem(n);
-  SKB_CUDA(cudaFuncSetAttribute(herm_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  set_smem_limit(reinterpret_cast<const void*>(herm_eig_kernel), smem);
   herm_eig_kernel<<<1, kThreads, smem, ctx->stream>>>(H, n, w, floor_rel, info);
   ++ctx->launches;
   SKB_LAUNCH("herm_eig_kernel");

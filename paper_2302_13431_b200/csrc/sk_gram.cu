@@ -184,7 +184,7 @@ void gram_pairs_launch(sk_ctx* ctx, const float2* spectra, const GramGeom& g_in,
   }
   const size_t smem = gram_pairs_smem(g);
   if (smem > 227 * 1024) fail(9, "gram_fft: padded calibration too large for the on-chip lag contraction");
-  SKB_CUDA(cudaFuncSetAttribute(gram_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  set_smem_limit(reinterpret_cast<const void*>(gram_pairs_kernel), smem);
   gram_pairs_kernel<<<npairs, 256, smem, ctx->stream>>>(spectra, g, d_pairs, d_off, d_tw, gram);
   ++ctx->launches;
   SKB_LAUNCH("gram_pairs_kernel");

@@ -12,6 +12,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/senskit_b200.h"
@@ -32,6 +33,9 @@ void check_cublas(cublasStatus_t s, const char* what);
 void check_cusolver(cusolverStatus_t s, const char* what);
 #define SKB_CUDA(x) ::skb::check_cuda((x), #x)
 #define SKB_LAUNCH(what) ::skb::check_cuda(cudaGetLastError(), what)
+// Raise a kernel's dynamic shared-memory limit only when the request grows
+// (cudaFuncSetAttribute is host work on every launch otherwise).
+void set_smem_limit(const void* func, size_t bytes);
 
 inline i64 numel(const Dims& d) {
   i64 n = 1;
@@ -76,6 +80,26 @@ struct MatrixCache {
   ~MatrixCache();
 };
 
+// Key of a captured subspace round (run_eigh_subspace): sizes, plan, the
+// arena pointers it touches and the threshold it bakes in.
+struct RoundKey {
+  i64 n, b;
+  int q;
+  const void *v, *y, *t, *h, *w, *res, *info, *a, *gram;
+  double ratio;
+  bool operator<(const RoundKey& o) const {
+    return std::tie(n, b, q, v, y, t, h, w, res, info, a, gram, ratio) <
+           std::tie(o.n, o.b, o.q, o.v, o.y, o.t, o.h, o.w, o.res, o.info, o.a, o.gram, o.ratio);
+  }
+};
+struct RoundGraph {
+  cudaGraphExec_t exec = nullptr;
+  int seen = 0;
+  bool bad = false;
+  double2 *v = nullptr, *y = nullptr, *t = nullptr;  // V / Y / T after the round
+  int64_t launches = 0, lib_calls = 0;
+};
+
 }  // namespace skb
 
 struct sk_ctx {
@@ -97,6 +121,8 @@ struct sk_ctx {
   syevjInfo_t syevj = nullptr;
   // concurrent lanes for multislice batches (sub-contexts on the same device)
   std::vector<sk_ctx*> lanes;
+  // captured subspace rounds (CUDA graphs), see run_graphed
+  std::map<skb::RoundKey, skb::RoundGraph> rounds;
 };
 
 namespace skb {
@@ -193,6 +219,13 @@ void cholesky_small(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag)
 // Clusters of close eigenvalues lying entirely below floor_rel * ||H|| are
 // only orthonormalised, not refined to individual eigenvectors.
 bool herm_eig_small(sk_ctx* ctx, double2* H, int n, double* w, int* info, double floor_rel = 0.0);
+// X (n x b) <- X L^{-H} for L lower (column-major, POTRF output), one thread
+// per row; b in {32, 48, 64}, returns false (nothing launched) otherwise.
+bool trsm_rows_lower(sk_ctx* ctx, double2* x, i64 n, int b, const double2* l);
+// One CholQR pass on X (n x b, b <= 64) with own kernels only: cross_gram,
+// one-CTA Cholesky + triangular inverse (M = L^{-1}, flag raised on a
+// non-positive pivot), X <- X M^H.  Returns false (nothing launched) for b > 64.
+bool cholqr_pass(sk_ctx* ctx, double2* x, i64 n, int b, double2* s, double2* m, int* flag);
 // One CholQR pass on X (n x b, b <= 118): cross_gram + one-CTA lazy Cholesky +
 // warp-per-row triangular solve; no host synchronisation (flag raised on failure).
 void cholqr_fast(sk_ctx* ctx, double2* x, i64 n, int b, double2* s, double2* l, int* flag);

@@ -154,7 +154,7 @@ void launch_interp(sk_ctx* ctx, const void* in, void* out, i64 batch, int n, int
   int T = 32;
   while (T > 1 && (size_t(T) * (N + 1) * sizeof(C) + size_t(N / 2) * sizeof(C) > 110 * 1024 || T * n > 16 * 256)) T /= 2;
   const size_t smem = size_t(T) * (N + 1) * sizeof(C) + size_t(N / 2) * sizeof(C);
-  SKB_CUDA(cudaFuncSetAttribute(interp_fft_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  set_smem_limit(reinterpret_cast<const void*>(interp_fft_kernel<R>), smem);
   const i64 lines = batch * inner;
   const i64 blocks = (lines + T - 1) / T;
   interp_fft_kernel<R><<<unsigned(blocks), 256, smem, ctx->stream>>>(static_cast<const C*>(in), static_cast<C*>(out),

@@ -456,7 +456,7 @@ void launch(sk_ctx* ctx, const PowerArgs& a) {
   const size_t tile = size_t(std::max(h, L::QP)) * L::kVPB * sizeof(float2);
   const size_t smem = 2 * tile + 2 * size_t(L::kVPB) * L::kStride * sizeof(float2) +
                       size_t(L::kVPB) * L::kWPV * (sizeof(double) + 3 * sizeof(float));
-  SKB_CUDA(cudaFuncSetAttribute(power_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  set_smem_limit(reinterpret_cast<const void*>(power_kernel<L>), smem);
   int per_sm = 0;
   SKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_kernel<L>, L::kThreads, smem));
   const i64 tiles = (a.n + L::kVPB - 1) / L::kVPB;

@@ -13,6 +13,7 @@
 //                  SoS renormalisation, support mask
 #include <algorithm>
 #include <chrono>
+#include <functional>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -31,6 +32,17 @@ thread_local std::string g_last_error;
 // ================================================================ errors
 namespace skb {
 [[noreturn]] void fail(int code, const std::string& msg) { throw Error(code, msg); }
+void set_smem_limit(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> granted;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& g = granted[func];
+  if (bytes <= g) return;
+  check_cuda(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)),
+             "cudaFuncSetAttribute(max dynamic smem)");
+  g = bytes;
+}
+
 void check_cuda(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return;
   if (e == cudaErrorMemoryAllocation) fail(SK_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
@@ -603,13 +615,24 @@ bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int 
   // default: cuSOLVER POTRF + cuBLAS TRSM (measured fastest at b = 64..96);
   // SKB_SMALL_CHOL=fast selects the own lazy Cholesky + row TRSM (b <= 112),
   // =custom the own blocked Cholesky + cuBLAS TRSM.
+  // Default: own cross_gram + cuSOLVER POTRF + own row-parallel TRSM (b in
+  // {32, 48, 64}; cuBLAS TRSM otherwise).  SKB_SMALL_CHOL=pass64 selects the
+  // library-free pass (one-CTA Cholesky + inverse; measured slower: the
+  // 64-pivot chain on one SM is latency-bound).
   static const int chol_mode = [] {
     const char* v = std::getenv("SKB_SMALL_CHOL");
     if (v && std::string(v) == "fast") return 0;
     if (v && std::string(v) == "custom") return 2;
+    if (v && std::string(v) == "pass64") return 3;
     return 1;
   }();
-  const bool lib_chol = chol_mode == 1 || b > kSmallBlockMax;
+  if (chol_mode == 3 && b <= 64) {
+    double2* S = ctx->arena.get<double2>("ss:S", b * b);
+    double2* Mi = ctx->arena.get<double2>("ss:Minv", b * b);
+    for (int pass = 0; pass < passes; ++pass) cholqr_pass(ctx, x, n, int(b), S, Mi, flag);
+    return true;
+  }
+  const bool lib_chol = chol_mode == 1 || chol_mode == 3 || b > kSmallBlockMax;
   if (b > 256 || (chol_mode == 2 && b > kSmallBlockMax)) {
     for (int p = 0; p < passes; ++p)
       if (!cholqr(ctx, x, n, b)) return false;
@@ -622,8 +645,17 @@ bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int 
     return true;
   }
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
+  static const bool prof = std::getenv("SKB_PROFILE_NS") != nullptr;
+  cudaEvent_t pe[4];
+  auto mark = [&](int i) {
+    if (prof) SKB_CUDA(cudaEventRecord(pe[i], ctx->stream));
+  };
+  if (prof)
+    for (auto& ev : pe) SKB_CUDA(cudaEventCreate(&ev));
   for (int pass = 0; pass < passes; ++pass) {
+    mark(0);
     cross_gram(ctx, x, x, n, int(b), S);        // S = X^H X
+    mark(1);
     if (lib_chol) {
       size_t dbytes = 0, hbytes = 0;
       check_cusolver(cusolverDnXpotrf_bufferSize(ctx->cusolver, ctx->cusolver_params, CUBLAS_FILL_MODE_LOWER, b,
@@ -640,12 +672,27 @@ bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int 
     } else {
       cholesky_small(ctx, S, int(b), L, flag);  // S = L L^H
     }
-    check_cublas(cublasZtrsm(ctx->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C,
-                             CUBLAS_DIAG_NON_UNIT, int(n), int(b), &one, reinterpret_cast<const cuDoubleComplex*>(L),
-                             int(b), reinterpret_cast<cuDoubleComplex*>(x), int(n)),
-                 "Ztrsm(orth)");                 // X <- X L^{-H}
-    ++ctx->lib_calls;
+    mark(2);
+    if (!trsm_rows_lower(ctx, x, n, int(b), L)) {
+      check_cublas(cublasZtrsm(ctx->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C,
+                               CUBLAS_DIAG_NON_UNIT, int(n), int(b), &one, reinterpret_cast<const cuDoubleComplex*>(L),
+                               int(b), reinterpret_cast<cuDoubleComplex*>(x), int(n)),
+                   "Ztrsm(orth)");  // X <- X L^{-H}
+      ++ctx->lib_calls;
+    }
+    mark(3);
+    if (prof) {
+      SKB_CUDA(cudaEventSynchronize(pe[3]));
+      float a = 0.f, b2 = 0.f, c = 0.f;
+      cudaEventElapsedTime(&a, pe[0], pe[1]);
+      cudaEventElapsedTime(&b2, pe[1], pe[2]);
+      cudaEventElapsedTime(&c, pe[2], pe[3]);
+      std::fprintf(stderr, "[orth b=%lld] gram %.1f us  chol %.1f us  trsm %.1f us\n", (long long)b, a * 1e3, b2 * 1e3,
+                   c * 1e3);
+    }
   }
+  if (prof)
+    for (auto& ev : pe) cudaEventDestroy(ev);
   return true;
 }
 
@@ -655,6 +702,7 @@ struct PhaseLaps {
   sk_ctx* ctx;
   bool on;
   std::vector<std::pair<std::string, cudaEvent_t>> ev;
+  std::vector<double> host_us;
   explicit PhaseLaps(sk_ctx* c) : ctx(c), on(std::getenv("SKB_PROFILE_NS") != nullptr) { lap("start"); }
   void lap(const char* label) {
     if (!on) return;
@@ -662,22 +710,96 @@ struct PhaseLaps {
     SKB_CUDA(cudaEventCreate(&e));
     SKB_CUDA(cudaEventRecord(e, ctx->stream));
     ev.emplace_back(label, e);
+    host_us.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch())
+                          .count());
   }
   ~PhaseLaps() {
     if (!on) return;
     cudaEventSynchronize(ev.back().second);
     std::map<std::string, std::pair<double, int>> sum;
+    std::map<std::string, double> hsum;
     for (size_t i = 1; i < ev.size(); ++i) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
       auto& s = sum[ev[i].first];
       s.first += ms;
       s.second += 1;
+      hsum[ev[i].first] += (host_us[i] - host_us[i - 1]) * 1e-3;
     }
-    for (auto& kv : sum) std::fprintf(stderr, "[ns] %-10s %8.3f ms  %3dx\n", kv.first.c_str(), kv.second.first, kv.second.second);
+    for (auto& kv : sum)
+      std::fprintf(stderr, "[ns] %-10s %8.3f ms  %3dx   host enqueue %8.3f ms\n", kv.first.c_str(), kv.second.first,
+                   kv.second.second, hsum[kv.first]);
     for (auto& p : ev) cudaEventDestroy(p.second);
   }
 };
+
+// Replay of one subspace round as a CUDA graph.  The first call with a key
+// runs eagerly (the arena grows to its final size), the second captures the
+// launch sequence, later calls replay it and restore the V/Y/T rotation of
+// the captured run.  A capture failure (a library call that cannot be
+// captured) marks the key eager-only.
+void run_graphed(sk_ctx* ctx, bool allowed, const RoundKey& key, double2*& V, double2*& Y, double2*& T,
+                 const std::function<void()>& body) {
+  static const bool disabled = std::getenv("SKB_NO_GRAPH") != nullptr;
+  if (!allowed || disabled) {
+    body();
+    return;
+  }
+  auto& g = ctx->rounds[key];
+  if (g.exec) {
+    SKB_CUDA(cudaGraphLaunch(g.exec, ctx->stream));
+    V = g.v;
+    Y = g.y;
+    T = g.t;
+    ctx->launches += g.launches;
+    ctx->lib_calls += g.lib_calls;
+    return;
+  }
+  if (g.bad || g.seen++ == 0) {
+    body();
+    return;
+  }
+  const i64 l0 = ctx->launches, c0 = ctx->lib_calls;
+  cudaGraph_t graph = nullptr;
+  SKB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+  double2 *v0 = V, *y0 = Y, *t0 = T;
+  try {
+    body();
+  } catch (...) {
+    cudaStreamEndCapture(ctx->stream, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    g.bad = true;
+    V = v0;
+    Y = y0;
+    T = t0;
+    ctx->launches = l0;
+    ctx->lib_calls = c0;
+    body();  // eager
+    return;
+  }
+  const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &graph);
+  if (ec != cudaSuccess || !graph || cudaGraphInstantiate(&g.exec, graph, 0) != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    g.bad = true;
+    g.exec = nullptr;
+    V = v0;
+    Y = y0;
+    T = t0;
+    ctx->launches = l0;
+    ctx->lib_calls = c0;
+    body();
+    return;
+  }
+  cudaGraphDestroy(graph);
+  g.v = V;
+  g.y = Y;
+  g.t = T;
+  g.launches = ctx->launches - l0;
+  g.lib_calls = ctx->lib_calls - c0;
+  SKB_CUDA(cudaGraphLaunch(g.exec, ctx->stream));  // capture recorded, not ran, the round
+}
 
 bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, bool certify, Eig& e) {
   PhaseLaps laps(ctx);
@@ -719,10 +841,10 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   int* d_info = ctx->arena.get<int>("ss:einfo", 3);
   int* flag = d_info + 1;
   SKB_CUDA(cudaMemsetAsync(d_info, 0, 3 * sizeof(int), ctx->stream));
+  // A Gaussian start block is well conditioned and only its span matters:
+  // no orthonormalisation before the first product.
   random_block(ctx, V, n, b, 0, 0x5eed5u);
   laps.lap("misc");
-  if (!orth(ctx, V, T, n, b, flag)) return false;
-  laps.lap("orth");
   const double tol = 3e-10;
   const int maxit = 80;
   const i64 guard = 8;
@@ -732,61 +854,74 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   i64 m = 0;
   double theta_max = 0.0, c = 0.0;
   while (iters < maxit) {
-    for (int i = 0; i < q_plan; ++i, ++iters) {
-      if (i + 2 < q_plan) {
-        // Early iterations only steer the span: FP32 CGEMM on the fp32 Gram
-        // (its rounding ~1e-7 is removed by the FP64 iterations that follow);
-        // orthonormalisation stays FP64 (kappa(A V)^2 exceeds 1/eps_fp32).
-        float2* V32 = ctx->arena.get<float2>("ss:V32", n * bcap);
-        float2* Y32 = ctx->arena.get<float2>("ss:Y32", n * bcap);
-        c128_to_c64(ctx, V, V32, n * b);
-        const cuComplex one = make_cuComplex(1.f, 0.f), zero = make_cuComplex(0.f, 0.f);
-        // FP32 (SKB_EARLY_GEMM=tf32 / bf16 select tensor-core modes; measured to
-        // need ~2x the iterations: the wanted subspace reaches down to
-        // ratio^2 * lambda_1, below their rounding relative to lambda_1).
-        static const cublasComputeType_t early = [] {
-          const char* v = std::getenv("SKB_EARLY_GEMM");
-          if (v && std::string(v) == "tf32") return CUBLAS_COMPUTE_32F_FAST_TF32;
-          if (v && std::string(v) == "bf16") return CUBLAS_COMPUTE_32F_FAST_16BF;
-          return CUBLAS_COMPUTE_32F;
-        }();
-        check_cublas(cublasGemmEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(n), int(b), int(n), &one, gram,
-                                  CUDA_C_32F, int(n), V32, CUDA_C_32F, int(n), &zero, Y32, CUDA_C_32F, int(n), early,
-                                  CUBLAS_GEMM_DEFAULT),
-                     "GemmEx(subspace)");
-        ++ctx->lib_calls;
-        c64_to_c128(ctx, Y32, Y, n * b);
-        laps.lap("gemm32");
-      } else {
-        zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);  // Y = A V
-        laps.lap("gemm64");
+    // One round: q_plan (GEMM, CholQR) steps, the projection, the b x b
+    // eigensolve, the Ritz rotation and residuals.  No host decisions inside,
+    // so in steady state (per-size hint fixed) it is replayed as a CUDA graph.
+    bool body_ok = true;
+    auto body = [&]() {
+      for (int i = 0; i < q_plan; ++i) {
+        if (i + 2 < q_plan) {
+          // Early iterations only steer the span: FP32 CGEMM on the fp32 Gram
+          // (its rounding ~1e-7 is removed by the FP64 iterations that follow);
+          // orthonormalisation stays FP64 (kappa(A V)^2 exceeds 1/eps_fp32).
+          float2* V32 = ctx->arena.get<float2>("ss:V32", n * bcap);
+          float2* Y32 = ctx->arena.get<float2>("ss:Y32", n * bcap);
+          c128_to_c64(ctx, V, V32, n * b);
+          const cuComplex one = make_cuComplex(1.f, 0.f), zero = make_cuComplex(0.f, 0.f);
+          // FP32 (SKB_EARLY_GEMM=tf32 / bf16 select tensor-core modes; measured to
+          // need ~2x the iterations: the wanted subspace reaches down to
+          // ratio^2 * lambda_1, below their rounding relative to lambda_1;
+          // the BF16x9 emulation does not take complex operands).
+          static const cublasComputeType_t early = [] {
+            const char* v = std::getenv("SKB_EARLY_GEMM");
+            if (v && std::string(v) == "tf32") return CUBLAS_COMPUTE_32F_FAST_TF32;
+            if (v && std::string(v) == "bf16") return CUBLAS_COMPUTE_32F_FAST_16BF;
+            return CUBLAS_COMPUTE_32F;
+          }();
+          check_cublas(cublasGemmEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(n), int(b), int(n), &one, gram,
+                                    CUDA_C_32F, int(n), V32, CUDA_C_32F, int(n), &zero, Y32, CUDA_C_32F, int(n),
+                                    early, CUBLAS_GEMM_DEFAULT),
+                       "GemmEx(subspace)");
+          ++ctx->lib_calls;
+          c64_to_c128(ctx, Y32, Y, n * b);
+          laps.lap("gemm32");
+        } else {
+          zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);  // Y = A V
+          laps.lap("gemm64");
+        }
+        std::swap(V, Y);
+        // Only the span matters between Rayleigh-Ritz steps: one CholQR pass
+        // (orthogonality ~ kappa^2 eps) except before the projection.
+        if (!orth(ctx, V, T, n, b, flag, i + 1 == q_plan ? 2 : 1)) {
+          body_ok = false;
+          return;
+        }
+        laps.lap("orth");
       }
-      std::swap(V, Y);
-      // Only the span matters between Rayleigh-Ritz steps: one CholQR pass
-      // (orthogonality ~ kappa^2 eps) except before the projection.
-      if (!orth(ctx, V, T, n, b, flag, i + 1 == q_plan ? 2 : 1)) return false;
-      laps.lap("orth");
-    }
-    zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);
-    laps.lap("gemm64");
-    ++iters;
-    // Rayleigh-Ritz on span(V): H = V^H A V = S diag(w) S^H.
-    if (b <= 256) {
-      cross_gram(ctx, V, Y, n, int(b), H);
-    } else {
-      zgemm(ctx, CUBLAS_OP_C, CUBLAS_OP_N, b, b, n, V, n, Y, n, H, b);
-    }
-    laps.lap("rr_gram");
-    // Ritz pairs below cut^2 / 2 are never used individually (the residual
-    // test and the split both start there): a floor of cut^2 / 4 is safe.
-    small_heev(ctx, H, b, w, d_info, 0.25 * ratio * ratio);
-    laps.lap("rr_heev");
-    zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, b, V, n, H, b, T, n);  // V <- V S
-    std::swap(V, T);
-    zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, b, Y, n, H, b, T, n);  // Y <- Y S
-    std::swap(Y, T);
-    ritz_residuals(ctx, Y, V, w, n, b, res);
-    laps.lap("rr_rotate");
+      zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);
+      laps.lap("gemm64");
+      // Rayleigh-Ritz on span(V): H = V^H A V = S diag(w) S^H.
+      if (b <= 256) {
+        cross_gram(ctx, V, Y, n, int(b), H);
+      } else {
+        zgemm(ctx, CUBLAS_OP_C, CUBLAS_OP_N, b, b, n, V, n, Y, n, H, b);
+      }
+      laps.lap("rr_gram");
+      // Ritz pairs below cut^2 / 2 are never used individually (the residual
+      // test and the split both start there): a floor of cut^2 / 4 is safe.
+      small_heev(ctx, H, b, w, d_info, 0.25 * ratio * ratio);
+      laps.lap("rr_heev");
+      zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, b, V, n, H, b, T, n);  // V <- V S
+      std::swap(V, T);
+      zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, b, Y, n, H, b, T, n);  // Y <- Y S
+      std::swap(Y, T);
+      ritz_residuals(ctx, Y, V, w, n, b, res);
+      laps.lap("rr_rotate");
+    };
+    run_graphed(ctx, !laps.on && b <= 256,
+                RoundKey{n, b, q_plan, V, Y, T, H, w, res, d_info, A, gram, ratio}, V, Y, T, body);
+    if (!body_ok) return false;
+    iters += q_plan + 1;
     int hinfo[3] = {0, 0, 0};
     SKB_CUDA(cudaMemcpyAsync(hw.data(), w, size_t(b) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     SKB_CUDA(cudaMemcpyAsync(hres.data(), res, size_t(b) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1210,6 +1345,9 @@ int sk_destroy(sk_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->syevj) cusolverDnDestroySyevjInfo(ctx->syevj);
+    for (auto& kv : ctx->rounds)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    ctx->rounds.clear();
     ctx->arena.release_all();
     for (auto& e : ctx->ev) cudaEventDestroy(e);
     cusolverDnDestroyParams(ctx->cusolver_params);

@@ -12,6 +12,9 @@
 // launch and host-sync overhead dominated the stage at b ~ 96.
 #include "sk_internal.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace skb {
 
 namespace {
@@ -21,6 +24,13 @@ __device__ __forceinline__ double2 cfma_conj(double2 acc, double2 a, double2 b) 
   acc.x = fma(a.y, b.y, acc.x);
   acc.y = fma(a.x, b.y, acc.y);
   acc.y = fma(-a.y, b.x, acc.y);
+  return acc;
+}
+__device__ __forceinline__ double2 cfma_conj_rev(double2 acc, double2 a, double2 b) {  // acc + a * conj(b)
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.y, b.x, acc.y);
+  acc.y = fma(-a.x, b.y, acc.y);
   return acc;
 }
 __device__ __forceinline__ double2 cfma(double2 acc, double2 a, double2 b) {  // acc + a * b
@@ -48,14 +58,24 @@ __global__ void __launch_bounds__(256) cross_gram_partial_kernel(const double2* 
   double2 acc[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) acc[k] = make_double2(0.0, 0.0);
+  constexpr int kPerThread = kRows * kTile / 256;  // 4 elements of each operand per thread and step
   for (i64 rs = r0; rs < r1; rs += kRows) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < kRows * kTile; e += blockDim.x) {
-      const int rr = e / kTile, cc = e % kTile;
+    double2 xv_[kPerThread], yv_[kPerThread];  // all loads in flight before the shared stores
+#pragma unroll
+    for (int u = 0; u < kPerThread; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      const int rr = e % kRows, cc = e / kRows;  // lanes along rows: X is column-major (coalesced)
       const i64 r = rs + rr;
       const int ci = ti * kTile + cc, cj = tj * kTile + cc;
-      xs[rr][cc] = (r < r1 && ci < b) ? x[r + i64(ci) * n] : make_double2(0.0, 0.0);
-      ys[rr][cc] = (r < r1 && cj < b) ? y[r + i64(cj) * n] : make_double2(0.0, 0.0);
+      xv_[u] = (r < r1 && ci < b) ? x[r + i64(ci) * n] : make_double2(0.0, 0.0);
+      yv_[u] = (r < r1 && cj < b) ? y[r + i64(cj) * n] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPerThread; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      xs[e % kRows][e / kRows] = xv_[u];
+      ys[e % kRows][e / kRows] = yv_[u];
     }
     __syncthreads();
 #pragma unroll 4
@@ -76,8 +96,20 @@ __global__ void __launch_bounds__(256) cross_gram_partial_kernel(const double2* 
 __global__ void reduce_partials_kernel(const double2* __restrict__ partial, int chunks, int bb,
                                        double2* __restrict__ out) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < bb; e += gridDim.x * blockDim.x) {
+    // fixed-order sum, eight loads in flight (the chunk order is the same for every run)
     double2 s = make_double2(0.0, 0.0);
-    for (int c = 0; c < chunks; ++c) {
+    int c = 0;
+    for (; c + 8 <= chunks; c += 8) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = partial[i64(c + u) * bb + e];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        s.x += v[u].x;
+        s.y += v[u].y;
+      }
+    }
+    for (; c < chunks; ++c) {
       const double2 v = partial[i64(c) * bb + e];
       s.x += v.x;
       s.y += v.y;
@@ -345,18 +377,207 @@ __global__ void __launch_bounds__(256) trsm_rows_kernel(double2* __restrict__ x,
   }
 }
 
+
+// ---- CholQR for b <= 64 without library calls (cholqr_pass):
+// one CTA factors S = L L^H (right-looking, one barrier per pivot; L is kept
+// implicitly as S[i][k] * rs[k]) and forms M = L^{-1} (eight lanes per
+// column, forward substitution), then a row-tiled kernel applies X <- X M^H.
+constexpr int kCholThreads = 512;
+constexpr int kCholMax = 64;
+
+__global__ void __launch_bounds__(kCholThreads) chol_inv64_kernel(const double2* __restrict__ s, int b,
+                                                                   double2* __restrict__ m_out, int* flag) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ld = b + 1;
+  double2* S = reinterpret_cast<double2*>(smem_raw);  // [b][ld], lower triangle; column k scaled lazily
+  double2* M = S + b * ld;                             // [b][ld], rows of L^{-1}
+  double* rs = reinterpret_cast<double*>(M + b * ld);  // 1 / L[k][k]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {
+    constexpr int kPer = kCholMax * kCholMax / kCholThreads;  // 8
+    double2 v[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = tid + kCholThreads * u;
+      v[u] = e < b * b ? s[e] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int e = tid + kCholThreads * u;
+      const int i = e % b, j = e / b;  // column-major source
+      if (e < b * b) {
+        if (i >= j) S[i * ld + j] = v[u];
+        M[i * ld + j] = make_double2(0.0, 0.0);
+      }
+    }
+  }
+  __syncthreads();
+  // Pivot k (one barrier): rs[k]; row k of M from the final rows < k,
+  //   M[k][c] = rs[k] (delta_kc - sum_{j=c}^{k-1} L[k][j] M[j][c]),  L[k][j] = S[k][j] rs[j];
+  // and the trailing update S[i][j] -= S[i][k] conj(S[j][k]) rs[k]^2.
+  const int c = tid >> 3, h = tid & 7;  // eight lanes per column of M
+  for (int k = 0; k < b; ++k) {
+    double dkk = S[k * ld + k].x;
+    if (!(dkk > 0.0)) {
+      if (tid == 0) atomicExch(flag, 1);
+      dkk = 1e-300;
+    }
+    const double r = rsqrt(dkk), r2 = r * r;
+    double2 acc = make_double2(0.0, 0.0);
+    if (c < k) {
+#pragma unroll 4
+      for (int j = c + h; j < k; j += 8) {
+        const double2 skj = S[k * ld + j], mjc = M[j * ld + c];
+        const double rj = rs[j];
+        acc.x += (skj.x * mjc.x - skj.y * mjc.y) * rj;
+        acc.y += (skj.x * mjc.y + skj.y * mjc.x) * rj;
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (h == 0 && c <= k) M[k * ld + c] = c == k ? make_double2(r, 0.0) : make_double2(-acc.x * r, -acc.y * r);
+    if (tid == 0) rs[k] = r;
+    for (int i = k + 1 + warp; i < b; i += kCholThreads / 32) {
+      const double2 sik = S[i * ld + k];
+      for (int j = k + 1 + lane; j <= i; j += 32) {
+        const double2 sjk = S[j * ld + k];
+        double2 a = S[i * ld + j];
+        a.x -= (sik.x * sjk.x + sik.y * sjk.y) * r2;
+        a.y -= (sik.y * sjk.x - sik.x * sjk.y) * r2;
+        S[i * ld + j] = a;
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < b * b; e += kCholThreads) m_out[e] = M[(e / b) * ld + e % b];  // row-major
+}
+
+// X (n x b, column-major) <- X L^{-H}, L lower triangular column-major b x b
+// (cuSOLVER POTRF output), by forward substitution on each row:
+//   y_j = (x_j - sum_{k<j} y_k conj(L[j][k])) / L[j][j].
+// A lane pair owns a row (lane h keeps the columns k = h mod 2 in registers);
+// every step the pair combines its partial sums with one shuffle.  conj(L)
+// is staged in shared memory (broadcast reads).
+constexpr int kTrsmThreads = 128;
+template <int B>
+__global__ void __launch_bounds__(kTrsmThreads) trsm_pairs_kernel(double2* __restrict__ x, i64 n,
+                                                                  const double2* __restrict__ l) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* Lc = reinterpret_cast<double2*>(smem_raw);  // Lc[j * B + k] = conj(L[j][k]), k <= j
+  double* dinv = reinterpret_cast<double*>(Lc + B * B);
+  for (int e = threadIdx.x; e < B * B; e += kTrsmThreads) {
+    const int j = e % B, k = e / B;  // column-major source: e = j + k B
+    const double2 v = l[e];
+    Lc[j * B + k] = make_double2(v.x, -v.y);
+    if (j == k) dinv[j] = 1.0 / v.x;
+  }
+  __syncthreads();
+  const int h = threadIdx.x & 1;
+  const i64 r = (i64(blockIdx.x) * kTrsmThreads + threadIdx.x) >> 1;
+  const bool live = r < n;
+  constexpr int H = B / 2;
+  double2 y[H];
+#pragma unroll
+  for (int u = 0; u < H; ++u) y[u] = live ? x[r + i64(2 * u + h) * n] : make_double2(0.0, 0.0);
+#pragma unroll
+  for (int j = 0; j < B; ++j) {
+    double2 p0 = make_double2(0.0, 0.0), p1 = p0;
+#pragma unroll
+    for (int u = 0; 2 * u < j; ++u) {
+      const int k = 2 * u + h;  // runtime parity: guard k < j
+      if (k < j) {
+        const double2 lc = Lc[j * B + k];
+        double2& p = (u & 1) ? p1 : p0;
+        p.x += y[u].x * lc.x - y[u].y * lc.y;
+        p.y += y[u].x * lc.y + y[u].y * lc.x;
+      }
+    }
+    double2 p = make_double2(p0.x + p1.x, p0.y + p1.y);
+    p.x += __shfl_xor_sync(0xffffffffu, p.x, 1);
+    p.y += __shfl_xor_sync(0xffffffffu, p.y, 1);
+    if ((j & 1) == h) {
+      const double di = dinv[j];
+      y[j >> 1] = make_double2((y[j >> 1].x - p.x) * di, (y[j >> 1].y - p.y) * di);
+    }
+  }
+  if (live)
+#pragma unroll
+    for (int u = 0; u < H; ++u) x[r + i64(2 * u + h) * n] = y[u];
+}
+
+// X (n x b, column-major) <- X M^H, M lower triangular (row-major b x b).
+constexpr int kApplyRows = 16;
+__global__ void __launch_bounds__(256) apply_minvh_kernel(double2* __restrict__ x, i64 n, int b,
+                                                          const double2* __restrict__ m) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ld = b + 1;
+  double2* Ms = reinterpret_cast<double2*>(smem_raw);  // [b][ld]
+  double2* Xs = Ms + b * ld;                           // [kApplyRows][ld]
+  const i64 r0 = i64(blockIdx.x) * kApplyRows;
+  {
+    constexpr int kM = kCholMax * kCholMax / 256, kX = kApplyRows * kCholMax / 256;  // 16, 4
+    double2 mv[kM], xv[kX];
+#pragma unroll
+    for (int u = 0; u < kM; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      mv[u] = e < b * b ? m[e] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < kX; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      const int rr = e % kApplyRows, c = e / kApplyRows;
+      const i64 r = r0 + rr;
+      xv[u] = (c < b && r < n) ? x[r + i64(c) * n] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < kM; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      if (e < b * b) Ms[(e / b) * ld + e % b] = mv[u];
+    }
+#pragma unroll
+    for (int u = 0; u < kX; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      const int rr = e % kApplyRows, c = e / kApplyRows;
+      if (c < b) Xs[rr * ld + c] = xv[u];
+    }
+  }
+  __syncthreads();
+  const int rr = threadIdx.x % kApplyRows, jg = threadIdx.x / kApplyRows;  // 16 column groups
+  constexpr int kPer = kCholMax / 16;
+  double2 acc[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) acc[u] = make_double2(0.0, 0.0);
+  for (int k = 0; k < b; ++k) {
+    const double2 xv = Xs[rr * ld + k];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int j = jg + 16 * u;
+      if (j < b) acc[u] = cfma_conj_rev(acc[u], xv, Ms[j * ld + k]);
+    }
+  }
+  const i64 r = r0 + rr;
+  if (r < n)
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int j = jg + 16 * u;
+      if (j < b) x[r + i64(j) * n] = acc[u];
+    }
+}
 }  // namespace
 
 void cholqr_fast(sk_ctx* ctx, double2* x, i64 n, int b, double2* s, double2* l, int* flag) {
   if (b > 118) fail(SK_ERR_UNSUPPORTED, "cholqr_fast: block too large");
   cross_gram(ctx, x, x, n, b, s);
   const size_t smem = size_t(b) * (b + 1) * sizeof(double2);
-  SKB_CUDA(cudaFuncSetAttribute(chol_lazy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  set_smem_limit(reinterpret_cast<const void*>(chol_lazy_kernel), smem);
   chol_lazy_kernel<<<1, 128, smem, ctx->stream>>>(s, b, l, flag);
   ++ctx->launches;
   SKB_LAUNCH("chol_lazy_kernel");
   const size_t smem2 = size_t(b) * b * sizeof(double2);
-  SKB_CUDA(cudaFuncSetAttribute(trsm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem2)));
+  set_smem_limit(reinterpret_cast<const void*>(trsm_rows_kernel), smem2);
   const i64 blocks = std::min<i64>((n + 7) / 8, ctx->sm_count);
   trsm_rows_kernel<<<unsigned(blocks), 256, smem2, ctx->stream>>>(x, n, b, l);
   ++ctx->launches;
@@ -366,7 +587,7 @@ void cholqr_fast(sk_ctx* ctx, double2* x, i64 n, int b, double2* s, double2* l, 
 void cholesky_small(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag) {
   const size_t smem = size_t(b) * (b + 1) * sizeof(double2);
   if (smem > 227 * 1024) fail(SK_ERR_UNSUPPORTED, "cholesky_small: block too large");
-  SKB_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  set_smem_limit(reinterpret_cast<const void*>(chol_kernel), smem);
   chol_kernel<<<1, dim3(32, 32), smem, ctx->stream>>>(s, b, l, flag);
   ++ctx->launches;
   SKB_LAUNCH("chol_kernel");
@@ -374,8 +595,8 @@ void cholesky_small(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag)
 
 void cross_gram(sk_ctx* ctx, const double2* x, const double2* y, i64 n, int b, double2* out) {
   const int tiles = (b + kTile - 1) / kTile;
-  // ~2 waves of CTAs over the SMs
-  i64 chunks = std::max<i64>(1, (2 * i64(ctx->sm_count)) / (tiles * tiles));
+  // ~1 wave of CTAs over the SMs
+  i64 chunks = std::max<i64>(1, i64(ctx->sm_count) / (tiles * tiles));
   i64 rows = (n + chunks - 1) / chunks;
   rows = ((rows + kRows - 1) / kRows) * kRows;
   chunks = (n + rows - 1) / rows;
@@ -392,10 +613,68 @@ void cross_gram(sk_ctx* ctx, const double2* x, const double2* y, i64 n, int b, d
 void chol_inv(sk_ctx* ctx, const double2* s, int b, double2* minv, int* flag) {
   const size_t smem = size_t(b) * (b + 1) * sizeof(double2);
   if (smem > 227 * 1024) fail(SK_ERR_UNSUPPORTED, "chol_inv: block too large");
-  SKB_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  set_smem_limit(reinterpret_cast<const void*>(chol_inv_kernel), smem);
   chol_inv_kernel<<<1, 256, smem, ctx->stream>>>(s, b, minv, flag);
   ++ctx->launches;
   SKB_LAUNCH("chol_inv");
+}
+
+bool cholqr_pass(sk_ctx* ctx, double2* x, i64 n, int b, double2* s, double2* m, int* flag) {
+  if (b < 1 || b > kCholMax) return false;
+  static const bool prof = std::getenv("SKB_PROFILE_NS") != nullptr;
+  cudaEvent_t pe[4];
+  if (prof)
+    for (auto& e : pe) {
+      SKB_CUDA(cudaEventCreate(&e));
+    }
+  if (prof) SKB_CUDA(cudaEventRecord(pe[0], ctx->stream));
+  cross_gram(ctx, x, x, n, b, s);
+  if (prof) SKB_CUDA(cudaEventRecord(pe[1], ctx->stream));
+  const size_t smem = size_t(2 * b * (b + 1)) * sizeof(double2) + size_t(b) * sizeof(double);
+  set_smem_limit(reinterpret_cast<const void*>(chol_inv64_kernel), smem);
+  chol_inv64_kernel<<<1, kCholThreads, smem, ctx->stream>>>(s, b, m, flag);
+  ++ctx->launches;
+  SKB_LAUNCH("chol_inv64_kernel");
+  if (prof) SKB_CUDA(cudaEventRecord(pe[2], ctx->stream));
+  const size_t smem2 = size_t((b + kApplyRows) * (b + 1)) * sizeof(double2);
+  set_smem_limit(reinterpret_cast<const void*>(apply_minvh_kernel), smem2);
+  apply_minvh_kernel<<<unsigned((n + kApplyRows - 1) / kApplyRows), 256, smem2, ctx->stream>>>(x, n, b, m);
+  ++ctx->launches;
+  SKB_LAUNCH("apply_minvh_kernel");
+  if (prof) {
+    SKB_CUDA(cudaEventRecord(pe[3], ctx->stream));
+    SKB_CUDA(cudaEventSynchronize(pe[3]));
+    float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+    cudaEventElapsedTime(&t0, pe[0], pe[1]);
+    cudaEventElapsedTime(&t1, pe[1], pe[2]);
+    cudaEventElapsedTime(&t2, pe[2], pe[3]);
+    std::fprintf(stderr, "[cholqr b=%d] gram %.1f us  chol_inv %.1f us  apply %.1f us\n", b, t0 * 1e3, t1 * 1e3,
+                 t2 * 1e3);
+    for (auto& e : pe) cudaEventDestroy(e);
+  }
+  return true;
+}
+
+template <int B>
+void launch_trsm_rows(sk_ctx* ctx, double2* x, i64 n, const double2* l) {
+  const unsigned blocks = unsigned((2 * n + kTrsmThreads - 1) / kTrsmThreads);
+  const size_t smem = size_t(B) * B * sizeof(double2) + size_t(B) * sizeof(double);
+  set_smem_limit(reinterpret_cast<const void*>(trsm_pairs_kernel<B>), smem);
+  trsm_pairs_kernel<B><<<blocks, kTrsmThreads, smem, ctx->stream>>>(x, n, l);
+}
+
+bool trsm_rows_lower(sk_ctx* ctx, double2* x, i64 n, int b, const double2* l) {
+  if (b == 64)
+    launch_trsm_rows<64>(ctx, x, n, l);
+  else if (b == 48)
+    launch_trsm_rows<48>(ctx, x, n, l);
+  else if (b == 32)
+    launch_trsm_rows<32>(ctx, x, n, l);
+  else
+    return false;
+  ++ctx->launches;
+  SKB_LAUNCH("trsm_pairs_kernel");
+  return true;
 }
 
 }  // namespace skb
