@@ -615,8 +615,7 @@ bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int 
   // default: cuSOLVER POTRF + cuBLAS TRSM (measured fastest at b = 64..96);
   // SKB_SMALL_CHOL=fast selects the own lazy Cholesky + row TRSM (b <= 112),
   // =custom the own blocked Cholesky + cuBLAS TRSM.
-  // Default: own cross_gram + cuSOLVER POTRF + own row-parallel TRSM (b in
-  // {32, 48, 64}; cuBLAS TRSM otherwise).  SKB_SMALL_CHOL=pass64 selects the
+  // Default: own cross_gram + cuSOLVER POTRF + cuBLAS TRSM.  SKB_SMALL_CHOL=pass64 selects the
   // library-free pass (one-CTA Cholesky + inverse; measured slower: the
   // 64-pivot chain on one SM is latency-bound).
   static const int chol_mode = [] {
@@ -673,7 +672,10 @@ bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int 
       cholesky_small(ctx, S, int(b), L, flag);  // S = L L^H
     }
     mark(2);
-    if (!trsm_rows_lower(ctx, x, n, int(b), L)) {
+    // cuBLAS TRSM (measured faster on the device than the own lane-pair
+    // kernel once graphs hide its host cost); SKB_TRSM_OWN=1 selects the latter.
+    static const bool own_trsm = std::getenv("SKB_TRSM_OWN") != nullptr;
+    if (!own_trsm || !trsm_rows_lower(ctx, x, n, int(b), L)) {
       check_cublas(cublasZtrsm(ctx->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C,
                                CUBLAS_DIAG_NON_UNIT, int(n), int(b), &one, reinterpret_cast<const cuDoubleComplex*>(L),
                                int(b), reinterpret_cast<cuDoubleComplex*>(x), int(n)),
