@@ -1369,8 +1369,19 @@ int sk_set_stream(sk_ctx* ctx, void* stream) {
   });
 }
 
-int64_t sk_kernel_launches(const sk_ctx* ctx) { return ctx ? ctx->launches : 0; }
-int64_t sk_library_calls(const sk_ctx* ctx) { return ctx ? ctx->lib_calls : 0; }
+// Counters include the concurrent lanes (sub-contexts) of batched calls.
+int64_t sk_kernel_launches(const sk_ctx* ctx) {
+  if (!ctx) return 0;
+  int64_t n = ctx->launches;
+  for (const sk_ctx* l : ctx->lanes) n += sk_kernel_launches(l);
+  return n;
+}
+int64_t sk_library_calls(const sk_ctx* ctx) {
+  if (!ctx) return 0;
+  int64_t n = ctx->lib_calls;
+  for (const sk_ctx* l : ctx->lanes) n += sk_library_calls(l);
+  return n;
+}
 
 int sk_make_support(int shape, int tau, int ndim, int32_t* offsets, int64_t* count) {
   return guarded([&] {
