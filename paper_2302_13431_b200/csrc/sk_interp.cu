@@ -42,40 +42,70 @@ __device__ __forceinline__ C cmul(C a, C b) {
   return r;
 }
 
-// In-place radix-2 DIT over `lines` lines of length len (bit-reversed input),
-// twiddles tw[k * step] = exp(sign i 2 pi k / (len*step))... sign via conj flag.
+// Padded position of element i in a line: one slot every 16 elements keeps
+// the strided radix-16 accesses off a single bank.
+__device__ __forceinline__ int pz(int i) { return i + (i >> 4); }
+
+// In-place DIT FFT over 2^log_lines lines of length 2^log2len (bit-reversed
+// input, padded positions, row stride ld), up to four radix-2 stages per pass
+// done in registers (a thread owns 2^r elements spaced by the first stage's
+// half distance); twiddles tw[k << log_tw_stride] = exp(-i 2 pi k / (len << log_tw_stride)),
+// conjugated for the inverse.  All index math is shifts/masks.
 template <typename C>
-__device__ void fft_lines(C* buf, int lines, int ld, int len, int log2len, const C* tw, int tw_stride, bool inverse) {
-  for (int s = 1; s <= log2len; ++s) {
-    const int m = 1 << s, half = m >> 1;
-    const int per_line = len >> 1;
-    for (int e = threadIdx.x; e < lines * per_line; e += blockDim.x) {
-      const int line = e / per_line, k = e % per_line;
-      const int grp = k / half, j = k % half;
-      const int i0 = grp * m + j, i1 = i0 + half;
-      C w = tw[j * (len / m) * tw_stride];
-      if (inverse) w.y = -w.y;
+__device__ void fft_lines(C* buf, int log_lines, int ld, int log2len, const C* tw, int log_tw_stride, bool inverse) {
+  constexpr int RM = 4;
+  for (int s0 = 1; s0 <= log2len; s0 += RM) {
+    const int r = min(RM, log2len - s0 + 1);
+    const int hl0 = s0 - 1;
+    const int glog = log2len - r;  // items per line
+    const int total = 1 << (log_lines + glog);
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int line = e >> glog, it = e & ((1 << glog) - 1);
+      const int j = it & ((1 << hl0) - 1), g = it >> hl0;
+      const int base = (g << (hl0 + r)) + j;
       C* b = buf + line * ld;
-      const C u = b[i0];
-      const C t = cmul(w, b[i1]);
-      b[i0].x = u.x + t.x;
-      b[i0].y = u.y + t.y;
-      b[i1].x = u.x - t.x;
-      b[i1].y = u.y - t.y;
+      C x[1 << RM];
+#pragma unroll
+      for (int m = 0; m < (1 << RM); ++m)
+        if (m < (1 << r)) x[m] = b[pz(base + (m << hl0))];
+#pragma unroll
+      for (int q = 0; q < RM; ++q) {
+        if (q < r) {
+          const int sh = log2len - (s0 + q) + log_tw_stride;
+#pragma unroll
+          for (int m = 0; m < (1 << RM); ++m) {
+            if (m < (1 << r) && !(m & (1 << q))) {
+              C w = tw[(j + ((m & ((1 << q) - 1)) << hl0)) << sh];
+              if (inverse) w.y = -w.y;
+              const C t = cmul(w, x[m + (1 << q)]);
+              const C u = x[m];
+              x[m].x = u.x + t.x;
+              x[m].y = u.y + t.y;
+              x[m + (1 << q)].x = u.x - t.x;
+              x[m + (1 << q)].y = u.y - t.y;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < (1 << RM); ++m)
+        if (m < (1 << r)) b[pz(base + (m << hl0))] = x[m];
     }
     __syncthreads();
   }
 }
 
+// Lines are (b, i) pairs of a [batch][len][inner] volume; inner = 2^log_inner.
 template <typename R>
 __global__ void __launch_bounds__(256) interp_fft_kernel(const typename Cplx<R>::T* __restrict__ in,
-                                                         typename Cplx<R>::T* __restrict__ out, i64 batch, int n, int N,
-                                                         i64 inner, int T, int logn, int logN) {
+                                                         typename Cplx<R>::T* __restrict__ out, unsigned lines_total,
+                                                         int log_inner, int logT, int logn, int logN) {
   using C = typename Cplx<R>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = 1 << logn, N = 1 << logN, T = 1 << logT;
   C* tw = reinterpret_cast<C*>(smem_raw);  // N/2 forward twiddles exp(-i 2 pi k / N)
-  C* buf = tw + N / 2;                     // [T][N + 1]
-  const int ld = N + 1;
+  C* buf = tw + N / 2;                     // [T][ld], padded lines
+  const int ld = N + N / 16 + 1;
   for (int k = threadIdx.x; k < N / 2; k += blockDim.x) {
     R s, c;
     if constexpr (sizeof(R) == 8) {
@@ -86,63 +116,69 @@ __global__ void __launch_bounds__(256) interp_fft_kernel(const typename Cplx<R>:
     tw[k].x = c;
     tw[k].y = s;
   }
-  // lines handled by this block: line id = blockIdx.x * T + t, line -> (b, i)
-  const i64 lines_total = batch * inner;
-  const i64 l0 = i64(blockIdx.x) * T;
+  const unsigned l0 = blockIdx.x << logT;
   const int cl = n / 2, CL = N / 2;
-  const bool across = inner >= T;  // coalesce across lines (columns) or along the line
-  for (int e = threadIdx.x; e < T * n; e += blockDim.x) {
-    const int t = across ? e % T : e / n;
-    const int a = across ? e / T : e % n;
-    const i64 line = l0 + t;
+  const bool across = log_inner >= logT;  // coalesce across lines (columns) or along the line
+  const unsigned imask = (1u << log_inner) - 1u;
+  auto src_index = [&](unsigned line, int a) -> size_t {  // element a of line (b, i)
+    const unsigned b = line >> log_inner, i = line & imask;
+    return ((size_t(b) << logn) + a) * (size_t(1) << log_inner) + i;
+  };
+  for (int e = threadIdx.x; e < (T << logn); e += blockDim.x) {
+    const int t = across ? (e & (T - 1)) : (e >> logn);
+    const int a = across ? (e >> logT) : (e & (n - 1));
+    const unsigned line = l0 + t;
     C v;
     v.x = R(0);
     v.y = R(0);
-    if (line < lines_total) {
-      const i64 b = line / inner, i = line % inner;
-      v = in[(b * n + (a + cl) % n) * inner + i];  // ifftshift
-    }
-    buf[t * ld + bitrev(a, logn)] = v;
+    if (line < lines_total) v = in[src_index(line, (a + cl) & (n - 1))];  // ifftshift
+    buf[t * ld + pz(bitrev(a, logn))] = v;
   }
   __syncthreads();
-  fft_lines(buf, T, ld, n, logn, tw, N / n, false);  // Y = FFT_n
+  fft_lines(buf, logT, ld, logn, tw, logN - logn, false);  // Y = FFT_n
   // Re-place Y into the zero-padded N line in bit-reversed order for the inverse.
   // Every thread reads its Y entries into registers first (in-place overlap).
-  constexpr int kMaxPer = 16;
+  constexpr int kMaxPer = 16;  // T * n <= 16 * 256 (launcher)
   C keep[kMaxPer];
   int dst[kMaxPer];
-  int cnt = 0;
   const R inv_n = R(1) / R(n);
-  for (int e = threadIdx.x; e < T * n && cnt < kMaxPer; e += blockDim.x, ++cnt) {
-    const int t = e / n, k = e % n;
-    const int f = k < n - cl ? k : k - n;  // signed frequency of Y[k] (f in [-c, n - c))
-    const int a = (f + N) % N;             // its slot in the unshifted N-point spectrum
-    C v = buf[t * ld + k];
-    v.x *= inv_n;
-    v.y *= inv_n;
-    keep[cnt] = v;
-    dst[cnt] = t * ld + bitrev(a, logN);
+#pragma unroll
+  for (int u = 0; u < kMaxPer; ++u) {
+    const int e = threadIdx.x + u * 256;
+    dst[u] = -1;
+    if (e < (T << logn)) {
+      const int t = e >> logn, k = e & (n - 1);
+      const int f = k < n - cl ? k : k - n;  // signed frequency of Y[k] (f in [-c, n - c))
+      const int a = (f + N) & (N - 1);       // its slot in the unshifted N-point spectrum
+      C v = buf[t * ld + pz(k)];
+      v.x *= inv_n;
+      v.y *= inv_n;
+      keep[u] = v;
+      dst[u] = t * ld + pz(bitrev(a, logN));
+    }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < T * N; e += blockDim.x) {
-    const int t = e / N, a = e % N;
+  for (int e = threadIdx.x; e < T * ld; e += blockDim.x) {
     C z;
     z.x = R(0);
     z.y = R(0);
-    buf[t * ld + a] = z;
+    buf[e] = z;
   }
   __syncthreads();
-  for (int k = 0; k < cnt; ++k) buf[dst[k]] = keep[k];
+#pragma unroll
+  for (int u = 0; u < kMaxPer; ++u)
+    if (dst[u] >= 0) buf[dst[u]] = keep[u];
   __syncthreads();
-  fft_lines(buf, T, ld, N, logN, tw, 1, true);  // IFFT_N (unscaled, kspace_to_image)
-  for (int e = threadIdx.x; e < T * N; e += blockDim.x) {
-    const int t = across ? e % T : e / N;
-    const int j = across ? e / T : e % N;
-    const i64 line = l0 + t;
-    if (line < lines_total) {
-      const i64 b = line / inner, i = line % inner;
-      out[(b * N + j) * inner + i] = buf[t * ld + (j - CL + N) % N];  // fftshift
-    }
+  fft_lines(buf, logT, ld, logN, tw, 0, true);  // IFFT_N (unscaled, kspace_to_image)
+  auto dst_index = [&](unsigned line, int jj) -> size_t {
+    const unsigned b = line >> log_inner, i = line & imask;
+    return ((size_t(b) << logN) + jj) * (size_t(1) << log_inner) + i;
+  };
+  for (int e = threadIdx.x; e < (T << logN); e += blockDim.x) {
+    const int t = across ? (e & (T - 1)) : (e >> logN);
+    const int jj = across ? (e >> logT) : (e & (N - 1));
+    const unsigned line = l0 + t;
+    if (line < lines_total) out[dst_index(line, jj)] = buf[t * ld + pz((jj - CL) & (N - 1))];  // fftshift
   }
 }
 
@@ -151,14 +187,18 @@ void launch_interp(sk_ctx* ctx, const void* in, void* out, i64 batch, int n, int
   using C = typename Cplx<R>::T;
   const int logn = __builtin_ctz(unsigned(n)), logN = __builtin_ctz(unsigned(N));
   // lines per block: keep T*n <= 16*256 (register staging) and smem <= ~110 KB
+  const int ld = N + N / 16 + 1;
   int T = 32;
-  while (T > 1 && (size_t(T) * (N + 1) * sizeof(C) + size_t(N / 2) * sizeof(C) > 110 * 1024 || T * n > 16 * 256)) T /= 2;
-  const size_t smem = size_t(T) * (N + 1) * sizeof(C) + size_t(N / 2) * sizeof(C);
+  while (T > 1 && (size_t(T) * ld * sizeof(C) + size_t(N / 2) * sizeof(C) > 110 * 1024 || T * n > 16 * 256)) T /= 2;
+  const int logT = __builtin_ctz(unsigned(T));
+  const size_t smem = size_t(T) * ld * sizeof(C) + size_t(N / 2) * sizeof(C);
   set_smem_limit(reinterpret_cast<const void*>(interp_fft_kernel<R>), smem);
   const i64 lines = batch * inner;
   const i64 blocks = (lines + T - 1) / T;
   interp_fft_kernel<R><<<unsigned(blocks), 256, smem, ctx->stream>>>(static_cast<const C*>(in), static_cast<C*>(out),
-                                                                    batch, n, N, inner, T, logn, logN);
+                                                                    unsigned(lines), __builtin_ctzll(
+                                                                        static_cast<unsigned long long>(inner)),
+                                                                    logT, logn, logN);
   ++ctx->launches;
   SKB_LAUNCH("interp_fft_kernel");
 }
@@ -166,8 +206,8 @@ void launch_interp(sk_ctx* ctx, const void* in, void* out, i64 batch, int n, int
 }  // namespace
 
 bool interp_axis_fft(sk_ctx* ctx, const void* in, void* out, i64 batch, int n, int N, i64 inner, bool fp64) {
-  const bool pow2 = n > 0 && N > 0 && !(n & (n - 1)) && !(N & (N - 1));
-  if (!pow2 || n > N || N > 1024 || n < 2) return false;
+  const bool pow2 = n > 0 && N > 0 && !(n & (n - 1)) && !(N & (N - 1)) && inner > 0 && !(inner & (inner - 1));
+  if (!pow2 || n > N || N > 1024 || n < 2 || batch * inner >= (i64(1) << 31)) return false;
   if (fp64)
     launch_interp<double>(ctx, in, out, batch, n, N, inner);
   else

@@ -1111,7 +1111,8 @@ void run_interp(sk_ctx* ctx, const float2* low, float2* out, i64 batch, const Di
       i64 b = batch, inner = 1;
       for (int k = 0; k < a; ++k) b *= cur[size_t(k)];
       for (int k = a + 1; k < nd; ++k) inner *= cur[size_t(k)];
-      interp_axis_fft(ctx, src, dst, b, int(low_dims[size_t(a)]), int(full[size_t(a)]), inner, false);
+      if (!interp_axis_fft(ctx, src, dst, b, int(low_dims[size_t(a)]), int(full[size_t(a)]), inner, false))
+        fail(SK_ERR_UNSUPPORTED, "interpolate_maps: FFT path refused a planned axis");
       cur[size_t(a)] = full[size_t(a)];
       src = dst;
     }
@@ -1139,7 +1140,8 @@ void run_interp_lambda(sk_ctx* ctx, const float* low, const Dims& low_dims, cons
       i64 b = 1, inner = 1;
       for (int k = 0; k < a; ++k) b *= cur[size_t(k)];
       for (int k = a + 1; k < nd; ++k) inner *= cur[size_t(k)];
-      interp_axis_fft(ctx, src, dst, b, int(low_dims[size_t(a)]), int(full[size_t(a)]), inner, true);
+      if (!interp_axis_fft(ctx, src, dst, b, int(low_dims[size_t(a)]), int(full[size_t(a)]), inner, true))
+        fail(SK_ERR_UNSUPPORTED, "interpolate_real: FFT path refused a planned axis");
       cur = next;
       src = dst;
     }
