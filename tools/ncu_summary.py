@@ -1,0 +1,48 @@
+"""Build profiles/ncu_summary_r01.json from ncu --set full reports (raw page)."""
+import csv
+import json
+import subprocess
+import sys
+
+KEYS = {
+    "gpu__time_duration.sum": "duration_ms",
+    "dram__bytes_read.sum": "dram_read",
+    "dram__bytes_write.sum": "dram_write",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pipe_active_pct",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active": "fma_inst_pct",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_active_pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+    "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
+    "launch__registers_per_thread": "registers",
+    "sm__cycles_elapsed.avg.per_second": "sm_clock_ghz",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_throughput_pct",
+}
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "msecond": 1, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1, "us": 1e-3, "ns": 1e-6}
+
+
+def read(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    d = {"kernel": vals[hdr.index("Kernel Name")][:120]}
+    for i, n in enumerate(hdr):
+        if n in KEYS:
+            try:
+                v = float(vals[i].replace(",", ""))
+            except ValueError:
+                continue
+            if KEYS[n] in ("dram_read", "dram_write", "duration_ms"):
+                v *= UNIT.get(units[i], 1)
+            d[KEYS[n]] = v
+    if "dram_read" in d:
+        d["dram_bytes_per_launch"] = d.get("dram_read", 0) + d.get("dram_write", 0)
+    return d
+
+
+out = json.load(open(sys.argv[1])) if len(sys.argv) > 1 and sys.argv[1].endswith(".json") else {}
+args = sys.argv[2:] if len(sys.argv) > 1 and sys.argv[1].endswith(".json") else sys.argv[1:]
+for spec in args:  # group:config=report
+    key, rep = spec.split("=")
+    group, cfg = key.split(":")
+    out.setdefault(group, {})[cfg] = read(rep)
+print(json.dumps(out, indent=1))
