@@ -403,18 +403,22 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     for (int it = 1; it < a.iters; ++it) {
       const int b = it & 1;
       voxel_bar<L>(vox);
-      const float n2 = published_norm(own, b);
       float2 mv[RPT];
       matvec(vb(b), mv);
-      if (it > 1 && n2 < 1e-28f && !done) done = true;
+      // ||u_k||^2 (the previous iteration's shuffle reduction) is consumed only
+      // after the products: the empty asm ties it to mv so ptxas cannot hoist
+      // the test above the loads, and the reduction overlaps the matvec.
+      float n2 = published_norm(own, b);
+      asm("" : "+f"(n2) : "f"(mv[0].x));
+      done = done || (it > 1 && n2 < 1e-28f);
       const float inv = rsqrtf(n2);
-      if (!done) {
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          vprev[r] = make_float2(up[r].x * inv, up[r].y * inv);
-          up[r] = make_float2((a.alpha * up[r].x + a.beta * mv[r].x) * inv,
-                              (a.alpha * up[r].y + a.beta * mv[r].y) * inv);
-        }
+      for (int r = 0; r < RPT; ++r) {  // branch-free: one basic block per iteration
+        const float2 nv = make_float2(up[r].x * inv, up[r].y * inv);
+        const float2 nu = make_float2((a.alpha * up[r].x + a.beta * mv[r].x) * inv,
+                                      (a.alpha * up[r].y + a.beta * mv[r].y) * inv);
+        vprev[r] = done ? vprev[r] : nv;
+        up[r] = done ? up[r] : nu;
       }
       own = publish(up, b ^ 1);
     }
