@@ -105,14 +105,15 @@ struct TmaTiles {
   int hb = 0, nb = 0;
 };
 
-template <int QP_, int RPT_, int THREADS_, int MINB_>
+template <int QP_, int RPT_, int THREADS_, int MINB_, int ACC_ = 0, int CHUNK_ = 8>
 struct Layout {
   static constexpr int QP = QP_, RPT = RPT_, kThreads = THREADS_, kMinBlocks = MINB_;
+  static constexpr int kChunkCols = CHUNK_;  // v columns staged per load batch
   static constexpr int kTPV = QP / RPT;          // threads per voxel
   static constexpr int kVPB = kThreads / kTPV;   // voxels per block
   static constexpr int kWPV = kTPV > 32 ? kTPV / 32 : 1;  // warps per voxel
   static constexpr int kStride = QP + 2;         // float2 per v row (16-B aligned, bank-skewed)
-  static constexpr int kAcc = RPT >= 4 ? 1 : 4 / RPT;     // accumulator pairs per row
+  static constexpr int kAcc = ACC_ > 0 ? ACC_ : (RPT >= 4 ? 1 : 4 / RPT);  // accumulator pairs per row
 };
 
 // Sum over the voxel's threads.  Multi-warp voxels go through shared memory
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       for (int r = 0; r < RPT; ++r)
 #pragma unroll
         for (int k = 0; k < A; ++k) acc[r][k] = acc2[r][k] = 0ull;
-      constexpr int kChunk = QP < 8 ? QP : 8;
+      constexpr int kChunk = QP < L::kChunkCols ? QP : L::kChunkCols;
 #pragma unroll
       for (int cb = 0; cb < QP; cb += kChunk) {
         float4 vv[kChunk / 2];
@@ -589,6 +590,7 @@ void power_iteration(sk_ctx* ctx, const PowerArgs& a) {
   // Rows per thread for Q in (16, 32]; SKB_POWER_RPT32=2 selects the
   // two-row layout (measured equal with FFMA2, but it spills).
   static const int rpt32 = env_int("SKB_POWER_RPT32", 1);
+  static const int k4v = env_int("SKB_K4_VARIANT", 0);
   if (a.q <= 4)
     launch<Layout<4, 1, 256, 2>>(ctx, a);
   else if (a.q <= 8)
@@ -596,7 +598,12 @@ void power_iteration(sk_ctx* ctx, const PowerArgs& a) {
   else if (a.q <= 16)
     launch<Layout<16, 1, 256, 2>>(ctx, a);
   else if (a.q <= 32)
-    rpt32 == 1 ? launch<Layout<32, 1, 256, 2>>(ctx, a) : launch<Layout<32, 2, 128, 3>>(ctx, a);
+    switch (k4v) {  // SKB_K4_VARIANT: accumulator pairs / staged columns (experiments)
+      case 1: launch<Layout<32, 1, 256, 2, 2, 8>>(ctx, a); break;
+      case 2: launch<Layout<32, 1, 256, 2, 4, 8>>(ctx, a); break;
+      case 3: launch<Layout<32, 1, 256, 2, 4, 16>>(ctx, a); break;
+      default: rpt32 == 1 ? launch<Layout<32, 1, 256, 2, 2, 16>>(ctx, a) : launch<Layout<32, 2, 128, 3>>(ctx, a);
+    }
   else if (a.q <= 64)
     launch<Layout<64, 1, 256, 1>>(ctx, a);
   else
