@@ -153,6 +153,24 @@ int sk_interpolate_real(sk_ctx* ctx, int ndim, const int64_t* low_dims, const fl
 /* support_mask (maps.hpp:105, maps.cpp:47-52). */
 int sk_support_mask(sk_ctx* ctx, int64_t voxels, const float* lambda, double mask_threshold, uint8_t* mask);
 
+/* ------------------------------------------------- z-slab sharding (§8e) */
+/* pipeline::compute_field + solve_field + the per-voxel half of finalize
+ * (maps.hpp:115-123, maps.cpp:195-230, 117-172) restricted to rows
+ * [slab_begin, slab_end) of axis 0 of the map grid (grid_dims_for or
+ * cfg->grid_dims): maps = Q x slab voxels (SoS-normalised, phase referenced,
+ * not yet interpolated), lambda = slab voxels.  Every rank computes the same
+ * Gram and nullspace (deterministic), so concatenating the slabs along axis 0
+ * reproduces the map-grid result; interpolation then runs per channel subset
+ * (sk_interpolate_maps) with the renormalisation split below. */
+int sk_estimate_raw_slab(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset,
+                         int64_t channels, const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg,
+                         int64_t slab_begin, int64_t slab_end, sk_c64* maps, float* lambda, sk_provenance* prov);
+/* Renormalisation after interpolation (maps.cpp:236-258) split over channel
+ * subsets: sos[j] += sum_c |maps[c][j]|^2; then maps[c][j] /= sqrt(sos[j])
+ * where sos[j] > 0, with sos the sum over all subsets (an all-reduce). */
+int sk_sos_accumulate(sk_ctx* ctx, int64_t voxels, int64_t channels, const sk_c64* maps, float* sos);
+int sk_renormalize_sos(sk_ctx* ctx, int64_t voxels, int64_t channels, sk_c64* maps, const float* sos);
+
 /* Test hook for the K2 Rayleigh-Ritz eigensolver (no reference counterpart;
  * the reference uses Eigen's SelfAdjointEigenSolver, nullspace.cpp:13):
  * h is an n x n Hermitian complex128 matrix, column-major, interleaved

@@ -171,6 +171,9 @@ _SIGS = {
     "sk_interpolate_real": ([_VP, _I32, _VP, _VP, _VP, _VP], _I32),
     "sk_support_mask": ([_VP, _I64, _VP, _D, _VP], _I32),
     "sk_debug_small_eigh": ([_VP, _I64, _VP, _VP], _I32),
+    "sk_estimate_raw_slab": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _I64, _I64, _VP, _VP, _VP], _I32),
+    "sk_sos_accumulate": ([_VP, _I64, _I64, _VP, _VP], _I32),
+    "sk_renormalize_sos": ([_VP, _I64, _I64, _VP, _VP], _I32),
     "sk_estimate_maps": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP], _I32),
     "sk_estimate_maps_debug": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                 _VP, _VP], _I32),
@@ -457,6 +460,64 @@ def estimate_maps(calib: Calib, full_dims, cfg: PipelineConfig, ctx: Context | N
         fieldb.reshape(ngrid, q, q).transpose(0, 2, 1) if want_field else None, raw, raw_l,
         extra={"eig_solver": "full" if prov.eig_solver_used == 1 else "subspace", "certified": bool(prov.certified),
                "subspace_iterations": int(prov.subspace_iterations), "subspace_block": int(prov.subspace_block)})
+
+
+def estimate_raw_slab(calib: Calib, full_dims, cfg: PipelineConfig, slab, ctx: Context | None = None):
+    """z-slab sharding (SURVEY §8e): pipeline::compute_field + solve_field + the
+    per-voxel normalisation (maps.hpp:115-123) on map-grid rows slab = (begin,
+    end) of axis 0.  Returns (maps (Q, end-begin, *grid[1:]) complex64,
+    lambda (end-begin, *grid[1:]) float32, provenance)."""
+    d = _c64(calib.data)
+    q, cdims = d.shape[0], d.shape[1:]
+    grid = _grid_for(cdims, full_dims, cfg)
+    b, e = int(slab[0]), int(slab[1])
+    shape = (e - b,) + tuple(grid[1:])
+    maps = np.zeros((q,) + shape, dtype=np.complex64)
+    lam = np.zeros(shape, dtype=np.float32)
+    prov = sk_provenance()
+    cfgc = cfg.to_c()
+    _check(lib().sk_estimate_raw_slab(_ctx(ctx), len(cdims), _p(_i64(cdims)), _p(_i64(calib.center_offset)), q,
+                                      _p(d), _p(_i64(full_dims)), C.byref(cfgc), b, e, _p(maps), _p(lam),
+                                      C.byref(prov)))
+    return maps, lam, prov
+
+
+def estimate_raw_slab_device(ctx: Context, calib_ptr: int, calib_dims, center_offset, q: int, full_dims,
+                             cfg: PipelineConfig, slab, maps_ptr: int, lambda_ptr: int) -> sk_provenance:
+    """Device-buffer variant of estimate_raw_slab."""
+    prov = sk_provenance()
+    cfgc = cfg.to_c()
+    _check(lib().sk_estimate_raw_slab(ctx.handle, len(calib_dims), _p(_i64(calib_dims)), _p(_i64(center_offset)), q,
+                                      C.c_void_p(calib_ptr), _p(_i64(full_dims)), C.byref(cfgc), int(slab[0]),
+                                      int(slab[1]), C.c_void_p(maps_ptr), C.c_void_p(lambda_ptr), C.byref(prov)))
+    return prov
+
+
+def sos_accumulate(maps, sos, ctx: Context | None = None):
+    """sos += sum_c |maps_c|^2 per voxel (maps.cpp:236-258 renorm, one channel subset).
+    maps: (C, *vox) complex64 array or DevicePtr-like with .data_ptr(); sos: float32, updated in place."""
+    if hasattr(maps, "data_ptr"):
+        _check(lib().sk_sos_accumulate(_ctx(ctx), sos.numel(), maps.shape[0], C.c_void_p(maps.data_ptr()),
+                                       C.c_void_p(sos.data_ptr())))
+        return sos
+    m = _c64(maps)
+    if not (isinstance(sos, np.ndarray) and sos.dtype == np.float32 and sos.flags.c_contiguous):
+        raise ValueError("sos must be a contiguous float32 array")
+    _check(lib().sk_sos_accumulate(_ctx(ctx), sos.size, m.shape[0], _p(m), _p(sos)))
+    return sos
+
+
+def renormalize_sos(maps, sos, ctx: Context | None = None):
+    """maps /= sqrt(sos) where sos > 0 (in place); sos is the all-channel sum of squares."""
+    if hasattr(maps, "data_ptr"):
+        _check(lib().sk_renormalize_sos(_ctx(ctx), sos.numel(), maps.shape[0], C.c_void_p(maps.data_ptr()),
+                                        C.c_void_p(sos.data_ptr())))
+        return maps
+    if not (isinstance(maps, np.ndarray) and maps.dtype == np.complex64 and maps.flags.c_contiguous):
+        raise ValueError("maps must be a contiguous complex64 array")
+    s = np.ascontiguousarray(sos, dtype=np.float32)
+    _check(lib().sk_renormalize_sos(_ctx(ctx), s.size, maps.shape[0], _p(maps), _p(s)))
+    return maps
 
 
 def estimate_maps_device(ctx: Context, calib_ptr: int, calib_dims, center_offset, q: int, full_dims,

@@ -193,6 +193,8 @@ void espirit_field(sk_ctx* ctx, float2* field, i64 n, int q, float inv_lam);
 void renormalize_and_mask(sk_ctx* ctx, float2* maps, i64 n, int q, const float2* lambda_c, float* lambda,
                           uint8_t* mask, float thr);
 void mask_kernel(sk_ctx* ctx, const float* lambda, i64 n, float thr, uint8_t* mask);
+void sos_accumulate(sk_ctx* ctx, const float2* maps, i64 n, int q, float* sos);   // sos += sum_c |maps_c|^2
+void renorm_with_sos(sk_ctx* ctx, float2* maps, i64 n, int q, const float* sos);  // maps /= sqrt(sos) where > 0
 void real_to_c64(sk_ctx* ctx, const float* in, float2* out, i64 n);
 void real_to_c128(sk_ctx* ctx, const float* in, double2* out, i64 n);
 void lam64_to_f32_mask(sk_ctx* ctx, const double2* lam_c, i64 n, float* lam, uint8_t* mask, float thr);

@@ -101,6 +101,33 @@ __global__ void renorm_mask_kernel(float2* __restrict__ maps, i64 n, int q, cons
   }
 }
 
+// Channel-split renormalisation (z-slab sharding, maps.cpp:236-258): partial
+// sum of squares over a channel subset, then division by the all-reduced sum.
+__global__ void sos_accumulate_kernel(const float2* __restrict__ maps, i64 n, int q, float* __restrict__ sos) {
+  for (i64 j = i64(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += i64(gridDim.x) * blockDim.x) {
+    float acc = sos[j];
+    for (int c = 0; c < q; ++c) {
+      const float2 v = maps[i64(c) * n + j];
+      acc += v.x * v.x + v.y * v.y;
+    }
+    sos[j] = acc;
+  }
+}
+__global__ void renorm_sos_kernel(float2* __restrict__ maps, i64 n, int q, const float* __restrict__ sos) {
+  for (i64 j = i64(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += i64(gridDim.x) * blockDim.x) {
+    const float s = sos[j];
+    if (s > 0.f) {
+      const float inv = 1.0f / sqrtf(s);
+      for (int c = 0; c < q; ++c) {
+        float2 v = maps[i64(c) * n + j];
+        v.x *= inv;
+        v.y *= inv;
+        maps[i64(c) * n + j] = v;
+      }
+    }
+  }
+}
+
 __global__ void mask_only_kernel(const float* __restrict__ lam, i64 n, float thr, uint8_t* __restrict__ mask) {
   for (i64 j = i64(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += i64(gridDim.x) * blockDim.x)
     mask[j] = lam[j] < thr ? 1 : 0;
@@ -280,6 +307,16 @@ void renormalize_and_mask(sk_ctx* ctx, float2* maps, i64 n, int q, const float2*
   renorm_mask_kernel<<<SKB_GRID(n)>>>(maps, n, q, lambda_c, lambda, mask, thr);
   ++ctx->launches;
   SKB_LAUNCH("renorm_mask");
+}
+void sos_accumulate(sk_ctx* ctx, const float2* maps, i64 n, int q, float* sos) {
+  sos_accumulate_kernel<<<SKB_GRID(n)>>>(maps, n, q, sos);
+  ++ctx->launches;
+  SKB_LAUNCH("sos_accumulate");
+}
+void renorm_with_sos(sk_ctx* ctx, float2* maps, i64 n, int q, const float* sos) {
+  renorm_sos_kernel<<<SKB_GRID(n)>>>(maps, n, q, sos);
+  ++ctx->launches;
+  SKB_LAUNCH("renorm_sos");
 }
 void mask_kernel(sk_ctx* ctx, const float* lambda, i64 n, float thr, uint8_t* mask) {
   mask_only_kernel<<<SKB_GRID(n)>>>(lambda, n, thr, mask);

@@ -291,7 +291,10 @@ double2* symdft_table64(sk_ctx* ctx, int N, int H, i64 j0, int sign) {
 // G(x) lag expansion (spatial_gram.cpp:125-138): FP64 lag box [h][lb]^D ->
 // fp32 hi/lo planes [h][grid] (sk_expand.cu).  Axes are transformed last to
 // first; intermediates stay FP64.
-void expand_lags(sk_ctx* ctx, const double2* lags, float2* hi, float2* lo, i64 h, int tau, const Dims& grid) {
+// slab0/slab1: optional axis-0 row range [slab0, slab1) of the grid (z-slab
+// sharding); the outputs then cover only those rows.
+void expand_lags(sk_ctx* ctx, const double2* lags, float2* hi, float2* lo, i64 h, int tau, const Dims& grid,
+                 i64 slab0 = 0, i64 slab1 = -1) {
   const int nd = int(grid.size()), lb = 4 * tau + 1, H = 2 * tau;
   Dims cur(static_cast<size_t>(nd), lb);
   const double2* src = lags;
@@ -306,8 +309,13 @@ void expand_lags(sk_ctx* ctx, const double2* lags, float2* hi, float2* lo, i64 h
     for (int k = 0; k < a; ++k) b *= cur[size_t(k)];
     for (int k = a + 1; k < nd; ++k) inner *= cur[size_t(k)];
     const int N = int(grid[size_t(a)]);
-    expand_stage_f64(ctx, src, b, inner, H, N, symdft_table64(ctx, N, H, center_index(N), -1), dst,
-                     a == 0 ? hi : nullptr, a == 0 ? lo : nullptr);
+    const double2* cs = symdft_table64(ctx, N, H, center_index(N), -1);
+    int Nout = N;
+    if (a == 0 && slab1 >= 0) {  // rows [slab0, slab1) of the last (axis-0) stage only
+      cs += slab0 * std::max(H, 1);
+      Nout = int(slab1 - slab0);
+    }
+    expand_stage_f64(ctx, src, b, inner, H, Nout, cs, dst, a == 0 ? hi : nullptr, a == 0 ? lo : nullptr);
     cur[size_t(a)] = grid[size_t(a)];
     src = dst;
   }
@@ -1031,7 +1039,8 @@ Eig run_nullspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, int solv
 
 // ---------------------------------------------------------------- K3
 // Lag kernels from the signal subspace, expanded onto the grid as packed planes.
-Planes run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims& grid) {
+Planes run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims& grid, i64 slab0 = 0,
+                 i64 slab1 = -1) {
   const i64 n = e.n, k = e.k;
   const int lam = int(s.count);
   SupportTables& t = tables_for(ctx, s, q);
@@ -1050,9 +1059,10 @@ Planes run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims&
   double2* lags = ctx->arena.get<double2>("field:lags64", i64(h) * t.nbox);
   fold_lags_f64(ctx, ws, n, h, lam, t.nbox, t.pairs, t.lag_ptr, t.lag_st, true, lags);
   Planes p;
-  p.hi = ctx->arena.get<float2>("field:planes", i64(h) * numel(grid));
-  p.lo = ctx->arena.get<float2>("field:planes_lo", i64(h) * numel(grid));
-  expand_lags(ctx, lags, p.hi, p.lo, h, s.tau, grid);
+  const i64 nvox = slab1 >= 0 ? numel(grid) / grid[0] * (slab1 - slab0) : numel(grid);
+  p.hi = ctx->arena.get<float2>("field:planes", i64(h) * nvox);
+  p.lo = ctx->arena.get<float2>("field:planes_lo", i64(h) * nvox);
+  expand_lags(ctx, lags, p.hi, p.lo, h, s.tau, grid, slab0, slab1);
   return p;
 }
 
@@ -1072,7 +1082,7 @@ Planes run_field_from_w(sk_ctx* ctx, const float2* w, const Support& s, int q, c
 
 // ---------------------------------------------------------------- K5 pieces
 float2* run_recon(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float2* calib, const Dims& grid,
-                  double apod_width) {  // maps.cpp:130-160
+                  double apod_width, i64 slab0 = 0, i64 slab1 = -1) {  // maps.cpp:130-160
   const int nd = int(cdims.size());
   std::vector<float2*> mats(static_cast<size_t>(nd));
   for (int a = 0; a < nd; ++a) {
@@ -1080,8 +1090,13 @@ float2* run_recon(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const f
     mats[size_t(a)] = dft_matrix(ctx, int(grid[size_t(a)]), int(cdims[size_t(a)]), co[size_t(a)],
                                  center_index(grid[size_t(a)]), +1, sigma);
   }
-  float2* recon = ctx->arena.get<float2>("post:recon", q * numel(grid));
-  separable(ctx, calib, recon, q, cdims, grid, mats, "post:tmp");
+  Dims out_grid = grid;
+  if (slab1 >= 0) {  // axis-0 rows [slab0, slab1): the row-major N x L matrix offset by slab0 rows
+    mats[0] += slab0 * cdims[0];
+    out_grid[0] = slab1 - slab0;
+  }
+  float2* recon = ctx->arena.get<float2>("post:recon", q * numel(out_grid));
+  separable(ctx, calib, recon, q, cdims, out_grid, mats, "post:tmp");
   return recon;
 }
 
@@ -1165,6 +1180,10 @@ struct PipelineOut {
   float2* raw_maps = nullptr; // debug: device [Q][N_grid]
   float* raw_lambda = nullptr;
   double* spectrum = nullptr; // host n
+  // z-slab mode (sk_estimate_raw_slab): axis-0 grid rows [slab0, slab1); the
+  // normalised maps / raw lambda of those rows go to maps / lambda and the
+  // interpolation stage is skipped.
+  i64 slab0 = 0, slab1 = -1;
 };
 
 void validate_config(const sk_config* cfg) {
@@ -1203,8 +1222,12 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
     if (full[size_t(a)] < grid[size_t(a)])
       fail(SK_ERR_DIM, "interpolation target smaller than source on axis " + std::to_string(a));
   }
-  const i64 lam = s.count, n = q * lam, ngrid = numel(grid), nfull = numel(full);
-  const bool interp = grid != full;
+  const bool slab = out.slab1 >= 0;
+  if (slab && (out.slab0 < 0 || out.slab1 <= out.slab0 || out.slab1 > grid[0]))
+    fail(SK_ERR_DIM, "slab rows must satisfy 0 <= begin < end <= grid_dims[0]");
+  const i64 lam = s.count, n = q * lam, nfull = numel(full);
+  const i64 ngrid = slab ? numel(grid) / grid[0] * (out.slab1 - out.slab0) : numel(grid);  // voxels computed here
+  const bool interp = !slab && grid != full;
 
   cudaEvent_t* ev = ctx->ev;
   SKB_CUDA(cudaEventRecord(ev[0], ctx->stream));
@@ -1216,12 +1239,12 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
                         cfg->certify != 0);
   SKB_CUDA(cudaEventRecord(ev[2], ctx->stream));
   // field
-  const Planes pl = run_field(ctx, e, s, int(q), grid);
+  const Planes pl = run_field(ctx, e, s, int(q), grid, out.slab0, out.slab1);
   float2* planes = pl.hi;
   if (out.field) planes_to_field_full(ctx, pl.hi, pl.lo, ngrid, int(q), out.field);
   SKB_CUDA(cudaEventRecord(ev[3], ctx->stream));
   // post (part 1): apodised recon on the map grid, consumed by K4's epilogue
-  float2* recon = run_recon(ctx, cdims, co, q, calib, grid, cfg->apod_width);
+  float2* recon = run_recon(ctx, cdims, co, q, calib, grid, cfg->apod_width, out.slab0, out.slab1);
   SKB_CUDA(cudaEventRecord(ev[4], ctx->stream));
   // eigensolve (+ fused normalisation)
   unsigned long long* zeroed = ctx->arena.get<unsigned long long>("post:zeroed", 1);
@@ -1248,7 +1271,7 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   pa.recon = recon;
   pa.maps = maps_grid;
   pa.lambda = lam_grid;
-  pa.mask = (!interp && out.mask) ? out.mask : nullptr;
+  pa.mask = (!interp && !slab && out.mask) ? out.mask : nullptr;
   pa.mask_threshold = float(cfg->mask_threshold);
   pa.zeroed = zeroed;
   power_iteration(ctx, pa);
@@ -1655,6 +1678,72 @@ int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, con
     orl.finish(ctx);
     SKB_CUDA(cudaStreamSynchronize(ctx->stream));
     if (spectrum) std::copy(spec.begin(), spec.begin() + n, spectrum);
+  });
+}
+
+int sk_estimate_raw_slab(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset,
+                         int64_t q, const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg,
+                         int64_t slab_begin, int64_t slab_end, sk_c64* maps, float* lambda, sk_provenance* prov) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (ndim < 1 || !cfg) fail(SK_ERR_DIM, "bad arguments");
+    const Dims cd = dims_of(ndim, calib_dims), co = dims_of(ndim, center_offset), fd = dims_of(ndim, full_dims);
+    for (i64 d : cd)
+      if (d < 1) fail(SK_ERR_DIM, "stack axis extents must be >= 1");
+    if (q < 1) fail(SK_ERR_DIM, "stack needs at least one channel");
+    Dims grid(static_cast<size_t>(ndim));
+    bool ex = true;
+    for (int a = 0; a < ndim; ++a) ex = ex && cfg->grid_dims[a] > 0;
+    for (int a = 0; a < ndim; ++a)
+      grid[size_t(a)] = ex ? cfg->grid_dims[a]
+                           : (cfg->grid == 1 ? std::min(cd[size_t(a)] + cfg->grid_pad, fd[size_t(a)]) : fd[size_t(a)]);
+    if (slab_begin < 0 || slab_end <= slab_begin || slab_end > grid[0])
+      fail(SK_ERR_DIM, "slab rows must satisfy 0 <= begin < end <= grid_dims[0]");
+    const i64 nvox = numel(grid) / grid[0] * (slab_end - slab_begin);
+    const float2* d_cal = device_in(ctx, reinterpret_cast<const float2*>(calib), q * numel(cd), "in:calib");
+    Out<float2> om(ctx, reinterpret_cast<float2*>(maps), q * nvox, "out:slab_maps");
+    Out<float> ol(ctx, lambda, nvox, "out:slab_lambda");
+    PipelineOut po;
+    po.maps = om.dev ? om.dev : ctx->arena.get<float2>("out:slab_maps", q * nvox);
+    po.lambda = ol.dev ? ol.dev : ctx->arena.get<float>("out:slab_lambda", nvox);
+    po.slab0 = slab_begin;
+    po.slab1 = slab_end;
+    pipeline(ctx, cd, co, q, d_cal, fd, cfg, po, prov);
+    om.finish(ctx);
+    ol.finish(ctx);
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_sos_accumulate(sk_ctx* ctx, int64_t voxels, int64_t channels, const sk_c64* maps, float* sos) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (voxels < 0 || channels < 0) fail(SK_ERR_DIM, "bad arguments");
+    const float2* d_m = device_in(ctx, reinterpret_cast<const float2*>(maps), channels * voxels, "in:maps");
+    const bool host = sos && !is_device_ptr(sos);
+    float* d_s = host ? ctx->arena.get<float>("io:sos", voxels) : sos;
+    if (host) SKB_CUDA(cudaMemcpyAsync(d_s, sos, size_t(voxels) * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+    sos_accumulate(ctx, d_m, voxels, int(channels), d_s);
+    if (host) SKB_CUDA(cudaMemcpyAsync(sos, d_s, size_t(voxels) * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_renormalize_sos(sk_ctx* ctx, int64_t voxels, int64_t channels, sk_c64* maps, const float* sos) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (voxels < 0 || channels < 0) fail(SK_ERR_DIM, "bad arguments");
+    const float* d_s = device_in(ctx, sos, voxels, "in:sos");
+    const bool host = maps && !is_device_ptr(maps);
+    float2* d_m = host ? ctx->arena.get<float2>("io:renorm_maps", channels * voxels) : reinterpret_cast<float2*>(maps);
+    if (host)
+      SKB_CUDA(cudaMemcpyAsync(d_m, maps, size_t(channels * voxels) * sizeof(float2), cudaMemcpyHostToDevice,
+                               ctx->stream));
+    renorm_with_sos(ctx, d_m, voxels, int(channels), d_s);
+    if (host)
+      SKB_CUDA(cudaMemcpyAsync(maps, d_m, size_t(channels * voxels) * sizeof(float2), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

@@ -59,3 +59,127 @@ def gather_slices(local: np.ndarray, n_items: int, group=None, device=None):
         arr = p.cpu().numpy().reshape((pad,) + (-1,)).view(local.dtype).reshape((pad,) + shape)
         rows.append(arr[: cnt[r]])
     return np.concatenate(rows, axis=0)
+
+
+# --------------------------------------------------------------- C4: z-slabs
+# A 3-D volume shards by z-slab (axis 0 of the map grid).  Every rank runs the
+# Gram and the nullspace (deterministic, so identical everywhere), expands G(x)
+# and runs the power iteration + normalisation only on its rows of the map
+# grid (sk_estimate_raw_slab); one all-gather assembles the low-resolution maps
+# and eigenvalues; the interpolation is split by channel, its sum-of-squares
+# renormalisation by an all-reduce of the per-voxel SoS (maps.cpp:236-258).
+# Tensors stay where the ops put them (HBM with NCCL on the box, host memory
+# with gloo in the CPU tests).
+
+def _gather_rows(t, n_total: int, group=None):
+    """all_gather of per-rank row blocks (dim 0, sizes from partition) -> (n_total, ...) on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    cnt = counts(n_total, world)
+    pad = max(cnt)
+    real = torch.view_as_real(t) if t.is_complex() else t
+    buf = real.new_zeros((pad,) + tuple(real.shape[1:]))
+    buf[: real.shape[0]] = real
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    out = torch.cat([p[:c] for p, c in zip(parts, cnt)], 0)
+    return torch.view_as_complex(out.contiguous()) if t.is_complex() else out
+
+
+class DeviceOps:
+    """The z-slab driver's operations on the C-ABI with device tensors."""
+
+    def __init__(self, ctx, device):
+        self.ctx, self.device = ctx, device
+
+    def raw_slab(self, calib, full_dims, cfg, slab):
+        import torch
+        from . import api
+        grid = api._grid_for(calib.dims, full_dims, cfg)
+        q = calib.channels
+        shape = (slab[1] - slab[0],) + tuple(grid[1:])
+        cal = torch.from_numpy(np.ascontiguousarray(calib.data, dtype=np.complex64)).to(self.device)
+        maps = torch.empty((q,) + shape, dtype=torch.complex64, device=self.device)
+        lam = torch.empty(shape, dtype=torch.float32, device=self.device)
+        api.estimate_raw_slab_device(self.ctx, cal.data_ptr(), calib.dims, calib.center_offset, q, full_dims, cfg,
+                                     slab, maps.data_ptr(), lam.data_ptr())
+        return maps, lam
+
+    def interpolate_maps(self, low, full_dims):
+        import ctypes as C
+        import torch
+        from . import api
+        low = low.contiguous()
+        out = torch.empty((low.shape[0],) + tuple(full_dims), dtype=torch.complex64, device=low.device)
+        api._check(api.lib().sk_interpolate_maps(self.ctx.handle, low.dim() - 1, api._p(api._i64(low.shape[1:])),
+                                                 low.shape[0], C.c_void_p(low.data_ptr()),
+                                                 api._p(api._i64(full_dims)), C.c_void_p(out.data_ptr())))
+        return out
+
+    def interpolate_real(self, low, full_dims):
+        import ctypes as C
+        import torch
+        from . import api
+        low = low.contiguous()
+        out = torch.empty(tuple(full_dims), dtype=torch.float32, device=low.device)
+        api._check(api.lib().sk_interpolate_real(self.ctx.handle, low.dim(), api._p(api._i64(low.shape)),
+                                                 C.c_void_p(low.data_ptr()), api._p(api._i64(full_dims)),
+                                                 C.c_void_p(out.data_ptr())))
+        return out
+
+    def sos_accumulate(self, maps, sos):
+        from . import api
+        return api.sos_accumulate(maps, sos, self.ctx)
+
+    def renormalize(self, maps, sos):
+        from . import api
+        return api.renormalize_sos(maps, sos, self.ctx)
+
+    def support_mask(self, lam, thr):
+        import ctypes as C
+        import torch
+        from . import api
+        out = torch.empty(lam.shape, dtype=torch.uint8, device=lam.device)
+        api._check(api.lib().sk_support_mask(self.ctx.handle, lam.numel(), C.c_void_p(lam.data_ptr()), float(thr),
+                                             C.c_void_p(out.data_ptr())))
+        return out
+
+
+def estimate_maps_zslab(calib, full_dims, cfg, ops, group=None, gather_maps=True):
+    """estimate_maps (maps.cpp:265-330) sharded by z-slab across the ranks of `group`.
+
+    Returns (maps, lambda, mask, info): maps (Q, *full) when gather_maps else
+    this rank's channel block (info["channels"]); lambda and mask on every rank.
+    """
+    import torch
+    import torch.distributed as dist
+    from . import api
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    grid = api._grid_for(calib.dims, full_dims, cfg)
+    q = calib.channels
+    slab = partition(grid[0], world, rank)
+    maps_s, lam_s = ops.raw_slab(calib, full_dims, cfg, slab)  # (Q, nz, ...), (nz, ...)
+    if world > 1:
+        maps_low = _gather_rows(maps_s.transpose(0, 1).contiguous(), grid[0], group).transpose(0, 1).contiguous()
+        lam_low = _gather_rows(lam_s, grid[0], group)
+    else:
+        maps_low, lam_low = maps_s, lam_s
+    ch = partition(q, world, rank)
+    if tuple(grid) == tuple(full_dims):  # no interpolation, no renormalisation (maps.cpp:236-237)
+        mine = maps_low[ch[0]:ch[1]].contiguous()
+        lam = lam_low
+    else:
+        mine = ops.interpolate_maps(maps_low[ch[0]:ch[1]].contiguous(), full_dims)
+        sos = torch.zeros(tuple(full_dims), dtype=torch.float32, device=mine.device)
+        ops.sos_accumulate(mine, sos)
+        if world > 1:
+            dist.all_reduce(sos, group=group)
+        ops.renormalize(mine, sos)
+        lam = ops.interpolate_real(lam_low, full_dims)
+    mask = ops.support_mask(lam, cfg.mask_threshold)
+    maps = _gather_rows(mine, q, group) if (gather_maps and world > 1) else mine
+    return maps, lam, mask, {"slab": slab, "channels": ch, "grid": grid}

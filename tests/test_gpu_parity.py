@@ -357,3 +357,65 @@ def test_determinism_and_device_buffers(K):
                                maps.data_ptr(), lam.data_ptr(), mask.data_ptr())
     assert np.array_equal(maps.cpu().numpy(), a.maps)
     assert np.array_equal(mask.cpu().numpy(), a.support_mask)
+
+
+# ------------------------------------------------------- z-slab sharding (§8e)
+@pytest.mark.parametrize("grid,full", [((14, 12, 10), (20, 18, 16)), ((8, 8, 8), (16, 16, 16))])
+def test_zslab_composition_matches_pipeline(K, O, grid, full):
+    """C4's z-slab split, ranks simulated in one process: per-slab
+    compute_field + solve_field + normalisation (sk_estimate_raw_slab),
+    concatenation along axis 0, channel-split interpolation with the SoS
+    renormalisation summed over the splits.  Must reproduce the unsharded
+    pipeline (and the oracle) — the collectives are exactly these
+    concatenations and sums."""
+    from paper_2302_13431_b200 import shard
+    sc3 = O.simulate(4, full, 1, 9, noise_sigma=0.01, noise_seed=2)
+    cal3 = O.extract_calibration(sc3["kspace"], (8, 8, 6))
+    calib = K.Calib(cal3.data.astype(np.complex64), tuple(cal3.center_offset))
+    ck = K.PipelineConfig(kernel=K.ELLIPSOID, tau=2, power_iters=15, grid_dims=grid)
+    ref = K.estimate_maps(calib, full, ck)
+    co = O.PipelineConfig.pisco()
+    co.tau, co.power_iters = 2, 15
+    ro = O.estimate_maps(O.Calib(f32(cal3.data), cal3.center_offset), full, co, grid_dims=grid)
+    q = calib.channels
+    for world in (1, 2, 3):
+        slabs = [shard.partition(grid[0], world, r) for r in range(world)]
+        parts = [K.api.estimate_raw_slab(calib, full, ck, s) for s in slabs]
+        maps_low = np.concatenate([p[0] for p in parts], axis=1)
+        lam_low = np.concatenate([p[1] for p in parts], axis=0)
+        assert maps_low.shape == (q,) + grid
+        chans = [shard.partition(q, world, r) for r in range(world)]
+        blocks = [K.interpolate_maps(maps_low[a:b], full) for a, b in chans]
+        sos = np.zeros(full, dtype=np.float32)
+        for blk in blocks:
+            K.api.sos_accumulate(blk, sos)
+        for blk in blocks:
+            K.api.renormalize_sos(blk, sos)
+        maps = np.concatenate(blocks, axis=0)
+        lam = K.interpolate_real(lam_low, full)
+        mask = K.support_mask(lam, ck.mask_threshold)
+        err = PM.rel_fro(maps, ref.maps)
+        err_o = PM.rel_fro(maps, ro.maps)
+        report("zslab", grid=list(grid), world=world, maps_vs_pipeline=err, maps_vs_oracle=err_o,
+               lam_max_abs=float(np.abs(lam - ref.lambda_min_map).max()))
+        assert err < 1e-5 and err_o < 1e-4
+        assert np.allclose(lam, ref.lambda_min_map, rtol=1e-6, atol=1e-9)
+        assert np.array_equal(mask, ref.support_mask)
+
+
+def test_zslab_driver_device_ops(K):
+    """shard.estimate_maps_zslab on device tensors (DeviceOps, single process)."""
+    import torch
+    from paper_2302_13431_b200 import shard
+    from oracle import oracle as O
+    full, grid = (16, 16, 16), (8, 8, 8)
+    sc3 = O.simulate(4, full, 1, 9, noise_sigma=0.01, noise_seed=2)
+    cal3 = O.extract_calibration(sc3["kspace"], (8, 8, 6))
+    calib = K.Calib(cal3.data.astype(np.complex64), tuple(cal3.center_offset))
+    ck = K.PipelineConfig(kernel=K.ELLIPSOID, tau=2, power_iters=15, grid_dims=grid)
+    ref = K.estimate_maps(calib, full, ck)
+    maps, lam, mask, info = shard.estimate_maps_zslab(calib, full, ck, shard.DeviceOps(K.default_context(0), "cuda"))
+    assert info["slab"] == (0, grid[0])
+    assert PM.rel_fro(maps.cpu().numpy(), ref.maps) < 1e-5
+    assert np.allclose(lam.cpu().numpy(), ref.lambda_min_map, rtol=1e-6, atol=1e-9)
+    assert np.array_equal(mask.cpu().numpy(), ref.support_mask)

@@ -88,3 +88,97 @@ def test_slice_data_independent_of_partition():
     full = phantom.generate("C3", slices=6, full_dims=(32, 32), channels=4)
     part = phantom.generate("C3", slices=6, full_dims=(32, 32), channels=4, slice_range=(3, 6))
     assert np.array_equal(full.calib[3:], part.calib)
+
+
+# --------------------------------------------------------------- C4: z-slabs
+ZS = dict(full=(12, 10, 10), grid=(8, 8, 6), calib=(6, 6, 6), q=3)
+
+
+class _OracleOps:
+    """The z-slab driver's operations on the FP64 oracle (CPU tensors)."""
+
+    def __init__(self, calib, cfg_o):
+        from oracle import oracle as O
+        self.O = O
+        res = O.estimate_maps(O.Calib(calib.data.astype(np.complex128), calib.center_offset), ZS["full"], cfg_o,
+                              grid_dims=ZS["grid"], want_raw=True)
+        self.norm = O.normalize_maps(res.raw_maps, O.Calib(calib.data.astype(np.complex128),
+                                                           calib.center_offset))[0].astype(np.complex64)
+        self.lam = res.raw_lambda.astype(np.float32)
+        self.final = res
+
+    def raw_slab(self, calib, full_dims, cfg, slab):
+        import torch
+        a, b = slab
+        return torch.from_numpy(self.norm[:, a:b].copy()), torch.from_numpy(self.lam[a:b].copy())
+
+    def interpolate_maps(self, low, full_dims):
+        import torch
+        return torch.from_numpy(self.O.interpolate_maps(low.numpy(), full_dims).astype(np.complex64))
+
+    def interpolate_real(self, low, full_dims):
+        import torch
+        return torch.from_numpy(self.O.interpolate_real(low.numpy(), full_dims).astype(np.float32))
+
+    def sos_accumulate(self, maps, sos):
+        sos += (maps.real ** 2 + maps.imag ** 2).sum(0)
+        return sos
+
+    def renormalize(self, maps, sos):
+        import torch
+        pos = sos > 0
+        maps[:, pos] = maps[:, pos] / torch.sqrt(sos[pos])
+        return maps
+
+    def support_mask(self, lam, thr):
+        return (lam < thr).to(dtype=__import__("torch").uint8)
+
+
+def _zs_case():
+    from oracle import oracle as O
+    from paper_2302_13431_b200 import api as A
+    sc = O.simulate(ZS["q"], ZS["full"], 1, 5, noise_sigma=0.01, noise_seed=3)
+    cal = O.extract_calibration(sc["kspace"], ZS["calib"])
+    calib = A.Calib(cal.data.astype(np.complex64), tuple(cal.center_offset))
+    ck = A.PipelineConfig(kernel=A.ELLIPSOID, tau=1, power_iters=12, grid_dims=ZS["grid"])
+    co = O.PipelineConfig.pisco()
+    co.tau, co.power_iters = 1, 12
+    return calib, ck, co
+
+
+def _zs_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    calib, ck, co = _zs_case()
+    maps, lam, mask, info = shard.estimate_maps_zslab(calib, ZS["full"], ck, _OracleOps(calib, co))
+    if rank == 0:
+        np.save(os.path.join(out_dir, "maps.npy"), maps.numpy())
+        np.save(os.path.join(out_dir, "lam.npy"), lam.numpy())
+        np.save(os.path.join(out_dir, "mask.npy"), mask.numpy())
+    np.save(os.path.join(out_dir, f"slab{rank}.npy"), np.array(info["slab"]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_zslab_two_rank_gloo_equals_single_process(tmp_path):
+    """SURVEY §8e for C4: z-slab G(x)/power iteration per rank, all-gather of the
+    low-resolution maps, channel-split interpolation with an all-reduced SoS.
+    Two gloo ranks must reproduce the single-process composition and the
+    oracle's own finalize (maps.cpp:236-258)."""
+    import torch.multiprocessing as mp
+    mp.spawn(_zs_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    calib, ck, co = _zs_case()
+    ops = _OracleOps(calib, co)
+    maps1, lam1, mask1, _ = shard.estimate_maps_zslab(calib, ZS["full"], ck, ops)
+    maps2 = np.load(tmp_path / "maps.npy")
+    assert [tuple(np.load(tmp_path / f"slab{r}.npy")) for r in range(2)] == [(0, 4), (4, 8)]
+    assert maps2.shape == maps1.shape == (ZS["q"],) + ZS["full"]
+    assert np.allclose(maps2, maps1.numpy(), rtol=1e-5, atol=1e-6)
+    assert np.array_equal(np.load(tmp_path / "lam.npy"), lam1.numpy())
+    assert np.array_equal(np.load(tmp_path / "mask.npy"), mask1.numpy())
+    ref = ops.final  # the oracle's own interpolate + renormalise + mask
+    num = np.linalg.norm(maps2 - ref.maps)
+    assert num / np.linalg.norm(ref.maps) < 1e-5
+    assert np.allclose(np.load(tmp_path / "lam.npy"), ref.lambda_min_map, rtol=1e-5, atol=1e-7)
