@@ -100,7 +100,9 @@ class DeviceOps:
         grid = api._grid_for(calib.dims, full_dims, cfg)
         q = calib.channels
         shape = (slab[1] - slab[0],) + tuple(grid[1:])
-        cal = torch.from_numpy(np.ascontiguousarray(calib.data, dtype=np.complex64)).to(self.device)
+        cal = calib.data if isinstance(calib.data, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(calib.data, dtype=np.complex64))
+        cal = cal.to(self.device).contiguous()
         maps = torch.empty((q,) + shape, dtype=torch.complex64, device=self.device)
         lam = torch.empty(shape, dtype=torch.float32, device=self.device)
         api.estimate_raw_slab_device(self.ctx, cal.data_ptr(), calib.dims, calib.center_offset, q, full_dims, cfg,
