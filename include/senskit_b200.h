@@ -153,6 +153,14 @@ int sk_interpolate_real(sk_ctx* ctx, int ndim, const int64_t* low_dims, const fl
 /* support_mask (maps.hpp:105, maps.cpp:47-52). */
 int sk_support_mask(sk_ctx* ctx, int64_t voxels, const float* lambda, double mask_threshold, uint8_t* mask);
 
+/* ------------------------------------------------------------- metrics */
+/* projection_residual (metrics.hpp, metrics.cpp:11-49): sqrt(sum_j ||rho_j -
+ * c_j c_j^H rho_j / ||c_j||^2||^2 / sum_j ||rho_j||^2) with rho the unitary
+ * image of the k-space stack (channels x dims, channel-major) and c the maps
+ * (same shape).  FP64 accumulation, deterministic. */
+int sk_projection_residual(sk_ctx* ctx, int ndim, const int64_t* dims, int64_t channels, const sk_c64* kspace,
+                           const sk_c64* maps, double* value);
+
 /* ------------------------------------------------- z-slab sharding (§8e) */
 /* pipeline::compute_field + solve_field + the per-voxel half of finalize
  * (maps.hpp:115-123, maps.cpp:195-230, 117-172) restricted to rows

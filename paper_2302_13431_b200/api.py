@@ -173,6 +173,7 @@ _SIGS = {
     "sk_debug_small_eigh": ([_VP, _I64, _VP, _VP], _I32),
     "sk_estimate_raw_slab": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _I64, _I64, _VP, _VP, _VP], _I32),
     "sk_sos_accumulate": ([_VP, _I64, _I64, _VP, _VP], _I32),
+    "sk_projection_residual": ([_VP, _I32, _VP, _I64, _VP, _VP, _VP], _I32),
     "sk_renormalize_sos": ([_VP, _I64, _I64, _VP, _VP], _I32),
     "sk_estimate_maps": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP], _I32),
     "sk_estimate_maps_debug": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
@@ -460,6 +461,18 @@ def estimate_maps(calib: Calib, full_dims, cfg: PipelineConfig, ctx: Context | N
         fieldb.reshape(ngrid, q, q).transpose(0, 2, 1) if want_field else None, raw, raw_l,
         extra={"eig_solver": "full" if prov.eig_solver_used == 1 else "subspace", "certified": bool(prov.certified),
                "subspace_iterations": int(prov.subspace_iterations), "subspace_block": int(prov.subspace_block)})
+
+
+def projection_residual(kspace: np.ndarray, maps: np.ndarray, ctx: Context | None = None) -> float:
+    """projection_residual (metrics.cpp:11-49): kspace and maps (Q, *dims)."""
+    k = _c64(kspace)
+    m = _c64(maps)
+    if k.shape != m.shape:
+        raise DimError("data and maps must share dims and channel count")
+    v = C.c_double(0.0)
+    _check(lib().sk_projection_residual(_ctx(ctx), k.ndim - 1, _p(_i64(k.shape[1:])), k.shape[0], _p(k), _p(m),
+                                        C.byref(v)))
+    return float(v.value)
 
 
 def estimate_raw_slab(calib: Calib, full_dims, cfg: PipelineConfig, slab, ctx: Context | None = None):

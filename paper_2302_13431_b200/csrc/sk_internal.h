@@ -194,6 +194,13 @@ void renormalize_and_mask(sk_ctx* ctx, float2* maps, i64 n, int q, const float2*
                           uint8_t* mask, float thr);
 void mask_kernel(sk_ctx* ctx, const float* lambda, i64 n, float thr, uint8_t* mask);
 void sos_accumulate(sk_ctx* ctx, const float2* maps, i64 n, int q, float* sos);   // sos += sum_c |maps_c|^2
+// projection_residual value (metrics.cpp:11-49) from the unitary image and the maps (synchronous).
+double projection_residual_value(sk_ctx* ctx, const float2* img, const float2* maps, i64 n, int q);
+// Centred transform along one axis (fft.cpp kspace_to_image / image_to_kspace):
+// out = fftshift(DFT(ifftshift(in))) * scale, inverse = conjugate kernel.
+// Returns false (nothing launched) unless N and inner are powers of two.
+bool centered_fft_axis(sk_ctx* ctx, const void* in, void* out, i64 batch, int N, i64 inner, bool inverse,
+                       double scale);
 void renorm_with_sos(sk_ctx* ctx, float2* maps, i64 n, int q, const float* sos);  // maps /= sqrt(sos) where > 0
 void real_to_c64(sk_ctx* ctx, const float* in, float2* out, i64 n);
 void real_to_c128(sk_ctx* ctx, const float* in, double2* out, i64 n);

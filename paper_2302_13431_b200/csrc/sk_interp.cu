@@ -182,6 +182,62 @@ __global__ void __launch_bounds__(256) interp_fft_kernel(const typename Cplx<R>:
   }
 }
 
+// Centred transform along one axis (fft.cpp:71-112 kspace_to_image /
+// image_to_kspace): out = fftshift(DFT_sign(ifftshift(x))) * scale, one CTA
+// per T lines, same shared-memory FFT as the interpolation.
+template <typename R>
+__global__ void __launch_bounds__(256) centered_fft_kernel(const typename Cplx<R>::T* __restrict__ in,
+                                                           typename Cplx<R>::T* __restrict__ out, unsigned lines_total,
+                                                           int log_inner, int logT, int logN, bool inverse, R scale) {
+  using C = typename Cplx<R>::T;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int N = 1 << logN, T = 1 << logT;
+  C* tw = reinterpret_cast<C*>(smem_raw);
+  C* buf = tw + N / 2;
+  const int ld = N + N / 16 + 1;
+  for (int k = threadIdx.x; k < N / 2; k += blockDim.x) {
+    R s, c;
+    if constexpr (sizeof(R) == 8) {
+      sincospi(-2.0 * double(k) / double(N), &s, &c);
+    } else {
+      sincospif(-2.0f * float(k) / float(N), &s, &c);
+    }
+    tw[k].x = c;
+    tw[k].y = s;
+  }
+  const unsigned l0 = blockIdx.x << logT;
+  const int CL = N / 2;
+  const bool across = log_inner >= logT;
+  const unsigned imask = (1u << log_inner) - 1u;
+  auto index = [&](unsigned line, int a) -> size_t {
+    const unsigned b = line >> log_inner, i = line & imask;
+    return ((size_t(b) << logN) + a) * (size_t(1) << log_inner) + i;
+  };
+  for (int e = threadIdx.x; e < (T << logN); e += blockDim.x) {
+    const int t = across ? (e & (T - 1)) : (e >> logN);
+    const int a = across ? (e >> logT) : (e & (N - 1));
+    const unsigned line = l0 + t;
+    C v;
+    v.x = R(0);
+    v.y = R(0);
+    if (line < lines_total) v = in[index(line, (a + CL) & (N - 1))];  // ifftshift
+    buf[t * ld + pz(bitrev(a, logN))] = v;
+  }
+  __syncthreads();
+  fft_lines(buf, logT, ld, logN, tw, 0, inverse);
+  for (int e = threadIdx.x; e < (T << logN); e += blockDim.x) {
+    const int t = across ? (e & (T - 1)) : (e >> logN);
+    const int jj = across ? (e >> logT) : (e & (N - 1));
+    const unsigned line = l0 + t;
+    if (line < lines_total) {
+      C v = buf[t * ld + pz((jj - CL) & (N - 1))];  // fftshift
+      v.x *= scale;
+      v.y *= scale;
+      out[index(line, jj)] = v;
+    }
+  }
+}
+
 template <typename R>
 void launch_interp(sk_ctx* ctx, const void* in, void* out, i64 batch, int n, int N, i64 inner) {
   using C = typename Cplx<R>::T;
@@ -204,6 +260,27 @@ void launch_interp(sk_ctx* ctx, const void* in, void* out, i64 batch, int n, int
 }
 
 }  // namespace
+
+bool centered_fft_axis(sk_ctx* ctx, const void* in, void* out, i64 batch, int N, i64 inner, bool inverse,
+                       double scale) {
+  const bool pow2 = N >= 2 && !(N & (N - 1)) && inner > 0 && !(inner & (inner - 1));
+  if (!pow2 || N > 1024 || batch * inner >= (i64(1) << 31)) return false;
+  using C = float2;
+  const int logN = __builtin_ctz(unsigned(N));
+  const int ld = N + N / 16 + 1;
+  int T = 32;
+  while (T > 1 && size_t(T) * ld * sizeof(C) + size_t(N / 2) * sizeof(C) > 110 * 1024) T /= 2;
+  const int logT = __builtin_ctz(unsigned(T));
+  const size_t smem = size_t(T) * ld * sizeof(C) + size_t(N / 2) * sizeof(C);
+  set_smem_limit(reinterpret_cast<const void*>(centered_fft_kernel<float>), smem);
+  const i64 lines = batch * inner;
+  centered_fft_kernel<float><<<unsigned((lines + T - 1) / T), 256, smem, ctx->stream>>>(
+      static_cast<const C*>(in), static_cast<C*>(out), unsigned(lines),
+      __builtin_ctzll(static_cast<unsigned long long>(inner)), logT, logN, inverse, float(scale));
+  ++ctx->launches;
+  SKB_LAUNCH("centered_fft_kernel");
+  return true;
+}
 
 bool interp_axis_fft(sk_ctx* ctx, const void* in, void* out, i64 batch, int n, int N, i64 inner, bool fp64) {
   const bool pow2 = n > 0 && N > 0 && !(n & (n - 1)) && !(N & (N - 1)) && inner > 0 && !(inner & (inner - 1));

@@ -5,6 +5,9 @@
 // (maps.cpp:242-258), and the standalone normalize_maps epilogue.
 #include "sk_internal.h"
 
+#include <cmath>
+#include <vector>
+
 namespace skb {
 
 namespace {
@@ -318,6 +321,68 @@ void renorm_with_sos(sk_ctx* ctx, float2* maps, i64 n, int q, const float* sos) 
   ++ctx->launches;
   SKB_LAUNCH("renorm_sos");
 }
+// projection_residual (metrics.cpp:11-49), per block: sum_j ||rho_j||^2 and
+// sum_j ||rho_j - c_j (c_j^H rho_j / ||c_j||^2)||^2 in FP64 (rho = unitary
+// image of the k-space data, c = maps, voxel-major over channels).
+__global__ void __launch_bounds__(256) residual_partial_kernel(const float2* __restrict__ img,
+                                                               const float2* __restrict__ maps, i64 n, int q,
+                                                               double2* __restrict__ partial) {
+  double num = 0.0, den = 0.0;
+  for (i64 j = i64(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += i64(gridDim.x) * blockDim.x) {
+    double rr = 0.0, cn = 0.0, dx = 0.0, dy = 0.0;
+    for (int c = 0; c < q; ++c) {
+      const float2 r = img[i64(c) * n + j], m = maps[i64(c) * n + j];
+      rr += double(r.x) * r.x + double(r.y) * r.y;
+      cn += double(m.x) * m.x + double(m.y) * m.y;
+      dx += double(m.x) * r.x + double(m.y) * r.y;  // conj(c) . rho
+      dy += double(m.x) * r.y - double(m.y) * r.x;
+    }
+    den += rr;
+    if (cn > 0.0) {
+      const double kx = dx / cn, ky = dy / cn;
+      double s = 0.0;
+      for (int c = 0; c < q; ++c) {
+        const float2 r = img[i64(c) * n + j], m = maps[i64(c) * n + j];
+        const double ex = double(r.x) - (double(m.x) * kx - double(m.y) * ky);
+        const double ey = double(r.y) - (double(m.x) * ky + double(m.y) * kx);
+        s += ex * ex + ey * ey;
+      }
+      num += s;
+    } else {
+      num += rr;
+    }
+  }
+  __shared__ double sn[256], sd[256];
+  sn[threadIdx.x] = num;
+  sd[threadIdx.x] = den;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (int(threadIdx.x) < o) {
+      sn[threadIdx.x] += sn[threadIdx.x + o];
+      sd[threadIdx.x] += sd[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = make_double2(sn[0], sd[0]);
+}
+
+double projection_residual_value(sk_ctx* ctx, const float2* img, const float2* maps, i64 n, int q) {
+  const int blocks = int(std::min<i64>((n + 255) / 256, 4 * i64(ctx->sm_count)));
+  double2* partial = ctx->arena.get<double2>("res:partial", std::max(blocks, 1));
+  residual_partial_kernel<<<std::max(blocks, 1), 256, 0, ctx->stream>>>(img, maps, n, q, partial);
+  ++ctx->launches;
+  SKB_LAUNCH("residual_partial");
+  std::vector<double2> h(size_t(std::max(blocks, 1)));
+  SKB_CUDA(cudaMemcpyAsync(h.data(), partial, h.size() * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+  SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  double num = 0.0, den = 0.0;
+  for (const double2& v : h) {  // fixed order: deterministic
+    num += v.x;
+    den += v.y;
+  }
+  return den > 0.0 ? std::sqrt(num / den) : 0.0;
+}
+
 void mask_kernel(sk_ctx* ctx, const float* lambda, i64 n, float thr, uint8_t* mask) {
   mask_only_kernel<<<SKB_GRID(n)>>>(lambda, n, thr, mask);
   ++ctx->launches;

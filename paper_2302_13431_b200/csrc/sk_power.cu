@@ -542,9 +542,17 @@ bool encode_planes(CUtensorMap* m, const float2* base, i64 n, int h, int vpb, in
   const cuuint64_t strides[1] = {cuuint64_t(n) * 8};
   const cuuint32_t box[2] = {cuuint32_t(vpb), cuuint32_t(hb)};
   const cuuint32_t estr[2] = {1, 1};
+  // L2 promotion of the 8*vpb-byte box rows (SKB_TMA_PROMO = 0 none, 64, 128, 256)
+  static const CUtensorMapL2promotion promo = [] {
+    const char* v = std::getenv("SKB_TMA_PROMO");
+    const int p = v ? std::atoi(v) : 256;
+    return p == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                  : p == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                            : p == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }();
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<float2*>(base), dims, strides, box, estr,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
 }
 
 template <class L>

@@ -1681,6 +1681,43 @@ int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, con
   });
 }
 
+int sk_projection_residual(sk_ctx* ctx, int ndim, const int64_t* dims, int64_t channels, const sk_c64* kspace,
+                           const sk_c64* maps, double* value) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (ndim < 1 || channels < 1 || !value) fail(SK_ERR_DIM, "bad arguments");
+    const Dims d = dims_of(ndim, dims);
+    for (i64 e : d)
+      if (e < 1) fail(SK_ERR_DIM, "stack axis extents must be >= 1");
+    const i64 n = numel(d), cnt = channels * n;
+    const float2* d_k = device_in(ctx, reinterpret_cast<const float2*>(kspace), cnt, "in:res_kspace");
+    const float2* d_m = device_in(ctx, reinterpret_cast<const float2*>(maps), cnt, "in:res_maps");
+    // image = kspace_to_image_unitary per channel (metrics.cpp:21-27, fft.cpp:105-112)
+    float2* bufs[2] = {ctx->arena.get<float2>("res:img_a", cnt), ctx->arena.get<float2>("res:img_b", cnt)};
+    const float2* src = d_k;
+    int which = 0;
+    for (int a = ndim - 1; a >= 0; --a) {
+      const int N = int(d[size_t(a)]);
+      if (N == 1) continue;
+      i64 b = channels, inner = 1;
+      for (int k = 0; k < a; ++k) b *= d[size_t(k)];
+      for (int k = a + 1; k < ndim; ++k) inner *= d[size_t(k)];
+      float2* dst = bufs[which];
+      if (!centered_fft_axis(ctx, src, dst, b, N, inner, true, 1.0))
+        apply_axis(ctx, src, dst, dft_matrix(ctx, N, N, center_index(N), center_index(N), +1, 0.0), b, N, N, inner);
+      src = dst;
+      which ^= 1;
+    }
+    float2* img = const_cast<float2*>(src);
+    if (src == d_k) {  // every extent is 1
+      img = bufs[0];
+      SKB_CUDA(cudaMemcpyAsync(img, d_k, size_t(cnt) * sizeof(float2), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    // the unitary scale 1/sqrt(N) cancels in sqrt(num / den): both sums scale by 1/N
+    *value = projection_residual_value(ctx, img, d_m, n, int(channels));
+  });
+}
+
 int sk_estimate_raw_slab(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset,
                          int64_t q, const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg,
                          int64_t slab_begin, int64_t slab_end, sk_c64* maps, float* lambda, sk_provenance* prov) {

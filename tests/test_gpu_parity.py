@@ -419,3 +419,68 @@ def test_zslab_driver_device_ops(K):
     assert PM.rel_fro(maps.cpu().numpy(), ref.maps) < 1e-5
     assert np.allclose(lam.cpu().numpy(), ref.lambda_min_map, rtol=1e-6, atol=1e-9)
     assert np.array_equal(mask.cpu().numpy(), ref.support_mask)
+
+
+# ------------------------------------------------- metrics
+def test_projection_residual_known_answers(K, O):  # test_metrics.cpp:24-70
+    sc = O.simulate(4, (32, 32), 2, 91, noise_sigma=0.0)
+    assert K.api.projection_residual(sc["kspace"], sc["true_maps"]) < 1e-6  # true maps span noiseless data
+    single = O.simulate(1, (16, 16), 1, 92, noise_sigma=0.0)["kspace"]
+    data = np.zeros((2, 16, 16), np.complex64)
+    data[0] = single[0]
+    maps = np.zeros((2, 16, 16), np.complex64)
+    maps[1] = 1.0
+    assert abs(K.api.projection_residual(data, maps) - 1.0) < 1e-7  # orthogonal maps
+    d = rnd((3, 12, 12), 93)
+    m = rnd((3, 12, 12), 94)
+    base = K.api.projection_residual(d, m)
+    ph = np.exp(1j * np.random.default_rng(95).uniform(0, 6.28, (12, 12)))
+    pert = K.api.projection_residual(d * (-1.7 + 0.4j), m * ph[None])
+    assert abs(pert - base) < 1e-6  # invariant to data scaling and per-voxel map phase
+    with pytest.raises(K.DimError):
+        K.api.projection_residual(rnd((2, 8, 8), 96), rnd((2, 8, 10), 97))
+
+
+@pytest.mark.parametrize("dims", [(64, 64), (24, 20), (16, 12, 8)])
+def test_projection_residual_parity(K, O, dims):
+    """GPU residual (FFT path for power-of-two extents, DFT matrices otherwise)
+    against the oracle on estimated maps."""
+    sc = O.simulate(6, dims, 1, 7, noise_sigma=0.02, noise_seed=4)
+    k = sc["kspace"].astype(np.complex64)
+    maps = (sc["true_maps"] * np.exp(0.3j)).astype(np.complex64) + 0.05 * rnd((6,) + dims, 8)
+    got = K.api.projection_residual(k, maps)
+    ref = O.projection_residual(f32(k), f32(maps))
+    report("projection_residual", dims=list(dims), got=got, ref=ref)
+    assert abs(got - ref) <= 1e-5 * ref
+
+
+# ----------------------------------------------- CLI estimate (SURVEY §8f item 2)
+def test_cli_estimate_end_to_end(K, O, tmp_path, capsys):
+    """senskit estimate on the B200 path: CStack in, CStacks + spectrum + provenance out
+    (senskit_main.cpp:139-184); maps equal the API's, residual matches the oracle."""
+    from paper_2302_13431_b200 import cli
+    from paper_2302_13431_b200.cstack import Stack, load_stack, save_stack
+    sc = O.simulate(4, (48, 48), 2, 21, noise_sigma=0.01, noise_seed=5)
+    k = sc["kspace"].astype(np.complex64)
+    save_stack(Stack(k, "kspace"), str(tmp_path / "in"))
+    out = str(tmp_path / "run")
+    rc = cli.main(["estimate", "--input", str(tmp_path / "in"), "--calib", "20", "--tau", "2", "--grid", "reduced",
+                   "--grid-pad", "12", "--power-iters", "20", "--output", out])
+    assert rc == 0
+    line = capsys.readouterr().out.strip().splitlines()[-1]
+    assert line.startswith("R=") and "residual=" in line
+    maps = load_stack(out + "_maps")
+    lam = load_stack(out + "_lambda")
+    mask = load_stack(out + "_mask")
+    prov = json.load(open(out + "_provenance.json"))
+    calib = cli.extract_calibration(k, (20, 20))
+    cfg = K.PipelineConfig(tau=2, grid=K.GRID_REDUCED, grid_pad=12, power_iters=20)
+    ref = K.estimate_maps(calib, (48, 48), cfg)
+    assert maps.domain == "image" and maps.data.shape == (4, 48, 48)
+    assert np.array_equal(maps.data, ref.maps)
+    assert np.array_equal(lam.data[0].real, ref.lambda_min_map)
+    assert np.array_equal(mask.data[0].real.astype(np.uint8), ref.support_mask)
+    assert prov["nullspace_rank"] == ref.nullspace_rank and prov["subcommand"] == "estimate"
+    ref_res = O.projection_residual(f32(k), f32(ref.maps))
+    assert abs(prov["residual"] - ref_res) <= 1e-5 * ref_res
+    assert (tmp_path / "run_mag_ch03.pgm").exists() and (tmp_path / "run_spectrum.csv").exists()
