@@ -105,10 +105,10 @@ struct TmaTiles {
   int hb = 0, nb = 0;
 };
 
-template <int QP_, int RPT_, int THREADS_, int MINB_, int ACC_ = 0, int CHUNK_ = 8>
+template <int QP_, int RPT_, int THREADS_, int MINB_, int ACC_ = 0, int PF_ = 4>
 struct Layout {
   static constexpr int QP = QP_, RPT = RPT_, kThreads = THREADS_, kMinBlocks = MINB_;
-  static constexpr int kChunkCols = CHUNK_;  // v columns staged per load batch
+  static constexpr int kPrefetch = PF_;  // LDS.128 of v kept in flight ahead of their use
   static constexpr int kTPV = QP / RPT;          // threads per voxel
   static constexpr int kVPB = kThreads / kTPV;   // voxels per block
   static constexpr int kWPV = kTPV > 32 ? kTPV / 32 : 1;  // warps per voxel
@@ -327,23 +327,30 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       for (int r = 0; r < RPT; ++r)
 #pragma unroll
         for (int k = 0; k < A; ++k) acc[r][k] = acc2[r][k] = 0ull;
-      constexpr int kChunk = QP < L::kChunkCols ? QP : L::kChunkCols;
+      // v arrives as NT float4 (two columns each) through a rotating buffer
+      // of D register sets.  (ptxas re-sinks each load next to its use under
+      // the 128-register budget whatever D is — measured: the loop is
+      // short-scoreboard bound on these loads; 1-block/255-register and
+      // two-rows-per-thread layouts that could keep loads in flight lose more
+      // to the halved occupancy.)
+      constexpr int NT = QP / 2 > 0 ? QP / 2 : 1;
+      constexpr int D = L::kPrefetch < NT ? L::kPrefetch : NT;
+      float4 buf[D];
 #pragma unroll
-      for (int cb = 0; cb < QP; cb += kChunk) {
-        float4 vv[kChunk / 2];
+      for (int t = 0; t < D; ++t) buf[t] = v4[t];
 #pragma unroll
-        for (int t = 0; t < kChunk / 2; ++t) vv[t] = v4[cb / 2 + t];
+      for (int t = 0; t < NT; ++t) {
+        const float4 vt = buf[t % D];
+        if (t + D < NT) buf[t % D] = v4[t + D];
 #pragma unroll
-        for (int t = 0; t < kChunk / 2; ++t)
-#pragma unroll
-          for (int r = 0; r < RPT; ++r) {
-            const float2 ma = m[r][cb + 2 * t], mb = m[r][cb + 2 * t + 1];
-            const int ka = (2 * t) % A, kb = (2 * t + 1) % A;
-            ffma2(acc[r][ka], pk(ma.x, ma.x), pk(vv[t].x, vv[t].y));
-            ffma2(acc2[r][ka], pk(ma.y, ma.y), pk(vv[t].y, vv[t].x));
-            ffma2(acc[r][kb], pk(mb.x, mb.x), pk(vv[t].z, vv[t].w));
-            ffma2(acc2[r][kb], pk(mb.y, mb.y), pk(vv[t].w, vv[t].z));
-          }
+        for (int r = 0; r < RPT; ++r) {
+          const float2 ma = m[r][2 * t], mb = m[r][2 * t + 1];
+          const int ka = (2 * t) % A, kb = (2 * t + 1) % A;
+          ffma2(acc[r][ka], pk(ma.x, ma.x), pk(vt.x, vt.y));
+          ffma2(acc2[r][ka], pk(ma.y, ma.y), pk(vt.y, vt.x));
+          ffma2(acc[r][kb], pk(mb.x, mb.x), pk(vt.z, vt.w));
+          ffma2(acc2[r][kb], pk(mb.y, mb.y), pk(vt.w, vt.z));
+        }
       }
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
@@ -607,10 +614,14 @@ void power_iteration(sk_ctx* ctx, const PowerArgs& a) {
     launch<Layout<16, 1, 256, 2>>(ctx, a);
   else if (a.q <= 32)
     switch (k4v) {  // SKB_K4_VARIANT: accumulator pairs / staged columns (experiments)
-      case 1: launch<Layout<32, 1, 256, 2, 2, 8>>(ctx, a); break;
-      case 2: launch<Layout<32, 1, 256, 2, 4, 8>>(ctx, a); break;
-      case 3: launch<Layout<32, 1, 256, 2, 4, 16>>(ctx, a); break;
-      default: rpt32 == 1 ? launch<Layout<32, 1, 256, 2, 2, 16>>(ctx, a) : launch<Layout<32, 2, 128, 3>>(ctx, a);
+      case 1: launch<Layout<32, 1, 256, 2, 2, 2>>(ctx, a); break;
+      case 2: launch<Layout<32, 1, 256, 2, 2, 6>>(ctx, a); break;
+      case 3: launch<Layout<32, 1, 256, 2, 4, 4>>(ctx, a); break;
+      case 4: launch<Layout<32, 1, 256, 2, 2, 3>>(ctx, a); break;
+      case 5: launch<Layout<32, 1, 256, 1, 2, 4>>(ctx, a); break;
+      case 6: launch<Layout<32, 2, 256, 1, 2, 4>>(ctx, a); break;
+      case 7: launch<Layout<32, 1, 256, 1, 4, 6>>(ctx, a); break;
+      default: rpt32 == 1 ? launch<Layout<32, 1, 256, 2, 2, 4>>(ctx, a) : launch<Layout<32, 2, 128, 3>>(ctx, a);
     }
   else if (a.q <= 64)
     launch<Layout<64, 1, 256, 1>>(ctx, a);
