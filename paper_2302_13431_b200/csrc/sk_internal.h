@@ -235,6 +235,8 @@ bool trsm_rows_lower(sk_ctx* ctx, double2* x, i64 n, int b, const double2* l);
 // one-CTA Cholesky + triangular inverse (M = L^{-1}, flag raised on a
 // non-positive pivot), X <- X M^H.  Returns false (nothing launched) for b > 64.
 bool cholqr_pass(sk_ctx* ctx, double2* x, i64 n, int b, double2* s, double2* m, int* flag);
+// One-CTA blocked Cholesky (b <= 64): S = L L^H, L lower column-major like POTRF; *flag on a bad pivot.
+void cholesky_blocked(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag);
 // One CholQR pass on X (n x b, b <= 118): cross_gram + one-CTA lazy Cholesky +
 // warp-per-row triangular solve; no host synchronisation (flag raised on failure).
 void cholqr_fast(sk_ctx* ctx, double2* x, i64 n, int b, double2* s, double2* l, int* flag);

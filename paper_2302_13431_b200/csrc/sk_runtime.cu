@@ -631,6 +631,7 @@ bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int 
     if (v && std::string(v) == "fast") return 0;
     if (v && std::string(v) == "custom") return 2;
     if (v && std::string(v) == "pass64") return 3;
+    if (v && std::string(v) == "blocked") return 4;
     return 1;
   }();
   if (chol_mode == 3 && b <= 64) {
@@ -639,7 +640,8 @@ bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int 
     for (int pass = 0; pass < passes; ++pass) cholqr_pass(ctx, x, n, int(b), S, Mi, flag);
     return true;
   }
-  const bool lib_chol = chol_mode == 1 || chol_mode == 3 || b > kSmallBlockMax;
+  const bool own_blocked = chol_mode == 4 && b <= 64;
+  const bool lib_chol = !own_blocked && (chol_mode == 1 || chol_mode == 3 || b > kSmallBlockMax);
   if (b > 256 || (chol_mode == 2 && b > kSmallBlockMax)) {
     for (int p = 0; p < passes; ++p)
       if (!cholqr(ctx, x, n, b)) return false;
@@ -676,6 +678,8 @@ bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int 
                      "Xpotrf");
       ++ctx->lib_calls;
       L = S;
+    } else if (own_blocked) {
+      cholesky_blocked(ctx, S, int(b), L, flag + 1);  // S = L L^H (POTRF layout)
     } else {
       cholesky_small(ctx, S, int(b), L, flag);  // S = L L^H
     }

@@ -455,6 +455,110 @@ __global__ void __launch_bounds__(kCholThreads) chol_inv64_kernel(const double2*
   for (int e = tid; e < b * b; e += kCholThreads) m_out[e] = M[(e / b) * ld + e % b];  // row-major
 }
 
+// Blocked one-CTA Cholesky S = L L^H for b <= 64 (lower, column-major in and
+// out, like cusolverDnXpotrf): 16-column block steps; the diagonal block is
+// factored by one warp (warp-synchronous), the panel below by row-parallel
+// forward substitution, the trailing lower triangle by all threads.  A
+// non-positive pivot raises *flag (POTRF's info).
+constexpr int kBlkNB = 16;
+__global__ void __launch_bounds__(256) chol_blocked_kernel(const double2* __restrict__ s, int b,
+                                                           double2* __restrict__ l_out, int* flag) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* Am = reinterpret_cast<double2*>(smem_raw);  // [64][65]
+  double* rd = reinterpret_cast<double*>(Am + 64 * 65);  // 1 / L[j][j]
+#define A(i, c) Am[(i) * 65 + (c)]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {
+    double2 v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = tid + 256 * u;
+      v[u] = e < b * b ? s[e] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int e = tid + 256 * u;
+      if (e < b * b) A(e % b, e / b) = v[u];  // column-major source
+    }
+  }
+  __syncthreads();
+  for (int k0 = 0; k0 < b; k0 += kBlkNB) {
+    const int m = min(kBlkNB, b - k0);
+    // (1) diagonal block, warp 0
+    if (warp == 0) {
+      for (int j = 0; j < m; ++j) {
+        const int jj = k0 + j;
+        double d = A(jj, jj).x;
+        if (!(d > 0.0)) {
+          if (lane == 0) atomicExch(flag, 1);
+          d = 1e-300;
+        }
+        const double r = rsqrt(d);
+        __syncwarp();
+        if (lane == 0) {
+          A(jj, jj) = make_double2(d * r, 0.0);  // sqrt(d)
+          rd[jj] = r;
+        }
+        for (int i = j + 1 + lane; i < m; i += 32) {
+          const double2 a = A(k0 + i, jj);
+          A(k0 + i, jj) = make_double2(a.x * r, a.y * r);
+        }
+        __syncwarp();
+        // trailing update inside the block: A(i, c) -= L[i][j] conj(L[c][j]), j < c <= i < m
+        for (int e = lane; e < (m - j - 1) * (m - j - 1); e += 32) {
+          const int i = j + 1 + e / (m - j - 1), c = j + 1 + e % (m - j - 1);
+          if (c <= i) {
+            const double2 li = A(k0 + i, jj), lc = A(k0 + c, jj);
+            double2 a = A(k0 + i, k0 + c);
+            a.x -= li.x * lc.x + li.y * lc.y;
+            a.y -= li.y * lc.x - li.x * lc.y;
+            A(k0 + i, k0 + c) = a;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // (2) panel: rows i >= k0 + m solve A(i, k0:k0+m) <- A(i, k0:k0+m) L_kk^{-H}
+    for (int i = k0 + m + tid; i < b; i += 256) {
+      for (int j = 0; j < m; ++j) {
+        double2 a = A(i, k0 + j);
+        for (int c = 0; c < j; ++c) {  // a -= A(i, k0+c) conj(L[k0+j][k0+c])
+          const double2 x = A(i, k0 + c), lj = A(k0 + j, k0 + c);
+          a.x -= x.x * lj.x + x.y * lj.y;
+          a.y -= x.y * lj.x - x.x * lj.y;
+        }
+        const double r = rd[k0 + j];
+        A(i, k0 + j) = make_double2(a.x * r, a.y * r);
+      }
+    }
+    __syncthreads();
+    // (3) trailing lower triangle: A(i, c) -= sum_{j<m} L[i][k0+j] conj(L[c][k0+j]), k0+m <= c <= i < b
+    const int t0 = k0 + m, tn = b - t0;
+    for (int e = tid; e < tn * tn; e += 256) {
+      const int i = t0 + e / tn, c = t0 + e % tn;
+      if (c > i) continue;
+      double ax = 0.0, ay = 0.0;
+#pragma unroll 4
+      for (int j = 0; j < m; ++j) {
+        const double2 li = A(i, k0 + j), lc = A(c, k0 + j);
+        ax += li.x * lc.x + li.y * lc.y;
+        ay += li.y * lc.x - li.x * lc.y;
+      }
+      double2 a = A(i, c);
+      a.x -= ax;
+      a.y -= ay;
+      A(i, c) = a;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < b * b; e += 256) {
+    const int i = e % b, c = e / b;
+    l_out[e] = c <= i ? A(i, c) : make_double2(0.0, 0.0);
+  }
+}
+#undef A
+
 // X (n x b, column-major) <- X L^{-H}, L lower triangular column-major b x b
 // (cuSOLVER POTRF output), by forward substitution on each row:
 //   y_j = (x_j - sum_{k<j} y_k conj(L[j][k])) / L[j][j].
@@ -675,6 +779,15 @@ bool trsm_rows_lower(sk_ctx* ctx, double2* x, i64 n, int b, const double2* l) {
   ++ctx->launches;
   SKB_LAUNCH("trsm_pairs_kernel");
   return true;
+}
+
+void cholesky_blocked(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag) {
+  if (b < 1 || b > 64) fail(SK_ERR_UNSUPPORTED, "cholesky_blocked: b must be in [1, 64]");
+  const size_t smem = 64 * 65 * sizeof(double2) + 64 * sizeof(double);
+  set_smem_limit(reinterpret_cast<const void*>(chol_blocked_kernel), smem);
+  chol_blocked_kernel<<<1, 256, smem, ctx->stream>>>(s, b, l, flag);
+  ++ctx->launches;
+  SKB_LAUNCH("chol_blocked_kernel");
 }
 
 }  // namespace skb
