@@ -383,6 +383,70 @@ double projection_residual_value(sk_ctx* ctx, const float2* img, const float2* m
   return den > 0.0 ? std::sqrt(num / den) : 0.0;
 }
 
+// 3xTF32 split of complex operands for the K2 FP32 products (tensor cores):
+// x = hi + lo with hi = tf32(x), lo = tf32(x - hi); complex n x m (column-major)
+// becomes real [Re; Im] (2n x m) for the Gram and [Re, Im] (n x 2m) for the block.
+__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
+  unsigned h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  hi = __uint_as_float(h);
+  unsigned l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
+  lo = __uint_as_float(l);
+}
+__global__ void split_gram_kernel(const float2* __restrict__ a, i64 n, float* __restrict__ hi, float* __restrict__ lo) {
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n * n; e += i64(gridDim.x) * blockDim.x) {
+    const i64 r = e % n, c = e / n;
+    const float2 v = a[e];
+    float h, l;
+    tf32_split(v.x, h, l);
+    hi[r + c * 2 * n] = h;
+    lo[r + c * 2 * n] = l;
+    tf32_split(v.y, h, l);
+    hi[n + r + c * 2 * n] = h;
+    lo[n + r + c * 2 * n] = l;
+  }
+}
+__global__ void split_block_kernel(const double2* __restrict__ v, i64 n, i64 m, float* __restrict__ hi,
+                                   float* __restrict__ lo) {
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n * m; e += i64(gridDim.x) * blockDim.x) {
+    const i64 r = e % n, c = e / n;
+    const double2 x = v[e];
+    float h, l;
+    tf32_split(float(x.x), h, l);
+    hi[r + c * n] = h;
+    lo[r + c * n] = l;
+    tf32_split(float(x.y), h, l);
+    hi[r + (c + m) * n] = h;
+    lo[r + (c + m) * n] = l;
+  }
+}
+// Y = (C11 - C22) + i (C12 + C21) from C = [Re A; Im A] [Re V, Im V] (2n x 2m).
+__global__ void combine_block_kernel(const float* __restrict__ c, i64 n, i64 m, double2* __restrict__ y) {
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n * m; e += i64(gridDim.x) * blockDim.x) {
+    const i64 r = e % n, k = e / n;
+    const float c11 = c[r + k * 2 * n], c21 = c[n + r + k * 2 * n];
+    const float c12 = c[r + (k + m) * 2 * n], c22 = c[n + r + (k + m) * 2 * n];
+    y[e] = make_double2(double(c11) - double(c22), double(c12) + double(c21));
+  }
+}
+
+void split_gram_tf32(sk_ctx* ctx, const float2* a, i64 n, float* hi, float* lo) {
+  split_gram_kernel<<<SKB_GRID(n * n)>>>(a, n, hi, lo);
+  ++ctx->launches;
+  SKB_LAUNCH("split_gram");
+}
+void split_block_tf32(sk_ctx* ctx, const double2* v, i64 n, i64 m, float* hi, float* lo) {
+  split_block_kernel<<<SKB_GRID(n * m)>>>(v, n, m, hi, lo);
+  ++ctx->launches;
+  SKB_LAUNCH("split_block");
+}
+void combine_block(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y) {
+  combine_block_kernel<<<SKB_GRID(n * m)>>>(c, n, m, y);
+  ++ctx->launches;
+  SKB_LAUNCH("combine_block");
+}
+
 void mask_kernel(sk_ctx* ctx, const float* lambda, i64 n, float thr, uint8_t* mask) {
   mask_only_kernel<<<SKB_GRID(n)>>>(lambda, n, thr, mask);
   ++ctx->launches;

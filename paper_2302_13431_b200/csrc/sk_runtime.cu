@@ -822,6 +822,19 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   e.full = false;
   double2* A = ctx->arena.get<double2>("eig:A", n * n);
   c64_to_c128(ctx, gram, A, n * n);
+  // SKB_EARLY_GEMM: steering products as 3xTF32 tensor-core GEMMs (default),
+  // plain FP32 CGEMM ("fp32"), or single TF32 / BF16 (measured to slow convergence).
+  static const bool tf32x3 = [] {
+    const char* v = std::getenv("SKB_EARLY_GEMM");
+    return !v || std::string(v) == "tf32x3";
+  }();
+  float* ghi = nullptr;
+  float* glo = nullptr;
+  if (tf32x3) {
+    ghi = ctx->arena.get<float>("ss:ghi", 2 * n * n);
+    glo = ctx->arena.get<float>("ss:glo", 2 * n * n);
+    split_gram_tf32(ctx, gram, n, ghi, glo);
+  }
   laps.lap("promote");
   // Per-size hints from the previous call: block size and the number of
   // orthogonalised iterations before the (single) Rayleigh-Ritz check.
@@ -874,7 +887,26 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
     bool body_ok = true;
     auto body = [&]() {
       for (int i = 0; i < q_plan; ++i) {
-        if (i + 2 < q_plan) {
+        if (i + 2 < q_plan && tf32x3) {
+          // 3xTF32 on tensor cores: one real GEMM [Re A; Im A] [Re V, Im V] per
+          // hi/lo combination (hi.hi + hi.lo + lo.hi), FP32-level accuracy.
+          float* vh = ctx->arena.get<float>("ss:vh", n * 2 * bcap);
+          float* vl = ctx->arena.get<float>("ss:vl", n * 2 * bcap);
+          float* cc = ctx->arena.get<float>("ss:cc", 2 * n * 2 * bcap);
+          split_block_tf32(ctx, V, n, b, vh, vl);
+          const float one = 1.f, zero = 0.f;
+          const float* as[3] = {ghi, ghi, glo};
+          const float* bs[3] = {vh, vl, vh};
+          for (int g = 0; g < 3; ++g) {
+            check_cublas(cublasGemmEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(2 * n), int(2 * b), int(n), &one,
+                                      as[g], CUDA_R_32F, int(2 * n), bs[g], CUDA_R_32F, int(n), g == 0 ? &zero : &one,
+                                      cc, CUDA_R_32F, int(2 * n), CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT),
+                         "GemmEx(3xTF32)");
+            ++ctx->lib_calls;
+          }
+          combine_block(ctx, cc, n, b, Y);
+          laps.lap("gemm32");
+        } else if (i + 2 < q_plan) {
           // Early iterations only steer the span: FP32 CGEMM on the fp32 Gram
           // (its rounding ~1e-7 is removed by the FP64 iterations that follow);
           // orthonormalisation stays FP64 (kappa(A V)^2 exceeds 1/eps_fp32).
@@ -888,7 +920,7 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
           // the BF16x9 emulation does not take complex operands).
           static const cublasComputeType_t early = [] {
             const char* v = std::getenv("SKB_EARLY_GEMM");
-            if (v && std::string(v) == "tf32") return CUBLAS_COMPUTE_32F_FAST_TF32;
+            if (v && std::string(v) == "tf32") return CUBLAS_COMPUTE_32F_FAST_TF32;  // single TF32
             if (v && std::string(v) == "bf16") return CUBLAS_COMPUTE_32F_FAST_16BF;
             return CUBLAS_COMPUTE_32F;
           }();
