@@ -52,7 +52,8 @@ __device__ __forceinline__ int pz(int i) { return i + (i >> 4); }
 // half distance); twiddles tw[k << log_tw_stride] = exp(-i 2 pi k / (len << log_tw_stride)),
 // conjugated for the inverse.  All index math is shifts/masks.
 template <typename C>
-__device__ void fft_lines(C* buf, int log_lines, int ld, int log2len, const C* tw, int log_tw_stride, bool inverse) {
+__device__ __forceinline__ void fft_lines(C* buf, int log_lines, int ld, int log2len, const C* tw, int log_tw_stride,
+                                          bool inverse) {
   constexpr int RM = 4;
   for (int s0 = 1; s0 <= log2len; s0 += RM) {
     const int r = min(RM, log2len - s0 + 1);
@@ -96,11 +97,16 @@ __device__ void fft_lines(C* buf, int log_lines, int ld, int log2len, const C* t
 }
 
 // Lines are (b, i) pairs of a [batch][len][inner] volume; inner = 2^log_inner.
-template <typename R>
+// LOGN_ / LOGNN_ / LOGT_ >= 0 fix log2(n), log2(N), log2(T) at compile time
+// (all index math then folds to constants); -1 = runtime sizes.
+template <typename R, int LOGN_ = -1, int LOGNN_ = -1, int LOGT_ = -1>
 __global__ void __launch_bounds__(256) interp_fft_kernel(const typename Cplx<R>::T* __restrict__ in,
                                                          typename Cplx<R>::T* __restrict__ out, unsigned lines_total,
-                                                         int log_inner, int logT, int logn, int logN) {
+                                                         int log_inner, int logT_arg, int logn_arg, int logN_arg) {
   using C = typename Cplx<R>::T;
+  const int logn = LOGN_ >= 0 ? LOGN_ : logn_arg;
+  const int logN = LOGNN_ >= 0 ? LOGNN_ : logN_arg;
+  const int logT = LOGT_ >= 0 ? LOGT_ : logT_arg;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = 1 << logn, N = 1 << logN, T = 1 << logT;
   C* tw = reinterpret_cast<C*>(smem_raw);  // N/2 forward twiddles exp(-i 2 pi k / N)
@@ -238,6 +244,15 @@ __global__ void __launch_bounds__(256) centered_fft_kernel(const typename Cplx<R
   }
 }
 
+template <typename R, int LN, int LNN, int LT>
+void launch_interp_k(sk_ctx* ctx, const void* in, void* out, unsigned lines, int log_inner, int logT, int logn,
+                     int logN, size_t smem, unsigned blocks) {
+  using C = typename Cplx<R>::T;
+  set_smem_limit(reinterpret_cast<const void*>(interp_fft_kernel<R, LN, LNN, LT>), smem);
+  interp_fft_kernel<R, LN, LNN, LT><<<blocks, 256, smem, ctx->stream>>>(static_cast<const C*>(in), static_cast<C*>(out),
+                                                                        lines, log_inner, logT, logn, logN);
+}
+
 template <typename R>
 void launch_interp(sk_ctx* ctx, const void* in, void* out, i64 batch, int n, int N, i64 inner) {
   using C = typename Cplx<R>::T;
@@ -248,13 +263,21 @@ void launch_interp(sk_ctx* ctx, const void* in, void* out, i64 batch, int n, int
   while (T > 1 && (size_t(T) * ld * sizeof(C) + size_t(N / 2) * sizeof(C) > 110 * 1024 || T * n > 16 * 256)) T /= 2;
   const int logT = __builtin_ctz(unsigned(T));
   const size_t smem = size_t(T) * ld * sizeof(C) + size_t(N / 2) * sizeof(C);
-  set_smem_limit(reinterpret_cast<const void*>(interp_fft_kernel<R>), smem);
   const i64 lines = batch * inner;
-  const i64 blocks = (lines + T - 1) / T;
-  interp_fft_kernel<R><<<unsigned(blocks), 256, smem, ctx->stream>>>(static_cast<const C*>(in), static_cast<C*>(out),
-                                                                    unsigned(lines), __builtin_ctzll(
-                                                                        static_cast<unsigned long long>(inner)),
-                                                                    logT, logn, logN);
+  const unsigned blocks = unsigned((lines + T - 1) / T);
+  const int li = __builtin_ctzll(static_cast<unsigned long long>(inner));
+  // compile-time sizes for the BASELINE grids (64 -> 128/256, 128 -> 256), runtime otherwise
+  const int key = logn * 100 + logN * 10 + logT;
+  if constexpr (sizeof(R) == 4) {
+    switch (key) {
+      case 6 * 100 + 7 * 10 + 5: launch_interp_k<R, 6, 7, 5>(ctx, in, out, unsigned(lines), li, logT, logn, logN, smem, blocks); break;
+      case 6 * 100 + 8 * 10 + 5: launch_interp_k<R, 6, 8, 5>(ctx, in, out, unsigned(lines), li, logT, logn, logN, smem, blocks); break;
+      case 7 * 100 + 8 * 10 + 5: launch_interp_k<R, 7, 8, 5>(ctx, in, out, unsigned(lines), li, logT, logn, logN, smem, blocks); break;
+      default: launch_interp_k<R, -1, -1, -1>(ctx, in, out, unsigned(lines), li, logT, logn, logN, smem, blocks);
+    }
+  } else {
+    launch_interp_k<R, -1, -1, -1>(ctx, in, out, unsigned(lines), li, logT, logn, logN, smem, blocks);
+  }
   ++ctx->launches;
   SKB_LAUNCH("interp_fft_kernel");
 }
