@@ -105,9 +105,10 @@ struct TmaTiles {
   int hb = 0, nb = 0;
 };
 
-template <int QP_, int RPT_, int THREADS_, int MINB_, int ACC_ = 0, int PF_ = 4>
+template <int QP_, int RPT_, int THREADS_, int MINB_, int ACC_ = 0, int PF_ = 4, int QF_ = 0>
 struct Layout {
   static constexpr int QP = QP_, RPT = RPT_, kThreads = THREADS_, kMinBlocks = MINB_;
+  static constexpr int QF = QF_;  // > 0: the channel count is fixed at compile time (Q == QF)
   static constexpr int kPrefetch = PF_;  // LDS.128 of v kept in flight ahead of their use
   static constexpr int kTPV = QP / RPT;          // threads per voxel
   static constexpr int kVPB = kThreads / kTPV;   // voxels per block
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
                  TmaTiles tt, int tile_rows) {
   constexpr int QP = L::QP, RPT = L::RPT, VPB = L::kVPB, WPV = L::kWPV, TPV = L::kTPV;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int Q = a.q;
+  const int Q = L::QF > 0 ? L::QF : a.q;
   const int h = Q * (Q + 1) / 2;
   const int tile_elems = tile_rows * VPB;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw);  // [0..1] hi buffers, [2] lo
@@ -608,6 +609,8 @@ void power_iteration(sk_ctx* ctx, const PowerArgs& a) {
   static const int k4v = env_int("SKB_K4_VARIANT", 0);
   if (a.q <= 4)
     launch<Layout<4, 1, 256, 2>>(ctx, a);
+  else if (a.q == 8)
+    launch<Layout<8, 1, 256, 2, 0, 4, 8>>(ctx, a);
   else if (a.q <= 8)
     launch<Layout<8, 1, 256, 2>>(ctx, a);
   else if (a.q <= 16)
@@ -621,10 +624,16 @@ void power_iteration(sk_ctx* ctx, const PowerArgs& a) {
       case 5: launch<Layout<32, 1, 256, 1, 2, 4>>(ctx, a); break;
       case 6: launch<Layout<32, 2, 256, 1, 2, 4>>(ctx, a); break;
       case 7: launch<Layout<32, 1, 256, 1, 4, 6>>(ctx, a); break;
-      default: rpt32 == 1 ? launch<Layout<32, 1, 256, 2, 2, 4>>(ctx, a) : launch<Layout<32, 2, 128, 3>>(ctx, a);
+      default:
+        if (rpt32 != 1)
+          launch<Layout<32, 2, 128, 3>>(ctx, a);
+        else if (a.q == 32)
+          launch<Layout<32, 1, 256, 2, 2, 4, 32>>(ctx, a);
+        else
+          launch<Layout<32, 1, 256, 2, 2, 4>>(ctx, a);
     }
   else if (a.q <= 64)
-    launch<Layout<64, 1, 256, 1>>(ctx, a);
+    a.q == 64 ? launch<Layout<64, 1, 256, 1, 0, 4, 64>>(ctx, a) : launch<Layout<64, 1, 256, 1>>(ctx, a);
   else
     fail(9, "eig_power_field: more than 64 channels is outside the B200 path");
 }
