@@ -170,8 +170,12 @@ __device__ void tri_solve(const double* d, const double* e, int n, double s, dou
   }
 }
 
-__global__ void __launch_bounds__(kThreads) herm_eig_kernel(double2* __restrict__ H, int n, double* __restrict__ w,
+// NF > 0: the order is fixed at compile time (n == NF; loop bounds and
+// strides fold); 0: runtime n.
+template <int NF>
+__global__ void __launch_bounds__(kThreads) herm_eig_kernel(double2* __restrict__ H, int n_arg, double* __restrict__ w,
                                                              double floor_rel, int* __restrict__ info) {
+  const int n = NF > 0 ? NF : n_arg;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int ld = n + 1;  // padded row stride (double2) of the full Hermitian A (bank skew)
   const int xs = n + 1;  // padded row stride of X
@@ -570,8 +574,13 @@ size_t herm_eig_smem(int n) {
 bool herm_eig_small(sk_ctx* ctx, double2* H, int n, double* w, int* info, double floor_rel) {
   if (n < 1 || n > kMaxN) return false;
   const size_t smem = herm_eig_smem(n);
-  set_smem_limit(reinterpret_cast<const void*>(herm_eig_kernel), smem);
-  herm_eig_kernel<<<1, kThreads, smem, ctx->stream>>>(H, n, w, floor_rel, info);
+  if (n == 64) {
+    set_smem_limit(reinterpret_cast<const void*>(herm_eig_kernel<64>), smem);
+    herm_eig_kernel<64><<<1, kThreads, smem, ctx->stream>>>(H, n, w, floor_rel, info);
+  } else {
+    set_smem_limit(reinterpret_cast<const void*>(herm_eig_kernel<0>), smem);
+    herm_eig_kernel<0><<<1, kThreads, smem, ctx->stream>>>(H, n, w, floor_rel, info);
+  }
   ++ctx->launches;
   SKB_LAUNCH("herm_eig_kernel");
   if (std::getenv("SKB_PROFILE_NS")) {
