@@ -84,12 +84,16 @@ __global__ void __launch_bounds__(256) expand_row_kernel(const double2* __restri
   }
 }
 
-template <int H>
+// FULL: the whole (c, s) table (N x H) is staged once per CTA (dynamic shared
+// memory, no per-chunk barriers); otherwise kColRows rows at a time.
+template <int H, bool FULL>
 __global__ void __launch_bounds__(256) expand_col_kernel(const double2* __restrict__ in, i64 inner, int N,
                                                          const double2* __restrict__ cs, double2* out64, float2* hi,
                                                          float2* lo) {
   constexpr int L = 2 * H + 1;
-  __shared__ __align__(16) double2 tab[kColRows * (H > 0 ? H : 1)];
+  __shared__ __align__(16) double2 tab_chunk[FULL ? 1 : kColRows * (H > 0 ? H : 1)];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* tab = FULL ? reinterpret_cast<double2*>(smem_raw) : tab_chunk;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const i64 nchunk = (inner + 31) / 32;
   const i64 b = i64(blockIdx.x) / nchunk;
@@ -107,17 +111,23 @@ __global__ void __launch_bounds__(256) expand_col_kernel(const double2* __restri
     S[l] = make_double2(xp.x + xm.x, xp.y + xm.y);
     D[l] = make_double2(xp.x - xm.x, xp.y - xm.y);
   }
+  if constexpr (FULL) {
+    for (int e = ty * 32 + tx; e < N * H; e += 256) tab[e] = cs[e];
+    __syncthreads();
+  }
   for (int j_begin = 0; j_begin < N; j_begin += kColRows) {
     const int j_count = min(kColRows, N - j_begin);
-    __syncthreads();
-    for (int e = ty * 32 + tx; e < kColRows * H; e += 256) {
-      const int jj = e / H, l = e % H;
-      tab[e] = jj < j_count ? cs[i64(j_begin + jj) * H + l] : make_double2(0.0, 0.0);
+    if constexpr (!FULL) {
+      __syncthreads();
+      for (int e = ty * 32 + tx; e < kColRows * H; e += 256) {
+        const int jj = e / H, l = e % H;
+        tab[e] = jj < j_count ? cs[i64(j_begin + jj) * H + l] : make_double2(0.0, 0.0);
+      }
+      __syncthreads();
     }
-    __syncthreads();
     if (!live) continue;
     for (int jj = ty; jj < j_count; jj += 8) {
-      const double2* row = tab + jj * H;
+      const double2* row = tab + (FULL ? (j_begin + jj) : jj) * H;
       double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
 #pragma unroll
       for (int l = 0; l < H; l += 2) {
@@ -143,7 +153,15 @@ void launch_stage(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int N, c
   if (inner >= 32) {
     const i64 gx = (inner + 31) / 32 * batch;
     if (gx > 0x7fffffffLL) fail(SK_ERR_UNSUPPORTED, "expand: grid too large");
-    expand_col_kernel<H><<<dim3{unsigned(gx)}, dim3{32, 8}, 0, ctx->stream>>>(in, inner, N, cs, out64, hi, lo);
+    const size_t full_bytes = size_t(N) * (H > 0 ? H : 1) * sizeof(double2);
+    if (full_bytes <= 110 * 1024) {  // two CTAs per SM still fit
+      set_smem_limit(reinterpret_cast<const void*>(expand_col_kernel<H, true>), full_bytes);
+      expand_col_kernel<H, true><<<dim3{unsigned(gx)}, dim3{32, 8}, full_bytes, ctx->stream>>>(in, inner, N, cs, out64,
+                                                                                               hi, lo);
+    } else {
+      expand_col_kernel<H, false><<<dim3{unsigned(gx)}, dim3{32, 8}, 0, ctx->stream>>>(in, inner, N, cs, out64, hi,
+                                                                                        lo);
+    }
   } else {
     const i64 rows = batch * inner;
     const int threads = N >= 256 ? 256 : (N >= 128 ? 128 : 64);
