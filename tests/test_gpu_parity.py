@@ -203,6 +203,34 @@ def test_interpolation_parity(K, O):
         K.interpolate_maps(rnd((1, 8, 8), 64), (4, 8))
 
 
+@pytest.mark.parametrize("low,full", [((2, 64, 64), (128, 128)), ((2, 32, 64), (32, 256)), ((1, 128, 8), (256, 8)),
+                                      ((2, 16, 32, 8), (32, 64, 16))])
+def test_interpolation_fft_sizes(K, O, low, full):
+    """K5 FFT path at the compile-time specialised line lengths (64 -> 128/256,
+    128 -> 256) and the runtime path, every axis order, against the oracle."""
+    x = rnd(low, 66)
+    got = K.interpolate_maps(x, full)
+    ref = O.interpolate_maps(f32(x), full)
+    err = PM.rel_fro(got, ref)
+    report("interp_fft", low=list(low), full=list(full), rel_fro=err)
+    assert err < 1e-5
+    lr = np.random.default_rng(2).random(low[1:]).astype(np.float32)
+    assert PM.rel_fro(K.interpolate_real(lr, full), O.interpolate_real(lr.astype(np.float64), full)) < 1e-6
+
+
+def test_power_odd_voxel_count_fallback(K, O):
+    """K4 with an odd voxel count: the plane stride is not a multiple of 16
+    bytes, so tiles load through the cp.async fallback instead of TMA."""
+    n, q = 301, 32
+    m = rnd((n, q, q), 12, np.complex128)
+    herm = ((m + m.conj().transpose(0, 2, 1)) / 2 + 2.5 * q ** 0.5 * np.eye(q)).astype(np.complex64)
+    vg, valg = K.eig_power_field(herm, 30)
+    vo, valo = O.eig_power_field(f32(herm), 30)
+    ph = np.sum(vo.conj() * vg, 0)
+    ph = ph / np.abs(ph)
+    assert np.abs(vg - vo * ph[None]).max() < 1e-3 and PM.rel_fro(valg, valo) < 1e-5
+
+
 def test_normalize_parity(K, O):
     raw = rnd((4, 20, 18), 65)
     cal = rnd((4, 8, 8), 66)
