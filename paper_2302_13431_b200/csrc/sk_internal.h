@@ -116,8 +116,15 @@ struct sk_ctx {
   int64_t launches = 0;   // our kernels
   int64_t lib_calls = 0;  // cuSOLVER / cuBLAS calls
   cudaEvent_t ev[8] = {};
-  // subspace solver hints per Gram size: (signal count, orthogonalised iterations)
-  std::map<int64_t, std::pair<int64_t, int>> subspace_hint;
+  // subspace solver hints per Gram size: signal count, orthogonalised steps
+  // planned before the first Rayleigh-Ritz check, and the largest plan that
+  // once needed an extra round (never planned again)
+  struct SubspaceHint {
+    int64_t m = 0;
+    int plan = 3;
+    int failed_plan = 0;
+  };
+  std::map<int64_t, SubspaceHint> subspace_hint;
   syevjInfo_t syevj = nullptr;
   // concurrent lanes for multislice batches (sub-contexts on the same device)
   std::vector<sk_ctx*> lanes;

@@ -846,14 +846,16 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   int q_plan = 3;
   auto it_h = hint.find(n);
   if (it_h != hint.end()) {
-    const i64 k_prev = it_h->second.first;
+    const i64 k_prev = it_h->second.m;
     b = big ? std::max<i64>(128, ((k_prev + 48 + 31) / 32) * 32) : std::max<i64>(64, ((k_prev + 16 + 15) / 16) * 16);
-    q_plan = it_h->second.second;
+    q_plan = it_h->second.plan;
   }
+  const int first_plan = q_plan;
+  int rounds = 0;
   if (const char* v = std::getenv("SKB_BLOCK")) {  // experiment override
     const i64 fixed = std::atoll(v);
     if (fixed > 0) {
-      if (it_h == hint.end() || it_h->second.first + 8 > fixed) q_plan = 3;
+      if (it_h == hint.end() || it_h->second.m + 8 > fixed) q_plan = 3;
       b = fixed;
     }
   }
@@ -877,6 +879,7 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   const i64 guard = 8;
   std::vector<double> hw(static_cast<size_t>(bcap)), hres(static_cast<size_t>(bcap));
   bool converged = false;
+  double last_worst = 0.0, last_rate = 0.0;
   int iters = 0;
   i64 m = 0;
   double theta_max = 0.0, c = 0.0;
@@ -968,6 +971,7 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
                 RoundKey{n, b, q_plan, V, Y, T, H, w, res, d_info, A, gram, ratio}, V, Y, T, body);
     if (!body_ok) return false;
     iters += q_plan + 1;
+    ++rounds;
     int hinfo[3] = {0, 0, 0};
     SKB_CUDA(cudaMemcpyAsync(hw.data(), w, size_t(b) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     SKB_CUDA(cudaMemcpyAsync(hres.data(), res, size_t(b) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -987,6 +991,7 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
       b = nb;
       if (!orth(ctx, V, T, n, b, flag)) return false;
       q_plan = 3;
+      rounds = -1000;  // block grown: this call says nothing about the plan
       continue;
     }
     // Converged when every Ritz pair at or above cut^2/2 has a small residual and
@@ -1001,6 +1006,8 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
     }
     if (reaches && worst <= tol) {
       converged = true;
+      last_worst = worst;
+      last_rate = rate;
       break;
     }
     // Predict the remaining iterations from the observed Ritz-value ratios.
@@ -1056,7 +1063,21 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   e.margin = margin;
   e.iterations = iters;
   e.block = int(b);
-  hint[n] = {m, std::max(1, iters - 1)};
+  // Step plan for the next call of this size: the steps this call used, one
+  // fewer when the final residual shows that one step less would still have
+  // converged (residual one step earlier ~ worst / rate, 0.8x margin) and
+  // that plan never needed an extra round before.
+  auto& h = hint[n];
+  if (rounds > 1 && it_h != hint.end()) h.failed_plan = std::max(h.failed_plan, first_plan);
+  int plan = std::max(1, iters - 1);
+  if (last_rate > 0.0 && last_rate < 1.0 && last_worst <= 0.8 * tol * last_rate && plan > 3 &&
+      plan - 1 > h.failed_plan)
+    --plan;
+  if (std::getenv("SKB_PROFILE_NS"))
+    std::fprintf(stderr, "[ns] n=%lld iters=%d rounds=%d worst=%.3e rate=%.3e next_plan=%d failed=%d\n", (long long)n,
+                 iters, rounds, last_worst, last_rate, plan, h.failed_plan);
+  h.m = m;
+  h.plan = plan;
   return true;
 }
 
