@@ -187,6 +187,16 @@ int sk_renormalize_sos(sk_ctx* ctx, int64_t voxels, int64_t channels, sk_c64* ma
  * cuSOLVER Jacobi. */
 int sk_debug_small_eigh(sk_ctx* ctx, int64_t n, double* h, double* w);
 
+/* Test hooks for the K2 block kernels (the reference's dense path has no
+ * equivalent entry point; they expose the steps eigen_dense/orthonormalise
+ * stand-ins run between subspace products, maps.cpp:151-175).
+ * sk_debug_cholqr: x (n x b complex128, column-major) <- x R^{-1}, R the
+ *   Cholesky factor of x^H x, `passes` times (CholQR / CholQR2).
+ * sk_debug_cross_gram: out (b x b complex128, column-major) = x^H y
+ *   (y == NULL: x^H x). */
+int sk_debug_cholqr(sk_ctx* ctx, int64_t n, int64_t b, double* x, int passes);
+int sk_debug_cross_gram(sk_ctx* ctx, int64_t n, int64_t b, const double* x, const double* y, double* out);
+
 /* ----------------------------------------------------------- full pipeline */
 /* estimate_maps (maps.hpp:85-86, maps.cpp:265-330).  Outputs on full_dims:
  * maps Q x N_full, lambda_min_map N_full, support_mask N_full (each may be

@@ -171,6 +171,8 @@ _SIGS = {
     "sk_interpolate_real": ([_VP, _I32, _VP, _VP, _VP, _VP], _I32),
     "sk_support_mask": ([_VP, _I64, _VP, _D, _VP], _I32),
     "sk_debug_small_eigh": ([_VP, _I64, _VP, _VP], _I32),
+    "sk_debug_cholqr": ([_VP, _I64, _I64, _VP, _I32], _I32),
+    "sk_debug_cross_gram": ([_VP, _I64, _I64, _VP, _VP, _VP], _I32),
     "sk_estimate_raw_slab": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _I64, _I64, _VP, _VP, _VP], _I32),
     "sk_sos_accumulate": ([_VP, _I64, _I64, _VP, _VP], _I32),
     "sk_projection_residual": ([_VP, _I32, _VP, _I64, _VP, _VP, _VP], _I32),
@@ -401,6 +403,28 @@ def small_eigh(h: np.ndarray, ctx: Context | None = None) -> tuple[np.ndarray, n
     w = np.zeros(n, dtype=np.float64)
     _check(lib().sk_debug_small_eigh(_ctx(ctx), n, a.ctypes.data, w.ctypes.data))
     return w, a
+
+
+def cholqr(x: np.ndarray, passes: int = 1, ctx: Context | None = None) -> np.ndarray:
+    """Test hook: the K2 block orthonormalisation (CholQR, `passes` times) on a
+    complex128 n x b block; returns the orthonormal block with the same span."""
+    a = np.array(x, dtype=np.complex128, order="F", copy=True)
+    n, b = a.shape
+    _check(lib().sk_debug_cholqr(_ctx(ctx), n, b, a.ctypes.data, int(passes)))
+    return a
+
+
+def cross_gram(x: np.ndarray, y: np.ndarray | None = None, ctx: Context | None = None) -> np.ndarray:
+    """Test hook: X^H Y (X^H X when y is None) with the K2 block kernels."""
+    xa = np.asfortranarray(x, dtype=np.complex128)
+    n, b = xa.shape
+    ya = None if y is None else np.asfortranarray(y, dtype=np.complex128)
+    if ya is not None and ya.shape != xa.shape:
+        raise ValueError("cross_gram: x and y must have the same shape")
+    out = np.zeros((b, b), dtype=np.complex128, order="F")
+    _check(lib().sk_debug_cross_gram(_ctx(ctx), n, b, xa.ctypes.data, None if ya is None else ya.ctypes.data,
+                                     out.ctypes.data))
+    return out
 
 
 def support_mask(lam: np.ndarray, threshold: float, ctx: Context | None = None) -> np.ndarray:

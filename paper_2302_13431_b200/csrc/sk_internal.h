@@ -128,6 +128,8 @@ struct sk_ctx {
   syevjInfo_t syevj = nullptr;
   // concurrent lanes for multislice batches (sub-contexts on the same device)
   std::vector<sk_ctx*> lanes;
+  // arena slots zeroed once at allocation (kernel-maintained counters)
+  std::map<std::string, void*> arena_zeroed;
   // captured subspace rounds (CUDA graphs), see run_graphed
   std::map<skb::RoundKey, skb::RoundGraph> rounds;
 };
@@ -233,6 +235,11 @@ void ritz_residuals(sk_ctx* ctx, const double2* y, const double2* v, const doubl
                     double* res);
 void shift_negate(sk_ctx* ctx, const double2* a, double2* m, i64 n, double shift);
 void cross_gram(sk_ctx* ctx, const double2* x, const double2* y, i64 n, int b, double2* out);
+// b = 64 block kernels (sk_cholqr.cu): X^H Y (X^H X when y == x) into a
+// 64 x 64 column-major matrix, and `passes` CholQR passes X <- X L^{-H}
+// (one-CTA Cholesky; a non-positive pivot raises *flag).
+void gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, double2* out);
+void cholqr64(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag);
 void chol_inv(sk_ctx* ctx, const double2* s, int b, double2* minv, int* flag);
 void cholesky_small(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag);
 // One-CTA Hermitian eigensolver (sk_eig.cu) for b <= 64: eigenvalues ascending

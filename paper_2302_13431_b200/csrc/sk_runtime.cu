@@ -623,7 +623,8 @@ bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int 
   // default: cuSOLVER POTRF + cuBLAS TRSM (measured fastest at b = 64..96);
   // SKB_SMALL_CHOL=fast selects the own lazy Cholesky + row TRSM (b <= 112),
   // =custom the own blocked Cholesky + cuBLAS TRSM.
-  // Default: own cross_gram + cuSOLVER POTRF + cuBLAS TRSM.  SKB_SMALL_CHOL=pass64 selects the
+  // Default at b = 64: sk_cholqr.cu (three own kernels per pass).  Otherwise
+  // own cross_gram + cuSOLVER POTRF + cuBLAS TRSM.  SKB_SMALL_CHOL=pass64 selects the
   // library-free pass (one-CTA Cholesky + inverse; measured slower: the
   // 64-pivot chain on one SM is latency-bound).
   static const int chol_mode = [] {
@@ -632,8 +633,13 @@ bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int 
     if (v && std::string(v) == "custom") return 2;
     if (v && std::string(v) == "pass64") return 3;
     if (v && std::string(v) == "blocked") return 4;
-    return 1;
+    if (v && std::string(v) == "lib") return 1;
+    return 5;
   }();
+  if (chol_mode == 5 && b == 64 && n >= 1024) {  // own gram + one-CTA Cholesky + blocked row TRSM (fixed costs pay from n ~ 1k)
+    cholqr64(ctx, x, n, passes, flag);
+    return true;
+  }
   if (chol_mode == 3 && b <= 64) {
     double2* S = ctx->arena.get<double2>("ss:S", b * b);
     double2* Mi = ctx->arena.get<double2>("ss:Minv", b * b);
@@ -950,7 +956,10 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
       zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);
       laps.lap("gemm64");
       // Rayleigh-Ritz on span(V): H = V^H A V = S diag(w) S^H.
-      if (b <= 256) {
+      static const bool lib_gram = std::getenv("SKB_SMALL_CHOL") != nullptr;
+      if (b == 64 && n >= 1024 && !lib_gram) {
+        gram64(ctx, V, Y, n, H);
+      } else if (b <= 256) {
         cross_gram(ctx, V, Y, n, int(b), H);
       } else {
         zgemm(ctx, CUBLAS_OP_C, CUBLAS_OP_N, b, b, n, V, n, Y, n, H, b);
@@ -1680,6 +1689,46 @@ int sk_debug_small_eigh(sk_ctx* ctx, int64_t n, double* h, double* w) {
     SKB_CUDA(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     SKB_CUDA(cudaStreamSynchronize(ctx->stream));
     if (hinfo != 0) fail(SK_ERR_OTHER, "sk_debug_small_eigh: solver reported failure");
+  });
+}
+
+int sk_debug_cholqr(sk_ctx* ctx, int64_t n, int64_t b, double* x, int passes) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (n < 1 || b < 1 || b > n || b > 256 || passes < 1 || passes > 4 || x == nullptr)
+      fail(SK_ERR_DIM, "sk_debug_cholqr: bad arguments");
+    double2* dx = ctx->arena.get<double2>("dbg:x", n * b);
+    double2* dt = ctx->arena.get<double2>("dbg:t", n * b);
+    int* info = ctx->arena.get<int>("dbg:qinfo", 3);
+    SKB_CUDA(cudaMemsetAsync(info, 0, 3 * sizeof(int), ctx->stream));
+    SKB_CUDA(cudaMemcpyAsync(dx, x, size_t(n * b) * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    double2* px = dx;
+    double2* pt = dt;
+    if (!orth(ctx, px, pt, n, b, info + 1, passes)) fail(SK_ERR_OTHER, "sk_debug_cholqr: orthonormalisation failed");
+    int hinfo[3] = {0, 0, 0};
+    SKB_CUDA(cudaMemcpyAsync(x, px, size_t(n * b) * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    SKB_CUDA(cudaMemcpyAsync(hinfo, info, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hinfo[1] != 0 || hinfo[2] != 0) fail(SK_ERR_OTHER, "sk_debug_cholqr: non-positive pivot");
+  });
+}
+
+int sk_debug_cross_gram(sk_ctx* ctx, int64_t n, int64_t b, const double* x, const double* y, double* out) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (n < 1 || b < 1 || b > 256 || x == nullptr || out == nullptr)
+      fail(SK_ERR_DIM, "sk_debug_cross_gram: bad arguments");
+    double2* dx = ctx->arena.get<double2>("dbg:x", n * b);
+    double2* dy = y ? ctx->arena.get<double2>("dbg:y", n * b) : dx;
+    double2* dh = ctx->arena.get<double2>("dbg:h", b * b);
+    SKB_CUDA(cudaMemcpyAsync(dx, x, size_t(n * b) * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    if (y) SKB_CUDA(cudaMemcpyAsync(dy, y, size_t(n * b) * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    if (b == 64)
+      gram64(ctx, dx, dy, n, dh);
+    else
+      cross_gram(ctx, dx, dy, n, int(b), dh);
+    SKB_CUDA(cudaMemcpyAsync(out, dh, size_t(b * b) * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
 

@@ -86,6 +86,70 @@ def _hermitian_with_spectrum(n, lam, seed):
     return 0.5 * (h + h.conj().T)
 
 
+def _block_with_condition(n, b, kappa, seed):
+    r = np.random.default_rng(seed)
+    q, _ = np.linalg.qr(r.standard_normal((n, b)) + 1j * r.standard_normal((n, b)))
+    w, _ = np.linalg.qr(r.standard_normal((b, b)) + 1j * r.standard_normal((b, b)))
+    sv = np.geomspace(1.0, 1.0 / kappa, b) * 3.1
+    return (q * sv) @ w.conj().T
+
+
+@pytest.mark.parametrize("n", [1, 5, 64, 232, 1568, 2592, 3936, 9001])
+@pytest.mark.parametrize("herm", [True, False])
+def test_block_cross_gram(K, n, herm):
+    """K2 block Gram X^H X / X^H Y (b = 64: cluster-reduced gram64 kernel)
+    against numpy; bitwise repeatable (fixed reduction order)."""
+    b = 64
+    x = rnd((n, b), 500 + n, np.complex128)
+    y = None if herm else rnd((n, b), 600 + n, np.complex128)
+    g = K.api.cross_gram(x, y)
+    ref = x.conj().T @ (x if herm else y)
+    err = np.abs(g - ref).max() / np.abs(ref).max()
+    report("block_cross_gram", n=n, herm=herm, rel_err=float(err))
+    assert err < 1e-13
+    if herm:
+        assert np.array_equal(g, g.conj().T)
+    assert np.array_equal(g, K.api.cross_gram(x, y))
+
+
+@pytest.mark.parametrize("n,b,kappa,passes", [
+    (64, 64, 10.0, 1), (232, 64, 1e3, 2), (2592, 64, 10.0, 1), (2592, 64, 1e6, 2), (3936, 64, 1e4, 2),
+    (9001, 64, 1e2, 1), (2592, 48, 1e3, 2), (2592, 96, 1e3, 2),
+])
+def test_block_cholqr(K, n, b, kappa, passes):
+    """K2 block orthonormalisation (b = 64: gram64 + one-CTA Cholesky + blocked
+    row TRSM; other b: library path): orthonormal, same span, R = Q^H X upper
+    triangular with a positive diagonal, and equal to X chol(X^H X)^{-H}."""
+    x = _block_with_condition(n, b, kappa, 700 + n + b)
+    q = K.api.cholqr(x, passes)
+    orth = np.abs(q.conj().T @ q - np.eye(b)).max()
+    r = q.conj().T @ x
+    lower = np.abs(np.tril(r, -1)).max() / np.abs(r).max()
+    recon = np.abs(q @ r - x).max() / np.abs(x).max()
+    rn = np.linalg.cholesky(x.conj().T @ x).conj().T
+    qn = np.linalg.solve(rn.T, x.T).T  # x rn^{-1}
+    qerr = np.abs(q - qn).max()
+    report("block_cholqr", n=n, b=b, kappa=kappa, passes=passes, orth=float(orth), lower=float(lower),
+           recon=float(recon), vs_numpy=float(qerr))
+    bound = 1e-13 if passes == 2 else max(1e-13, 50 * kappa ** 2 * 2.2e-16)
+    assert orth < bound
+    assert recon < 1e-12
+    assert lower < 1e-10 * kappa
+    assert np.all(np.diag(r).real > 0)
+    if passes == 1:
+        assert qerr < 1e-12 * kappa ** 2
+    assert np.array_equal(q, K.api.cholqr(x, passes))
+
+
+def test_block_cholqr_rank_deficient_raises(K):
+    """A rank-deficient block makes the Cholesky pivot non-positive: the hook
+    reports the failure (the solver falls back on it) instead of returning NaNs."""
+    x = rnd((500, 64), 901, np.complex128)
+    x[:, 17] = 0.0
+    with pytest.raises(Exception):
+        K.api.cholqr(x, 1)
+
+
 @pytest.mark.parametrize("n,kind", [
     (1, "random"), (2, "random"), (7, "random"), (33, "ritz"), (48, "degenerate"), (64, "ritz"), (64, "degenerate"),
     (64, "close"), (64, "random"), (96, "ritz"),
