@@ -105,8 +105,11 @@ class ClockSampler:
 
     def start(self):
         try:
+            if os.environ.get("SKB_BENCH_CLOCK_MS") == "0":  # experiment: no sampling
+                raise RuntimeError("clock sampling disabled")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms",
+                                          os.environ.get("SKB_BENCH_CLOCK_MS", "100")],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()

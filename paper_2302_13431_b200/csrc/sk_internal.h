@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -130,6 +131,9 @@ struct sk_ctx {
   std::vector<sk_ctx*> lanes;
   // arena slots zeroed once at allocation (kernel-maintained counters)
   std::map<std::string, void*> arena_zeroed;
+  // (n, b) sizes whose round already ran eagerly (buffers allocated): a new
+  // step plan for such a size is captured on first sight
+  std::set<std::pair<int64_t, int64_t>> warm_rounds;
   // captured subspace rounds (CUDA graphs), see run_graphed
   std::map<skb::RoundKey, skb::RoundGraph> rounds;
 };

@@ -20,10 +20,12 @@ KEYS = {
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "msecond": 1, "usecond": 1e-3, "nsecond": 1e-6, "ms": 1, "us": 1e-3, "ns": 1e-6}
 
 
-def read(rep):
+def read(rep, name=None):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units = rows[0], rows[1]
+    k = hdr.index("Kernel Name")
+    vals = next(r for r in rows[2:] if name is None or name in r[k])
     d = {"kernel": vals[hdr.index("Kernel Name")][:120]}
     for i, n in enumerate(hdr):
         if n in KEYS:
@@ -41,8 +43,9 @@ def read(rep):
 
 out = json.load(open(sys.argv[1])) if len(sys.argv) > 1 and sys.argv[1].endswith(".json") else {}
 args = sys.argv[2:] if len(sys.argv) > 1 and sys.argv[1].endswith(".json") else sys.argv[1:]
-for spec in args:  # group:config=report
+for spec in args:  # group:config=report[@kernel-name-substring]
     key, rep = spec.split("=")
+    rep, _, name = rep.partition("@")
     group, cfg = key.split(":")
-    out.setdefault(group, {})[cfg] = read(rep)
+    out.setdefault(group, {})[cfg] = read(rep, name or None)
 print(json.dumps(out, indent=1))
