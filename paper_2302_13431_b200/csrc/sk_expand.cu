@@ -19,6 +19,9 @@
 //    with the (c, s) table broadcast from shared memory (256-byte stores).
 #include "sk_internal.h"
 
+#include <cstdlib>
+#include <string>
+
 namespace skb {
 
 namespace {
@@ -87,7 +90,7 @@ __global__ void __launch_bounds__(256) expand_row_kernel(const double2* __restri
 // FULL: the whole (c, s) table (N x H) is staged once per CTA (dynamic shared
 // memory, no per-chunk barriers); otherwise kColRows rows at a time.
 template <int H, bool FULL>
-__global__ void __launch_bounds__(256) expand_col_kernel(const double2* __restrict__ in, i64 inner, int N,
+__global__ void __launch_bounds__(256) expand_col_kernel(const double2* __restrict__ in, i64 inner, int N, int jc,
                                                          const double2* __restrict__ cs, double2* out64, float2* hi,
                                                          float2* lo) {
   constexpr int L = 2 * H + 1;
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(256) expand_col_kernel(const double2* __restri
     for (int e = ty * 32 + tx; e < N * H; e += 256) tab[e] = cs[e];
     __syncthreads();
   }
-  for (int j_begin = 0; j_begin < N; j_begin += kColRows) {
+  for (int j_begin = 0; j_begin < (FULL ? 1 : N); j_begin += kColRows) {
     const int j_count = min(kColRows, N - j_begin);
     if constexpr (!FULL) {
       __syncthreads();
@@ -126,41 +129,166 @@ __global__ void __launch_bounds__(256) expand_col_kernel(const double2* __restri
       __syncthreads();
     }
     if (!live) continue;
-    for (int jj = ty; jj < j_count; jj += 8) {
-      const double2* row = tab + (FULL ? (j_begin + jj) : jj) * H;
+    if constexpr (FULL) {
+      // Mirrored pairs: rows jc + k and jc - k share c_l and negate s_l, so
+      // A = sum c_l S_l and B = i sum s_l D_l give both outputs (A + B, A - B)
+      // for half the FP64 MACs.
+      // jc: the grid centre relative to the first output row (a z-slab may
+      // start above or end below it).  Items: rows jp >= jc (mirror 2 jc - jp
+      // when it is another output row), then the rows below jc whose mirror
+      // lies past the last output row, alone.
+      const int p0 = max(jc, 0), P = max(0, N - p0);
+      const int S1 = jc > 0 ? max(0, min(min(jc, N), 2 * jc - N + 1)) : 0;
+      for (int t = ty; t < P + S1; t += 8) {
+        const bool single = t >= P;
+        const int jp = single ? t - P : p0 + t;
+        const int jm = single ? -1 : 2 * jc - jp;
+        const double2* row = tab + jp * H;
+        double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
+#pragma unroll
+        for (int l = 0; l < H; ++l) {
+          const double2 tcs = row[l];
+          ax = fma(tcs.x, S[l].x, ax);
+          ay = fma(tcs.x, S[l].y, ay);
+          bx = fma(-tcs.y, D[l].y, bx);
+          by = fma(tcs.y, D[l].x, by);
+        }
+        store_out(make_double2(x0.x + (ax + bx), x0.y + (ay + by)), out64, hi, lo, (b * N + jp) * inner + i);
+        if (jm >= 0 && jm < N && jm != jp)
+          store_out(make_double2(x0.x + (ax - bx), x0.y + (ay - by)), out64, hi, lo, (b * N + jm) * inner + i);
+      }
+    } else {
+      for (int jj = ty; jj < j_count; jj += 8) {
+        const double2* row = tab + jj * H;
+        double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
+#pragma unroll
+        for (int l = 0; l < H; l += 2) {
+          const double2 t0 = row[l], t1 = row[l + 1];
+          ax = fma(t0.x, S[l].x, ax);
+          ax = fma(-t0.y, D[l].y, ax);
+          ay = fma(t0.x, S[l].y, ay);
+          ay = fma(t0.y, D[l].x, ay);
+          bx = fma(t1.x, S[l + 1].x, bx);
+          bx = fma(-t1.y, D[l + 1].y, bx);
+          by = fma(t1.x, S[l + 1].y, by);
+          by = fma(t1.y, D[l + 1].x, by);
+        }
+        store_out(make_double2(x0.x + (ax + bx), x0.y + (ay + by)), out64, hi, lo,
+                  (b * N + j_begin + jj) * inner + i);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+  const unsigned d = unsigned(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gmem), "r"(bytes) : "memory");
+}
+
+// Persistent form of the FULL expand_col: the (c, s) table is staged once per
+// CTA, and the next column block's 2H+1 input rows (32 columns each) are
+// prefetched into shared memory with cp.async while the current block is
+// expanded (no per-CTA load bubble, no table reloads).
+template <int H>
+__global__ void __launch_bounds__(256) expand_col_persist_kernel(const double2* __restrict__ in, i64 inner, int N,
+                                                                 int jc, int items, i64 nblocks,
+                                                                 const double2* __restrict__ cs, double2* out64,
+                                                                 float2* hi, float2* lo) {
+  constexpr int L = 2 * H + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* tab = reinterpret_cast<double2*>(smem_raw);  // [items][H] (items = P + S1, computed by the host)
+  double2* xin = tab + items * H;                       // [2][L][32]
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const i64 nchunk = (inner + 31) / 32;
+  auto issue = [&](i64 cb, int buf) {
+    const i64 b = cb / nchunk, ib = (cb % nchunk) * 32;
+    for (int e = tid; e < L * 32; e += 256) {
+      const int l = e >> 5, c = e & 31;
+      const bool ok = ib + c < inner;
+      cp_async16(xin + (buf * L + l) * 32 + c, in + (b * L + l) * inner + (ok ? ib + c : 0), ok ? 16 : 0);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  i64 cb = blockIdx.x;
+  if (cb < nblocks) issue(cb, 0);
+  const int p0 = max(jc, 0), P = max(0, N - p0);
+  const int S1 = jc > 0 ? max(0, min(min(jc, N), 2 * jc - N + 1)) : 0;
+  // table rows in item order: item t < P is row p0 + t, item P + s is row s
+  for (int e = tid; e < (P + S1) * H; e += 256) {
+    const int t = e / H, l = e % H;
+    tab[e] = cs[(t < P ? p0 + t : t - P) * H + l];
+  }
+  for (int buf = 0; cb < nblocks; cb += gridDim.x, buf ^= 1) {
+    const i64 next = cb + gridDim.x;
+    if (next < nblocks) {
+      issue(next, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();  // xin[buf] (and, on the first pass, the table) visible to all
+    const i64 b = cb / nchunk, i = (cb % nchunk) * 32 + tx;
+    const double2* xb = xin + buf * L * 32 + tx;
+    const double2 x0 = xb[H * 32];
+    double2 S[H > 0 ? H : 1], D[H > 0 ? H : 1];
+#pragma unroll
+    for (int l = 0; l < H; ++l) {
+      const double2 xp = xb[(H + 1 + l) * 32], xm = xb[(H - 1 - l) * 32];
+      S[l] = make_double2(xp.x + xm.x, xp.y + xm.y);
+      D[l] = make_double2(xp.x - xm.x, xp.y - xm.y);
+    }
+    __syncthreads();  // every thread has its column: xin[buf] may be refilled (issued next iteration)
+    if (i >= inner) continue;
+    for (int t = ty; t < P + S1; t += 8) {
+      const bool single = t >= P;
+      const int jp = single ? t - P : p0 + t;
+      const int jm = single ? -1 : 2 * jc - jp;
+      const double2* row = tab + t * H;
       double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
 #pragma unroll
-      for (int l = 0; l < H; l += 2) {
-        const double2 t0 = row[l], t1 = row[l + 1];
-        ax = fma(t0.x, S[l].x, ax);
-        ax = fma(-t0.y, D[l].y, ax);
-        ay = fma(t0.x, S[l].y, ay);
-        ay = fma(t0.y, D[l].x, ay);
-        bx = fma(t1.x, S[l + 1].x, bx);
-        bx = fma(-t1.y, D[l + 1].y, bx);
-        by = fma(t1.x, S[l + 1].y, by);
-        by = fma(t1.y, D[l + 1].x, by);
+      for (int l = 0; l < H; ++l) {
+        const double2 tcs = row[l];
+        ax = fma(tcs.x, S[l].x, ax);
+        ay = fma(tcs.x, S[l].y, ay);
+        bx = fma(-tcs.y, D[l].y, bx);
+        by = fma(tcs.y, D[l].x, by);
       }
-      store_out(make_double2(x0.x + (ax + bx), x0.y + (ay + by)), out64, hi, lo,
-                (b * N + j_begin + jj) * inner + i);
+      store_out(make_double2(x0.x + (ax + bx), x0.y + (ay + by)), out64, hi, lo, (b * N + jp) * inner + i);
+      if (jm >= 0 && jm < N && jm != jp)
+        store_out(make_double2(x0.x + (ax - bx), x0.y + (ay - by)), out64, hi, lo, (b * N + jm) * inner + i);
     }
   }
 }
 
 template <int H>
-void launch_stage(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int N, const double2* cs, double2* out64,
-                  float2* hi, float2* lo) {
+void launch_stage(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int N, int jc, const double2* cs,
+                  double2* out64, float2* hi, float2* lo) {
   if (inner >= 32) {
     const i64 gx = (inner + 31) / 32 * batch;
     if (gx > 0x7fffffffLL) fail(SK_ERR_UNSUPPORTED, "expand: grid too large");
     const size_t full_bytes = size_t(N) * (H > 0 ? H : 1) * sizeof(double2);
-    if (full_bytes <= 110 * 1024) {  // two CTAs per SM still fit
+    static const bool persist = std::getenv("SKB_EXPAND_PERSIST") == nullptr ||
+                                std::string(std::getenv("SKB_EXPAND_PERSIST")) != "0";
+    // items: output rows at or past the centre (with their mirrors) plus the
+    // rows below it whose mirror lies past the last output row (kernel rules)
+    const int p0 = std::max(jc, 0), P = std::max(0, N - p0);
+    const int S1 = jc > 0 ? std::max(0, std::min(std::min(jc, N), 2 * jc - N + 1)) : 0;
+    const int items = P + S1;
+    const size_t pbytes = size_t(items) * (H > 0 ? H : 1) * sizeof(double2) +
+                          size_t(2 * (2 * H + 1) * 32) * sizeof(double2);
+    if (persist && H > 0 && pbytes <= 110 * 1024) {  // two CTAs per SM
+      set_smem_limit(reinterpret_cast<const void*>(expand_col_persist_kernel<H>), pbytes);
+      const i64 nblocks = gx;
+      const unsigned grid = unsigned(std::min<i64>(nblocks, 2 * ctx->sm_count));
+      expand_col_persist_kernel<H><<<grid, dim3{32, 8}, pbytes, ctx->stream>>>(in, inner, N, jc, items, nblocks, cs,
+                                                                              out64, hi, lo);
+    } else if (full_bytes <= 110 * 1024) {  // two CTAs per SM still fit
       set_smem_limit(reinterpret_cast<const void*>(expand_col_kernel<H, true>), full_bytes);
-      expand_col_kernel<H, true><<<dim3{unsigned(gx)}, dim3{32, 8}, full_bytes, ctx->stream>>>(in, inner, N, cs, out64,
-                                                                                               hi, lo);
+      expand_col_kernel<H, true><<<dim3{unsigned(gx)}, dim3{32, 8}, full_bytes, ctx->stream>>>(in, inner, N, jc, cs,
+                                                                                               out64, hi, lo);
     } else {
-      expand_col_kernel<H, false><<<dim3{unsigned(gx)}, dim3{32, 8}, 0, ctx->stream>>>(in, inner, N, cs, out64, hi,
-                                                                                        lo);
+      expand_col_kernel<H, false><<<dim3{unsigned(gx)}, dim3{32, 8}, 0, ctx->stream>>>(in, inner, N, jc, cs, out64,
+                                                                                        hi, lo);
     }
   } else {
     const i64 rows = batch * inner;
@@ -174,18 +302,18 @@ void launch_stage(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int N, c
 
 }  // namespace
 
-void expand_stage_f64(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int H, int N, const double2* cs,
+void expand_stage_f64(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int H, int N, int jc, const double2* cs,
                       double2* out64, float2* hi, float2* lo) {
   if (batch <= 0 || N <= 0 || inner <= 0) return;
   switch (H) {
-    case 0: launch_stage<0>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
-    case 2: launch_stage<2>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
-    case 4: launch_stage<4>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
-    case 6: launch_stage<6>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
-    case 8: launch_stage<8>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
-    case 10: launch_stage<10>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
-    case 12: launch_stage<12>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
-    case 14: launch_stage<14>(ctx, in, batch, inner, N, cs, out64, hi, lo); break;
+    case 0: launch_stage<0>(ctx, in, batch, inner, N, jc, cs, out64, hi, lo); break;
+    case 2: launch_stage<2>(ctx, in, batch, inner, N, jc, cs, out64, hi, lo); break;
+    case 4: launch_stage<4>(ctx, in, batch, inner, N, jc, cs, out64, hi, lo); break;
+    case 6: launch_stage<6>(ctx, in, batch, inner, N, jc, cs, out64, hi, lo); break;
+    case 8: launch_stage<8>(ctx, in, batch, inner, N, jc, cs, out64, hi, lo); break;
+    case 10: launch_stage<10>(ctx, in, batch, inner, N, jc, cs, out64, hi, lo); break;
+    case 12: launch_stage<12>(ctx, in, batch, inner, N, jc, cs, out64, hi, lo); break;
+    case 14: launch_stage<14>(ctx, in, batch, inner, N, jc, cs, out64, hi, lo); break;
     default: fail(SK_ERR_UNSUPPORTED, "G(x) expansion: kernel radius > 7 is outside the B200 path");
   }
 }

@@ -171,7 +171,9 @@ void fold_lags_f32(sk_ctx* ctx, const float2* w, i64 n, int npairs, int lam, int
                    const int* d_lag_ptr, const int* d_lag_st, double2* lags);
 // One FP64 stage of the G(x) lag expansion (sk_expand.cu): in [batch][2H+1][inner]
 // -> out [batch][N][inner]; final stage writes the fp32 hi/lo pair (out64 == nullptr).
-void expand_stage_f64(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int H, int N, const double2* cs,
+// jc: row of the grid centre relative to the first output row (the table
+// cs starts at that row; used to pair mirrored rows).
+void expand_stage_f64(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int H, int N, int jc, const double2* cs,
                       double2* out64, float2* hi, float2* lo);
 
 // K4: batched per-voxel power iteration over packed Hermitian planes

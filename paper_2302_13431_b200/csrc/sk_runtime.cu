@@ -311,11 +311,13 @@ void expand_lags(sk_ctx* ctx, const double2* lags, float2* hi, float2* lo, i64 h
     const int N = int(grid[size_t(a)]);
     const double2* cs = symdft_table64(ctx, N, H, center_index(N), -1);
     int Nout = N;
+    int jc = int(center_index(N));  // centre row relative to the first output row
     if (a == 0 && slab1 >= 0) {  // rows [slab0, slab1) of the last (axis-0) stage only
       cs += slab0 * std::max(H, 1);
       Nout = int(slab1 - slab0);
+      jc -= int(slab0);
     }
-    expand_stage_f64(ctx, src, b, inner, H, Nout, cs, dst, a == 0 ? hi : nullptr, a == 0 ? lo : nullptr);
+    expand_stage_f64(ctx, src, b, inner, H, Nout, jc, cs, dst, a == 0 ? hi : nullptr, a == 0 ? lo : nullptr);
     cur[size_t(a)] = grid[size_t(a)];
     src = dst;
   }
