@@ -100,10 +100,22 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 }
 
 // Tile geometry of the TMA path: nb boxes of hb plane rows x VPB voxels.
+// With a tile row of 32/64/128 B the boxes land swizzled (TMA SWIZZLE_32B/
+// 64B/128B: the 16-B chunk index within each row is XORed with address bits
+// 7..): the unpack and the epilogue read a warp's 32 matrix rows from as
+// many different plane rows, which a dense [pair][VPB] tile maps onto 2-4
+// banks (16-way conflicts for Q = 32); swizzled they spread over 8 chunks.
 struct TmaTiles {
   int use = 0;  // 0: cp.async fallback (plane stride not a multiple of 16 B)
   int hb = 0, nb = 0;
+  int swz = 0;  // swizzle mask applied by the readers (0: dense tile)
 };
+
+// float2 index of tile element idx under the TMA swizzle (buffer 1 KB aligned).
+__device__ __forceinline__ int swz_at(int idx, int mask) {
+  const int b = idx << 3;
+  return (b ^ (((b >> 7) & mask) << 4)) >> 3;
+}
 
 template <int QP_, int RPT_, int THREADS_, int MINB_, int ACC_ = 0, int PF_ = 4, int QF_ = 0>
 struct Layout {
@@ -161,13 +173,13 @@ __device__ __forceinline__ void voxel_bar(int vox) {
 __device__ __forceinline__ int pair_index(int p, int c, int Q) { return p * Q - p * (p - 1) / 2 + (c - p); }
 
 // Element (p, c) of the Hermitian matrix from the packed tile (zero outside Q).
-__device__ __forceinline__ float2 herm_at(const float2* gs, int p, int c, int Q, int VPB, int vox) {
+__device__ __forceinline__ float2 herm_at(const float2* gs, int p, int c, int Q, int VPB, int vox, int swz) {
   float2 val = make_float2(0.f, 0.f);
   if (p < Q && c < Q) {
     if (p <= c) {
-      val = gs[pair_index(p, c, Q) * VPB + vox];
+      val = gs[swz_at(pair_index(p, c, Q) * VPB + vox, swz)];
     } else {
-      const float2 t = gs[pair_index(c, p, Q) * VPB + vox];
+      const float2 t = gs[swz_at(pair_index(c, p, Q) * VPB + vox, swz)];
       val = make_float2(t.x, -t.y);
     }
     if (p == c) val.y = 0.f;  // spatial_gram.cpp:140-146
@@ -183,9 +195,11 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int Q = L::QF > 0 ? L::QF : a.q;
   const int h = Q * (Q + 1) / 2;
-  const int tile_elems = tile_rows * VPB;
+  const int tile_elems = tile_rows * VPB;  // tile bytes: a multiple of 1 KB
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw);  // [0..1] hi buffers, [2] lo
-  float2* gbuf = reinterpret_cast<float2*>(smem_raw + 128);              // [2][tile_elems] hi planes
+  // tile buffers start on a 1 KB boundary (the swizzle pattern follows address bits 4..9)
+  float2* gbuf = reinterpret_cast<float2*>(smem_raw + ((smem_u32(smem_raw) + 128 + 1023) & ~1023u) -
+                                           smem_u32(smem_raw));  // [2][tile_elems] hi planes
   float2* lbuf = gbuf + 2 * tile_elems;                                  // [tile_elems] lo planes
   float2* vs = lbuf + tile_elems;                                        // [2][VPB][kStride]
   double2* vds = reinterpret_cast<double2*>(vs + 2 * VPB * L::kStride);  // [VPB][QP] final v in FP64
@@ -259,7 +273,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
 #pragma unroll
     for (int r = 0; r < RPT; ++r)
 #pragma unroll
-      for (int c = 0; c < QP; ++c) m[r][c] = herm_at(gs, local + r * TPV, c, Q, VPB, vox);
+      for (int c = 0; c < QP; ++c) m[r][c] = herm_at(gs, local + r * TPV, c, Q, VPB, vox, tt.swz);
     // Stream the lo residual planes of this tile while the iterations run
     // (its own buffer: the final Rayleigh quotient reads hi and lo packed).
     if (a.planes_lo != nullptr) load_tile(tile, lbuf, a.planes_lo, &tm_lo, 2);
@@ -463,10 +477,10 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       const double2* vd = vds + vox * QP;
       for (int e = local; e < h; e += TPV) {
         const int pc = pct[e], pp = pc >> 8, cc = pc & 0xff;
-        const float2 hv = gs[e * VPB + vox];
+        const float2 hv = gs[swz_at(e * VPB + vox, tt.swz)];
         double mx = double(hv.x), my = double(hv.y);
         if (a.planes_lo != nullptr) {
-          const float2 lv = lbuf[e * VPB + vox];
+          const float2 lv = lbuf[swz_at(e * VPB + vox, tt.swz)];
           mx += double(lv.x);
           my += double(lv.y);
         }
@@ -536,7 +550,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
 
 // 2-D tensor map over packed planes [h][n] (float2 as one 8-byte element):
 // box {VPB voxels, hb plane rows}.  Returns false when TMA cannot address it.
-bool encode_planes(CUtensorMap* m, const float2* base, i64 n, int h, int vpb, int hb) {
+bool encode_planes(CUtensorMap* m, const float2* base, i64 n, int h, int vpb, int hb, CUtensorMapSwizzle swz) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -559,7 +573,7 @@ bool encode_planes(CUtensorMap* m, const float2* base, i64 n, int h, int vpb, in
                             : p == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   }();
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<float2*>(base), dims, strides, box, estr,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
 
@@ -567,21 +581,33 @@ template <class L>
 void launch(sk_ctx* ctx, const PowerArgs& a) {
   const int h = a.q * (a.q + 1) / 2;
   static const bool no_tma = std::getenv("SKB_NO_TMA") != nullptr;
+  static const bool no_swz = std::getenv("SKB_K4_NO_SWIZZLE") != nullptr;
   TmaTiles tt;
   CUtensorMap tm_hi{}, tm_lo{};
-  // box rows: <= 256, and every box / tile a multiple of 128 bytes (TMA smem alignment)
-  const int al = std::max(1, 16 / L::kVPB);
+  // box rows: <= 256; every box a multiple of 128 B (TMA smem alignment) and of 8 rows when
+  // swizzled (the pattern's period); a swizzled tile a multiple of 1 KB (buffers stay 1 KB aligned)
+  const int row_bytes = L::kVPB * int(sizeof(float2));
+  const CUtensorMapSwizzle swz = no_swz ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                 : row_bytes == 32  ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : row_bytes == 64  ? CU_TENSOR_MAP_SWIZZLE_64B
+                                 : row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                                    : CU_TENSOR_MAP_SWIZZLE_NONE;
+  const bool swizzled = swz != CU_TENSOR_MAP_SWIZZLE_NONE;
+  const int al = std::max(std::max(1, 128 / row_bytes), swizzled ? 8 : 1);
   tt.nb = (h + 255) / 256;
   for (;; ++tt.nb) {
     tt.hb = ((h + tt.nb - 1) / tt.nb + al - 1) / al * al;
     if (tt.hb <= 256) break;
   }
-  tt.use = !no_tma && encode_planes(&tm_hi, a.planes, a.n, h, L::kVPB, tt.hb) &&
-           (a.planes_lo == nullptr || encode_planes(&tm_lo, a.planes_lo, a.n, h, L::kVPB, tt.hb));
+  tt.use = !no_tma && encode_planes(&tm_hi, a.planes, a.n, h, L::kVPB, tt.hb, swz) &&
+           (a.planes_lo == nullptr || encode_planes(&tm_lo, a.planes_lo, a.n, h, L::kVPB, tt.hb, swz));
   if (a.planes_lo == nullptr) tm_lo = tm_hi;
-  const int tile_rows = (std::max(std::max(h, L::QP), tt.use ? tt.nb * tt.hb : 0) + al - 1) / al * al;
+  tt.swz = !tt.use ? 0 : swz == CU_TENSOR_MAP_SWIZZLE_32B ? 1 : swz == CU_TENSOR_MAP_SWIZZLE_64B ? 3
+                                                          : swz == CU_TENSOR_MAP_SWIZZLE_128B ? 7 : 0;
+  const int alt = tt.swz ? std::max(al, 1024 / row_bytes) : al;
+  const int tile_rows = (std::max(std::max(h, L::QP), tt.use ? tt.nb * tt.hb : 0) + alt - 1) / alt * alt;
   const size_t tile = size_t(tile_rows) * L::kVPB * sizeof(float2);
-  const size_t smem = 128 + 3 * tile + 2 * size_t(L::kVPB) * L::kStride * sizeof(float2) +
+  const size_t smem = 1024 + 128 + 3 * tile + 2 * size_t(L::kVPB) * L::kStride * sizeof(float2) +
                       size_t(L::kVPB) * L::QP * sizeof(double2) +
                       size_t(L::kVPB) * L::kWPV * (sizeof(double) + 3 * sizeof(float)) + size_t(h) * sizeof(int);
   set_smem_limit(reinterpret_cast<const void*>(power_kernel<L>), smem);
@@ -624,6 +650,9 @@ void power_iteration(sk_ctx* ctx, const PowerArgs& a) {
       case 5: launch<Layout<32, 1, 256, 1, 2, 4>>(ctx, a); break;
       case 6: launch<Layout<32, 2, 256, 1, 2, 4>>(ctx, a); break;
       case 7: launch<Layout<32, 1, 256, 1, 4, 6>>(ctx, a); break;
+      case 8: launch<Layout<32, 2, 128, 3, 0, 4, 32>>(ctx, a); break;
+      case 9: launch<Layout<32, 2, 128, 3, 2, 2, 32>>(ctx, a); break;
+      case 10: launch<Layout<32, 2, 192, 2, 0, 4, 32>>(ctx, a); break;
       default:
         if (rpt32 != 1)
           launch<Layout<32, 2, 128, 3>>(ctx, a);
