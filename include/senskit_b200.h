@@ -43,8 +43,10 @@ enum {
 typedef struct { float re, im; } sk_c64;
 typedef struct sk_ctx sk_ctx;
 
-/* PipelineConfig (maps.hpp:23-45).  Only the `pisco` arm is implemented on
- * the GPU: gram = fft, eig = power, field = fast (others -> SK_ERR_UNSUPPORTED).
+/* PipelineConfig (maps.hpp:23-45).  Both presets run on the GPU: `pisco`
+ * (gram = fft, eig = power) and `baseline` (gram = explicit, eig = dense,
+ * method nullspace or espirit); field = naive (the H(x) filter field) returns
+ * SK_ERR_UNSUPPORTED.
  * grid_dims: explicit map grid (all > 0) overrides grid/grid_pad, which is
  * how the reference drives anisotropic grids (pipeline::compute_field /
  * finalize with explicit dims, maps.hpp:115-123). */
@@ -117,6 +119,16 @@ int sk_reduced_grid_dims(int ndim, const int64_t* calib_dims, int64_t pad, const
 int sk_gram_fft(sk_ctx* ctx, int ndim, const int64_t* calib_dims, int64_t channels, const sk_c64* calib,
                 int shape, int tau, sk_c64* gram);
 
+/* build_calib_matrix (calibration.hpp:32, calibration.cpp:30-68): cmat is
+ * P x n column-major (P = prod(E - 2 tau) valid shifts, row-major shift
+ * order; column q*|Lambda| + i); *rows = P.  cmat == NULL only reports P. */
+int sk_build_calib_matrix(sk_ctx* ctx, int ndim, const int64_t* calib_dims, int64_t channels, const sk_c64* calib,
+                          int shape, int tau, sk_c64* cmat, int64_t* rows);
+
+/* gram_explicit (calibration.hpp:35, calibration.cpp:70-78): gram = C^H C
+ * (n x n column-major, exactly Hermitian), accumulated in FP64. */
+int sk_gram_explicit(sk_ctx* ctx, int64_t rows, int64_t n, const sk_c64* cmat, sk_c64* gram);
+
 /* extract_nullspace (nullspace.hpp:24, nullspace.cpp:7-35): spectrum = all n
  * singular values, descending; filters (may be NULL) n x R column-major.
  * filters_capacity: number of columns the caller allocated (>= R or error). */
@@ -138,6 +150,13 @@ int sk_espirit_inplace(sk_ctx* ctx, int64_t voxels, int64_t channels, sk_c64* fi
  * GramField layout; vectors Q x N (column per voxel); values = Re(v^H B v). */
 int sk_eig_power_field(sk_ctx* ctx, int64_t voxels, int64_t channels, const sk_c64* b_field, int iters,
                        sk_c64* vectors, float* values);
+
+/* eig_dense_field (eigensolve.hpp:21, eigensolve.cpp:9-38): field in the
+ * GramField layout; largest = 0 selects Extremal::smallest.  vectors Q x N
+ * (unit column per voxel), values = extremal eigenvalue, second_values = the
+ * runner-up (each output may be NULL).  FP64 cyclic Jacobi per voxel. */
+int sk_eig_dense_field(sk_ctx* ctx, int64_t voxels, int64_t channels, const sk_c64* field, int largest,
+                       sk_c64* vectors, float* values, float* second_values);
 
 /* normalize_maps (maps.hpp:92-94, maps.cpp:101-176). */
 int sk_normalize_maps(sk_ctx* ctx, int ndim, const int64_t* dims, int64_t channels, const sk_c64* raw,

@@ -19,6 +19,7 @@ __all__ = [
     "RECT", "ELLIPSOID", "GRID_FULL", "GRID_REDUCED", "PipelineConfig", "Calib", "SensitivityResult",
     "SensKitError", "NullspaceEmptyError", "DimError", "LengthError", "CudaError", "UnsupportedError",
     "Context", "default_context", "lib", "library_path", "make_support", "reduced_grid_dims", "gram_fft",
+    "build_calib_matrix", "gram_explicit", "eig_dense_field",
     "extract_nullspace", "aggregate_w", "gram_field_fast", "espirit", "eig_power_field", "normalize_maps",
     "interpolate_maps", "interpolate_real", "support_mask", "estimate_maps", "estimate_maps_batched",
     "DevicePtr", "STAGES",
@@ -80,7 +81,8 @@ class sk_provenance(C.Structure):
 
 @dataclass
 class PipelineConfig:
-    """PipelineConfig (maps.hpp:23-45).  The B200 path implements the pisco arm."""
+    """PipelineConfig (maps.hpp:23-45).  Dataclass defaults are the pisco preset (the
+    reference's struct defaults are the baseline one; both presets run on the GPU)."""
     kernel: int = ELLIPSOID
     tau: int = 3
     gram: int = 1            # fft
@@ -100,6 +102,10 @@ class PipelineConfig:
     @staticmethod
     def pisco() -> "PipelineConfig":   # maps.cpp:21-28
         return PipelineConfig()
+
+    @staticmethod
+    def baseline() -> "PipelineConfig":   # maps.cpp:12-19: rect kernel, explicit Gram, full grid, dense eig
+        return PipelineConfig(kernel=RECT, gram=0, grid=GRID_FULL, eig=0)
 
     def to_c(self) -> sk_config:
         gd = (C.c_int64 * 3)(*(list(self.grid_dims or ()) + [0, 0, 0])[:3])
@@ -161,6 +167,9 @@ _SIGS = {
     "sk_make_support": ([_I32, _I32, _I32, _VP, _VP], _I32),
     "sk_reduced_grid_dims": ([_I32, _VP, _I64, _VP, _VP], _I32),
     "sk_gram_fft": ([_VP, _I32, _VP, _I64, _VP, _I32, _I32, _VP], _I32),
+    "sk_build_calib_matrix": ([_VP, _I32, _VP, _I64, _VP, _I32, _I32, _VP, _VP], _I32),
+    "sk_gram_explicit": ([_VP, _I64, _I64, _VP, _VP], _I32),
+    "sk_eig_dense_field": ([_VP, _I64, _I64, _VP, _I32, _VP, _VP, _VP], _I32),
     "sk_extract_nullspace": ([_VP, _I64, _VP, _D, _VP, _VP, _VP, _I64], _I32),
     "sk_aggregate_w": ([_VP, _I64, _I64, _VP, _VP], _I32),
     "sk_gram_field_fast": ([_VP, _I64, _VP, _I32, _I32, _I32, _VP, _VP], _I32),
@@ -300,6 +309,30 @@ def gram_fft(calib: Calib, shape: int, tau: int, ctx: Context | None = None) -> 
     return g
 
 
+def build_calib_matrix(calib: Calib, shape: int, tau: int, ctx: Context | None = None) -> np.ndarray:
+    """build_calib_matrix (calibration.hpp:32) -> (P, n) complex64, P valid shifts."""
+    d = _c64(calib.data)
+    q, dims = d.shape[0], d.shape[1:]
+    rows = C.c_int64(0)
+    _check(lib().sk_build_calib_matrix(_ctx(ctx), len(dims), _p(_i64(dims)), q, _p(d), int(shape), int(tau), None,
+                                       C.byref(rows)))
+    n = q * make_support(shape, tau, len(dims)).shape[0]
+    c = np.zeros((rows.value, n), dtype=np.complex64, order="F")
+    if c.size:
+        _check(lib().sk_build_calib_matrix(_ctx(ctx), len(dims), _p(_i64(dims)), q, _p(d), int(shape), int(tau),
+                                           c.ctypes.data_as(C.c_void_p), C.byref(rows)))
+    return c
+
+
+def gram_explicit(cmat: np.ndarray, ctx: Context | None = None) -> np.ndarray:
+    """gram_explicit (calibration.hpp:35) -> (n, n) complex64 C^H C (FP64 accumulation)."""
+    c = np.asfortranarray(cmat, dtype=np.complex64)
+    rows, n = c.shape
+    g = np.zeros((n, n), dtype=np.complex64, order="F")
+    _check(lib().sk_gram_explicit(_ctx(ctx), rows, n, c.ctypes.data_as(C.c_void_p), g.ctypes.data_as(C.c_void_p)))
+    return g
+
+
 @dataclass
 class NullspaceBasis:
     """NullspaceBasis (nullspace.hpp:11-19)."""
@@ -362,6 +395,17 @@ def eig_power_field(bfield: np.ndarray, iters: int = 10, ctx: Context | None = N
     val = np.zeros(n, dtype=np.float32)
     _check(lib().sk_eig_power_field(_ctx(ctx), n, q, _p(buf), int(iters), _p(vec), _p(val)))
     return vec.reshape(n, q).T.copy(), val
+
+
+def eig_dense_field(field: np.ndarray, largest: bool, ctx: Context | None = None):
+    """eig_dense_field (eigensolve.hpp:21) -> (vectors (Q, N), values (N,), second_values (N,))."""
+    n, q, _ = field.shape
+    buf = _field_buf(field)
+    vec = np.zeros(q * n, dtype=np.complex64)
+    val = np.zeros(n, dtype=np.float32)
+    sec = np.zeros(n, dtype=np.float32)
+    _check(lib().sk_eig_dense_field(_ctx(ctx), n, q, _p(buf), 1 if largest else 0, _p(vec), _p(val), _p(sec)))
+    return vec.reshape(n, q).T.copy(), val, sec
 
 
 def normalize_maps(raw: np.ndarray, calib: Calib, apod_width: float = -1.0, ctx: Context | None = None):

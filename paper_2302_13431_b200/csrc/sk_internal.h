@@ -199,6 +199,31 @@ struct PowerArgs {
 };
 void power_iteration(sk_ctx* ctx, const PowerArgs& a);
 
+// Baseline preset (sk_dense.cu).
+// build_calib_matrix (calibration.cpp:30-68): P x Q|Lambda| column-major, FP64.
+void calib_matrix(sk_ctx* ctx, const float2* calib, const Dims& cdims, int q, const Support& s, const int* d_off,
+                  double2* c);
+// gram_explicit (calibration.cpp:70-78): lower <- C^H C (ZHERK), gram <- full Hermitian c64.
+void gram_explicit_dev(sk_ctx* ctx, const double2* c, i64 rows, i64 n, double2* lower, float2* gram);
+// eig_dense_field (eigensolve.cpp:9-38) on packed planes: per voxel the extremal
+// eigenpair of B = alpha I + beta (hi + lo) by FP64 cyclic Jacobi.
+struct DenseEigArgs {
+  const float2* planes;
+  const float2* planes_lo;  // nullable
+  i64 n;
+  int q;
+  int largest;              // 1: largest (ESPIRiT), 0: smallest (nullspace method)
+  double alpha, beta;
+  float2* vec;              // [Q][N] unit eigenvectors
+  float* value;             // [N] nullable
+  float* second;            // [N] runner-up eigenvalue, nullable
+  float* lambda;            // [N] lam_add + lam_mul * value, nullable
+  uint8_t* mask;            // [N] lambda < mask_threshold, nullable
+  double lam_add, lam_mul;
+  float mask_threshold;
+};
+void dense_eig(sk_ctx* ctx, const DenseEigArgs& a);
+
 // Conversions / small elementwise kernels.
 void c64_to_c128(sk_ctx* ctx, const float2* in, double2* out, i64 n);
 void c128_to_c64(sk_ctx* ctx, const double2* in, float2* out, i64 n);

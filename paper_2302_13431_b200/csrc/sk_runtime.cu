@@ -433,6 +433,37 @@ float2* run_gram(sk_ctx* ctx, const Dims& cdims, i64 q, const float2* calib, con
   return gram;
 }
 
+// Support offsets (|Lambda| x nd, kernels.cpp:7-35) on the device, cached per context.
+const int* support_offsets_dev(sk_ctx* ctx, const Support& s) {
+  const std::string key = "suppoff:" + std::to_string(s.shape) + ":" + std::to_string(s.tau) + ":" + std::to_string(s.nd);
+  auto it = ctx->tables.find(key);
+  if (it != ctx->tables.end()) return static_cast<const int*>(it->second);
+  void* d = nullptr;
+  SKB_CUDA(cudaMalloc(&d, std::max<size_t>(1, s.offsets.size()) * sizeof(int)));
+  SKB_CUDA(cudaMemcpy(d, s.offsets.data(), s.offsets.size() * sizeof(int), cudaMemcpyHostToDevice));
+  ctx->tables[key] = d;
+  return static_cast<const int*>(d);
+}
+
+i64 valid_shift_rows(const Dims& cdims, int tau) {
+  i64 p = 1;
+  for (i64 d : cdims) p *= std::max<i64>(0, d - 2 * tau);
+  return p;
+}
+
+// Baseline Gram (calibration.cpp:30-78): C gathered in FP64, C^H C by one
+// ZHERK, mirrored into the full Hermitian c64 matrix.
+float2* run_gram_explicit(sk_ctx* ctx, const Dims& cdims, i64 q, const float2* calib, const Support& s,
+                          float2* gram_dst) {
+  const i64 n = q * s.count, rows = valid_shift_rows(cdims, s.tau);
+  double2* c = ctx->arena.get<double2>("gramx:C", std::max<i64>(1, rows * n));
+  double2* lower = ctx->arena.get<double2>("gramx:lower", n * n);
+  calib_matrix(ctx, calib, cdims, int(q), s, support_offsets_dev(ctx, s), c);
+  float2* gram = gram_dst ? gram_dst : ctx->arena.get<float2>("gram:G", n * n);
+  gram_explicit_dev(ctx, c, rows, n, lower, gram);
+  return gram;
+}
+
 // ---------------------------------------------------------------- K2
 struct Eig {
   std::vector<double> evals;  // ascending
@@ -1262,8 +1293,9 @@ struct PipelineOut {
 
 void validate_config(const sk_config* cfg) {
   if (!cfg) fail(SK_ERR_DIM, "null config");
-  if (cfg->gram != 1) fail(SK_ERR_UNSUPPORTED, "gram = explicit is the baseline arm; the B200 path runs gram_fft");
-  if (cfg->eig != 1) fail(SK_ERR_UNSUPPORTED, "eig = dense is the baseline arm; the B200 path runs power iteration");
+  if (cfg->gram != 0 && cfg->gram != 1) fail(SK_ERR_DIM, "unknown gram method");
+  if (cfg->eig != 0 && cfg->eig != 1) fail(SK_ERR_DIM, "unknown eig method");
+  if (cfg->method != 0 && cfg->method != 1) fail(SK_ERR_DIM, "unknown map method");
   if (cfg->field != 1) fail(SK_ERR_UNSUPPORTED, "field = naive is the H(x) baseline; the B200 path runs the fast field");
   if (cfg->kernel != 0 && cfg->kernel != 1) fail(SK_ERR_DIM, "unknown kernel shape");
   if (cfg->power_iters < 0) fail(SK_ERR_DIM, "power_iters must be >= 0");
@@ -1306,7 +1338,9 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   cudaEvent_t* ev = ctx->ev;
   SKB_CUDA(cudaEventRecord(ev[0], ctx->stream));
   // gram
-  float2* gram = run_gram(ctx, cdims, q, calib, s, out.gram);
+  // compute_gram (maps.cpp:180-186)
+  float2* gram = cfg->gram == 0 ? run_gram_explicit(ctx, cdims, q, calib, s, out.gram)
+                                : run_gram(ctx, cdims, q, calib, s, out.gram);
   SKB_CUDA(cudaEventRecord(ev[1], ctx->stream));
   // nullspace
   Eig e = run_nullspace(ctx, gram, n, cfg->nullspace_threshold, cfg->eig_solver, out.spectrum != nullptr,
@@ -1325,6 +1359,35 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   SKB_CUDA(cudaMemsetAsync(zeroed, 0, sizeof(unsigned long long), ctx->stream));
   float2* maps_grid = (!interp && out.maps) ? out.maps : ctx->arena.get<float2>("post:maps_grid", q * ngrid);
   float* lam_grid = (!interp && out.lambda) ? out.lambda : ctx->arena.get<float>("post:lam_grid", ngrid);
+  if (cfg->eig == 0) {
+    // solve_field, dense arm (maps.cpp:207-218): nullspace method -> smallest
+    // eigenpair of G, lambda = value / |Lambda|; ESPIRiT -> largest eigenpair
+    // of B = I - G/|Lambda|, lambda = 1 - value.  Then normalize_maps.
+    const bool nullspace = cfg->method == 0;
+    DenseEigArgs d{};
+    d.planes = planes;
+    d.planes_lo = pl.lo;
+    d.n = ngrid;
+    d.q = int(q);
+    d.largest = nullspace ? 0 : 1;
+    d.alpha = nullspace ? 0.0 : 1.0;
+    d.beta = nullspace ? 1.0 : -1.0 / double(lam);
+    d.lam_add = nullspace ? 0.0 : 1.0;
+    d.lam_mul = nullspace ? 1.0 / double(lam) : -1.0;
+    d.vec = out.raw_maps ? out.raw_maps : maps_grid;
+    d.lambda = lam_grid;
+    d.mask = (!interp && !slab && out.mask) ? out.mask : nullptr;
+    d.mask_threshold = float(cfg->mask_threshold);
+    dense_eig(ctx, d);
+    if (out.raw_maps) {
+      if (out.raw_lambda)
+        SKB_CUDA(cudaMemcpyAsync(out.raw_lambda, lam_grid, size_t(ngrid) * sizeof(float), cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+      SKB_CUDA(cudaMemcpyAsync(maps_grid, out.raw_maps, size_t(q * ngrid) * sizeof(float2), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+    }
+    normalize_standalone(ctx, maps_grid, ngrid, int(q), recon, zeroed);
+  } else {
   if (out.raw_maps) {
     // raw (pre-normalisation) eigenvectors for parity dumps: run K4 without the epilogue first
     PowerArgs r{};
@@ -1349,6 +1412,7 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   pa.mask_threshold = float(cfg->mask_threshold);
   pa.zeroed = zeroed;
   power_iteration(ctx, pa);
+  }
   SKB_CUDA(cudaEventRecord(ev[5], ctx->stream));
   // post (part 2): interpolation + renormalisation + mask (maps.cpp:236-258)
   if (interp) {
@@ -1508,6 +1572,76 @@ int sk_gram_fft(sk_ctx* ctx, int ndim, const int64_t* calib_dims, int64_t channe
     Out<float2> g(ctx, reinterpret_cast<float2*>(gram), n * n, "out:gram");
     run_gram(ctx, cd, channels, d_cal, s, g.dev);
     g.finish(ctx);
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_build_calib_matrix(sk_ctx* ctx, int ndim, const int64_t* calib_dims, int64_t channels, const sk_c64* calib,
+                          int shape, int tau, sk_c64* cmat, int64_t* rows) {
+  return guarded([&] {
+    require_ctx(ctx);
+    const Dims cd = dims_of(ndim, calib_dims);
+    const Support s = make_support(shape, tau, ndim);
+    check_calib(cd, channels, s);
+    const i64 n = channels * s.count, p = valid_shift_rows(cd, s.tau);
+    if (rows) *rows = p;
+    if (cmat == nullptr) return;
+    const float2* d_cal = device_in(ctx, reinterpret_cast<const float2*>(calib), channels * numel(cd), "in:calib");
+    double2* c = ctx->arena.get<double2>("gramx:C", std::max<i64>(1, p * n));
+    calib_matrix(ctx, d_cal, cd, int(channels), s, support_offsets_dev(ctx, s), c);
+    Out<float2> o(ctx, reinterpret_cast<float2*>(cmat), p * n, "out:cmat");
+    c128_to_c64(ctx, c, o.dev, p * n);
+    o.finish(ctx);
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_gram_explicit(sk_ctx* ctx, int64_t rows, int64_t n, const sk_c64* cmat, sk_c64* gram) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (rows < 0 || n < 1) fail(SK_ERR_DIM, "gram_explicit: bad calibration matrix shape");
+    const float2* d_c = device_in(ctx, reinterpret_cast<const float2*>(cmat), rows * n, "in:cmat");
+    double2* c = ctx->arena.get<double2>("gramx:C", std::max<i64>(1, rows * n));
+    c64_to_c128(ctx, d_c, c, rows * n);
+    double2* lower = ctx->arena.get<double2>("gramx:lower", n * n);
+    Out<float2> g(ctx, reinterpret_cast<float2*>(gram), n * n, "out:gram");
+    gram_explicit_dev(ctx, c, rows, n, lower, g.dev);
+    g.finish(ctx);
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_eig_dense_field(sk_ctx* ctx, int64_t voxels, int64_t q, const sk_c64* field, int largest, sk_c64* vectors,
+                       float* values, float* second_values) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (voxels < 0 || q < 1) fail(SK_ERR_DIM, "eig_dense_field: bad field shape");
+    if (q > 64) fail(SK_ERR_UNSUPPORTED, "more than 64 channels is outside the B200 path");
+    if (voxels == 0) return;
+    const float2* d_f = device_in(ctx, reinterpret_cast<const float2*>(field), voxels * q * q, "in:field");
+    float2* planes = ctx->arena.get<float2>("field:planes", voxels * q * (q + 1) / 2);
+    field_full_to_planes(ctx, d_f, voxels, int(q), planes);
+    float2* vec = ctx->arena.get<float2>("dense:vec", voxels * q);
+    Out<float> val(ctx, values, voxels, "out:values");
+    Out<float> sec(ctx, second_values, voxels, "out:second");
+    DenseEigArgs d{};
+    d.planes = planes;
+    d.n = voxels;
+    d.q = int(q);
+    d.largest = largest ? 1 : 0;
+    d.alpha = 0.0;
+    d.beta = 1.0;
+    d.vec = vec;
+    d.value = val.dev;
+    d.second = sec.dev;
+    dense_eig(ctx, d);
+    if (vectors) {  // [Q][N] -> Q x N column per voxel (eigensolve.hpp:13)
+      Out<float2> v(ctx, reinterpret_cast<float2*>(vectors), voxels * q, "out:vectors");
+      copy_strided(ctx, vec, 1, voxels, v.dev, q, 1, voxels, q);
+      v.finish(ctx);
+    }
+    val.finish(ctx);
+    sec.finish(ctx);
     SKB_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }

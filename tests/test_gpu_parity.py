@@ -428,7 +428,7 @@ def test_pipeline_errors(K):  # test_maps.cpp:192-217
     with pytest.raises(K.DimError):
         K.estimate_maps(K.Calib(st, (6, 6)), (8, 8), K.PipelineConfig())
     with pytest.raises(K.UnsupportedError):
-        K.estimate_maps(K.Calib(st, (6, 6)), (12, 12), K.PipelineConfig(gram=0))
+        K.estimate_maps(K.Calib(st, (6, 6)), (12, 12), K.PipelineConfig(field=0))
 
 
 def test_determinism_and_device_buffers(K):
@@ -604,3 +604,104 @@ def test_batched_multislice_equals_per_slice(K):
         assert d_maps < 1e-6, s
         assert np.allclose(lam[s], ref.lambda_min_map, rtol=1e-6, atol=1e-7), s  # ~1 ulp near 1
         assert (mask[s] == ref.support_mask).mean() > 0.9999, s
+
+
+# ------------------------------------------------- baseline preset
+@pytest.mark.parametrize("shape,tau,dims,q", [(0, 3, (24, 24), 8), (1, 2, (12, 14), 3), (0, 1, (9, 10, 8), 2),
+                                              (0, 2, (13,), 4)])
+def test_build_calib_matrix_and_gram_explicit(K, O, shape, tau, dims, q):  # test_calibration.cpp:9-60
+    cal = rnd((q,) + dims, 21)
+    cm = K.build_calib_matrix(K.Calib(cal, tuple(d // 2 for d in dims)), shape, tau)
+    ref = O.build_calib_matrix(O.Calib(f32(cal), tuple(d // 2 for d in dims)), shape, tau)
+    assert cm.shape == ref.shape and np.array_equal(cm.astype(np.complex128), ref)  # a gather: bit-exact
+    g = K.gram_explicit(cm)
+    gref = O.gram_explicit(O.Calib(f32(cal), tuple(d // 2 for d in dims)), shape, tau)
+    err = PM.rel_fro(g, gref)
+    report("gram_explicit", shape=shape, tau=tau, dims=dims, q=q, rel_fro=err)
+    assert err < 1e-6  # FP64 accumulation, one float32 rounding
+    assert np.abs(g - g.conj().T).max() == 0.0 and np.all(np.diag(g).imag == 0)
+
+
+def test_gram_explicit_equals_fft_when_support_is_one_point(K):  # calibration.hpp:40-41
+    cal = rnd((3, 10, 12), 22)
+    c = K.Calib(cal, (5, 6))
+    g1 = K.gram_explicit(K.build_calib_matrix(c, K.RECT, 0))
+    g2 = K.gram_fft(c, K.RECT, 0)
+    assert PM.rel_fro(g1, g2) < 1e-6
+
+
+@pytest.mark.parametrize("q", [1, 2, 3, 8, 13, 32, 64])
+@pytest.mark.parametrize("largest", [False, True])
+def test_dense_eig_parity(K, O, q, largest):
+    n = 200 if q < 32 else 60
+    m = rnd((n, q, q), 31, np.complex128)
+    herm = (m + m.conj().transpose(0, 2, 1)) / 2
+    shift = (2.5 if largest else -2.5) * q ** 0.5 * np.eye(q)
+    herm = (herm + shift).astype(np.complex64)  # well-separated extremal eigenvalue
+    vg, valg, secg = K.eig_dense_field(herm, largest)
+    vo, valo, seco = O.eig_dense_field(f32(herm), largest)
+    ph = np.sum(vo.conj() * vg, 0)
+    ph = ph / np.maximum(np.abs(ph), 1e-300)
+    err_v = np.abs(vg - vo * ph[None]).max()
+    err_l = np.abs(valg - valo).max() / np.abs(valo).max()
+    err_s = np.abs(secg - seco).max() / np.abs(valo).max() if q > 1 else 0.0
+    report("dense_eig", q=q, largest=largest, vec_max=float(err_v), value_rel=float(err_l), second_rel=float(err_s))
+    assert err_v < 1e-5 and err_l < 1e-6 and err_s < 1e-6
+    assert np.abs(np.sum(np.abs(vg) ** 2, 0) - 1).max() < 1e-6
+
+
+def test_dense_eig_known_answers(K):  # test_eigensolve.cpp:9-40
+    d = np.diag([3.0, -1.0, 2.0]).astype(np.complex64)[None]
+    v, val, sec = K.eig_dense_field(d, largest=False)
+    assert val[0] == -1.0 and sec[0] == 2.0 and abs(abs(v[1, 0]) - 1) < 1e-7
+    v, val, sec = K.eig_dense_field(d, largest=True)
+    assert val[0] == 3.0 and sec[0] == 2.0 and abs(abs(v[0, 0]) - 1) < 1e-7
+    v, val, _ = K.eig_dense_field(np.zeros((2, 4, 4), np.complex64), largest=False)
+    assert np.all(val == 0) and np.array_equal(v[:, 0], [1, 0, 0, 0])
+    h = np.array([[2, 1j], [-1j, 2]], dtype=np.complex64)[None]  # eigenvalues 1, 3
+    v, val, sec = K.eig_dense_field(h, largest=True)
+    assert abs(val[0] - 3) < 1e-6 and abs(sec[0] - 1) < 1e-6
+    assert np.abs(h[0] @ v[:, 0] - 3 * v[:, 0]).max() < 1e-6
+
+
+def _baseline_check(K, O, calib, co, full, ck, cfo, name, grid=None):
+    ref = O.estimate_maps(O.Calib(f32(calib), co), full, cfo, grid_dims=grid, want_raw=True)
+    res = K.estimate_maps(K.Calib(calib, co), full, ck, want_raw=True)
+    assert res.nullspace_rank == ref.nullspace_rank, (res.nullspace_rank, ref.nullspace_rank)
+    lam_raw = PM.lambda_errors(res.raw_lambda, ref.raw_lambda)
+    lam_fin = PM.lambda_errors(res.lambda_min_map, ref.lambda_min_map, ref.support_mask)
+    nrmse = PM.maps_nrmse(res.maps, ref.maps, ref.support_mask)
+    mask_agree = float(np.mean(res.support_mask == ref.support_mask))
+    report("estimate_maps_baseline", case=name, rank=res.nullspace_rank, lambda_raw=lam_raw, lambda_final=lam_fin,
+           maps_nrmse=nrmse, mask_agree=mask_agree, stage_ms=res.stage_ms, total_ms=res.total_ms)
+    assert lam_raw["normwise"] < PM.TOL_LAMBDA and lam_fin["normwise"] < PM.TOL_LAMBDA
+    assert nrmse < PM.TOL_MAPS
+    assert mask_agree > 0.999
+    m = res.maps.reshape(res.maps.shape[0], -1)[:, res.support_mask.ravel() > 0]
+    assert np.abs(np.sum(np.abs(m) ** 2, 0) - 1).max() < 1e-4
+    return res, ref, lam_raw
+
+
+def test_estimate_maps_baseline_preset(K, O):
+    """PipelineConfig::baseline() (maps.cpp:12-19) on the C1 scene: rect kernel, explicit Gram, full grid,
+    dense per-voxel eigensolve with the nullspace method (lambda = smallest eigenvalue / |Lambda|)."""
+    from paper_2302_13431_b200 import phantom
+    case = phantom.generate("C1")
+    ck = K.PipelineConfig.baseline()
+    cfo = O.PipelineConfig.baseline()
+    _, _, lam = _baseline_check(K, O, case.calib[0], case.center_offset, case.spec.full_dims, ck, cfo, "C1/baseline")
+    assert lam["pointwise_p99"] < PM.TOL_LAMBDA
+
+
+def test_estimate_maps_dense_espirit_reduced(K, O):
+    """eig = dense with method = espirit (largest eigenpair of B = I - G/|Lambda|) on a reduced grid, both Gram
+    paths, next to the power arm."""
+    sc = O.simulate(6, (48, 40), 2, 5, noise_sigma=0.01, noise_seed=6)
+    cal = O.extract_calibration(sc["kspace"], (20, 18))
+    calib = cal.data.astype(np.complex64)
+    for gram in (0, 1):
+        ck = K.PipelineConfig(kernel=K.RECT, tau=2, grid_pad=10, eig=0, method=1, gram=gram)
+        cfo = O.PipelineConfig.pisco()
+        cfo.kernel, cfo.tau, cfo.grid_pad, cfo.eig, cfo.method, cfo.gram = O.RECT, 2, 10, 0, 1, gram
+        _, _, lam = _baseline_check(K, O, calib, cal.center_offset, (48, 40), ck, cfo, f"dense-espirit/gram{gram}")
+        assert lam["pointwise_max"] < PM.TOL_LAMBDA

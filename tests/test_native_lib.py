@@ -24,7 +24,8 @@ def test_header_declares_the_reference_entry_points():
     syms = declared_symbols()
     for name in ["sk_gram_fft", "sk_extract_nullspace", "sk_aggregate_w", "sk_gram_field_fast", "sk_espirit_inplace",
                  "sk_eig_power_field", "sk_normalize_maps", "sk_interpolate_maps", "sk_interpolate_real",
-                 "sk_support_mask", "sk_estimate_maps", "sk_make_support", "sk_reduced_grid_dims"]:
+                 "sk_support_mask", "sk_estimate_maps", "sk_make_support", "sk_reduced_grid_dims",
+                 "sk_build_calib_matrix", "sk_gram_explicit", "sk_eig_dense_field"]:
         assert name in syms
 
 
