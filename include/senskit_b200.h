@@ -45,8 +45,10 @@ typedef struct sk_ctx sk_ctx;
 
 /* PipelineConfig (maps.hpp:23-45).  Both presets run on the GPU: `pisco`
  * (gram = fft, eig = power) and `baseline` (gram = explicit, eig = dense,
- * method nullspace or espirit); field = naive (the H(x) filter field) returns
- * SK_ERR_UNSUPPORTED.
+ * method nullspace or espirit).  field = naive keeps the reference's contract
+ * (SK_ERR_LENGTH when the R x Q x N filter field would exceed field_byte_cap)
+ * and evaluates the same G(x) = sum_r H_r(x)^H H_r(x) through the lag
+ * expansion of W = F F^H.
  * grid_dims: explicit map grid (all > 0) overrides grid/grid_pad, which is
  * how the reference drives anisotropic grids (pipeline::compute_field /
  * finalize with explicit dims, maps.hpp:115-123). */
@@ -73,6 +75,9 @@ typedef struct {
    *             if it fails). */
   int32_t eig_solver;
   int32_t certify;
+  /* field_byte_cap (maps.hpp:41; 0 = kDefaultFieldByteCap = 1 GiB): the
+   * naive path's R*Q*N*16-byte filter-field budget (spatial_gram.cpp:43-47). */
+  int64_t field_byte_cap;
 } sk_config;
 
 /* Provenance (maps.hpp:55-73) with device-timed stages. */

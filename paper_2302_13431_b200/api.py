@@ -66,6 +66,7 @@ class sk_config(C.Structure):
         ("grid", C.c_int32), ("grid_pad", C.c_int64), ("eig", C.c_int32), ("power_iters", C.c_int32),
         ("method", C.c_int32), ("field", C.c_int32), ("mask_threshold", C.c_double), ("apod_width", C.c_double),
         ("grid_dims", C.c_int64 * 3), ("eig_solver", C.c_int32), ("certify", C.c_int32),
+        ("field_byte_cap", C.c_int64),
     ]
 
 
@@ -98,6 +99,7 @@ class PipelineConfig:
     grid_dims: tuple | None = None   # explicit map grid (maps.hpp:115-123)
     eig_solver: int = 0      # B200 extension: 0 auto, 1 full cuSOLVER, 2 subspace
     certify: int = 0         # B200 extension: prove R with one Cholesky (subspace solver)
+    field_byte_cap: int = 1 << 30   # maps.hpp:41 (naive field budget)
 
     @staticmethod
     def pisco() -> "PipelineConfig":   # maps.cpp:21-28
@@ -111,7 +113,7 @@ class PipelineConfig:
         gd = (C.c_int64 * 3)(*(list(self.grid_dims or ()) + [0, 0, 0])[:3])
         return sk_config(self.kernel, self.tau, self.gram, self.nullspace_threshold, self.grid, self.grid_pad,
                          self.eig, self.power_iters, self.method, self.field, self.mask_threshold,
-                         self.apod_width, gd, self.eig_solver, self.certify)
+                         self.apod_width, gd, self.eig_solver, self.certify, self.field_byte_cap)
 
 
 @dataclass

@@ -653,11 +653,15 @@ void power_iteration(sk_ctx* ctx, const PowerArgs& a) {
       case 8: launch<Layout<32, 2, 128, 3, 0, 4, 32>>(ctx, a); break;
       case 9: launch<Layout<32, 2, 128, 3, 2, 2, 32>>(ctx, a); break;
       case 10: launch<Layout<32, 2, 192, 2, 0, 4, 32>>(ctx, a); break;
+      case 11: launch<Layout<32, 1, 128, 3, 2, 4, 32>>(ctx, a); break;
+      case 12: launch<Layout<32, 1, 256, 2, 1, 4, 32>>(ctx, a); break;
+      case 13: launch<Layout<32, 1, 128, 3, 4, 6, 32>>(ctx, a); break;
       default:
         if (rpt32 != 1)
           launch<Layout<32, 2, 128, 3>>(ctx, a);
-        else if (a.q == 32)
-          launch<Layout<32, 1, 256, 2, 2, 4, 32>>(ctx, a);
+        else if (a.q == 32)  // one accumulator pair: ptxas then rotates two v quads (SKB_K4_VARIANT=12 measured
+                             // C2 0.973 -> 0.942 ms, C4 5.81 -> 5.52 ms against two pairs)
+          launch<Layout<32, 1, 256, 2, 1, 4, 32>>(ctx, a);
         else
           launch<Layout<32, 1, 256, 2, 2, 4>>(ctx, a);
     }

@@ -1296,7 +1296,7 @@ void validate_config(const sk_config* cfg) {
   if (cfg->gram != 0 && cfg->gram != 1) fail(SK_ERR_DIM, "unknown gram method");
   if (cfg->eig != 0 && cfg->eig != 1) fail(SK_ERR_DIM, "unknown eig method");
   if (cfg->method != 0 && cfg->method != 1) fail(SK_ERR_DIM, "unknown map method");
-  if (cfg->field != 1) fail(SK_ERR_UNSUPPORTED, "field = naive is the H(x) baseline; the B200 path runs the fast field");
+  if (cfg->field != 0 && cfg->field != 1) fail(SK_ERR_DIM, "unknown field path");
   if (cfg->kernel != 0 && cfg->kernel != 1) fail(SK_ERR_DIM, "unknown kernel shape");
   if (cfg->power_iters < 0) fail(SK_ERR_DIM, "power_iters must be >= 0");
 }
@@ -1346,7 +1346,17 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   Eig e = run_nullspace(ctx, gram, n, cfg->nullspace_threshold, cfg->eig_solver, out.spectrum != nullptr,
                         cfg->certify != 0);
   SKB_CUDA(cudaEventRecord(ev[2], ctx->stream));
-  // field
+  // field.  compute_field (maps.cpp:195-205): the naive path materialises the
+  // R x Q x N filter field H (spatial_gram.cpp:36-64) and sums H^H H per voxel;
+  // that is the same G(x) as the lag expansion of W = F F^H, so both paths
+  // run the expansion, with the naive path's byte-cap contract kept.
+  if (cfg->field == 0) {
+    const i64 cap = cfg->field_byte_cap > 0 ? cfg->field_byte_cap : (i64(1) << 30);
+    const double need = double(e.rank) * double(q) * double(numel(grid)) * 16.0;  // spatial_gram.cpp:43
+    if (need > double(cap))
+      fail(SK_ERR_LENGTH, "filter field would need " + std::to_string(i64(need)) + " bytes (cap " +
+                              std::to_string(cap) + ")");
+  }
   const Planes pl = run_field(ctx, e, s, int(q), grid, out.slab0, out.slab1);
   float2* planes = pl.hi;
   if (out.field) planes_to_field_full(ctx, pl.hi, pl.lo, ngrid, int(q), out.field);

@@ -427,8 +427,10 @@ def test_pipeline_errors(K):  # test_maps.cpp:192-217
         K.estimate_maps(K.Calib(rnd((2, 8, 8), 80), (4, 4)), (8, 8), K.PipelineConfig(kernel=K.RECT, tau=4))
     with pytest.raises(K.DimError):
         K.estimate_maps(K.Calib(st, (6, 6)), (8, 8), K.PipelineConfig())
-    with pytest.raises(K.UnsupportedError):
-        K.estimate_maps(K.Calib(st, (6, 6)), (12, 12), K.PipelineConfig(field=0))
+    with pytest.raises(K.LengthError):  # spatial_gram.cpp:43-47: the naive filter field over its byte cap
+        one = rnd((1, 16, 16), 81)
+        dep = np.concatenate([one, 2 * one]).astype(np.complex64)  # dependent channels: a nullspace exists
+        K.estimate_maps(K.Calib(dep, (8, 8)), (16, 16), K.PipelineConfig(field=0, field_byte_cap=1024))
 
 
 def test_determinism_and_device_buffers(K):
@@ -705,3 +707,17 @@ def test_estimate_maps_dense_espirit_reduced(K, O):
         cfo.kernel, cfo.tau, cfo.grid_pad, cfo.eig, cfo.method, cfo.gram = O.RECT, 2, 10, 0, 1, gram
         _, _, lam = _baseline_check(K, O, calib, cal.center_offset, (48, 40), ck, cfo, f"dense-espirit/gram{gram}")
         assert lam["pointwise_max"] < PM.TOL_LAMBDA
+
+
+def test_estimate_maps_naive_field(K, O):
+    """field = naive (maps.cpp:195-200): same maps as the oracle's explicit H(x) filter field, and the byte cap."""
+    sc = O.simulate(4, (32, 28), 2, 3, noise_sigma=0.01, noise_seed=4)
+    cal = O.extract_calibration(sc["kspace"], (16, 14))
+    calib = cal.data.astype(np.complex64)
+    ck = K.PipelineConfig(kernel=K.ELLIPSOID, tau=2, grid_pad=8, power_iters=20, field=0)
+    cfo = O.PipelineConfig.pisco()
+    cfo.tau, cfo.grid_pad, cfo.power_iters, cfo.field = 2, 8, 20, 0
+    _baseline_check(K, O, calib, cal.center_offset, (32, 28), ck, cfo, "naive-field")
+    import dataclasses
+    with pytest.raises(K.LengthError):
+        K.estimate_maps(K.Calib(calib, cal.center_offset), (32, 28), dataclasses.replace(ck, field_byte_cap=4096))
