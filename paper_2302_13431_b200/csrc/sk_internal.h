@@ -261,6 +261,8 @@ void normalize_standalone(sk_ctx* ctx, float2* maps, i64 n, int q, const float2*
 void split_gram_tf32(sk_ctx* ctx, const float2* a, i64 n, float* hi, float* lo);
 void split_block_tf32(sk_ctx* ctx, const double2* v, i64 n, i64 m, float* hi, float* lo);
 void combine_block(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y);
+void split_block_cat_tf32(sk_ctx* ctx, const double2* v, i64 n, i64 m, float* vc);
+void combine_block_cat(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y);
 void random_block(sk_ctx* ctx, double2* v, i64 n, i64 cols, i64 col0, unsigned int seed);
 void ritz_residuals(sk_ctx* ctx, const double2* y, const double2* v, const double* theta, i64 n, i64 cols,
                     double* res);

@@ -431,6 +431,49 @@ __global__ void combine_block_kernel(const float* __restrict__ c, i64 n, i64 m, 
   }
 }
 
+// K-concatenated 3xTF32 operand: V' (2n x 4m, column-major) = [[V_hi, V_lo]; [0, V_hi]]
+// so that [A_hi | A_lo] V' = [A_hi V_hi, A_hi V_lo + A_lo V_hi] in ONE GEMM that
+// reads the split Gram once ([Re, Im] column blocks of width m inside each half).
+__global__ void split_block_cat_kernel(const double2* __restrict__ v, i64 n, i64 m, float* __restrict__ vc) {
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n * m; e += i64(gridDim.x) * blockDim.x) {
+    const i64 r = e % n, c = e / n;
+    const double2 x = v[e];
+    const i64 ld = 2 * n;
+    float h, l;
+    tf32_split(float(x.x), h, l);
+    vc[r + c * ld] = h;                    // [V_hi; 0], Re columns
+    vc[n + r + c * ld] = 0.f;
+    vc[r + (2 * m + c) * ld] = l;          // [V_lo; V_hi], Re columns
+    vc[n + r + (2 * m + c) * ld] = h;
+    tf32_split(float(x.y), h, l);
+    vc[r + (m + c) * ld] = h;              // Im columns
+    vc[n + r + (m + c) * ld] = 0.f;
+    vc[r + (3 * m + c) * ld] = l;
+    vc[n + r + (3 * m + c) * ld] = h;
+  }
+}
+// Y from C' = [A_hi | A_lo] V' (2n x 4m): C = C'[:, :2m] + C'[:, 2m:], then as combine_block.
+__global__ void combine_block_cat_kernel(const float* __restrict__ c, i64 n, i64 m, double2* __restrict__ y) {
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n * m; e += i64(gridDim.x) * blockDim.x) {
+    const i64 r = e % n, k = e / n, ld = 2 * n, h = 2 * m * ld;
+    const double c11 = double(c[r + k * ld]) + double(c[h + r + k * ld]);
+    const double c21 = double(c[n + r + k * ld]) + double(c[h + n + r + k * ld]);
+    const double c12 = double(c[r + (k + m) * ld]) + double(c[h + r + (k + m) * ld]);
+    const double c22 = double(c[n + r + (k + m) * ld]) + double(c[h + n + r + (k + m) * ld]);
+    y[e] = make_double2(c11 - c22, c12 + c21);
+  }
+}
+void split_block_cat_tf32(sk_ctx* ctx, const double2* v, i64 n, i64 m, float* vc) {
+  split_block_cat_kernel<<<SKB_GRID(n * m)>>>(v, n, m, vc);
+  ++ctx->launches;
+  SKB_LAUNCH("split_block_cat");
+}
+void combine_block_cat(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y) {
+  combine_block_cat_kernel<<<SKB_GRID(n * m)>>>(c, n, m, y);
+  ++ctx->launches;
+  SKB_LAUNCH("combine_block_cat");
+}
+
 void split_gram_tf32(sk_ctx* ctx, const float2* a, i64 n, float* hi, float* lo) {
   split_gram_kernel<<<SKB_GRID(n * n)>>>(a, n, hi, lo);
   ++ctx->launches;

@@ -875,9 +875,15 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   }();
   float* ghi = nullptr;
   float* glo = nullptr;
+  // SKB_TF32_CAT=0: three GEMMs (hi.hi, hi.lo, lo.hi); default one GEMM over
+  // the K-concatenated [A_hi | A_lo] (the split Gram is stored that way).
+  static const bool tf32_cat = [] {
+    const char* v = std::getenv("SKB_TF32_CAT");
+    return !v || std::atoi(v) != 0;
+  }();
   if (tf32x3) {
-    ghi = ctx->arena.get<float>("ss:ghi", 2 * n * n);
-    glo = ctx->arena.get<float>("ss:glo", 2 * n * n);
+    ghi = ctx->arena.get<float>("ss:gcat", 4 * n * n);
+    glo = ghi + 2 * n * n;
     split_gram_tf32(ctx, gram, n, ghi, glo);
   }
   laps.lap("promote");
@@ -938,21 +944,36 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
         if (i + 2 < q_plan && tf32x3) {
           // 3xTF32 on tensor cores: one real GEMM [Re A; Im A] [Re V, Im V] per
           // hi/lo combination (hi.hi + hi.lo + lo.hi), FP32-level accuracy.
-          float* vh = ctx->arena.get<float>("ss:vh", n * 2 * bcap);
-          float* vl = ctx->arena.get<float>("ss:vl", n * 2 * bcap);
-          float* cc = ctx->arena.get<float>("ss:cc", 2 * n * 2 * bcap);
-          split_block_tf32(ctx, V, n, b, vh, vl);
           const float one = 1.f, zero = 0.f;
-          const float* as[3] = {ghi, ghi, glo};
-          const float* bs[3] = {vh, vl, vh};
-          for (int g = 0; g < 3; ++g) {
-            check_cublas(cublasGemmEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(2 * n), int(2 * b), int(n), &one,
-                                      as[g], CUDA_R_32F, int(2 * n), bs[g], CUDA_R_32F, int(n), g == 0 ? &zero : &one,
-                                      cc, CUDA_R_32F, int(2 * n), CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT),
-                         "GemmEx(3xTF32)");
+          if (tf32_cat) {
+            // [A_hi | A_lo] (2n x 2n) [[V_hi, V_lo]; [0, V_hi]] (2n x 4b): the split
+            // Gram is read once per step instead of three times.
+            float* vcat = ctx->arena.get<float>("ss:vcat", 2 * n * 4 * bcap);
+            float* ccat = ctx->arena.get<float>("ss:ccat", 2 * n * 4 * bcap);
+            split_block_cat_tf32(ctx, V, n, b, vcat);
+            check_cublas(cublasGemmEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(2 * n), int(4 * b), int(2 * n), &one,
+                                      ghi, CUDA_R_32F, int(2 * n), vcat, CUDA_R_32F, int(2 * n), &zero, ccat,
+                                      CUDA_R_32F, int(2 * n), CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT),
+                         "GemmEx(3xTF32 cat)");
             ++ctx->lib_calls;
+            combine_block_cat(ctx, ccat, n, b, Y);
+          } else {
+            float* vh = ctx->arena.get<float>("ss:vh", n * 2 * bcap);
+            float* vl = ctx->arena.get<float>("ss:vl", n * 2 * bcap);
+            float* cc = ctx->arena.get<float>("ss:cc", 2 * n * 2 * bcap);
+            split_block_tf32(ctx, V, n, b, vh, vl);
+            const float* as[3] = {ghi, ghi, glo};
+            const float* bs[3] = {vh, vl, vh};
+            for (int g = 0; g < 3; ++g) {
+              check_cublas(cublasGemmEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(2 * n), int(2 * b), int(n), &one,
+                                        as[g], CUDA_R_32F, int(2 * n), bs[g], CUDA_R_32F, int(n),
+                                        g == 0 ? &zero : &one, cc, CUDA_R_32F, int(2 * n),
+                                        CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT),
+                           "GemmEx(3xTF32)");
+              ++ctx->lib_calls;
+            }
+            combine_block(ctx, cc, n, b, Y);
           }
-          combine_block(ctx, cc, n, b, Y);
           laps.lap("gemm32");
         } else if (i + 2 < q_plan) {
           // Early iterations only steer the span: FP32 CGEMM on the fp32 Gram
