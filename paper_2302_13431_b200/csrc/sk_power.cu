@@ -109,6 +109,7 @@ struct TmaTiles {
   int use = 0;  // 0: cp.async fallback (plane stride not a multiple of 16 B)
   int hb = 0, nb = 0;
   int swz = 0;  // swizzle mask applied by the readers (0: dense tile)
+  int lo_smem = 1;  // 1: lo planes staged by TMA into their own tile; 0: read from global in the epilogue
 };
 
 // float2 index of tile element idx under the TMA swizzle (buffer 1 KB aligned).
@@ -200,8 +201,8 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
   // tile buffers start on a 1 KB boundary (the swizzle pattern follows address bits 4..9)
   float2* gbuf = reinterpret_cast<float2*>(smem_raw + ((smem_u32(smem_raw) + 128 + 1023) & ~1023u) -
                                            smem_u32(smem_raw));  // [2][tile_elems] hi planes
-  float2* lbuf = gbuf + 2 * tile_elems;                                  // [tile_elems] lo planes
-  float2* vs = lbuf + tile_elems;                                        // [2][VPB][kStride]
+  float2* lbuf = gbuf + 2 * tile_elems;                                  // [tile_elems] lo planes (lo_smem)
+  float2* vs = lbuf + (tt.lo_smem ? tile_elems : 0);                     // [2][VPB][kStride]
   double2* vds = reinterpret_cast<double2*>(vs + 2 * VPB * L::kStride);  // [VPB][QP] final v in FP64
   double* redd = reinterpret_cast<double*>(vds + VPB * QP);              // [VPB][kWPV]
   float* red = reinterpret_cast<float*>(redd + VPB * WPV);               // [VPB][kWPV]
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       for (int c = 0; c < QP; ++c) m[r][c] = herm_at(gs, local + r * TPV, c, Q, VPB, vox, tt.swz);
     // Stream the lo residual planes of this tile while the iterations run
     // (its own buffer: the final Rayleigh quotient reads hi and lo packed).
-    if (a.planes_lo != nullptr) load_tile(tile, lbuf, a.planes_lo, &tm_lo, 2);
+    if (a.planes_lo != nullptr && tt.lo_smem) load_tile(tile, lbuf, a.planes_lo, &tm_lo, 2);
     // recon values for the epilogue, loaded while the iterations run
     float2 rcv[RPT];
 #pragma unroll
@@ -465,7 +466,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
 #pragma unroll
       for (int r = 0; r < RPT; ++r) vd[local + r * TPV] = make_double2(double(vp[r].x), double(vp[r].y));
     }
-    if (a.planes_lo != nullptr) {
+    if (a.planes_lo != nullptr && tt.lo_smem) {
       if (tt.use)
         wait_tile(2);
       else
@@ -480,7 +481,9 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
         const float2 hv = gs[swz_at(e * VPB + vox, tt.swz)];
         double mx = double(hv.x), my = double(hv.y);
         if (a.planes_lo != nullptr) {
-          const float2 lv = lbuf[swz_at(e * VPB + vox, tt.swz)];
+          const float2 lv = tt.lo_smem ? lbuf[swz_at(e * VPB + vox, tt.swz)]
+                            : live      ? __ldg(a.planes_lo + i64(e) * a.n + j)
+                                        : make_float2(0.f, 0.f);
           mx += double(lv.x);
           my += double(lv.y);
         }
@@ -577,6 +580,8 @@ bool encode_planes(CUtensorMap* m, const float2* base, i64 n, int h, int vpb, in
          CUDA_SUCCESS;
 }
 
+int env_int(const char* name, int dflt);
+
 template <class L>
 void launch(sk_ctx* ctx, const PowerArgs& a) {
   const int h = a.q * (a.q + 1) / 2;
@@ -607,7 +612,12 @@ void launch(sk_ctx* ctx, const PowerArgs& a) {
   const int alt = tt.swz ? std::max(al, 1024 / row_bytes) : al;
   const int tile_rows = (std::max(std::max(h, L::QP), tt.use ? tt.nb * tt.hb : 0) + alt - 1) / alt * alt;
   const size_t tile = size_t(tile_rows) * L::kVPB * sizeof(float2);
-  const size_t smem = 1024 + 128 + 3 * tile + 2 * size_t(L::kVPB) * L::kStride * sizeof(float2) +
+  // lo planes: their own TMA tile, or (SKB_K4_LO_SMEM=0, experiment) read from
+  // global in the epilogue — a third less shared memory per voxel, but the
+  // strided 8-byte reads cost more than they free (C2 two-row layout 1.64 ms).
+  static const int lo_env = env_int("SKB_K4_LO_SMEM", -1);
+  tt.lo_smem = lo_env >= 0 ? lo_env : 1;
+  const size_t smem = 1024 + 128 + (tt.lo_smem ? 3 : 2) * tile + 2 * size_t(L::kVPB) * L::kStride * sizeof(float2) +
                       size_t(L::kVPB) * L::QP * sizeof(double2) +
                       size_t(L::kVPB) * L::kWPV * (sizeof(double) + 3 * sizeof(float)) + size_t(h) * sizeof(int);
   set_smem_limit(reinterpret_cast<const void*>(power_kernel<L>), smem);
