@@ -110,6 +110,8 @@ struct TmaTiles {
   int hb = 0, nb = 0;
   int swz = 0;  // swizzle mask applied by the readers (0: dense tile)
   int lo_smem = 1;  // 1: lo planes staged by TMA into their own tile; 0: read from global in the epilogue
+  int single_hi = 0;  // 1: one hi tile, refilled with the next tile right after the unpack (the
+                      // epilogue takes hi from the registers): two tile buffers per block instead of three
 };
 
 // float2 index of tile element idx under the TMA swizzle (buffer 1 KB aligned).
@@ -201,8 +203,8 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
   // tile buffers start on a 1 KB boundary (the swizzle pattern follows address bits 4..9)
   float2* gbuf = reinterpret_cast<float2*>(smem_raw + ((smem_u32(smem_raw) + 128 + 1023) & ~1023u) -
                                            smem_u32(smem_raw));  // [2][tile_elems] hi planes
-  float2* lbuf = gbuf + 2 * tile_elems;                                  // [tile_elems] lo planes (lo_smem)
-  float2* vs = lbuf + (tt.lo_smem ? tile_elems : 0);                     // [2][VPB][kStride]
+  float2* lbuf = gbuf + (tt.single_hi ? 1 : 2) * tile_elems;            // [tile_elems] lo planes (lo_smem)
+  float2* vs = lbuf + ((tt.lo_smem || tt.single_hi) ? tile_elems : 0);   // [2][VPB][kStride]
   double2* vds = reinterpret_cast<double2*>(vs + 2 * VPB * L::kStride);  // [VPB][QP] final v in FP64
   double* redd = reinterpret_cast<double*>(vds + VPB * QP);              // [VPB][kWPV]
   float* red = reinterpret_cast<float*>(redd + VPB * WPV);               // [VPB][kWPV]
@@ -254,17 +256,26 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
   if (tile < tiles) load_tile(tile, gbuf, a.planes, &tm_hi, 0);
   for (; tile < tiles; tile += gridDim.x, buf ^= 1) {
     const i64 next = tile + gridDim.x;
-    if (next < tiles) load_tile(next, gbuf + (buf ^ 1) * tile_elems, a.planes, &tm_hi, buf ^ 1);
-    if (tt.use) {
-      wait_tile(buf);
-    } else {
-      if (next < tiles)
-        cp_async_wait<1>();
-      else
+    if (tt.single_hi) {
+      if (tt.use) {
+        wait_tile(0);
+      } else {
         cp_async_wait<0>();
-      __syncthreads();
+        __syncthreads();
+      }
+    } else {
+      if (next < tiles) load_tile(next, gbuf + (buf ^ 1) * tile_elems, a.planes, &tm_hi, buf ^ 1);
+      if (tt.use) {
+        wait_tile(buf);
+      } else {
+        if (next < tiles)
+          cp_async_wait<1>();
+        else
+          cp_async_wait<0>();
+        __syncthreads();
+      }
     }
-    float2* gs = gbuf + buf * tile_elems;
+    float2* gs = gbuf + (tt.single_hi ? 0 : buf * tile_elems);
     const i64 j0 = tile * VPB;
     const i64 j = j0 + vox;
     const bool live = j < a.n;
@@ -277,7 +288,14 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       for (int c = 0; c < QP; ++c) m[r][c] = herm_at(gs, local + r * TPV, c, Q, VPB, vox, tt.swz);
     // Stream the lo residual planes of this tile while the iterations run
     // (its own buffer: the final Rayleigh quotient reads hi and lo packed).
-    if (a.planes_lo != nullptr && tt.lo_smem) load_tile(tile, lbuf, a.planes_lo, &tm_lo, 2);
+    // single_hi: the hi tile is free once unpacked and receives the next tile.
+    if (tt.single_hi) {
+      __syncthreads();  // every unpack read of gs precedes its refill
+      if (a.planes_lo != nullptr) load_tile(tile, lbuf, a.planes_lo, &tm_lo, 2);
+      if (next < tiles) load_tile(next, gbuf, a.planes, &tm_hi, 0);
+    } else if (a.planes_lo != nullptr && tt.lo_smem) {
+      load_tile(tile, lbuf, a.planes_lo, &tm_lo, 2);
+    }
     // recon values for the epilogue, loaded while the iterations run
     float2 rcv[RPT];
 #pragma unroll
@@ -466,15 +484,48 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
 #pragma unroll
       for (int r = 0; r < RPT; ++r) vd[local + r * TPV] = make_double2(double(vp[r].x), double(vp[r].y));
     }
-    if (a.planes_lo != nullptr && tt.lo_smem) {
+    if (a.planes_lo != nullptr && (tt.lo_smem || tt.single_hi)) {
       if (tt.use)
         wait_tile(2);
+      else if (tt.single_hi && next < tiles)
+        cp_async_wait<1>();  // lo(t) was committed before hi(t+1)
       else
         cp_async_wait<0>();
     }
     __syncthreads();
     double xd = 0.0;
-    {
+    if (tt.single_hi) {
+      // hi part from the registers: sum over this thread's rows p of
+      // Re(conj(v_p) (M_hi v)_p); the lo part over the packed triangle.
+      const double2* vd = vds + vox * QP;
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int p = local + r * TPV;
+        double yx = 0.0, yy = 0.0;
+#pragma unroll
+        for (int c = 0; c < QP; ++c) {
+          const double2 vc = vd[c];
+          const double mx = double(m[r][c].x), my = double(m[r][c].y);
+          yx = fma(mx, vc.x, fma(-my, vc.y, yx));
+          yy = fma(mx, vc.y, fma(my, vc.x, yy));
+        }
+        if (p < Q) xd = fma(vd[p].x, yx, fma(vd[p].y, yy, xd));
+      }
+      if (a.planes_lo != nullptr) {
+        for (int e = local; e < h; e += TPV) {
+          const int pc = pct[e], pp = pc >> 8, cc = pc & 0xff;
+          const float2 lv = lbuf[swz_at(e * VPB + vox, tt.swz)];
+          const double mx = double(lv.x), my = double(lv.y);
+          const double2 vpp = vd[pp], vc = vd[cc];
+          if (pp == cc) {
+            xd = fma(mx, vpp.x * vpp.x + vpp.y * vpp.y, xd);
+          } else {
+            const double tx = mx * vc.x - my * vc.y, ty = mx * vc.y + my * vc.x;
+            xd = fma(2.0, vpp.x * tx + vpp.y * ty, xd);
+          }
+        }
+      }
+    } else {
       const double2* vd = vds + vox * QP;
       for (int e = local; e < h; e += TPV) {
         const int pc = pct[e], pp = pc >> 8, cc = pc & 0xff;
@@ -531,9 +582,10 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       }
     }
 
-    // Stage maps for channel-major coalesced stores: reuse the plane tile.
+    // Stage maps for channel-major coalesced stores: reuse a plane tile (the
+    // lo tile under single_hi: the hi tile is already receiving the next tile).
     __syncthreads();
-    float2* ms = gs;  // [QP][VPB]
+    float2* ms = tt.single_hi ? lbuf : gs;  // [QP][VPB]
 #pragma unroll
     for (int r = 0; r < RPT; ++r) ms[(local + r * TPV) * VPB + vox] = vp[r];
     __syncthreads();
@@ -617,7 +669,11 @@ void launch(sk_ctx* ctx, const PowerArgs& a) {
   // strided 8-byte reads cost more than they free (C2 two-row layout 1.64 ms).
   static const int lo_env = env_int("SKB_K4_LO_SMEM", -1);
   tt.lo_smem = lo_env >= 0 ? lo_env : 1;
-  const size_t smem = 1024 + 128 + (tt.lo_smem ? 3 : 2) * tile + 2 * size_t(L::kVPB) * L::kStride * sizeof(float2) +
+  static const int single_env = env_int("SKB_K4_SINGLE_HI", -1);
+  tt.single_hi = single_env >= 0 ? single_env : 0;
+  if (tt.single_hi) tt.lo_smem = 1;
+  const size_t smem = 1024 + 128 + (tt.single_hi ? 2 : tt.lo_smem ? 3 : 2) * tile +
+                      2 * size_t(L::kVPB) * L::kStride * sizeof(float2) +
                       size_t(L::kVPB) * L::QP * sizeof(double2) +
                       size_t(L::kVPB) * L::kWPV * (sizeof(double) + 3 * sizeof(float)) + size_t(h) * sizeof(int);
   set_smem_limit(reinterpret_cast<const void*>(power_kernel<L>), smem);
