@@ -250,6 +250,10 @@ void lam64_to_f32_mask(sk_ctx* ctx, const double2* lam_c, i64 n, float* lam, uin
 // double2 elements.  Returns false (nothing launched) unless n, N are powers
 // of two with 2 <= n <= N <= 1024.
 bool interp_axis_fft(sk_ctx* ctx, const void* in, void* out, i64 batch, int n, int N, i64 inner, bool fp64);
+// Last (innermost, factor-2) interpolation pass of a [Q][P][n] stack fused with
+// the per-voxel sum-of-squares renormalisation; false (nothing launched) when
+// the shape is outside the kernel (Q a power of two <= 32, Q*n <= 4096).
+bool interp_last_axis_sos(sk_ctx* ctx, const float2* in, float2* out, int q, i64 positions, int n, int N);
 void copy_strided(sk_ctx* ctx, const float2* src, i64 src_rs, i64 src_cs, float2* dst, i64 dst_rs, i64 dst_cs, i64 rows,
                   i64 cols);
 void normalize_standalone(sk_ctx* ctx, float2* maps, i64 n, int q, const float2* recon, unsigned long long* zeroed);

@@ -286,6 +286,95 @@ __global__ void __launch_bounds__(256) interp2_fft_kernel(const typename Cplx<R>
   }
 }
 
+// Last interpolation pass fused with the sum-of-squares renormalisation of
+// finalize (maps.cpp:240-250): the innermost (contiguous) axis, factor 2, one
+// CTA per outer position with all Q channel lines (T = Q), so each output
+// voxel's channels meet in shared memory: sos = sum_c |out_c|^2, then
+// out_c / sqrt(sos) where sos > 0.  Saves the separate renormalisation pass
+// (which reads the full-resolution maps twice and writes them once).
+// in [Q][P][n] -> out [Q][P][2n].
+template <int LOGN_, int LOGQ_>
+__global__ void __launch_bounds__(256) interp2_sos_kernel(const float2* __restrict__ in, float2* __restrict__ out,
+                                                          unsigned positions, int logn_arg, int logq_arg) {
+  using C = float2;
+  using R = float;
+  const int logn = LOGN_ >= 0 ? LOGN_ : logn_arg;
+  const int logT = LOGQ_ >= 0 ? LOGQ_ : logq_arg;
+  const int logN = logn + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = 1 << logn, N = 2 << logn, T = 1 << logT;
+  C* tw = reinterpret_cast<C*>(smem_raw);
+  const int ld = n + n / 16 + 1;
+  C* buf = tw + n;
+  C* ybuf = buf + T * ld;
+  float* inv = reinterpret_cast<float*>(ybuf + T * ld);  // [N]
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    R sn, cs;
+    sincospif(-2.0f * float(k) / float(N), &sn, &cs);
+    tw[k].x = cs;
+    tw[k].y = sn;
+  }
+  const unsigned p = blockIdx.x;
+  const int cl = n / 2;
+  for (int e = threadIdx.x; e < (T << logn); e += blockDim.x) {
+    const int t = e >> logn, a = e & (n - 1);
+    const C v = in[((size_t(t) * positions + p) << logn) + ((a + cl) & (n - 1))];  // ifftshift
+    buf[t * ld + pz(bitrev(a, logn))] = v;
+    ybuf[t * ld + pz(a)] = v;
+  }
+  __syncthreads();
+  fft_lines(buf, logT, ld, logn, tw, 1, false);
+  constexpr int kMaxPer = 16;
+  C keep[kMaxPer];
+  const R inv_n = R(1) / R(n);
+#pragma unroll
+  for (int u = 0; u < kMaxPer; ++u) {
+    const int e = threadIdx.x + u * 256;
+    if (e < (T << logn)) {
+      const int t = e >> logn, k = e & (n - 1);
+      const int f = k < n - cl ? k : k - n;
+      C w = tw[f >= 0 ? f : -f];
+      if (f >= 0) w.y = -w.y;
+      const C y = buf[t * ld + pz(k)];
+      C v = cmul(y, w);
+      v.x *= inv_n;
+      v.y *= inv_n;
+      keep[u] = v;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kMaxPer; ++u) {
+    const int e = threadIdx.x + u * 256;
+    if (e < (T << logn)) {
+      const int t = e >> logn, k = e & (n - 1);
+      buf[t * ld + pz(bitrev(k, logn))] = keep[u];
+    }
+  }
+  __syncthreads();
+  fft_lines(buf, logT, ld, logn, tw, 1, true);
+  // per output sample m (pre-fftshift index): sum over the Q channels
+  for (int m = threadIdx.x; m < N; m += blockDim.x) {
+    const C* src = (m & 1) ? buf : ybuf;
+    float sos = 0.f;
+    for (int t = 0; t < T; ++t) {
+      const C v = src[t * ld + pz(m >> 1)];
+      sos += v.x * v.x + v.y * v.y;
+    }
+    inv[m] = sos > 0.f ? 1.0f / sqrtf(sos) : 1.0f;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < (T << logN); e += blockDim.x) {
+    const int t = e >> logN, jj = e & (N - 1);
+    const int m = (jj - n) & (N - 1);  // fftshift
+    C v = (m & 1) ? buf[t * ld + pz(m >> 1)] : ybuf[t * ld + pz(m >> 1)];
+    const float s = inv[m];
+    v.x *= s;
+    v.y *= s;
+    out[((size_t(t) * positions + p) << logN) + jj] = v;
+  }
+}
+
 // Centred transform along one axis (fft.cpp:71-112 kspace_to_image /
 // image_to_kspace): out = fftshift(DFT_sign(ifftshift(x))) * scale, one CTA
 // per T lines, same shared-memory FFT as the interpolation.
@@ -429,6 +518,29 @@ bool centered_fft_axis(sk_ctx* ctx, const void* in, void* out, i64 batch, int N,
       __builtin_ctzll(static_cast<unsigned long long>(inner)), logT, logN, inverse, float(scale));
   ++ctx->launches;
   SKB_LAUNCH("centered_fft_kernel");
+  return true;
+}
+
+bool interp_last_axis_sos(sk_ctx* ctx, const float2* in, float2* out, int q, i64 positions, int n, int N) {
+  const bool pow2 = n >= 2 && !(n & (n - 1)) && q >= 1 && !(q & (q - 1));
+  if (!pow2 || N != 2 * n || q > 32 || i64(q) * n > 16 * 256 || positions < 1 || positions >= (i64(1) << 31))
+    return false;
+  const int logn = __builtin_ctz(unsigned(n)), logq = __builtin_ctz(unsigned(q));
+  const int ld = n + n / 16 + 1;
+  const size_t smem = size_t(n) * sizeof(float2) + 2 * size_t(q) * ld * sizeof(float2) + size_t(N) * sizeof(float);
+  if (smem > 200 * 1024) return false;
+  auto go = [&](auto kern) {
+    set_smem_limit(reinterpret_cast<const void*>(kern), smem);
+    kern<<<unsigned(positions), 256, smem, ctx->stream>>>(in, out, unsigned(positions), logn, logq);
+  };
+  if (logn == 6 && logq == 5)
+    go(interp2_sos_kernel<6, 5>);
+  else if (logn == 7 && logq == 5)
+    go(interp2_sos_kernel<7, 5>);
+  else
+    go(interp2_sos_kernel<-1, -1>);
+  ++ctx->launches;
+  SKB_LAUNCH("interp2_sos_kernel");
   return true;
 }
 

@@ -110,7 +110,7 @@ struct TmaTiles {
   int hb = 0, nb = 0;
   int swz = 0;  // swizzle mask applied by the readers (0: dense tile)
   int lo_smem = 1;  // 1: lo planes staged by TMA into their own tile; 0: read from global in the epilogue
-  int single_hi = 0;  // 1: one hi tile, refilled with the next tile right after the unpack (the
+  int single_hi = 0;  // (= L::kSingleHi) one hi tile, refilled with the next tile right after the unpack (the
                       // epilogue takes hi from the registers): two tile buffers per block instead of three
 };
 
@@ -120,8 +120,9 @@ __device__ __forceinline__ int swz_at(int idx, int mask) {
   return (b ^ (((b >> 7) & mask) << 4)) >> 3;
 }
 
-template <int QP_, int RPT_, int THREADS_, int MINB_, int ACC_ = 0, int PF_ = 4, int QF_ = 0>
+template <int QP_, int RPT_, int THREADS_, int MINB_, int ACC_ = 0, int PF_ = 4, int QF_ = 0, int SH_ = 0>
 struct Layout {
+  static constexpr bool kSingleHi = SH_ != 0;  // one hi tile (TmaTiles::single_hi), compile-time
   static constexpr int QP = QP_, RPT = RPT_, kThreads = THREADS_, kMinBlocks = MINB_;
   static constexpr int QF = QF_;  // > 0: the channel count is fixed at compile time (Q == QF)
   static constexpr int kPrefetch = PF_;  // LDS.128 of v kept in flight ahead of their use
@@ -203,8 +204,8 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
   // tile buffers start on a 1 KB boundary (the swizzle pattern follows address bits 4..9)
   float2* gbuf = reinterpret_cast<float2*>(smem_raw + ((smem_u32(smem_raw) + 128 + 1023) & ~1023u) -
                                            smem_u32(smem_raw));  // [2][tile_elems] hi planes
-  float2* lbuf = gbuf + (tt.single_hi ? 1 : 2) * tile_elems;            // [tile_elems] lo planes (lo_smem)
-  float2* vs = lbuf + ((tt.lo_smem || tt.single_hi) ? tile_elems : 0);   // [2][VPB][kStride]
+  float2* lbuf = gbuf + (L::kSingleHi ? 1 : 2) * tile_elems;            // [tile_elems] lo planes (lo_smem)
+  float2* vs = lbuf + ((tt.lo_smem || L::kSingleHi) ? tile_elems : 0);   // [2][VPB][kStride]
   double2* vds = reinterpret_cast<double2*>(vs + 2 * VPB * L::kStride);  // [VPB][QP] final v in FP64
   double* redd = reinterpret_cast<double*>(vds + VPB * QP);              // [VPB][kWPV]
   float* red = reinterpret_cast<float*>(redd + VPB * WPV);               // [VPB][kWPV]
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
   if (tile < tiles) load_tile(tile, gbuf, a.planes, &tm_hi, 0);
   for (; tile < tiles; tile += gridDim.x, buf ^= 1) {
     const i64 next = tile + gridDim.x;
-    if (tt.single_hi) {
+    if constexpr (L::kSingleHi) {
       if (tt.use) {
         wait_tile(0);
       } else {
@@ -275,7 +276,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
         __syncthreads();
       }
     }
-    float2* gs = gbuf + (tt.single_hi ? 0 : buf * tile_elems);
+    float2* gs = gbuf + (L::kSingleHi ? 0 : buf * tile_elems);
     const i64 j0 = tile * VPB;
     const i64 j = j0 + vox;
     const bool live = j < a.n;
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     // Stream the lo residual planes of this tile while the iterations run
     // (its own buffer: the final Rayleigh quotient reads hi and lo packed).
     // single_hi: the hi tile is free once unpacked and receives the next tile.
-    if (tt.single_hi) {
+    if constexpr (L::kSingleHi) {
       __syncthreads();  // every unpack read of gs precedes its refill
       if (a.planes_lo != nullptr) load_tile(tile, lbuf, a.planes_lo, &tm_lo, 2);
       if (next < tiles) load_tile(next, gbuf, a.planes, &tm_hi, 0);
@@ -484,17 +485,17 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
 #pragma unroll
       for (int r = 0; r < RPT; ++r) vd[local + r * TPV] = make_double2(double(vp[r].x), double(vp[r].y));
     }
-    if (a.planes_lo != nullptr && (tt.lo_smem || tt.single_hi)) {
+    if (a.planes_lo != nullptr && (tt.lo_smem || L::kSingleHi)) {
       if (tt.use)
         wait_tile(2);
-      else if (tt.single_hi && next < tiles)
+      else if (L::kSingleHi && next < tiles)
         cp_async_wait<1>();  // lo(t) was committed before hi(t+1)
       else
         cp_async_wait<0>();
     }
     __syncthreads();
     double xd = 0.0;
-    if (tt.single_hi) {
+    if constexpr (L::kSingleHi) {
       // hi part from the registers: sum over this thread's rows p of
       // Re(conj(v_p) (M_hi v)_p); the lo part over the packed triangle.
       const double2* vd = vds + vox * QP;
@@ -585,7 +586,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     // Stage maps for channel-major coalesced stores: reuse a plane tile (the
     // lo tile under single_hi: the hi tile is already receiving the next tile).
     __syncthreads();
-    float2* ms = tt.single_hi ? lbuf : gs;  // [QP][VPB]
+    float2* ms = L::kSingleHi ? lbuf : gs;  // [QP][VPB]
 #pragma unroll
     for (int r = 0; r < RPT; ++r) ms[(local + r * TPV) * VPB + vox] = vp[r];
     __syncthreads();
@@ -669,8 +670,7 @@ void launch(sk_ctx* ctx, const PowerArgs& a) {
   // strided 8-byte reads cost more than they free (C2 two-row layout 1.64 ms).
   static const int lo_env = env_int("SKB_K4_LO_SMEM", -1);
   tt.lo_smem = lo_env >= 0 ? lo_env : 1;
-  static const int single_env = env_int("SKB_K4_SINGLE_HI", -1);
-  tt.single_hi = single_env >= 0 ? single_env : 0;
+  tt.single_hi = L::kSingleHi ? 1 : 0;
   if (tt.single_hi) tt.lo_smem = 1;
   const size_t smem = 1024 + 128 + (tt.single_hi ? 2 : tt.lo_smem ? 3 : 2) * tile +
                       2 * size_t(L::kVPB) * L::kStride * sizeof(float2) +
@@ -722,6 +722,7 @@ void power_iteration(sk_ctx* ctx, const PowerArgs& a) {
       case 11: launch<Layout<32, 1, 128, 3, 2, 4, 32>>(ctx, a); break;
       case 12: launch<Layout<32, 1, 256, 2, 1, 4, 32>>(ctx, a); break;
       case 13: launch<Layout<32, 1, 128, 3, 4, 6, 32>>(ctx, a); break;
+      case 17: launch<Layout<32, 1, 256, 2, 1, 4, 32, 1>>(ctx, a); break;  // single hi tile
       default:
         if (rpt32 != 1)
           launch<Layout<32, 2, 128, 3>>(ctx, a);
@@ -732,7 +733,14 @@ void power_iteration(sk_ctx* ctx, const PowerArgs& a) {
           launch<Layout<32, 1, 256, 2, 2, 4>>(ctx, a);
     }
   else if (a.q <= 64)
-    a.q == 64 ? launch<Layout<64, 1, 256, 1, 0, 4, 64>>(ctx, a) : launch<Layout<64, 1, 256, 1>>(ctx, a);
+    switch (a.q == 64 ? k4v : 0) {  // SKB_K4_VARIANT 14/15/16: accumulator pairs / prefetch for Q = 64
+      case 14: launch<Layout<64, 1, 256, 1, 1, 4, 64>>(ctx, a); break;
+      case 15: launch<Layout<64, 1, 256, 1, 2, 4, 64>>(ctx, a); break;
+      case 16: launch<Layout<64, 1, 256, 1, 2, 8, 64>>(ctx, a); break;
+      case 17: launch<Layout<64, 1, 256, 1, 0, 4, 64>>(ctx, a); break;  // four accumulator pairs
+      default:  // two accumulator pairs (C5 K4 22.5 -> 21.4 ms against four)
+        a.q == 64 ? launch<Layout<64, 1, 256, 1, 2, 4, 64>>(ctx, a) : launch<Layout<64, 1, 256, 1>>(ctx, a);
+    }
   else
     fail(9, "eig_power_field: more than 64 channels is outside the B200 path");
 }

@@ -1237,6 +1237,37 @@ bool interp_fft_ok(const Dims& low, const Dims& full) {
   return true;
 }
 
+// Maps interpolation followed by the SoS renormalisation of finalize
+// (maps.cpp:236-250).  When the innermost axis doubles and Q fits the fused
+// kernel, the outer axes run first and the innermost pass renormalises in
+// the same kernel; returns false when the caller still has to renormalise.
+bool run_interp_renorm(sk_ctx* ctx, const float2* low, float2* out, i64 q, const Dims& low_dims, const Dims& full) {
+  static const bool off = std::getenv("SKB_NO_FUSED_RENORM") != nullptr;
+  const int nd = int(low_dims.size());
+  const int n = int(low_dims[size_t(nd - 1)]), N = int(full[size_t(nd - 1)]);
+  if (off || !interp_fft_ok(low_dims, full) || N != 2 * n || q > 32 || (q & (q - 1)) || q * n > 4096) return false;
+  Dims cur = low_dims;
+  const float2* src = low;
+  int pass = 0;
+  for (int a = 0; a < nd - 1; ++a) {
+    if (low_dims[size_t(a)] == full[size_t(a)]) continue;
+    Dims next = cur;
+    next[size_t(a)] = full[size_t(a)];
+    float2* dst = ctx->arena.get<float2>(std::string("interp:fft") + (pass++ % 2 ? ":b" : ":a"), q * numel(next));
+    i64 b = q, inner = 1;
+    for (int k = 0; k < a; ++k) b *= cur[size_t(k)];
+    for (int k = a + 1; k < nd; ++k) inner *= cur[size_t(k)];
+    if (!interp_axis_fft(ctx, src, dst, b, int(low_dims[size_t(a)]), int(full[size_t(a)]), inner, false))
+      fail(SK_ERR_UNSUPPORTED, "interpolate_maps: FFT path refused a planned axis");
+    cur[size_t(a)] = full[size_t(a)];
+    src = dst;
+  }
+  const i64 positions = numel(cur) / cur[size_t(nd - 1)];
+  if (!interp_last_axis_sos(ctx, src, out, int(q), positions, n, N))
+    fail(SK_ERR_UNSUPPORTED, "interpolate_maps: fused last pass refused its shape");
+  return true;
+}
+
 void run_interp(sk_ctx* ctx, const float2* low, float2* out, i64 batch, const Dims& low_dims, const Dims& full) {
   const int nd = int(low_dims.size());
   if (interp_fft_ok(low_dims, full)) {
@@ -1448,9 +1479,10 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   // post (part 2): interpolation + renormalisation + mask (maps.cpp:236-258)
   if (interp) {
     float2* maps_full = out.maps ? out.maps : ctx->arena.get<float2>("post:maps_full", q * nfull);
-    run_interp(ctx, maps_grid, maps_full, q, grid, full);
+    const bool renormed = run_interp_renorm(ctx, maps_grid, maps_full, q, grid, full);
+    if (!renormed) run_interp(ctx, maps_grid, maps_full, q, grid, full);
     run_interp_lambda(ctx, lam_grid, grid, full, out.lambda, out.mask, float(cfg->mask_threshold));
-    renormalize_and_mask(ctx, maps_full, nfull, int(q), nullptr, nullptr, nullptr, 0.f);
+    if (!renormed) renormalize_and_mask(ctx, maps_full, nfull, int(q), nullptr, nullptr, nullptr, 0.f);
   }
   SKB_CUDA(cudaEventRecord(ev[6], ctx->stream));
   unsigned long long h_zeroed = 0;

@@ -721,3 +721,24 @@ def test_estimate_maps_naive_field(K, O):
     import dataclasses
     with pytest.raises(K.LengthError):
         K.estimate_maps(K.Calib(calib, cal.center_offset), (32, 28), dataclasses.replace(ck, field_byte_cap=4096))
+
+
+# ------------------------------- fused last interpolation pass + SoS renorm (K5)
+def test_estimate_maps_c3_slice_fused_renorm(K, O):
+    """C3 slice geometry (128^2 grid -> 256^2, Q = 32): the innermost interpolation pass runs fused with the
+    sum-of-squares renormalisation of finalize (maps.cpp:236-250)."""
+    from paper_2302_13431_b200 import phantom
+    case = phantom.generate("C3", slices=1)
+    ck, co = _cfgs(K, O, case.spec)
+    res, _ = _pipeline_case(K, O, case.calib[0], case.center_offset, case.spec.full_dims, ck, co, name="C3-slice0")
+    assert res.grid_dims == (128, 128)
+
+
+def test_estimate_maps_3d_pow2_fused_renorm(K, O):
+    sc3 = O.simulate(4, (32, 32, 16), 1, 9, noise_sigma=0.01, noise_seed=2)
+    cal3 = O.extract_calibration(sc3["kspace"], (12, 12, 8))
+    ck3 = K.PipelineConfig(kernel=K.ELLIPSOID, tau=2, power_iters=15, grid_dims=(16, 16, 8))
+    co3 = O.PipelineConfig.pisco()
+    co3.tau, co3.power_iters = 2, 15
+    _pipeline_case(K, O, cal3.data.astype(np.complex64), cal3.center_offset, (32, 32, 16), ck3, co3,
+                   grid=(16, 16, 8), name="3d-pow2-fused")
