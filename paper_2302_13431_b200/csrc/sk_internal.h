@@ -196,6 +196,10 @@ struct PowerArgs {
   uint8_t* mask;         // nullable
   float mask_threshold;
   unsigned long long* zeroed;  // nullable
+  // > 0: a voxel whose FP32 Rayleigh quotient on hi gives mv * lam_scale >= rq32_min
+  // keeps it and skips the FP64 (hi + lo) evaluation (pipeline: ||G/|Lambda| || <= 1,
+  // so FP32 rounding is ~1e-7 absolute; the FP64 pass is for small lambda)
+  float rq32_min;
 };
 void power_iteration(sk_ctx* ctx, const PowerArgs& a);
 

@@ -476,6 +476,24 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       fb = (a.iters & 1) ^ 1;  // last read by iteration iters-1, before the barrier above
     }
     (void)fb;
+    // FP32 Rayleigh quotient on hi first (one more matvec from registers): a
+    // voxel whose value is large relative to ||M|| (rq32_min, pipeline only)
+    // keeps it and skips the FP64 evaluation below.
+    bool need64 = true;
+    float mv32 = 0.f;
+    if (a.rq32_min > 0.f) {
+      voxel_bar<L>(vox);  // every read of the v buffers precedes the overwrite
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) vb(0)[local + r * TPV] = vp[r];
+      voxel_sync<L>();
+      float2 y[RPT];
+      matvec(vb(0), y);
+      float x = 0.f;
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) x = fmaf(vp[r].x, y[r].x, fmaf(vp[r].y, y[r].y, x));  // Re(conj(v) y)
+      mv32 = voxel_sum<L>(x, red, vox);
+      need64 = !(mv32 * a.lam_scale >= a.rq32_min);
+    }
     // Rayleigh quotient in FP64 on M = hi + lo over the packed triangle,
     //   Re(v^H M v) = sum_p M_pp |v_p|^2 + 2 Re sum_{p<c} conj(v_p) M_pc v_c,
     // split evenly over the voxel's threads (the FP32 iterate v enters only to
@@ -495,7 +513,9 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     }
     __syncthreads();
     double xd = 0.0;
-    if constexpr (L::kSingleHi) {
+    if (!need64) {
+      // FP32 value kept (voxel_sum below still runs: its shuffles span voxels)
+    } else if constexpr (L::kSingleHi) {
       // hi part from the registers: sum over this thread's rows p of
       // Re(conj(v_p) (M_hi v)_p); the lo part over the packed triangle.
       const double2* vd = vds + vox * QP;
@@ -551,7 +571,8 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     float xn = 0.f;
 #pragma unroll
     for (int r = 0; r < RPT; ++r) xn += vp[r].x * vp[r].x + vp[r].y * vp[r].y;
-    const double mv = voxel_sum<L>(xd, redd, vox);
+    const double mv64 = voxel_sum<L>(xd, redd, vox);
+    const double mv = need64 ? mv64 : double(mv32);
     const float vn2 = voxel_sum<L>(xn, red, vox);
 
     if (a.recon != nullptr) {

@@ -1343,6 +1343,18 @@ struct PipelineOut {
   i64 slab0 = 0, slab1 = -1;
 };
 
+// K4 epilogue: voxels with lambda >= this keep the FP32 Rayleigh quotient
+// (||G/|Lambda| || <= 1 for W a projection, so FP32 rounding is ~1e-7 absolute,
+// < 1e-5 relative above 0.25); SKB_RQ32_MIN=0 forces FP64 everywhere.
+// Used on full-resolution map grids only (see the pipeline).
+float rq32_min() {
+  static const float v = [] {
+    const char* e = std::getenv("SKB_RQ32_MIN");
+    return e ? float(std::atof(e)) : 0.25f;
+  }();
+  return v;
+}
+
 void validate_config(const sk_config* cfg) {
   if (!cfg) fail(SK_ERR_DIM, "null config");
   if (cfg->gram != 0 && cfg->gram != 1) fail(SK_ERR_DIM, "unknown gram method");
@@ -1456,6 +1468,7 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
     r.planes = planes; r.planes_lo = pl.lo; r.n = ngrid; r.q = int(q); r.iters = cfg->power_iters;
     r.alpha = 1.f; r.beta = -1.f / float(lam); r.lam_scale = 1.f / float(lam);
     r.maps = out.raw_maps; r.lambda = out.raw_lambda;
+    r.rq32_min = grid != full ? 0.f : rq32_min();
     power_iteration(ctx, r);
   }
   PowerArgs pa{};
@@ -1473,6 +1486,10 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   pa.mask = (!interp && !slab && out.mask) ? out.mask : nullptr;
   pa.mask_threshold = float(cfg->mask_threshold);
   pa.zeroed = zeroed;
+  // Not when an interpolation follows: the periodic-sinc interpolation spreads
+  // the FP32 path's ~1e-7 absolute error of large-lambda voxels into the small
+  // in-support values (measured: C3 in-mask lambda 3.4e-5 -> 5.6e-5 relative).
+  pa.rq32_min = grid != full ? 0.f : rq32_min();  // slabs are interpolated by the caller
   power_iteration(ctx, pa);
   }
   SKB_CUDA(cudaEventRecord(ev[5], ctx->stream));
