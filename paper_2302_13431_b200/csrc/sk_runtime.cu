@@ -124,6 +124,18 @@ bool is_device_ptr(const void* p) {
   return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+// Device alias of caller-pinned host memory (cudaHostAlloc / registered), or
+// nullptr (pageable host or device memory).
+void* pinned_alias(const void* p) {
+  if (!p) return nullptr;
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return attr.type == cudaMemoryTypeHost ? attr.devicePointer : nullptr;
+}
+
 // Device view of a caller input: the pointer itself, or an arena upload.
 template <typename T>
 const T* device_in(sk_ctx* ctx, const T* p, i64 count, const std::string& slot) {
@@ -1982,13 +1994,31 @@ int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, con
                              : (cfg->grid == 1 ? std::min(cd[size_t(a)] + cfg->grid_pad, fd[size_t(a)]) : fd[size_t(a)]);
     }
     const i64 ng = numel(grid);
+    // Pinned host maps on a full-resolution power-iteration grid: K4 is the
+    // only writer of the maps (coalesced channel-major stores of 32-64 B per
+    // tile row), so it can write them straight into the caller's pinned
+    // buffer over the host link while it computes, instead of a device
+    // staging buffer and a D2H copy after the pipeline.  Worth it only when
+    // K4 runs long enough per map byte (rate ~ FP32 rate / (iters * Q)):
+    // measured C5 (iters*Q = 5120) e2e 7.2 -> 7.8 M voxels/s, C2 (1600)
+    // 20.6 -> 16.6 (the short, write-rate-bound K4 slows down).
+    // SKB_ZERO_COPY=0 disables, =2 forces.
+    static const int zero_copy = [] {
+      const char* v = std::getenv("SKB_ZERO_COPY");
+      return v ? std::atoi(v) : 1;
+    }();
+    float2* maps_alias = nullptr;
+    if (zero_copy && maps && cfg && cfg->eig == 1 && grid == fd &&
+        (zero_copy == 2 || i64(cfg->power_iters) * q >= 4096))
+      maps_alias = static_cast<float2*>(pinned_alias(maps));
+    if (maps_alias) om = Out<float2>(ctx, nullptr, 0, "out:maps");
     Out<float2> og(ctx, reinterpret_cast<float2*>(gram_out), n * n, "dbg:gram");
     Out<float2> of(ctx, reinterpret_cast<float2*>(field_out), ng * q * q, "dbg:field");
     Out<float2> orm(ctx, reinterpret_cast<float2*>(raw_maps_out), q * ng, "dbg:raw");
     Out<float> orl(ctx, raw_lambda_out, ng, "dbg:rawl");
     std::vector<double> spec(size_t(std::max<i64>(n, 1)));
     PipelineOut po;
-    po.maps = om.dev;
+    po.maps = maps_alias ? maps_alias : om.dev;
     po.lambda = ol.dev;
     po.mask = ok.dev;
     po.gram = og.dev;

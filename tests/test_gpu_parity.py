@@ -742,3 +742,30 @@ def test_estimate_maps_3d_pow2_fused_renorm(K, O):
     co3.tau, co3.power_iters = 2, 15
     _pipeline_case(K, O, cal3.data.astype(np.complex64), cal3.center_offset, (32, 32, 16), ck3, co3,
                    grid=(16, 16, 8), name="3d-pow2-fused")
+
+
+def test_pinned_host_outputs_zero_copy(K):
+    """Pinned host output buffers on a full-resolution grid: K4 writes the maps straight into them (zero-copy);
+    the result equals the device-buffer call bit for bit, and pageable host buffers take the staged path."""
+    import torch
+    from paper_2302_13431_b200 import phantom
+    case = phantom.generate("C1", full_dims=(64, 64))
+    ck = K.PipelineConfig(tau=3, power_iters=512, grid=K.GRID_FULL, eig_solver=2)  # iters * Q >= 4096
+    ctx = K.default_context(0)
+    cal_h = torch.from_numpy(case.calib[0]).pin_memory()
+    dev = [torch.empty((8, 64, 64), dtype=torch.complex64, device="cuda"),
+           torch.empty((64, 64), dtype=torch.float32, device="cuda"),
+           torch.empty((64, 64), dtype=torch.uint8, device="cuda")]
+    pin = [torch.full((8, 64, 64), 7 + 7j, dtype=torch.complex64).pin_memory(),
+           torch.empty((64, 64), dtype=torch.float32).pin_memory(),
+           torch.empty((64, 64), dtype=torch.uint8).pin_memory()]
+    torch.cuda.synchronize()
+    for bufs in (dev, pin):
+        K.api.estimate_maps_device(ctx, cal_h.data_ptr(), (24, 24), case.center_offset, 8, (64, 64), ck,
+                                   bufs[0].data_ptr(), bufs[1].data_ptr(), bufs[2].data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(pin[0].numpy(), dev[0].cpu().numpy())
+    assert np.array_equal(pin[1].numpy(), dev[1].cpu().numpy())
+    assert np.array_equal(pin[2].numpy(), dev[2].cpu().numpy())
+    res = K.estimate_maps(K.Calib(case.calib[0], case.center_offset), (64, 64), ck)  # pageable numpy buffers
+    assert np.array_equal(res.maps, pin[0].numpy())
