@@ -136,6 +136,9 @@ struct sk_ctx {
   std::set<std::pair<int64_t, int64_t>> warm_rounds;
   // captured subspace rounds (CUDA graphs), see run_graphed
   std::map<skb::RoundKey, skb::RoundGraph> rounds;
+  // chunked K4 + overlapped device->host copies of the maps (pinned host outputs)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t chunk_ev[9] = {};
 };
 
 namespace skb {
@@ -200,6 +203,9 @@ struct PowerArgs {
   // keeps it and skips the FP64 (hi + lo) evaluation (pipeline: ||G/|Lambda| || <= 1,
   // so FP32 rounding is ~1e-7 absolute; the FP64 pass is for small lambda)
   float rq32_min;
+  // > 0: stride of planes / recon / maps (the pointers address voxel n0 of a
+  // larger grid of ld voxels; n voxels are processed).  0: ld = n.
+  i64 ld;
 };
 void power_iteration(sk_ctx* ctx, const PowerArgs& a);
 

@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
   const int vox = threadIdx.x / TPV;
   const int local = threadIdx.x % TPV;  // rows local + r * TPV
   const i64 tiles = (a.n + VPB - 1) / VPB;
+  const i64 ld = a.ld > 0 ? a.ld : a.n;  // plane / channel stride (a voxel range of a larger grid)
 
   // Tile loads.  TMA path: one thread issues nb boxes (hb plane rows x VPB
   // voxels, OOB zero-filled) completing on the buffer's mbarrier; every
@@ -243,7 +244,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     for (int e = threadIdx.x; e < h * VPB; e += blockDim.x) {
       const int pair = e / VPB, v = e % VPB;
       const bool ok = jj0 + v < a.n;
-      cp_async8(dst + e, src + (ok ? i64(pair) * a.n + jj0 + v : 0), ok ? 8 : 0);
+      cp_async8(dst + e, src + (ok ? i64(pair) * ld + jj0 + v : 0), ok ? 8 : 0);
     }
     cp_async_commit();
   };
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
       const int p = local + r * TPV;
-      rcv[r] = (a.recon != nullptr && p < Q && live) ? a.recon[i64(p) * a.n + j] : make_float2(0.f, 0.f);
+      rcv[r] = (a.recon != nullptr && p < Q && live) ? a.recon[i64(p) * ld + j] : make_float2(0.f, 0.f);
     }
 
     // v is double-buffered in shared memory (buffers 0 and 1) together with
@@ -554,7 +555,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
         double mx = double(hv.x), my = double(hv.y);
         if (a.planes_lo != nullptr) {
           const float2 lv = tt.lo_smem ? lbuf[swz_at(e * VPB + vox, tt.swz)]
-                            : live      ? __ldg(a.planes_lo + i64(e) * a.n + j)
+                            : live      ? __ldg(a.planes_lo + i64(e) * ld + j)
                                         : make_float2(0.f, 0.f);
           mx += double(lv.x);
           my += double(lv.y);
@@ -613,7 +614,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     __syncthreads();
     for (int e = threadIdx.x; e < Q * VPB; e += blockDim.x) {
       const int c = e / VPB, v = e % VPB;
-      if (j0 + v < a.n) a.maps[i64(c) * a.n + j0 + v] = ms[c * VPB + v];
+      if (j0 + v < a.n) a.maps[i64(c) * ld + j0 + v] = ms[c * VPB + v];
     }
     if (local == 0 && live) {
       const float lam = float(mv * double(a.lam_scale));
@@ -627,7 +628,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
 
 // 2-D tensor map over packed planes [h][n] (float2 as one 8-byte element):
 // box {VPB voxels, hb plane rows}.  Returns false when TMA cannot address it.
-bool encode_planes(CUtensorMap* m, const float2* base, i64 n, int h, int vpb, int hb, CUtensorMapSwizzle swz) {
+bool encode_planes(CUtensorMap* m, const float2* base, i64 n, i64 ld, int h, int vpb, int hb, CUtensorMapSwizzle swz) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -636,9 +637,9 @@ bool encode_planes(CUtensorMap* m, const float2* base, i64 n, int h, int vpb, in
       fn = nullptr;
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
-  if (!encode || base == nullptr || (n * 8) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  if (!encode || base == nullptr || (ld * 8) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
   const cuuint64_t dims[2] = {cuuint64_t(n), cuuint64_t(h)};
-  const cuuint64_t strides[1] = {cuuint64_t(n) * 8};
+  const cuuint64_t strides[1] = {cuuint64_t(ld) * 8};
   const cuuint32_t box[2] = {cuuint32_t(vpb), cuuint32_t(hb)};
   const cuuint32_t estr[2] = {1, 1};
   // L2 promotion of the 8*vpb-byte box rows (SKB_TMA_PROMO = 0 none, 64, 128, 256)
@@ -678,8 +679,9 @@ void launch(sk_ctx* ctx, const PowerArgs& a) {
     tt.hb = ((h + tt.nb - 1) / tt.nb + al - 1) / al * al;
     if (tt.hb <= 256) break;
   }
-  tt.use = !no_tma && encode_planes(&tm_hi, a.planes, a.n, h, L::kVPB, tt.hb, swz) &&
-           (a.planes_lo == nullptr || encode_planes(&tm_lo, a.planes_lo, a.n, h, L::kVPB, tt.hb, swz));
+  const i64 ld = a.ld > 0 ? a.ld : a.n;
+  tt.use = !no_tma && encode_planes(&tm_hi, a.planes, a.n, ld, h, L::kVPB, tt.hb, swz) &&
+           (a.planes_lo == nullptr || encode_planes(&tm_lo, a.planes_lo, a.n, ld, h, L::kVPB, tt.hb, swz));
   if (a.planes_lo == nullptr) tm_lo = tm_hi;
   tt.swz = !tt.use ? 0 : swz == CU_TENSOR_MAP_SWIZZLE_32B ? 1 : swz == CU_TENSOR_MAP_SWIZZLE_64B ? 3
                                                           : swz == CU_TENSOR_MAP_SWIZZLE_128B ? 7 : 0;

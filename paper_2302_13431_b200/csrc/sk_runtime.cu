@@ -1349,6 +1349,10 @@ struct PipelineOut {
   float2* raw_maps = nullptr; // debug: device [Q][N_grid]
   float* raw_lambda = nullptr;
   double* spectrum = nullptr; // host n
+  // pinned host destination of `maps` (full-resolution power grid): K4 runs in
+  // voxel chunks and each chunk's maps go to the host on a copy stream while
+  // the next chunk computes
+  float2* maps_host = nullptr;
   // z-slab mode (sk_estimate_raw_slab): axis-0 grid rows [slab0, slab1); the
   // normalised maps / raw lambda of those rows go to maps / lambda and the
   // interpolation stage is skipped.
@@ -1502,7 +1506,39 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   // the FP32 path's ~1e-7 absolute error of large-lambda voxels into the small
   // in-support values (measured: C3 in-mask lambda 3.4e-5 -> 5.6e-5 relative).
   pa.rq32_min = grid != full ? 0.f : rq32_min();  // slabs are interpolated by the caller
-  power_iteration(ctx, pa);
+  if (out.maps_host && !interp && !slab && maps_grid == out.maps) {
+    // K4 in voxel chunks (multiples of 8 voxels: 16-byte aligned TMA bases)
+    // with the maps copied to the host behind each chunk on a second stream.
+    constexpr int kChunks = 4;
+    if (!ctx->copy_stream) {
+      SKB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+      for (auto& e : ctx->chunk_ev) SKB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const i64 step = ((ngrid + kChunks - 1) / kChunks + 7) / 8 * 8;
+    int c = 0;
+    for (i64 jb = 0; jb < ngrid; jb += step, ++c) {
+      const i64 cnt = std::min(step, ngrid - jb);
+      PowerArgs ca = pa;
+      ca.planes = pa.planes + jb;
+      ca.planes_lo = pa.planes_lo ? pa.planes_lo + jb : nullptr;
+      ca.recon = pa.recon ? pa.recon + jb : nullptr;
+      ca.maps = pa.maps + jb;
+      ca.lambda = pa.lambda ? pa.lambda + jb : nullptr;
+      ca.mask = pa.mask ? pa.mask + jb : nullptr;
+      ca.n = cnt;
+      ca.ld = ngrid;
+      power_iteration(ctx, ca);
+      SKB_CUDA(cudaEventRecord(ctx->chunk_ev[c], ctx->stream));
+      SKB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->chunk_ev[c], 0));
+      SKB_CUDA(cudaMemcpy2DAsync(out.maps_host + jb, size_t(ngrid) * sizeof(float2), maps_grid + jb,
+                                 size_t(ngrid) * sizeof(float2), size_t(cnt) * sizeof(float2), size_t(q),
+                                 cudaMemcpyDeviceToHost, ctx->copy_stream));
+    }
+    SKB_CUDA(cudaEventRecord(ctx->chunk_ev[8], ctx->copy_stream));
+    SKB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[8], 0));
+  } else {
+    power_iteration(ctx, pa);
+  }
   }
   SKB_CUDA(cudaEventRecord(ev[5], ctx->stream));
   // post (part 2): interpolation + renormalisation + mask (maps.cpp:236-258)
@@ -1607,6 +1643,9 @@ int sk_destroy(sk_ctx* ctx) {
     ctx->rounds.clear();
     ctx->arena.release_all();
     for (auto& e : ctx->ev) cudaEventDestroy(e);
+    for (auto& e : ctx->chunk_ev)
+      if (e) cudaEventDestroy(e);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     cusolverDnDestroyParams(ctx->cusolver_params);
     cusolverDnDestroy(ctx->cusolver);
     cublasDestroy(ctx->cublas);
@@ -2012,6 +2051,11 @@ int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, con
         (zero_copy == 2 || i64(cfg->power_iters) * q >= 4096))
       maps_alias = static_cast<float2*>(pinned_alias(maps));
     if (maps_alias) om = Out<float2>(ctx, nullptr, 0, "out:maps");
+    // otherwise pinned host maps on a full-resolution power grid are copied
+    // out chunk by chunk behind K4 (PipelineOut::maps_host)
+    float2* maps_host = nullptr;
+    if (!maps_alias && zero_copy && maps && om.host && cfg && cfg->eig == 1 && grid == fd && pinned_alias(maps))
+      maps_host = reinterpret_cast<float2*>(maps);
     Out<float2> og(ctx, reinterpret_cast<float2*>(gram_out), n * n, "dbg:gram");
     Out<float2> of(ctx, reinterpret_cast<float2*>(field_out), ng * q * q, "dbg:field");
     Out<float2> orm(ctx, reinterpret_cast<float2*>(raw_maps_out), q * ng, "dbg:raw");
@@ -2019,6 +2063,7 @@ int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, con
     std::vector<double> spec(size_t(std::max<i64>(n, 1)));
     PipelineOut po;
     po.maps = maps_alias ? maps_alias : om.dev;
+    po.maps_host = maps_host;
     po.lambda = ol.dev;
     po.mask = ok.dev;
     po.gram = og.dev;
@@ -2027,7 +2072,7 @@ int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, con
     po.raw_lambda = orl.dev;
     po.spectrum = spectrum ? spec.data() : nullptr;
     pipeline(ctx, cd, co, q, d_cal, fd, cfg, po, prov);
-    om.finish(ctx);
+    if (!maps_host) om.finish(ctx);
     ol.finish(ctx);
     ok.finish(ctx);
     og.finish(ctx);

@@ -744,13 +744,15 @@ def test_estimate_maps_3d_pow2_fused_renorm(K, O):
                    grid=(16, 16, 8), name="3d-pow2-fused")
 
 
-def test_pinned_host_outputs_zero_copy(K):
-    """Pinned host output buffers on a full-resolution grid: K4 writes the maps straight into them (zero-copy);
-    the result equals the device-buffer call bit for bit, and pageable host buffers take the staged path."""
+@pytest.mark.parametrize("iters", [512, 30])
+def test_pinned_host_outputs_zero_copy(K, iters):
+    """Pinned host output buffers on a full-resolution grid: K4 writes the maps straight into them (zero-copy,
+    iters * Q >= 4096) or runs in voxel chunks with each chunk's maps copied out behind it; either way the
+    result equals the device-buffer call bit for bit, and pageable host buffers take the staged path."""
     import torch
     from paper_2302_13431_b200 import phantom
     case = phantom.generate("C1", full_dims=(64, 64))
-    ck = K.PipelineConfig(tau=3, power_iters=512, grid=K.GRID_FULL, eig_solver=2)  # iters * Q >= 4096
+    ck = K.PipelineConfig(tau=3, power_iters=iters, grid=K.GRID_FULL, eig_solver=2)
     ctx = K.default_context(0)
     cal_h = torch.from_numpy(case.calib[0]).pin_memory()
     dev = [torch.empty((8, 64, 64), dtype=torch.complex64, device="cuda"),
