@@ -1509,7 +1509,10 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   if (out.maps_host && !interp && !slab && maps_grid == out.maps) {
     // K4 in voxel chunks (multiples of 8 voxels: 16-byte aligned TMA bases)
     // with the maps copied to the host behind each chunk on a second stream.
-    constexpr int kChunks = 4;
+    static const int kChunks = [] {
+      const char* v = std::getenv("SKB_K4_CHUNKS");
+      return v ? std::max(1, std::min(8, std::atoi(v))) : 4;
+    }();
     if (!ctx->copy_stream) {
       SKB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
       for (auto& e : ctx->chunk_ev) SKB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
