@@ -911,6 +911,10 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   if (it_h != hint.end()) {
     const i64 k_prev = it_h->second.m;
     b = big ? std::max<i64>(128, ((k_prev + 48 + 31) / 32) * 32) : std::max<i64>(64, ((k_prev + 16 + 15) / 16) * 16);
+    // small Grams (library CholQR path, n < 1024) with a small signal space:
+    // a 32-column block (C1, k = 21: K2 0.65 -> 0.54 ms; 48 columns measured
+    // in between, C3's n = 1568 slower with 48 than with 64)
+    if (!big && n < 1024 && k_prev + 11 <= 32) b = 32;
     q_plan = it_h->second.plan;
   }
   const int first_plan = q_plan;
