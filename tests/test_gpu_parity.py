@@ -438,6 +438,10 @@ def test_determinism_and_device_buffers(K):
     from paper_2302_13431_b200 import phantom
     case = phantom.generate("C1")
     ck = K.PipelineConfig(tau=3, power_iters=30, grid_pad=40, eig_solver=2)  # same solver on both paths
+    # the subspace solver's step plan (and block) comes from the context's history for this Gram size
+    # (DESIGN.md §5): let it settle, then two calls with the same history are bit-identical
+    for _ in range(3):
+        K.estimate_maps(K.Calib(case.calib[0], case.center_offset), (256, 256), ck)
     a = K.estimate_maps(K.Calib(case.calib[0], case.center_offset), (256, 256), ck)
     b = K.estimate_maps(K.Calib(case.calib[0], case.center_offset), (256, 256), ck)
     assert np.array_equal(a.maps, b.maps) and np.array_equal(a.lambda_min_map, b.lambda_min_map)
