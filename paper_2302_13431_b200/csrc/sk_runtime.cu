@@ -557,7 +557,14 @@ struct SubspaceStatus {
 void zgemm(sk_ctx* ctx, cublasOperation_t ta, cublasOperation_t tb, i64 m, i64 n, i64 k, const double2* a, i64 lda,
            const double2* b, i64 ldb, double2* c, i64 ldc) {
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
-  check_cublas(cublasZgemm(ctx->cublas, ta, tb, int(m), int(n), int(k), &one,
+  // Gauss 3M form (three real DGEMMs instead of four) for the large n x b x n
+  // products; SKB_ZGEMM3M=0 keeps plain ZGEMM (experiment knob)
+  static const bool use3m = [] {
+    const char* v = std::getenv("SKB_ZGEMM3M");
+    return !v || std::atoi(v) != 0;
+  }();
+  auto gemm = (use3m && m * n * k >= (i64(1) << 26)) ? cublasZgemm3m : cublasZgemm;
+  check_cublas(gemm(ctx->cublas, ta, tb, int(m), int(n), int(k), &one,
                            reinterpret_cast<const cuDoubleComplex*>(a), int(lda),
                            reinterpret_cast<const cuDoubleComplex*>(b), int(ldb), &zero,
                            reinterpret_cast<cuDoubleComplex*>(c), int(ldc)),

@@ -31,6 +31,8 @@ def main():
     ap.add_argument("config")
     ap.add_argument("--slices", default=None, help="a:b slice block (C3)")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--solver", default="bench", choices=["bench", "full"],
+                    help="bench: the nullspace solver bench.py runs (auto -> subspace, no spectrum); full: cuSOLVER")
     args = ap.parse_args()
     sr = tuple(int(x) for x in args.slices.split(":")) if args.slices else None
     case = phantom.generate(args.config, slice_range=sr)
@@ -48,7 +50,8 @@ def main():
     first = sr[0] if sr else 0
     for i, cal in enumerate(case.calib):
         t0 = time.time()
-        res = K.estimate_maps(K.Calib(cal, case.center_offset), spec.full_dims, ck)
+        res = K.estimate_maps(K.Calib(cal, case.center_offset), spec.full_dims, ck,
+                              want_spectrum=args.solver == "full")
         t1 = time.time()
         ref = O.estimate_maps(O.Calib(cal.astype(np.complex128), case.center_offset), spec.full_dims, co,
                               grid_dims=grid)
@@ -57,7 +60,7 @@ def main():
         rec = {
             "config": args.config, "slice": first + i, "grid": list(spec.grid_dims), "full": list(spec.full_dims),
             "rank_gpu": int(res.nullspace_rank), "rank_oracle": int(ref.nullspace_rank),
-            "cut_margin": float(res.cut_margin), "subspace": res.extra,
+            "cut_margin": float(res.cut_margin), "solver": res.extra,
             "maps_nrmse_in_mask": PM.maps_nrmse(res.maps, ref.maps, ref.support_mask),
             "lambda": lam, "mask_agree": float(np.mean(res.support_mask == ref.support_mask)),
             "mask_fraction": float(np.mean(ref.support_mask)),
