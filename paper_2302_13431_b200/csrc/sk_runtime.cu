@@ -910,14 +910,16 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   // orthogonalised iterations before the (single) Rayleigh-Ritz check.
   auto& hint = ctx->subspace_hint;
   // Block size: small-matrix latency dominates up to n ~ 4k (b = 64 measured
-  // best for C2/C3/C4), the n^2 b GEMM beyond (b = 128 best for C5).
+  // best for C2/C3/C4), the n^2 b GEMM beyond (b = 96 best for C5).
   const bool big = n > 4096;
-  i64 b = big ? 128 : 64;
+  i64 b = big ? 96 : 64;
   int q_plan = 3;
   auto it_h = hint.find(n);
   if (it_h != hint.end()) {
     const i64 k_prev = it_h->second.m;
-    b = big ? std::max<i64>(128, ((k_prev + 48 + 31) / 32) * 32) : std::max<i64>(64, ((k_prev + 16 + 15) / 16) * 16);
+    // big Grams: k + 32 rounded to 32, at least 96 (C5, k = 59: K2 8.3 -> 7.0 ms
+    // against 128 columns once the FP64 products moved to ZGEMM 3M)
+    b = big ? std::max<i64>(96, ((k_prev + 32 + 31) / 32) * 32) : std::max<i64>(64, ((k_prev + 16 + 15) / 16) * 16);
     // small Grams (library CholQR path, n < 1024) with a small signal space:
     // a 32-column block (C1, k = 21: K2 0.65 -> 0.54 ms; 48 columns measured
     // in between, C3's n = 1568 slower with 48 than with 64)
