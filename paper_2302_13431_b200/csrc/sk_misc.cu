@@ -474,6 +474,29 @@ void combine_block_cat(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y) {
   SKB_LAUNCH("combine_block_cat");
 }
 
+// One pass over the c64 Gram: the FP64 copy for the ZGEMM steps and the
+// [Re; Im] TF32 hi/lo split for the 3xTF32 steps (split_gram_kernel layout).
+__global__ void promote_split_kernel(const float2* __restrict__ a, i64 n, double2* __restrict__ a64,
+                                     float* __restrict__ hi, float* __restrict__ lo) {
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n * n; e += i64(gridDim.x) * blockDim.x) {
+    const i64 r = e % n, c = e / n;
+    const float2 v = a[e];
+    a64[e] = make_double2(double(v.x), double(v.y));
+    float h, l;
+    tf32_split(v.x, h, l);
+    hi[r + c * 2 * n] = h;
+    lo[r + c * 2 * n] = l;
+    tf32_split(v.y, h, l);
+    hi[n + r + c * 2 * n] = h;
+    lo[n + r + c * 2 * n] = l;
+  }
+}
+void promote_split_gram(sk_ctx* ctx, const float2* a, i64 n, double2* a64, float* hi, float* lo) {
+  promote_split_kernel<<<SKB_GRID(n * n)>>>(a, n, a64, hi, lo);
+  ++ctx->launches;
+  SKB_LAUNCH("promote_split");
+}
+
 void split_gram_tf32(sk_ctx* ctx, const float2* a, i64 n, float* hi, float* lo) {
   split_gram_kernel<<<SKB_GRID(n * n)>>>(a, n, hi, lo);
   ++ctx->launches;

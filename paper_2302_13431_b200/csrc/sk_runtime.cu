@@ -885,7 +885,6 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   e.n = n;
   e.full = false;
   double2* A = ctx->arena.get<double2>("eig:A", n * n);
-  c64_to_c128(ctx, gram, A, n * n);
   // SKB_EARLY_GEMM: steering products as 3xTF32 tensor-core GEMMs (default),
   // plain FP32 CGEMM ("fp32"), or single TF32 / BF16 (measured to slow convergence).
   static const bool tf32x3 = [] {
@@ -903,7 +902,9 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   if (tf32x3) {
     ghi = ctx->arena.get<float>("ss:gcat", 4 * n * n);
     glo = ghi + 2 * n * n;
-    split_gram_tf32(ctx, gram, n, ghi, glo);
+    promote_split_gram(ctx, gram, n, A, ghi, glo);  // FP64 copy + split in one pass
+  } else {
+    c64_to_c128(ctx, gram, A, n * n);
   }
   laps.lap("promote");
   // Per-size hints from the previous call: block size and the number of
