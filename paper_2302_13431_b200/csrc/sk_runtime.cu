@@ -1197,6 +1197,22 @@ Planes run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims&
   const int lam = int(s.count);
   SupportTables& t = tables_for(ctx, s, q);
   const int h = q * (q + 1) / 2;
+  double2* lags = ctx->arena.get<double2>("field:lags64", i64(h) * t.nbox);
+  // Fold straight from U when a pair block is small (<= 64 KB: C1, C3 0.122 -> 0.109 ms;
+  // C2 measured slower at 105 KB); otherwise Ws = U U^H by ZHERK and the fold reads it.
+  static const bool from_u = [] {
+    const char* v = std::getenv("SKB_FOLD_FROM_U");
+    return !v || std::atoi(v) != 0;
+  }();
+  if (from_u && k > 0 && fold_from_u_smem(lam) <= 64 * 1024) {
+    fold_lags_from_u(ctx, e.usig, n, int(k), h, lam, t.nbox, t.pairs, t.lag_ptr, t.lag_st, lags);
+    Planes p;
+    const i64 nvox = slab1 >= 0 ? numel(grid) / grid[0] * (slab1 - slab0) : numel(grid);
+    p.hi = ctx->arena.get<float2>("field:planes", i64(h) * nvox);
+    p.lo = ctx->arena.get<float2>("field:planes_lo", i64(h) * nvox);
+    expand_lags(ctx, lags, p.hi, p.lo, h, s.tau, grid, slab0, slab1);
+    return p;
+  }
   double2* ws = ctx->arena.get<double2>("field:Ws", n * n);
   if (k > 0) {
     const double one = 1.0, zero = 0.0;
@@ -1208,7 +1224,6 @@ Planes run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims&
   } else {
     SKB_CUDA(cudaMemsetAsync(ws, 0, size_t(n * n) * sizeof(double2), ctx->stream));
   }
-  double2* lags = ctx->arena.get<double2>("field:lags64", i64(h) * t.nbox);
   fold_lags_f64(ctx, ws, n, h, lam, t.nbox, t.pairs, t.lag_ptr, t.lag_st, true, lags);
   Planes p;
   const i64 nvox = slab1 >= 0 ? numel(grid) / grid[0] * (slab1 - slab0) : numel(grid);
