@@ -39,16 +39,21 @@ __device__ __forceinline__ void cmac(float2& acc, float2 a, float2 b) {
 // reduces with a mask (two's complement handles negative lags).
 __device__ __forceinline__ float2 twiddle(const float2* tw, int k, int lag, int P) { return tw[(k * lag) & (P - 1)]; }
 
-__global__ void __launch_bounds__(256) gram_pairs_kernel(const float2* __restrict__ spectra, GramGeom g,
+// LB > 0: the lag-box extent 4 tau + 1 fixed at compile time (register
+// accumulators sized to it, the unstaged axis-0 contraction unrolled over four
+// k0 with all their loads in flight); LB = 0: runtime extent (<= kMaxLb).
+template <int LB>
+__global__ void __launch_bounds__(512) gram_pairs_kernel(const float2* __restrict__ spectra, GramGeom g,
                                                          const int2* __restrict__ pairs,
                                                          const int* __restrict__ d_off,
                                                          const float2* __restrict__ tw_all,
                                                          float2* __restrict__ gram) {
+  constexpr int kAcc = LB > 0 ? LB : kMaxLb;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int2 pq = pairs[blockIdx.x];
   const int p = pq.x, q = pq.y;
   const int P0 = g.pad[0], P1 = g.pad[1], P2 = g.pad[2];
-  const int lb = g.lb, t2 = 2 * g.tau;
+  const int lb = LB > 0 ? LB : g.lb, t2 = 2 * g.tau;
   const i64 npad = i64(P0) * P1 * P2;
   const int rest = P1 * P2;
   // twiddle tables (axis a at offset sum_{b<a} P_b)
@@ -88,17 +93,35 @@ __global__ void __launch_bounds__(256) gram_pairs_kernel(const float2* __restric
     }
   }
   for (int r = threadIdx.x; !g.stage_prod && r < rest; r += blockDim.x) {
-    float2 acc[kMaxLb];
+    float2 acc[kAcc];
 #pragma unroll
-    for (int l = 0; l < kMaxLb; ++l) acc[l] = make_float2(0.f, 0.f);
-    for (int k0 = 0; k0 < P0; ++k0) {
+    for (int l = 0; l < kAcc; ++l) acc[l] = make_float2(0.f, 0.f);
+    int k0 = 0;
+    if (LB > 0) {
+      constexpr int U = 4;  // P0 is a power of two >= 4 on this path (3-D pads)
+      for (; k0 + U <= P0; k0 += U) {
+        float2 sp[U], sq[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          sp[u] = Sp[i64(k0 + u) * rest + r];
+          sq[u] = Sq[i64(k0 + u) * rest + r];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float2 prod = cconj_mul(sp[u], sq[u]);
+#pragma unroll
+          for (int l = 0; l < kAcc; ++l) cmac(acc[l], prod, twiddle(tw0, k0 + u, l - t2, P0));
+        }
+      }
+    }
+    for (; k0 < P0; ++k0) {
       const float2 prod = cconj_mul(Sp[i64(k0) * rest + r], Sq[i64(k0) * rest + r]);
 #pragma unroll
-      for (int l = 0; l < kMaxLb; ++l)
+      for (int l = 0; l < kAcc; ++l)
         if (l < lb) cmac(acc[l], prod, twiddle(tw0, k0, l - t2, P0));
     }
 #pragma unroll
-    for (int l = 0; l < kMaxLb; ++l)
+    for (int l = 0; l < kAcc; ++l)
       if (l < lb) stageA_out[i64(l) * rest + r] = acc[l];
   }
   __syncthreads();
@@ -184,8 +207,22 @@ void gram_pairs_launch(sk_ctx* ctx, const float2* spectra, const GramGeom& g_in,
   }
   const size_t smem = gram_pairs_smem(g);
   if (smem > 227 * 1024) fail(9, "gram_fft: padded calibration too large for the on-chip lag contraction");
-  set_smem_limit(reinterpret_cast<const void*>(gram_pairs_kernel), smem);
-  gram_pairs_kernel<<<npairs, 256, smem, ctx->stream>>>(spectra, g, d_pairs, d_off, d_tw, gram);
+  // 512 threads when the axis-0 contraction is unstaged (3-D pads: one CTA per
+  // SM by shared memory, the column loop needs the warps), 256 otherwise.
+  const int threads = g.stage_prod ? 256 : 512;
+  static const bool generic = std::getenv("SKB_GRAM_GENERIC") != nullptr;
+  auto go = [&](auto kern) {
+    set_smem_limit(reinterpret_cast<const void*>(kern), smem);
+    kern<<<npairs, threads, smem, ctx->stream>>>(spectra, g, d_pairs, d_off, d_tw, gram);
+  };
+  switch (generic ? 0 : g.lb) {
+    case 9: go(gram_pairs_kernel<9>); break;
+    case 13: go(gram_pairs_kernel<13>); break;
+    case 17: go(gram_pairs_kernel<17>); break;
+    case 21: go(gram_pairs_kernel<21>); break;
+    case 25: go(gram_pairs_kernel<25>); break;
+    default: go(gram_pairs_kernel<0>); break;
+  }
   ++ctx->launches;
   SKB_LAUNCH("gram_pairs_kernel");
 }
