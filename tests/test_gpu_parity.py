@@ -51,6 +51,7 @@ def f32(a):
 @pytest.mark.parametrize("shape,tau,dims,q", [
     (1, 3, (24, 24), 8), (1, 5, (32, 32), 4), (0, 2, (14, 16), 3), (1, 2, (9, 10, 8), 2), (0, 1, (12,), 3),
     (1, 4, (24, 24), 6),
+    (1, 3, (20, 20, 20), 2),  # 32^3 pad: the unstaged axis-0 contraction (C4's path), lag box 13 templated
 ])
 def test_gram_fft_parity(K, O, shape, tau, dims, q):
     cal = rnd((q,) + dims, 1)
