@@ -209,7 +209,8 @@ void gram_pairs_launch(sk_ctx* ctx, const float2* spectra, const GramGeom& g_in,
   if (smem > 227 * 1024) fail(9, "gram_fft: padded calibration too large for the on-chip lag contraction");
   // 512 threads when the axis-0 contraction is unstaged (3-D pads: one CTA per
   // SM by shared memory, the column loop needs the warps), 256 otherwise.
-  const int threads = g.stage_prod ? 256 : 512;
+  static const int t2d = [] { const char* v = std::getenv("SKB_GRAM_THREADS_2D"); return v ? std::atoi(v) : 256; }();
+  const int threads = g.stage_prod ? t2d : 512;
   static const bool generic = std::getenv("SKB_GRAM_GENERIC") != nullptr;
   auto go = [&](auto kern) {
     set_smem_limit(reinterpret_cast<const void*>(kern), smem);
