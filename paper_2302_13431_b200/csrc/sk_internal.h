@@ -139,6 +139,12 @@ struct sk_ctx {
   // chunked K4 + overlapped device->host copies of the maps (pinned host outputs)
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t chunk_ev[9] = {};
+  // multislice lanes: host outputs copied on copy_stream behind the pipeline
+  // (double-buffered staging), drained by the batched driver
+  int defer_d2h = 0;
+  int d2h_slot = 0;
+  cudaEvent_t d2h_done[2] = {};
+  cudaEvent_t d2h_ready = nullptr;
 };
 
 namespace skb {

@@ -163,9 +163,9 @@ struct Out {
       dev = ctx->arena.get<T>(slot, n);
     }
   }
-  void finish(sk_ctx* ctx) {
-    if (host && user)
-      SKB_CUDA(cudaMemcpyAsync(user, dev, size_t(count) * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+  void finish(sk_ctx* ctx) { finish_on(ctx->stream); }
+  void finish_on(cudaStream_t st) {
+    if (host && user) SKB_CUDA(cudaMemcpyAsync(user, dev, size_t(count) * sizeof(T), cudaMemcpyDeviceToHost, st));
   }
 };
 
@@ -1677,6 +1677,9 @@ int sk_destroy(sk_ctx* ctx) {
     for (auto& e : ctx->ev) cudaEventDestroy(e);
     for (auto& e : ctx->chunk_ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->d2h_done)
+      if (e) cudaEventDestroy(e);
+    if (ctx->d2h_ready) cudaEventDestroy(ctx->d2h_ready);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     cusolverDnDestroyParams(ctx->cusolver_params);
     cusolverDnDestroy(ctx->cusolver);
@@ -2050,9 +2053,26 @@ int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, con
     if (q < 1) fail(SK_ERR_DIM, "stack needs at least one channel");
     const i64 nfull = numel(fd);
     const float2* d_cal = device_in(ctx, reinterpret_cast<const float2*>(calib), q * numel(cd), "in:calib");
-    Out<float2> om(ctx, reinterpret_cast<float2*>(maps), q * nfull, "out:maps");
-    Out<float> ol(ctx, lambda, nfull, "out:lambda");
-    Out<uint8_t> ok(ctx, mask, nfull, "out:mask");
+    // Batched lanes (defer_d2h): the host outputs' staging alternates between
+    // two slots and is copied out on the copy stream while the lane's next
+    // slice computes; a slot is reused only after its copy completed.
+    const bool defer = ctx->defer_d2h != 0;
+    const std::string sfx = defer ? ":" + std::to_string(ctx->d2h_slot) : "";
+    Out<float2> om(ctx, reinterpret_cast<float2*>(maps), q * nfull, "out:maps" + sfx);
+    Out<float> ol(ctx, lambda, nfull, "out:lambda" + sfx);
+    Out<uint8_t> ok(ctx, mask, nfull, "out:mask" + sfx);
+    if (defer) {
+      if (!ctx->copy_stream) {
+        SKB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (auto& e : ctx->chunk_ev) SKB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      if (!ctx->d2h_ready) {
+        SKB_CUDA(cudaEventCreateWithFlags(&ctx->d2h_ready, cudaEventDisableTiming));
+        for (auto& e : ctx->d2h_done) SKB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : ctx->d2h_done) SKB_CUDA(cudaEventRecord(e, ctx->copy_stream));
+      }
+      SKB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->d2h_done[ctx->d2h_slot], 0));  // slot's last copy drained
+    }
     // debug dumps need sizes: derive them the same way the pipeline does
     const Support s = make_support(cfg ? cfg->kernel : 0, cfg ? cfg->tau : 0, ndim);
     const i64 n = q * s.count;
@@ -2079,14 +2099,15 @@ int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, con
       return v ? std::atoi(v) : 1;
     }();
     float2* maps_alias = nullptr;
-    if (zero_copy && maps && cfg && cfg->eig == 1 && grid == fd &&
+    if (!defer && zero_copy && maps && cfg && cfg->eig == 1 && grid == fd &&
         (zero_copy == 2 || i64(cfg->power_iters) * q >= 4096))
       maps_alias = static_cast<float2*>(pinned_alias(maps));
     if (maps_alias) om = Out<float2>(ctx, nullptr, 0, "out:maps");
     // otherwise pinned host maps on a full-resolution power grid are copied
     // out chunk by chunk behind K4 (PipelineOut::maps_host)
     float2* maps_host = nullptr;
-    if (!maps_alias && zero_copy && maps && om.host && cfg && cfg->eig == 1 && grid == fd && pinned_alias(maps))
+    if (!defer && !maps_alias && zero_copy && maps && om.host && cfg && cfg->eig == 1 && grid == fd &&
+        pinned_alias(maps))
       maps_host = reinterpret_cast<float2*>(maps);
     Out<float2> og(ctx, reinterpret_cast<float2*>(gram_out), n * n, "dbg:gram");
     Out<float2> of(ctx, reinterpret_cast<float2*>(field_out), ng * q * q, "dbg:field");
@@ -2104,9 +2125,19 @@ int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, con
     po.raw_lambda = orl.dev;
     po.spectrum = spectrum ? spec.data() : nullptr;
     pipeline(ctx, cd, co, q, d_cal, fd, cfg, po, prov);
-    if (!maps_host) om.finish(ctx);
-    ol.finish(ctx);
-    ok.finish(ctx);
+    if (defer) {
+      SKB_CUDA(cudaEventRecord(ctx->d2h_ready, ctx->stream));
+      SKB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->d2h_ready, 0));
+      om.finish_on(ctx->copy_stream);
+      ol.finish_on(ctx->copy_stream);
+      ok.finish_on(ctx->copy_stream);
+      SKB_CUDA(cudaEventRecord(ctx->d2h_done[ctx->d2h_slot], ctx->copy_stream));
+      ctx->d2h_slot ^= 1;
+    } else {
+      if (!maps_host) om.finish(ctx);
+      ol.finish(ctx);
+      ok.finish(ctx);
+    }
     og.finish(ctx);
     of.finish(ctx);
     orm.finish(ctx);
@@ -2254,9 +2285,17 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
   if (rc0 != SK_OK) return rc0;
   std::vector<int> rcs(size_t(lanes), SK_OK);
   std::vector<std::string> errs(static_cast<size_t>(lanes));
+  // Pinned host outputs: each lane copies a slice's outputs on its copy stream
+  // while it computes the next slice (SKB_DEFER_D2H=0 keeps the copy inline).
+  static const bool defer_env = [] {
+    const char* v = std::getenv("SKB_DEFER_D2H");
+    return !v || std::atoi(v) != 0;
+  }();
+  const bool defer = defer_env && maps && pinned_alias(maps) != nullptr;
   auto work = [&](int lane) {
     sk_ctx* sub = lanes == 1 ? ctx : ctx->lanes[size_t(lane)];
     cudaSetDevice(ctx->device);
+    sub->defer_d2h = defer ? 1 : 0;
     for (i64 s = lane; s < slices; s += lanes) {
       const int rc = sk_estimate_maps(sub, ndim, calib_dims, center_offset, q, calib + s * ncal, full_dims, cfg,
                                       maps ? maps + s * q * nfull : nullptr, lambda ? lambda + s * nfull : nullptr,
@@ -2264,8 +2303,14 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
       if (rc != SK_OK) {
         rcs[size_t(lane)] = rc;
         errs[size_t(lane)] = sk_last_error();
-        return;
+        break;
       }
+    }
+    sub->defer_d2h = 0;
+    if (defer && sub->copy_stream && cudaStreamSynchronize(sub->copy_stream) != cudaSuccess &&
+        rcs[size_t(lane)] == SK_OK) {
+      rcs[size_t(lane)] = SK_ERR_CUDA;
+      errs[size_t(lane)] = "multislice: deferred device-to-host copy failed";
     }
   };
   if (lanes == 1) {

@@ -776,3 +776,41 @@ def test_pinned_host_outputs_zero_copy(K, iters):
     assert np.array_equal(pin[2].numpy(), dev[2].cpu().numpy())
     res = K.estimate_maps(K.Calib(case.calib[0], case.center_offset), (64, 64), ck)  # pageable numpy buffers
     assert np.array_equal(res.maps, pin[0].numpy())
+
+
+def test_batched_multislice_pinned_outputs(K):
+    """Pinned host outputs for the batched multislice call: each lane copies a slice's outputs on its copy stream
+    while it computes the next slice (double-buffered staging); results equal the device-buffer batched call."""
+    import torch
+    from paper_2302_13431_b200 import phantom
+    case = phantom.generate("C3", slices=14, full_dims=(64, 64), channels=8)
+    spec = case.spec
+    cfg = K.PipelineConfig(kernel=spec.kernel, tau=spec.tau, nullspace_threshold=spec.nullspace_threshold,
+                           power_iters=spec.power_iters, grid=K.GRID_REDUCED,
+                           grid_pad=spec.grid_dims[0] - spec.calib[0])
+    ctx = K.Context(0)
+    s, q, full = case.calib.shape[0], spec.channels, spec.full_dims
+    cal = torch.from_numpy(case.calib).cuda()
+    outs = {}
+    for kind in ("dev", "pin", "pin2"):
+        if kind == "dev":
+            bufs = [torch.empty((s, q) + full, dtype=torch.complex64, device="cuda"),
+                    torch.empty((s,) + full, dtype=torch.float32, device="cuda"),
+                    torch.empty((s,) + full, dtype=torch.uint8, device="cuda")]
+        else:
+            bufs = [torch.full((s, q) + full, 3 + 3j, dtype=torch.complex64).pin_memory(),
+                    torch.full((s,) + full, -1.0, dtype=torch.float32).pin_memory(),
+                    torch.full((s,) + full, 7, dtype=torch.uint8).pin_memory()]
+        torch.cuda.synchronize()
+        K.api.estimate_maps_batched_device(ctx, cal.data_ptr(), s, spec.calib, case.center_offset, q, full, cfg,
+                                           bufs[0].data_ptr(), bufs[1].data_ptr(), bufs[2].data_ptr())
+        outs[kind] = [b.cpu().numpy() for b in bufs]
+    for kind in ("pin", "pin2"):
+        # every sentinel overwritten: all slices' copies landed before the call returned
+        assert not np.any(outs[kind][0] == 3 + 3j) and not np.any(outs[kind][1] == -1.0)
+        assert not np.any(outs[kind][2] == 7)
+        # against the device-buffer call: converged results (lane step plans differ with the call
+        # history, DESIGN.md §5, so not bit for bit)
+        assert PM.rel_fro(outs[kind][0], outs["dev"][0]) < 1e-6
+        assert np.allclose(outs[kind][1], outs["dev"][1], rtol=1e-6, atol=1e-7)
+        assert (outs[kind][2] == outs["dev"][2]).mean() > 0.9999
