@@ -6,24 +6,28 @@
 // Layout: G arrives as packed Hermitian planes [h][N] (h = Q(Q+1)/2; plane
 // (p <= q) holds G(row p, col q) for every voxel, written by the K3
 // expansion) as an fp32 hi/lo pair.  Blocks are persistent and walk voxel
-// tiles; the next tile's h x VPB slab of hi planes is prefetched with
-// cp.async (double buffer) while the current tile iterates.  Each voxel is
-// unpacked into registers: a thread holds RPT full matrix rows
-// (p = local + r * QP/RPT), QP = Q rounded up to a power of two (padding
-// rows/cols are zero).
+// tiles; the next tile's h x VPB slab of hi planes is prefetched by TMA
+// (cp.async.bulk.tensor boxes on an mbarrier, double buffer; swizzled 32/64 B
+// rows so that the unpack and the epilogue reads spread over the banks; an
+// 8-byte cp.async fallback when TMA cannot address the planes) while the
+// current tile iterates.  Each voxel is unpacked into registers: a thread
+// holds RPT full matrix rows (p = local + r * QP/RPT), QP = Q rounded up to a
+// power of two (padding rows/cols are zero).
 //
 // Per iteration a thread loads v once from shared memory (float4 broadcast
-// pairs) and does RPT * QP complex MACs with it, then rescales its own
-// components; v and the per-warp partials of ||u||^2 are double-buffered so
-// an iteration costs one voxel-scoped barrier (named barrier when a voxel
-// spans several warps, __syncwarp otherwise).  RPT = 2 halves the shared
-// loads and the reduction overhead per FMA for Q = 32 (the main loop is then
-// ~80% FFMA).  The matrix never leaves registers across the `iters`
-// iterations, so the stage is FP32-bound: 8 Q^2 flops per voxel-iteration
-// against one read of the planes.  The final Rayleigh quotient is evaluated
-// in FP64 on hi + lo (lo streamed into the free tile buffer during the
-// iterations), which keeps per-voxel eigenvalues at ~FP64 accuracy
-// (DESIGN.md §5).
+// pairs) and does RPT * QP complex MACs with it as FFMA2 pairs, then rescales
+// its own components; v and the per-warp partials of ||u||^2 are
+// double-buffered so an iteration costs one voxel-scoped barrier (named
+// barrier when a voxel spans several warps, __syncwarp otherwise).  With one
+// row per thread the v broadcasts need as many shared-memory wavefronts as
+// the FFMA2 pipe needs cycles (tools/k4_loop_micro.cu).  The
+// matrix never leaves registers across the `iters` iterations: 8 Q^2 flops
+// per voxel-iteration against one read of the planes.  The final Rayleigh
+// quotient is evaluated in FP64 on hi + lo (lo streamed into its own tile
+// buffer during the iterations), which keeps per-voxel eigenvalues at ~FP64
+// accuracy; on full-resolution grids an FP32 quotient from the
+// registers is kept for lambda >= rq32_min (||G/|Lambda| || <= 1).  A voxel
+// range of a larger grid (PowerArgs::ld) lets the pipeline run K4 in chunks.
 //
 // Exactly the reference's control flow: fixed iteration count; at it == 0 an
 // annihilated all-ones start restarts from e_0; a norm below 1e-14 freezes v.
