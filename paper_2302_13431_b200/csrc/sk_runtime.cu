@@ -3,14 +3,18 @@
 // point validates like the reference, runs on the context stream, and
 // synchronises before returning.
 //
-// Pipeline (maps.cpp:265-330, pisco preset) as run here:
+// Pipeline (maps.cpp:265-330) as run here:
 //   gram       K1: channel spectra (apply_axis DFT) + pair lag contraction
-//   nullspace  K2: FP64 cuSOLVER Xsyevd on the promoted Gram, cut on the
-//                  host, Ws = U_sig U_sig^H by cuBLAS ZHERK (W = I - Ws)
-//   field      fold W into lag kernels, K3 lag expansion -> packed G planes
-//   eigensolve K4: power iteration (+ fused normalize epilogue)
-//   post       K5: apodised recon (before K4, timed here), interpolation,
-//                  SoS renormalisation, support mask
+//                  (baseline preset: calibration-matrix gather + FP64 ZHERK)
+//   nullspace  K2: FP64 block subspace iteration on the signal subspace
+//                  (3xTF32 / ZGEMM-3M products, own CholQR and Ritz kernels,
+//                  CUDA-graph replay), or cuSOLVER Xsyevd for the full spectrum
+//   field      fold W = I - U_sig U_sig^H into lag kernels (ZHERK or straight
+//                  from U_sig), K3 lag expansion -> packed G hi/lo planes
+//   eigensolve K4: power iteration (+ fused normalize epilogue), or the
+//                  warp-per-voxel Jacobi of the baseline preset
+//   post       K5: apodised recon (before K4, timed here), interpolation with
+//                  the fused SoS renormalisation, support mask
 #include <algorithm>
 #include <chrono>
 #include <functional>
@@ -542,9 +546,10 @@ Eig run_eigh(sk_ctx* ctx, const float2* gram, i64 n, double ratio) {  // nullspa
 // ---------------------------------------------------------------- K2 (subspace)
 // The pipeline needs only the signal subspace {lambda >= (ratio*sigma_1)^2}
 // (k = n - R ~ 20-50 vectors) and the count R.  Block subspace
-// iteration with Rayleigh-Ritz on the FP64-promoted Gram (cuBLAS ZGEMM for
-// A*V, CholQR2 orthonormalisation, cuSOLVER on the b x b projection) returns
-// exactly that.  Convergence: every Ritz pair with theta >= cut^2/2 has
+// iteration with Rayleigh-Ritz on the FP64-promoted Gram (3xTF32 steering
+// products, ZGEMM-3M for the last steps, CholQR orthonormalisation, the own
+// one-CTA eigensolver for b <= 64 else cuSOLVER on the b x b projection)
+// returns exactly that.  Convergence: every Ritz pair with theta >= cut^2/2 has
 // ||A v - theta v|| <= tol*theta_max, and the block extends below cut^2/2 so
 // no eigenvalue above the cut can hide outside it.  Optional certification:
 // Cholesky of cut^2*I - A + 2 theta_max U U^H succeeds iff lambda_{k+1} < cut^2
