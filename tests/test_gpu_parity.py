@@ -814,3 +814,16 @@ def test_batched_multislice_pinned_outputs(K):
         assert PM.rel_fro(outs[kind][0], outs["dev"][0]) < 1e-6
         assert np.allclose(outs[kind][1], outs["dev"][1], rtol=1e-6, atol=1e-7)
         assert (outs[kind][2] == outs["dev"][2]).mean() > 0.9999
+
+
+def test_estimate_maps_baseline_3d(K, O):
+    """Baseline preset (explicit Gram, dense per-voxel eigensolve, nullspace method) on a 3-D explicit grid."""
+    sc3 = O.simulate(4, (20, 18, 16), 1, 9, noise_sigma=0.01, noise_seed=2)
+    cal3 = O.extract_calibration(sc3["kspace"], (10, 10, 8))
+    ck = K.PipelineConfig.baseline()
+    ck.tau, ck.grid_dims = 1, (14, 12, 10)
+    cfo = O.PipelineConfig.baseline()
+    cfo.tau = 1
+    _, _, lam = _baseline_check(K, O, cal3.data.astype(np.complex64), cal3.center_offset, (20, 18, 16), ck, cfo,
+                                "3d/baseline", grid=(14, 12, 10))
+    assert lam["pointwise_p99"] < PM.TOL_LAMBDA
