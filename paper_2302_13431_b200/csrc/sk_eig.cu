@@ -577,6 +577,9 @@ bool herm_eig_small(sk_ctx* ctx, double2* H, int n, double* w, int* info, double
   if (n == 64) {
     set_smem_limit(reinterpret_cast<const void*>(herm_eig_kernel<64>), smem);
     herm_eig_kernel<64><<<1, kThreads, smem, ctx->stream>>>(H, n, w, floor_rel, info);
+  } else if (n == 32) {  // the 32-column block of small Grams (C1)
+    set_smem_limit(reinterpret_cast<const void*>(herm_eig_kernel<32>), smem);
+    herm_eig_kernel<32><<<1, kThreads, smem, ctx->stream>>>(H, n, w, floor_rel, info);
   } else {
     set_smem_limit(reinterpret_cast<const void*>(herm_eig_kernel<0>), smem);
     herm_eig_kernel<0><<<1, kThreads, smem, ctx->stream>>>(H, n, w, floor_rel, info);
