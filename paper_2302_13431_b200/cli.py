@@ -46,19 +46,26 @@ def extract_calibration(data: np.ndarray, size: tuple):  # types.cpp:58-90
     return Calib(np.ascontiguousarray(data[sl]), tuple(e // 2 for e in size))
 
 
-def config_from_flags(a):  # senskit_main.cpp:54-76
-    from .api import ELLIPSOID, GRID_FULL, GRID_REDUCED, RECT, PipelineConfig, UnsupportedError
-    if a.preset not in ("pisco", "baseline"):
+def config_from_flags(a):  # senskit_main.cpp:54-76 (both presets run on the GPU)
+    from .api import ELLIPSOID, GRID_FULL, GRID_REDUCED, RECT, PipelineConfig
+    if a.preset == "baseline":
+        cfg = PipelineConfig.baseline()
+    elif a.preset == "pisco":
+        cfg = PipelineConfig.pisco()
+    else:
         raise argparse.ArgumentTypeError(f"unknown preset '{a.preset}'")
-    if a.preset == "baseline" or a.gram == "explicit" or a.eig == "dense" or a.method == "nullspace" or \
-            a.field == "naive":
-        raise UnsupportedError("only the pisco arm (gram=fft, eig=power, method=espirit, field=fast) runs on "
-                               "the B200 path")
-    cfg = PipelineConfig()
     if a.kernel:
         cfg.kernel = RECT if a.kernel == "rect" else ELLIPSOID
+    if a.gram:
+        cfg.gram = 0 if a.gram == "explicit" else 1
     if a.grid:
         cfg.grid = GRID_FULL if a.grid == "full" else GRID_REDUCED
+    if a.eig:
+        cfg.eig = 0 if a.eig == "dense" else 1
+    if a.method:
+        cfg.method = 0 if a.method == "nullspace" else 1
+    if a.field:
+        cfg.field = 0 if a.field == "naive" else 1
     if a.tau >= 0:
         cfg.tau = a.tau
     if a.power_iters > 0:

@@ -77,7 +77,20 @@ def test_exit_codes_before_device_work(tmp_path, capsys):  # senskit_main.cpp:23
     save_stack(_stack((2, 16, 16), domain="image"), str(tmp_path / "img"))
     assert cli.main(["estimate", "--input", str(tmp_path / "img"), "--calib", "8", "--output", base + "o"]) == 3
     assert cli.main(["estimate", "--input", base, "--calib", "32", "--output", base + "o"]) == 5  # DimError
-    assert cli.main(["estimate", "--input", base, "--calib", "8", "--preset", "baseline",
-                     "--output", base + "o"]) == 1  # outside the pisco arm
     assert cli.main(["estimate", "--input", base, "--calib", "8", "--preset", "nope",
                      "--output", base + "o"]) == 2
+
+
+def test_config_from_flags_mirrors_reference():  # senskit_main.cpp:54-76
+    import argparse
+    ns = argparse.Namespace(preset="baseline", kernel=None, gram=None, grid=None, eig=None, method=None, field=None,
+                            tau=-1, power_iters=0, nullspace_threshold=0.0, mask_threshold=-1.0, apod_width=0.0,
+                            grid_pad=-1)
+    cfg = cli.config_from_flags(ns)
+    assert (cfg.kernel, cfg.gram, cfg.grid, cfg.eig) == (0, 0, 0, 0)  # maps.cpp:12-19
+    ns.preset, ns.eig, ns.method, ns.field, ns.gram, ns.tau = "pisco", "dense", "nullspace", "naive", "explicit", 4
+    cfg = cli.config_from_flags(ns)
+    assert (cfg.kernel, cfg.grid, cfg.eig, cfg.method, cfg.field, cfg.gram, cfg.tau) == (1, 1, 0, 0, 0, 0, 4)
+    ns.preset = "nope"
+    with pytest.raises(argparse.ArgumentTypeError):
+        cli.config_from_flags(ns)

@@ -583,6 +583,14 @@ def test_cli_estimate_end_to_end(K, O, tmp_path, capsys):
     ref_res = O.projection_residual(f32(k), f32(ref.maps))
     assert abs(prov["residual"] - ref_res) <= 1e-5 * ref_res
     assert (tmp_path / "run_mag_ch03.pgm").exists() and (tmp_path / "run_spectrum.csv").exists()
+    # --preset baseline (senskit_main.cpp:56-57): rect kernel, explicit Gram, full grid, dense eigensolve
+    outb = str(tmp_path / "runb")
+    rc = cli.main(["estimate", "--input", str(tmp_path / "in"), "--calib", "20", "--preset", "baseline", "--tau", "2",
+                   "--output", outb])
+    assert rc == 0
+    refb = K.estimate_maps(calib, (48, 48), K.PipelineConfig(kernel=K.RECT, tau=2, gram=0, grid=K.GRID_FULL, eig=0))
+    assert np.array_equal(load_stack(outb + "_maps").data, refb.maps)
+    assert json.load(open(outb + "_provenance.json"))["preset"] == "baseline"
 
 
 # ------------------------------------------------ multislice batched (C3 path)
