@@ -21,6 +21,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "lib", "libsk_oracle.so")
+# The reference itself (unmodified /root/reference/proj/src compiled against
+# oracle/ref_shim by oracle/Makefile.ref); `oracle.ref` binds this same API to it.
+REF_LIB_PATH = os.path.join(_HERE, "_ref", "libsk_ref.so")
 
 RECT, ELLIPSOID = 0, 1
 EXPLICIT, FFT = 0, 1
@@ -132,6 +135,11 @@ _SIGS = {
     "sko_simulate": [_I64, _I32, _VP, _I32, _U64, _I32, _D, _U64, _VP, _VP, _VP, _VP, _VP],
     "sko_projection_residual": [_I32, _VP, _I64, _VP, _VP, _VP],
 }
+# Only in oracle/_ref/libsk_ref.so (golden-fixture sampling, oracle/ref_capi.cpp).
+_SIGS_REF = {
+    "skr_estimate_sampled": [_I32, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _I64, _VP, _VP, _VP, _I64, _VP, _VP, _VP,
+                             _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP],
+}
 
 
 _lib = None
@@ -145,7 +153,9 @@ def lib():
         L = C.CDLL(_LIB_PATH)
         L.sko_last_error.restype = C.c_char_p
         L.sko_max_threads.restype = C.c_int
-        for name, args in _SIGS.items():
+        for name, args in list(_SIGS.items()) + list(_SIGS_REF.items()):
+            if not hasattr(L, name):
+                continue
             getattr(L, name).argtypes = args
             if name not in ('sko_set_max_threads', 'sko_set_lapack_threads', 'sko_fft_counters'):
                 getattr(L, name).restype = C.c_int
@@ -474,6 +484,52 @@ def simulate(q: int, dims, tau_gen: int, seed: int, kind: int = DISK, noise_sigm
                               gc.ctypes.data_as(C.c_void_p)))
     del n
     return {"kspace": ks, "true_maps": tm, "support_mask_true": mask, "phantom": ph, "gen_coeffs": gc}
+
+
+def estimate_sampled(calib: Calib, full_dims, cfg: PipelineConfig, grid_dims=None, gram_idx=None, field_idx=None,
+                     vox_idx=None) -> dict:
+    """The reference pipeline (maps.cpp:265-330, staged as in maps.hpp:115-123) with
+    the Gram sampled at (row, col) pairs ``gram_idx`` (K,2), G(x) at (voxel, row, col)
+    triples ``field_idx`` (K,3) before the eigensolve consumes it, and the final
+    maps / lambda / mask gathered at ``vox_idx``.  Only the oracle/_ref library
+    exports it (golden-fixture generation, tools/make_golden.py)."""
+    L = lib()
+    if not hasattr(L, "skr_estimate_sampled"):
+        raise RuntimeError("estimate_sampled needs oracle/_ref (the reference build)")
+    d = _c128(calib.data)
+    q, cdims = d.shape[0], d.shape[1:]
+    nd = len(cdims)
+    n = q * make_support(cfg.kernel, cfg.tau, nd).shape[0]
+    gi = _i64(np.zeros((0, 2)) if gram_idx is None else gram_idx).reshape(-1, 2)
+    fi = _i64(np.zeros((0, 3)) if field_idx is None else field_idx).reshape(-1, 3)
+    vi = _i64(np.zeros(0) if vox_idx is None else vox_idx).reshape(-1)
+    if grid_dims is None:
+        gshape = list(full_dims)
+        if cfg.grid == GRID_REDUCED:
+            gshape = [min(c + cfg.grid_pad, f) for c, f in zip(cdims, full_dims)]
+    else:
+        gshape = list(grid_dims)
+    gv = np.zeros(len(gi), dtype=np.complex128)
+    fv = np.zeros(len(fi), dtype=np.complex128)
+    gfro, ffro = C.c_double(0), C.c_double(0)
+    raw_l = np.zeros(tuple(gshape))
+    ms = np.zeros((q, len(vi)), dtype=np.complex128)
+    ls = np.zeros(len(vi))
+    mk = np.zeros(len(vi), dtype=np.uint8)
+    gd = np.zeros(nd, dtype=np.int64)
+    rank, s1 = C.c_int64(0), C.c_double(0)
+    spec = np.zeros(n)
+    st = np.zeros(5)
+    cfgc = cfg.to_c()
+    _check(L.skr_estimate_sampled(
+        nd, _p(_i64(cdims)), _p(_i64(calib.center_offset)), q, _p(d), _p(_i64(full_dims)), C.byref(cfgc),
+        _p(_i64(grid_dims)) if grid_dims is not None else None, len(gi), _p(gi), _p(gv), C.byref(gfro),
+        len(fi), _p(fi), _p(fv), C.byref(ffro), _p(raw_l), len(vi), _p(vi), _p(ms), _p(ls), _p(mk), _p(gd),
+        C.byref(rank), C.byref(s1), _p(spec), _p(st)))
+    return {"gram_vals": gv, "gram_fro": gfro.value, "field_vals": fv, "field_fro": ffro.value,
+            "raw_lambda": raw_l, "maps": ms, "lambda": ls, "mask": mk, "grid_dims": tuple(int(x) for x in gd),
+            "rank": rank.value, "sigma1": s1.value, "spectrum_normalized": spec,
+            "stages": dict(zip(STAGES, st.tolist()))}
 
 
 def projection_residual(kspace: np.ndarray, maps: np.ndarray) -> float:

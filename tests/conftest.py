@@ -18,3 +18,24 @@ def O():
     from oracle import oracle
     oracle.lib()
     return oracle
+
+
+def load_ref():
+    """oracle/_ref: the unmodified reference sources compiled against oracle/ref_shim.
+    Built on demand where /root/reference exists (this container); on the GPU box
+    the prebuilt library travels with the repo snapshot."""
+    import subprocess
+    from oracle import ref
+    if not ref.available():
+        if os.path.isdir("/root/reference/proj/src"):
+            subprocess.run(["make", "-C", ROOT, "-f", "oracle/Makefile.ref"], check=True,
+                           stdout=subprocess.DEVNULL)
+        else:
+            pytest.skip("oracle/_ref not built and /root/reference absent")
+    ref.lib()
+    return ref
+
+
+@pytest.fixture(scope="session")
+def R():
+    return load_ref()

@@ -1,14 +1,27 @@
 """Pins the C++ FP64 oracle (oracle/) before it is trusted as the GPU checker.
 
-Two kinds of evidence, since the reference ships no golden vectors
+Three kinds of evidence, since the reference ships no golden vectors
 (SURVEY.md §8c): (1) the reference's own known-answer tests, re-asserted with
-the reference file:line they come from; (2) an independent numpy restatement
-(tests/npref.py) on small cases.
+the reference file:line they come from — run against BOTH the restatement
+(``port``) and the reference itself compiled from its unmodified sources
+(``ref``, oracle/_ref, which also validates the Eigen-subset shim it is built
+on); (2) an independent numpy restatement (tests/npref.py) on small cases;
+(3) call-for-call equality of port and ref (tests/test_ref_pin.py).
 """
 import numpy as np
 import pytest
 
 from tests import npref
+from tests.conftest import load_ref
+
+
+@pytest.fixture(scope="module", params=["port", "ref"])
+def O(request):
+    if request.param == "ref":
+        return load_ref()
+    from oracle import oracle
+    oracle.lib()
+    return oracle
 
 
 def rnd(shape, seed):
