@@ -240,6 +240,22 @@ int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, con
                            double* spectrum_normalized, sk_provenance* prov, sk_c64* gram_out,
                            sk_c64* field_out, sk_c64* raw_maps_out, float* raw_lambda_out);
 
+/* Parity probe (test hook; the config-scale parity suite): estimate_maps on
+ * exactly the path sk_estimate_maps runs (same solver selection: no spectrum,
+ * so the subspace eigensolver), plus in-place samples of the intermediates:
+ * gram_vals[k] = Gram(gram_idx[2k], gram_idx[2k+1]) (calibration.hpp:25-30,
+ * column-major n x n), field_vals[k] = G_j(row, col) for (j, row, col) =
+ * field_idx[3k..3k+2] (spatial_gram.hpp:36-51, hi + lo in FP64), their
+ * Frobenius norms over the whole Gram / map grid, and the native-grid lambda
+ * (RawMaps::lambda, maps.hpp:110-113).  Complex samples are interleaved
+ * float64.  Any output may be NULL (then n_* must be 0 for the samples). */
+int sk_estimate_maps_probe(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset,
+                           int64_t channels, const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg,
+                           sk_c64* maps, float* lambda_min_map, uint8_t* support_mask, sk_provenance* prov,
+                           int64_t n_gram, const int64_t* gram_idx, double* gram_vals, double* gram_fro,
+                           int64_t n_field, const int64_t* field_idx, double* field_vals, double* field_fro,
+                           float* raw_lambda);
+
 /* Multislice: `slices` independent calibrations (slice-major, each
  * channel-major), one estimate_maps per slice on this GPU, outputs
  * slice-major.  prov may be NULL or an array of `slices` records. */

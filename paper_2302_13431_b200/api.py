@@ -191,6 +191,8 @@ _SIGS = {
     "sk_estimate_maps": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP], _I32),
     "sk_estimate_maps_debug": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                 _VP, _VP], _I32),
+    "sk_estimate_maps_probe": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _VP, _VP,
+                                _I64, _VP, _VP, _VP, _VP], _I32),
     "sk_estimate_maps_batched": ([_VP, _I64, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP], _I32),
 }
 
@@ -531,6 +533,40 @@ def estimate_maps(calib: Calib, full_dims, cfg: PipelineConfig, ctx: Context | N
         fieldb.reshape(ngrid, q, q).transpose(0, 2, 1) if want_field else None, raw, raw_l,
         extra={"eig_solver": "full" if prov.eig_solver_used == 1 else "subspace", "certified": bool(prov.certified),
                "subspace_iterations": int(prov.subspace_iterations), "subspace_block": int(prov.subspace_block)})
+
+
+def estimate_maps_probe(calib: Calib, full_dims, cfg: PipelineConfig, ctx: Context | None = None, *,
+                        gram_idx=None, field_idx=None) -> tuple[SensitivityResult, dict]:
+    """estimate_maps on exactly the sk_estimate_maps path (no spectrum requested, so
+    the same nullspace solver the bench runs) plus in-place samples of the Gram at
+    (row, col) ``gram_idx`` and of G(x) at (voxel, row, col) ``field_idx``, their
+    Frobenius norms and the native-grid lambda (sk_estimate_maps_probe)."""
+    d = _c64(calib.data)
+    q, cdims = d.shape[0], d.shape[1:]
+    nd = len(cdims)
+    grid = _grid_for(cdims, full_dims, cfg)
+    gi = _i64(np.zeros((0, 2)) if gram_idx is None else gram_idx).reshape(-1, 2)
+    fi = _i64(np.zeros((0, 3)) if field_idx is None else field_idx).reshape(-1, 3)
+    maps = np.zeros((q,) + tuple(full_dims), dtype=np.complex64)
+    lamb = np.zeros(tuple(full_dims), dtype=np.float32)
+    mask = np.zeros(tuple(full_dims), dtype=np.uint8)
+    gv = np.zeros(len(gi), dtype=np.complex128)
+    fv = np.zeros(len(fi), dtype=np.complex128)
+    gfro, ffro = C.c_double(0), C.c_double(0)
+    rawl = np.zeros(grid, dtype=np.float32)
+    prov = sk_provenance()
+    cfgc = cfg.to_c()
+    _check(lib().sk_estimate_maps_probe(
+        _ctx(ctx), nd, _p(_i64(cdims)), _p(_i64(calib.center_offset)), q, _p(d), _p(_i64(full_dims)), C.byref(cfgc),
+        _p(maps), _p(lamb), _p(mask), C.byref(prov), len(gi), _p(gi), _p(gv), C.byref(gfro), len(fi), _p(fi), _p(fv),
+        C.byref(ffro), _p(rawl)))
+    res = SensitivityResult(
+        maps, lamb, mask, tuple(int(prov.grid_dims[a]) for a in range(nd)), int(prov.support_size),
+        int(prov.nullspace_rank), float(prov.sigma1), float(prov.cut_margin), None,
+        dict(zip(STAGES, list(prov.stage_ms))), float(prov.total_ms), int(prov.zeroed_voxels), raw_lambda=rawl,
+        extra={"eig_solver": "full" if prov.eig_solver_used == 1 else "subspace", "certified": bool(prov.certified),
+               "subspace_iterations": int(prov.subspace_iterations), "subspace_block": int(prov.subspace_block)})
+    return res, {"gram_vals": gv, "gram_fro": gfro.value, "field_vals": fv, "field_fro": ffro.value}
 
 
 def projection_residual(kspace: np.ndarray, maps: np.ndarray, ctx: Context | None = None) -> float:

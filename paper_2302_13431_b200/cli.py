@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import re
 import sys
 
 import numpy as np
@@ -21,15 +22,40 @@ import numpy as np
 EXIT_OK, EXIT_OTHER, EXIT_FLAGS, EXIT_IO, EXIT_NULLSPACE, EXIT_SHAPE = 0, 1, 2, 3, 4, 5
 
 
+_STOLL = re.compile(r"[ \t\n\v\f\r]*([+-]?[0-9]+)")
+
+
+def _stoll(tok: str) -> int:
+    """std::stoll(tok) (base 10): leading whitespace, optional sign, digits; the
+    rest of the token is ignored.  No conversion -> std::invalid_argument, out of
+    range -> std::out_of_range; both reach the CLI's generic handler (exit 1)."""
+    m = _STOLL.match(tok)
+    if not m:
+        raise ValueError(f"stoll: no conversion of '{tok}'")
+    v = int(m.group(1))
+    if not -(1 << 63) <= v < (1 << 63):
+        raise OverflowError(f"stoll: '{tok}' out of range")
+    return v
+
+
 def parse_extents(text: str, rank: int) -> tuple:  # senskit_main.cpp:29-43
-    try:
-        out = [int(t) for t in text.split(",") if t != ""]
-    except ValueError:
-        raise argparse.ArgumentTypeError(f"bad extents '{text}'") from None
+    """Comma-separated extents, token by token as the reference scans them (an
+    empty token fails std::stoll; a trailing comma ends the scan).  A single
+    value is broadcast to every axis; a count mismatch is CLI::ValidationError,
+    a CLI11 ParseError -> exit 2 (senskit_main.cpp:40-41, 372-374)."""
+    out = []
+    pos = 0
+    while pos < len(text):
+        comma = text.find(",", pos)
+        tok = text[pos:] if comma < 0 else text[pos:comma]
+        out.append(_stoll(tok))
+        if comma < 0:
+            break
+        pos = comma + 1
     if len(out) == 1 and rank > 1:
         out = out * rank
     if rank and len(out) != rank:
-        raise ValueError(f"expected {rank} extents, got '{text}'")
+        raise argparse.ArgumentTypeError(f"expected {rank} comma-separated extents")
     return tuple(out)
 
 

@@ -65,8 +65,12 @@ class Arena {
     return static_cast<T*>(get(name, size_t(count) * sizeof(T)));
   }
   void release_all();
+  // Bumped whenever an existing slot is freed (grown or released): captured
+  // CUDA graphs that baked in arena pointers are stale after a bump.
+  uint64_t generation() const { return generation_; }
 
  private:
+  uint64_t generation_ = 0;
   struct Slot {
     void* ptr = nullptr;
     size_t bytes = 0;
@@ -93,6 +97,15 @@ struct RoundKey {
            std::tie(o.n, o.b, o.q, o.v, o.y, o.t, o.h, o.w, o.res, o.info, o.a, o.gram, o.ratio);
   }
 };
+// Cached device index tables per (support, q), owned by the context.
+struct SupportTables {
+  int2* pairs = nullptr;  // h entries (p <= q)
+  int* off = nullptr;     // lam: box index of n_s relative to lag 0
+  int* lag_ptr = nullptr; // nbox + 1
+  int* lag_st = nullptr;  // lam^2 packed (s | t << 16), grouped by lag n_t - n_s
+  int nbox = 0, lb = 0;
+};
+
 struct RoundGraph {
   cudaGraphExec_t exec = nullptr;
   int seen = 0;
@@ -114,6 +127,8 @@ struct sk_ctx {
   skb::Arena arena;
   skb::MatrixCache matrices;
   std::map<std::string, void*> tables;  // cached index tables (device)
+  std::map<std::string, skb::SupportTables> support_tables;  // per (support, q)
+  uint64_t rounds_generation = 0;       // arena generation the captured rounds were built against
   int64_t launches = 0;   // our kernels
   int64_t lib_calls = 0;  // cuSOLVER / cuBLAS calls
   cudaEvent_t ev[8] = {};
@@ -257,6 +272,11 @@ void mask_kernel(sk_ctx* ctx, const float* lambda, i64 n, float thr, uint8_t* ma
 void sos_accumulate(sk_ctx* ctx, const float2* maps, i64 n, int q, float* sos);   // sos += sum_c |maps_c|^2
 // projection_residual value (metrics.cpp:11-49) from the unitary image and the maps (synchronous).
 double projection_residual_value(sk_ctx* ctx, const float2* img, const float2* maps, i64 n, int q);
+// parity probe (sk_estimate_maps_probe): gathers + Frobenius sums, FP64
+void probe_gather_gram(sk_ctx* ctx, const float2* gram, i64 n, const long long* idx, i64 k, double2* out);
+void probe_gather_field(sk_ctx* ctx, const float2* hi, const float2* lo, i64 nvox, int q, const long long* idx,
+                        i64 k, double2* out);
+double probe_sumsq(sk_ctx* ctx, const float2* a, const float2* lo, i64 total, i64 plane_len, int q);
 // Centred transform along one axis (fft.cpp kspace_to_image / image_to_kspace):
 // out = fftshift(DFT(ifftshift(in))) * scale, inverse = conjugate kernel.
 // Returns false (nothing launched) unless N and inner are powers of two.

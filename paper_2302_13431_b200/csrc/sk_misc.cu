@@ -546,3 +546,112 @@ void normalize_standalone(sk_ctx* ctx, float2* maps, i64 n, int q, const float2*
 }
 
 }  // namespace skb
+
+namespace skb {
+
+// ---------------------------------------------------------------- parity probe
+// Test hook behind sk_estimate_maps_probe: gathers of the Gram and of G(x)
+// (hi + lo planes, FP64) at caller-chosen entries, and Frobenius norms with a
+// fixed-order reduction.  Reads only; the pipeline's own buffers are untouched.
+namespace {
+__device__ __forceinline__ int pair_row(int pair, int q) {
+  // pair index of (p, c), p <= c, is p*q - p*(p-1)/2 + (c - p): invert for p
+  const double b = 2.0 * q + 1.0;
+  int p = int((b - sqrt(b * b - 8.0 * pair)) * 0.5);
+  while (p > 0 && p * q - p * (p - 1) / 2 > pair) --p;
+  while ((p + 1) * q - (p + 1) * p / 2 <= pair) ++p;
+  return p;
+}
+
+__global__ void probe_gram_kernel(const float2* __restrict__ g, i64 n, const long long* __restrict__ idx, i64 k,
+                                  double2* __restrict__ out) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= k) return;
+  const float2 v = g[idx[2 * t] + idx[2 * t + 1] * n];
+  out[t] = make_double2(v.x, v.y);
+}
+
+__global__ void probe_field_kernel(const float2* __restrict__ hi, const float2* __restrict__ lo, i64 nvox, int q,
+                                   const long long* __restrict__ idx, i64 k, double2* __restrict__ out) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= k) return;
+  const i64 j = idx[3 * t];
+  const int row = int(idx[3 * t + 1]), col = int(idx[3 * t + 2]);
+  const int p = min(row, col), c = max(row, col);
+  const i64 pair = i64(p) * q - i64(p) * (p - 1) / 2 + (c - p);
+  const float2 h = hi[pair * nvox + j];
+  double re = h.x, im = h.y;
+  if (lo) {
+    const float2 l = lo[pair * nvox + j];
+    re += double(l.x);
+    im += double(l.y);
+  }
+  if (row > col) im = -im;   // G(q,p) = conj G(p,q)
+  if (row == col) im = 0.0;  // spatial_gram.cpp:140-146
+  out[t] = make_double2(re, im);
+}
+
+// sum |a (+ lo)|^2; planes mode (q > 0): element e lies in plane e / plane_len,
+// off-diagonal planes count twice (their mirrored half of the full matrix).
+__global__ void __launch_bounds__(256) sumsq_partial_kernel(const float2* __restrict__ a,
+                                                            const float2* __restrict__ lo, i64 total,
+                                                            i64 plane_len, int q, double* __restrict__ partial) {
+  __shared__ double s[256];
+  double acc = 0.0;
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
+    const float2 v = a[e];
+    double re = v.x, im = v.y;
+    if (lo) {
+      re += double(lo[e].x);
+      im += double(lo[e].y);
+    }
+    double w = 1.0;
+    if (q > 0) {
+      const int pair = int(e / plane_len);
+      const int p = pair_row(pair, q);
+      const bool diag = pair == p * q - p * (p - 1) / 2;
+      w = diag ? 1.0 : 2.0;
+      if (diag) im = 0.0;
+    }
+    acc += w * (re * re + im * im);
+  }
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (int(threadIdx.x) < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = s[0];
+}
+}  // namespace
+
+void probe_gather_gram(sk_ctx* ctx, const float2* gram, i64 n, const long long* idx, i64 k, double2* out) {
+  if (k <= 0) return;
+  probe_gram_kernel<<<unsigned((k + 255) / 256), 256, 0, ctx->stream>>>(gram, n, idx, k, out);
+  ++ctx->launches;
+  SKB_LAUNCH("probe_gram");
+}
+
+void probe_gather_field(sk_ctx* ctx, const float2* hi, const float2* lo, i64 nvox, int q, const long long* idx,
+                        i64 k, double2* out) {
+  if (k <= 0) return;
+  probe_field_kernel<<<unsigned((k + 255) / 256), 256, 0, ctx->stream>>>(hi, lo, nvox, q, idx, k, out);
+  ++ctx->launches;
+  SKB_LAUNCH("probe_field");
+}
+
+double probe_sumsq(sk_ctx* ctx, const float2* a, const float2* lo, i64 total, i64 plane_len, int q) {
+  const int blocks = int(std::max<i64>(1, std::min<i64>((total + 255) / 256, 4 * i64(ctx->sm_count))));
+  double* partial = ctx->arena.get<double>("probe:partial", blocks);
+  sumsq_partial_kernel<<<blocks, 256, 0, ctx->stream>>>(a, lo, total, plane_len, q, partial);
+  ++ctx->launches;
+  SKB_LAUNCH("probe_sumsq");
+  std::vector<double> h(static_cast<size_t>(blocks));
+  SKB_CUDA(cudaMemcpyAsync(h.data(), partial, h.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  double s = 0.0;
+  for (double v : h) s += v;
+  return s;
+}
+
+}  // namespace skb

@@ -37,10 +37,13 @@ thread_local std::string g_last_error;
 namespace skb {
 [[noreturn]] void fail(int code, const std::string& msg) { throw Error(code, msg); }
 void set_smem_limit(const void* func, size_t bytes) {
+  // cudaFuncAttributeMaxDynamicSharedMemorySize is per device: key on both
   static std::mutex mu;
-  static std::map<const void*, size_t> granted;
+  static std::map<std::pair<int, const void*>, size_t> granted;
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
   std::lock_guard<std::mutex> lock(mu);
-  size_t& g = granted[func];
+  size_t& g = granted[{dev, func}];
   if (bytes <= g) return;
   check_cuda(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)),
              "cudaFuncSetAttribute(max dynamic smem)");
@@ -66,7 +69,10 @@ void* Arena::get(const std::string& name, size_t bytes) {
   if (bytes == 0) bytes = 16;
   Slot& s = slots_[name];
   if (s.bytes < bytes) {
-    if (s.ptr) cudaFree(s.ptr);
+    if (s.ptr) {
+      cudaFree(s.ptr);
+      ++generation_;
+    }
     s.ptr = nullptr;
     s.bytes = 0;
     const size_t want = (bytes + 255) & ~size_t(255);
@@ -79,6 +85,7 @@ void Arena::release_all() {
   for (auto& kv : slots_)
     if (kv.second.ptr) cudaFree(kv.second.ptr);
   slots_.clear();
+  ++generation_;
 }
 MatrixCache::~MatrixCache() {
   for (auto& kv : mats) cudaFree(kv.second);
@@ -344,23 +351,12 @@ struct Planes {
   float2* lo = nullptr;
 };
 
-// Cached device tables per (support, q).
-struct SupportTables {
-  int2* pairs = nullptr;  // h entries (p <= q)
-  int* off = nullptr;     // lam: box index of n_s relative to lag 0
-  int* lag_ptr = nullptr; // nbox + 1
-  int* lag_st = nullptr;  // lam^2 packed (s | t << 16), grouped by lag n_t - n_s
-  int nbox = 0, lb = 0;
-};
-
+// Device index tables per (support, q), cached in the context (freed by sk_destroy).
 SupportTables& tables_for(sk_ctx* ctx, const Support& s, int q) {
-  static std::map<std::pair<sk_ctx*, std::string>, SupportTables> cache;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lock(mu);
   const std::string key = std::to_string(s.shape) + ":" + std::to_string(s.tau) + ":" + std::to_string(s.nd) + ":" +
                           std::to_string(q);
-  auto it = cache.find({ctx, key});
-  if (it != cache.end()) return it->second;
+  auto it = ctx->support_tables.find(key);
+  if (it != ctx->support_tables.end()) return it->second;
   SupportTables t;
   t.lb = 4 * s.tau + 1;
   t.nbox = 1;
@@ -398,7 +394,7 @@ SupportTables& tables_for(sk_ctx* ctx, const Support& s, int q) {
   t.off = static_cast<int*>(up(off.data(), off.size() * sizeof(int)));
   t.lag_ptr = static_cast<int*>(up(ptr.data(), ptr.size() * sizeof(int)));
   t.lag_st = static_cast<int*>(up(st.data(), std::max<size_t>(st.size(), 1) * sizeof(int)));
-  return cache.emplace(std::make_pair(ctx, key), t).first->second;
+  return ctx->support_tables.emplace(key, t).first->second;
 }
 
 i64 next_pow2(i64 n) {
@@ -814,7 +810,17 @@ struct PhaseLaps {
 // runs eagerly (the arena grows to its final size), the second captures the
 // launch sequence, later calls replay it and restore the V/Y/T rotation of
 // the captured run.  A capture failure (a library call that cannot be
-// captured) marks the key eager-only.
+// captured) marks the key eager-only.  Graphs bake in arena pointers beyond
+// the key (Cholesky / Ritz scratch slots), so every captured round is dropped
+// as soon as the arena frees any slot (Arena::generation).
+void drop_stale_rounds(sk_ctx* ctx) {
+  if (ctx->rounds_generation == ctx->arena.generation()) return;
+  for (auto& kv : ctx->rounds)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  ctx->rounds.clear();
+  ctx->rounds_generation = ctx->arena.generation();
+}
+
 void run_graphed(sk_ctx* ctx, bool allowed, const RoundKey& key, double2*& V, double2*& Y, double2*& T,
                  const std::function<void()>& body) {
   static const bool disabled = std::getenv("SKB_NO_GRAPH") != nullptr;
@@ -822,6 +828,7 @@ void run_graphed(sk_ctx* ctx, bool allowed, const RoundKey& key, double2*& V, do
     body();
     return;
   }
+  drop_stale_rounds(ctx);
   auto& g = ctx->rounds[key];
   if (g.exec) {
     SKB_CUDA(cudaGraphLaunch(g.exec, ctx->stream));
@@ -881,7 +888,18 @@ void run_graphed(sk_ctx* ctx, bool allowed, const RoundKey& key, double2*& V, do
   g.t = T;
   g.launches = ctx->launches - l0;
   g.lib_calls = ctx->lib_calls - c0;
-  SKB_CUDA(cudaGraphLaunch(g.exec, ctx->stream));  // capture recorded, not ran, the round
+  if (ctx->rounds_generation != ctx->arena.generation()) {
+    // the capture itself grew a slot: older rounds are stale, this one is current
+    for (auto& kv : ctx->rounds) {
+      const bool same = !(kv.first < key) && !(key < kv.first);
+      if (!same && kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    }
+    RoundGraph keep = g;
+    ctx->rounds.clear();
+    ctx->rounds[key] = keep;
+    ctx->rounds_generation = ctx->arena.generation();
+  }
+  SKB_CUDA(cudaGraphLaunch(ctx->rounds[key].exec, ctx->stream));  // capture recorded, not ran, the round
 }
 
 bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, bool certify, Eig& e) {
@@ -1391,6 +1409,16 @@ struct PipelineOut {
   // normalised maps / raw lambda of those rows go to maps / lambda and the
   // interpolation stage is skipped.
   i64 slab0 = 0, slab1 = -1;
+  // parity probe (sk_estimate_maps_probe): device index lists in, FP64 samples out
+  struct Probe {
+    i64 n_gram = 0, n_field = 0;
+    const long long* gram_idx = nullptr;   // device, (row, col) pairs
+    const long long* field_idx = nullptr;  // device, (voxel, row, col) triples
+    double2* gram_vals = nullptr;          // device
+    double2* field_vals = nullptr;         // device
+    double gram_sumsq = 0.0, field_sumsq = 0.0;
+    float* raw_lambda = nullptr;           // device, N_grid
+  }* probe = nullptr;
 };
 
 // K4 epilogue: voxels with lambda >= this keep the FP32 Rayleigh quotient
@@ -1455,6 +1483,10 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   // compute_gram (maps.cpp:180-186)
   float2* gram = cfg->gram == 0 ? run_gram_explicit(ctx, cdims, q, calib, s, out.gram)
                                 : run_gram(ctx, cdims, q, calib, s, out.gram);
+  if (out.probe) {
+    probe_gather_gram(ctx, gram, q * s.count, out.probe->gram_idx, out.probe->n_gram, out.probe->gram_vals);
+    out.probe->gram_sumsq = probe_sumsq(ctx, gram, nullptr, q * s.count * q * s.count, 0, 0);
+  }
   SKB_CUDA(cudaEventRecord(ev[1], ctx->stream));
   // nullspace
   Eig e = run_nullspace(ctx, gram, n, cfg->nullspace_threshold, cfg->eig_solver, out.spectrum != nullptr,
@@ -1474,6 +1506,11 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   const Planes pl = run_field(ctx, e, s, int(q), grid, out.slab0, out.slab1);
   float2* planes = pl.hi;
   if (out.field) planes_to_field_full(ctx, pl.hi, pl.lo, ngrid, int(q), out.field);
+  if (out.probe) {
+    probe_gather_field(ctx, pl.hi, pl.lo, ngrid, int(q), out.probe->field_idx, out.probe->n_field,
+                       out.probe->field_vals);
+    out.probe->field_sumsq = probe_sumsq(ctx, pl.hi, pl.lo, i64(q * (q + 1) / 2) * ngrid, ngrid, int(q));
+  }
   SKB_CUDA(cudaEventRecord(ev[3], ctx->stream));
   // post (part 1): apodised recon on the map grid, consumed by K4's epilogue
   float2* recon = run_recon(ctx, cdims, co, q, calib, grid, cfg->apod_width, out.slab0, out.slab1);
@@ -1577,6 +1614,9 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
     power_iteration(ctx, pa);
   }
   }
+  if (out.probe && out.probe->raw_lambda)
+    SKB_CUDA(cudaMemcpyAsync(out.probe->raw_lambda, lam_grid, size_t(ngrid) * sizeof(float), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
   SKB_CUDA(cudaEventRecord(ev[5], ctx->stream));
   // post (part 2): interpolation + renormalisation + mask (maps.cpp:236-258)
   if (interp) {
@@ -1679,6 +1719,15 @@ int sk_destroy(sk_ctx* ctx) {
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     ctx->rounds.clear();
     ctx->arena.release_all();
+    for (auto& kv : ctx->support_tables) {
+      cudaFree(kv.second.pairs);
+      cudaFree(kv.second.off);
+      cudaFree(kv.second.lag_ptr);
+      cudaFree(kv.second.lag_st);
+    }
+    ctx->support_tables.clear();
+    for (auto& kv : ctx->tables) cudaFree(kv.second);
+    ctx->tables.clear();
     for (auto& e : ctx->ev) cudaEventDestroy(e);
     for (auto& e : ctx->chunk_ev)
       if (e) cudaEventDestroy(e);
@@ -2045,10 +2094,24 @@ int sk_debug_cross_gram(sk_ctx* ctx, int64_t n, int64_t b, const double* x, cons
   });
 }
 
-int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset,
-                           int64_t q, const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg,
-                           sk_c64* maps, float* lambda, uint8_t* mask, double* spectrum, sk_provenance* prov,
-                           sk_c64* gram_out, sk_c64* field_out, sk_c64* raw_maps_out, float* raw_lambda_out) {
+}  // extern "C"
+
+namespace {
+struct ProbeIn {
+  int64_t n_gram = 0, n_field = 0;
+  const int64_t* gram_idx = nullptr;
+  const int64_t* field_idx = nullptr;
+  double* gram_vals = nullptr;
+  double* field_vals = nullptr;
+  double* gram_fro = nullptr;
+  double* field_fro = nullptr;
+  float* raw_lambda = nullptr;  // host, N_grid
+};
+
+int estimate_impl(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset, int64_t q,
+                  const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg, sk_c64* maps, float* lambda,
+                  uint8_t* mask, double* spectrum, sk_provenance* prov, sk_c64* gram_out, sk_c64* field_out,
+                  sk_c64* raw_maps_out, float* raw_lambda_out, const ProbeIn* pin) {
   return guarded([&] {
     require_ctx(ctx);
     if (ndim < 1) fail(SK_ERR_DIM, "stack needs at least one axis");
@@ -2129,7 +2192,43 @@ int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, con
     po.raw_maps = orm.dev;
     po.raw_lambda = orl.dev;
     po.spectrum = spectrum ? spec.data() : nullptr;
+    PipelineOut::Probe probe;
+    Out<float> opl(ctx, pin ? pin->raw_lambda : nullptr, ng, "probe:rawl");
+    if (pin) {
+      const i64 ng_idx = std::max<int64_t>(pin->n_gram, 0), nf_idx = std::max<int64_t>(pin->n_field, 0);
+      long long* gi = ctx->arena.get<long long>("probe:gram_idx", std::max<i64>(1, 2 * ng_idx));
+      long long* fi = ctx->arena.get<long long>("probe:field_idx", std::max<i64>(1, 3 * nf_idx));
+      if (ng_idx)
+        SKB_CUDA(cudaMemcpyAsync(gi, pin->gram_idx, size_t(2 * ng_idx) * 8, cudaMemcpyHostToDevice, ctx->stream));
+      if (nf_idx)
+        SKB_CUDA(cudaMemcpyAsync(fi, pin->field_idx, size_t(3 * nf_idx) * 8, cudaMemcpyHostToDevice, ctx->stream));
+      for (i64 k = 0; k < 2 * ng_idx; ++k)
+        if (pin->gram_idx[k] < 0 || pin->gram_idx[k] >= n) fail(SK_ERR_DIM, "probe gram index out of range");
+      for (i64 k = 0; k < nf_idx; ++k)
+        if (pin->field_idx[3 * k] < 0 || pin->field_idx[3 * k] >= ng || pin->field_idx[3 * k + 1] < 0 ||
+            pin->field_idx[3 * k + 1] >= q || pin->field_idx[3 * k + 2] < 0 || pin->field_idx[3 * k + 2] >= q)
+          fail(SK_ERR_DIM, "probe field index out of range");
+      probe.n_gram = ng_idx;
+      probe.n_field = nf_idx;
+      probe.gram_idx = gi;
+      probe.field_idx = fi;
+      probe.gram_vals = ctx->arena.get<double2>("probe:gram_vals", std::max<i64>(1, ng_idx));
+      probe.field_vals = ctx->arena.get<double2>("probe:field_vals", std::max<i64>(1, nf_idx));
+      probe.raw_lambda = opl.dev;
+      po.probe = &probe;
+    }
     pipeline(ctx, cd, co, q, d_cal, fd, cfg, po, prov);
+    if (pin) {
+      if (pin->n_gram > 0)
+        SKB_CUDA(cudaMemcpyAsync(pin->gram_vals, probe.gram_vals, size_t(pin->n_gram) * 16, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+      if (pin->n_field > 0)
+        SKB_CUDA(cudaMemcpyAsync(pin->field_vals, probe.field_vals, size_t(pin->n_field) * 16,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+      if (pin->gram_fro) *pin->gram_fro = std::sqrt(probe.gram_sumsq);
+      if (pin->field_fro) *pin->field_fro = std::sqrt(probe.field_sumsq);
+      opl.finish(ctx);
+    }
     if (defer) {
       SKB_CUDA(cudaEventRecord(ctx->d2h_ready, ctx->stream));
       SKB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->d2h_ready, 0));
@@ -2150,6 +2249,36 @@ int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, con
     SKB_CUDA(cudaStreamSynchronize(ctx->stream));
     if (spectrum) std::copy(spec.begin(), spec.begin() + n, spectrum);
   });
+}
+}  // namespace
+
+extern "C" {
+
+int sk_estimate_maps_debug(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset,
+                           int64_t q, const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg,
+                           sk_c64* maps, float* lambda, uint8_t* mask, double* spectrum, sk_provenance* prov,
+                           sk_c64* gram_out, sk_c64* field_out, sk_c64* raw_maps_out, float* raw_lambda_out) {
+  return estimate_impl(ctx, ndim, calib_dims, center_offset, q, calib, full_dims, cfg, maps, lambda, mask, spectrum,
+                       prov, gram_out, field_out, raw_maps_out, raw_lambda_out, nullptr);
+}
+
+int sk_estimate_maps_probe(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset,
+                           int64_t q, const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg,
+                           sk_c64* maps, float* lambda, uint8_t* mask, sk_provenance* prov, int64_t n_gram,
+                           const int64_t* gram_idx, double* gram_vals, double* gram_fro, int64_t n_field,
+                           const int64_t* field_idx, double* field_vals, double* field_fro, float* raw_lambda) {
+  ProbeIn pin;
+  pin.n_gram = n_gram;
+  pin.n_field = n_field;
+  pin.gram_idx = gram_idx;
+  pin.field_idx = field_idx;
+  pin.gram_vals = gram_vals;
+  pin.field_vals = field_vals;
+  pin.gram_fro = gram_fro;
+  pin.field_fro = field_fro;
+  pin.raw_lambda = raw_lambda;
+  return estimate_impl(ctx, ndim, calib_dims, center_offset, q, calib, full_dims, cfg, maps, lambda, mask, nullptr,
+                       prov, nullptr, nullptr, nullptr, nullptr, &pin);
 }
 
 int sk_projection_residual(sk_ctx* ctx, int ndim, const int64_t* dims, int64_t channels, const sk_c64* kspace,

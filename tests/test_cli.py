@@ -61,10 +61,18 @@ def test_extract_calibration_centered():  # types.cpp:58-90
 
 
 def test_parse_extents():  # senskit_main.cpp:29-43
+    import argparse
     assert cli.parse_extents("24", 2) == (24, 24)
     assert cli.parse_extents("24,20,8", 3) == (24, 20, 8)
-    with pytest.raises(ValueError):
+    assert cli.parse_extents("24,20,", 2) == (24, 20)       # trailing comma ends the scan
+    assert cli.parse_extents(" 24x,+8", 2) == (24, 8)       # std::stoll: whitespace, sign, trailing text
+    with pytest.raises(argparse.ArgumentTypeError):          # CLI::ValidationError -> exit 2
         cli.parse_extents("24,20", 3)
+    with pytest.raises(argparse.ArgumentTypeError):
+        cli.parse_extents("", 2)
+    for bad in ("abc", ",24", "24,,8", "99999999999999999999"):  # std::invalid_argument / out_of_range -> exit 1
+        with pytest.raises((ValueError, OverflowError)):
+            cli.parse_extents(bad, 2)
 
 
 def test_exit_codes_before_device_work(tmp_path, capsys):  # senskit_main.cpp:23-27
@@ -79,6 +87,8 @@ def test_exit_codes_before_device_work(tmp_path, capsys):  # senskit_main.cpp:23
     assert cli.main(["estimate", "--input", base, "--calib", "32", "--output", base + "o"]) == 5  # DimError
     assert cli.main(["estimate", "--input", base, "--calib", "8", "--preset", "nope",
                      "--output", base + "o"]) == 2
+    assert cli.main(["estimate", "--input", base, "--calib", "8,8,8", "--output", base + "o"]) == 2  # count
+    assert cli.main(["estimate", "--input", base, "--calib", "8,x", "--output", base + "o"]) == 1  # stoll
 
 
 def test_config_from_flags_mirrors_reference():  # senskit_main.cpp:54-76
