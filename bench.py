@@ -15,12 +15,20 @@ Legs:
             between steps by a 256 MiB write (untimed).
   e2e       the same call through the public C-ABI with pinned HOST buffers:
             calibration H2D + maps/lambda/mask D2H inside the timed region.
-  cpu_baseline  the FP64 oracle (C++ restatement of the reference, its own
-            std::thread parallel_for, single-threaded LAPACK eigensolve as the
-            reference's Eigen) on rank 0 at N=1, one full C2 pipeline.
-`--impl reference` times that oracle as the reference arm.
+  cpu_baseline  the reference's own CPU implementation on rank 0 at N=1, one
+            full pipeline: oracle/_ref (the unmodified reference sources
+            compiled against oracle/ref_shim, kind "reference"; its own
+            std::thread parallel_for, dense algebra single-threaded as the
+            reference's Eigen), or the FP64 restatement in oracle/ (kind
+            "port") where _ref was not built.
+`--impl reference` times the same CPU implementation as the reference arm.
+
+Inputs: every step (warm-up, timed, e2e) gets its own seeded calibration
+(phantom.generate_variants: same phantom and coils, a fresh noise draw per
+step), so no step re-solves the Gram the previous one saw.
 """
 import argparse
+import glob
 import json
 import os
 import subprocess
@@ -149,9 +157,20 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def cpu_impl():
+    """The reference's CPU implementation: oracle/_ref when it was built (the
+    reference itself), else the FP64 restatement.  Returns (module, kind)."""
+    from oracle import ref
+    if ref.available():
+        ref.lib()
+        return ref, "reference"
+    from oracle import oracle as O
+    return O, "port"
+
+
 def oracle_run(case, threads=None):
     """One full reference-algorithm pipeline on the host (the CPU baseline)."""
-    from oracle import oracle as O
+    O, _ = cpu_impl()
     spec = case.spec
     if threads:
         O.set_max_threads(threads)
@@ -176,16 +195,20 @@ def reference_arm(args, spec, rank, world):
         return
     # bounded sample: one full pipeline per step (one slice for multislice
     # configs, voxels/s extrapolated); at most 2 steps so the arm ends in minutes
-    case = phantom.generate(args.config, seed=args.seed, slices=1 if spec.slices > 1 else None)
-    steps = max(1, min(args.steps, 2))
-    warm = min(args.warmup, 0)
-    for _ in range(warm):
-        oracle_run(case)
+    # (one full pipeline per step, C3: one slice; at most 1 warm-up + 3 timed
+    # steps so the arm ends within minutes); each step its own input variant.
+    steps = max(1, min(args.steps, 3))
+    warm = min(args.warmup, 1)
+    var = phantom.generate_variants(args.config, warm + steps, seed=args.seed,
+                                    slice_range=(0, 1) if spec.slices > 1 else None)
+    _, kind = cpu_impl()
     times = []
     threads = None
-    for _ in range(steps):
-        dt, _, threads = oracle_run(case)
-        times.append(dt)
+    for i in range(warm + steps):
+        one = phantom.Case(spec, var.calib[i], var.center_offset)
+        dt, _, threads = oracle_run(one)
+        if i >= warm:
+            times.append(dt)
     t = float(np.mean(times))
     vox = output_voxels(spec) // spec.slices
     value = vox / t
@@ -194,9 +217,12 @@ def reference_arm(args, spec, rank, world):
         "warmup": warm, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "c128 (fp64 complex)", "data": "synthetic (seeded phantom/coil generator, paper_2302_13431_b200/phantom.py)",
         "config": {"workload": workload(spec)},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{steps} full {args.config} pipeline(s) ({vox} output voxels each); parallel_for on "
-                                   f"{threads} threads, LAPACK zheevd/zgemm single-threaded as the reference's Eigen"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{steps} full {args.config} pipeline(s) ({vox} output voxels each, "
+                                   f"{'one slice of ' + str(spec.slices) + ', voxels/s per slice' if spec.slices > 1 else 'whole job'}) "
+                                   f"after {warm} warm-up; " + ("oracle/_ref = the reference's own sources" if kind == "reference"
+                                                                else "oracle/ FP64 restatement") +
+                                   f"; parallel_for on {threads} threads, dense algebra single-threaded as the reference's Eigen"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -212,7 +238,8 @@ def zslab_arm(args, spec, rank, world, local, dist):
     import torch
     import paper_2302_13431_b200 as K
     from paper_2302_13431_b200 import phantom, shard
-    case = phantom.generate(args.config, seed=args.seed)  # the same volume on every rank
+    nvar = max(1, min(args.warmup + args.steps, 16))
+    case = phantom.generate_variants(args.config, nvar, seed=args.seed)  # the same volumes on every rank
     full = spec.full_dims
     cfg = K.PipelineConfig(kernel=spec.kernel, tau=spec.tau, nullspace_threshold=spec.nullspace_threshold,
                            power_iters=spec.power_iters, grid=K.GRID_REDUCED,
@@ -221,12 +248,15 @@ def zslab_arm(args, spec, rank, world, local, dist):
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     dev = torch.device("cuda", local)
-    d_calib = K.Calib(torch.from_numpy(case.calib[0]).to(dev), case.center_offset)
+    d_calibs = [K.Calib(torch.from_numpy(case.calib[v, 0]).to(dev), case.center_offset) for v in range(nvar)]
     ops = shard.DeviceOps(ctx, dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    counter = {"i": 0}
 
     def step():
-        return shard.estimate_maps_zslab(d_calib, full, cfg, ops, gather_maps=False)
+        v = counter["i"] % nvar
+        counter["i"] += 1
+        return shard.estimate_maps_zslab(d_calibs[v], full, cfg, ops, gather_maps=False)
 
     def timed(fn, k, host=False):
         total = 0.0
@@ -237,7 +267,9 @@ def zslab_arm(args, spec, rank, world, local, dist):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             if host:
-                cal = K.Calib(torch.from_numpy(case.calib[0]).pin_memory().to(dev, non_blocking=True),
+                v = counter["i"] % nvar
+                counter["i"] += 1
+                cal = K.Calib(torch.from_numpy(case.calib[v, 0]).pin_memory().to(dev, non_blocking=True),
                               case.center_offset)
                 maps, lam, mask, _ = shard.estimate_maps_zslab(cal, full, cfg, ops, gather_maps=False)
                 maps.cpu(), lam.cpu(), mask.cpu()
@@ -275,7 +307,7 @@ def zslab_arm(args, spec, rank, world, local, dist):
         "config": {"workload": workload(spec), "parallelism": f"z-slab x{world} (NCCL all-gather + all-reduce)",
                    "l2": "flushed between steps (256 MiB write, untimed)"},
         "e2e": {"value": vox / (e2e_ms / e2e_steps / 1e3), "unit": UNIT,
-                "h2d_bytes_per_step": int(case.calib[0].size * 8),
+                "h2d_bytes_per_step": int(case.calib[0, 0].size * 8),
                 "d2h_bytes_per_step": int((own[1] - own[0]) * int(np.prod(full)) * 8 + int(np.prod(full)) * 5)},
         "gpu_launches": int(launches), "library_calls": int(libcalls), "clocks": clk,
     }
@@ -309,13 +341,15 @@ def main():
         zslab_arm(args, spec, rank, world, local, dist)
         return
     sharded = spec.slices > 1
+    nvar = max(1, min(args.warmup + args.steps, 16))  # distinct inputs, cycled if K + W > 16
     if sharded:
         # multislice: contiguous slice blocks per rank, strong scaling
         block = shard.partition(spec.slices, world, rank)
-        case = phantom.generate(args.config, seed=args.seed, slice_range=block)
+        var = phantom.generate_variants(args.config, nvar, seed=args.seed, slice_range=block)
     else:
         # single slice: independent replicas, weak scaling
-        case = phantom.generate(args.config, seed=args.seed + rank)
+        var = phantom.generate_variants(args.config, nvar, seed=args.seed + rank)
+    case = phantom.Case(spec, var.calib[0], var.center_offset)
     q = spec.channels
     full = spec.full_dims
     nfull = int(np.prod(full))
@@ -328,22 +362,27 @@ def main():
     ctx.set_stream(stream.cuda_stream)
 
     slices = case.calib.shape[0]
-    d_cal = torch.from_numpy(case.calib).to("cuda")
+    d_var = torch.from_numpy(var.calib).to("cuda")  # (nvar, S, Q, *E)
     d_maps = torch.empty((slices, q) + tuple(full), dtype=torch.complex64, device="cuda")
     d_lam = torch.empty((slices,) + tuple(full), dtype=torch.float32, device="cuda")
     d_mask = torch.empty((slices,) + tuple(full), dtype=torch.uint8, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    cal_stride = d_cal[0].numel() * 8
+    cal_stride = d_var[0, 0].numel() * 8
+    counter = {"i": 0}
 
-    def step_device():
-        if sharded:  # all local slices in one call (concurrent lanes inside the library)
-            return K.api.estimate_maps_batched_device(ctx, d_cal.data_ptr(), slices, spec.calib, case.center_offset,
+    def step_device(v=None, sequential=False):
+        if v is None:
+            v = counter["i"] % nvar
+            counter["i"] += 1
+        base = d_var[v].data_ptr()
+        if sharded and not sequential:  # all local slices in one call (concurrent lanes inside the library)
+            return K.api.estimate_maps_batched_device(ctx, base, slices, spec.calib, case.center_offset,
                                                       q, full, cfg, d_maps.data_ptr(), d_lam.data_ptr(),
                                                       d_mask.data_ptr())
         provs = []
         for s in range(slices):
             provs.append(K.api.estimate_maps_device(
-                ctx, d_cal.data_ptr() + s * cal_stride, spec.calib, case.center_offset, q, full, cfg,
+                ctx, base + s * cal_stride, spec.calib, case.center_offset, q, full, cfg,
                 d_maps[s].data_ptr(), d_lam[s].data_ptr(), d_mask[s].data_ptr()))
         return provs
 
@@ -389,24 +428,36 @@ def main():
     # all ranks' output voxels: sharded -> the whole volume once; replicas -> one volume per rank
     vox = output_voxels(spec) if sharded else output_voxels(spec) * world
     value = vox / (ms_per_step / 1e3)
+    stage_note = "per-step device stage times of the timed steps (library CUDA events)"
+    if sharded:
+        # the batched call runs slices on concurrent lanes, so its per-slice stage
+        # times overlap: take the stage split from one sequential (untimed) pass
+        _, stages = timed(lambda: step_device(0, sequential=True), 1, flush_l2=False)
+        stage_note = ("sum over this rank's slices of one sequential, untimed pass (slice by slice; the timed "
+                      "batched call overlaps slices on concurrent lanes)")
 
     # ---- e2e through the public API with pinned host buffers (one slice-sized
     # output buffer reused per slice; every slice's result is read back)
-    h_cal = torch.from_numpy(case.calib).pin_memory()
+    h_var = torch.from_numpy(var.calib).pin_memory()
     hs = slices if sharded else 1
     h_maps = torch.empty((hs, q) + tuple(full), dtype=torch.complex64).pin_memory()
     h_lam = torch.empty((hs,) + tuple(full), dtype=torch.float32).pin_memory()
     h_mask = torch.empty((hs,) + tuple(full), dtype=torch.uint8).pin_memory()
+    hcount = {"i": 0}
 
     def step_host():
+        v = hcount["i"] % nvar
+        hcount["i"] += 1
+        hcount["last"] = v
+        base = h_var[v].data_ptr()
         if sharded:
-            return K.api.estimate_maps_batched_device(ctx, h_cal.data_ptr(), slices, spec.calib, case.center_offset,
+            return K.api.estimate_maps_batched_device(ctx, base, slices, spec.calib, case.center_offset,
                                                       q, full, cfg, h_maps.data_ptr(), h_lam.data_ptr(),
                                                       h_mask.data_ptr())
         provs = []
         for s in range(slices):
             provs.append(K.api.estimate_maps_device(
-                ctx, h_cal.data_ptr() + s * cal_stride, spec.calib, case.center_offset, q, full, cfg,
+                ctx, base + s * cal_stride, spec.calib, case.center_offset, q, full, cfg,
                 h_maps.data_ptr(), h_lam.data_ptr(), h_mask.data_ptr()))
         return provs
 
@@ -418,6 +469,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_value = vox / (e2e_ms / e2e_steps / 1e3)
+    step_device(hcount["last"])  # the same input through the device leg: the legs must agree
+    torch.cuda.synchronize()
     assert np.array_equal(h_mask[hs - 1].numpy(), d_mask[slices - 1].cpu().numpy()), "host/device legs disagree"
 
     peaks, peak_src = load_peaks()
@@ -426,13 +479,16 @@ def main():
     k4_ms = stages[3]
     k4_work = k4_flops(spec) * slices
     achieved = k4_work / (k4_ms / 1e3) / 1e12 if k4_ms > 0 else 0.0
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
-    if os.path.exists(prof):
+    traffic, traffic_src = None, None
+    for prof in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_summary_r*.json")), reverse=True):
         try:
             traffic = json.load(open(prof)).get("power_kernel", {}).get(args.config, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+        if traffic:
+            traffic_src = (f"ncu --set full capture ({os.path.relpath(prof, ROOT)}): dram__bytes_read.sum + "
+                           "dram__bytes_write.sum per launch; profile-derived, not measured in this run")
+            break
 
     # per-stage roofline fractions (stage device time from the library's CUDA events)
     sup = K.make_support(spec.kernel, spec.tau, spec.ndim).shape[0]
@@ -465,11 +521,14 @@ def main():
                    "parallelism": (f"slice-sharded x{world}" if sharded else f"replicas x{world}") if world > 1
                    else "single GPU",
                    "l2": "flushed between steps (256 MiB write, untimed)",
+                   "inputs": f"{nvar} distinct seeded calibrations (fresh noise per step), cycled",
                    "output_voxels_per_rank": output_voxels(spec) // spec.slices * slices},
+        "stages_note": stage_note,
         "stages_ms": dict(zip(("gram", "nullspace", "field", "eigensolve", "post"), [round(x, 4) for x in stages])),
         "stages_roofline": stage_roof,
         "roofline": {"kernel": "power_kernel (K4)", "bound": "fp32", "achieved": achieved, "peak": fp32_peak,
                      "unit": "TFLOP/s", "frac": achieved / fp32_peak if fp32_peak else None, "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "peak_source": f"SMs x 128 FP32 lanes x 2 x sm_max_mhz ({peak_src} MEASURED_PEAKS sm_max_mhz)",
                      "flops_per_launch": k4_flops(spec)},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h_cal.numel() * 8),
@@ -481,10 +540,10 @@ def main():
         one = phantom.Case(spec, case.calib[:1], case.center_offset) if sharded else case
         dt, _, threads = oracle_run(one)
         per = output_voxels(spec) // spec.slices
-        line["cpu_baseline"] = {"value": per / dt, "unit": UNIT, "cores": threads, "kind": "port",
+        line["cpu_baseline"] = {"value": per / dt, "unit": UNIT, "cores": threads, "kind": cpu_impl()[1],
                                 "sample": (f"one full {args.config} slice pipeline ({per} voxels, {dt:.1f} s)"
                                            + (f"; voxels/s extrapolated to {spec.slices} slices" if sharded else "")
-                                           + "; LAPACK single-threaded as the reference's Eigen")}
+                                           + "; dense algebra single-threaded as the reference's Eigen")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -218,3 +218,25 @@ def generate(name: str, seed: int = 1234, with_kspace: bool = False, slices: int
     co = tuple(e // 2 for e in spec.calib)
     return Case(spec, np.stack(calibs), co, np.stack(kss) if with_kspace else None,
                 np.stack(tms) if with_kspace else None)
+
+
+def generate_variants(name: str, count: int, seed: int = 1234, slice_range=None) -> Case:
+    """`count` distinct inputs of config `name` for the bench's timed steps:
+    variant 0 is exactly generate(name, seed, slice_range=...); variant v >= 1
+    keeps each slice's phantom and coils and draws a fresh noise realisation
+    from the stream (seed, slice, v), so every step sees a different Gram.
+    Returns a Case whose calib is (count, S, Q, *E) complex64."""
+    spec = CONFIGS[name]
+    dims = spec.full_dims
+    start, stop = slice_range if slice_range is not None else (0, spec.slices)
+    out = np.empty((count, stop - start, spec.channels) + tuple(spec.calib), dtype=np.complex64)
+    for i, s in enumerate(range(start, stop)):
+        rng = np.random.Generator(np.random.PCG64([seed, s]))
+        z = (s - spec.slices // 2) / spec.slices if spec.slices > 1 else 0.0
+        img = coil_maps(spec, dims, z_slice=z) * phantom(dims, rng)[None]
+        sigma = np.sqrt(np.mean(np.abs(img) ** 2) / (2.0 * 10.0 ** (spec.snr_db / 10.0)))
+        clean = _partial_dft(img, spec.calib)
+        for v in range(count):
+            r = rng if v == 0 else np.random.Generator(np.random.PCG64([seed, s, v]))
+            out[v, i] = clean + sigma * (r.standard_normal(clean.shape) + 1j * r.standard_normal(clean.shape))
+    return Case(spec, out, tuple(e // 2 for e in spec.calib))
