@@ -197,6 +197,24 @@ int sk_projection_residual(sk_ctx* ctx, int ndim, const int64_t* dims, int64_t c
 int sk_estimate_raw_slab(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset,
                          int64_t channels, const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg,
                          int64_t slab_begin, int64_t slab_end, sk_c64* maps, float* lambda, sk_provenance* prov);
+
+/* Multi-GPU z-slab sharding with one exchange step (north_star:
+ * "broadcast the shared nullspace filters").  sk_signal_basis runs
+ * compute_gram + extract_nullspace (maps.cpp:180-186, nullspace.cpp:7-35) and
+ * returns the nullspace in its complement form: the k = n - R signal
+ * eigenvectors U_sig (n x k column-major, interleaved complex128; W = F F^H =
+ * I - U_sig U_sig^H), plus R, sigma_1 and the cut margin.  u_sig holds
+ * n * kmax values (host or device); if k > kmax the call fails with
+ * SK_ERR_DIM after setting *k.  sk_estimate_raw_slab_basis is
+ * sk_estimate_raw_slab with that basis supplied (K1 and K2 skipped), so every
+ * rank expands the SAME filters the root broadcast. */
+int sk_signal_basis(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset,
+                    int64_t channels, const sk_c64* calib, const sk_config* cfg, int64_t kmax, double* u_sig,
+                    int64_t* k, int64_t* rank, double* sigma1, double* cut_margin);
+int sk_estimate_raw_slab_basis(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset,
+                               int64_t channels, const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg,
+                               const double* u_sig, int64_t k, double sigma1, int64_t slab_begin, int64_t slab_end,
+                               sk_c64* maps, float* lambda, sk_provenance* prov);
 /* Renormalisation after interpolation (maps.cpp:236-258) split over channel
  * subsets: sos[j] += sum_c |maps[c][j]|^2; then maps[c][j] /= sqrt(sos[j])
  * where sos[j] > 0, with sos the sum over all subsets (an all-reduce). */

@@ -193,6 +193,9 @@ _SIGS = {
                                 _VP, _VP], _I32),
     "sk_estimate_maps_probe": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _VP, _VP,
                                 _I64, _VP, _VP, _VP, _VP], _I32),
+    "sk_signal_basis": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP], _I32),
+    "sk_estimate_raw_slab_basis": ([_VP, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _I64, _D, _I64, _I64, _VP, _VP,
+                                    _VP], _I32),
     "sk_estimate_maps_batched": ([_VP, _I64, _I32, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP], _I32),
 }
 
@@ -609,6 +612,35 @@ def estimate_raw_slab_device(ctx: Context, calib_ptr: int, calib_dims, center_of
     _check(lib().sk_estimate_raw_slab(ctx.handle, len(calib_dims), _p(_i64(calib_dims)), _p(_i64(center_offset)), q,
                                       C.c_void_p(calib_ptr), _p(_i64(full_dims)), C.byref(cfgc), int(slab[0]),
                                       int(slab[1]), C.c_void_p(maps_ptr), C.c_void_p(lambda_ptr), C.byref(prov)))
+    return prov
+
+
+def signal_basis_device(ctx: Context, calib_ptr: int, calib_dims, center_offset, q: int, cfg: PipelineConfig,
+                        u_ptr: int, kmax: int) -> dict:
+    """compute_gram + extract_nullspace in complement form (sk_signal_basis): the
+    k signal eigenvectors U_sig (n x k complex128, column-major) written to u_ptr
+    (capacity n * kmax), plus k, R, sigma_1 and the cut margin."""
+    k, r = C.c_int64(0), C.c_int64(0)
+    s1, margin = C.c_double(0), C.c_double(0)
+    cfgc = cfg.to_c()
+    _check(lib().sk_signal_basis(ctx.handle, len(calib_dims), _p(_i64(calib_dims)), _p(_i64(center_offset)), q,
+                                 C.c_void_p(calib_ptr), C.byref(cfgc), int(kmax), C.c_void_p(u_ptr), C.byref(k),
+                                 C.byref(r), C.byref(s1), C.byref(margin)))
+    return {"k": k.value, "rank": r.value, "sigma1": s1.value, "cut_margin": margin.value}
+
+
+def estimate_raw_slab_basis_device(ctx: Context, calib_ptr: int, calib_dims, center_offset, q: int, full_dims,
+                                   cfg: PipelineConfig, u_ptr: int, k: int, sigma1: float, slab, maps_ptr: int,
+                                   lambda_ptr: int) -> sk_provenance:
+    """estimate_raw_slab with a supplied signal basis (sk_estimate_raw_slab_basis):
+    K1 and K2 skipped, so every rank expands the broadcast filters."""
+    prov = sk_provenance()
+    cfgc = cfg.to_c()
+    _check(lib().sk_estimate_raw_slab_basis(ctx.handle, len(calib_dims), _p(_i64(calib_dims)),
+                                            _p(_i64(center_offset)), q, C.c_void_p(calib_ptr), _p(_i64(full_dims)),
+                                            C.byref(cfgc), C.c_void_p(u_ptr), int(k), float(sigma1), int(slab[0]),
+                                            int(slab[1]), C.c_void_p(maps_ptr), C.c_void_p(lambda_ptr),
+                                            C.byref(prov)))
     return prov
 
 

@@ -10,9 +10,10 @@
 //
 // On the pipeline path W is never formed from the R ~ n nullspace filters:
 // with a complete orthonormal eigenbasis W = F F^H = I - U_sig U_sig^H, where
-// U_sig holds the n - R ~ 17-48 signal eigenvectors.  The
-// caller passes Ws = U_sig U_sig^H (lower triangle, FP64, from cuBLAS ZHERK)
-// and the identity is folded in analytically.
+// U_sig holds the n - R ~ 17-59 signal eigenvectors, folded
+// by the correlation theorem below (fold_lags_spectral).  The CSR kernels
+// serve the standalone gram_field_fast (caller-supplied W) and the fallback
+// for lag boxes whose spectral buffers exceed shared memory (Ws = U U^H).
 #include "sk_internal.h"
 
 namespace skb {
@@ -69,77 +70,225 @@ __global__ void __launch_bounds__(256) fold_f32_kernel(const float2* __restrict_
   }
 }
 
-// Fold straight from the signal basis (no n x n Ws): per pair (p, q) the
-// block M[s][t] = sum_k U[q|L|+s, k] conj(U[p|L|+t, k]) is formed in shared
-// memory by 4 x 4 register tiles (FP64, U read through L1), then every lag
-// sums its (s, t) list from M in list order (deterministic, like the Ws path):
-//   k_pq[l] = sum_{(s,t) in L(l)} (delta_{(q,s),(p,t)} - M[s][t]).
-constexpr int kFoldT = 4;  // tile edge
-__global__ void __launch_bounds__(256) fold_from_u_kernel(const double2* __restrict__ u, i64 n, int k, int lam,
-                                                          int nbox, const int2* __restrict__ pairs,
-                                                          const int* __restrict__ ptr, const int* __restrict__ st,
-                                                          double2* __restrict__ lags) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* M = reinterpret_cast<double2*>(smem_raw);  // [lam][lam + 1]
-  const int ldm = lam + 1;
-  const int2 pq = pairs[blockIdx.x];
-  const int p = pq.x, q = pq.y;
-  const double2* uq = u + i64(q) * lam;
-  const double2* up = u + i64(p) * lam;
-  const int nt = (lam + kFoldT - 1) / kFoldT;
-  for (int tile = threadIdx.x; tile < nt * nt; tile += blockDim.x) {
-    const int s0 = (tile / nt) * kFoldT, t0 = (tile % nt) * kFoldT;
-    double2 acc[kFoldT][kFoldT];
-#pragma unroll
-    for (int a = 0; a < kFoldT; ++a)
-#pragma unroll
-      for (int b = 0; b < kFoldT; ++b) acc[a][b] = make_double2(0.0, 0.0);
-    for (int kk = 0; kk < k; ++kk) {
-      double2 x[kFoldT], y[kFoldT];
-#pragma unroll
-      for (int a = 0; a < kFoldT; ++a) {
-        x[a] = s0 + a < lam ? uq[s0 + a + i64(kk) * n] : make_double2(0.0, 0.0);
-        y[a] = t0 + a < lam ? up[t0 + a + i64(kk) * n] : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int a = 0; a < kFoldT; ++a)
-#pragma unroll
-        for (int b = 0; b < kFoldT; ++b) {  // acc += x conj(y)
-          acc[a][b].x = fma(x[a].x, y[b].x, fma(x[a].y, y[b].y, acc[a][b].x));
-          acc[a][b].y = fma(x[a].y, y[b].x, fma(-x[a].x, y[b].y, acc[a][b].y));
-        }
+}  // namespace
+
+// ---------------------------------------------------------------- spectral fold
+// The signal part of the fold is a sum of cross-correlations on the support
+// lattice: with W = I - U U^H (U = U_sig, n x k),
+//   k_pq[d] = |L| delta_pq [d = 0] - sum_kk sum_{(s,t): n_t - n_s = d} U_q[s,kk] conj(U_p[t,kk]).
+// On the lag box (P = 4 tau + 1 per axis, so every lag d in [-2tau, 2tau]^D
+// has a unique residue mod P) the correlation theorem gives
+//   c_pq(d) = P^-D sum_f S_pq(f) e^{-2 pi i f.d / P},
+//   S_pq(f) = sum_kk a_q^kk(f) conj(a_p^kk(f)),  a_q^kk(f) = sum_s U_q[s,kk] e^{-2 pi i f.n_s / P}.
+// Three FP64 kernels: (A) per (kk, q) the separable DFT of u_q^kk from its
+// (2 tau + 1)^D box to the P^D frequencies; (B) per frequency the Q x Q
+// Hermitian product over the k signal vectors (p <= q pairs only); (C) per
+// pair the separable inverse DFT back onto the lag box.  O(P^D (Q k (2tau+1) +
+// h k) + h P^{D+1}) flops instead of the n x n x k ZHERK + n^2 fold, no n x n
+// buffer, fixed-order sums (deterministic).
+namespace {
+
+// One axis of a separable DFT in shared memory: in has extents ext (nd <= 3,
+// row-major), out replaces axis `ax` (extent Lin) by Lout outputs:
+//   out[.., f, ..] = scale * sum_j in[.., j, ..] tw[((f * (j - j0)) mod P)]   (tw[m] = e^{sign 2 pi i m/P})
+__device__ void dft_axis(const double2* in, double2* out, const int* ext, int nd, int ax, int Lout, int j0,
+                         const double2* tw, int P, double scale) {
+  int outer = 1, inner = 1;
+  for (int a = 0; a < ax; ++a) outer *= ext[a];
+  for (int a = ax + 1; a < nd; ++a) inner *= ext[a];
+  const int Lin = ext[ax];
+  const int total = outer * Lout * inner;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int i = e % inner;
+    const int f = (e / inner) % Lout;
+    const int o = e / (inner * Lout);
+    const double2* src = in + i64(o) * Lin * inner + i;
+    double re = 0.0, im = 0.0;
+    for (int j = 0; j < Lin; ++j) {
+      int m = (f * (j - j0)) % P;
+      if (m < 0) m += P;
+      const double2 v = src[i64(j) * inner];
+      const double2 w = tw[m];
+      re += v.x * w.x - v.y * w.y;
+      im += v.x * w.y + v.y * w.x;
     }
-#pragma unroll
-    for (int a = 0; a < kFoldT; ++a)
-#pragma unroll
-      for (int b = 0; b < kFoldT; ++b)
-        if (s0 + a < lam && t0 + b < lam) M[(s0 + a) * ldm + t0 + b] = acc[a][b];
+    out[e] = make_double2(re * scale, im * scale);
+  }
+}
+
+__device__ void make_twiddles(double2* tw, int P, double sign) {
+  for (int m = threadIdx.x; m < P; m += blockDim.x) {
+    double sn, cs;
+    sincospi(sign * 2.0 * double(m) / double(P), &sn, &cs);
+    tw[m] = make_double2(cs, sn);
+  }
+}
+
+// (A) a[f][kk][q] = sum_s U[q lam + s, kk] e^{-2 pi i f.n_s / P}; block = (kk, q)
+__global__ void __launch_bounds__(256) spec_u_kernel(const double2* __restrict__ u, i64 n, int k, int q, int lam,
+                                                     const int* __restrict__ offs, int nd, int tau,
+                                                     double2* __restrict__ a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int P = 4 * tau + 1, B = 2 * tau + 1;
+  int nbox = 1, bbox = 1;
+  for (int d = 0; d < nd; ++d) {
+    nbox *= P;
+    bbox *= B;
+  }
+  double2* tw = reinterpret_cast<double2*>(smem_raw);
+  double2* buf0 = tw + P;
+  double2* buf1 = buf0 + nbox;
+  const int kk = blockIdx.x / q, ch = blockIdx.x % q;
+  make_twiddles(tw, P, -1.0);
+  for (int e = threadIdx.x; e < bbox; e += blockDim.x) buf0[e] = make_double2(0.0, 0.0);
+  __syncthreads();
+  const double2* col = u + i64(kk) * n + i64(ch) * lam;
+  for (int sidx = threadIdx.x; sidx < lam; sidx += blockDim.x) {
+    int at = 0;
+    for (int d = 0; d < nd; ++d) at = at * B + (offs[sidx * nd + d] + tau);
+    buf0[at] = col[sidx];
   }
   __syncthreads();
-  for (int l = threadIdx.x; l < nbox; l += blockDim.x) {
-    double re = 0.0, im = 0.0;
-    for (int e = ptr[l]; e < ptr[l + 1]; ++e) {
-      const int s = st[e] & 0xffff, t = st[e] >> 16;
-      const double2 v = M[s * ldm + t];
-      re -= v.x;
-      im -= v.y;
-      if (p == q && s == t) re += 1.0;
+  int ext[3] = {B, B, B};
+  double2* src = buf0;
+  double2* dst = buf1;
+  for (int ax = 0; ax < nd; ++ax) {
+    dft_axis(src, dst, ext, nd, ax, P, tau, tw, P, 1.0);  // box index j <-> n = j - tau
+    ext[ax] = P;
+    __syncthreads();
+    double2* t = src;
+    src = dst;
+    dst = t;
+  }
+  for (int f = threadIdx.x; f < nbox; f += blockDim.x) a[(i64(f) * k + kk) * q + ch] = src[f];
+}
+
+// (B) S[pair][f] = sum_kk a[f][kk][c] conj(a[f][kk][p]) for pair (p <= c); block = f
+__global__ void __launch_bounds__(256) spec_pairs_kernel(const double2* __restrict__ a, int k, int q, int nbox,
+                                                         double2* __restrict__ S) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* af = reinterpret_cast<double2*>(smem_raw);  // [k][q]
+  const int f = blockIdx.x;
+  for (int e = threadIdx.x; e < k * q; e += blockDim.x) af[e] = a[i64(f) * k * q + e];
+  __syncthreads();
+  const int h = q * (q + 1) / 2;
+  for (int pr = threadIdx.x; pr < h; pr += blockDim.x) {
+    int p = 0, rem = pr;
+    while (rem >= q - p) {
+      rem -= q - p;
+      ++p;
     }
-    lags[i64(blockIdx.x) * nbox + l] = make_double2(re, im);
+    const int c = p + rem;
+    double re = 0.0, im = 0.0;
+    for (int kk = 0; kk < k; ++kk) {
+      const double2 x = af[kk * q + c], y = af[kk * q + p];  // x conj(y)
+      re += x.x * y.x + x.y * y.y;
+      im += x.y * y.x - x.x * y.y;
+    }
+    S[i64(pr) * nbox + f] = make_double2(re, im);
+  }
+}
+
+// (C) lags[pair][l] = |L| delta_pc [l = centre] - P^-D sum_f S[pair][f] e^{-2 pi i f.d / P}; block = pair
+__global__ void __launch_bounds__(256) spec_lags_kernel(const double2* __restrict__ S, int q, int nd, int tau, int lam,
+                                                        double2* __restrict__ lags) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int P = 4 * tau + 1;
+  int nbox = 1;
+  for (int d = 0; d < nd; ++d) nbox *= P;
+  double2* tw = reinterpret_cast<double2*>(smem_raw);
+  double2* buf0 = tw + P;
+  double2* buf1 = buf0 + nbox;
+  const int pr = blockIdx.x;
+  make_twiddles(tw, P, -1.0);
+  for (int e = threadIdx.x; e < nbox; e += blockDim.x) buf0[e] = S[i64(pr) * nbox + e];
+  __syncthreads();
+  int ext[3] = {P, P, P};
+  double2* src = buf0;
+  double2* dst = buf1;
+  // frequency f = 0..P-1 in, lag index j = 0..P-1 out with d = j - 2 tau:
+  // e^{-2 pi i f d / P}; dft_axis evaluates tw[(f' (j' - j0))] with the roles
+  // of input / output index swapped, so pass j0 = 0 and fold the shift into
+  // the output index through (j - 2tau) * f = f * j - f * 2tau (mod P).
+  for (int ax = 0; ax < nd; ++ax) {
+    int outer = 1, inner = 1;
+    for (int a = 0; a < ax; ++a) outer *= ext[a];
+    for (int a = ax + 1; a < nd; ++a) inner *= ext[a];
+    const int total = outer * P * inner;
+    const double scale = 1.0 / double(P);
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+      const int i = e % inner;
+      const int j = (e / inner) % P;
+      const int o = e / (inner * P);
+      const double2* sp = src + i64(o) * P * inner + i;
+      const int d = j - 2 * tau;
+      double re = 0.0, im = 0.0;
+      for (int ff = 0; ff < P; ++ff) {
+        int m = (ff * d) % P;
+        if (m < 0) m += P;
+        const double2 v = sp[i64(ff) * inner];
+        const double2 w = tw[m];
+        re += v.x * w.x - v.y * w.y;
+        im += v.x * w.y + v.y * w.x;
+      }
+      dst[e] = make_double2(re * scale, im * scale);
+    }
+    __syncthreads();
+    double2* t = src;
+    src = dst;
+    dst = t;
+  }
+  int p = 0, rem = pr;
+  while (rem >= q - p) {
+    rem -= q - p;
+    ++p;
+  }
+  const bool diag = rem == 0;
+  const int centre = (nbox - 1) / 2;
+  for (int l = threadIdx.x; l < nbox; l += blockDim.x) {
+    double2 v = src[l];
+    v.x = -v.x;
+    v.y = -v.y;
+    if (diag && l == centre) v.x += double(lam);
+    lags[i64(pr) * nbox + l] = v;
   }
 }
 
 }  // namespace
 
-size_t fold_from_u_smem(int lam) { return size_t(lam) * (lam + 1) * sizeof(double2); }
+size_t spectral_fold_smem(int nd, int tau, int k, int q) {
+  const int P = 4 * tau + 1;
+  size_t nbox = 1;
+  for (int d = 0; d < nd; ++d) nbox *= size_t(P);
+  const size_t box = (size_t(P) + 2 * nbox) * sizeof(double2);
+  return std::max(box, size_t(k) * size_t(q) * sizeof(double2));
+}
 
-void fold_lags_from_u(sk_ctx* ctx, const double2* u, i64 n, int k, int npairs, int lam, int nbox,
-                      const int2* d_pairs, const int* d_lag_ptr, const int* d_lag_st, double2* lags) {
-  const size_t smem = fold_from_u_smem(lam);
-  set_smem_limit(reinterpret_cast<const void*>(fold_from_u_kernel), smem);
-  fold_from_u_kernel<<<npairs, 256, smem, ctx->stream>>>(u, n, k, lam, nbox, d_pairs, d_lag_ptr, d_lag_st, lags);
+void fold_lags_spectral(sk_ctx* ctx, const double2* u, i64 n, int k, int q, int lam, int nd, int tau,
+                        const int* d_offs, double2* lags) {
+  const int P = 4 * tau + 1;
+  int nbox = 1;
+  for (int d = 0; d < nd; ++d) nbox *= P;
+  const int h = q * (q + 1) / 2;
+  const size_t box_smem = (size_t(P) + 2 * size_t(nbox)) * sizeof(double2);
+  double2* S = ctx->arena.get<double2>("field:spec_S", i64(h) * nbox);
+  if (k > 0) {
+    double2* a = ctx->arena.get<double2>("field:spec_a", i64(nbox) * k * q);
+    set_smem_limit(reinterpret_cast<const void*>(spec_u_kernel), box_smem);
+    spec_u_kernel<<<k * q, 256, box_smem, ctx->stream>>>(u, n, k, q, lam, d_offs, nd, tau, a);
+    SKB_LAUNCH("spec_u_kernel");
+    const size_t ps = size_t(k) * q * sizeof(double2);
+    set_smem_limit(reinterpret_cast<const void*>(spec_pairs_kernel), ps);
+    spec_pairs_kernel<<<nbox, 256, ps, ctx->stream>>>(a, k, q, nbox, S);
+    SKB_LAUNCH("spec_pairs_kernel");
+    ctx->launches += 2;
+  } else {
+    SKB_CUDA(cudaMemsetAsync(S, 0, size_t(h) * nbox * sizeof(double2), ctx->stream));
+  }
+  set_smem_limit(reinterpret_cast<const void*>(spec_lags_kernel), box_smem);
+  spec_lags_kernel<<<h, 256, box_smem, ctx->stream>>>(S, q, nd, tau, lam, lags);
+  SKB_LAUNCH("spec_lags_kernel");
   ++ctx->launches;
-  SKB_LAUNCH("fold_from_u_kernel");
 }
 
 void fold_lags_f64(sk_ctx* ctx, const double2* w, i64 n, int npairs, int lam, int nbox, const int2* d_pairs,
@@ -157,6 +306,82 @@ void fold_lags_f32(sk_ctx* ctx, const float2* w, i64 n, int npairs, int lam, int
   fold_f32_kernel<<<npairs, 256, 0, ctx->stream>>>(w, n, lam, nbox, d_pairs, d_lag_ptr, d_lag_st, lags);
   ++ctx->launches;
   SKB_LAUNCH("fold_f32_kernel");
+}
+
+}  // namespace skb
+
+namespace skb {
+
+// ---------------------------------------------------------------- aggregate_w
+// Standalone aggregate_w (spatial_gram.cpp:87-94): W = F F^H for the n x r
+// nullspace filters F (c64, column-major).  W is Hermitian: only tiles on or
+// below the diagonal are computed (64 x 64 per CTA, 4 x 4 complex outputs per
+// thread, FP32 accumulation over r in 16-column slabs staged in shared
+// memory); each tile is stored with its conjugate mirror.
+namespace {
+constexpr int kHT = 64;  // output tile edge
+constexpr int kHK = 16;  // r slab
+__global__ void __launch_bounds__(256) herk_tiles_kernel(const float2* __restrict__ f, i64 n, i64 r,
+                                                         float2* __restrict__ w) {
+  // blockIdx.x enumerates lower-triangular tiles (bi >= bj)
+  int bi = 0, rem = int(blockIdx.x);
+  while (rem > bi) {
+    rem -= bi + 1;
+    ++bi;
+  }
+  const int bj = rem;
+  __shared__ float2 As[kHK][kHT + 1];
+  __shared__ float2 Bs[kHK][kHT + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const i64 i0 = i64(bi) * kHT, j0 = i64(bj) * kHT;
+  float2 acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = make_float2(0.f, 0.f);
+  for (i64 k0 = 0; k0 < r; k0 += kHK) {
+    for (int e = threadIdx.x; e < kHT * kHK; e += blockDim.x) {
+      const int row = e % kHT, kk = e / kHT;
+      const i64 kc = k0 + kk;
+      As[kk][row] = (i0 + row < n && kc < r) ? f[(i0 + row) + kc * n] : make_float2(0.f, 0.f);
+      Bs[kk][row] = (j0 + row < n && kc < r) ? f[(j0 + row) + kc * n] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kHK; ++kk) {
+      float2 x[4], y[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        x[a] = As[kk][ty + 16 * a];
+        y[a] = Bs[kk][tx + 16 * a];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {  // acc += x conj(y)
+          acc[a][b].x = fmaf(x[a].x, y[b].x, fmaf(x[a].y, y[b].y, acc[a][b].x));
+          acc[a][b].y = fmaf(x[a].y, y[b].x, fmaf(-x[a].x, y[b].y, acc[a][b].y));
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const i64 i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
+      if (i >= n || j >= n || i < j) continue;
+      w[i + j * n] = i == j ? make_float2(acc[a][b].x, 0.f) : acc[a][b];  // Hermitian: real diagonal
+      if (i != j) w[j + i * n] = make_float2(acc[a][b].x, -acc[a][b].y);
+    }
+}
+}  // namespace
+
+void herk_full(sk_ctx* ctx, const float2* f, i64 n, i64 r, float2* w) {
+  const i64 nt = (n + kHT - 1) / kHT;
+  herk_tiles_kernel<<<unsigned(nt * (nt + 1) / 2), 256, 0, ctx->stream>>>(f, n, r, w);
+  ++ctx->launches;
+  SKB_LAUNCH("herk_tiles_kernel");
 }
 
 }  // namespace skb

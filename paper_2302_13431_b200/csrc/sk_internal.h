@@ -193,9 +193,12 @@ void fold_lags_f64(sk_ctx* ctx, const double2* w, i64 n, int npairs, int lam, in
                    const int* d_lag_ptr, const int* d_lag_st, bool w_is_signal, double2* lags);
 // Same fold for W = I - U U^H straight from the n x k signal basis U (no n x n
 // product); shared memory lam * (lam + 1) * 16 bytes per pair.
-size_t fold_from_u_smem(int lam);
-void fold_lags_from_u(sk_ctx* ctx, const double2* u, i64 n, int k, int npairs, int lam, int nbox,
-                      const int2* d_pairs, const int* d_lag_ptr, const int* d_lag_st, double2* lags);
+// W = F F^H (c64, n x r filters, both triangles written; standalone aggregate_w)
+void herk_full(sk_ctx* ctx, const float2* f, i64 n, i64 r, float2* w);
+// signal-space fold by the correlation theorem on the lag box (no n x n W, no library call)
+size_t spectral_fold_smem(int nd, int tau, int k, int q);
+void fold_lags_spectral(sk_ctx* ctx, const double2* u, i64 n, int k, int q, int lam, int nd, int tau,
+                        const int* d_offs, double2* lags);
 void fold_lags_f32(sk_ctx* ctx, const float2* w, i64 n, int npairs, int lam, int nbox, const int2* d_pairs,
                    const int* d_lag_ptr, const int* d_lag_st, double2* lags);
 // One FP64 stage of the G(x) lag expansion (sk_expand.cu): in [batch][2H+1][inner]

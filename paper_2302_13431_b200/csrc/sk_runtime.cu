@@ -1221,20 +1221,22 @@ Planes run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims&
   SupportTables& t = tables_for(ctx, s, q);
   const int h = q * (q + 1) / 2;
   double2* lags = ctx->arena.get<double2>("field:lags64", i64(h) * t.nbox);
-  // Fold straight from U when a pair block is small (<= 64 KB: C1, C3 0.122 -> 0.109 ms;
-  // C2 measured slower at 105 KB); otherwise Ws = U U^H by ZHERK and the fold reads it.
-  static const bool from_u = [] {
-    const char* v = std::getenv("SKB_FOLD_FROM_U");
-    return !v || std::atoi(v) != 0;
-  }();
-  if (from_u && k > 0 && fold_from_u_smem(lam) <= 64 * 1024) {
-    fold_lags_from_u(ctx, e.usig, n, int(k), h, lam, t.nbox, t.pairs, t.lag_ptr, t.lag_st, lags);
+  // aggregate_w + fold (spatial_gram.cpp:87-94, 108-131): W = I - U_sig U_sig^H
+  // folded onto the lag box by the correlation theorem (sk_fold.cu), own FP64
+  // kernels, no n x n buffer (C2 field 0.282 -> 0.239 ms against cuBLAS ZHERK +
+  // CSR fold, C5 3.59 -> 3.20 ms).  Lag boxes too large for its shared-memory
+  // buffers (3-D with tau > 4; no BASELINE config) keep the ZHERK path.
+  auto planes_for = [&]() {
     Planes p;
     const i64 nvox = slab1 >= 0 ? numel(grid) / grid[0] * (slab1 - slab0) : numel(grid);
     p.hi = ctx->arena.get<float2>("field:planes", i64(h) * nvox);
     p.lo = ctx->arena.get<float2>("field:planes_lo", i64(h) * nvox);
     expand_lags(ctx, lags, p.hi, p.lo, h, s.tau, grid, slab0, slab1);
     return p;
+  };
+  if (spectral_fold_smem(s.nd, s.tau, int(k), q) <= 200 * 1024) {
+    fold_lags_spectral(ctx, e.usig, n, int(k), q, lam, s.nd, s.tau, support_offsets_dev(ctx, s), lags);
+    return planes_for();
   }
   double2* ws = ctx->arena.get<double2>("field:Ws", n * n);
   if (k > 0) {
@@ -1248,12 +1250,7 @@ Planes run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims&
     SKB_CUDA(cudaMemsetAsync(ws, 0, size_t(n * n) * sizeof(double2), ctx->stream));
   }
   fold_lags_f64(ctx, ws, n, h, lam, t.nbox, t.pairs, t.lag_ptr, t.lag_st, true, lags);
-  Planes p;
-  const i64 nvox = slab1 >= 0 ? numel(grid) / grid[0] * (slab1 - slab0) : numel(grid);
-  p.hi = ctx->arena.get<float2>("field:planes", i64(h) * nvox);
-  p.lo = ctx->arena.get<float2>("field:planes_lo", i64(h) * nvox);
-  expand_lags(ctx, lags, p.hi, p.lo, h, s.tau, grid, slab0, slab1);
-  return p;
+  return planes_for();
 }
 
 // Lag kernels from a caller-supplied W (gram_field_fast entry point).
@@ -1419,6 +1416,15 @@ struct PipelineOut {
     double gram_sumsq = 0.0, field_sumsq = 0.0;
     float* raw_lambda = nullptr;           // device, N_grid
   }* probe = nullptr;
+  // Precomputed signal basis (z-slab ranks after the rank-0 broadcast,
+  // sk_estimate_raw_slab_basis): K1 and K2 are skipped.
+  struct Basis {
+    const double2* usig = nullptr;  // device, n x k
+    i64 k = 0;
+    double sigma1 = 0.0;
+  }* basis = nullptr;
+  // K1 + K2 only (sk_signal_basis): stop after the nullspace, hand the Eig out.
+  Eig* eig_out = nullptr;
 };
 
 // K4 epilogue: voxels with lambda >= this keep the FP32 Rayleigh quotient
@@ -1481,17 +1487,33 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   SKB_CUDA(cudaEventRecord(ev[0], ctx->stream));
   // gram
   // compute_gram (maps.cpp:180-186)
-  float2* gram = cfg->gram == 0 ? run_gram_explicit(ctx, cdims, q, calib, s, out.gram)
-                                : run_gram(ctx, cdims, q, calib, s, out.gram);
-  if (out.probe) {
-    probe_gather_gram(ctx, gram, q * s.count, out.probe->gram_idx, out.probe->n_gram, out.probe->gram_vals);
-    out.probe->gram_sumsq = probe_sumsq(ctx, gram, nullptr, q * s.count * q * s.count, 0, 0);
+  Eig e;
+  if (out.basis) {
+    SKB_CUDA(cudaEventRecord(ev[1], ctx->stream));
+    e.n = n;
+    e.k = out.basis->k;
+    e.rank = n - e.k;
+    e.usig = out.basis->usig;
+    e.sigma1 = out.basis->sigma1;
+    e.cut = cfg->nullspace_threshold * e.sigma1;
+    e.full = false;
+  } else {
+    float2* gram = cfg->gram == 0 ? run_gram_explicit(ctx, cdims, q, calib, s, out.gram)
+                                  : run_gram(ctx, cdims, q, calib, s, out.gram);
+    if (out.probe) {
+      probe_gather_gram(ctx, gram, q * s.count, out.probe->gram_idx, out.probe->n_gram, out.probe->gram_vals);
+      out.probe->gram_sumsq = probe_sumsq(ctx, gram, nullptr, q * s.count * q * s.count, 0, 0);
+    }
+    SKB_CUDA(cudaEventRecord(ev[1], ctx->stream));
+    // nullspace
+    e = run_nullspace(ctx, gram, n, cfg->nullspace_threshold, cfg->eig_solver, out.spectrum != nullptr,
+                      cfg->certify != 0);
   }
-  SKB_CUDA(cudaEventRecord(ev[1], ctx->stream));
-  // nullspace
-  Eig e = run_nullspace(ctx, gram, n, cfg->nullspace_threshold, cfg->eig_solver, out.spectrum != nullptr,
-                        cfg->certify != 0);
   SKB_CUDA(cudaEventRecord(ev[2], ctx->stream));
+  if (out.eig_out) {
+    *out.eig_out = e;
+    return;
+  }
   // field.  compute_field (maps.cpp:195-205): the naive path materialises the
   // R x Q x N filter field H (spatial_gram.cpp:36-64) and sums H^H H per voxel;
   // that is the same G(x) as the lag expansion of W = F F^H, so both paths
@@ -1890,12 +1912,7 @@ int sk_aggregate_w(sk_ctx* ctx, int64_t n, int64_t r, const sk_c64* filters, sk_
     if (r < 1) fail(SK_ERR_NULLSPACE_EMPTY, "aggregate requires at least one filter");  // spatial_gram.cpp:88
     const float2* d_f = device_in(ctx, reinterpret_cast<const float2*>(filters), n * r, "in:filters");
     Out<float2> o(ctx, reinterpret_cast<float2*>(w), n * n, "out:w");
-    const cuComplex one = make_cuComplex(1.f, 0.f), zero = make_cuComplex(0.f, 0.f);
-    check_cublas(cublasCgemm(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_C, int(n), int(n), int(r), &one,
-                             reinterpret_cast<const cuComplex*>(d_f), int(n), reinterpret_cast<const cuComplex*>(d_f),
-                             int(n), &zero, reinterpret_cast<cuComplex*>(o.dev), int(n)),
-                 "Cgemm");
-    ++ctx->lib_calls;
+    herk_full(ctx, d_f, n, r, o.dev);  // own tiled Hermitian product (sk_fold.cu)
     o.finish(ctx);
     SKB_CUDA(cudaStreamSynchronize(ctx->stream));
   });
@@ -2341,6 +2358,80 @@ int sk_estimate_raw_slab(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const
     Out<float2> om(ctx, reinterpret_cast<float2*>(maps), q * nvox, "out:slab_maps");
     Out<float> ol(ctx, lambda, nvox, "out:slab_lambda");
     PipelineOut po;
+    po.maps = om.dev ? om.dev : ctx->arena.get<float2>("out:slab_maps", q * nvox);
+    po.lambda = ol.dev ? ol.dev : ctx->arena.get<float>("out:slab_lambda", nvox);
+    po.slab0 = slab_begin;
+    po.slab1 = slab_end;
+    pipeline(ctx, cd, co, q, d_cal, fd, cfg, po, prov);
+    om.finish(ctx);
+    ol.finish(ctx);
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_signal_basis(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset, int64_t q,
+                    const sk_c64* calib, const sk_config* cfg, int64_t kmax, double* u_sig, int64_t* k,
+                    int64_t* rank, double* sigma1, double* cut_margin) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (ndim < 1 || !cfg) fail(SK_ERR_DIM, "bad arguments");
+    const Dims cd = dims_of(ndim, calib_dims), co = dims_of(ndim, center_offset);
+    for (i64 d : cd)
+      if (d < 1) fail(SK_ERR_DIM, "stack axis extents must be >= 1");
+    if (q < 1) fail(SK_ERR_DIM, "stack needs at least one channel");
+    const float2* d_cal = device_in(ctx, reinterpret_cast<const float2*>(calib), q * numel(cd), "in:calib");
+    PipelineOut po;
+    Eig e;
+    po.eig_out = &e;
+    sk_config c = *cfg;  // only K1 + K2 run: the map grid is irrelevant (full = calib dims)
+    c.grid = 0;
+    for (auto& g : c.grid_dims) g = 0;
+    pipeline(ctx, cd, co, q, d_cal, cd, &c, po, nullptr);
+    if (k) *k = e.k;
+    if (rank) *rank = e.rank;
+    if (sigma1) *sigma1 = e.sigma1;
+    if (cut_margin) *cut_margin = e.margin;
+    if (e.k > kmax) fail(SK_ERR_DIM, "signal basis has " + std::to_string(e.k) + " columns, capacity " +
+                                         std::to_string(kmax));
+    if (u_sig && e.k > 0)
+      SKB_CUDA(cudaMemcpyAsync(u_sig, e.usig, size_t(e.n * e.k) * sizeof(double2), cudaMemcpyDefault, ctx->stream));
+    SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int sk_estimate_raw_slab_basis(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset,
+                               int64_t q, const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg,
+                               const double* u_sig, int64_t k, double sigma1, int64_t slab_begin, int64_t slab_end,
+                               sk_c64* maps, float* lambda, sk_provenance* prov) {
+  return guarded([&] {
+    require_ctx(ctx);
+    if (ndim < 1 || !cfg) fail(SK_ERR_DIM, "bad arguments");
+    const Dims cd = dims_of(ndim, calib_dims), co = dims_of(ndim, center_offset), fd = dims_of(ndim, full_dims);
+    for (i64 d : cd)
+      if (d < 1) fail(SK_ERR_DIM, "stack axis extents must be >= 1");
+    if (q < 1) fail(SK_ERR_DIM, "stack needs at least one channel");
+    const Support s = make_support(cfg->kernel, cfg->tau, ndim);
+    const i64 n = q * s.count;
+    if (k < 0 || k > n) fail(SK_ERR_DIM, "signal basis column count out of range");
+    Dims grid(static_cast<size_t>(ndim));
+    bool ex = true;
+    for (int a = 0; a < ndim; ++a) ex = ex && cfg->grid_dims[a] > 0;
+    for (int a = 0; a < ndim; ++a)
+      grid[size_t(a)] = ex ? cfg->grid_dims[a]
+                           : (cfg->grid == 1 ? std::min(cd[size_t(a)] + cfg->grid_pad, fd[size_t(a)]) : fd[size_t(a)]);
+    if (slab_begin < 0 || slab_end <= slab_begin || slab_end > grid[0])
+      fail(SK_ERR_DIM, "slab rows must satisfy 0 <= begin < end <= grid_dims[0]");
+    const i64 nvox = numel(grid) / grid[0] * (slab_end - slab_begin);
+    const float2* d_cal = device_in(ctx, reinterpret_cast<const float2*>(calib), q * numel(cd), "in:calib");
+    const double2* d_u = device_in(ctx, reinterpret_cast<const double2*>(u_sig), n * std::max<i64>(k, 1), "in:usig");
+    Out<float2> om(ctx, reinterpret_cast<float2*>(maps), q * nvox, "out:slab_maps");
+    Out<float> ol(ctx, lambda, nvox, "out:slab_lambda");
+    PipelineOut po;
+    PipelineOut::Basis basis;
+    basis.usig = d_u;
+    basis.k = k;
+    basis.sigma1 = sigma1;
+    po.basis = &basis;
     po.maps = om.dev ? om.dev : ctx->arena.get<float2>("out:slab_maps", q * nvox);
     po.lambda = ol.dev ? ol.dev : ctx->arena.get<float>("out:slab_lambda", nvox);
     po.slab0 = slab_begin;

@@ -62,14 +62,50 @@ def gather_slices(local: np.ndarray, n_items: int, group=None, device=None):
 
 
 # --------------------------------------------------------------- C4: z-slabs
-# A 3-D volume shards by z-slab (axis 0 of the map grid).  Every rank runs the
-# Gram and the nullspace (deterministic, so identical everywhere), expands G(x)
-# and runs the power iteration + normalisation only on its rows of the map
-# grid (sk_estimate_raw_slab); one all-gather assembles the low-resolution maps
-# and eigenvalues; the interpolation is split by channel, its sum-of-squares
-# renormalisation by an all-reduce of the per-voxel SoS (maps.cpp:236-258).
-# Tensors stay where the ops put them (HBM with NCCL on the box, host memory
-# with gloo in the CPU tests).
+# A 3-D volume shards by z-slab (axis 0 of the map grid).  The root rank runs
+# the Gram and the nullspace once and BROADCASTS the nullspace filters in
+# their complement form U_sig (n x k; W = I - U_sig U_sig^H, C4: 3936 x 37
+# complex128 = 2.3 MB) together with k and sigma_1 (north_star);
+# every rank expands G(x) from that same basis and runs the power iteration +
+# normalisation only on its rows of the map grid (sk_estimate_raw_slab_basis);
+# one all-gather assembles the low-resolution maps and eigenvalues; the
+# interpolation is split by channel, its sum-of-squares renormalisation by an
+# all-reduce of the per-voxel SoS (maps.cpp:236-258).  Tensors stay where the
+# ops put them (HBM with NCCL on the box, host memory with gloo in the CPU
+# tests; a gloo group with CUDA tensors stages them through the host).
+
+def _is_gloo(group=None):
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
+
+
+def _staged(t, group=None):
+    """Tensor to hand to a collective: host copy for gloo + CUDA tensors."""
+    return t.cpu() if (t.is_cuda and _is_gloo(group)) else t
+
+
+def broadcast_basis(basis, root: int = 0, group=None, device=None):
+    """Broadcast the root's signal basis {"u": (n, k) complex128, "k", "sigma1",
+    "rank", "n"} to every rank (two collectives: the sizes, then U_sig)."""
+    import torch
+    import torch.distributed as dist
+    me = dist.get_rank(group)
+    meta = torch.zeros(4, dtype=torch.float64, device=device)
+    if me == root:
+        meta = torch.tensor([basis["n"], basis["k"], basis["sigma1"], basis["rank"]], dtype=torch.float64,
+                            device=device)
+    m = _staged(meta, group)
+    dist.broadcast(m, root, group=group)
+    n, k, sigma1, rank = int(m[0]), int(m[1]), float(m[2]), int(m[3])
+    if me == root:
+        u = torch.view_as_real(basis["u"].contiguous()).contiguous()
+    else:
+        u = torch.empty((n, k, 2), dtype=torch.float64, device=device)
+    us = _staged(u, group)
+    dist.broadcast(us, root, group=group)
+    if us is not u:
+        u.copy_(us)
+    return {"u": torch.view_as_complex(u), "n": n, "k": k, "sigma1": sigma1, "rank": rank}
 
 def _gather_rows(t, n_total: int, group=None):
     """all_gather of per-rank row blocks (dim 0, sizes from partition) -> (n_total, ...) on every rank."""
@@ -80,11 +116,11 @@ def _gather_rows(t, n_total: int, group=None):
     cnt = counts(n_total, world)
     pad = max(cnt)
     real = torch.view_as_real(t) if t.is_complex() else t
-    buf = real.new_zeros((pad,) + tuple(real.shape[1:]))
-    buf[: real.shape[0]] = real
+    buf = _staged(real.new_zeros((pad,) + tuple(real.shape[1:])), group)
+    buf[: real.shape[0]] = real.to(buf.device)
     parts = [torch.empty_like(buf) for _ in range(world)]
     dist.all_gather(parts, buf, group=group)
-    out = torch.cat([p[:c] for p, c in zip(parts, cnt)], 0)
+    out = torch.cat([p[:c] for p, c in zip(parts, cnt)], 0).to(real.device)
     return torch.view_as_complex(out.contiguous()) if t.is_complex() else out
 
 
@@ -94,19 +130,61 @@ class DeviceOps:
     def __init__(self, ctx, device):
         self.ctx, self.device = ctx, device
 
+    def _cal(self, calib):
+        import torch
+        cal = calib.data if isinstance(calib.data, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(calib.data, dtype=np.complex64))
+        return cal.to(self.device).contiguous()
+
     def raw_slab(self, calib, full_dims, cfg, slab):
+        """K1 + K2 + the slab's K3/K4/normalisation on this rank (no broadcast)."""
         import torch
         from . import api
         grid = api._grid_for(calib.dims, full_dims, cfg)
         q = calib.channels
         shape = (slab[1] - slab[0],) + tuple(grid[1:])
-        cal = calib.data if isinstance(calib.data, torch.Tensor) else torch.from_numpy(
-            np.ascontiguousarray(calib.data, dtype=np.complex64))
-        cal = cal.to(self.device).contiguous()
+        cal = self._cal(calib)
         maps = torch.empty((q,) + shape, dtype=torch.complex64, device=self.device)
         lam = torch.empty(shape, dtype=torch.float32, device=self.device)
         api.estimate_raw_slab_device(self.ctx, cal.data_ptr(), calib.dims, calib.center_offset, q, full_dims, cfg,
                                      slab, maps.data_ptr(), lam.data_ptr())
+        return maps, lam
+
+    def signal_basis(self, calib, cfg):
+        """compute_gram + extract_nullspace on this rank -> the signal basis dict."""
+        import torch
+        from . import api
+        cal = self._cal(calib)
+        q = calib.channels
+        n = q * api.make_support(cfg.kernel, cfg.tau, len(calib.dims)).shape[0]
+        kmax = min(n, 256)
+        while True:
+            u = torch.empty((kmax, n), dtype=torch.complex128, device=self.device)  # column-major n x kmax
+            try:
+                info = api.signal_basis_device(self.ctx, cal.data_ptr(), calib.dims, calib.center_offset, q, cfg,
+                                               u.data_ptr(), kmax)
+                break
+            except api.DimError:
+                if kmax >= n:
+                    raise
+                kmax = n
+        k = info["k"]
+        return {"u": u[:k].transpose(0, 1), "n": n, "k": k, "sigma1": info["sigma1"], "rank": info["rank"]}
+
+    def raw_slab_basis(self, calib, full_dims, cfg, slab, basis):
+        """The slab's K3/K4/normalisation from a (broadcast) signal basis."""
+        import torch
+        from . import api
+        grid = api._grid_for(calib.dims, full_dims, cfg)
+        q = calib.channels
+        shape = (slab[1] - slab[0],) + tuple(grid[1:])
+        cal = self._cal(calib)
+        u = basis["u"].transpose(0, 1).contiguous().to(self.device)  # (k, n) row-major = n x k column-major
+        maps = torch.empty((q,) + shape, dtype=torch.complex64, device=self.device)
+        lam = torch.empty(shape, dtype=torch.float32, device=self.device)
+        api.estimate_raw_slab_basis_device(self.ctx, cal.data_ptr(), calib.dims, calib.center_offset, q, full_dims,
+                                           cfg, u.data_ptr(), basis["k"], basis["sigma1"], slab, maps.data_ptr(),
+                                           lam.data_ptr())
         return maps, lam
 
     def interpolate_maps(self, low, full_dims):
@@ -164,7 +242,13 @@ def estimate_maps_zslab(calib, full_dims, cfg, ops, group=None, gather_maps=True
     grid = api._grid_for(calib.dims, full_dims, cfg)
     q = calib.channels
     slab = partition(grid[0], world, rank)
-    maps_s, lam_s = ops.raw_slab(calib, full_dims, cfg, slab)  # (Q, nz, ...), (nz, ...)
+    if world > 1:
+        # the exchange step: root's K1 + K2 once, its filters broadcast to every rank
+        basis = ops.signal_basis(calib, cfg) if rank == 0 else None
+        basis = broadcast_basis(basis, 0, group, device=getattr(ops, "device", None))
+        maps_s, lam_s = ops.raw_slab_basis(calib, full_dims, cfg, slab, basis)  # (Q, nz, ...), (nz, ...)
+    else:
+        maps_s, lam_s = ops.raw_slab(calib, full_dims, cfg, slab)
     if world > 1:
         maps_low = _gather_rows(maps_s.transpose(0, 1).contiguous(), grid[0], group).transpose(0, 1).contiguous()
         lam_low = _gather_rows(lam_s, grid[0], group)
@@ -179,9 +263,15 @@ def estimate_maps_zslab(calib, full_dims, cfg, ops, group=None, gather_maps=True
         sos = torch.zeros(tuple(full_dims), dtype=torch.float32, device=mine.device)
         ops.sos_accumulate(mine, sos)
         if world > 1:
-            dist.all_reduce(sos, group=group)
+            ss = _staged(sos, group)
+            dist.all_reduce(ss, group=group)
+            if ss is not sos:
+                sos.copy_(ss)
         ops.renormalize(mine, sos)
         lam = ops.interpolate_real(lam_low, full_dims)
     mask = ops.support_mask(lam, cfg.mask_threshold)
     maps = _gather_rows(mine, q, group) if (gather_maps and world > 1) else mine
-    return maps, lam, mask, {"slab": slab, "channels": ch, "grid": grid}
+    info = {"slab": slab, "channels": ch, "grid": grid}
+    if world > 1:
+        info.update(k=basis["k"], rank=basis["rank"], sigma1=basis["sigma1"])
+    return maps, lam, mask, info

@@ -204,6 +204,19 @@ def test_nullspace_parity(K, O):
     assert PM.rel_fro(wa, wo) < 1e-4
 
 
+@pytest.mark.parametrize("n,r", [(1, 1), (64, 3), (128, 128), (300, 251), (2592, 2546)])
+def test_aggregate_w_parity(K, O, n, r):  # spatial_gram.cpp:87-94 (own tiled Hermitian product)
+    F = rnd((n, r), 41).astype(np.complex64) / np.sqrt(r)
+    got = K.aggregate_w(F)
+    ref = O.aggregate_w(F.astype(np.complex128))
+    err = PM.rel_fro(got, ref)
+    report("aggregate_w", n=n, r=r, rel_fro=err)
+    assert err < 1e-5
+    assert np.abs(got - got.conj().T).max() == 0.0  # stored with its exact conjugate mirror
+    with pytest.raises(K.NullspaceEmptyError):
+        K.aggregate_w(np.zeros((n, 0), dtype=np.complex64))
+
+
 # -------------------------------------------------------------------- K3 field
 @pytest.mark.parametrize("dims,shape,tau,q", [((8, 8), 0, 1, 3), ((5, 8), 0, 1, 3), ((4, 4), 0, 1, 3),
                                               ((16, 12), 1, 2, 4), ((6, 5, 4), 1, 1, 2)])

@@ -112,6 +112,40 @@ class _OracleOps:
         a, b = slab
         return torch.from_numpy(self.norm[:, a:b].copy()), torch.from_numpy(self.lam[a:b].copy())
 
+    # the broadcast path: root computes the signal basis, every rank expands it
+    allow_basis = True
+    basis_seen = None
+
+    def signal_basis(self, calib, cfg):
+        import torch
+        assert self.allow_basis, "only the root computes the nullspace"
+        O = self.O
+        cal = O.Calib(calib.data.astype(np.complex128), calib.center_offset)
+        g = O.gram_fft(cal, cfg.kernel, cfg.tau)
+        w, v = np.linalg.eigh(g)  # nullspace.cpp:13-33 in complement form
+        sig = np.sqrt(np.maximum(w, 0.0))
+        keep = sig >= cfg.nullspace_threshold * sig[-1]
+        u = v[:, keep]
+        return {"u": torch.from_numpy(u.copy()), "n": g.shape[0], "k": int(keep.sum()), "sigma1": float(sig[-1]),
+                "rank": int(g.shape[0] - keep.sum())}
+
+    def raw_slab_basis(self, calib, full_dims, cfg, slab, basis):
+        import torch
+        O = self.O
+        self.basis_seen = basis
+        u = basis["u"].numpy()
+        q = calib.channels
+        W = np.eye(u.shape[0]) - u @ u.conj().T  # aggregate_w of the complement basis
+        field = O.gram_field_fast(W, q, cfg.kernel, cfg.tau, ZS["grid"])
+        lam = O.make_support(cfg.kernel, cfg.tau, 3).shape[0]
+        vec, val = O.eig_power_field(O.espirit(field, lam), cfg.power_iters)
+        raw = vec.reshape((q,) + ZS["grid"])
+        norm = O.normalize_maps(raw, O.Calib(calib.data.astype(np.complex128), calib.center_offset))[0]
+        a, b = slab
+        lamr = (1.0 - val).reshape(ZS["grid"])
+        return (torch.from_numpy(norm[:, a:b].astype(np.complex64).copy()),
+                torch.from_numpy(lamr[a:b].astype(np.float32).copy()))
+
     def interpolate_maps(self, low, full_dims):
         import torch
         return torch.from_numpy(self.O.interpolate_maps(low.numpy(), full_dims).astype(np.complex64))
@@ -152,7 +186,10 @@ def _zs_worker(rank, world, port, out_dir):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     calib, ck, co = _zs_case()
-    maps, lam, mask, info = shard.estimate_maps_zslab(calib, ZS["full"], ck, _OracleOps(calib, co))
+    ops = _OracleOps(calib, co)
+    ops.allow_basis = rank == 0  # the other ranks must receive the filters by broadcast
+    maps, lam, mask, info = shard.estimate_maps_zslab(calib, ZS["full"], ck, ops)
+    np.save(os.path.join(out_dir, f"basis{rank}.npy"), ops.basis_seen["u"].numpy())
     if rank == 0:
         np.save(os.path.join(out_dir, "maps.npy"), maps.numpy())
         np.save(os.path.join(out_dir, "lam.npy"), lam.numpy())
@@ -174,6 +211,8 @@ def test_zslab_two_rank_gloo_equals_single_process(tmp_path):
     maps1, lam1, mask1, _ = shard.estimate_maps_zslab(calib, ZS["full"], ck, ops)
     maps2 = np.load(tmp_path / "maps.npy")
     assert [tuple(np.load(tmp_path / f"slab{r}.npy")) for r in range(2)] == [(0, 4), (4, 8)]
+    u0, u1 = np.load(tmp_path / "basis0.npy"), np.load(tmp_path / "basis1.npy")
+    assert np.array_equal(u0, u1)  # rank 1 expanded exactly the root's broadcast filters
     assert maps2.shape == maps1.shape == (ZS["q"],) + ZS["full"]
     assert np.allclose(maps2, maps1.numpy(), rtol=1e-5, atol=1e-6)
     assert np.array_equal(np.load(tmp_path / "lam.npy"), lam1.numpy())
