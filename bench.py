@@ -531,7 +531,7 @@ def main():
                      "traffic_source": traffic_src,
                      "peak_source": f"SMs x 128 FP32 lanes x 2 x sm_max_mhz ({peak_src} MEASURED_PEAKS sm_max_mhz)",
                      "flops_per_launch": k4_flops(spec)},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h_cal.numel() * 8),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h_var[0].numel() * 8),
                 "d2h_bytes_per_step": int((h_maps.numel() * 8 + h_lam.numel() * 4 + h_mask.numel()) * slices // hs)},
         "gpu_launches": int(launches), "library_calls": int(libcalls),
         "clocks": clk,

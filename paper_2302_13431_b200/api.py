@@ -495,7 +495,7 @@ def _grid_for(cdims, full_dims, cfg: PipelineConfig):
 
 
 def estimate_maps(calib: Calib, full_dims, cfg: PipelineConfig, ctx: Context | None = None, *,
-                  want_spectrum: bool = True, want_gram: bool = False, want_field: bool = False,
+                  want_spectrum: bool = False, want_gram: bool = False, want_field: bool = False,
                   want_raw: bool = False, out=None) -> SensitivityResult:
     """estimate_maps (maps.hpp:85-86).
 

@@ -117,7 +117,8 @@ def run_estimate(a) -> int:
     calib = extract_calibration(stack.data, calib_size)
     cfg = config_from_flags(a)
     ctx = api.Context(a.device)
-    result = api.estimate_maps(calib, stack.dims, cfg, ctx)
+    # the reference writes all n singular values (senskit_main.cpp:160-166): full spectrum requested
+    result = api.estimate_maps(calib, stack.dims, cfg, ctx, want_spectrum=True)
     residual = api.projection_residual(stack.data, result.maps, ctx)
 
     save_stack(Stack(result.maps, "image"), a.output + "_maps")
