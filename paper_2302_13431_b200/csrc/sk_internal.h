@@ -18,6 +18,15 @@
 
 #include "../../include/senskit_b200.h"
 
+// Device-side bounds/invariant checks: compiled in with -DSKB_CHECKED (a
+// debug build of the library; the sanitizer is not available on the GPU pool).
+#ifdef SKB_CHECKED
+#include <cassert>
+#define SKB_DCHECK(x) assert(x)
+#else
+#define SKB_DCHECK(x) ((void)0)
+#endif
+
 namespace skb {
 
 using i64 = std::int64_t;

@@ -113,9 +113,6 @@ struct TmaTiles {
   int use = 0;  // 0: cp.async fallback (plane stride not a multiple of 16 B)
   int hb = 0, nb = 0;
   int swz = 0;  // swizzle mask applied by the readers (0: dense tile)
-  int lo_smem = 1;  // 1: lo planes staged by TMA into their own tile; 0: read from global in the epilogue
-  int single_hi = 0;  // (= L::kSingleHi) one hi tile, refilled with the next tile right after the unpack (the
-                      // epilogue takes hi from the registers): two tile buffers per block instead of three
 };
 
 // float2 index of tile element idx under the TMA swizzle (buffer 1 KB aligned).
@@ -124,17 +121,32 @@ __device__ __forceinline__ int swz_at(int idx, int mask) {
   return (b ^ (((b >> 7) & mask) << 4)) >> 3;
 }
 
-template <int QP_, int RPT_, int THREADS_, int MINB_, int ACC_ = 0, int PF_ = 4, int QF_ = 0, int SH_ = 0>
+template <int QP_, int RPT_, int THREADS_, int MINB_, int ACC_ = 0, int PF_ = 4, int QF_ = 0, int TILE_ = 0>
 struct Layout {
-  static constexpr bool kSingleHi = SH_ != 0;  // one hi tile (TmaTiles::single_hi), compile-time
   static constexpr int QP = QP_, RPT = RPT_, kThreads = THREADS_, kMinBlocks = MINB_;
   static constexpr int QF = QF_;  // > 0: the channel count is fixed at compile time (Q == QF)
   static constexpr int kPrefetch = PF_;  // LDS.128 of v kept in flight ahead of their use
   static constexpr int kTPV = QP / RPT;          // threads per voxel
   static constexpr int kVPB = kThreads / kTPV;   // voxels per block
   static constexpr int kWPV = kTPV > 32 ? kTPV / 32 : 1;  // warps per voxel
-  static constexpr int kStride = QP + 2;         // float2 per v row (16-B aligned, bank-skewed)
   static constexpr int kAcc = ACC_ > 0 ? ACC_ : (RPT >= 4 ? 1 : 4 / RPT);  // accumulator pairs per row
+  // Tiled matvec (TILE_ != 0, RPT == 1): thread `local` = 4 rg + cg holds the
+  // 4 x kTC block of rows 4 rg.., columns kTC cg.. instead of a full row: a
+  // product needs only its kTC entries of v and two shuffle rounds over the
+  // column groups (lane xor 2, 1) leave (M v)[local] in thread `local`
+  // (row_of(local) == local).  Used for Q = 64 (C5 K4 20.4 -> 18.5 ms); for
+  // Q = 32 it measured slower than one row per thread (0.95 vs 0.92 ms, C2:
+  // the shared-memory wavefronts barely drop and the shuffles add latency).
+  static constexpr bool kTile = TILE_ != 0;
+  static constexpr int kTR = 4, kTC = QP / 4;
+  // float2 per v row: column group g starts at g (kTC + 2) in the tiled
+  // layout (16-B aligned, the four groups on disjoint banks), else QP + 2.
+  static constexpr int kStride = kTile ? QP + 8 : QP + 2;
+  __device__ static constexpr int vidx(int c) { return kTile ? c + (c / kTC) * 2 : c; }
+  __device__ static constexpr int col_group(int local) { return local & 3; }
+  __device__ static constexpr int row_group(int local) { return local >> 2; }
+  __device__ static constexpr int row_of(int local) { return kTile ? 4 * row_group(local) + col_group(local) : local; }
+  static_assert(!kTile || (RPT == 1 && QP >= 8), "tiled matvec: one row per thread");
 };
 
 // Sum over the voxel's threads.  Multi-warp voxels go through shared memory
@@ -183,6 +195,8 @@ __device__ __forceinline__ int pair_index(int p, int c, int Q) { return p * Q - 
 // Element (p, c) of the Hermitian matrix from the packed tile (zero outside Q).
 __device__ __forceinline__ float2 herm_at(const float2* gs, int p, int c, int Q, int VPB, int vox, int swz) {
   float2 val = make_float2(0.f, 0.f);
+  SKB_DCHECK(p >= 0 && c >= 0 && vox >= 0 && vox < VPB);
+  SKB_DCHECK(p >= Q || c >= Q || pair_index(min(p, c), max(p, c), Q) < Q * (Q + 1) / 2);
   if (p < Q && c < Q) {
     if (p <= c) {
       val = gs[swz_at(pair_index(p, c, Q) * VPB + vox, swz)];
@@ -193,6 +207,18 @@ __device__ __forceinline__ float2 herm_at(const float2* gs, int p, int c, int Q,
     if (p == c) val.y = 0.f;  // spatial_gram.cpp:140-146
   }
   return val;
+}
+
+// herm_at for row AND column indices known only at run time (the tiled
+// layout): the packed element (min, max) with a conditional conjugate, no
+// branches around the load (the branchy form faulted under ptxas 12.9 when
+// both indices were run-time values in the fully unrolled unpack).
+__device__ __forceinline__ float2 herm_at_bf(const float2* gs, int p, int c, int Q, int VPB, int vox, int swz) {
+  const int lo = min(p, c), hi = max(p, c);
+  const bool in = hi < Q;
+  SKB_DCHECK(lo >= 0 && vox >= 0 && vox < VPB);
+  const float2 t = gs[swz_at((in ? pair_index(lo, hi, Q) : 0) * VPB + vox, swz)];
+  return in ? make_float2(t.x, p == c ? 0.f : (p <= c ? t.y : -t.y)) : make_float2(0.f, 0.f);
 }
 
 template <class L>
@@ -208,8 +234,8 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
   // tile buffers start on a 1 KB boundary (the swizzle pattern follows address bits 4..9)
   float2* gbuf = reinterpret_cast<float2*>(smem_raw + ((smem_u32(smem_raw) + 128 + 1023) & ~1023u) -
                                            smem_u32(smem_raw));  // [2][tile_elems] hi planes
-  float2* lbuf = gbuf + (L::kSingleHi ? 1 : 2) * tile_elems;            // [tile_elems] lo planes (lo_smem)
-  float2* vs = lbuf + ((tt.lo_smem || L::kSingleHi) ? tile_elems : 0);   // [2][VPB][kStride]
+  float2* lbuf = gbuf + 2 * tile_elems;                                  // [tile_elems] lo planes
+  float2* vs = lbuf + tile_elems;                                        // [2][VPB][kStride]
   double2* vds = reinterpret_cast<double2*>(vs + 2 * VPB * L::kStride);  // [VPB][QP] final v in FP64
   double* redd = reinterpret_cast<double*>(vds + VPB * QP);              // [VPB][kWPV]
   float* red = reinterpret_cast<float*>(redd + VPB * WPV);               // [VPB][kWPV]
@@ -222,7 +248,8 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
   }
 
   const int vox = threadIdx.x / TPV;
-  const int local = threadIdx.x % TPV;  // rows local + r * TPV
+  const int local = threadIdx.x % TPV;
+  const int prow = L::row_of(local);    // the thread's rows: prow + r * TPV
   const i64 tiles = (a.n + VPB - 1) / VPB;
   const i64 ld = a.ld > 0 ? a.ld : a.n;  // plane / channel stride (a voxel range of a larger grid)
 
@@ -262,51 +289,47 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
   if (tile < tiles) load_tile(tile, gbuf, a.planes, &tm_hi, 0);
   for (; tile < tiles; tile += gridDim.x, buf ^= 1) {
     const i64 next = tile + gridDim.x;
-    if constexpr (L::kSingleHi) {
-      if (tt.use) {
-        wait_tile(0);
-      } else {
-        cp_async_wait<0>();
-        __syncthreads();
-      }
+    if (next < tiles) load_tile(next, gbuf + (buf ^ 1) * tile_elems, a.planes, &tm_hi, buf ^ 1);
+    if (tt.use) {
+      wait_tile(buf);
     } else {
-      if (next < tiles) load_tile(next, gbuf + (buf ^ 1) * tile_elems, a.planes, &tm_hi, buf ^ 1);
-      if (tt.use) {
-        wait_tile(buf);
-      } else {
-        if (next < tiles)
-          cp_async_wait<1>();
-        else
-          cp_async_wait<0>();
-        __syncthreads();
-      }
+      if (next < tiles)
+        cp_async_wait<1>();
+      else
+        cp_async_wait<0>();
+      __syncthreads();
     }
-    float2* gs = gbuf + (L::kSingleHi ? 0 : buf * tile_elems);
+    float2* gs = gbuf + buf * tile_elems;
     const i64 j0 = tile * VPB;
     const i64 j = j0 + vox;
     const bool live = j < a.n;
 
     // Unpack this thread's rows.
     float2 m[RPT][QP];
+    float2 mc0[RPT];  // M[p][0] of the thread's rows p (the e_0 restart of iteration 0)
+    if constexpr (L::kTile) {
+      const int r0 = 4 * L::row_group(local), c0 = L::kTC * L::col_group(local);
 #pragma unroll
-    for (int r = 0; r < RPT; ++r)
+      for (int tr = 0; tr < 4; ++tr)
 #pragma unroll
-      for (int c = 0; c < QP; ++c) m[r][c] = herm_at(gs, local + r * TPV, c, Q, VPB, vox, tt.swz);
+        for (int tc = 0; tc < L::kTC; ++tc) m[0][tr * L::kTC + tc] = herm_at_bf(gs, r0 + tr, c0 + tc, Q, VPB, vox, tt.swz);
+      mc0[0] = herm_at_bf(gs, prow, 0, Q, VPB, vox, tt.swz);
+    } else {
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+#pragma unroll
+        for (int c = 0; c < QP; ++c) m[r][c] = herm_at(gs, prow + r * TPV, c, Q, VPB, vox, tt.swz);
+        mc0[r] = m[r][0];
+      }
+    }
     // Stream the lo residual planes of this tile while the iterations run
     // (its own buffer: the final Rayleigh quotient reads hi and lo packed).
-    // single_hi: the hi tile is free once unpacked and receives the next tile.
-    if constexpr (L::kSingleHi) {
-      __syncthreads();  // every unpack read of gs precedes its refill
-      if (a.planes_lo != nullptr) load_tile(tile, lbuf, a.planes_lo, &tm_lo, 2);
-      if (next < tiles) load_tile(next, gbuf, a.planes, &tm_hi, 0);
-    } else if (a.planes_lo != nullptr && tt.lo_smem) {
-      load_tile(tile, lbuf, a.planes_lo, &tm_lo, 2);
-    }
+    if (a.planes_lo != nullptr) load_tile(tile, lbuf, a.planes_lo, &tm_lo, 2);
     // recon values for the epilogue, loaded while the iterations run
     float2 rcv[RPT];
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
-      const int p = local + r * TPV;
+      const int p = prow + r * TPV;
       rcv[r] = (a.recon != nullptr && p < Q && live) ? a.recon[i64(p) * ld + j] : make_float2(0.f, 0.f);
     }
 
@@ -317,8 +340,8 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     float2 vp[RPT];
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
-      vp[r] = (local + r * TPV < Q) ? make_float2(init, 0.f) : make_float2(0.f, 0.f);
-      vb(0)[local + r * TPV] = vp[r];
+      vp[r] = (prow + r * TPV < Q) ? make_float2(init, 0.f) : make_float2(0.f, 0.f);
+      vb(0)[L::vidx(prow + r * TPV)] = vp[r];
     }
     bool done = false;
     voxel_sync<L>();
@@ -329,7 +352,8 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       float x = 0.f;
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
-        vb(b)[local + r * TPV] = u[r];
+        SKB_DCHECK(L::vidx(prow + r * TPV) < L::kStride);
+        vb(b)[L::vidx(prow + r * TPV)] = u[r];
         x = fmaf(u[r].x, u[r].x, fmaf(u[r].y, u[r].y, x));
       }
       if constexpr (TPV <= 32) {
@@ -360,6 +384,51 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     // Complex MAC as two FFMA2: acc += m.x * (v.x, v.y), acc2 += m.y * (v.y, v.x);
     // (M v) = (acc.x - acc2.x, acc.y + acc2.y).
     auto matvec = [&](const float2* v, float2 (&out)[RPT]) {
+      if constexpr (L::kTile) {
+        // 4 x kTC block times v[kTC cg ..]: acc += m.x (v.x, v.y), acc2 += m.y (v.y, v.x)
+        // (two accumulators per row: C5 K4 18.5 ms against 22.7 with one)
+        constexpr int TC = L::kTC;
+        const int cg = L::col_group(local);
+        const float4* v4 = reinterpret_cast<const float4*>(v + cg * (TC + 2));
+        SKB_DCHECK(v >= vs && v + cg * (TC + 2) + TC <= vs + 2 * VPB * L::kStride);
+        u64 acc[4], acc2[4];
+#pragma unroll
+        for (int tr = 0; tr < 4; ++tr) acc[tr] = acc2[tr] = 0ull;
+#pragma unroll
+        for (int t = 0; t < TC / 2; ++t) {
+          const float4 vt = v4[t];
+#pragma unroll
+          for (int tr = 0; tr < 4; ++tr) {
+            const float2 ma = m[0][tr * TC + 2 * t], mb = m[0][tr * TC + 2 * t + 1];
+            ffma2(acc[tr], pk(ma.x, ma.x), pk(vt.x, vt.y));
+            ffma2(acc2[tr], pk(ma.y, ma.y), pk(vt.y, vt.x));
+            ffma2(acc[tr], pk(mb.x, mb.x), pk(vt.z, vt.w));
+            ffma2(acc2[tr], pk(mb.y, mb.y), pk(vt.w, vt.z));
+          }
+        }
+        float2 s4[4];
+#pragma unroll
+        for (int tr = 0; tr < 4; ++tr) {
+          const float2 x = unpk(acc[tr]), y = unpk(acc2[tr]);
+          s4[tr] = make_float2(x.x - y.x, x.y + y.y);
+        }
+        // reduce-scatter over the column groups: bit 1 of cg keeps rows {2,3}
+        // (else {0,1}), bit 0 then keeps the odd (else even) one: row 4 rg + cg.
+        // cg is lane bits 0..1: partners at lane xor 2, then xor 1.
+        const bool b1 = (cg & 2) != 0, b0 = (cg & 1) != 0;
+        float2 k0 = b1 ? s4[2] : s4[0], k1 = b1 ? s4[3] : s4[1];
+        const float2 o0 = b1 ? s4[0] : s4[2], o1 = b1 ? s4[1] : s4[3];
+        k0.x += __shfl_xor_sync(0xffffffffu, o0.x, 2);
+        k0.y += __shfl_xor_sync(0xffffffffu, o0.y, 2);
+        k1.x += __shfl_xor_sync(0xffffffffu, o1.x, 2);
+        k1.y += __shfl_xor_sync(0xffffffffu, o1.y, 2);
+        float2 kk = b0 ? k1 : k0;
+        const float2 oo = b0 ? k0 : k1;
+        kk.x += __shfl_xor_sync(0xffffffffu, oo.x, 1);
+        kk.y += __shfl_xor_sync(0xffffffffu, oo.y, 1);
+        out[0] = kk;
+        return;
+      }
       constexpr int A = L::kAcc;
       const float4* v4 = reinterpret_cast<const float4*>(v);
       u64 acc[RPT][A], acc2[RPT][A];
@@ -413,9 +482,9 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
         w[r] = make_float2(a.alpha * vp[r].x + a.beta * mv[r].x, a.alpha * vp[r].y + a.beta * mv[r].y);
-        v0[r] = (local + r * TPV == 0) ? make_float2(1.f, 0.f) : make_float2(0.f, 0.f);
+        v0[r] = (prow + r * TPV == 0) ? make_float2(1.f, 0.f) : make_float2(0.f, 0.f);
         // (B e_0)[p] = alpha e_0[p] + beta M[p][0]
-        w0[r] = make_float2(a.alpha * v0[r].x + a.beta * m[r][0].x, a.alpha * v0[r].y + a.beta * m[r][0].y);
+        w0[r] = make_float2(a.alpha * v0[r].x + a.beta * mc0[r].x, a.alpha * v0[r].y + a.beta * mc0[r].y);
         x += w[r].x * w[r].x + w[r].y * w[r].y;
         x0 += w0[r].x * w0[r].x + w0[r].y * w0[r].y;
       }
@@ -489,7 +558,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     if (a.rq32_min > 0.f) {
       voxel_bar<L>(vox);  // every read of the v buffers precedes the overwrite
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) vb(0)[local + r * TPV] = vp[r];
+      for (int r = 0; r < RPT; ++r) vb(0)[L::vidx(prow + r * TPV)] = vp[r];
       voxel_sync<L>();
       float2 y[RPT];
       matvec(vb(0), y);
@@ -506,13 +575,11 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     {
       double2* vd = vds + vox * QP;
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) vd[local + r * TPV] = make_double2(double(vp[r].x), double(vp[r].y));
+      for (int r = 0; r < RPT; ++r) vd[prow + r * TPV] = make_double2(double(vp[r].x), double(vp[r].y));
     }
-    if (a.planes_lo != nullptr && (tt.lo_smem || L::kSingleHi)) {
+    if (a.planes_lo != nullptr) {
       if (tt.use)
         wait_tile(2);
-      else if (L::kSingleHi && next < tiles)
-        cp_async_wait<1>();  // lo(t) was committed before hi(t+1)
       else
         cp_async_wait<0>();
     }
@@ -520,37 +587,6 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     double xd = 0.0;
     if (!need64) {
       // FP32 value kept (voxel_sum below still runs: its shuffles span voxels)
-    } else if constexpr (L::kSingleHi) {
-      // hi part from the registers: sum over this thread's rows p of
-      // Re(conj(v_p) (M_hi v)_p); the lo part over the packed triangle.
-      const double2* vd = vds + vox * QP;
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        const int p = local + r * TPV;
-        double yx = 0.0, yy = 0.0;
-#pragma unroll
-        for (int c = 0; c < QP; ++c) {
-          const double2 vc = vd[c];
-          const double mx = double(m[r][c].x), my = double(m[r][c].y);
-          yx = fma(mx, vc.x, fma(-my, vc.y, yx));
-          yy = fma(mx, vc.y, fma(my, vc.x, yy));
-        }
-        if (p < Q) xd = fma(vd[p].x, yx, fma(vd[p].y, yy, xd));
-      }
-      if (a.planes_lo != nullptr) {
-        for (int e = local; e < h; e += TPV) {
-          const int pc = pct[e], pp = pc >> 8, cc = pc & 0xff;
-          const float2 lv = lbuf[swz_at(e * VPB + vox, tt.swz)];
-          const double mx = double(lv.x), my = double(lv.y);
-          const double2 vpp = vd[pp], vc = vd[cc];
-          if (pp == cc) {
-            xd = fma(mx, vpp.x * vpp.x + vpp.y * vpp.y, xd);
-          } else {
-            const double tx = mx * vc.x - my * vc.y, ty = mx * vc.y + my * vc.x;
-            xd = fma(2.0, vpp.x * tx + vpp.y * ty, xd);
-          }
-        }
-      }
     } else {
       const double2* vd = vds + vox * QP;
       for (int e = local; e < h; e += TPV) {
@@ -558,9 +594,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
         const float2 hv = gs[swz_at(e * VPB + vox, tt.swz)];
         double mx = double(hv.x), my = double(hv.y);
         if (a.planes_lo != nullptr) {
-          const float2 lv = tt.lo_smem ? lbuf[swz_at(e * VPB + vox, tt.swz)]
-                            : live      ? __ldg(a.planes_lo + i64(e) * ld + j)
-                                        : make_float2(0.f, 0.f);
+          const float2 lv = lbuf[swz_at(e * VPB + vox, tt.swz)];
           mx += double(lv.x);
           my += double(lv.y);
         }
@@ -593,7 +627,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       float xr = 0.f, xi = 0.f;
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
-        const int p = local + r * TPV;
+        const int p = prow + r * TPV;
         const float2 rc = rcv[r];
         xr += vp[r].x * rc.x + vp[r].y * rc.y;  // conj(v) * recon
         xi += vp[r].x * rc.y - vp[r].y * rc.x;
@@ -609,12 +643,11 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       }
     }
 
-    // Stage maps for channel-major coalesced stores: reuse a plane tile (the
-    // lo tile under single_hi: the hi tile is already receiving the next tile).
+    // Stage maps for channel-major coalesced stores: reuse the hi plane tile.
     __syncthreads();
-    float2* ms = L::kSingleHi ? lbuf : gs;  // [QP][VPB]
+    float2* ms = gs;  // [QP][VPB]
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) ms[(local + r * TPV) * VPB + vox] = vp[r];
+    for (int r = 0; r < RPT; ++r) ms[(prow + r * TPV) * VPB + vox] = vp[r];
     __syncthreads();
     for (int e = threadIdx.x; e < Q * VPB; e += blockDim.x) {
       const int c = e / VPB, v = e % VPB;
@@ -646,33 +679,22 @@ bool encode_planes(CUtensorMap* m, const float2* base, i64 n, i64 ld, int h, int
   const cuuint64_t strides[1] = {cuuint64_t(ld) * 8};
   const cuuint32_t box[2] = {cuuint32_t(vpb), cuuint32_t(hb)};
   const cuuint32_t estr[2] = {1, 1};
-  // L2 promotion of the 8*vpb-byte box rows (SKB_TMA_PROMO = 0 none, 64, 128, 256)
-  static const CUtensorMapL2promotion promo = [] {
-    const char* v = std::getenv("SKB_TMA_PROMO");
-    const int p = v ? std::atoi(v) : 256;
-    return p == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-                  : p == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                            : p == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  }();
+  // L2 promotion of the 8*vpb-byte box rows: 256 B
+  constexpr CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<float2*>(base), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
 
-int env_int(const char* name, int dflt);
-
 template <class L>
 void launch(sk_ctx* ctx, const PowerArgs& a) {
   const int h = a.q * (a.q + 1) / 2;
-  static const bool no_tma = std::getenv("SKB_NO_TMA") != nullptr;
-  static const bool no_swz = std::getenv("SKB_K4_NO_SWIZZLE") != nullptr;
   TmaTiles tt;
   CUtensorMap tm_hi{}, tm_lo{};
   // box rows: <= 256; every box a multiple of 128 B (TMA smem alignment) and of 8 rows when
   // swizzled (the pattern's period); a swizzled tile a multiple of 1 KB (buffers stay 1 KB aligned)
   const int row_bytes = L::kVPB * int(sizeof(float2));
-  const CUtensorMapSwizzle swz = no_swz ? CU_TENSOR_MAP_SWIZZLE_NONE
-                                 : row_bytes == 32  ? CU_TENSOR_MAP_SWIZZLE_32B
+  const CUtensorMapSwizzle swz = row_bytes == 32  ? CU_TENSOR_MAP_SWIZZLE_32B
                                  : row_bytes == 64  ? CU_TENSOR_MAP_SWIZZLE_64B
                                  : row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                                                     : CU_TENSOR_MAP_SWIZZLE_NONE;
@@ -684,7 +706,7 @@ void launch(sk_ctx* ctx, const PowerArgs& a) {
     if (tt.hb <= 256) break;
   }
   const i64 ld = a.ld > 0 ? a.ld : a.n;
-  tt.use = !no_tma && encode_planes(&tm_hi, a.planes, a.n, ld, h, L::kVPB, tt.hb, swz) &&
+  tt.use = encode_planes(&tm_hi, a.planes, a.n, ld, h, L::kVPB, tt.hb, swz) &&
            (a.planes_lo == nullptr || encode_planes(&tm_lo, a.planes_lo, a.n, ld, h, L::kVPB, tt.hb, swz));
   if (a.planes_lo == nullptr) tm_lo = tm_hi;
   tt.swz = !tt.use ? 0 : swz == CU_TENSOR_MAP_SWIZZLE_32B ? 1 : swz == CU_TENSOR_MAP_SWIZZLE_64B ? 3
@@ -692,14 +714,8 @@ void launch(sk_ctx* ctx, const PowerArgs& a) {
   const int alt = tt.swz ? std::max(al, 1024 / row_bytes) : al;
   const int tile_rows = (std::max(std::max(h, L::QP), tt.use ? tt.nb * tt.hb : 0) + alt - 1) / alt * alt;
   const size_t tile = size_t(tile_rows) * L::kVPB * sizeof(float2);
-  // lo planes: their own TMA tile, or (SKB_K4_LO_SMEM=0, experiment) read from
-  // global in the epilogue — a third less shared memory per voxel, but the
-  // strided 8-byte reads cost more than they free (C2 two-row layout 1.64 ms).
-  static const int lo_env = env_int("SKB_K4_LO_SMEM", -1);
-  tt.lo_smem = lo_env >= 0 ? lo_env : 1;
-  tt.single_hi = L::kSingleHi ? 1 : 0;
-  if (tt.single_hi) tt.lo_smem = 1;
-  const size_t smem = 1024 + 128 + (tt.single_hi ? 2 : tt.lo_smem ? 3 : 2) * tile +
+  // two hi tile buffers (double-buffered prefetch) + the lo tile
+  const size_t smem = 1024 + 128 + 3 * tile +
                       2 * size_t(L::kVPB) * L::kStride * sizeof(float2) +
                       size_t(L::kVPB) * L::QP * sizeof(double2) +
                       size_t(L::kVPB) * L::kWPV * (sizeof(double) + 3 * sizeof(float)) + size_t(h) * sizeof(int);
@@ -713,19 +729,17 @@ void launch(sk_ctx* ctx, const PowerArgs& a) {
   SKB_LAUNCH("power_kernel");
 }
 
-int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoi(v) : dflt;
-}
-
 }  // namespace
 
 void power_iteration(sk_ctx* ctx, const PowerArgs& a) {
   if (a.n <= 0) return;
-  // Rows per thread for Q in (16, 32]; SKB_POWER_RPT32=2 selects the
-  // two-row layout (measured equal with FFMA2, but it spills).
-  static const int rpt32 = env_int("SKB_POWER_RPT32", 1);
-  static const int k4v = env_int("SKB_K4_VARIANT", 0);
+  // One matrix row per thread, Q fixed at compile time for the BASELINE
+  // channel counts.  Q = 32: one accumulator pair per row (ptxas then rotates
+  // two v quads; measured C2 0.973 -> 0.942 ms, C4 5.81 -> 5.52 ms against
+  // two pairs).  Q = 64: the tiled matvec (4 x 16 blocks, C5 20.4 -> 18.5 ms
+  // against one row per thread).  Measured and dropped: two rows per thread
+  // (three 128-thread blocks, 1.12 vs 0.95 ms on C2), one 256-thread block
+  // per SM, deeper v prefetch, the tiled matvec for Q = 32.
   if (a.q <= 4)
     launch<Layout<4, 1, 256, 2>>(ctx, a);
   else if (a.q == 8)
@@ -734,40 +748,14 @@ void power_iteration(sk_ctx* ctx, const PowerArgs& a) {
     launch<Layout<8, 1, 256, 2>>(ctx, a);
   else if (a.q <= 16)
     launch<Layout<16, 1, 256, 2>>(ctx, a);
+  else if (a.q == 32)
+    launch<Layout<32, 1, 256, 2, 1, 4, 32>>(ctx, a);
   else if (a.q <= 32)
-    switch (k4v) {  // SKB_K4_VARIANT: accumulator pairs / staged columns (experiments)
-      case 1: launch<Layout<32, 1, 256, 2, 2, 2>>(ctx, a); break;
-      case 2: launch<Layout<32, 1, 256, 2, 2, 6>>(ctx, a); break;
-      case 3: launch<Layout<32, 1, 256, 2, 4, 4>>(ctx, a); break;
-      case 4: launch<Layout<32, 1, 256, 2, 2, 3>>(ctx, a); break;
-      case 5: launch<Layout<32, 1, 256, 1, 2, 4>>(ctx, a); break;
-      case 6: launch<Layout<32, 2, 256, 1, 2, 4>>(ctx, a); break;
-      case 7: launch<Layout<32, 1, 256, 1, 4, 6>>(ctx, a); break;
-      case 8: launch<Layout<32, 2, 128, 3, 0, 4, 32>>(ctx, a); break;
-      case 9: launch<Layout<32, 2, 128, 3, 2, 2, 32>>(ctx, a); break;
-      case 10: launch<Layout<32, 2, 192, 2, 0, 4, 32>>(ctx, a); break;
-      case 11: launch<Layout<32, 1, 128, 3, 2, 4, 32>>(ctx, a); break;
-      case 12: launch<Layout<32, 1, 256, 2, 1, 4, 32>>(ctx, a); break;
-      case 13: launch<Layout<32, 1, 128, 3, 4, 6, 32>>(ctx, a); break;
-      case 17: launch<Layout<32, 1, 256, 2, 1, 4, 32, 1>>(ctx, a); break;  // single hi tile
-      default:
-        if (rpt32 != 1)
-          launch<Layout<32, 2, 128, 3>>(ctx, a);
-        else if (a.q == 32)  // one accumulator pair: ptxas then rotates two v quads (SKB_K4_VARIANT=12 measured
-                             // C2 0.973 -> 0.942 ms, C4 5.81 -> 5.52 ms against two pairs)
-          launch<Layout<32, 1, 256, 2, 1, 4, 32>>(ctx, a);
-        else
-          launch<Layout<32, 1, 256, 2, 2, 4>>(ctx, a);
-    }
+    launch<Layout<32, 1, 256, 2, 2, 4>>(ctx, a);
+  else if (a.q == 64)
+    launch<Layout<64, 1, 256, 1, 2, 4, 64, 1>>(ctx, a);
   else if (a.q <= 64)
-    switch (a.q == 64 ? k4v : 0) {  // SKB_K4_VARIANT 14/15/16: accumulator pairs / prefetch for Q = 64
-      case 14: launch<Layout<64, 1, 256, 1, 1, 4, 64>>(ctx, a); break;
-      case 15: launch<Layout<64, 1, 256, 1, 2, 4, 64>>(ctx, a); break;
-      case 16: launch<Layout<64, 1, 256, 1, 2, 8, 64>>(ctx, a); break;
-      case 17: launch<Layout<64, 1, 256, 1, 0, 4, 64>>(ctx, a); break;  // four accumulator pairs
-      default:  // two accumulator pairs (C5 K4 22.5 -> 21.4 ms against four)
-        a.q == 64 ? launch<Layout<64, 1, 256, 1, 2, 4, 64>>(ctx, a) : launch<Layout<64, 1, 256, 1>>(ctx, a);
-    }
+    launch<Layout<64, 1, 256, 1>>(ctx, a);
   else
     fail(9, "eig_power_field: more than 64 channels is outside the B200 path");
 }
