@@ -211,9 +211,11 @@ __global__ void __launch_bounds__(kThreads) herm_eig_kernel(double2* __restrict_
   __syncthreads();
 
   // ---- 1. tridiagonalisation (zhetd2, lower): x = A(k+1:, k) = conj(A(k, k+1:))
-  long long tacc0 = 0, tacc1 = 0, tacc2 = 0, tc = 0;
+  // Three block barriers per column: v published, p published, A22 updated.
+  // Row i of the trailing matrix belongs to the 8 lanes tid >> 3 == i (lane h
+  // takes columns h, h + 8, ...) in both the product and the update, so every
+  // chain is short and the loads of a thread are independent.
   for (int k = 0; k + 1 < n; ++k) {
-    tc = clock64();
     const int m = n - k - 1;
     const double2* rowk = A + k * ld + k + 1;  // conj(x)
     // ||x[1:]||^2, redundantly per warp (m <= 63)
@@ -240,22 +242,19 @@ __global__ void __launch_bounds__(kThreads) herm_eig_kernel(double2* __restrict_
       tau[k] = t;
     }
     if (t.x == 0.0 && t.y == 0.0) continue;  // H_k = I (uniform across the block; A unchanged)
-    tacc0 += clock64() - tc;
-    tc = clock64();
-    auto vj_of = [&](int j) { return j == 0 ? make_double2(1.0, 0.0) : cmul(cconj(rowk[j]), scale); };
-    if (tid < m) vv[tid] = vj_of(tid);
-    // p = tau * A22 v, eight lanes per row, v formed on the fly
-    {
-      const int i = tid >> 3, h = tid & 7;
-      double2 acc0 = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-      if (i < m) {
-        const double2* ar = A + (k + 1 + i) * ld + k + 1;
-        int j = h;
-        for (; j + 8 < m; j += 16) {
-          acc0 = cfma(acc0, ar[j], vj_of(j));
-          acc1 = cfma(acc1, ar[j + 8], vj_of(j + 8));
+    if (tid < m) vv[tid] = tid == 0 ? make_double2(1.0, 0.0) : cmul(cconj(rowk[tid]), scale);
+    __syncthreads();
+    const int ri = tid >> 3, rh = tid & 7;
+    const bool row_live = ri < m;
+    double2* ar = A + (k + 1 + ri) * ld + k + 1;
+    {  // p = tau * A22 v
+      double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0;
+      if (row_live) {
+#pragma unroll 4
+        for (int j = rh; j < m; j += 16) {
+          acc0 = cfma(acc0, ar[j], vv[j]);
+          if (j + 8 < m) acc1 = cfma(acc1, ar[j + 8], vv[j + 8]);
         }
-        if (j < m) acc0 = cfma(acc0, ar[j], vj_of(j));
       }
       double2 acc = cadd(acc0, acc1);
 #pragma unroll
@@ -263,56 +262,32 @@ __global__ void __launch_bounds__(kThreads) herm_eig_kernel(double2* __restrict_
         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
         acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
       }
-      if (i < m && h == 0) pv[i] = cmul(t, acc);
+      if (row_live && rh == 0) pv[ri] = cmul(t, acc);
     }
     __syncthreads();
-    tacc1 += clock64() - tc;
-    tc = clock64();
-    // a2 = -tau/2 (p^H v), redundantly per warp; w = p + a2 v on the fly
+    // a2 = -tau/2 (p^H v), redundantly per warp; w = p + a2 v
     double2 dp = make_double2(0.0, 0.0);
     for (int i = lane; i < m; i += 32) dp = cfma_conj(dp, pv[i], vv[i]);
     dp.x = warp_sum(dp.x);
     dp.y = warp_sum(dp.y);
     const double2 a2 = cmul(make_double2(-0.5 * t.x, -0.5 * t.y), dp);
-    // A22 -= v w^H + w v^H (both triangles); v_k goes to row k (dead after this step)
-    if (tid < m) A[k * ld + k + 1 + tid] = vv[tid];
-    {
-      // this lane's columns j = lane, lane + 32 (m <= 63)
-      const int j0 = lane, j1 = lane + 32;
-      double2 vc0 = make_double2(0.0, 0.0), wc0 = vc0, vc1 = vc0, wc1 = vc0;
-      if (j0 < m) {
-        vc0 = cconj(vv[j0]);
-        wc0 = cconj(cfma(pv[j0], a2, vv[j0]));
-      }
-      if (j1 < m) {
-        vc1 = cconj(vv[j1]);
-        wc1 = cconj(cfma(pv[j1], a2, vv[j1]));
-      }
-      for (int i = warp; i < m; i += kThreads / 32) {
-        const double2 vi = vv[i], wi = cfma(pv[i], a2, vi);
-        double2* ar = A + (k + 1 + i) * ld + k + 1;
-        if (j0 < m) {
-          const double2 sub = cadd(cmul(vi, wc0), cmul(wi, vc0));
-          double2 a = ar[j0];
+    if (tid < m) A[k * ld + k + 1 + tid] = vv[tid];  // v_k into row k (dead after this step)
+    if (row_live) {  // A22 -= v w^H + w v^H (both triangles)
+      const double2 vi = vv[ri], wi = cfma(pv[ri], a2, vi);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = rh + 8 * u;
+        if (j < m) {
+          const double2 vj = vv[j], wj = cfma(pv[j], a2, vj);
+          const double2 sub = cadd(cmul(vi, cconj(wj)), cmul(wi, cconj(vj)));
+          double2 a = ar[j];
           a.x -= sub.x;
-          a.y = (i == j0) ? 0.0 : a.y - sub.y;
-          ar[j0] = a;
-        }
-        if (j1 < m) {
-          const double2 sub = cadd(cmul(vi, wc1), cmul(wi, vc1));
-          double2 a = ar[j1];
-          a.x -= sub.x;
-          a.y = (i == j1) ? 0.0 : a.y - sub.y;
-          ar[j1] = a;
+          a.y = (ri == j) ? 0.0 : a.y - sub.y;
+          ar[j] = a;
         }
       }
     }
     __syncthreads();
-    tacc2 += clock64() - tc;
-  }
-  if (tid == 0) {
-    g_phase_clock[6] = tacc0;
-    g_phase_clock[7] = tacc1 * 1000000 + tacc2 / 1000;
   }
   if (tid == 0) {
     d[n - 1] = A[(n - 1) * ld + n - 1].x;
@@ -590,11 +565,9 @@ bool herm_eig_small(sk_ctx* ctx, double2* H, int n, double* w, int* info, double
     long long c[8];
     SKB_CUDA(cudaStreamSynchronize(ctx->stream));
     SKB_CUDA(cudaMemcpyFromSymbol(c, g_phase_clock, sizeof c));
-    std::fprintf(stderr,
-                 "[eig n=%d] kcycles tridiag %.1f (norm %.1f p %.1f r2 %.1f) bisect %.1f invit %.1f clusters %.1f "
-                 "back %.1f\n",
-                 n, (c[1] - c[0]) / 1e3, c[6] / 1e3, (c[7] / 1000000) / 1e3, double(c[7] % 1000000), (c[2] - c[1]) / 1e3,
-                 (c[3] - c[2]) / 1e3, (c[4] - c[3]) / 1e3, (c[5] - c[4]) / 1e3);
+    std::fprintf(stderr, "[eig n=%d] kcycles tridiag %.1f bisect %.1f invit %.1f clusters %.1f back %.1f\n", n,
+                 (c[1] - c[0]) / 1e3, (c[2] - c[1]) / 1e3, (c[3] - c[2]) / 1e3, (c[4] - c[3]) / 1e3,
+                 (c[5] - c[4]) / 1e3);
   }
   return true;
 }

@@ -315,10 +315,7 @@ void normalize_standalone(sk_ctx* ctx, float2* maps, i64 n, int q, const float2*
 // 3xTF32 tensor-core products for K2's steering steps (sk_misc.cu): the complex
 // Gram as real [Re; Im] hi/lo (2n x n), the block as [Re, Im] hi/lo (n x 2m),
 // and the recombination of C = [Re; Im] [Re, Im] into the complex product.
-void split_gram_tf32(sk_ctx* ctx, const float2* a, i64 n, float* hi, float* lo);
 void promote_split_gram(sk_ctx* ctx, const float2* a, i64 n, double2* a64, float* hi, float* lo);
-void split_block_tf32(sk_ctx* ctx, const double2* v, i64 n, i64 m, float* hi, float* lo);
-void combine_block(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y);
 void split_block_cat_tf32(sk_ctx* ctx, const double2* v, i64 n, i64 m, float* vc);
 void combine_block_cat(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y);
 void random_block(sk_ctx* ctx, double2* v, i64 n, i64 cols, i64 col0, unsigned int seed);

@@ -394,42 +394,6 @@ __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
   lo = __uint_as_float(l);
 }
-__global__ void split_gram_kernel(const float2* __restrict__ a, i64 n, float* __restrict__ hi, float* __restrict__ lo) {
-  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n * n; e += i64(gridDim.x) * blockDim.x) {
-    const i64 r = e % n, c = e / n;
-    const float2 v = a[e];
-    float h, l;
-    tf32_split(v.x, h, l);
-    hi[r + c * 2 * n] = h;
-    lo[r + c * 2 * n] = l;
-    tf32_split(v.y, h, l);
-    hi[n + r + c * 2 * n] = h;
-    lo[n + r + c * 2 * n] = l;
-  }
-}
-__global__ void split_block_kernel(const double2* __restrict__ v, i64 n, i64 m, float* __restrict__ hi,
-                                   float* __restrict__ lo) {
-  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n * m; e += i64(gridDim.x) * blockDim.x) {
-    const i64 r = e % n, c = e / n;
-    const double2 x = v[e];
-    float h, l;
-    tf32_split(float(x.x), h, l);
-    hi[r + c * n] = h;
-    lo[r + c * n] = l;
-    tf32_split(float(x.y), h, l);
-    hi[r + (c + m) * n] = h;
-    lo[r + (c + m) * n] = l;
-  }
-}
-// Y = (C11 - C22) + i (C12 + C21) from C = [Re A; Im A] [Re V, Im V] (2n x 2m).
-__global__ void combine_block_kernel(const float* __restrict__ c, i64 n, i64 m, double2* __restrict__ y) {
-  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n * m; e += i64(gridDim.x) * blockDim.x) {
-    const i64 r = e % n, k = e / n;
-    const float c11 = c[r + k * 2 * n], c21 = c[n + r + k * 2 * n];
-    const float c12 = c[r + (k + m) * 2 * n], c22 = c[n + r + (k + m) * 2 * n];
-    y[e] = make_double2(double(c11) - double(c22), double(c12) + double(c21));
-  }
-}
 
 // K-concatenated 3xTF32 operand: V' (2n x 4m, column-major) = [[V_hi, V_lo]; [0, V_hi]]
 // so that [A_hi | A_lo] V' = [A_hi V_hi, A_hi V_lo + A_lo V_hi] in ONE GEMM that
@@ -475,7 +439,7 @@ void combine_block_cat(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y) {
 }
 
 // One pass over the c64 Gram: the FP64 copy for the ZGEMM steps and the
-// [Re; Im] TF32 hi/lo split for the 3xTF32 steps (split_gram_kernel layout).
+// [Re; Im] TF32 hi/lo split for the 3xTF32 steps ([Re A; Im A] column blocks, hi then lo).
 __global__ void promote_split_kernel(const float2* __restrict__ a, i64 n, double2* __restrict__ a64,
                                      float* __restrict__ hi, float* __restrict__ lo) {
   for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n * n; e += i64(gridDim.x) * blockDim.x) {
@@ -497,21 +461,6 @@ void promote_split_gram(sk_ctx* ctx, const float2* a, i64 n, double2* a64, float
   SKB_LAUNCH("promote_split");
 }
 
-void split_gram_tf32(sk_ctx* ctx, const float2* a, i64 n, float* hi, float* lo) {
-  split_gram_kernel<<<SKB_GRID(n * n)>>>(a, n, hi, lo);
-  ++ctx->launches;
-  SKB_LAUNCH("split_gram");
-}
-void split_block_tf32(sk_ctx* ctx, const double2* v, i64 n, i64 m, float* hi, float* lo) {
-  split_block_kernel<<<SKB_GRID(n * m)>>>(v, n, m, hi, lo);
-  ++ctx->launches;
-  SKB_LAUNCH("split_block");
-}
-void combine_block(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y) {
-  combine_block_kernel<<<SKB_GRID(n * m)>>>(c, n, m, y);
-  ++ctx->launches;
-  SKB_LAUNCH("combine_block");
-}
 
 void mask_kernel(sk_ctx* ctx, const float* lambda, i64 n, float thr, uint8_t* mask) {
   mask_only_kernel<<<SKB_GRID(n)>>>(lambda, n, thr, mask);

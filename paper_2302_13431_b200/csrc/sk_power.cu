@@ -40,12 +40,6 @@ namespace skb {
 
 namespace {
 
-__device__ __forceinline__ void cmac(float2& acc, float2 m, float2 x) {
-  acc.x = fmaf(m.x, x.x, acc.x);
-  acc.x = fmaf(-m.y, x.y, acc.x);
-  acc.y = fmaf(m.x, x.y, acc.y);
-  acc.y = fmaf(m.y, x.x, acc.y);
-}
 
 // Packed FP32x2 FMA (FFMA2, sm_100): same FMA-pipe rate as FFMA at half the
 // issue slots.  ptxas folds pk(s, s) into a scalar-broadcast operand and
@@ -138,7 +132,7 @@ struct Layout {
   // Q = 32 it measured slower than one row per thread (0.95 vs 0.92 ms, C2:
   // the shared-memory wavefronts barely drop and the shuffles add latency).
   static constexpr bool kTile = TILE_ != 0;
-  static constexpr int kTR = 4, kTC = QP / 4;
+  static constexpr int kTC = QP / 4;  // tile: 4 rows x kTC columns
   // float2 per v row: column group g starts at g (kTC + 2) in the tiled
   // layout (16-B aligned, the four groups on disjoint banks), else QP + 2.
   static constexpr int kStride = kTile ? QP + 8 : QP + 2;
@@ -627,7 +621,6 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       float xr = 0.f, xi = 0.f;
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
-        const int p = prow + r * TPV;
         const float2 rc = rcv[r];
         xr += vp[r].x * rc.x + vp[r].y * rc.y;  // conj(v) * recon
         xi += vp[r].x * rc.y - vp[r].y * rc.x;

@@ -908,27 +908,13 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   e.n = n;
   e.full = false;
   double2* A = ctx->arena.get<double2>("eig:A", n * n);
-  // SKB_EARLY_GEMM: steering products as 3xTF32 tensor-core GEMMs (default),
-  // plain FP32 CGEMM ("fp32"), or single TF32 / BF16 (measured to slow convergence).
-  static const bool tf32x3 = [] {
-    const char* v = std::getenv("SKB_EARLY_GEMM");
-    return !v || std::string(v) == "tf32x3";
-  }();
-  float* ghi = nullptr;
-  float* glo = nullptr;
-  // SKB_TF32_CAT=0: three GEMMs (hi.hi, hi.lo, lo.hi); default one GEMM over
-  // the K-concatenated [A_hi | A_lo] (the split Gram is stored that way).
-  static const bool tf32_cat = [] {
-    const char* v = std::getenv("SKB_TF32_CAT");
-    return !v || std::atoi(v) != 0;
-  }();
-  if (tf32x3) {
-    ghi = ctx->arena.get<float>("ss:gcat", 4 * n * n);
-    glo = ghi + 2 * n * n;
-    promote_split_gram(ctx, gram, n, A, ghi, glo);  // FP64 copy + split in one pass
-  } else {
-    c64_to_c128(ctx, gram, A, n * n);
-  }
+  // Steering products as 3xTF32 tensor-core GEMMs over the K-concatenated
+  // split Gram [A_hi | A_lo] (measured: plain FP32 CGEMM slower; single TF32
+  // or BF16 double the step count, the wanted subspace reaching down to
+  // ratio^2 * lambda_1; three separate hi/lo GEMMs read the split Gram 3x).
+  float* ghi = ctx->arena.get<float>("ss:gcat", 4 * n * n);
+  float* glo = ghi + 2 * n * n;
+  promote_split_gram(ctx, gram, n, A, ghi, glo);  // FP64 copy + split in one pass
   laps.lap("promote");
   // Per-size hints from the previous call: block size and the number of
   // orthogonalised iterations before the (single) Rayleigh-Ritz check.
@@ -990,64 +976,19 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
     bool body_ok = true;
     auto body = [&]() {
       for (int i = 0; i < q_plan; ++i) {
-        if (i + 2 < q_plan && tf32x3) {
-          // 3xTF32 on tensor cores: one real GEMM [Re A; Im A] [Re V, Im V] per
-          // hi/lo combination (hi.hi + hi.lo + lo.hi), FP32-level accuracy.
+        if (i + 2 < q_plan) {
+          // 3xTF32 on tensor cores: [A_hi | A_lo] (2n x 2n) [[V_hi, V_lo]; [0, V_hi]]
+          // (2n x 4b), the split Gram read once per step.
           const float one = 1.f, zero = 0.f;
-          if (tf32_cat) {
-            // [A_hi | A_lo] (2n x 2n) [[V_hi, V_lo]; [0, V_hi]] (2n x 4b): the split
-            // Gram is read once per step instead of three times.
-            float* vcat = ctx->arena.get<float>("ss:vcat", 2 * n * 4 * bcap);
-            float* ccat = ctx->arena.get<float>("ss:ccat", 2 * n * 4 * bcap);
-            split_block_cat_tf32(ctx, V, n, b, vcat);
-            check_cublas(cublasGemmEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(2 * n), int(4 * b), int(2 * n), &one,
-                                      ghi, CUDA_R_32F, int(2 * n), vcat, CUDA_R_32F, int(2 * n), &zero, ccat,
-                                      CUDA_R_32F, int(2 * n), CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT),
-                         "GemmEx(3xTF32 cat)");
-            ++ctx->lib_calls;
-            combine_block_cat(ctx, ccat, n, b, Y);
-          } else {
-            float* vh = ctx->arena.get<float>("ss:vh", n * 2 * bcap);
-            float* vl = ctx->arena.get<float>("ss:vl", n * 2 * bcap);
-            float* cc = ctx->arena.get<float>("ss:cc", 2 * n * 2 * bcap);
-            split_block_tf32(ctx, V, n, b, vh, vl);
-            const float* as[3] = {ghi, ghi, glo};
-            const float* bs[3] = {vh, vl, vh};
-            for (int g = 0; g < 3; ++g) {
-              check_cublas(cublasGemmEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(2 * n), int(2 * b), int(n), &one,
-                                        as[g], CUDA_R_32F, int(2 * n), bs[g], CUDA_R_32F, int(n),
-                                        g == 0 ? &zero : &one, cc, CUDA_R_32F, int(2 * n),
-                                        CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT),
-                           "GemmEx(3xTF32)");
-              ++ctx->lib_calls;
-            }
-            combine_block(ctx, cc, n, b, Y);
-          }
-          laps.lap("gemm32");
-        } else if (i + 2 < q_plan) {
-          // Early iterations only steer the span: FP32 CGEMM on the fp32 Gram
-          // (its rounding ~1e-7 is removed by the FP64 iterations that follow);
-          // orthonormalisation stays FP64 (kappa(A V)^2 exceeds 1/eps_fp32).
-          float2* V32 = ctx->arena.get<float2>("ss:V32", n * bcap);
-          float2* Y32 = ctx->arena.get<float2>("ss:Y32", n * bcap);
-          c128_to_c64(ctx, V, V32, n * b);
-          const cuComplex one = make_cuComplex(1.f, 0.f), zero = make_cuComplex(0.f, 0.f);
-          // FP32 (SKB_EARLY_GEMM=tf32 / bf16 select tensor-core modes; measured to
-          // need ~2x the iterations: the wanted subspace reaches down to
-          // ratio^2 * lambda_1, below their rounding relative to lambda_1;
-          // the BF16x9 emulation does not take complex operands).
-          static const cublasComputeType_t early = [] {
-            const char* v = std::getenv("SKB_EARLY_GEMM");
-            if (v && std::string(v) == "tf32") return CUBLAS_COMPUTE_32F_FAST_TF32;  // single TF32
-            if (v && std::string(v) == "bf16") return CUBLAS_COMPUTE_32F_FAST_16BF;
-            return CUBLAS_COMPUTE_32F;
-          }();
-          check_cublas(cublasGemmEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(n), int(b), int(n), &one, gram,
-                                    CUDA_C_32F, int(n), V32, CUDA_C_32F, int(n), &zero, Y32, CUDA_C_32F, int(n),
-                                    early, CUBLAS_GEMM_DEFAULT),
-                       "GemmEx(subspace)");
+          float* vcat = ctx->arena.get<float>("ss:vcat", 2 * n * 4 * bcap);
+          float* ccat = ctx->arena.get<float>("ss:ccat", 2 * n * 4 * bcap);
+          split_block_cat_tf32(ctx, V, n, b, vcat);
+          check_cublas(cublasGemmEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(2 * n), int(4 * b), int(2 * n), &one,
+                                    ghi, CUDA_R_32F, int(2 * n), vcat, CUDA_R_32F, int(2 * n), &zero, ccat,
+                                    CUDA_R_32F, int(2 * n), CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT),
+                       "GemmEx(3xTF32 cat)");
           ++ctx->lib_calls;
-          c64_to_c128(ctx, Y32, Y, n * b);
+          combine_block_cat(ctx, ccat, n, b, Y);
           laps.lap("gemm32");
         } else {
           zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);  // Y = A V
