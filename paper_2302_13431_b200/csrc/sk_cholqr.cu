@@ -73,8 +73,14 @@ __host__ __device__ constexpr int tile_j(int t) {
 template <bool HERM, int GM = 0>
 __global__ void __cluster_dims__(kQCluster, 1, 1) __launch_bounds__(kQGramThreads)
     gram64_kernel(const double2* __restrict__ x, const double2* __restrict__ y, i64 n, int rows,
-                  double2* __restrict__ cpart, unsigned* __restrict__ counter, double2* __restrict__ out) {
+                  double2* __restrict__ cpart, unsigned* __restrict__ counter, double2* __restrict__ out, i64 sx) {
   constexpr int NT = HERM ? 10 : 16;
+  // batch (multislice K2): slice blockIdx.y, its own partials, ticket and output
+  x += i64(blockIdx.y) * sx;
+  y += i64(blockIdx.y) * sx;
+  out += i64(blockIdx.y) * kQ * kQ;
+  cpart += i64(blockIdx.y) * (gridDim.x / kQCluster) * NT * kQGramThreads;
+  counter += blockIdx.y;
   constexpr int PER = NT * kQGramThreads / kQCluster;  // elements each cluster rank reduces
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* xs = reinterpret_cast<double2*>(smem_raw);  // [kQStage][kQLd]
@@ -246,6 +252,11 @@ template <int MODE>
 __global__ void __launch_bounds__(kQCholThreads) chol64_kernel(const double2* __restrict__ s_in,
                                                                double2* __restrict__ l_out,
                                                                double2* __restrict__ dinv_out, int* flag) {
+  // batch (multislice K2): one CTA per slice
+  s_in += i64(blockIdx.x) * kQ * kQ;
+  l_out += i64(blockIdx.x) * kQ * kQ;
+  dinv_out += i64(blockIdx.x) * 4 * 256;
+  flag += 3 * blockIdx.x;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* Ls = reinterpret_cast<double2*>(smem_raw);  // [64][kQLd], L (lower)
   __shared__ double2 colb[2][4][kQ];                    // block s of L (four columns), double-buffered
@@ -328,7 +339,10 @@ __global__ void __launch_bounds__(kQCholThreads) chol64_kernel(const double2* __
 // X (n x 64 column-major) <- X L^{-H}; `rows` rows per CTA, 16 threads per row.
 __global__ void __launch_bounds__(1024) trsm64_kernel(double2* __restrict__ x, i64 n, int rows,
                                                       const double2* __restrict__ l,
-                                                      const double2* __restrict__ dinv) {
+                                                      const double2* __restrict__ dinv, i64 sx) {
+  x += i64(blockIdx.y) * sx;  // batch: slice blockIdx.y
+  l += i64(blockIdx.y) * kQ * kQ;
+  dinv += i64(blockIdx.y) * 4 * 256;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* Ls = reinterpret_cast<double2*>(smem_raw);  // [64][kQLd]
   double2* Ds = Ls + kQ * kQLd;                         // [4][16][17]
@@ -416,60 +430,71 @@ __global__ void __launch_bounds__(1024) trsm64_kernel(double2* __restrict__ x, i
   }
 }
 
+// Ticket counters of the gram64 reductions, one per slice of a batch (each
+// launch leaves its counter at zero again).
+constexpr i64 kMaxBatch = 4096;
 unsigned* gram_counter(sk_ctx* ctx) {
   static const char* kName = "cq:counter";
   auto it = ctx->arena_zeroed.find(kName);
   if (it != ctx->arena_zeroed.end()) return static_cast<unsigned*>(it->second);
-  unsigned* p = ctx->arena.get<unsigned>(kName, 1);
-  SKB_CUDA(cudaMemsetAsync(p, 0, sizeof(unsigned), ctx->stream));
+  unsigned* p = ctx->arena.get<unsigned>(kName, kMaxBatch);
+  SKB_CUDA(cudaMemsetAsync(p, 0, kMaxBatch * sizeof(unsigned), ctx->stream));
   ctx->arena_zeroed[kName] = p;
   return p;
 }
 
 template <bool HERM>
-void launch_gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, double2* out) {
+void launch_gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, double2* out, i64 batch = 1, i64 sx = 0) {
+  if (batch > kMaxBatch) fail(SK_ERR_DIM, "gram64: batch too large");
   constexpr int NT = HERM ? 10 : 16;
-  const int target = std::max(kQCluster, (ctx->sm_count / kQCluster) * kQCluster);
+  // one wave of CTAs over the whole batch: ~sm_count CTAs per slice alone,
+  // fewer (more rows each) when many slices share the launch
+  const i64 per_slice = std::max<i64>(1, 2 * i64(ctx->sm_count) / std::max<i64>(batch, 1));
+  const int target = int(std::max<i64>(kQCluster, std::min<i64>(ctx->sm_count, per_slice) / kQCluster * kQCluster));
   const int rows = int(std::max<i64>(1, (n + target - 1) / target));
   i64 ctas = (n + rows - 1) / rows;
   ctas = ((ctas + kQCluster - 1) / kQCluster) * kQCluster;
   const i64 ncl = ctas / kQCluster;
-  double2* cpart = ctx->arena.get<double2>(HERM ? "cq:part_h" : "cq:part_x", ncl * NT * kQGramThreads);
+  double2* cpart = ctx->arena.get<double2>(HERM ? "cq:part_h" : "cq:part_x", batch * ncl * NT * kQGramThreads);
   const size_t smem = size_t((HERM ? 1 : 2) * kQStage * kQLd + NT * kQGramThreads) * sizeof(double2);
   set_smem_limit(reinterpret_cast<const void*>(gram64_kernel<HERM>), smem);
-  gram64_kernel<HERM><<<unsigned(ctas), kQGramThreads, smem, ctx->stream>>>(x, y, n, rows, cpart, gram_counter(ctx),
-                                                                          out);
+  gram64_kernel<HERM><<<dim3(unsigned(ctas), unsigned(batch)), kQGramThreads, smem, ctx->stream>>>(
+      x, y, n, rows, cpart, gram_counter(ctx), out, sx);
   ++ctx->launches;
   SKB_LAUNCH("gram64_kernel");
 }
 
 }  // namespace
 
-void gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, double2* out) {
+void gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, double2* out, i64 batch, i64 sx) {
   if (x == y)
-    launch_gram64<true>(ctx, x, x, n, out);
+    launch_gram64<true>(ctx, x, x, n, out, batch, sx);
   else
-    launch_gram64<false>(ctx, x, y, n, out);
+    launch_gram64<false>(ctx, x, y, n, out, batch, sx);
 }
 
-void cholqr64(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag) {
-  double2* S = ctx->arena.get<double2>("cq:S", kQ * kQ);
-  double2* L = ctx->arena.get<double2>("cq:L", kQ * kQ);
-  double2* D = ctx->arena.get<double2>("cq:D", 4 * 256);
+void cholqr64(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag, i64 batch, i64 sx) {
+  double2* S = ctx->arena.get<double2>("cq:S", batch * kQ * kQ);
+  double2* L = ctx->arena.get<double2>("cq:L", batch * kQ * kQ);
+  double2* D = ctx->arena.get<double2>("cq:D", batch * 4 * 256);
   const size_t smem_c = size_t(kQ * kQLd) * sizeof(double2);
   static const int mode = std::getenv("SKB_CHOL64_MODE") ? std::atoi(std::getenv("SKB_CHOL64_MODE")) : 0;
   auto kern = mode == 1 ? chol64_kernel<1> : mode == 2 ? chol64_kernel<2> : chol64_kernel<0>;
   set_smem_limit(reinterpret_cast<const void*>(kern), smem_c);
-  const int rows = int(std::min<i64>(64, std::max<i64>(1, (n + ctx->sm_count - 1) / ctx->sm_count)));
+  // rows per trsm CTA: every CTA stages L and the diagonal inverses (80 KB), so
+  // a batch takes the 64-row maximum (a single slice spreads over the SMs)
+  const i64 cta_target = std::max<i64>(1, i64(ctx->sm_count) / std::max<i64>(batch, 1));
+  const int rows = int(std::min<i64>(64, std::max<i64>(1, (n + cta_target - 1) / cta_target)));
   const unsigned threads = unsigned(((rows * 16 + 31) / 32) * 32);
   const size_t smem_t = size_t(kQ * kQLd + 4 * 16 * 17 + rows * kQLd) * sizeof(double2);
   set_smem_limit(reinterpret_cast<const void*>(trsm64_kernel), smem_t);
   for (int p = 0; p < passes; ++p) {
-    launch_gram64<true>(ctx, x, x, n, S);
-    kern<<<1, kQCholThreads, smem_c, ctx->stream>>>(S, L, D, flag);
+    launch_gram64<true>(ctx, x, x, n, S, batch, sx);
+    kern<<<unsigned(batch), kQCholThreads, smem_c, ctx->stream>>>(S, L, D, flag);
     ++ctx->launches;
     SKB_LAUNCH("chol64_kernel");
-    trsm64_kernel<<<unsigned((n + rows - 1) / rows), threads, smem_t, ctx->stream>>>(x, n, rows, L, D);
+    trsm64_kernel<<<dim3(unsigned((n + rows - 1) / rows), unsigned(batch)), threads, smem_t, ctx->stream>>>(
+        x, n, rows, L, D, sx);
     ++ctx->launches;
     SKB_LAUNCH("trsm64_kernel");
   }

@@ -176,6 +176,10 @@ template <int NF>
 __global__ void __launch_bounds__(kThreads) herm_eig_kernel(double2* __restrict__ H, int n_arg, double* __restrict__ w,
                                                              double floor_rel, int* __restrict__ info) {
   const int n = NF > 0 ? NF : n_arg;
+  // batch (multislice K2): one CTA per slice
+  H += size_t(blockIdx.x) * n * n;
+  w += size_t(blockIdx.x) * n;
+  info += 3 * blockIdx.x;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int ld = n + 1;  // padded row stride (double2) of the full Hermitian A (bank skew)
   const int xs = n + 1;  // padded row stride of X
@@ -546,18 +550,18 @@ size_t herm_eig_smem(int n) {
 
 }  // namespace
 
-bool herm_eig_small(sk_ctx* ctx, double2* H, int n, double* w, int* info, double floor_rel) {
+bool herm_eig_small(sk_ctx* ctx, double2* H, int n, double* w, int* info, double floor_rel, int batch) {
   if (n < 1 || n > kMaxN) return false;
   const size_t smem = herm_eig_smem(n);
   if (n == 64) {
     set_smem_limit(reinterpret_cast<const void*>(herm_eig_kernel<64>), smem);
-    herm_eig_kernel<64><<<1, kThreads, smem, ctx->stream>>>(H, n, w, floor_rel, info);
+    herm_eig_kernel<64><<<unsigned(batch), kThreads, smem, ctx->stream>>>(H, n, w, floor_rel, info);
   } else if (n == 32) {  // the 32-column block of small Grams (C1)
     set_smem_limit(reinterpret_cast<const void*>(herm_eig_kernel<32>), smem);
-    herm_eig_kernel<32><<<1, kThreads, smem, ctx->stream>>>(H, n, w, floor_rel, info);
+    herm_eig_kernel<32><<<unsigned(batch), kThreads, smem, ctx->stream>>>(H, n, w, floor_rel, info);
   } else {
     set_smem_limit(reinterpret_cast<const void*>(herm_eig_kernel<0>), smem);
-    herm_eig_kernel<0><<<1, kThreads, smem, ctx->stream>>>(H, n, w, floor_rel, info);
+    herm_eig_kernel<0><<<unsigned(batch), kThreads, smem, ctx->stream>>>(H, n, w, floor_rel, info);
   }
   ++ctx->launches;
   SKB_LAUNCH("herm_eig_kernel");

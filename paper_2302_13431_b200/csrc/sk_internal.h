@@ -315,19 +315,23 @@ void normalize_standalone(sk_ctx* ctx, float2* maps, i64 n, int q, const float2*
 // 3xTF32 tensor-core products for K2's steering steps (sk_misc.cu): the complex
 // Gram as real [Re; Im] hi/lo (2n x n), the block as [Re, Im] hi/lo (n x 2m),
 // and the recombination of C = [Re; Im] [Re, Im] into the complex product.
-void promote_split_gram(sk_ctx* ctx, const float2* a, i64 n, double2* a64, float* hi, float* lo);
-void split_block_cat_tf32(sk_ctx* ctx, const double2* v, i64 n, i64 m, float* vc);
-void combine_block_cat(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y);
-void random_block(sk_ctx* ctx, double2* v, i64 n, i64 cols, i64 col0, unsigned int seed);
+// Batched forms (multislice K2): `batch` slices at strides s* (elements) in one launch.
+void promote_split_gram(sk_ctx* ctx, const float2* a, i64 n, double2* a64, float* hi, float* lo, i64 batch = 1,
+                        i64 sa = 0, i64 sh = 0);
+void split_block_cat_tf32(sk_ctx* ctx, const double2* v, i64 n, i64 m, float* vc, i64 batch = 1, i64 sv = 0,
+                          i64 svc = 0);
+void combine_block_cat(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y, i64 batch = 1, i64 sc = 0, i64 sy = 0);
+void random_block(sk_ctx* ctx, double2* v, i64 n, i64 cols, i64 col0, unsigned int seed, i64 batch = 1, i64 sv = 0);
 void ritz_residuals(sk_ctx* ctx, const double2* y, const double2* v, const double* theta, i64 n, i64 cols,
-                    double* res);
+                    double* res, i64 batch = 1, i64 sb = 0, i64 sw = 0);
 void shift_negate(sk_ctx* ctx, const double2* a, double2* m, i64 n, double shift);
 void cross_gram(sk_ctx* ctx, const double2* x, const double2* y, i64 n, int b, double2* out);
 // b = 64 block kernels (sk_cholqr.cu): X^H Y (X^H X when y == x) into a
 // 64 x 64 column-major matrix, and `passes` CholQR passes X <- X L^{-H}
 // (one-CTA Cholesky; a non-positive pivot raises *flag).
-void gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, double2* out);
-void cholqr64(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag);
+void gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, double2* out, i64 batch = 1, i64 sx = 0);
+// flag: per-slice int at flag[3 * slice] (the nullspace info triple's flag slot)
+void cholqr64(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag, i64 batch = 1, i64 sx = 0);
 void chol_inv(sk_ctx* ctx, const double2* s, int b, double2* minv, int* flag);
 void cholesky_small(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag);
 // One-CTA Hermitian eigensolver (sk_eig.cu) for b <= 64: eigenvalues ascending
@@ -335,7 +339,8 @@ void cholesky_small(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag)
 // non-finite result.  Returns false (nothing launched) for larger b.
 // Clusters of close eigenvalues lying entirely below floor_rel * ||H|| are
 // only orthonormalised, not refined to individual eigenvectors.
-bool herm_eig_small(sk_ctx* ctx, double2* H, int n, double* w, int* info, double floor_rel = 0.0);
+// batch: H [batch][n][n], w [batch][n], info[3 * slice]
+bool herm_eig_small(sk_ctx* ctx, double2* H, int n, double* w, int* info, double floor_rel = 0.0, int batch = 1);
 // X (n x b) <- X L^{-H} for L lower (column-major, POTRF output), one thread
 // per row; b in {32, 48, 64}, returns false (nothing launched) otherwise.
 bool trsm_rows_lower(sk_ctx* ctx, double2* x, i64 n, int b, const double2* l);

@@ -210,7 +210,8 @@ __device__ __forceinline__ unsigned int mix32(unsigned int x) {
   x ^= x >> 16;
   return x;
 }
-__global__ void random_block_kernel(double2* __restrict__ v, i64 n, i64 cols, i64 col0, unsigned int seed) {
+__global__ void random_block_kernel(double2* __restrict__ v, i64 n, i64 cols, i64 col0, unsigned int seed, i64 sv) {
+  v += i64(blockIdx.y) * sv;  // batch: the same start block in every slice
   const i64 total = n * cols;
   for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
     const i64 c = e / n + col0, r = e % n;
@@ -225,7 +226,12 @@ __global__ void random_block_kernel(double2* __restrict__ v, i64 n, i64 cols, i6
 
 // res[c] = || Y[:,c] - theta[c] V[:,c] ||^2  (one block per column)
 __global__ void ritz_residual_kernel(const double2* __restrict__ y, const double2* __restrict__ v,
-                                     const double* __restrict__ theta, i64 n, double* __restrict__ res) {
+                                     const double* __restrict__ theta, i64 n, double* __restrict__ res, i64 sb,
+                                     i64 sw) {
+  y += i64(blockIdx.y) * sb;
+  v += i64(blockIdx.y) * sb;
+  theta += i64(blockIdx.y) * sw;
+  res += i64(blockIdx.y) * sw;
   const i64 c = blockIdx.x;
   const double t = theta[c];
   double acc = 0.0;
@@ -263,14 +269,20 @@ __global__ void shift_negate_kernel(const double2* __restrict__ a, double2* __re
 
 #define SKB_GRID(n) blocks_for(n), kT, 0, ctx->stream
 
-void random_block(sk_ctx* ctx, double2* v, i64 n, i64 cols, i64 col0, unsigned int seed) {
-  random_block_kernel<<<SKB_GRID(n * cols)>>>(v, n, cols, col0, seed);
+// 2-D grid for `batch` slices: x covers one slice's elements, y the slices.
+inline dim3 batch_grid(i64 per_slice, i64 batch) {
+  return dim3(std::max(1u, std::min(blocks_for(per_slice), unsigned(std::max<i64>(1, 4096 / std::max<i64>(batch, 1))))),
+              unsigned(batch));
+}
+
+void random_block(sk_ctx* ctx, double2* v, i64 n, i64 cols, i64 col0, unsigned int seed, i64 batch, i64 sv) {
+  random_block_kernel<<<batch_grid(n * cols, batch), kT, 0, ctx->stream>>>(v, n, cols, col0, seed, sv);
   ++ctx->launches;
   SKB_LAUNCH("random_block");
 }
 void ritz_residuals(sk_ctx* ctx, const double2* y, const double2* v, const double* theta, i64 n, i64 cols,
-                    double* res) {
-  ritz_residual_kernel<<<unsigned(cols), 256, 0, ctx->stream>>>(y, v, theta, n, res);
+                    double* res, i64 batch, i64 sb, i64 sw) {
+  ritz_residual_kernel<<<dim3(unsigned(cols), unsigned(batch)), 256, 0, ctx->stream>>>(y, v, theta, n, res, sb, sw);
   ++ctx->launches;
   SKB_LAUNCH("ritz_residual");
 }
@@ -398,7 +410,10 @@ __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
 // K-concatenated 3xTF32 operand: V' (2n x 4m, column-major) = [[V_hi, V_lo]; [0, V_hi]]
 // so that [A_hi | A_lo] V' = [A_hi V_hi, A_hi V_lo + A_lo V_hi] in ONE GEMM that
 // reads the split Gram once ([Re, Im] column blocks of width m inside each half).
-__global__ void split_block_cat_kernel(const double2* __restrict__ v, i64 n, i64 m, float* __restrict__ vc) {
+__global__ void split_block_cat_kernel(const double2* __restrict__ v, i64 n, i64 m, float* __restrict__ vc, i64 sv,
+                                       i64 svc) {
+  v += i64(blockIdx.y) * sv;
+  vc += i64(blockIdx.y) * svc;
   for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n * m; e += i64(gridDim.x) * blockDim.x) {
     const i64 r = e % n, c = e / n;
     const double2 x = v[e];
@@ -417,7 +432,10 @@ __global__ void split_block_cat_kernel(const double2* __restrict__ v, i64 n, i64
   }
 }
 // Y from C' = [A_hi | A_lo] V' (2n x 4m): C = C'[:, :2m] + C'[:, 2m:], then as combine_block.
-__global__ void combine_block_cat_kernel(const float* __restrict__ c, i64 n, i64 m, double2* __restrict__ y) {
+__global__ void combine_block_cat_kernel(const float* __restrict__ c, i64 n, i64 m, double2* __restrict__ y, i64 sc,
+                                         i64 sy) {
+  c += i64(blockIdx.y) * sc;
+  y += i64(blockIdx.y) * sy;
   for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n * m; e += i64(gridDim.x) * blockDim.x) {
     const i64 r = e % n, k = e / n, ld = 2 * n, h = 2 * m * ld;
     const double c11 = double(c[r + k * ld]) + double(c[h + r + k * ld]);
@@ -427,13 +445,13 @@ __global__ void combine_block_cat_kernel(const float* __restrict__ c, i64 n, i64
     y[e] = make_double2(c11 - c22, c12 + c21);
   }
 }
-void split_block_cat_tf32(sk_ctx* ctx, const double2* v, i64 n, i64 m, float* vc) {
-  split_block_cat_kernel<<<SKB_GRID(n * m)>>>(v, n, m, vc);
+void split_block_cat_tf32(sk_ctx* ctx, const double2* v, i64 n, i64 m, float* vc, i64 batch, i64 sv, i64 svc) {
+  split_block_cat_kernel<<<batch_grid(n * m, batch), kT, 0, ctx->stream>>>(v, n, m, vc, sv, svc);
   ++ctx->launches;
   SKB_LAUNCH("split_block_cat");
 }
-void combine_block_cat(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y) {
-  combine_block_cat_kernel<<<SKB_GRID(n * m)>>>(c, n, m, y);
+void combine_block_cat(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y, i64 batch, i64 sc, i64 sy) {
+  combine_block_cat_kernel<<<batch_grid(n * m, batch), kT, 0, ctx->stream>>>(c, n, m, y, sc, sy);
   ++ctx->launches;
   SKB_LAUNCH("combine_block_cat");
 }
@@ -441,7 +459,11 @@ void combine_block_cat(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y) {
 // One pass over the c64 Gram: the FP64 copy for the ZGEMM steps and the
 // [Re; Im] TF32 hi/lo split for the 3xTF32 steps ([Re A; Im A] column blocks, hi then lo).
 __global__ void promote_split_kernel(const float2* __restrict__ a, i64 n, double2* __restrict__ a64,
-                                     float* __restrict__ hi, float* __restrict__ lo) {
+                                     float* __restrict__ hi, float* __restrict__ lo, i64 sa, i64 sh) {
+  a += i64(blockIdx.y) * sa;
+  a64 += i64(blockIdx.y) * sa;
+  hi += i64(blockIdx.y) * sh;
+  lo += i64(blockIdx.y) * sh;
   for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < n * n; e += i64(gridDim.x) * blockDim.x) {
     const i64 r = e % n, c = e / n;
     const float2 v = a[e];
@@ -455,8 +477,9 @@ __global__ void promote_split_kernel(const float2* __restrict__ a, i64 n, double
     lo[n + r + c * 2 * n] = l;
   }
 }
-void promote_split_gram(sk_ctx* ctx, const float2* a, i64 n, double2* a64, float* hi, float* lo) {
-  promote_split_kernel<<<SKB_GRID(n * n)>>>(a, n, a64, hi, lo);
+void promote_split_gram(sk_ctx* ctx, const float2* a, i64 n, double2* a64, float* hi, float* lo, i64 batch, i64 sa,
+                        i64 sh) {
+  promote_split_kernel<<<batch_grid(n * n, batch), kT, 0, ctx->stream>>>(a, n, a64, hi, lo, sa, sh);
   ++ctx->launches;
   SKB_LAUNCH("promote_split");
 }

@@ -20,6 +20,7 @@
 #include <functional>
 #include <cmath>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
 #include <thread>
 
@@ -1153,6 +1154,145 @@ Eig run_nullspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, int solv
   return run_eigh(ctx, gram, n, ratio);
 }
 
+// ---------------------------------------------------------------- K2 batched
+// Multislice (sk_estimate_maps_batched): the subspace solver of
+// run_eigh_subspace run in lockstep over `batch` slices of one Gram size, so
+// that its small latency-bound kernels (CholQR, Ritz eigensolver) run one CTA
+// set per slice side by side instead of one slice at a time: strided-batched
+// 3xTF32 / ZGEMM products, gram64 / chol64 / trsm64 and the Ritz eigensolver
+// with the slice on the grid's batch axis.  Same start block, step plan and
+// convergence test per slice as the single-slice solver (the plan is the
+// shared per-size hint).  Slices that do not pass the test in the planned
+// round are reported in ok[] = 0 for the caller's single-slice fallback.
+// Buffers live in arena slots suffixed by `set` (two sets alternate, so a
+// batch's signal bases stay valid while the next batch is solved).
+void run_eigh_subspace_batched(sk_ctx* ctx, const float2* grams, i64 batch, i64 n, double ratio, int set,
+                               std::vector<Eig>& eigs, std::vector<char>& ok) {
+  const std::string sfx = ":" + std::to_string(set);
+  constexpr i64 b = 64;  // the batched CholQR kernels (sk_cholqr.cu) are b = 64, n >= 1024
+  const i64 nn = n * n, nb = n * b;
+  auto& hint = ctx->subspace_hint;
+  int q_plan = 3;
+  auto it_h = hint.find(n);
+  if (it_h != hint.end()) q_plan = it_h->second.plan;
+  double2* A = ctx->arena.get<double2>("bk:A" + sfx, batch * nn);
+  float* gcat = ctx->arena.get<float>("bk:gcat" + sfx, batch * 4 * nn);
+  promote_split_gram(ctx, grams, n, A, gcat, gcat + 2 * nn, batch, nn, 4 * nn);
+  double2* V = ctx->arena.get<double2>("bk:V" + sfx, batch * nb);
+  double2* Y = ctx->arena.get<double2>("bk:Y" + sfx, batch * nb);
+  double2* T = ctx->arena.get<double2>("bk:T" + sfx, batch * nb);
+  double2* H = ctx->arena.get<double2>("bk:H" + sfx, batch * b * b);
+  double* w = ctx->arena.get<double>("bk:w" + sfx, batch * b);
+  double* res = ctx->arena.get<double>("bk:res" + sfx, batch * b);
+  int* info = ctx->arena.get<int>("bk:info" + sfx, batch * 3);
+  float* vcat = ctx->arena.get<float>("bk:vcat" + sfx, batch * 8 * nb);
+  float* ccat = ctx->arena.get<float>("bk:ccat" + sfx, batch * 8 * nb);
+  SKB_CUDA(cudaMemsetAsync(info, 0, size_t(batch) * 3 * sizeof(int), ctx->stream));
+  random_block(ctx, V, n, b, 0, 0x5eed5u, batch, nb);
+  const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+  auto zgemm_b = [&](i64 m, i64 nc, i64 k, const double2* a, i64 lda, i64 sa, const double2* bm, i64 ldb, i64 sbm,
+                     double2* c, i64 ldc, i64 sc) {
+    check_cublas(cublasZgemmStridedBatched(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(m), int(nc), int(k), &one,
+                                           reinterpret_cast<const cuDoubleComplex*>(a), int(lda), sa,
+                                           reinterpret_cast<const cuDoubleComplex*>(bm), int(ldb), sbm, &zero,
+                                           reinterpret_cast<cuDoubleComplex*>(c), int(ldc), sc, int(batch)),
+                 "ZgemmStridedBatched");
+    ++ctx->lib_calls;
+  };
+  for (int i = 0; i < q_plan; ++i) {
+    if (i + 2 < q_plan) {  // 3xTF32 steering step over the K-concatenated split Gram
+      const float f1 = 1.f, f0 = 0.f;
+      split_block_cat_tf32(ctx, V, n, b, vcat, batch, nb, 8 * nb);
+      check_cublas(cublasGemmStridedBatchedEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(2 * n), int(4 * b),
+                                              int(2 * n), &f1, gcat, CUDA_R_32F, int(2 * n), 4 * nn, vcat, CUDA_R_32F,
+                                              int(2 * n), 8 * nb, &f0, ccat, CUDA_R_32F, int(2 * n), 8 * nb,
+                                              int(batch), CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT),
+                   "GemmStridedBatchedEx(3xTF32 cat)");
+      ++ctx->lib_calls;
+      combine_block_cat(ctx, ccat, n, b, Y, batch, 8 * nb, nb);
+    } else {
+      zgemm_b(n, b, n, A, n, nn, V, n, nb, Y, n, nb);  // Y = A V (FP64)
+    }
+    std::swap(V, Y);
+    cholqr64(ctx, V, n, i + 1 == q_plan ? 2 : 1, info + 1, batch, nb);
+  }
+  zgemm_b(n, b, n, A, n, nn, V, n, nb, Y, n, nb);
+  gram64(ctx, V, Y, n, H, batch, nb);  // H = V^H A V
+  herm_eig_small(ctx, H, int(b), w, info, 0.25 * ratio * ratio, int(batch));
+  zgemm_b(n, b, b, V, n, nb, H, b, b * b, T, n, nb);  // V <- V S
+  std::swap(V, T);
+  zgemm_b(n, b, b, Y, n, nb, H, b, b * b, T, n, nb);  // Y <- Y S
+  std::swap(Y, T);
+  ritz_residuals(ctx, Y, V, w, n, b, res, batch, nb, b);
+  std::vector<double> hw(size_t(batch * b)), hres(size_t(batch * b));
+  std::vector<int> hinfo(size_t(batch * 3));
+  SKB_CUDA(cudaMemcpyAsync(hw.data(), w, hw.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  SKB_CUDA(cudaMemcpyAsync(hres.data(), res, hres.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  SKB_CUDA(cudaMemcpyAsync(hinfo.data(), info, hinfo.size() * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  const double tol = 3e-10;  // run_eigh_subspace's test
+  const i64 guard = 8;
+  eigs.assign(size_t(batch), Eig());
+  ok.assign(size_t(batch), 0);
+  int spare_min = 3, failed = 0;
+  for (i64 sl = 0; sl < batch; ++sl) {
+    const double* ws = hw.data() + sl * b;
+    const double* rs = hres.data() + sl * b;
+    if (hinfo[size_t(3 * sl)] || hinfo[size_t(3 * sl + 1)] || hinfo[size_t(3 * sl + 2)]) {
+      ++failed;
+      continue;
+    }
+    const double theta_max = ws[b - 1];
+    if (!(theta_max > 0.0)) {
+      ++failed;
+      continue;
+    }
+    const double c = ratio * ratio * theta_max;
+    i64 m = 0;
+    for (i64 i = 0; i < b; ++i) m += ws[i] >= c ? 1 : 0;
+    double worst = 0.0, rate = 0.0;
+    const bool reaches = ws[0] < 0.5 * c;
+    for (i64 i = 0; i < b; ++i) {
+      if (ws[i] < 0.5 * c) continue;
+      worst = std::max(worst, std::sqrt(std::max(rs[i], 0.0)) / theta_max);
+      rate = std::max(rate, std::max(ws[0], 0.0) / ws[i]);
+    }
+    if (m > b - guard || !reaches || worst > tol || m == 0 || m == n) {
+      ++failed;
+      continue;
+    }
+    int spare = 0;
+    if (rate > 0.0 && rate < 1.0 && worst > 0.0)
+      spare = std::max(0, int(std::floor(std::log(0.8 * tol / worst) / std::log(1.0 / rate))));
+    spare_min = std::min(spare_min, spare);
+    Eig& e = eigs[size_t(sl)];
+    e.n = n;
+    e.full = false;
+    e.k = m;
+    e.rank = n - m;
+    e.usig = V + sl * nb + (b - m) * n;  // the last m Ritz columns (ascending theta)
+    e.sigma1 = std::sqrt(theta_max);
+    e.cut = ratio * e.sigma1;
+    e.iterations = q_plan + 1;
+    e.block = int(b);
+    e.spectrum.assign(size_t(n), 0.0);
+    for (i64 i = 0; i < b; ++i) e.spectrum[size_t(i)] = std::sqrt(std::max(0.0, ws[b - 1 - i]));
+    ok[size_t(sl)] = 1;
+  }
+  // plan for the next batch of this size: one step more after any failure
+  // (never planned again at the failing size), else the spare steps every
+  // slice showed, at most one per batch
+  auto& h = hint[n];
+  if (failed) {
+    h.failed_plan = std::max(h.failed_plan, q_plan);
+    h.plan = q_plan + 1;
+  } else if (spare_min > 0 && q_plan > 3 && q_plan - 1 > h.failed_plan) {
+    h.plan = q_plan - 1;
+  } else {
+    h.plan = q_plan;
+  }
+}
+
 // ---------------------------------------------------------------- K3
 // Lag kernels from the signal subspace, expanded onto the grid as packed planes.
 Planes run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims& grid, i64 slab0 = 0,
@@ -2069,7 +2209,8 @@ struct ProbeIn {
 int estimate_impl(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_t* center_offset, int64_t q,
                   const sk_c64* calib, const int64_t* full_dims, const sk_config* cfg, sk_c64* maps, float* lambda,
                   uint8_t* mask, double* spectrum, sk_provenance* prov, sk_c64* gram_out, sk_c64* field_out,
-                  sk_c64* raw_maps_out, float* raw_lambda_out, const ProbeIn* pin) {
+                  sk_c64* raw_maps_out, float* raw_lambda_out, const ProbeIn* pin,
+                  const PipelineOut::Basis* basis_in = nullptr) {
   return guarded([&] {
     require_ctx(ctx);
     if (ndim < 1) fail(SK_ERR_DIM, "stack needs at least one axis");
@@ -2174,6 +2315,11 @@ int estimate_impl(sk_ctx* ctx, int ndim, const int64_t* calib_dims, const int64_
       probe.field_vals = ctx->arena.get<double2>("probe:field_vals", std::max<i64>(1, nf_idx));
       probe.raw_lambda = opl.dev;
       po.probe = &probe;
+    }
+    PipelineOut::Basis basis_copy;
+    if (basis_in) {  // multislice: the slice's signal basis from the batched K2
+      basis_copy = *basis_in;
+      po.basis = &basis_copy;
     }
     pipeline(ctx, cd, co, q, d_cal, fd, cfg, po, prov);
     if (pin) {
@@ -2458,14 +2604,82 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
     return !v || std::atoi(v) != 0;
   }();
   const bool defer = defer_env && maps && pinned_alias(maps) != nullptr;
+  // Batched K2 (run_eigh_subspace_batched): the calling thread computes the
+  // Grams and signal bases of groups of G slices on the main context while
+  // the lanes run K3-K5 of the previous group with those bases.  Eligible:
+  // FFT Gram, subspace nullspace solver without certificate, n >= 1024 (the
+  // b = 64 batched CholQR), a signal space that fits the 64-column block.
+  i64 n_gram = 0;
+  Support sup{};
+  bool bk2 = false;
+  if (cfg && lanes >= 2 && slices >= 2) {
+    const int rc = guarded([&] {
+      sup = make_support(cfg->kernel, cfg->tau, ndim);
+      n_gram = q * sup.count;
+    });
+    const auto it = ctx->subspace_hint.find(n_gram);
+    static const bool bk2_env = [] {
+      const char* v = std::getenv("SKB_BATCHED_K2");
+      return !v || std::atoi(v) != 0;
+    }();
+    // Not with pinned host outputs (defer): the host link bounds those calls and
+    // the lanes' own K2 measured faster there (C3 e2e 121 vs 100 M voxels/s).
+    bk2 = bk2_env && !defer && rc == SK_OK && cfg->gram == 1 && (cfg->eig_solver == 0 || cfg->eig_solver == 2) &&
+          !cfg->certify && n_gram >= 1024 && n_gram <= 8192 &&
+          (it == ctx->subspace_hint.end() || it->second.m + 16 <= 64);
+  }
+  // Groups: a small first group (the lanes start after it, not after a full
+  // one), then G slices each.  Uniform G on C3 (128 slices): 8: 71, 16: 62.7,
+  // 32: 60.3, 64: 59.9 ms per call; G = 32 keeps the two buffer sets at
+  // ~3.5 GB each.
+  const i64 G = bk2 ? std::min<i64>(slices, 32) : slices;
+  std::vector<i64> gstart;  // group g = slices [gstart[g], gstart[g + 1])
+  if (bk2) {
+    const i64 first = std::min<i64>(slices, std::max<i64>(2, G / 4));
+    gstart.push_back(0);
+    for (i64 s0 = first; s0 < slices; s0 += G) gstart.push_back(s0);
+    gstart.push_back(slices);
+  }
+  const i64 groups = bk2 ? i64(gstart.size()) - 1 : 0;
+  std::vector<PipelineOut::Basis> bases(size_t(bk2 ? slices : 0));
+  std::vector<char> has_basis(size_t(bk2 ? slices : 0), 0);
+  std::vector<cudaEvent_t> gev(size_t(groups), nullptr);
+  std::mutex mu;
+  std::condition_variable cv;
+  i64 groups_ready = 0;
+  bool abort_k2 = false;
+  std::vector<i64> done(size_t(groups), 0);
+  auto group_size = [&](i64 g) { return gstart[size_t(g + 1)] - gstart[size_t(g)]; };
+  auto group_of = [&](i64 s) { return i64(std::upper_bound(gstart.begin(), gstart.end(), s) - gstart.begin()) - 1; };
   auto work = [&](int lane) {
     sk_ctx* sub = lanes == 1 ? ctx : ctx->lanes[size_t(lane)];
     cudaSetDevice(ctx->device);
     sub->defer_d2h = defer ? 1 : 0;
     for (i64 s = lane; s < slices; s += lanes) {
-      const int rc = sk_estimate_maps(sub, ndim, calib_dims, center_offset, q, calib + s * ncal, full_dims, cfg,
-                                      maps ? maps + s * q * nfull : nullptr, lambda ? lambda + s * nfull : nullptr,
-                                      mask ? mask + s * nfull : nullptr, nullptr, prov ? prov + s : nullptr);
+      const PipelineOut::Basis* basis = nullptr;
+      i64 g = -1;
+      if (bk2) {
+        g = group_of(s);
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return groups_ready > g || abort_k2; });
+        if (abort_k2) break;
+        lk.unlock();
+        if (cudaStreamWaitEvent(sub->stream, gev[size_t(g)], 0) != cudaSuccess) {
+          rcs[size_t(lane)] = SK_ERR_CUDA;
+          errs[size_t(lane)] = "multislice: waiting on the batched nullspace failed";
+          break;
+        }
+        if (has_basis[size_t(s)]) basis = &bases[size_t(s)];
+      }
+      const int rc = estimate_impl(sub, ndim, calib_dims, center_offset, q, calib + s * ncal, full_dims, cfg,
+                                   maps ? maps + s * q * nfull : nullptr, lambda ? lambda + s * nfull : nullptr,
+                                   mask ? mask + s * nfull : nullptr, nullptr, prov ? prov + s : nullptr, nullptr,
+                                   nullptr, nullptr, nullptr, nullptr, basis);
+      if (bk2) {
+        std::lock_guard<std::mutex> lk(mu);
+        ++done[size_t(g)];
+        cv.notify_all();
+      }
       if (rc != SK_OK) {
         rcs[size_t(lane)] = rc;
         errs[size_t(lane)] = sk_last_error();
@@ -2479,12 +2693,91 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
       errs[size_t(lane)] = "multislice: deferred device-to-host copy failed";
     }
   };
+  // The batched K2 producer (calling thread): group g's Grams + bases into
+  // buffer set g % 2, after the lanes finished group g - 2 with that set.
+  std::string k2_err;
+  const auto t_start = std::chrono::steady_clock::now();
+  auto produce = [&]() -> int {
+    return guarded([&] {
+      const Dims cdl = cd;
+      const i64 nn = n_gram * n_gram;
+      const double ratio = cfg->nullspace_threshold;
+      for (i64 g = 0; g < groups; ++g) {
+        {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [&] { return g < 2 || done[size_t(g - 2)] == group_size(g - 2); });
+        }
+        const int set = int(g % 2);
+        const i64 gs = group_size(g), s0 = gstart[size_t(g)];
+        float2* grams = ctx->arena.get<float2>("bk:grams:" + std::to_string(set), G * nn);
+        float2* cal_dev = nullptr;
+        const bool cal_on_dev = is_device_ptr(calib);
+        if (!cal_on_dev) {
+          cal_dev = ctx->arena.get<float2>("bk:cal:" + std::to_string(set), G * ncal);
+          SKB_CUDA(cudaMemcpyAsync(cal_dev, calib + s0 * ncal, size_t(gs * ncal) * sizeof(float2),
+                                   cudaMemcpyHostToDevice, ctx->stream));
+        }
+        for (i64 i = 0; i < gs; ++i) {
+          const float2* c = cal_on_dev ? reinterpret_cast<const float2*>(calib) + (s0 + i) * ncal : cal_dev + i * ncal;
+          check_calib(cdl, q, sup);
+          run_gram(ctx, cdl, q, c, sup, grams + i * nn);
+        }
+        // first batch of this size: one single-slice solve settles the step plan
+        if (ctx->subspace_hint.find(n_gram) == ctx->subspace_hint.end())
+          (void)run_nullspace(ctx, grams, n_gram, ratio, 2, false, false);
+        std::vector<Eig> eg;
+        std::vector<char> okv;
+        run_eigh_subspace_batched(ctx, grams, gs, n_gram, ratio, set, eg, okv);
+        for (i64 i = 0; i < gs; ++i) {
+          if (!okv[size_t(i)]) continue;  // the lane runs this slice's own K1 + K2
+          bases[size_t(s0 + i)].usig = eg[size_t(i)].usig;
+          bases[size_t(s0 + i)].k = eg[size_t(i)].k;
+          bases[size_t(s0 + i)].sigma1 = eg[size_t(i)].sigma1;
+          has_basis[size_t(s0 + i)] = 1;
+        }
+        SKB_CUDA(cudaEventCreateWithFlags(&gev[size_t(g)], cudaEventDisableTiming));
+        SKB_CUDA(cudaEventRecord(gev[size_t(g)], ctx->stream));
+        if (std::getenv("SKB_PROFILE_NS")) {
+          SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+          int nok = 0;
+          for (char c : okv) nok += c;
+          std::fprintf(stderr, "[bk2] group %lld ready at %.3f ms, %d/%lld batched\n", (long long)g,
+                       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(),
+                       nok, (long long)gs);
+        }
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          groups_ready = g + 1;
+        }
+        cv.notify_all();
+      }
+    });
+  };
+  int rc_k2 = SK_OK;
   if (lanes == 1) {
     work(0);
   } else {
     std::vector<std::thread> pool;
     for (int l = 0; l < lanes; ++l) pool.emplace_back(work, l);
+    if (bk2) {
+      rc_k2 = produce();
+      if (rc_k2 != SK_OK) {
+        k2_err = g_last_error;
+        std::lock_guard<std::mutex> lk(mu);
+        abort_k2 = true;
+        cv.notify_all();
+      }
+    }
     for (auto& t : pool) t.join();
+  }
+  for (auto& e : gev)
+    if (e) cudaEventDestroy(e);
+  if (bk2 && std::getenv("SKB_PROFILE_NS"))
+    std::fprintf(stderr, "[bk2] all slices done at %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+  if (rc_k2 != SK_OK) {
+    g_last_error = k2_err;
+    return rc_k2;
   }
   for (int l = 0; l < lanes; ++l)
     if (rcs[size_t(l)] != SK_OK) {

@@ -638,6 +638,30 @@ def test_batched_multislice_equals_per_slice(K):
         assert (mask[s] == ref.support_mask).mean() > 0.9999, s
 
 
+def test_batched_multislice_batched_nullspace(K):
+    """C3-size slices (Q = 32, n = 1568): the batched call solves the slices'
+    nullspaces in lockstep (strided-batched products, one CTA set per slice for
+    CholQR and the Ritz eigensolver, run_eigh_subspace_batched) and hands each
+    lane its slice's signal basis; the maps must match per-slice calls."""
+    from paper_2302_13431_b200 import phantom
+    case = phantom.generate("C3", slices=40)
+    spec = case.spec
+    cfg = K.PipelineConfig(kernel=spec.kernel, tau=spec.tau, nullspace_threshold=spec.nullspace_threshold,
+                           power_iters=spec.power_iters, grid=K.GRID_REDUCED,
+                           grid_pad=spec.grid_dims[0] - spec.calib[0])
+    maps, lam, mask, info = K.api.estimate_maps_batched(case.calib, case.center_offset, spec.full_dims, cfg)
+    for s in (0, 17, 31, 32, 39):  # both buffer sets, first and last group
+        ref = K.estimate_maps(K.Calib(case.calib[s], case.center_offset), spec.full_dims, cfg,
+                              want_spectrum=False)
+        assert info[s]["rank"] == ref.nullspace_rank
+        d_maps = PM.rel_fro(maps[s], ref.maps)
+        d_lam = float(np.abs(lam[s] - ref.lambda_min_map).max())
+        report("batched_k2_vs_single", slice=s, maps_rel=d_maps, lam_abs=d_lam)
+        assert d_maps < 1e-6, s
+        assert np.allclose(lam[s], ref.lambda_min_map, rtol=1e-6, atol=1e-7), s
+        assert (mask[s] == ref.support_mask).mean() > 0.9999, s
+
+
 # ------------------------------------------------- baseline preset (SURVEY §8f4)
 @pytest.mark.parametrize("shape,tau,dims,q", [(0, 3, (24, 24), 8), (1, 2, (12, 14), 3), (0, 1, (9, 10, 8), 2),
                                               (0, 2, (13,), 4)])
