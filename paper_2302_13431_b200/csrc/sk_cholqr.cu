@@ -89,6 +89,7 @@ __global__ void __cluster_dims__(kQCluster, 1, 1) __launch_bounds__(kQGramThread
   __shared__ int last_flag;
   cg::cluster_group cluster = cg::this_cluster();
   const int tid = threadIdx.x;
+  SKB_DCHECK(blockDim.x == kQGramThreads && gridDim.x % kQCluster == 0);
   const int r = tid >> 4, c = tid & 15;
   const i64 row0 = i64(blockIdx.x) * rows, row1 = min(n, row0 + rows);
   double2 acc[NT];
@@ -252,6 +253,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kQCholThreads) chol64_kernel(const double2* __restrict__ s_in,
                                                                double2* __restrict__ l_out,
                                                                double2* __restrict__ dinv_out, int* flag) {
+  SKB_DCHECK(blockDim.x == kQCholThreads);  // warp w owns columns 4w..4w+3 of the 64
   // batch (multislice K2): one CTA per slice
   s_in += i64(blockIdx.x) * kQ * kQ;
   l_out += i64(blockIdx.x) * kQ * kQ;
@@ -348,6 +350,7 @@ __global__ void __launch_bounds__(1024) trsm64_kernel(double2* __restrict__ x, i
   double2* Ds = Ls + kQ * kQLd;                         // [4][16][17]
   double2* Xs = Ds + 4 * 16 * 17;                       // [rows][kQLd]
   const int tid = threadIdx.x, nt = blockDim.x;
+  SKB_DCHECK(rows >= 1 && rows <= 64 && rows * 16 <= nt + 15);  // one half-warp per staged row
   const i64 row0 = i64(blockIdx.x) * rows;
   const int nr = int(min(i64(rows), n - row0));
   // all loads of a thread in flight together (one L2 round trip, not one per element)

@@ -176,6 +176,7 @@ template <int NF>
 __global__ void __launch_bounds__(kThreads) herm_eig_kernel(double2* __restrict__ H, int n_arg, double* __restrict__ w,
                                                              double floor_rel, int* __restrict__ info) {
   const int n = NF > 0 ? NF : n_arg;
+  SKB_DCHECK(n >= 1 && n <= kMaxN && blockDim.x == kThreads);
   // batch (multislice K2): one CTA per slice
   H += size_t(blockIdx.x) * n * n;
   w += size_t(blockIdx.x) * n;

@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(256) expand_col_persist_kernel(const double2* 
   if (cb < nblocks) issue(cb, 0);
   const int p0 = max(jc, 0), P = max(0, N - p0);
   const int S1 = jc > 0 ? max(0, min(min(jc, N), 2 * jc - N + 1)) : 0;
+  SKB_DCHECK(blockDim.x == 32 && blockDim.y == 8 && P + S1 <= items);  // the host sized tab for `items` rows
   // table rows in item order: item t < P is row p0 + t, item P + s is row s
   for (int e = tid; e < (P + S1) * H; e += 256) {
     const int t = e / H, l = e % H;

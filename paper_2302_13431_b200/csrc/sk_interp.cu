@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(256) interp2_sos_kernel(const float2* __restri
   const int logN = logn + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = 1 << logn, N = 2 << logn, T = 1 << logT;
+  SKB_DCHECK(blockDim.x == 256 && (T << logn) <= 16 * 256);  // keep[] below holds 16 values per thread
   C* tw = reinterpret_cast<C*>(smem_raw);
   const int ld = n + n / 16 + 1;
   C* buf = tw + n;

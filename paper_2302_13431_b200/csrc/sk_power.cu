@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
   const int Q = L::QF > 0 ? L::QF : a.q;
   const int h = Q * (Q + 1) / 2;
   const int tile_elems = tile_rows * VPB;  // tile bytes: a multiple of 1 KB
+  SKB_DCHECK(blockDim.x == L::kThreads && h <= tile_rows && Q <= QP);  // every packed read lands in the tile
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw);  // [0..1] hi buffers, [2] lo
   // tile buffers start on a 1 KB boundary (the swizzle pattern follows address bits 4..9)
   float2* gbuf = reinterpret_cast<float2*>(smem_raw + ((smem_u32(smem_raw) + 128 + 1023) & ~1023u) -
