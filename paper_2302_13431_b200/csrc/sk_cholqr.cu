@@ -68,9 +68,7 @@ __host__ __device__ constexpr int tile_j(int t) {
   return HERM ? t - tile_i<HERM>(t) * (tile_i<HERM>(t) + 1) / 2 : t & 3;
 }
 
-// GM (timing experiments): 0 full; 1 stop after the cluster reduction; 2 stop
-// after the per-CTA partials.
-template <bool HERM, int GM = 0>
+template <bool HERM>
 __global__ void __cluster_dims__(kQCluster, 1, 1) __launch_bounds__(kQGramThreads)
     gram64_kernel(const double2* __restrict__ x, const double2* __restrict__ y, i64 n, int rows,
                   double2* __restrict__ cpart, unsigned* __restrict__ counter, double2* __restrict__ out, i64 sx) {
@@ -130,7 +128,6 @@ __global__ void __cluster_dims__(kQCluster, 1, 1) __launch_bounds__(kQGramThread
   }
 #pragma unroll
   for (int t = 0; t < NT; ++t) part[t * kQGramThreads + tid] = acc[t];
-  if (GM == 2) return;
   cluster.sync();
   const int rank = int(cluster.block_rank());
   const int cid = blockIdx.x / kQCluster, ncl = gridDim.x / kQCluster;
@@ -144,10 +141,6 @@ __global__ void __cluster_dims__(kQCluster, 1, 1) __launch_bounds__(kQGramThread
       s.y += p.y;
     }
     cpart[i64(cid) * NT * kQGramThreads + g] = s;
-  }
-  if (GM == 1) {
-    cluster.sync();
-    return;
   }
   __threadfence();
   cluster.sync();
@@ -247,9 +240,6 @@ __device__ __forceinline__ void chol64_factor4(double2 (&a)[4][2], double2 (*pub
     }
 }
 
-// MODE (timing experiments, tools/cholqr_micro.cu): 0 full; 1 no diagonal-block
-// inverses; 2 no factorisation; 3 no rank-4 updates; 4 no block factorisation.
-template <int MODE>
 __global__ void __launch_bounds__(kQCholThreads) chol64_kernel(const double2* __restrict__ s_in,
                                                                double2* __restrict__ l_out,
                                                                double2* __restrict__ dinv_out, int* flag) {
@@ -270,12 +260,12 @@ __global__ void __launch_bounds__(kQCholThreads) chol64_kernel(const double2* __
   for (int c = 0; c < 4; ++c)
 #pragma unroll
     for (int h = 0; h < 2; ++h) a[c][h] = s_in[(lane + 32 * h) + kQ * (j0 + c)];  // S[i][j], coalesced in i
-  if (MODE != 2) {
+  {
     if (w == 0) chol64_factor4(a, colb[0], Ls, rsv, w, lane, flag);
 #pragma unroll 1
     for (int s = 0; s < 15; ++s) {
       __syncthreads();
-      if (w > s && MODE != 3) {
+      if (w > s) {
         const double2 (*cb)[kQ] = colb[s & 1];
         double2 li[4][2];
 #pragma unroll
@@ -301,7 +291,7 @@ __global__ void __launch_bounds__(kQCholThreads) chol64_kernel(const double2* __
           }
         }
       }
-      if (w == s + 1 && MODE != 4) chol64_factor4(a, colb[(s + 1) & 1], Ls, rsv, w, lane, flag);
+      if (w == s + 1) chol64_factor4(a, colb[(s + 1) & 1], Ls, rsv, w, lane, flag);
     }
   }
   __syncthreads();
@@ -312,7 +302,7 @@ __global__ void __launch_bounds__(kQCholThreads) chol64_kernel(const double2* __
   // Dinv_b = L_bb^{-1}: warp b, lane c < 16 forms column c by forward
   // substitution with the column in registers (x_m = 0 for m < c, so the
   // sums need no bounds; the newest term enters last: short chain).
-  if (MODE != 1 && w < 4 && lane < 16) {
+  if (w < 4 && lane < 16) {
     const int b = w, c = lane, o = 16 * b;
     double2 xv[16];
 #pragma unroll
@@ -481,8 +471,7 @@ void cholqr64(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag, i64 batch, 
   double2* L = ctx->arena.get<double2>("cq:L", batch * kQ * kQ);
   double2* D = ctx->arena.get<double2>("cq:D", batch * 4 * 256);
   const size_t smem_c = size_t(kQ * kQLd) * sizeof(double2);
-  static const int mode = std::getenv("SKB_CHOL64_MODE") ? std::atoi(std::getenv("SKB_CHOL64_MODE")) : 0;
-  auto kern = mode == 1 ? chol64_kernel<1> : mode == 2 ? chol64_kernel<2> : chol64_kernel<0>;
+  auto kern = chol64_kernel;
   set_smem_limit(reinterpret_cast<const void*>(kern), smem_c);
   // rows per trsm CTA: every CTA stages L and the diagonal inverses (80 KB), so
   // a batch takes the 64-row maximum (a single slice spreads over the SMs)

@@ -21,9 +21,6 @@ namespace {
 
 constexpr int kMaxLb = 29;  // 4*tau+1 for tau <= 7
 
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
 __device__ __forceinline__ float2 cconj_mul(float2 a, float2 b) {  // conj(a) * b
   return make_float2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
 }
@@ -208,15 +205,14 @@ void gram_pairs_launch(sk_ctx* ctx, const float2* spectra, const GramGeom& g_in,
   const size_t smem = gram_pairs_smem(g);
   if (smem > 227 * 1024) fail(9, "gram_fft: padded calibration too large for the on-chip lag contraction");
   // 512 threads when the axis-0 contraction is unstaged (3-D pads: one CTA per
-  // SM by shared memory, the column loop needs the warps), 256 otherwise.
-  static const int t2d = [] { const char* v = std::getenv("SKB_GRAM_THREADS_2D"); return v ? std::atoi(v) : 256; }();
-  const int threads = g.stage_prod ? t2d : 512;
-  static const bool generic = std::getenv("SKB_GRAM_GENERIC") != nullptr;
+  // SM by shared memory, the column loop needs the warps), 256 otherwise
+  // (2-D: 128 / 256 / 512 measured equal).
+  const int threads = g.stage_prod ? 256 : 512;
   auto go = [&](auto kern) {
     set_smem_limit(reinterpret_cast<const void*>(kern), smem);
     kern<<<npairs, threads, smem, ctx->stream>>>(spectra, g, d_pairs, d_off, d_tw, gram);
   };
-  switch (generic ? 0 : g.lb) {
+  switch (g.lb) {  // lag-box extent fixed at compile time for the BASELINE radii, else run time
     case 9: go(gram_pairs_kernel<9>); break;
     case 13: go(gram_pairs_kernel<13>); break;
     case 17: go(gram_pairs_kernel<17>); break;

@@ -332,8 +332,6 @@ void cross_gram(sk_ctx* ctx, const double2* x, const double2* y, i64 n, int b, d
 void gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, double2* out, i64 batch = 1, i64 sx = 0);
 // flag: per-slice int at flag[3 * slice] (the nullspace info triple's flag slot)
 void cholqr64(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag, i64 batch = 1, i64 sx = 0);
-void chol_inv(sk_ctx* ctx, const double2* s, int b, double2* minv, int* flag);
-void cholesky_small(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag);
 // One-CTA Hermitian eigensolver (sk_eig.cu) for b <= 64: eigenvalues ascending
 // into w, eigenvectors overwrite H (column-major); info[0] = 1 on a
 // non-finite result.  Returns false (nothing launched) for larger b.
@@ -341,17 +339,5 @@ void cholesky_small(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag)
 // only orthonormalised, not refined to individual eigenvectors.
 // batch: H [batch][n][n], w [batch][n], info[3 * slice]
 bool herm_eig_small(sk_ctx* ctx, double2* H, int n, double* w, int* info, double floor_rel = 0.0, int batch = 1);
-// X (n x b) <- X L^{-H} for L lower (column-major, POTRF output), one thread
-// per row; b in {32, 48, 64}, returns false (nothing launched) otherwise.
-bool trsm_rows_lower(sk_ctx* ctx, double2* x, i64 n, int b, const double2* l);
-// One CholQR pass on X (n x b, b <= 64) with own kernels only: cross_gram,
-// one-CTA Cholesky + triangular inverse (M = L^{-1}, flag raised on a
-// non-positive pivot), X <- X M^H.  Returns false (nothing launched) for b > 64.
-bool cholqr_pass(sk_ctx* ctx, double2* x, i64 n, int b, double2* s, double2* m, int* flag);
-// One-CTA blocked Cholesky (b <= 64): S = L L^H, L lower column-major like POTRF; *flag on a bad pivot.
-void cholesky_blocked(sk_ctx* ctx, const double2* s, int b, double2* l, int* flag);
-// One CholQR pass on X (n x b, b <= 118): cross_gram + one-CTA lazy Cholesky +
-// warp-per-row triangular solve; no host synchronisation (flag raised on failure).
-void cholqr_fast(sk_ctx* ctx, double2* x, i64 n, int b, double2* s, double2* l, int* flag);
 
 }  // namespace skb

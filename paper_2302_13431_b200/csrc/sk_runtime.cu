@@ -182,11 +182,6 @@ struct Out {
 };
 
 Dims dims_of(int nd, const int64_t* d) { return Dims(d, d + nd); }
-std::string key_of(const Dims& d) {
-  std::string s;
-  for (i64 e : d) s += std::to_string(e) + "x";
-  return s;
-}
 
 // Upload an N x L matrix (row-major) followed by its transpose (L x N).
 float2* upload_matrix(sk_ctx* ctx, const std::string& key, int N, int L, const std::vector<std::complex<double>>& m) {
@@ -272,25 +267,6 @@ void separable(sk_ctx* ctx, const float2* in, float2* out, i64 batch, const Dims
     cur[size_t(a)] = out_ext[size_t(a)];
     src = dst;
   }
-}
-
-// (cos, sign*sin)(2 pi l (j - j0) / N) for j < N, l = 1..H (row-major [j][l-1]).
-float2* symdft_table(sk_ctx* ctx, int N, int H, i64 j0, int sign) {
-  const std::string key = "symcs:" + std::to_string(N) + ":" + std::to_string(H) + ":" + std::to_string(j0) + ":" +
-                          std::to_string(sign);
-  auto it = ctx->matrices.mats.find(key);
-  if (it != ctx->matrices.mats.end()) return it->second;
-  std::vector<float2> h(size_t(N) * H);
-  for (int j = 0; j < N; ++j)
-    for (int l = 1; l <= H; ++l) {
-      const std::complex<double> z = cis(+1, i64(l) * (j - j0), N);
-      h[size_t(j) * H + (l - 1)] = make_float2(float(z.real()), float(sign * z.imag()));
-    }
-  float2* d = nullptr;
-  SKB_CUDA(cudaMalloc(&d, h.size() * sizeof(float2)));
-  SKB_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice));
-  ctx->matrices.mats[key] = d;
-  return d;
 }
 
 // FP64 (cos, sign*sin)(2 pi l (j - j0) / N) for j < N, l = 1..H ([j][l-1]).
@@ -560,12 +536,8 @@ void zgemm(sk_ctx* ctx, cublasOperation_t ta, cublasOperation_t tb, i64 m, i64 n
            const double2* b, i64 ldb, double2* c, i64 ldc) {
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
   // Gauss 3M form (three real DGEMMs instead of four) for the large n x b x n
-  // products; SKB_ZGEMM3M=0 keeps plain ZGEMM (experiment knob)
-  static const bool use3m = [] {
-    const char* v = std::getenv("SKB_ZGEMM3M");
-    return !v || std::atoi(v) != 0;
-  }();
-  auto gemm = (use3m && m * n * k >= (i64(1) << 26)) ? cublasZgemm3m : cublasZgemm;
+  // products (C2 K2 1.376 -> 1.342 ms, C5 9.08 -> 8.28 ms against ZGEMM).
+  auto gemm = m * n * k >= (i64(1) << 26) ? cublasZgemm3m : cublasZgemm;
   check_cublas(gemm(ctx->cublas, ta, tb, int(m), int(n), int(k), &one,
                            reinterpret_cast<const cuDoubleComplex*>(a), int(lda),
                            reinterpret_cast<const cuDoubleComplex*>(b), int(ldb), &zero,
@@ -605,168 +577,68 @@ bool cholqr(sk_ctx* ctx, double2* x, i64 n, i64 b) {
   return h_info == 0;
 }
 
-constexpr i64 kSmallBlockMax = 112;  // custom one-CTA Cholesky limit (shared memory)
-
 // Eigendecomposition of the b x b Rayleigh-Ritz matrix (lower triangle used),
-// eigenvalues ascending into w, eigenvectors overwrite H.  Default: cuSOLVER
-// Jacobi (ZHEEVJ, tol 1e-14); SKB_SMALL_EIG=dc / batched select
-// divide-and-conquer (Xsyevd) / XsyevBatched for comparison.
+// eigenvalues ascending into w, eigenvectors overwrite H: the own one-CTA
+// solver for b <= 64 (sk_eig.cu; 0.27 ms at b = 64 against ~1 ms for
+// cuSOLVER's Jacobi, divide-and-conquer or batched solvers, all measured),
+// cuSOLVER Jacobi (ZHEEVJ, tol 1e-14) above.
 void small_heev(sk_ctx* ctx, double2* H, i64 b, double* w, int* d_info, double floor_rel = 0.0) {
-  static const int mode = [] {
-    const char* v = std::getenv("SKB_SMALL_EIG");
-    if (!v) return 3;  // default: own one-CTA solver for b <= 64, cuSOLVER Jacobi above
-    if (std::string(v) == "dc") return 0;
-    if (std::string(v) == "jacobi") return 1;
-    if (std::string(v) == "batched") return 2;
-    return 3;
-  }();
-  if (mode == 3 && herm_eig_small(ctx, H, int(b), w, d_info, floor_rel)) return;
-  const bool jacobi = mode == 1 || mode == 3;
-  if (mode == 2) {
-    size_t dbytes = 0, hbytes = 0;
-    check_cusolver(cusolverDnXsyevBatched_bufferSize(ctx->cusolver, ctx->cusolver_params, CUSOLVER_EIG_MODE_VECTOR,
-                                                     CUBLAS_FILL_MODE_LOWER, b, CUDA_C_64F, H, b, CUDA_R_64F, w,
-                                                     CUDA_C_64F, &dbytes, &hbytes, 1),
-                   "XsyevBatched_bufferSize");
-    void* dwork = ctx->arena.get("ss:syevb_work", dbytes);
-    static thread_local std::vector<unsigned char> hwork;
-    hwork.resize(std::max<size_t>(hbytes, 1));
-    check_cusolver(cusolverDnXsyevBatched(ctx->cusolver, ctx->cusolver_params, CUSOLVER_EIG_MODE_VECTOR,
-                                          CUBLAS_FILL_MODE_LOWER, b, CUDA_C_64F, H, b, CUDA_R_64F, w, CUDA_C_64F,
-                                          dwork, dbytes, hwork.data(), hbytes, d_info, 1),
-                   "XsyevBatched");
-  } else if (jacobi) {
-    if (!ctx->syevj) {
-      check_cusolver(cusolverDnCreateSyevjInfo(&ctx->syevj), "CreateSyevjInfo");
-      check_cusolver(cusolverDnXsyevjSetTolerance(ctx->syevj, 1e-14), "syevjSetTolerance");
-      check_cusolver(cusolverDnXsyevjSetMaxSweeps(ctx->syevj, 30), "syevjSetMaxSweeps");
-    }
-    syevjInfo_t params = ctx->syevj;
-    int lwork = 0;
-    check_cusolver(cusolverDnZheevj_bufferSize(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
-                                               int(b), reinterpret_cast<cuDoubleComplex*>(H), int(b), w, &lwork,
-                                               params),
-                   "Zheevj_bufferSize");
-    auto* work = ctx->arena.get<cuDoubleComplex>("ss:syevj_work", std::max(lwork, 1));
-    check_cusolver(cusolverDnZheevj(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, int(b),
-                                    reinterpret_cast<cuDoubleComplex*>(H), int(b), w, work, lwork, d_info, params),
-                   "Zheevj");
-  } else {
-    size_t dbytes = 0, hbytes = 0;
-    check_cusolver(cusolverDnXsyevd_bufferSize(ctx->cusolver, ctx->cusolver_params, CUSOLVER_EIG_MODE_VECTOR,
-                                               CUBLAS_FILL_MODE_LOWER, b, CUDA_C_64F, H, b, CUDA_R_64F, w,
-                                               CUDA_C_64F, &dbytes, &hbytes),
-                   "Xsyevd_bufferSize(ritz)");
-    void* dwork = ctx->arena.get("ss:syevd_work", dbytes);
-    static thread_local std::vector<unsigned char> hwork;
-    hwork.resize(std::max<size_t>(hbytes, 1));
-    check_cusolver(cusolverDnXsyevd(ctx->cusolver, ctx->cusolver_params, CUSOLVER_EIG_MODE_VECTOR,
-                                    CUBLAS_FILL_MODE_LOWER, b, CUDA_C_64F, H, b, CUDA_R_64F, w, CUDA_C_64F, dwork,
-                                    dbytes, hwork.data(), hbytes, d_info),
-                   "Xsyevd(ritz)");
+  if (herm_eig_small(ctx, H, int(b), w, d_info, floor_rel)) return;
+  if (!ctx->syevj) {
+    check_cusolver(cusolverDnCreateSyevjInfo(&ctx->syevj), "CreateSyevjInfo");
+    check_cusolver(cusolverDnXsyevjSetTolerance(ctx->syevj, 1e-14), "syevjSetTolerance");
+    check_cusolver(cusolverDnXsyevjSetMaxSweeps(ctx->syevj, 30), "syevjSetMaxSweeps");
   }
+  syevjInfo_t params = ctx->syevj;
+  int lwork = 0;
+  check_cusolver(cusolverDnZheevj_bufferSize(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, int(b),
+                                             reinterpret_cast<cuDoubleComplex*>(H), int(b), w, &lwork, params),
+                 "Zheevj_bufferSize");
+  auto* work = ctx->arena.get<cuDoubleComplex>("ss:syevj_work", std::max(lwork, 1));
+  check_cusolver(cusolverDnZheevj(ctx->cusolver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, int(b),
+                                  reinterpret_cast<cuDoubleComplex*>(H), int(b), w, work, lwork, d_info, params),
+                 "Zheevj");
   ++ctx->lib_calls;
 }
 
-// Orthonormalise X (n x b) in place by CholQR2.  b <= kSmallBlockMax uses the
-// custom no-sync kernels (cross_gram, chol_inv) + ZGEMM; larger blocks use
-// cuBLAS HERK/TRSM + cuSOLVER POTRF.  Returns false only on a detected
-// (synchronous path) failure; the fast path raises `flag` instead.
+// Orthonormalise X (n x b) in place by `passes` CholQR passes.  b = 64 and
+// n >= 1024: the own kernels of sk_cholqr.cu (gram64, chol64, trsm64; their
+// fixed costs pay from n ~ 1k).  b <= 256 otherwise: own cross_gram + cuSOLVER
+// POTRF + cuBLAS TRSM (measured against own one-CTA Cholesky variants and a
+// lane-pair TRSM: faster once graphs hide the library's host cost).  Larger
+// blocks: cuBLAS HERK + POTRF + TRSM with a synchronous check.  Returns false
+// only on a detected (synchronous path) failure; the other paths raise `flag`.
 bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int passes = 2) {
   (void)tmp;
-  // default: cuSOLVER POTRF + cuBLAS TRSM (measured fastest at b = 64..96);
-  // SKB_SMALL_CHOL=fast selects the own lazy Cholesky + row TRSM (b <= 112),
-  // =custom the own blocked Cholesky + cuBLAS TRSM.
-  // Default at b = 64: sk_cholqr.cu (three own kernels per pass).  Otherwise
-  // own cross_gram + cuSOLVER POTRF + cuBLAS TRSM.  SKB_SMALL_CHOL=pass64 selects the
-  // library-free pass (one-CTA Cholesky + inverse; measured slower: the
-  // 64-pivot chain on one SM is latency-bound).
-  static const int chol_mode = [] {
-    const char* v = std::getenv("SKB_SMALL_CHOL");
-    if (v && std::string(v) == "fast") return 0;
-    if (v && std::string(v) == "custom") return 2;
-    if (v && std::string(v) == "pass64") return 3;
-    if (v && std::string(v) == "blocked") return 4;
-    if (v && std::string(v) == "lib") return 1;
-    return 5;
-  }();
-  if (chol_mode == 5 && b == 64 && n >= 1024) {  // own gram + one-CTA Cholesky + blocked row TRSM (fixed costs pay from n ~ 1k)
+  if (b == 64 && n >= 1024) {
     cholqr64(ctx, x, n, passes, flag);
     return true;
   }
-  if (chol_mode == 3 && b <= 64) {
-    double2* S = ctx->arena.get<double2>("ss:S", b * b);
-    double2* Mi = ctx->arena.get<double2>("ss:Minv", b * b);
-    for (int pass = 0; pass < passes; ++pass) cholqr_pass(ctx, x, n, int(b), S, Mi, flag);
-    return true;
-  }
-  const bool own_blocked = chol_mode == 4 && b <= 64;
-  const bool lib_chol = !own_blocked && (chol_mode == 1 || chol_mode == 3 || chol_mode == 5 || b > kSmallBlockMax);
-  if (b > 256 || (chol_mode == 2 && b > kSmallBlockMax)) {
+  if (b > 256) {
     for (int p = 0; p < passes; ++p)
       if (!cholqr(ctx, x, n, b)) return false;
     return true;
   }
   double2* S = ctx->arena.get<double2>("ss:S", b * b);
-  double2* L = ctx->arena.get<double2>("ss:L", b * b);
-  if (chol_mode == 0 && b <= kSmallBlockMax) {
-    for (int pass = 0; pass < passes; ++pass) cholqr_fast(ctx, x, n, int(b), S, L, flag);
-    return true;
-  }
   const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0);
-  static const bool prof = std::getenv("SKB_PROFILE_NS") != nullptr;
-  cudaEvent_t pe[4];
-  auto mark = [&](int i) {
-    if (prof) SKB_CUDA(cudaEventRecord(pe[i], ctx->stream));
-  };
-  if (prof)
-    for (auto& ev : pe) SKB_CUDA(cudaEventCreate(&ev));
   for (int pass = 0; pass < passes; ++pass) {
-    mark(0);
-    cross_gram(ctx, x, x, n, int(b), S);        // S = X^H X
-    mark(1);
-    if (lib_chol) {
-      size_t dbytes = 0, hbytes = 0;
-      check_cusolver(cusolverDnXpotrf_bufferSize(ctx->cusolver, ctx->cusolver_params, CUBLAS_FILL_MODE_LOWER, b,
-                                                 CUDA_C_64F, S, b, CUDA_C_64F, &dbytes, &hbytes),
-                     "Xpotrf_bufferSize");
-      void* dwork = ctx->arena.get("ss:potrf_work", dbytes);
-      static thread_local std::vector<unsigned char> hwork;
-      hwork.resize(std::max<size_t>(hbytes, 1));
-      check_cusolver(cusolverDnXpotrf(ctx->cusolver, ctx->cusolver_params, CUBLAS_FILL_MODE_LOWER, b, CUDA_C_64F, S, b,
-                                      CUDA_C_64F, dwork, dbytes, hwork.data(), hbytes, flag + 1),
-                     "Xpotrf");
-      ++ctx->lib_calls;
-      L = S;
-    } else if (own_blocked) {
-      cholesky_blocked(ctx, S, int(b), L, flag + 1);  // S = L L^H (POTRF layout)
-    } else {
-      cholesky_small(ctx, S, int(b), L, flag);  // S = L L^H
-    }
-    mark(2);
-    // cuBLAS TRSM (measured faster on the device than the own lane-pair
-    // kernel once graphs hide its host cost); SKB_TRSM_OWN=1 selects the latter.
-    static const bool own_trsm = std::getenv("SKB_TRSM_OWN") != nullptr;
-    if (!own_trsm || !trsm_rows_lower(ctx, x, n, int(b), L)) {
-      check_cublas(cublasZtrsm(ctx->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C,
-                               CUBLAS_DIAG_NON_UNIT, int(n), int(b), &one, reinterpret_cast<const cuDoubleComplex*>(L),
-                               int(b), reinterpret_cast<cuDoubleComplex*>(x), int(n)),
-                   "Ztrsm(orth)");  // X <- X L^{-H}
-      ++ctx->lib_calls;
-    }
-    mark(3);
-    if (prof) {
-      SKB_CUDA(cudaEventSynchronize(pe[3]));
-      float a = 0.f, b2 = 0.f, c = 0.f;
-      cudaEventElapsedTime(&a, pe[0], pe[1]);
-      cudaEventElapsedTime(&b2, pe[1], pe[2]);
-      cudaEventElapsedTime(&c, pe[2], pe[3]);
-      std::fprintf(stderr, "[orth b=%lld] gram %.1f us  chol %.1f us  trsm %.1f us\n", (long long)b, a * 1e3, b2 * 1e3,
-                   c * 1e3);
-    }
+    cross_gram(ctx, x, x, n, int(b), S);  // S = X^H X
+    size_t dbytes = 0, hbytes = 0;
+    check_cusolver(cusolverDnXpotrf_bufferSize(ctx->cusolver, ctx->cusolver_params, CUBLAS_FILL_MODE_LOWER, b,
+                                               CUDA_C_64F, S, b, CUDA_C_64F, &dbytes, &hbytes),
+                   "Xpotrf_bufferSize");
+    void* dwork = ctx->arena.get("ss:potrf_work", dbytes);
+    static thread_local std::vector<unsigned char> hwork;
+    hwork.resize(std::max<size_t>(hbytes, 1));
+    check_cusolver(cusolverDnXpotrf(ctx->cusolver, ctx->cusolver_params, CUBLAS_FILL_MODE_LOWER, b, CUDA_C_64F, S, b,
+                                    CUDA_C_64F, dwork, dbytes, hwork.data(), hbytes, flag + 1),
+                   "Xpotrf");
+    check_cublas(cublasZtrsm(ctx->cublas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT,
+                             int(n), int(b), &one, reinterpret_cast<const cuDoubleComplex*>(S), int(b),
+                             reinterpret_cast<cuDoubleComplex*>(x), int(n)),
+                 "Ztrsm(orth)");  // X <- X L^{-H}
+    ctx->lib_calls += 2;
   }
-  if (prof)
-    for (auto& ev : pe) cudaEventDestroy(ev);
   return true;
 }
 
@@ -939,13 +811,6 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   }
   const int first_plan = q_plan;
   int rounds = 0;
-  if (const char* v = std::getenv("SKB_BLOCK")) {  // experiment override
-    const i64 fixed = std::atoll(v);
-    if (fixed > 0) {
-      if (it_h == hint.end() || it_h->second.m + 8 > fixed) q_plan = 3;
-      b = fixed;
-    }
-  }
   b = std::min(b, n);
   const i64 bcap = std::min(n, std::max<i64>(4 * b, 256));
   double2* V = ctx->arena.get<double2>("ss:V", n * bcap);
@@ -1007,8 +872,7 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
       zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);
       laps.lap("gemm64");
       // Rayleigh-Ritz on span(V): H = V^H A V = S diag(w) S^H.
-      static const bool lib_gram = std::getenv("SKB_SMALL_CHOL") != nullptr;
-      if (b == 64 && n >= 1024 && !lib_gram) {
+      if (b == 64 && n >= 1024) {
         gram64(ctx, V, Y, n, H);
       } else if (b <= 256) {
         cross_gram(ctx, V, Y, n, int(b), H);
@@ -1384,10 +1248,9 @@ bool interp_fft_ok(const Dims& low, const Dims& full) {
 // kernel, the outer axes run first and the innermost pass renormalises in
 // the same kernel; returns false when the caller still has to renormalise.
 bool run_interp_renorm(sk_ctx* ctx, const float2* low, float2* out, i64 q, const Dims& low_dims, const Dims& full) {
-  static const bool off = std::getenv("SKB_NO_FUSED_RENORM") != nullptr;
   const int nd = int(low_dims.size());
   const int n = int(low_dims[size_t(nd - 1)]), N = int(full[size_t(nd - 1)]);
-  if (off || !interp_fft_ok(low_dims, full) || N != 2 * n || q > 32 || (q & (q - 1)) || q * n > 4096) return false;
+  if (!interp_fft_ok(low_dims, full) || N != 2 * n || q > 32 || (q & (q - 1)) || q * n > 4096) return false;
   Dims cur = low_dims;
   const float2* src = low;
   int pass = 0;
@@ -1510,15 +1373,9 @@ struct PipelineOut {
 
 // K4 epilogue: voxels with lambda >= this keep the FP32 Rayleigh quotient
 // (||G/|Lambda| || <= 1 for W a projection, so FP32 rounding is ~1e-7 absolute,
-// < 1e-5 relative above 0.25); SKB_RQ32_MIN=0 forces FP64 everywhere.
-// Used on full-resolution map grids only (see the pipeline).
-float rq32_min() {
-  static const float v = [] {
-    const char* e = std::getenv("SKB_RQ32_MIN");
-    return e ? float(std::atof(e)) : 0.25f;
-  }();
-  return v;
-}
+// < 1e-5 relative above 0.25).  Used on full-resolution map grids only (see
+// the pipeline).
+constexpr float kRq32Min = 0.25f;
 
 void validate_config(const sk_config* cfg) {
   if (!cfg) fail(SK_ERR_DIM, "null config");
@@ -1658,7 +1515,7 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
     r.planes = planes; r.planes_lo = pl.lo; r.n = ngrid; r.q = int(q); r.iters = cfg->power_iters;
     r.alpha = 1.f; r.beta = -1.f / float(lam); r.lam_scale = 1.f / float(lam);
     r.maps = out.raw_maps; r.lambda = out.raw_lambda;
-    r.rq32_min = grid != full ? 0.f : rq32_min();
+    r.rq32_min = grid != full ? 0.f : kRq32Min;
     power_iteration(ctx, r);
   }
   PowerArgs pa{};
@@ -1679,7 +1536,7 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   // Not when an interpolation follows: the periodic-sinc interpolation spreads
   // the FP32 path's ~1e-7 absolute error of large-lambda voxels into the small
   // in-support values (measured: C3 in-mask lambda 3.4e-5 -> 5.6e-5 relative).
-  pa.rq32_min = grid != full ? 0.f : rq32_min();  // slabs are interpolated by the caller
+  pa.rq32_min = grid != full ? 0.f : kRq32Min;  // slabs are interpolated by the caller
   if (out.maps_host && !interp && !slab && maps_grid == out.maps) {
     // K4 in voxel chunks (multiples of 8 voxels: 16-byte aligned TMA bases)
     // with the maps copied to the host behind each chunk on a second stream.

@@ -14,6 +14,10 @@ void check_cuda(cudaError_t e, const char* what) {
   }
 }
 void* Arena::get(const std::string&, size_t) { return nullptr; }
+void fail(int, const std::string& m) {
+  std::fprintf(stderr, "%s\n", m.c_str());
+  std::exit(1);
+}
 Arena::~Arena() {}
 void set_smem_limit(const void* f, size_t bytes) {
   check_cuda(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)), "smem");
@@ -88,26 +92,19 @@ int main() {
   const int rows = int((n + 143) / 144);
   const size_t smem_g = size_t(1 * kQStage * kQLd + 10 * kQGramThreads) * sizeof(double2);
   set_smem_limit(reinterpret_cast<const void*>(gram64_kernel<true>), smem_g);
-  auto gram = [&] { gram64_kernel<true><<<144, kQGramThreads, smem_g>>>(x, x, n, rows, cp, counter, S); };
+  auto gram = [&] { gram64_kernel<true><<<144, kQGramThreads, smem_g>>>(x, x, n, rows, cp, counter, S, 0); };
   const size_t smem_c = size_t(kQ * kQLd + 4 * 16 * 17) * sizeof(double2);
-  set_smem_limit(reinterpret_cast<const void*>(chol64_kernel<0>), smem_c);
-  set_smem_limit(reinterpret_cast<const void*>(chol64_kernel<2>), smem_c);
-  auto chol = [&] { chol64_kernel<0><<<1, kQCholThreads, smem_c>>>(S, L, D, flag); };
-  auto chol_nopiv = [&] { chol64_kernel<2><<<1, kQCholThreads, smem_c>>>(S, L, D, flag); };
+  set_smem_limit(reinterpret_cast<const void*>(chol64_kernel), smem_c);
+  auto chol = [&] { chol64_kernel<<<1, kQCholThreads, smem_c>>>(S, L, D, flag); };
   const int trows = 18;
   const size_t smem_t = size_t(kQ * kQLd + 4 * 16 * 17 + trows * kQLd) * sizeof(double2);
   set_smem_limit(reinterpret_cast<const void*>(trsm64_kernel), smem_t);
-  auto trsm = [&] { trsm64_kernel<<<unsigned((n + trows - 1) / trows), 288, smem_t>>>(x, n, trows, L, D); };
+  auto trsm = [&] { trsm64_kernel<<<unsigned((n + trows - 1) / trows), 288, smem_t>>>(x, n, trows, L, D, 0); };
   gram();
   chol();
   cudaDeviceSynchronize();
   std::printf("gram64<herm>     %7.2f us\n", time_it(gram));
-  set_smem_limit(reinterpret_cast<const void*>(gram64_kernel<true, 1>), smem_g);
-  set_smem_limit(reinterpret_cast<const void*>(gram64_kernel<true, 2>), smem_g);
-  std::printf("gram64 no final reduce   %7.2f us\n", time_it([&] { gram64_kernel<true, 1><<<144, kQGramThreads, smem_g>>>(x, x, n, rows, cp, counter, S); }));
-  std::printf("gram64 no cluster reduce %7.2f us\n", time_it([&] { gram64_kernel<true, 2><<<144, kQGramThreads, smem_g>>>(x, x, n, rows, cp, counter, S); }));
   std::printf("chol64           %7.2f us\n", time_it(chol));
-  std::printf("chol64 no pivots %7.2f us\n", time_it(chol_nopiv));
   std::printf("trsm64           %7.2f us  (operates in place; values drift, timing only)\n", time_it(trsm));
   {
     long long* c;
@@ -118,9 +115,5 @@ int main() {
     cudaDeviceSynchronize();
     std::printf("factor4 alone (one warp): %lld cycles per 4-pivot block\n", c[0]);
   }
-  set_smem_limit(reinterpret_cast<const void*>(chol64_kernel<3>), smem_c);
-  set_smem_limit(reinterpret_cast<const void*>(chol64_kernel<4>), smem_c);
-  std::printf("chol64 factor4 only   %7.2f us\n", time_it([&] { chol64_kernel<3><<<1, kQCholThreads, smem_c>>>(S, L, D, flag); }));
-  std::printf("chol64 updates only   %7.2f us\n", time_it([&] { chol64_kernel<4><<<1, kQCholThreads, smem_c>>>(S, L, D, flag); }));
   std::printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
 }
