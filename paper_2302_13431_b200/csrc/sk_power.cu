@@ -313,7 +313,11 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
 #pragma unroll
-        for (int c = 0; c < QP; ++c) m[r][c] = herm_at(gs, prow + r * TPV, c, Q, VPB, vox, tt.swz);
+        for (int c = 0; c < QP; ++c)
+          // compile-time Q: the branch-free read (C2 K4 0.905 -> 0.878 ms, C4 5.62 -> 4.97 ms);
+          // run-time Q keeps the branchy one (the branch-free form spills there)
+          m[r][c] = L::QF > 0 ? herm_at_bf(gs, prow + r * TPV, c, Q, VPB, vox, tt.swz)
+                              : herm_at(gs, prow + r * TPV, c, Q, VPB, vox, tt.swz);
         mc0[r] = m[r][0];
       }
     }
@@ -343,6 +347,11 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
 
     // Publish u into buffer b and its squared norm: returned directly for a
     // single-warp voxel, left as per-warp partials in red2[b] otherwise.
+    // Single-warp voxels return the thread's own partial of ||u||^2: the
+    // butterfly over the voxel's lanes runs at the top of the next iteration,
+    // after its barrier, where ptxas interleaves the shuffle chain with the
+    // matvec's loads and FFMA2s (before the barrier it was exposed: 14% of the
+    // stall samples on C2).
     auto publish = [&](const float2 (&u)[RPT], int b) -> float {
       float x = 0.f;
 #pragma unroll
@@ -352,8 +361,6 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
         x = fmaf(u[r].x, u[r].x, fmaf(u[r].y, u[r].y, x));
       }
       if constexpr (TPV <= 32) {
-#pragma unroll
-        for (int o = TPV / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
         return x;
       } else {
 #pragma unroll
@@ -362,9 +369,14 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
         return 0.f;
       }
     };
+    auto voxel_butterfly = [&](float x) -> float {
+#pragma unroll
+      for (int o = TPV / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      return x;
+    };
     auto published_norm = [&](float own, int b) -> float {
       if constexpr (TPV <= 32) {
-        return own;
+        return own;  // already reduced by voxel_butterfly
       } else {
         float s = 0.f;
 #pragma unroll
@@ -515,6 +527,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     for (int it = 1; it < a.iters; ++it) {
       const int b = it & 1;
       voxel_bar<L>(vox);
+      if constexpr (TPV <= 32) own = voxel_butterfly(own);
       float2 mv[RPT];
       matvec(vb(b), mv);
       // ||u_k||^2 (the previous iteration's shuffle reduction) is consumed only
@@ -537,6 +550,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     int fb = 0;  // buffer that receives the final v
     if (a.iters > 1) {
       voxel_bar<L>(vox);
+      if constexpr (TPV <= 32) own = voxel_butterfly(own);
       const float n2 = published_norm(own, a.iters & 1);
       const bool keep = done || n2 < 1e-28f;
       const float inv = keep ? 0.f : rsqrtf(n2);
