@@ -390,7 +390,13 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     // independent accumulator pairs per row.
     // Complex MAC as two FFMA2: acc += m.x * (v.x, v.y), acc2 += m.y * (v.y, v.x);
     // (M v) = (acc.x - acc2.x, acc.y + acc2.y).
-    auto matvec = [&](const float2* v, float2 (&out)[RPT]) {
+    // side: a value whose butterfly over the voxel's lanes (single-warp voxels)
+    // is spread over the chunks of the product, one shuffle level every few
+    // chunks, so its latency hides behind the FFMA2s (nullptr: none).  For
+    // ||u||^2 in the iteration loop: C2 K4 0.878 -> 0.797 ms, C4 4.97 -> 4.71
+    // ms (the chain issued as one block, before or after the barrier, was
+    // 11-14% of the stall samples; the 48 B of spill it costs are harmless).
+    auto matvec = [&](const float2* v, float2 (&out)[RPT], float* side = nullptr) {
       if constexpr (L::kTile) {
         // 4 x kTC block times v[kTC cg ..]: acc += m.x (v.x, v.y), acc2 += m.y (v.y, v.x)
         // (two accumulators per row: C5 K4 18.5 ms against 22.7 with one)
@@ -454,6 +460,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       float4 buf[D];
 #pragma unroll
       for (int t = 0; t < D; ++t) buf[t] = v4[t];
+      constexpr int LV = TPV <= 32 ? (TPV >= 32 ? 5 : TPV >= 16 ? 4 : TPV >= 8 ? 3 : TPV >= 4 ? 2 : TPV >= 2 ? 1 : 0) : 0;
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
         const float4 vt = buf[t % D];
@@ -466,6 +473,11 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
           ffma2(acc2[r][ka], pk(ma.y, ma.y), pk(vt.y, vt.x));
           ffma2(acc[r][kb], pk(mb.x, mb.x), pk(vt.z, vt.w));
           ffma2(acc2[r][kb], pk(mb.y, mb.y), pk(vt.w, vt.z));
+        }
+        if (side != nullptr) {
+#pragma unroll
+          for (int j = 0; j < LV; ++j)
+            if (t == (j * NT) / LV) *side += __shfl_xor_sync(0xffffffffu, *side, TPV >> (j + 1));
         }
       }
 #pragma unroll
@@ -527,9 +539,11 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     for (int it = 1; it < a.iters; ++it) {
       const int b = it & 1;
       voxel_bar<L>(vox);
-      if constexpr (TPV <= 32) own = voxel_butterfly(own);
       float2 mv[RPT];
-      matvec(vb(b), mv);
+      if constexpr (TPV <= 32 && !L::kTile)
+        matvec(vb(b), mv, &own);  // the butterfly of ||u||^2 rides along
+      else
+        matvec(vb(b), mv);
       // ||u_k||^2 (the previous iteration's shuffle reduction) is consumed only
       // after the products: the empty asm ties it to mv so ptxas cannot hoist
       // the test above the loads, and the reduction overlaps the matvec.
@@ -598,7 +612,10 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       // FP32 value kept (voxel_sum below still runs: its shuffles span voxels)
     } else {
       const double2* vd = vds + vox * QP;
+      double xd1 = 0.0;  // second accumulator: alternate packed elements (C5 K4 18.7 -> 18.1 ms)
+#pragma unroll 2
       for (int e = local; e < h; e += TPV) {
+        double& acc = ((e / TPV) & 1) ? xd1 : xd;
         const int pc = pct[e], pp = pc >> 8, cc = pc & 0xff;
         const float2 hv = gs[swz_at(e * VPB + vox, tt.swz)];
         double mx = double(hv.x), my = double(hv.y);
@@ -609,12 +626,13 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
         }
         const double2 vpp = vd[pp], vc = vd[cc];
         if (pp == cc) {
-          xd = fma(mx, vpp.x * vpp.x + vpp.y * vpp.y, xd);  // spatial_gram.cpp:140-146 (real diagonal)
+          acc = fma(mx, vpp.x * vpp.x + vpp.y * vpp.y, acc);  // spatial_gram.cpp:140-146 (real diagonal)
         } else {
           const double tx = mx * vc.x - my * vc.y, ty = mx * vc.y + my * vc.x;  // M_pc v_c
-          xd = fma(2.0, vpp.x * tx + vpp.y * ty, xd);                           // 2 Re(conj(v_p) .)
+          acc = fma(2.0, vpp.x * tx + vpp.y * ty, acc);                         // 2 Re(conj(v_p) .)
         }
       }
+      xd += xd1;
     }
     float xn = 0.f;
 #pragma unroll
