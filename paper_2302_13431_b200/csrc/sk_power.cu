@@ -461,6 +461,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
 #pragma unroll
       for (int t = 0; t < D; ++t) buf[t] = v4[t];
       constexpr int LV = TPV <= 32 ? (TPV >= 32 ? 5 : TPV >= 16 ? 4 : TPV >= 8 ? 3 : TPV >= 4 ? 2 : TPV >= 2 ? 1 : 0) : 0;
+      float side_sh = 0.f;
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
         const float4 vt = buf[t % D];
@@ -475,9 +476,16 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
           ffma2(acc2[r][kb], pk(mb.y, mb.y), pk(vt.w, vt.z));
         }
         if (side != nullptr) {
+          // level j: the shuffle at chunk 3j, its sum two chunks later (in-order
+          // issue: an add right behind its shuffle stalls the warp); short
+          // products (NT < 3 LV) take one level per chunk
+          constexpr int SP = NT >= 3 * LV ? 3 : 1;
 #pragma unroll
-          for (int j = 0; j < LV; ++j)
-            if (t == (j * NT) / LV) *side += __shfl_xor_sync(0xffffffffu, *side, TPV >> (j + 1));
+          for (int j = 0; j < LV; ++j) {
+            const int ts = SP * j, ta = ts + (SP == 3 ? 2 : 0);
+            if (t == ts) side_sh = __shfl_xor_sync(0xffffffffu, *side, TPV >> (j + 1));
+            if (t == ta) *side += side_sh;
+          }
         }
       }
 #pragma unroll
