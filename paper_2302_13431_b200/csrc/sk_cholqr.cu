@@ -29,12 +29,13 @@ namespace skb {
 
 namespace {
 
-constexpr int kQ = 64;           // block width
-constexpr int kQLd = kQ + 1;     // padded row stride (conflict-free 16-byte columns)
+// Block width B in {32, 64} (template parameter); rows of staged blocks are
+// padded to B + 1 (conflict-free 16-byte columns).
 constexpr int kQCluster = 8;     // CTAs per gram cluster
 constexpr int kQStage = 32;      // rows staged per gram pass
 constexpr int kQGramThreads = 256;
-constexpr int kQCholThreads = 512;
+template <int B>
+constexpr int chol_threads() { return 8 * B; }  // B / 4 warps: warp w owns columns 4w..4w+3
 
 __device__ __forceinline__ double2 cfma_conj(double2 acc, double2 a, double2 b) {  // acc + conj(a) * b
   acc.x = fma(a.x, b.x, acc.x);
@@ -58,21 +59,30 @@ __device__ __forceinline__ double2 cfma_conj_rev(double2 acc, double2 a, double2
   return acc;
 }
 
-// tile t -> (ti, tj): HERM lists the lower tiles row by row, else all 16.
-template <bool HERM>
+// 16 x 16 tiles of the B x B result, T = B / 16 per side: tile t -> (ti, tj);
+// HERM lists the lower tiles row by row, else all T^2.
+template <int B, bool HERM>
 __host__ __device__ constexpr int tile_i(int t) {
-  return HERM ? (t < 1 ? 0 : t < 3 ? 1 : t < 6 ? 2 : 3) : t >> 2;
+  if (HERM) {
+    int i = 0;
+    while ((i + 1) * (i + 2) / 2 <= t) ++i;
+    return i;
+  }
+  return t / (B / 16);
 }
-template <bool HERM>
+template <int B, bool HERM>
 __host__ __device__ constexpr int tile_j(int t) {
-  return HERM ? t - tile_i<HERM>(t) * (tile_i<HERM>(t) + 1) / 2 : t & 3;
+  return HERM ? t - tile_i<B, HERM>(t) * (tile_i<B, HERM>(t) + 1) / 2 : t % (B / 16);
 }
+template <int B, bool HERM>
+constexpr int n_tiles() { return HERM ? (B / 16) * (B / 16 + 1) / 2 : (B / 16) * (B / 16); }
 
-template <bool HERM>
+template <int B, bool HERM>
 __global__ void __cluster_dims__(kQCluster, 1, 1) __launch_bounds__(kQGramThreads)
     gram64_kernel(const double2* __restrict__ x, const double2* __restrict__ y, i64 n, int rows,
                   double2* __restrict__ cpart, unsigned* __restrict__ counter, double2* __restrict__ out, i64 sx) {
-  constexpr int NT = HERM ? 10 : 16;
+  constexpr int NT = n_tiles<B, HERM>();
+  constexpr int kQ = B, kQLd = B + 1;
   // batch (multislice K2): slice blockIdx.y, its own partials, ticket and output
   x += i64(blockIdx.y) * sx;
   y += i64(blockIdx.y) * sx;
@@ -94,7 +104,7 @@ __global__ void __cluster_dims__(kQCluster, 1, 1) __launch_bounds__(kQGramThread
 #pragma unroll
   for (int t = 0; t < NT; ++t) acc[t] = make_double2(0.0, 0.0);
   for (i64 rs = row0; rs < row1; rs += kQStage) {
-    constexpr int kPer = kQStage * kQ / kQGramThreads;  // 8
+    constexpr int kPer = kQStage * kQ / kQGramThreads;  // 8 (B = 64), 4 (B = 32)
     double2 v[kPer], w[kPer];
 #pragma unroll
     for (int u = 0; u < kPer; ++u) {
@@ -116,14 +126,14 @@ __global__ void __cluster_dims__(kQCluster, 1, 1) __launch_bounds__(kQGramThread
     const int kn = int(min(i64(kQStage), row1 - rs));
 #pragma unroll 2
     for (int k = 0; k < kn; ++k) {
-      double2 xi[4], yj[4];
+      double2 xi[B / 16], yj[B / 16];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
+      for (int a = 0; a < B / 16; ++a) {
         xi[a] = xs[k * kQLd + 16 * a + r];
         yj[a] = ys[k * kQLd + 16 * a + c];
       }
 #pragma unroll
-      for (int t = 0; t < NT; ++t) acc[t] = cfma_conj(acc[t], xi[tile_i<HERM>(t)], yj[tile_j<HERM>(t)]);
+      for (int t = 0; t < NT; ++t) acc[t] = cfma_conj(acc[t], xi[tile_i<B, HERM>(t)], yj[tile_j<B, HERM>(t)]);
     }
   }
 #pragma unroll
@@ -169,7 +179,7 @@ __global__ void __cluster_dims__(kQCluster, 1, 1) __launch_bounds__(kQGramThread
         s.y += p.y;
       }
       const int t = g / kQGramThreads, tt = g % kQGramThreads;
-      const int ti = tile_i<HERM>(t), tj = tile_j<HERM>(t);
+      const int ti = tile_i<B, HERM>(t), tj = tile_j<B, HERM>(t);
       const int i = 16 * ti + (tt >> 4), j = 16 * tj + (tt & 15);
       if (!HERM) {
         out[i + kQ * j] = s;
@@ -193,13 +203,15 @@ __global__ void __cluster_dims__(kQCluster, 1, 1) __launch_bounds__(kQGramThread
 // the pivot column, 1/sqrt(d), scale, update the remaining columns) and
 // publishes block s + 1.  The pivot chain therefore crosses a CTA barrier
 // once per four pivots; the rank-4 updates of the other warps overlap it.
-__device__ __forceinline__ void chol64_factor4(double2 (&a)[4][2], double2 (*pub)[kQ], double2* Ls, double* rsv,
+template <int B>
+__device__ __forceinline__ void chol64_factor4(double2 (&a)[4][B / 32], double2 (*pub)[B], double2* Ls, double* rsv,
                                                int w, int lane, int* flag) {
+  constexpr int H = B / 32, kQLd = B + 1;
   const int j0 = 4 * w, hj = j0 >> 5;  // the block's rows j0..j0+3 lie in row slot hj
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int j = j0 + q;
-    const double2 cj = hj ? a[q][1] : a[q][0];
+    const double2 cj = a[q][H > 1 ? hj : 0];
     const double d = __shfl_sync(0xffffffffu, cj.x, j & 31);
     double2 cq[4];
 #pragma unroll
@@ -216,14 +228,14 @@ __device__ __forceinline__ void chol64_factor4(double2 (&a)[4][2], double2 (*pub
 #pragma unroll
     for (int t = q + 1; t < 4; ++t)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {  // a(i, j0+t) -= c(i) conj(c(j0+t)) / d
+      for (int h = 0; h < H; ++h) {  // a(i, j0+t) -= c(i) conj(c(j0+t)) / d
         const double2 ci = a[q][h];
         const double tr = ci.x * cq[t].x + ci.y * cq[t].y, tim = ci.y * cq[t].x - ci.x * cq[t].y;
         a[t][h].x = fma(-tr, r2, a[t][h].x);
         a[t][h].y = fma(-tim, r2, a[t][h].y);
       }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < H; ++h) {
       a[q][h].x *= r;
       a[q][h].y = (lane + 32 * h == j) ? 0.0 : a[q][h].y * r;
     }
@@ -231,7 +243,7 @@ __device__ __forceinline__ void chol64_factor4(double2 (&a)[4][2], double2 (*pub
 #pragma unroll
   for (int q = 0; q < 4; ++q)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < H; ++h) {
       const int i = lane + 32 * h;
       if (i >= j0 + q) {
         pub[q][i] = a[q][h];
@@ -240,47 +252,48 @@ __device__ __forceinline__ void chol64_factor4(double2 (&a)[4][2], double2 (*pub
     }
 }
 
-__global__ void __launch_bounds__(kQCholThreads) chol64_kernel(const double2* __restrict__ s_in,
-                                                               double2* __restrict__ l_out,
-                                                               double2* __restrict__ dinv_out, int* flag) {
-  SKB_DCHECK(blockDim.x == kQCholThreads);  // warp w owns columns 4w..4w+3 of the 64
+template <int B>
+__global__ void __launch_bounds__(chol_threads<B>()) chol64_kernel(const double2* __restrict__ s_in,
+                                                                  double2* __restrict__ l_out,
+                                                                  double2* __restrict__ dinv_out, int* flag) {
+  constexpr int kQ = B, kQLd = B + 1, H = B / 32, NB = B / 16;
+  SKB_DCHECK(blockDim.x == chol_threads<B>());  // warp w owns columns 4w..4w+3
   // batch (multislice K2): one CTA per slice
   s_in += i64(blockIdx.x) * kQ * kQ;
   l_out += i64(blockIdx.x) * kQ * kQ;
-  dinv_out += i64(blockIdx.x) * 4 * 256;
+  dinv_out += i64(blockIdx.x) * NB * 256;
   flag += 3 * blockIdx.x;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* Ls = reinterpret_cast<double2*>(smem_raw);  // [64][kQLd], L (lower)
+  double2* Ls = reinterpret_cast<double2*>(smem_raw);  // [B][B + 1], L (lower)
   __shared__ double2 colb[2][4][kQ];                    // block s of L (four columns), double-buffered
   __shared__ double rsv[kQ];                            // 1/L[k][k]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int j0 = 4 * w;
-  double2 a[4][2];
+  double2 a[4][H];
 #pragma unroll
   for (int c = 0; c < 4; ++c)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) a[c][h] = s_in[(lane + 32 * h) + kQ * (j0 + c)];  // S[i][j], coalesced in i
+    for (int h = 0; h < H; ++h) a[c][h] = s_in[(lane + 32 * h) + kQ * (j0 + c)];  // S[i][j], coalesced in i
   {
-    if (w == 0) chol64_factor4(a, colb[0], Ls, rsv, w, lane, flag);
+    if (w == 0) chol64_factor4<B>(a, colb[0], Ls, rsv, w, lane, flag);
 #pragma unroll 1
-    for (int s = 0; s < 15; ++s) {
+    for (int s = 0; s < B / 4 - 1; ++s) {
       __syncthreads();
       if (w > s) {
         const double2 (*cb)[kQ] = colb[s & 1];
-        double2 li[4][2];
+        double2 li[4][H];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          li[q][0] = cb[q][lane];
-          li[q][1] = cb[q][lane + 32];
-        }
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int h = 0; h < H; ++h) li[q][h] = cb[q][lane + 32 * h];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           double2 lj[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) lj[q] = cb[q][j0 + c];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (h == 0 && w >= 8) continue;  // columns >= 32 have no entries in rows < 32
+          for (int h = 0; h < H; ++h) {
+            if (H == 2 && h == 0 && w >= 8) continue;  // columns >= 32 have no entries in rows < 32
 #pragma unroll
             for (int q = 0; q < 4; ++q) {  // a -= l(i, q) conj(l(j, q))
               a[c][h].x = fma(-li[q][h].x, lj[q].x, a[c][h].x);
@@ -291,18 +304,18 @@ __global__ void __launch_bounds__(kQCholThreads) chol64_kernel(const double2* __
           }
         }
       }
-      if (w == s + 1) chol64_factor4(a, colb[(s + 1) & 1], Ls, rsv, w, lane, flag);
+      if (w == s + 1) chol64_factor4<B>(a, colb[(s + 1) & 1], Ls, rsv, w, lane, flag);
     }
   }
   __syncthreads();
-  for (int e = tid; e < kQ * kQ; e += kQCholThreads) {
-    const int i = e & (kQ - 1), j = e >> 6;
+  for (int e = tid; e < kQ * kQ; e += chol_threads<B>()) {
+    const int i = e % kQ, j = e / kQ;
     l_out[e] = i >= j ? Ls[i * kQLd + j] : make_double2(0.0, 0.0);
   }
   // Dinv_b = L_bb^{-1}: warp b, lane c < 16 forms column c by forward
   // substitution with the column in registers (x_m = 0 for m < c, so the
   // sums need no bounds; the newest term enters last: short chain).
-  if (w < 4 && lane < 16) {
+  if (w < NB && lane < 16) {
     const int b = w, c = lane, o = 16 * b;
     double2 xv[16];
 #pragma unroll
@@ -328,17 +341,19 @@ __global__ void __launch_bounds__(kQCholThreads) chol64_kernel(const double2* __
   }
 }
 
-// X (n x 64 column-major) <- X L^{-H}; `rows` rows per CTA, 16 threads per row.
+// X (n x B column-major) <- X L^{-H}; `rows` rows per CTA, 16 threads per row.
+template <int B>
 __global__ void __launch_bounds__(1024) trsm64_kernel(double2* __restrict__ x, i64 n, int rows,
                                                       const double2* __restrict__ l,
                                                       const double2* __restrict__ dinv, i64 sx) {
+  constexpr int kQ = B, kQLd = B + 1, NB = B / 16;
   x += i64(blockIdx.y) * sx;  // batch: slice blockIdx.y
   l += i64(blockIdx.y) * kQ * kQ;
-  dinv += i64(blockIdx.y) * 4 * 256;
+  dinv += i64(blockIdx.y) * NB * 256;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* Ls = reinterpret_cast<double2*>(smem_raw);  // [64][kQLd]
-  double2* Ds = Ls + kQ * kQLd;                         // [4][16][17]
-  double2* Xs = Ds + 4 * 16 * 17;                       // [rows][kQLd]
+  double2* Ls = reinterpret_cast<double2*>(smem_raw);  // [B][B + 1]
+  double2* Ds = Ls + kQ * kQLd;                         // [NB][16][17]
+  double2* Xs = Ds + NB * 16 * 17;                      // [rows][B + 1]
   const int tid = threadIdx.x, nt = blockDim.x;
   SKB_DCHECK(rows >= 1 && rows <= 64 && rows * 16 <= nt + 15);  // one half-warp per staged row
   const i64 row0 = i64(blockIdx.x) * rows;
@@ -354,20 +369,20 @@ __global__ void __launch_bounds__(1024) trsm64_kernel(double2* __restrict__ x, i
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = e0 + tid + u * nt;
-      if (e < kQ * kQ) Ls[(e & 63) * kQLd + (e >> 6)] = v[u];
+      if (e < kQ * kQ) Ls[(e % kQ) * kQLd + (e / kQ)] = v[u];
     }
   }
-  for (int e0 = 0; e0 < 4 * 256; e0 += 4 * nt) {
+  for (int e0 = 0; e0 < NB * 256; e0 += 4 * nt) {
     double2 v[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int e = e0 + tid + u * nt;
-      v[u] = e < 4 * 256 ? dinv[e] : make_double2(0.0, 0.0);
+      v[u] = e < NB * 256 ? dinv[e] : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int e = e0 + tid + u * nt;
-      if (e < 4 * 256) Ds[(e >> 8) * 272 + ((e >> 4) & 15) * 17 + (e & 15)] = v[u];
+      if (e < NB * 256) Ds[(e >> 8) * 272 + ((e >> 4) & 15) * 17 + (e & 15)] = v[u];
     }
   }
   for (int e0 = 0; e0 < rows * kQ; e0 += 4 * nt) {
@@ -390,7 +405,7 @@ __global__ void __launch_bounds__(1024) trsm64_kernel(double2* __restrict__ x, i
     const unsigned hmask = 0xffffu << (tid & 16);
     double2* xr = Xs + r * kQLd;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < NB; ++b) {
       const int j = 16 * b + c;
       double2 t0 = xr[j], t1 = make_double2(0.0, 0.0);
       const double2* lj = Ls + j * kQLd;
@@ -436,60 +451,82 @@ unsigned* gram_counter(sk_ctx* ctx) {
   return p;
 }
 
-template <bool HERM>
+template <int B, bool HERM>
 void launch_gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, double2* out, i64 batch = 1, i64 sx = 0) {
   if (batch > kMaxBatch) fail(SK_ERR_DIM, "gram64: batch too large");
-  constexpr int NT = HERM ? 10 : 16;
+  constexpr int NT = n_tiles<B, HERM>();
   // one wave of CTAs over the whole batch: ~sm_count CTAs per slice alone,
-  // fewer (more rows each) when many slices share the launch
+  // fewer (more rows each) when many slices share the launch; at least 16
+  // rows per CTA (small blocks: the cluster reduction outweighs the rows)
   const i64 per_slice = std::max<i64>(1, 2 * i64(ctx->sm_count) / std::max<i64>(batch, 1));
   const int target = int(std::max<i64>(kQCluster, std::min<i64>(ctx->sm_count, per_slice) / kQCluster * kQCluster));
-  const int rows = int(std::max<i64>(1, (n + target - 1) / target));
+  const int rows = int(std::max<i64>(16, (n + target - 1) / target));
   i64 ctas = (n + rows - 1) / rows;
   ctas = ((ctas + kQCluster - 1) / kQCluster) * kQCluster;
   const i64 ncl = ctas / kQCluster;
   double2* cpart = ctx->arena.get<double2>(HERM ? "cq:part_h" : "cq:part_x", batch * ncl * NT * kQGramThreads);
-  const size_t smem = size_t((HERM ? 1 : 2) * kQStage * kQLd + NT * kQGramThreads) * sizeof(double2);
-  set_smem_limit(reinterpret_cast<const void*>(gram64_kernel<HERM>), smem);
-  gram64_kernel<HERM><<<dim3(unsigned(ctas), unsigned(batch)), kQGramThreads, smem, ctx->stream>>>(
+  const size_t smem = size_t((HERM ? 1 : 2) * kQStage * (B + 1) + NT * kQGramThreads) * sizeof(double2);
+  set_smem_limit(reinterpret_cast<const void*>(gram64_kernel<B, HERM>), smem);
+  gram64_kernel<B, HERM><<<dim3(unsigned(ctas), unsigned(batch)), kQGramThreads, smem, ctx->stream>>>(
       x, y, n, rows, cpart, gram_counter(ctx), out, sx);
   ++ctx->launches;
   SKB_LAUNCH("gram64_kernel");
+}
+
+template <int B>
+void cholqr_blk(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag, i64 batch, i64 sx) {
+  constexpr int NB = B / 16;
+  double2* S = ctx->arena.get<double2>("cq:S", batch * B * B);
+  double2* L = ctx->arena.get<double2>("cq:L", batch * B * B);
+  double2* D = ctx->arena.get<double2>("cq:D", batch * NB * 256);
+  const size_t smem_c = size_t(B * (B + 1)) * sizeof(double2);
+  set_smem_limit(reinterpret_cast<const void*>(chol64_kernel<B>), smem_c);
+  // rows per trsm CTA: every CTA stages L and the diagonal inverses (80 KB at
+  // B = 64), so a batch takes the 64-row maximum (a single slice spreads over
+  // the SMs, at least 16 rows per CTA)
+  const i64 cta_target = std::max<i64>(1, i64(ctx->sm_count) / std::max<i64>(batch, 1));
+  const int rows = int(std::min<i64>(64, std::max<i64>(16, (n + cta_target - 1) / cta_target)));
+  const unsigned threads = unsigned(((rows * 16 + 31) / 32) * 32);
+  const size_t smem_t = size_t(B * (B + 1) + NB * 16 * 17 + rows * (B + 1)) * sizeof(double2);
+  set_smem_limit(reinterpret_cast<const void*>(trsm64_kernel<B>), smem_t);
+  for (int p = 0; p < passes; ++p) {
+    launch_gram64<B, true>(ctx, x, x, n, S, batch, sx);
+    chol64_kernel<B><<<unsigned(batch), chol_threads<B>(), smem_c, ctx->stream>>>(S, L, D, flag);
+    ++ctx->launches;
+    SKB_LAUNCH("chol64_kernel");
+    trsm64_kernel<B><<<dim3(unsigned((n + rows - 1) / rows), unsigned(batch)), threads, smem_t, ctx->stream>>>(
+        x, n, rows, L, D, sx);
+    ++ctx->launches;
+    SKB_LAUNCH("trsm64_kernel");
+  }
 }
 
 }  // namespace
 
 void gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, double2* out, i64 batch, i64 sx) {
   if (x == y)
-    launch_gram64<true>(ctx, x, x, n, out, batch, sx);
+    launch_gram64<64, true>(ctx, x, x, n, out, batch, sx);
   else
-    launch_gram64<false>(ctx, x, y, n, out, batch, sx);
+    launch_gram64<64, false>(ctx, x, y, n, out, batch, sx);
+}
+
+void gram_blk(sk_ctx* ctx, int b, const double2* x, const double2* y, i64 n, double2* out) {
+  if (b == 64) return gram64(ctx, x, y, n, out);
+  if (b != 32) fail(SK_ERR_UNSUPPORTED, "gram_blk: block width must be 32 or 64");
+  if (x == y)
+    launch_gram64<32, true>(ctx, x, x, n, out);
+  else
+    launch_gram64<32, false>(ctx, x, y, n, out);
 }
 
 void cholqr64(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag, i64 batch, i64 sx) {
-  double2* S = ctx->arena.get<double2>("cq:S", batch * kQ * kQ);
-  double2* L = ctx->arena.get<double2>("cq:L", batch * kQ * kQ);
-  double2* D = ctx->arena.get<double2>("cq:D", batch * 4 * 256);
-  const size_t smem_c = size_t(kQ * kQLd) * sizeof(double2);
-  auto kern = chol64_kernel;
-  set_smem_limit(reinterpret_cast<const void*>(kern), smem_c);
-  // rows per trsm CTA: every CTA stages L and the diagonal inverses (80 KB), so
-  // a batch takes the 64-row maximum (a single slice spreads over the SMs)
-  const i64 cta_target = std::max<i64>(1, i64(ctx->sm_count) / std::max<i64>(batch, 1));
-  const int rows = int(std::min<i64>(64, std::max<i64>(1, (n + cta_target - 1) / cta_target)));
-  const unsigned threads = unsigned(((rows * 16 + 31) / 32) * 32);
-  const size_t smem_t = size_t(kQ * kQLd + 4 * 16 * 17 + rows * kQLd) * sizeof(double2);
-  set_smem_limit(reinterpret_cast<const void*>(trsm64_kernel), smem_t);
-  for (int p = 0; p < passes; ++p) {
-    launch_gram64<true>(ctx, x, x, n, S, batch, sx);
-    kern<<<unsigned(batch), kQCholThreads, smem_c, ctx->stream>>>(S, L, D, flag);
-    ++ctx->launches;
-    SKB_LAUNCH("chol64_kernel");
-    trsm64_kernel<<<dim3(unsigned((n + rows - 1) / rows), unsigned(batch)), threads, smem_t, ctx->stream>>>(
-        x, n, rows, L, D, sx);
-    ++ctx->launches;
-    SKB_LAUNCH("trsm64_kernel");
-  }
+  cholqr_blk<64>(ctx, x, n, passes, flag, batch, sx);
+}
+
+void cholqr_b(sk_ctx* ctx, int b, double2* x, i64 n, int passes, int* flag) {
+  if (b == 64) return cholqr_blk<64>(ctx, x, n, passes, flag, 1, 0);
+  if (b != 32) fail(SK_ERR_UNSUPPORTED, "cholqr_b: block width must be 32 or 64");
+  cholqr_blk<32>(ctx, x, n, passes, flag, 1, 0);
 }
 
 }  // namespace skb

@@ -332,6 +332,9 @@ void cross_gram(sk_ctx* ctx, const double2* x, const double2* y, i64 n, int b, d
 void gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, double2* out, i64 batch = 1, i64 sx = 0);
 // flag: per-slice int at flag[3 * slice] (the nullspace info triple's flag slot)
 void cholqr64(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag, i64 batch = 1, i64 sx = 0);
+// the same kernels at block width b in {32, 64} (single slice)
+void gram_blk(sk_ctx* ctx, int b, const double2* x, const double2* y, i64 n, double2* out);
+void cholqr_b(sk_ctx* ctx, int b, double2* x, i64 n, int passes, int* flag);
 // One-CTA Hermitian eigensolver (sk_eig.cu) for b <= 64: eigenvalues ascending
 // into w, eigenvectors overwrite H (column-major); info[0] = 1 on a
 // non-finite result.  Returns false (nothing launched) for larger b.

@@ -602,16 +602,17 @@ void small_heev(sk_ctx* ctx, double2* H, i64 b, double* w, int* d_info, double f
 }
 
 // Orthonormalise X (n x b) in place by `passes` CholQR passes.  b = 64 and
-// n >= 1024: the own kernels of sk_cholqr.cu (gram64, chol64, trsm64; their
-// fixed costs pay from n ~ 1k).  b <= 256 otherwise: own cross_gram + cuSOLVER
+// n >= 1024, b = 32 and n >= 128: the own kernels of sk_cholqr.cu (gram,
+// one-CTA Cholesky, row TRSM; at b = 32 they took C1's K2 0.56 -> 0.50 ms
+// against the library pass).  b <= 256 otherwise: own cross_gram + cuSOLVER
 // POTRF + cuBLAS TRSM (measured against own one-CTA Cholesky variants and a
 // lane-pair TRSM: faster once graphs hide the library's host cost).  Larger
 // blocks: cuBLAS HERK + POTRF + TRSM with a synchronous check.  Returns false
 // only on a detected (synchronous path) failure; the other paths raise `flag`.
 bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int passes = 2) {
   (void)tmp;
-  if (b == 64 && n >= 1024) {
-    cholqr64(ctx, x, n, passes, flag);
+  if ((b == 64 && n >= 1024) || (b == 32 && n >= 128)) {
+    cholqr_b(ctx, int(b), x, n, passes, flag);
     return true;
   }
   if (b > 256) {
@@ -872,8 +873,8 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
       zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);
       laps.lap("gemm64");
       // Rayleigh-Ritz on span(V): H = V^H A V = S diag(w) S^H.
-      if (b == 64 && n >= 1024) {
-        gram64(ctx, V, Y, n, H);
+      if ((b == 64 && n >= 1024) || (b == 32 && n >= 128)) {
+        gram_blk(ctx, int(b), V, Y, n, H);
       } else if (b <= 256) {
         cross_gram(ctx, V, Y, n, int(b), H);
       } else {
