@@ -1549,10 +1549,13 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
       SKB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
       for (auto& e : ctx->chunk_ev) SKB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    const i64 step = ((ngrid + kChunks - 1) / kChunks + 7) / 8 * 8;
+    // decreasing chunk sizes (weights k, k-1, .., 1): the copy of the last
+    // chunk, which nothing overlaps, is the smallest
+    const i64 wsum = i64(kChunks) * (kChunks + 1) / 2;
     int c = 0;
-    for (i64 jb = 0; jb < ngrid; jb += step, ++c) {
-      const i64 cnt = std::min(step, ngrid - jb);
+    for (i64 jb = 0; jb < ngrid; ++c) {
+      const i64 want = c + 1 >= kChunks ? ngrid - jb : (ngrid * (kChunks - c) / wsum + 7) / 8 * 8;
+      const i64 cnt = std::min(std::max<i64>(want, 8), ngrid - jb);
       PowerArgs ca = pa;
       ca.planes = pa.planes + jb;
       ca.planes_lo = pa.planes_lo ? pa.planes_lo + jb : nullptr;
@@ -1568,6 +1571,7 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
       SKB_CUDA(cudaMemcpy2DAsync(out.maps_host + jb, size_t(ngrid) * sizeof(float2), maps_grid + jb,
                                  size_t(ngrid) * sizeof(float2), size_t(cnt) * sizeof(float2), size_t(q),
                                  cudaMemcpyDeviceToHost, ctx->copy_stream));
+      jb += cnt;
     }
     SKB_CUDA(cudaEventRecord(ctx->chunk_ev[8], ctx->copy_stream));
     SKB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->chunk_ev[8], 0));
