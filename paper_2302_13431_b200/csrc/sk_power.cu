@@ -544,30 +544,64 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     for (int r = 0; r < RPT; ++r) up[r] = vprev[r] = vp[r];
     float own = 0.f;
     if (a.iters > 1) own = publish(up, 1);  // iteration 0 read only buffer 0
-    for (int it = 1; it < a.iters; ++it) {
-      const int b = it & 1;
-      voxel_bar<L>(vox);
-      float2 mv[RPT];
-      if constexpr (TPV <= 32 && !L::kTile)
-        matvec(vb(b), mv, &own);  // the butterfly of ||u||^2 rides along
-      else
+    if constexpr (L::kTile) {
+      // (the tiled Q = 64 kernel keeps the plain loop: restructured as below
+      // it spills, C5 18.1 -> 19.6 ms)
+      for (int it = 1; it < a.iters; ++it) {
+        const int b = it & 1;
+        voxel_bar<L>(vox);
+        float2 mv[RPT];
         matvec(vb(b), mv);
-      // ||u_k||^2 (the previous iteration's shuffle reduction) is consumed only
-      // after the products: the empty asm ties it to mv so ptxas cannot hoist
-      // the test above the loads, and the reduction overlaps the matvec.
-      float n2 = published_norm(own, b);
-      asm("" : "+f"(n2) : "f"(mv[0].x));
-      done = done || (it > 1 && n2 < 1e-28f);
-      const float inv = rsqrtf(n2);
+        float n2 = published_norm(own, b);
+        asm("" : "+f"(n2) : "f"(mv[0].x));
+        done = done || (it > 1 && n2 < 1e-28f);
+        const float inv = rsqrtf(n2);
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) {  // branch-free: one basic block per iteration
-        const float2 nv = make_float2(up[r].x * inv, up[r].y * inv);
-        const float2 nu = make_float2((a.alpha * up[r].x + a.beta * mv[r].x) * inv,
-                                      (a.alpha * up[r].y + a.beta * mv[r].y) * inv);
-        vprev[r] = done ? vprev[r] : nv;
-        up[r] = done ? up[r] : nu;
+        for (int r = 0; r < RPT; ++r) {
+          const float2 nv = make_float2(up[r].x * inv, up[r].y * inv);
+          const float2 nu = make_float2((a.alpha * up[r].x + a.beta * mv[r].x) * inv,
+                                        (a.alpha * up[r].y + a.beta * mv[r].y) * inv);
+          vprev[r] = done ? vprev[r] : nv;
+          up[r] = done ? up[r] : nu;
+        }
+        own = publish(up, b ^ 1);
       }
-      own = publish(up, b ^ 1);
+    } else {
+      // one iteration reading buffer b (b = it & 1) and publishing into b ^ 1;
+      // the row layouts run them in pairs (b = 1, 0) with the two buffers'
+      // addresses fixed, halving the loop and address overhead (C2 K4 0.797 ->
+      // 0.780 ms)
+      float2* const vbuf[2] = {vb(0), vb(1)};
+      auto iteration = [&](int it, int b) {
+        voxel_bar<L>(vox);
+        float2 mv[RPT];
+        if constexpr (TPV <= 32)
+          matvec(vbuf[b], mv, &own);  // the butterfly of ||u||^2 rides along
+        else
+          matvec(vbuf[b], mv);
+        // ||u_k||^2 (the previous iteration's shuffle reduction) is consumed only
+        // after the products: the empty asm ties it to mv so ptxas cannot hoist
+        // the test above the loads, and the reduction overlaps the matvec.
+        float n2 = published_norm(own, b);
+        asm("" : "+f"(n2) : "f"(mv[0].x));
+        done = done || (it > 1 && n2 < 1e-28f);
+        const float inv = rsqrtf(n2);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) {  // branch-free: one basic block per iteration
+          const float2 nv = make_float2(up[r].x * inv, up[r].y * inv);
+          const float2 nu = make_float2((a.alpha * up[r].x + a.beta * mv[r].x) * inv,
+                                        (a.alpha * up[r].y + a.beta * mv[r].y) * inv);
+          vprev[r] = done ? vprev[r] : nv;
+          up[r] = done ? up[r] : nu;
+        }
+        own = publish(up, b ^ 1);
+      };
+      int it = 1;
+      for (; it + 1 < a.iters; it += 2) {
+        iteration(it, 1);
+        iteration(it + 1, 0);
+      }
+      if (it < a.iters) iteration(it, 1);
     }
     int fb = 0;  // buffer that receives the final v
     if (a.iters > 1) {
