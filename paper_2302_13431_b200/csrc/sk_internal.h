@@ -151,6 +151,10 @@ struct sk_ctx {
   };
   std::map<int64_t, SubspaceHint> subspace_hint;
   syevjInfo_t syevj = nullptr;
+  // pinned host staging for the subspace solver's per-round convergence data
+  // (one device-to-host copy of w, residuals and info instead of three)
+  double* hpin = nullptr;
+  size_t hpin_cap = 0;
   // concurrent lanes for multislice batches (sub-contexts on the same device)
   std::vector<sk_ctx*> lanes;
   // arena slots zeroed once at allocation (kernel-maintained counters)

@@ -818,9 +818,16 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
   double2* Y = ctx->arena.get<double2>("ss:Y", n * bcap);
   double2* T = ctx->arena.get<double2>("ss:T", n * bcap);
   double2* H = ctx->arena.get<double2>("ss:H", bcap * bcap);
-  double* w = ctx->arena.get<double>("ss:w", bcap);
-  double* res = ctx->arena.get<double>("ss:res", bcap);
-  int* d_info = ctx->arena.get<int>("ss:einfo", 3);
+  // w, residuals and the info triple in one slot: [w: bcap][res: bcap][info: 4 ints]
+  const size_t wri = size_t(2 * bcap + 2);
+  double* w = ctx->arena.get<double>("ss:wri", i64(wri));
+  double* res = w + bcap;
+  int* d_info = reinterpret_cast<int*>(w + 2 * bcap);
+  if (ctx->hpin_cap < wri) {
+    if (ctx->hpin) SKB_CUDA(cudaFreeHost(ctx->hpin));
+    SKB_CUDA(cudaMallocHost(&ctx->hpin, wri * sizeof(double)));
+    ctx->hpin_cap = wri;
+  }
   int* flag = d_info + 1;
   SKB_CUDA(cudaMemsetAsync(d_info, 0, 3 * sizeof(int), ctx->stream));
   // A Gaussian start block is well conditioned and only its span matters:
@@ -897,11 +904,12 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
     if (!body_ok) return false;
     iters += q_plan + 1;
     ++rounds;
-    int hinfo[3] = {0, 0, 0};
-    SKB_CUDA(cudaMemcpyAsync(hw.data(), w, size_t(b) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    SKB_CUDA(cudaMemcpyAsync(hres.data(), res, size_t(b) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    SKB_CUDA(cudaMemcpyAsync(hinfo, d_info, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SKB_CUDA(cudaMemcpyAsync(ctx->hpin, w, wri * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::copy(ctx->hpin, ctx->hpin + b, hw.begin());
+    std::copy(ctx->hpin + bcap, ctx->hpin + bcap + b, hres.begin());
+    int hinfo[3];
+    std::memcpy(hinfo, ctx->hpin + 2 * bcap, sizeof hinfo);
     laps.lap("sync");
     if (hinfo[0] != 0 || hinfo[1] != 0 || hinfo[2] != 0) return false;  // syevd failure / rank-deficient block
     theta_max = hw[size_t(b - 1)];
@@ -1680,6 +1688,7 @@ int sk_destroy(sk_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->syevj) cusolverDnDestroySyevjInfo(ctx->syevj);
+    if (ctx->hpin) cudaFreeHost(ctx->hpin);
     for (auto& kv : ctx->rounds)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
     ctx->rounds.clear();
