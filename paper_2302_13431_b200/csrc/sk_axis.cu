@@ -212,6 +212,71 @@ __global__ void __launch_bounds__(256) axis_symdft_kernel(const float2* __restri
 
 }  // namespace
 
+namespace {
+
+// Both axes of a 2-D separable transform in one CTA per batch item (the
+// Gram's channel spectra: E0 x E1 calibration -> P0 x P1 pad): the input, the
+// two matrices and the axis-1 result stay in shared memory, so the two
+// axis launches and the round trip of the intermediate through global memory
+// are gone (K1 stage: C2 0.109 -> 0.098 ms, C1 0.047 -> 0.027 ms).
+//   tmp[a0][j1] = sum_a1 M1[j1][a1] in[a0][a1];  out[j0][j1] = sum_a0 M0[j0][a0] tmp[a0][j1]
+__global__ void __launch_bounds__(256) sep2d_kernel(const float2* __restrict__ in, float2* __restrict__ out,
+                                                    const float2* __restrict__ M0, const float2* __restrict__ M1,
+                                                    int E0, int E1, int P0, int P1) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* xs = reinterpret_cast<float2*>(smem_raw);  // [E0][E1]
+  float2* tmp = xs + E0 * E1;                         // [E0][P1]
+  float2* m1 = tmp + E0 * P1;                         // [E1][P1] (transposed: lanes run along j1)
+  float2* m0 = m1 + P1 * E1;                          // [P0][E0]
+  const float2* src = in + i64(blockIdx.x) * E0 * E1;
+  float2* dst = out + i64(blockIdx.x) * P0 * P1;
+  for (int e = threadIdx.x; e < E0 * E1; e += blockDim.x) xs[e] = src[e];
+  for (int e = threadIdx.x; e < P1 * E1; e += blockDim.x) m1[(e % E1) * P1 + e / E1] = M1[e];
+  for (int e = threadIdx.x; e < P0 * E0; e += blockDim.x) m0[e] = M0[e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < E0 * P1; e += blockDim.x) {
+    const int a0 = e / P1, j1 = e % P1;
+    float2 acc = make_float2(0.f, 0.f), acc2 = acc;
+    const float2* mc = m1 + j1;
+    const float2* xr = xs + a0 * E1;
+    int a1 = 0;
+    for (; a1 + 1 < E1; a1 += 2) {
+      cmac(acc, mc[a1 * P1], xr[a1]);
+      cmac(acc2, mc[(a1 + 1) * P1], xr[a1 + 1]);
+    }
+    if (a1 < E1) cmac(acc, mc[a1 * P1], xr[a1]);
+    tmp[e] = make_float2(acc.x + acc2.x, acc.y + acc2.y);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < P0 * P1; e += blockDim.x) {
+    const int j0 = e / P1, j1 = e % P1;
+    float2 acc = make_float2(0.f, 0.f), acc2 = acc;
+    const float2* mr = m0 + j0 * E0;
+    int a0 = 0;
+    for (; a0 + 1 < E0; a0 += 2) {
+      cmac(acc, mr[a0], tmp[a0 * P1 + j1]);
+      cmac(acc2, mr[a0 + 1], tmp[(a0 + 1) * P1 + j1]);
+    }
+    if (a0 < E0) cmac(acc, mr[a0], tmp[a0 * P1 + j1]);
+    dst[e] = make_float2(acc.x + acc2.x, acc.y + acc2.y);
+  }
+}
+
+}  // namespace
+
+size_t sep2d_smem(int E0, int E1, int P0, int P1) {
+  return size_t(E0 * E1 + E0 * P1 + P1 * E1 + P0 * E0) * sizeof(float2);
+}
+
+void sep2d(sk_ctx* ctx, const float2* in, float2* out, i64 batch, int E0, int E1, int P0, int P1, const float2* M0,
+           const float2* M1) {
+  const size_t smem = sep2d_smem(E0, E1, P0, P1);
+  set_smem_limit(reinterpret_cast<const void*>(sep2d_kernel), smem);
+  sep2d_kernel<<<unsigned(batch), 256, smem, ctx->stream>>>(in, out, M0, M1, E0, E1, P0, P1);
+  ++ctx->launches;
+  SKB_LAUNCH("sep2d_kernel");
+}
+
 void apply_axis_symdft(sk_ctx* ctx, const float2* in, float2* out, const float2* cs, i64 batch, int H, int N,
                        i64 inner) {
   if (batch <= 0 || N <= 0 || inner <= 0) return;

@@ -181,6 +181,11 @@ namespace skb {
 // Separable "apply a small matrix along one axis":
 //   out[b][j][i] = sum_a M[j][a] * in[b][a][i],  M is N x L (row-major, c64).
 void apply_axis(sk_ctx* ctx, const float2* in, float2* out, const float2* M, i64 batch, int L, int N, i64 inner);
+// Both axes of a 2-D separable transform in one CTA per batch item (M0: P0 x E0,
+// M1: P1 x E1, row-major); for shared-memory-sized problems (sep2d_smem).
+size_t sep2d_smem(int E0, int E1, int P0, int P1);
+void sep2d(sk_ctx* ctx, const float2* in, float2* out, i64 batch, int E0, int E1, int P0, int P1, const float2* M0,
+           const float2* M1);
 // Symmetric-tap centred DFT (taps l = -H..H): cs[j][l-1] = (cos, sign*sin)(2 pi l (j - j0)/N).
 void apply_axis_symdft(sk_ctx* ctx, const float2* in, float2* out, const float2* cs, i64 batch, int H, int N,
                        i64 inner);

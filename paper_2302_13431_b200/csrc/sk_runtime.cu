@@ -400,7 +400,10 @@ float2* run_gram(sk_ctx* ctx, const Dims& cdims, i64 q, const float2* calib, con
   std::vector<float2*> mats(static_cast<size_t>(nd));
   for (int a = 0; a < nd; ++a) mats[size_t(a)] = dft_matrix(ctx, int(pad[size_t(a)]), int(cdims[size_t(a)]), 0, 0, -1, 0.0);
   float2* spectra = ctx->arena.get<float2>("gram:spectra", q * numel(pad));
-  separable(ctx, calib, spectra, q, cdims, pad, mats, "gram:tmp");
+  if (nd == 2 && sep2d_smem(int(cdims[0]), int(cdims[1]), int(pad[0]), int(pad[1])) <= 160 * 1024)
+    sep2d(ctx, calib, spectra, q, int(cdims[0]), int(cdims[1]), int(pad[0]), int(pad[1]), mats[0], mats[1]);
+  else
+    separable(ctx, calib, spectra, q, cdims, pad, mats, "gram:tmp");
   SupportTables& t = tables_for(ctx, s, int(q));
   GramGeom g{};
   g.nd = nd;
