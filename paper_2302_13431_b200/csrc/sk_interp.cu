@@ -57,6 +57,10 @@ template <typename C>
 __device__ __forceinline__ void fft_lines(C* buf, int log_lines, int ld, int log2len, const C* tw, int log_tw_stride,
                                           bool inverse) {
   constexpr int RM = 4;
+  // unrolled: with log2len known at compile time (the templated kernels) every
+  // pass's radix r and index masks fold (the rolled loop stalled on branch
+  // resolution: 12% of the C4 interpolation's samples)
+#pragma unroll
   for (int s0 = 1; s0 <= log2len; s0 += RM) {
     const int r = min(RM, log2len - s0 + 1);
     const int hl0 = s0 - 1;
