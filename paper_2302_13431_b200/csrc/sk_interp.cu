@@ -231,19 +231,37 @@ __global__ void __launch_bounds__(256) interp2_fft_kernel(const typename Cplx<R>
   const bool across = log_inner >= logT;
   const unsigned imask = (1u << log_inner) - 1u;
   const size_t stride = size_t(1) << log_inner;
-  for (int e = threadIdx.x; e < (T << logn); e += blockDim.x) {
-    const int t = across ? (e & (T - 1)) : (e >> logn);
-    const int a = across ? (e >> logT) : (e & (n - 1));
-    const unsigned line = l0 + t;
-    C v;
-    v.x = R(0);
-    v.y = R(0);
-    if (line < lines_total) {
-      const unsigned b = line >> log_inner, i = line & imask;
-      v = in[((size_t(b) << logn) + ((a + cl) & (n - 1))) * stride + i];  // ifftshift
+  // loads: a thread's elements all in flight before the shared-memory
+  // stores (one load-store pair per iteration kept one global load in flight:
+  // the dominant long-scoreboard stall of the pass)
+  constexpr int kLd = 16;  // T * n <= 16 * 256 (launcher)
+  {
+    C v[kLd];
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const int e = threadIdx.x + u * 256;
+      v[u].x = R(0);
+      v[u].y = R(0);
+      if (e < (T << logn)) {
+        const int t = across ? (e & (T - 1)) : (e >> logn);
+        const int a = across ? (e >> logT) : (e & (n - 1));
+        const unsigned line = l0 + t;
+        if (line < lines_total) {
+          const unsigned b = line >> log_inner, i = line & imask;
+          v[u] = in[((size_t(b) << logn) + ((a + cl) & (n - 1))) * stride + i];  // ifftshift
+        }
+      }
     }
-    buf[t * ld + pz(bitrev(a, logn))] = v;
-    ybuf[t * ld + pz(a)] = v;
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const int e = threadIdx.x + u * 256;
+      if (e < (T << logn)) {
+        const int t = across ? (e & (T - 1)) : (e >> logn);
+        const int a = across ? (e >> logT) : (e & (n - 1));
+        buf[t * ld + pz(bitrev(a, logn))] = v[u];
+        ybuf[t * ld + pz(a)] = v[u];
+      }
+    }
   }
   __syncthreads();
   fft_lines(buf, logT, ld, logn, tw, 1, false);  // Y = FFT_n (twiddles tw[2k])
@@ -321,11 +339,26 @@ __global__ void __launch_bounds__(256) interp2_sos_kernel(const float2* __restri
   }
   const unsigned p = blockIdx.x;
   const int cl = n / 2;
-  for (int e = threadIdx.x; e < (T << logn); e += blockDim.x) {
-    const int t = e >> logn, a = e & (n - 1);
-    const C v = in[((size_t(t) * positions + p) << logn) + ((a + cl) & (n - 1))];  // ifftshift
-    buf[t * ld + pz(bitrev(a, logn))] = v;
-    ybuf[t * ld + pz(a)] = v;
+  {  // all of a thread's loads in flight before the shared-memory stores (as interp2_fft_kernel)
+    constexpr int kLd = 16;
+    C v[kLd];
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const int e = threadIdx.x + u * 256;
+      if (e < (T << logn)) {
+        const int t = e >> logn, a = e & (n - 1);
+        v[u] = in[((size_t(t) * positions + p) << logn) + ((a + cl) & (n - 1))];  // ifftshift
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kLd; ++u) {
+      const int e = threadIdx.x + u * 256;
+      if (e < (T << logn)) {
+        const int t = e >> logn, a = e & (n - 1);
+        buf[t * ld + pz(bitrev(a, logn))] = v[u];
+        ybuf[t * ld + pz(a)] = v[u];
+      }
+    }
   }
   __syncthreads();
   fft_lines(buf, logT, ld, logn, tw, 1, false);
