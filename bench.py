@@ -432,8 +432,9 @@ def main():
     if sharded:
         # the batched call runs slices on concurrent lanes, so its per-slice stage
         # times overlap: take the stage split from one sequential (untimed) pass
+        timed(lambda: step_device(0, sequential=True), 1, flush_l2=False)  # warm the single-slice path
         _, stages = timed(lambda: step_device(0, sequential=True), 1, flush_l2=False)
-        stage_note = ("sum over this rank's slices of one sequential, untimed pass (slice by slice; the timed "
+        stage_note = ("sum over this rank's slices of one sequential, untimed pass after a warm-up pass (slice by slice; the timed "
                       "batched call overlaps slices on concurrent lanes)")
 
     # ---- e2e through the public API with pinned host buffers (one slice-sized
