@@ -1603,9 +1603,16 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
     if (!renormed) renormalize_and_mask(ctx, maps_full, nfull, int(q), nullptr, nullptr, nullptr, 0.f);
   }
   SKB_CUDA(cudaEventRecord(ev[6], ctx->stream));
-  unsigned long long h_zeroed = 0;
-  SKB_CUDA(cudaMemcpyAsync(&h_zeroed, zeroed, sizeof h_zeroed, cudaMemcpyDeviceToHost, ctx->stream));
+  // the zeroed-voxel count through the context's pinned staging (a pageable
+  // destination makes the copy a slower synchronous one)
+  if (ctx->hpin_cap < 1) {
+    SKB_CUDA(cudaMallocHost(&ctx->hpin, 64 * sizeof(double)));
+    ctx->hpin_cap = 64;
+  }
+  SKB_CUDA(cudaMemcpyAsync(ctx->hpin, zeroed, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
   SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  unsigned long long h_zeroed = 0;
+  std::memcpy(&h_zeroed, ctx->hpin, sizeof h_zeroed);
   if (out.spectrum)
     for (i64 i = 0; i < n; ++i) out.spectrum[i] = e.sigma1 > 0 ? e.spectrum[size_t(i)] / e.sigma1 : 0.0;
   if (prov) {
