@@ -360,8 +360,8 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
         vb(b)[L::vidx(prow + r * TPV)] = u[r];
         x = fmaf(u[r].x, u[r].x, fmaf(u[r].y, u[r].y, x));
       }
-      if constexpr (TPV <= 32) {
-        return x;
+      if constexpr (TPV <= 32 || L::kTile) {
+        return x;  // tiled: recomputed from v by the next matvec (tile_norm)
       } else {
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -375,8 +375,8 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       return x;
     };
     auto published_norm = [&](float own, int b) -> float {
-      if constexpr (TPV <= 32) {
-        return own;  // already reduced by voxel_butterfly
+      if constexpr (TPV <= 32 || L::kTile) {
+        return own;  // already reduced (voxel_butterfly / the tiled matvec)
       } else {
         float s = 0.f;
 #pragma unroll
@@ -404,12 +404,21 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
         const int cg = L::col_group(local);
         const float4* v4 = reinterpret_cast<const float4*>(v + cg * (TC + 2));
         SKB_DCHECK(v >= vs && v + cg * (TC + 2) + TC <= vs + 2 * VPB * L::kStride);
-        u64 acc[4], acc2[4];
+        // side (tiled): ||v||^2 of the buffer read, from the column-group
+        // quarter of v the thread loads anyway, summed over the four column
+        // groups with the reduce-scatter's shuffles -- no cross-warp exchange
+        // (publish's warp butterfly + shared partials were 17.7% of C5's K4
+        // stall samples)
+        u64 acc[4], acc2[4], nacc = 0ull;
 #pragma unroll
         for (int tr = 0; tr < 4; ++tr) acc[tr] = acc2[tr] = 0ull;
 #pragma unroll
         for (int t = 0; t < TC / 2; ++t) {
           const float4 vt = v4[t];
+          if (side != nullptr) {
+            ffma2(nacc, pk(vt.x, vt.y), pk(vt.x, vt.y));
+            ffma2(nacc, pk(vt.z, vt.w), pk(vt.z, vt.w));
+          }
 #pragma unroll
           for (int tr = 0; tr < 4; ++tr) {
             const float2 ma = m[0][tr * TC + 2 * t], mb = m[0][tr * TC + 2 * t + 1];
@@ -431,14 +440,18 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
         const bool b1 = (cg & 2) != 0, b0 = (cg & 1) != 0;
         float2 k0 = b1 ? s4[2] : s4[0], k1 = b1 ? s4[3] : s4[1];
         const float2 o0 = b1 ? s4[0] : s4[2], o1 = b1 ? s4[1] : s4[3];
+        const float2 nn = unpk(nacc);
+        float nq = nn.x + nn.y;
         k0.x += __shfl_xor_sync(0xffffffffu, o0.x, 2);
         k0.y += __shfl_xor_sync(0xffffffffu, o0.y, 2);
         k1.x += __shfl_xor_sync(0xffffffffu, o1.x, 2);
         k1.y += __shfl_xor_sync(0xffffffffu, o1.y, 2);
+        if (side != nullptr) nq += __shfl_xor_sync(0xffffffffu, nq, 2);
         float2 kk = b0 ? k1 : k0;
         const float2 oo = b0 ? k0 : k1;
         kk.x += __shfl_xor_sync(0xffffffffu, oo.x, 1);
         kk.y += __shfl_xor_sync(0xffffffffu, oo.y, 1);
+        if (side != nullptr) *side = nq + __shfl_xor_sync(0xffffffffu, nq, 1);
         out[0] = kk;
         return;
       }
@@ -551,7 +564,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
         const int b = it & 1;
         voxel_bar<L>(vox);
         float2 mv[RPT];
-        matvec(vb(b), mv);
+        matvec(vb(b), mv, &own);
         float n2 = published_norm(own, b);
         asm("" : "+f"(n2) : "f"(mv[0].x));
         done = done || (it > 1 && n2 < 1e-28f);
@@ -606,7 +619,12 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     int fb = 0;  // buffer that receives the final v
     if (a.iters > 1) {
       voxel_bar<L>(vox);
-      if constexpr (TPV <= 32) own = voxel_butterfly(own);
+      if constexpr (L::kTile) {
+        float2 unused[RPT];
+        matvec(vb(a.iters & 1), unused, &own);  // (the product itself is dead code)
+      } else if constexpr (TPV <= 32) {
+        own = voxel_butterfly(own);
+      }
       const float n2 = published_norm(own, a.iters & 1);
       const bool keep = done || n2 < 1e-28f;
       const float inv = keep ? 0.f : rsqrtf(n2);
