@@ -672,10 +672,14 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       // FP32 value kept (voxel_sum below still runs: its shuffles span voxels)
     } else {
       const double2* vd = vds + vox * QP;
-      double xd1 = 0.0;  // second accumulator: alternate packed elements (C5 K4 18.7 -> 18.1 ms)
-#pragma unroll 2
+      // four accumulators over alternate packed elements, loop unrolled by
+      // four: the loop is latency-bound (LDS -> F2F -> DFMA chains), so more
+      // elements in flight (two accumulators: C5 K4 18.7 -> 18.1 ms)
+      double xd1 = 0.0, xd2 = 0.0, xd3 = 0.0;
+#pragma unroll 4
       for (int e = local; e < h; e += TPV) {
-        double& acc = ((e / TPV) & 1) ? xd1 : xd;
+        const int sel = (e / TPV) & 3;
+        double& acc = sel == 0 ? xd : sel == 1 ? xd1 : sel == 2 ? xd2 : xd3;
         const int pc = pct[e], pp = pc >> 8, cc = pc & 0xff;
         const float2 hv = gs[swz_at(e * VPB + vox, tt.swz)];
         double mx = double(hv.x), my = double(hv.y);
@@ -692,14 +696,40 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
           acc = fma(2.0, vpp.x * tx + vpp.y * ty, acc);                         // 2 Re(conj(v_p) .)
         }
       }
-      xd += xd1;
+      xd = (xd + xd1) + (xd2 + xd3);
     }
-    float xn = 0.f;
+    // ||v||^2, v^H M v and (with recon) conj(v) . recon reduced together: the
+    // phase reference needs only the direction of the last, so it is formed
+    // from the unnormalised v and the four butterflies run interleaved.
+    float xn = 0.f, xr = 0.f, xi = 0.f;
 #pragma unroll
-    for (int r = 0; r < RPT; ++r) xn += vp[r].x * vp[r].x + vp[r].y * vp[r].y;
-    const double mv64 = voxel_sum<L>(xd, redd, vox);
+    for (int r = 0; r < RPT; ++r) {
+      xn += vp[r].x * vp[r].x + vp[r].y * vp[r].y;
+      const float2 rc = rcv[r];  // zero without recon
+      xr += vp[r].x * rc.x + vp[r].y * rc.y;  // conj(v) * recon
+      xi += vp[r].x * rc.y - vp[r].y * rc.x;
+    }
+    double mv64;
+    float vn2, ux, uy;
+    if constexpr (TPV <= 32) {
+#pragma unroll
+      for (int o = TPV / 2; o > 0; o >>= 1) {
+        xd += __shfl_xor_sync(0xffffffffu, xd, o);
+        xn += __shfl_xor_sync(0xffffffffu, xn, o);
+        xr += __shfl_xor_sync(0xffffffffu, xr, o);
+        xi += __shfl_xor_sync(0xffffffffu, xi, o);
+      }
+      mv64 = xd;
+      vn2 = xn;
+      ux = xr;
+      uy = xi;
+    } else {
+      mv64 = voxel_sum<L>(xd, redd, vox);
+      vn2 = voxel_sum<L>(xn, red, vox);
+      ux = voxel_sum<L>(xr, red, vox);
+      uy = voxel_sum<L>(xi, red, vox);
+    }
     const double mv = need64 ? mv64 : double(mv32);
-    const float vn2 = voxel_sum<L>(xn, red, vox);
 
     if (a.recon != nullptr) {
       // normalize_maps, per voxel: SoS (maps.cpp:117-128) then phase reference
@@ -711,15 +741,6 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       } else if (local == 0 && live && a.zeroed) {
         atomicAdd(a.zeroed, 1ull);
       }
-      float xr = 0.f, xi = 0.f;
-#pragma unroll
-      for (int r = 0; r < RPT; ++r) {
-        const float2 rc = rcv[r];
-        xr += vp[r].x * rc.x + vp[r].y * rc.y;  // conj(v) * recon
-        xi += vp[r].x * rc.y - vp[r].y * rc.x;
-      }
-      const float ux = voxel_sum<L>(xr, red, vox);
-      const float uy = voxel_sum<L>(xi, red, vox);
       const float mag = sqrtf(ux * ux + uy * uy);
       if (mag > 0.f) {
         const float cx = ux / mag, cy = uy / mag;
