@@ -17,15 +17,17 @@
 //      that rows are read contiguously without conjugation branches.  Two
 //      barriers per column: norms and p^H v are reduced redundantly by every
 //      warp, v and w = p - tau/2 (p^H v) v are formed on the fly.
-//   2. Eigenvalues of T by multisection (Sturm counts, dlaebz rules for tiny
-//      pivots): every eigenvalue is bracketed by TPE threads that evaluate
-//      two interior points each per step, to 1e-10 ||T||.
+//   2. Eigenvalues of T by multisection (Sturm counts from the scaled
+//      leading-minor recurrence, zero minors by the dlaebz rule): every
+//      eigenvalue is bracketed by TPE threads that evaluate two interior
+//      points each per step, to 1e-10 ||T||.
 //   3. Eigenvectors of T by inverse iteration (dstein): two solves of
 //      (T - lambda I) z = r with partial pivoting from a pseudo-random start
 //      (factors in shared memory), a Rayleigh-quotient refinement of lambda
 //      (to ~eps ||T||), and Gram-Schmidt plus shifted re-solves inside
 //      clusters of close eigenvalues.
-//   4. Back-transformation X = Q Z, one column per 8 lanes (no block barriers).
+//   4. Back-transformation X = Q Z, one column per 8 lanes with the column
+//      in registers (no block barriers, no shared-memory traffic for X).
 //
 // Output matches cusolverDnZheevj: eigenvalues ascending in w, eigenvectors
 // overwrite H column-major.  A non-finite intermediate raises info[0] (the
@@ -95,24 +97,58 @@ __device__ __forceinline__ double block_sum(double x, double* red) {
   return s;
 }
 
-// Number of eigenvalues of the symmetric tridiagonal (d, e2 = e^2) not above
-// x0 and x1 (two independent chains for ILP).
-__device__ __forceinline__ void sturm_count2(const double* d, const double* e2, int n, double x0, double x1,
-                                             double pivmin, int& c0, int& c1) {
-  double q0 = d[0] - x0, q1 = d[0] - x1;
-  if (fabs(q0) < pivmin) q0 = -pivmin;
-  if (fabs(q1) < pivmin) q1 = -pivmin;
-  c0 = q0 <= 0.0 ? 1 : 0;
-  c1 = q1 <= 0.0 ? 1 : 0;
-  for (int i = 1; i < n; ++i) {
-    const double di = d[i], ei = e2[i - 1];
-    q0 = (di - x0) - ei * frcp<1>(q0);
-    q1 = (di - x1) - ei * frcp<1>(q1);
-    if (fabs(q0) < pivmin) q0 = -pivmin;
-    if (fabs(q1) < pivmin) q1 = -pivmin;
-    c0 += q0 <= 0.0 ? 1 : 0;
-    c1 += q1 <= 0.0 ? 1 : 0;
+// Number of eigenvalues of the symmetric tridiagonal (ds = s d, e2s = (s e)^2) not
+// above x0 and x1 (two independent chains for ILP), from the signs of the
+// leading principal minors P_k = det(s (T_k - x I)) (Sturm sequence):
+//   P_k = (s d_k - s x) P_{k-1} - e2s_{k-1} P_{k-2},
+// one FMA on the dependent chain per step instead of the LDL pivot's
+// reciprocal (bisection phase 90 k -> 20 k cycles at n = 64).  A zero minor
+// counts as a sign change and takes the sign opposite to its predecessor,
+// which is the LDL rule's "zero pivot -> -pivmin" (dlaebz); s is a power of
+// two with s ||T|| < 1, so |P_k| grows at most ~3^8 per eight steps and the
+// pair is rescaled by 2^-+400 every eight steps.
+__device__ __forceinline__ void sturm_count2(const double* ds, const double* e2s, int n, double x0, double x1,
+                                             double s, int& c0, int& c1) {
+  const double y0 = x0 * s, y1 = x1 * s;
+  double a1 = 1.0, a2 = 0.0, b1 = 1.0, b2 = 0.0;  // P_{k-1}, P_{k-2} of the two chains
+  unsigned sa = 0u, sb = 0u;                       // sign taken for P_{k-1}
+  int na = 0, nb = 0;
+  for (int k0 = 0; k0 < n; k0 += 8) {
+    // eight steps per block: the shared loads of a block issue ahead of its chain
+    double dk[8], ek[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = k0 + j;
+      dk[j] = k < n ? ds[k] : 0.0;
+      ek[j] = (k > 0 && k < n) ? e2s[k - 1] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (k0 + j < n) {
+        const double pa = fma(dk[j] - y0, a1, -ek[j] * a2);
+        const double pb = fma(dk[j] - y1, b1, -ek[j] * b2);
+        const unsigned ta = pa == 0.0 ? sa ^ 1u : unsigned(__double2hiint(pa)) >> 31;
+        const unsigned tb = pb == 0.0 ? sb ^ 1u : unsigned(__double2hiint(pb)) >> 31;
+        na += int(ta != sa);
+        nb += int(tb != sb);
+        sa = ta;
+        sb = tb;
+        a2 = a1;
+        a1 = pa;
+        b2 = b1;
+        b1 = pb;
+      }
+    }
+    const double ma = fmax(fabs(a1), fabs(a2)), mb = fmax(fabs(b1), fabs(b2));
+    const double fa = ma < 0x1p-400 ? 0x1p400 : ma > 0x1p400 ? 0x1p-400 : 1.0;
+    const double fb = mb < 0x1p-400 ? 0x1p400 : mb > 0x1p400 ? 0x1p-400 : 1.0;
+    a1 *= fa;
+    a2 *= fa;
+    b1 *= fb;
+    b2 *= fb;
   }
+  c0 = na;
+  c1 = nb;
 }
 
 __device__ __forceinline__ double hash_unit(unsigned a, unsigned b) {  // deterministic value in (-1, 1)
@@ -183,12 +219,10 @@ __global__ void __launch_bounds__(kThreads) herm_eig_kernel(double2* __restrict_
   info += 3 * blockIdx.x;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int ld = n + 1;  // padded row stride (double2) of the full Hermitian A (bank skew)
-  const int xs = n + 1;  // padded row stride of X
   const int zs = n + 1;  // padded row stride of zr
-  const int uwords = (max(2 * n * xs, 3 * n * n) + 1) & ~1;  // X (complex) and the LU factors share it; even
+  const int uwords = (max(2 * n * (n + 1), 3 * n * n) + 1) & ~1;  // the LU factors (step 3); even
   double2* A = reinterpret_cast<double2*>(smem_raw);  // full Hermitian matrix; row k holds v_k after step k
-  double* un = reinterpret_cast<double*>(A + n * ld);  // union: LU factors (step 3), X (step 4)
-  double2* X = reinterpret_cast<double2*>(un);         // [n][xs] row-major
+  double* un = reinterpret_cast<double*>(A + n * ld);  // LU factors (step 3)
   double2* pv = reinterpret_cast<double2*>(un + uwords);  // [n]
   double2* vv = pv + n;                                    // [n]
   double2* tau = vv + n;                                   // [n]
@@ -196,7 +230,8 @@ __global__ void __launch_bounds__(kThreads) herm_eig_kernel(double2* __restrict_
   double* e = d + n;
   double* e2 = e + n;
   double* lam = e2 + n;
-  double* red = lam + n;  // [kThreads / 32]
+  double* dsc = lam + n;  // s d (the Sturm recurrence's scaled diagonal)
+  double* red = dsc + n;  // [kThreads / 32]
   double* zr = red + kThreads / 32;                // [n][zs] real eigenvectors of T, row-major [i][t]
   int* cl = reinterpret_cast<int*>(zr + n * zs);  // [2n + 1] cluster table
 
@@ -309,9 +344,11 @@ __global__ void __launch_bounds__(kThreads) herm_eig_kernel(double2* __restrict_
     hi = i == 0 ? d[i] + r : fmax(hi, d[i] + r);
     if (i + 1 < n) emax2 = fmax(emax2, e[i] * e[i]);
   }
-  if (tid < n - 1) e2[tid] = e[tid] * e[tid];
-  __syncthreads();
   const double tnorm = fmax(fabs(lo), fabs(hi));
+  const double sscale = tnorm > 0.0 ? ldexp(1.0, -(ilogb(tnorm) + 1)) : 1.0;  // sturm_count2's s
+  if (tid < n - 1) e2[tid] = (e[tid] * sscale) * (e[tid] * sscale);
+  if (tid < n) dsc[tid] = d[tid] * sscale;
+  __syncthreads();
   const double pivmin = DBL_MIN * fmax(1.0, emax2);
   lo -= 2.0 * DBL_EPSILON * tnorm + pivmin;
   hi += 2.0 * DBL_EPSILON * tnorm + pivmin;
@@ -329,7 +366,7 @@ __global__ void __launch_bounds__(kThreads) herm_eig_kernel(double2* __restrict_
       const double wdt = (b - a) / double(pts + 1);
       const double x0 = a + wdt * double(2 * s + 1), x1 = a + wdt * double(2 * s + 2);
       int k0 = 0, k1 = 0;
-      if (act) sturm_count2(d, e2, n, x0, x1, pivmin, k0, k1);
+      if (act) sturm_count2(dsc, e2, n, x0, x1, sscale, k0, k1);
       double na = a, nb = b;
       for (int q = 0; q < tpe; ++q) {
         const double y0 = __shfl_sync(0xffffffffu, x0, base + q), y1 = __shfl_sync(0xffffffffu, x1, base + q);
@@ -448,33 +485,48 @@ __global__ void __launch_bounds__(kThreads) herm_eig_kernel(double2* __restrict_
 
   SKB_EIG_STAMP(4);
   // ---- 4. back-transformation X = Q Z (H_0 ... H_{n-2} applied right to left)
-  for (int e0 = tid; e0 < n * n; e0 += kThreads) {
-    const int i = e0 / n, c = e0 % n;
-    X[i * xs + c] = make_double2(zr[i * zs + c], 0.0);
+  // c01 = v0^H v1 of every reflector pair (column-independent), one warp per pair
+  for (int k = n - 2 - 2 * warp; k >= 1; k -= 2 * (kThreads / 32)) {
+    const double2* v1 = A + k * ld + k + 1;
+    const double2* v0 = A + (k - 1) * ld + k;
+    double2 c = make_double2(0.0, 0.0);
+    for (int i = lane; i < n - k - 1; i += 32) c = cfma_conj(c, v0[i + 1], v1[i]);
+    c.x = warp_sum(c.x);
+    c.y = warp_sum(c.y);
+    if (lane == 0) vv[k] = c;
   }
   __syncthreads();
+  bool bad = false;
   {
     // Reflectors in pairs (k1 = k applied first, then k0 = k - 1):
     //   s1 = v1^H X,  s0 = v0^H X - tau1 (v0^H v1) s1,
     //   X -= tau1 v1 s1 + tau0 v0 s0      (v0 starts one row above v1).
-    const int c = tid >> 3, rs = tid & 7;  // 8 lanes per column, rows interleaved
+    // Column c of X lives in the registers of its 8 lanes (lane rs holds rows
+    // rs, rs + 8, ...); v_k's entry for row r is A[k][r] (zero above the
+    // reflector), so a pair needs no shared-memory traffic for X and no
+    // barrier (smem-resident X: 103 k cycles at n = 64).
+    constexpr int RJ = kMaxN / 8;
+    const int c = tid >> 3, rs = tid & 7;
     const bool act = c < n;
-    auto xat = [&](int r) -> double2& { return X[r * xs + c]; };
+    double2 xr[RJ];
+#pragma unroll
+    for (int j = 0; j < RJ; ++j) {
+      const int r = rs + 8 * j;
+      xr[j] = make_double2((act && r < n) ? zr[r * zs + c] : 0.0, 0.0);
+    }
     int k = n - 2;
     for (; k >= 1; k -= 2) {
-      const int k0 = k - 1;
-      const double2 t1 = tau[k], t0 = tau[k0];
-      const double2* v1 = A + k * ld + k + 1;    // rows k+1 .. n-1
-      const double2* v0 = A + k0 * ld + k0 + 1;  // rows k   .. n-1
-      const int m1 = n - k - 1;
-      double2 s1 = make_double2(0.0, 0.0), s0 = s1, c01 = s1;
-      if (act) {
-        if (rs == 0) s0 = cfma_conj(s0, v0[0], xat(k));
-        for (int i = rs; i < m1; i += 8) {
-          const double2 x = xat(k + 1 + i);
-          s1 = cfma_conj(s1, v1[i], x);
-          s0 = cfma_conj(s0, v0[i + 1], x);
-          c01 = cfma_conj(c01, v0[i + 1], v1[i]);
+      const double2 t1 = tau[k], t0 = tau[k - 1], c01 = vv[k];
+      const double2* a1 = A + k * ld;        // v1[r] = A[k][r], r >= k + 1
+      const double2* a0 = A + (k - 1) * ld;  // v0[r] = A[k-1][r], r >= k
+      double2 s1 = make_double2(0.0, 0.0), s0 = s1;
+#pragma unroll
+      for (int j = 0; j < RJ; ++j) {
+        const int r = rs + 8 * j;
+        if (r < n && r >= k) {
+          const double2 u1 = r > k ? a1[r] : make_double2(0.0, 0.0);
+          s1 = cfma_conj(s1, u1, xr[j]);
+          s0 = cfma_conj(s0, a0[r], xr[j]);
         }
       }
 #pragma unroll
@@ -483,56 +535,55 @@ __global__ void __launch_bounds__(kThreads) herm_eig_kernel(double2* __restrict_
         s1.y += __shfl_xor_sync(0xffffffffu, s1.y, o);
         s0.x += __shfl_xor_sync(0xffffffffu, s0.x, o);
         s0.y += __shfl_xor_sync(0xffffffffu, s0.y, o);
-        c01.x += __shfl_xor_sync(0xffffffffu, c01.x, o);
-        c01.y += __shfl_xor_sync(0xffffffffu, c01.y, o);
       }
       const double2 f1 = cmul(t1, s1);
       const double2 g = cmul(c01, f1);
       const double2 f0 = cmul(t0, make_double2(s0.x - g.x, s0.y - g.y));
-      if (act) {
-        if (rs == 0) {
-          double2& x = xat(k);
-          const double2 u = cmul(v0[0], f0);
-          x.x -= u.x;
-          x.y -= u.y;
-        }
-        for (int i = rs; i < m1; i += 8) {
-          double2& x = xat(k + 1 + i);
-          const double2 u = cadd(cmul(v1[i], f1), cmul(v0[i + 1], f0));
-          x.x -= u.x;
-          x.y -= u.y;
+#pragma unroll
+      for (int j = 0; j < RJ; ++j) {
+        const int r = rs + 8 * j;
+        if (r < n && r >= k) {
+          const double2 u1 = r > k ? a1[r] : make_double2(0.0, 0.0);
+          const double2 u = cadd(cmul(u1, f1), cmul(a0[r], f0));
+          xr[j].x -= u.x;
+          xr[j].y -= u.y;
         }
       }
     }
-    if (k == 0) {  // leftover single reflector
+    if (k == 0) {  // leftover single reflector: v[r] = A[0][r], r >= 1
       const double2 tk = tau[0];
-      const double2* vk = A + 1;
-      const int m = n - 1;
       double2 sd = make_double2(0.0, 0.0);
-      if (act)
-        for (int i = rs; i < m; i += 8) sd = cfma_conj(sd, vk[i], xat(1 + i));
+#pragma unroll
+      for (int j = 0; j < RJ; ++j) {
+        const int r = rs + 8 * j;
+        if (r < n && r >= 1) sd = cfma_conj(sd, A[r], xr[j]);
+      }
 #pragma unroll
       for (int o = 1; o < 8; o <<= 1) {
         sd.x += __shfl_xor_sync(0xffffffffu, sd.x, o);
         sd.y += __shfl_xor_sync(0xffffffffu, sd.y, o);
       }
       const double2 f = cmul(tk, sd);
-      if (act)
-        for (int i = rs; i < m; i += 8) {
-          double2& x = xat(1 + i);
-          const double2 u = cmul(vk[i], f);
-          x.x -= u.x;
-          x.y -= u.y;
+#pragma unroll
+      for (int j = 0; j < RJ; ++j) {
+        const int r = rs + 8 * j;
+        if (r < n && r >= 1) {
+          const double2 u = cmul(A[r], f);
+          xr[j].x -= u.x;
+          xr[j].y -= u.y;
         }
+      }
     }
-  }
-  __syncthreads();
-  bool bad = false;
-  for (int e0 = tid; e0 < n * n; e0 += kThreads) {
-    const int i = e0 % n, c = e0 / n;
-    const double2 x = X[i * xs + c];
-    bad |= !isfinite(x.x) || !isfinite(x.y);
-    H[i + size_t(c) * n] = x;
+    if (act) {
+#pragma unroll
+      for (int j = 0; j < RJ; ++j) {
+        const int r = rs + 8 * j;
+        if (r < n) {
+          bad |= !isfinite(xr[j].x) || !isfinite(xr[j].y);
+          H[r + size_t(c) * n] = xr[j];
+        }
+      }
+    }
   }
   if (tid < n) {
     w[tid] = lam[tid];
@@ -546,7 +597,7 @@ size_t herm_eig_smem(int n) {
   const size_t np = size_t(n) * (n + 1);  // full matrix, padded rows
   const size_t uwords = (std::max<size_t>(2 * size_t(n) * (n + 1), 3 * size_t(n) * n) + 1) & ~size_t(1);
   return np * sizeof(double2) + uwords * sizeof(double) + 3 * size_t(n) * sizeof(double2) +
-         (4 * size_t(n) + kThreads / 32 + size_t(n) * (n + 1)) * sizeof(double) + (2 * size_t(n) + 1) * sizeof(int);
+         (5 * size_t(n) + kThreads / 32 + size_t(n) * (n + 1)) * sizeof(double) + (2 * size_t(n) + 1) * sizeof(int);
 }
 
 }  // namespace
