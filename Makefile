@@ -24,7 +24,7 @@ clean:
 
 # ---- product library (CUDA sm_100a)
 PKG       := paper_2302_13431_b200
-CU_SRC    := $(PKG)/csrc/sk_axis.cu $(PKG)/csrc/sk_gram.cu $(PKG)/csrc/sk_fold.cu $(PKG)/csrc/sk_power.cu \
+CU_SRC    := $(PKG)/csrc/sk_axis.cu $(PKG)/csrc/sk_gram.cu $(PKG)/csrc/sk_fold.cu $(PKG)/csrc/sk_power.cu $(PKG)/csrc/sk_power_wide.cu \
              $(PKG)/csrc/sk_misc.cu $(PKG)/csrc/sk_small.cu $(PKG)/csrc/sk_expand.cu $(PKG)/csrc/sk_interp.cu $(PKG)/csrc/sk_eig.cu $(PKG)/csrc/sk_cholqr.cu $(PKG)/csrc/sk_dense.cu \
              $(PKG)/csrc/sk_runtime.cu
 CU_HDR    := $(PKG)/csrc/sk_internal.h include/senskit_b200.h

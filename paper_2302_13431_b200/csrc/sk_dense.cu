@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(256) dense_eig_kernel(DenseEigArgs a, int warp
       const float2 hv = a.planes[i64(e) * a.n + j];
       double2 g = make_double2(double(hv.x), double(hv.y));
       if (a.planes_lo) {
-        const float2 lv = a.planes_lo[i64(e) * a.n + j];
+        const float2 lv = lo_unpack(a.planes_lo[i64(e) * a.n + j]);
         g.x += double(lv.x);
         g.y += double(lv.y);
       }

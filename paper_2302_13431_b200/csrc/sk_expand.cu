@@ -6,10 +6,11 @@
 //   x_0 + sum_{l=1..H} [ c_l (x_l + x_-l) + i s_l (x_l - x_-l) ],
 // (c, s) = (cos, -sin)(2 pi l (j - j0) / N): half the MACs of a plain DFT.
 //
-// Arithmetic is FP64 and the final stage writes G as an fp32 pair
-// (hi = fl32(G), lo = fl32(G - hi)): K4 iterates on hi alone (FP32, registers)
-// and evaluates the Rayleigh quotient on hi + lo, so per-voxel eigenvalues
-// keep ~FP64 accuracy even where lambda ~ 1e-4.
+// Arithmetic is FP64 and the final stage writes G as an fp32 value plus a
+// bf16 residual (hi = fl32(G), lo = bf16(G - hi): 12 bytes per packed entry,
+// G known to 2^-33 |G|): K4 iterates on hi alone (FP32, registers) and
+// evaluates the Rayleigh quotient on hi + lo, so per-voxel eigenvalues stay
+// accurate even where lambda ~ 1e-4.
 //
 //  * expand_row: stage along an axis with small inner extent (always the last
 //    axis): a block stages RB rows' (S, D) in shared memory and each thread
@@ -29,20 +30,20 @@ namespace {
 constexpr int kRB = 8;       // rows per expand_row block
 constexpr int kColRows = 32; // table rows staged per chunk in expand_col
 
-__device__ __forceinline__ void store_out(double2 v, double2* out64, float2* hi, float2* lo, i64 idx) {
+__device__ __forceinline__ void store_out(double2 v, double2* out64, float2* hi, lo2* lo, i64 idx) {
   if (out64) {
     out64[idx] = v;
   } else {
     const float hx = float(v.x), hy = float(v.y);
     hi[idx] = make_float2(hx, hy);
-    lo[idx] = make_float2(float(v.x - double(hx)), float(v.y - double(hy)));
+    lo[idx] = lo_pack(v.x - double(hx), v.y - double(hy));
   }
 }
 
 template <int H>
 __global__ void __launch_bounds__(256) expand_row_kernel(const double2* __restrict__ in, i64 rows, i64 inner, int N,
                                                          const double2* __restrict__ cs, double2* out64, float2* hi,
-                                                         float2* lo) {
+                                                         lo2* lo) {
   constexpr int L = 2 * H + 1;
   __shared__ double2 sS[kRB][H + 1], sD[kRB][H + 1];  // [row][0] of sS holds x_0
   const i64 r0 = i64(blockIdx.x) * kRB;
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(256) expand_row_kernel(const double2* __restri
 template <int H, bool FULL>
 __global__ void __launch_bounds__(256) expand_col_kernel(const double2* __restrict__ in, i64 inner, int N, int jc,
                                                          const double2* __restrict__ cs, double2* out64, float2* hi,
-                                                         float2* lo) {
+                                                         lo2* lo) {
   constexpr int L = 2 * H + 1;
   __shared__ __align__(16) double2 tab_chunk[FULL ? 1 : kColRows * (H > 0 ? H : 1)];
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -193,7 +194,7 @@ template <int H>
 __global__ void __launch_bounds__(256) expand_col_persist_kernel(const double2* __restrict__ in, i64 inner, int N,
                                                                  int jc, int items, i64 nblocks,
                                                                  const double2* __restrict__ cs, double2* out64,
-                                                                 float2* hi, float2* lo) {
+                                                                 float2* hi, lo2* lo) {
   constexpr int L = 2 * H + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* tab = reinterpret_cast<double2*>(smem_raw);  // [items][H] (items = P + S1, computed by the host)
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(256) expand_col_persist_kernel(const double2* 
 
 template <int H>
 void launch_stage(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int N, int jc, const double2* cs,
-                  double2* out64, float2* hi, float2* lo) {
+                  double2* out64, float2* hi, lo2* lo) {
   if (inner >= 32) {
     const i64 gx = (inner + 31) / 32 * batch;
     if (gx > 0x7fffffffLL) fail(SK_ERR_UNSUPPORTED, "expand: grid too large");
@@ -302,7 +303,7 @@ void launch_stage(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int N, i
 }  // namespace
 
 void expand_stage_f64(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int H, int N, int jc, const double2* cs,
-                      double2* out64, float2* hi, float2* lo) {
+                      double2* out64, float2* hi, lo2* lo) {
   if (batch <= 0 || N <= 0 || inner <= 0) return;
   switch (H) {
     case 0: launch_stage<0>(ctx, in, batch, inner, N, jc, cs, out64, hi, lo); break;

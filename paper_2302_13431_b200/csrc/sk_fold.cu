@@ -124,11 +124,16 @@ __device__ void make_twiddles(double2* tw, int P, double sign) {
   }
 }
 
-// (A) a[f][kk][q] = sum_s U[q lam + s, kk] e^{-2 pi i f.n_s / P}; block = (kk, q)
-__global__ void __launch_bounds__(256) spec_u_kernel(const double2* __restrict__ u, i64 n, int k, int q, int lam,
+// (A) a[f][kk][q] = sum_s U[q lam + s, kk] e^{-2 pi i f.n_s / P}; block = (kk, q).
+// blockIdx.y: slice of a multislice group (its own basis and column count).
+__global__ void __launch_bounds__(256) spec_u_kernel(const FoldBatch fb, i64 n, i64 a_stride, int q, int lam,
                                                      const int* __restrict__ offs, int nd, int tau,
                                                      double2* __restrict__ a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int k = fb.k[blockIdx.y];
+  if (int(blockIdx.x) >= k * q) return;
+  const double2* __restrict__ u = fb.u[blockIdx.y];
+  a += i64(blockIdx.y) * a_stride;
   const int P = 4 * tau + 1, B = 2 * tau + 1;
   int nbox = 1, bbox = 1;
   for (int d = 0; d < nd; ++d) {
@@ -163,12 +168,15 @@ __global__ void __launch_bounds__(256) spec_u_kernel(const double2* __restrict__
   for (int f = threadIdx.x; f < nbox; f += blockDim.x) a[(i64(f) * k + kk) * q + ch] = src[f];
 }
 
-// (B) S[pair][f] = sum_kk a[f][kk][c] conj(a[f][kk][p]) for pair (p <= c); block = f
-__global__ void __launch_bounds__(256) spec_pairs_kernel(const double2* __restrict__ a, int k, int q, int nbox,
-                                                         double2* __restrict__ S) {
+// (B) S[pair][f] = sum_kk a[f][kk][c] conj(a[f][kk][p]) for pair (p <= c); block = (f, slice)
+__global__ void __launch_bounds__(256) spec_pairs_kernel(const double2* __restrict__ a, const FoldBatch fb,
+                                                         i64 a_stride, int q, int nbox, double2* __restrict__ S) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* af = reinterpret_cast<double2*>(smem_raw);  // [k][q]
   const int f = blockIdx.x;
+  const int k = fb.k[blockIdx.y];
+  a += i64(blockIdx.y) * a_stride;
+  S += i64(blockIdx.y) * (i64(q) * (q + 1) / 2) * nbox;
   for (int e = threadIdx.x; e < k * q; e += blockDim.x) af[e] = a[i64(f) * k * q + e];
   __syncthreads();
   const int h = q * (q + 1) / 2;
@@ -200,6 +208,8 @@ __global__ void __launch_bounds__(256) spec_lags_kernel(const double2* __restric
   double2* buf0 = tw + P;
   double2* buf1 = buf0 + nbox;
   const int pr = blockIdx.x;
+  S += i64(blockIdx.y) * (i64(q) * (q + 1) / 2) * nbox;     // blockIdx.y: slice of a multislice group
+  lags += i64(blockIdx.y) * (i64(q) * (q + 1) / 2) * nbox;
   make_twiddles(tw, P, -1.0);
   for (int e = threadIdx.x; e < nbox; e += blockDim.x) buf0[e] = S[i64(pr) * nbox + e];
   __syncthreads();
@@ -266,29 +276,42 @@ size_t spectral_fold_smem(int nd, int tau, int k, int q) {
 
 void fold_lags_spectral(sk_ctx* ctx, const double2* u, i64 n, int k, int q, int lam, int nd, int tau,
                         const int* d_offs, double2* lags) {
+  FoldBatch fb{};
+  fb.u[0] = u;
+  fb.k[0] = k;
+  fold_lags_spectral_batched(ctx, fb, 1, n, q, lam, nd, tau, d_offs, lags);
+}
+
+// The same for a group of slices (one launch per stage, the slice on grid.y):
+// lags [slices][h][nbox].
+void fold_lags_spectral_batched(sk_ctx* ctx, const FoldBatch& fb, int slices, i64 n, int q, int lam, int nd, int tau,
+                                const int* d_offs, double2* lags) {
   const int P = 4 * tau + 1;
   int nbox = 1;
   for (int d = 0; d < nd; ++d) nbox *= P;
   const int h = q * (q + 1) / 2;
+  int kmax = 0;
+  for (int i = 0; i < slices; ++i) kmax = std::max(kmax, fb.k[i]);
   const size_t box_smem = (size_t(P) + 2 * size_t(nbox)) * sizeof(double2);
-  double2* S = ctx->arena.get<double2>("field:spec_S", i64(h) * nbox);
-  if (k > 0) {
-    double2* a = ctx->arena.get<double2>("field:spec_a", i64(nbox) * k * q);
+  double2* S = ctx->arena.get<double2>("field:spec_S", i64(slices) * h * nbox);
+  const i64 a_stride = i64(nbox) * kmax * q;
+  double2* a = ctx->arena.get<double2>("field:spec_a", std::max<i64>(1, i64(slices) * a_stride));
+  if (kmax > 0) {
     set_smem_limit(reinterpret_cast<const void*>(spec_u_kernel), box_smem);
-    spec_u_kernel<<<k * q, 256, box_smem, ctx->stream>>>(u, n, k, q, lam, d_offs, nd, tau, a);
+    spec_u_kernel<<<dim3(unsigned(kmax * q), unsigned(slices)), 256, box_smem, ctx->stream>>>(fb, n, a_stride, q, lam,
+                                                                                             d_offs, nd, tau, a);
     SKB_LAUNCH("spec_u_kernel");
-    const size_t ps = size_t(k) * q * sizeof(double2);
-    set_smem_limit(reinterpret_cast<const void*>(spec_pairs_kernel), ps);
-    spec_pairs_kernel<<<nbox, 256, ps, ctx->stream>>>(a, k, q, nbox, S);
-    SKB_LAUNCH("spec_pairs_kernel");
-    ctx->launches += 2;
-  } else {
-    SKB_CUDA(cudaMemsetAsync(S, 0, size_t(h) * nbox * sizeof(double2), ctx->stream));
+    ++ctx->launches;
   }
+  // (a slice without signal columns sums nothing: S = 0)
+  const size_t ps = std::max<size_t>(16, size_t(kmax) * q * sizeof(double2));
+  set_smem_limit(reinterpret_cast<const void*>(spec_pairs_kernel), ps);
+  spec_pairs_kernel<<<dim3(unsigned(nbox), unsigned(slices)), 256, ps, ctx->stream>>>(a, fb, a_stride, q, nbox, S);
+  SKB_LAUNCH("spec_pairs_kernel");
   set_smem_limit(reinterpret_cast<const void*>(spec_lags_kernel), box_smem);
-  spec_lags_kernel<<<h, 256, box_smem, ctx->stream>>>(S, q, nd, tau, lam, lags);
+  spec_lags_kernel<<<dim3(unsigned(h), unsigned(slices)), 256, box_smem, ctx->stream>>>(S, q, nd, tau, lam, lags);
   SKB_LAUNCH("spec_lags_kernel");
-  ++ctx->launches;
+  ctx->launches += 2;
 }
 
 void fold_lags_f64(sk_ctx* ctx, const double2* w, i64 n, int npairs, int lam, int nbox, const int2* d_pairs,

@@ -4,6 +4,7 @@
 
 #include <cuComplex.h>
 #include <cublas_v2.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
@@ -31,6 +32,17 @@ namespace skb {
 
 using i64 = std::int64_t;
 using Dims = std::vector<i64>;
+
+// The residual planes of G(x) (lo = G - fl32(G), |lo| <= 2^-24 |G|) are kept
+// as bf16 pairs: 8 significant bits of the residual leave G known to
+// 2^-33 |G| per entry, far below the FP32 Gram's own ~1e-7, at half the
+// bytes of an fp32 residual (K3 writes and K4 reads 12 instead of 16 bytes
+// per packed entry).
+using lo2 = __nv_bfloat162;
+__host__ __device__ __forceinline__ lo2 lo_pack(double x, double y) {
+  return __floats2bfloat162_rn(float(x), float(y));
+}
+__host__ __device__ __forceinline__ float2 lo_unpack(lo2 v) { return __bfloat1622float2(v); }
 
 // Error classes mirror the reference's exceptions (types.hpp:22-32).
 struct Error : std::runtime_error {
@@ -166,6 +178,10 @@ struct sk_ctx {
   std::map<skb::RoundKey, skb::RoundGraph> rounds;
   // chunked K4 + overlapped device->host copies of the maps (pinned host outputs)
   cudaStream_t copy_stream = nullptr;
+  // multislice with the grouped tail: the batched K1 + K2 producer runs on a
+  // highest-priority stream so its short latency-bound kernels are scheduled
+  // ahead of the consumer's large K3-K5 launches
+  cudaStream_t hp_stream = nullptr;
   cudaEvent_t chunk_ev[9] = {};
   // multislice lanes: host outputs copied on copy_stream behind the pipeline
   // (double-buffered staging), drained by the batched driver
@@ -215,6 +231,14 @@ void fold_lags_f64(sk_ctx* ctx, const double2* w, i64 n, int npairs, int lam, in
 void herk_full(sk_ctx* ctx, const float2* f, i64 n, i64 r, float2* w);
 // signal-space fold by the correlation theorem on the lag box (no n x n W, no library call)
 size_t spectral_fold_smem(int nd, int tau, int k, int q);
+// A group of slices for the spectral fold (passed by value as a kernel parameter).
+constexpr int kFoldBatchMax = 32;
+struct FoldBatch {
+  const double2* u[kFoldBatchMax];  // device, n x k_i signal bases
+  int k[kFoldBatchMax];
+};
+void fold_lags_spectral_batched(sk_ctx* ctx, const FoldBatch& fb, int slices, i64 n, int q, int lam, int nd, int tau,
+                                const int* d_offs, double2* lags);
 void fold_lags_spectral(sk_ctx* ctx, const double2* u, i64 n, int k, int q, int lam, int nd, int tau,
                         const int* d_offs, double2* lags);
 void fold_lags_f32(sk_ctx* ctx, const float2* w, i64 n, int npairs, int lam, int nbox, const int2* d_pairs,
@@ -224,7 +248,7 @@ void fold_lags_f32(sk_ctx* ctx, const float2* w, i64 n, int npairs, int lam, int
 // jc: row of the grid centre relative to the first output row (the table
 // cs starts at that row; used to pair mirrored rows).
 void expand_stage_f64(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int H, int N, int jc, const double2* cs,
-                      double2* out64, float2* hi, float2* lo);
+                      double2* out64, float2* hi, lo2* lo);
 
 // K4: batched per-voxel power iteration over packed Hermitian planes
 // [h][N] (h = Q(Q+1)/2, plane (p<=q) holds M(row p, col q)).
@@ -233,7 +257,7 @@ void expand_stage_f64(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int 
 // against recon [Q][N] (maps.cpp:117-172), zeroed voxel count, mask.
 struct PowerArgs {
   const float2* planes;
-  const float2* planes_lo;  // nullable: fp32 residual G - hi, used only in the final Rayleigh quotient
+  const lo2* planes_lo;     // nullable: bf16 residual G - hi, used only in the final Rayleigh quotient
   i64 n;            // voxels
   int q;            // channels
   int iters;
@@ -253,8 +277,16 @@ struct PowerArgs {
   // > 0: stride of planes / recon / maps (the pointers address voxel n0 of a
   // larger grid of ld voxels; n voxels are processed).  0: ld = n.
   i64 ld;
+  // > 1: a stack of independent slices in one launch (multislice groups):
+  // planes [slices][h][ld], recon / maps [slices][Q][ld], lambda / value / mask
+  // [slices][ld], zeroed [slices]; n voxels per slice.  0 / 1: one slice.
+  int slices;
 };
 void power_iteration(sk_ctx* ctx, const PowerArgs& a);
+// More than 64 channels (sk_power_wide.cu): one CTA per voxel, the packed
+// triangle in shared memory; power_iteration dispatches to it.
+void power_iteration_wide(sk_ctx* ctx, const PowerArgs& a);
+int power_wide_max_q();
 
 // Baseline preset (sk_dense.cu).
 // build_calib_matrix (calibration.cpp:30-68): P x Q|Lambda| column-major, FP64.
@@ -266,7 +298,7 @@ void gram_explicit_dev(sk_ctx* ctx, const double2* c, i64 rows, i64 n, double2* 
 // eigenpair of B = alpha I + beta (hi + lo) by FP64 cyclic Jacobi.
 struct DenseEigArgs {
   const float2* planes;
-  const float2* planes_lo;  // nullable
+  const lo2* planes_lo;     // nullable
   i64 n;
   int q;
   int largest;              // 1: largest (ESPIRiT), 0: smallest (nullspace method)
@@ -285,7 +317,7 @@ void dense_eig(sk_ctx* ctx, const DenseEigArgs& a);
 void c64_to_c128(sk_ctx* ctx, const float2* in, double2* out, i64 n);
 void c128_to_c64(sk_ctx* ctx, const double2* in, float2* out, i64 n);
 void field_full_to_planes(sk_ctx* ctx, const float2* field, i64 n, int q, float2* planes);
-void planes_to_field_full(sk_ctx* ctx, const float2* planes, const float2* planes_lo, i64 n, int q, float2* field);
+void planes_to_field_full(sk_ctx* ctx, const float2* planes, const lo2* planes_lo, i64 n, int q, float2* field);
 void espirit_field(sk_ctx* ctx, float2* field, i64 n, int q, float inv_lam);
 void renormalize_and_mask(sk_ctx* ctx, float2* maps, i64 n, int q, const float2* lambda_c, float* lambda,
                           uint8_t* mask, float thr);
@@ -295,9 +327,9 @@ void sos_accumulate(sk_ctx* ctx, const float2* maps, i64 n, int q, float* sos); 
 double projection_residual_value(sk_ctx* ctx, const float2* img, const float2* maps, i64 n, int q);
 // parity probe (sk_estimate_maps_probe): gathers + Frobenius sums, FP64
 void probe_gather_gram(sk_ctx* ctx, const float2* gram, i64 n, const long long* idx, i64 k, double2* out);
-void probe_gather_field(sk_ctx* ctx, const float2* hi, const float2* lo, i64 nvox, int q, const long long* idx,
+void probe_gather_field(sk_ctx* ctx, const float2* hi, const lo2* lo, i64 nvox, int q, const long long* idx,
                         i64 k, double2* out);
-double probe_sumsq(sk_ctx* ctx, const float2* a, const float2* lo, i64 total, i64 plane_len, int q);
+double probe_sumsq(sk_ctx* ctx, const float2* a, const lo2* lo, i64 total, i64 plane_len, int q);
 // Centred transform along one axis (fft.cpp kspace_to_image / image_to_kspace):
 // out = fftshift(DFT(ifftshift(in))) * scale, inverse = conjugate kernel.
 // Returns false (nothing launched) unless N and inner are powers of two.
@@ -315,7 +347,7 @@ bool interp_axis_fft(sk_ctx* ctx, const void* in, void* out, i64 batch, int n, i
 // Last (innermost, factor-2) interpolation pass of a [Q][P][n] stack fused with
 // the per-voxel sum-of-squares renormalisation; false (nothing launched) when
 // the shape is outside the kernel (Q a power of two <= 32, Q*n <= 4096).
-bool interp_last_axis_sos(sk_ctx* ctx, const float2* in, float2* out, int q, i64 positions, int n, int N);
+bool interp_last_axis_sos(sk_ctx* ctx, const float2* in, float2* out, int q, i64 positions, int n, int N, int slices = 1);
 void copy_strided(sk_ctx* ctx, const float2* src, i64 src_rs, i64 src_cs, float2* dst, i64 dst_rs, i64 dst_cs, i64 rows,
                   i64 cols);
 void normalize_standalone(sk_ctx* ctx, float2* maps, i64 n, int q, const float2* recon, unsigned long long* zeroed);

@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(256) interp2_fft_kernel(const typename Cplx<R>
 // voxel's channels meet in shared memory: sos = sum_c |out_c|^2, then
 // out_c / sqrt(sos) where sos > 0.  Saves the separate renormalisation pass
 // (which reads the full-resolution maps twice and writes them once).
-// in [Q][P][n] -> out [Q][P][2n].
+// in [Q][P][n] -> out [Q][P][2n]; blockIdx.y: slice of a stack [slices][Q][P][.].
 template <int LOGN_, int LOGQ_>
 __global__ void __launch_bounds__(256) interp2_sos_kernel(const float2* __restrict__ in, float2* __restrict__ out,
                                                           unsigned positions, int logn_arg, int logq_arg) {
@@ -338,6 +338,8 @@ __global__ void __launch_bounds__(256) interp2_sos_kernel(const float2* __restri
     tw[k].y = sn;
   }
   const unsigned p = blockIdx.x;
+  in += (size_t(blockIdx.y) * T * positions) << logn;
+  out += (size_t(blockIdx.y) * T * positions) << logN;
   const int cl = n / 2;
   {  // all of a thread's loads in flight before the shared-memory stores (as interp2_fft_kernel)
     constexpr int kLd = 16;
@@ -558,9 +560,11 @@ bool centered_fft_axis(sk_ctx* ctx, const void* in, void* out, i64 batch, int N,
   return true;
 }
 
-bool interp_last_axis_sos(sk_ctx* ctx, const float2* in, float2* out, int q, i64 positions, int n, int N) {
+bool interp_last_axis_sos(sk_ctx* ctx, const float2* in, float2* out, int q, i64 positions, int n, int N,
+                          int slices) {
   const bool pow2 = n >= 2 && !(n & (n - 1)) && q >= 1 && !(q & (q - 1));
-  if (!pow2 || N != 2 * n || q > 32 || i64(q) * n > 16 * 256 || positions < 1 || positions >= (i64(1) << 31))
+  if (!pow2 || N != 2 * n || q > 32 || i64(q) * n > 16 * 256 || positions < 1 || positions >= (i64(1) << 31) ||
+      slices < 1 || slices > 65535)
     return false;
   const int logn = __builtin_ctz(unsigned(n)), logq = __builtin_ctz(unsigned(q));
   const int ld = n + n / 16 + 1;
@@ -568,7 +572,8 @@ bool interp_last_axis_sos(sk_ctx* ctx, const float2* in, float2* out, int q, i64
   if (smem > 200 * 1024) return false;
   auto go = [&](auto kern) {
     set_smem_limit(reinterpret_cast<const void*>(kern), smem);
-    kern<<<unsigned(positions), 256, smem, ctx->stream>>>(in, out, unsigned(positions), logn, logq);
+    kern<<<dim3(unsigned(positions), unsigned(slices)), 256, smem, ctx->stream>>>(in, out, unsigned(positions), logn,
+                                                                                 logq);
   };
   if (logn == 6 && logq == 5)
     go(interp2_sos_kernel<6, 5>);

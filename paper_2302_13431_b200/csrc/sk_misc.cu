@@ -43,7 +43,7 @@ __global__ void full_to_planes_kernel(const float2* __restrict__ field, i64 n, i
 
 // planes -> GramField with the conjugate mirror and real diagonal
 // (spatial_gram.cpp:133-146).
-__global__ void planes_to_full_kernel(const float2* __restrict__ planes, const float2* __restrict__ planes_lo, i64 n,
+__global__ void planes_to_full_kernel(const float2* __restrict__ planes, const lo2* __restrict__ planes_lo, i64 n,
                                       int q, float2* __restrict__ field) {
   const i64 total = n * q * q;
   for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += i64(gridDim.x) * blockDim.x) {
@@ -54,7 +54,7 @@ __global__ void planes_to_full_kernel(const float2* __restrict__ planes, const f
     const int pair = p * q - p * (p - 1) / 2 + (c - p);
     float2 v = planes[i64(pair) * n + j];
     if (planes_lo) {
-      const float2 l = planes_lo[i64(pair) * n + j];
+      const float2 l = lo_unpack(planes_lo[i64(pair) * n + j]);
       v = make_float2(float(double(v.x) + double(l.x)), float(double(v.y) + double(l.y)));
     }
     if (row > col) v.y = -v.y;
@@ -307,7 +307,7 @@ void field_full_to_planes(sk_ctx* ctx, const float2* field, i64 n, int q, float2
   ++ctx->launches;
   SKB_LAUNCH("full_to_planes");
 }
-void planes_to_field_full(sk_ctx* ctx, const float2* planes, const float2* planes_lo, i64 n, int q, float2* field) {
+void planes_to_field_full(sk_ctx* ctx, const float2* planes, const lo2* planes_lo, i64 n, int q, float2* field) {
   planes_to_full_kernel<<<SKB_GRID(n * q * q)>>>(planes, planes_lo, n, q, field);
   ++ctx->launches;
   SKB_LAUNCH("planes_to_full");
@@ -543,7 +543,7 @@ __global__ void probe_gram_kernel(const float2* __restrict__ g, i64 n, const lon
   out[t] = make_double2(v.x, v.y);
 }
 
-__global__ void probe_field_kernel(const float2* __restrict__ hi, const float2* __restrict__ lo, i64 nvox, int q,
+__global__ void probe_field_kernel(const float2* __restrict__ hi, const lo2* __restrict__ lo, i64 nvox, int q,
                                    const long long* __restrict__ idx, i64 k, double2* __restrict__ out) {
   const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= k) return;
@@ -554,7 +554,7 @@ __global__ void probe_field_kernel(const float2* __restrict__ hi, const float2* 
   const float2 h = hi[pair * nvox + j];
   double re = h.x, im = h.y;
   if (lo) {
-    const float2 l = lo[pair * nvox + j];
+    const float2 l = lo_unpack(lo[pair * nvox + j]);
     re += double(l.x);
     im += double(l.y);
   }
@@ -566,7 +566,7 @@ __global__ void probe_field_kernel(const float2* __restrict__ hi, const float2* 
 // sum |a (+ lo)|^2; planes mode (q > 0): element e lies in plane e / plane_len,
 // off-diagonal planes count twice (their mirrored half of the full matrix).
 __global__ void __launch_bounds__(256) sumsq_partial_kernel(const float2* __restrict__ a,
-                                                            const float2* __restrict__ lo, i64 total,
+                                                            const lo2* __restrict__ lo, i64 total,
                                                             i64 plane_len, int q, double* __restrict__ partial) {
   __shared__ double s[256];
   double acc = 0.0;
@@ -574,8 +574,9 @@ __global__ void __launch_bounds__(256) sumsq_partial_kernel(const float2* __rest
     const float2 v = a[e];
     double re = v.x, im = v.y;
     if (lo) {
-      re += double(lo[e].x);
-      im += double(lo[e].y);
+      const float2 l = lo_unpack(lo[e]);
+      re += double(l.x);
+      im += double(l.y);
     }
     double w = 1.0;
     if (q > 0) {
@@ -604,7 +605,7 @@ void probe_gather_gram(sk_ctx* ctx, const float2* gram, i64 n, const long long* 
   SKB_LAUNCH("probe_gram");
 }
 
-void probe_gather_field(sk_ctx* ctx, const float2* hi, const float2* lo, i64 nvox, int q, const long long* idx,
+void probe_gather_field(sk_ctx* ctx, const float2* hi, const lo2* lo, i64 nvox, int q, const long long* idx,
                         i64 k, double2* out) {
   if (k <= 0) return;
   probe_field_kernel<<<unsigned((k + 255) / 256), 256, 0, ctx->stream>>>(hi, lo, nvox, q, idx, k, out);
@@ -612,7 +613,7 @@ void probe_gather_field(sk_ctx* ctx, const float2* hi, const float2* lo, i64 nvo
   SKB_LAUNCH("probe_field");
 }
 
-double probe_sumsq(sk_ctx* ctx, const float2* a, const float2* lo, i64 total, i64 plane_len, int q) {
+double probe_sumsq(sk_ctx* ctx, const float2* a, const lo2* lo, i64 total, i64 plane_len, int q) {
   const int blocks = int(std::max<i64>(1, std::min<i64>((total + 255) / 256, 4 * i64(ctx->sm_count))));
   double* partial = ctx->arena.get<double>("probe:partial", blocks);
   sumsq_partial_kernel<<<blocks, 256, 0, ctx->stream>>>(a, lo, total, plane_len, q, partial);

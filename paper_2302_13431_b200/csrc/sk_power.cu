@@ -5,7 +5,7 @@
 //
 // Layout: G arrives as packed Hermitian planes [h][N] (h = Q(Q+1)/2; plane
 // (p <= q) holds G(row p, col q) for every voxel, written by the K3
-// expansion) as an fp32 hi/lo pair.  Blocks are persistent and walk voxel
+// expansion) as an fp32 hi plane plus a bf16 residual lo plane.  Blocks are persistent and walk voxel
 // tiles; the next tile's h x VPB slab of hi planes is prefetched by TMA
 // (cp.async.bulk.tensor boxes on an mbarrier, double buffer; swizzled 32/64 B
 // rows so that the unpack and the epilogue reads spread over the banks; an
@@ -63,6 +63,10 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -107,12 +111,18 @@ struct TmaTiles {
   int use = 0;  // 0: cp.async fallback (plane stride not a multiple of 16 B)
   int hb = 0, nb = 0;
   int swz = 0;  // swizzle mask applied by the readers (0: dense tile)
+  int swz_lo = 0;  // the same for the lo tile (4-byte elements: rows half as long)
 };
 
 // float2 index of tile element idx under the TMA swizzle (buffer 1 KB aligned).
 __device__ __forceinline__ int swz_at(int idx, int mask) {
   const int b = idx << 3;
   return (b ^ (((b >> 7) & mask) << 4)) >> 3;
+}
+// lo2 index of lo-tile element idx under its swizzle.
+__device__ __forceinline__ int swz_lo_at(int idx, int mask) {
+  const int b = idx << 2;
+  return (b ^ (((b >> 7) & mask) << 4)) >> 2;
 }
 
 template <int QP_, int RPT_, int THREADS_, int MINB_, int ACC_ = 0, int PF_ = 4, int QF_ = 0, int TILE_ = 0>
@@ -215,7 +225,9 @@ __device__ __forceinline__ float2 herm_at_bf(const float2* gs, int p, int c, int
   return in ? make_float2(t.x, p == c ? 0.f : (p <= c ? t.y : -t.y)) : make_float2(0.f, 0.f);
 }
 
-template <class L>
+// STACK: a.slices > 1 (the tile index also selects the slice; compiled out of
+// the single-slice kernel, where the extra index math cost 2% on C2/C4).
+template <class L, bool STACK>
 __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     power_kernel(PowerArgs a, const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
                  TmaTiles tt, int tile_rows) {
@@ -229,8 +241,8 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
   // tile buffers start on a 1 KB boundary (the swizzle pattern follows address bits 4..9)
   float2* gbuf = reinterpret_cast<float2*>(smem_raw + ((smem_u32(smem_raw) + 128 + 1023) & ~1023u) -
                                            smem_u32(smem_raw));  // [2][tile_elems] hi planes
-  float2* lbuf = gbuf + 2 * tile_elems;                                  // [tile_elems] lo planes
-  float2* vs = lbuf + tile_elems;                                        // [2][VPB][kStride]
+  lo2* lbuf = reinterpret_cast<lo2*>(gbuf + 2 * tile_elems);             // [tile_elems] lo planes (bf16 pairs)
+  float2* vs = reinterpret_cast<float2*>(lbuf + tile_elems);             // [2][VPB][kStride]
   double2* vds = reinterpret_cast<double2*>(vs + 2 * VPB * L::kStride);  // [VPB][QP] final v in FP64
   double* redd = reinterpret_cast<double*>(vds + VPB * QP);              // [VPB][kWPV]
   float* red = reinterpret_cast<float*>(redd + VPB * WPV);               // [VPB][kWPV]
@@ -245,7 +257,8 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
   const int vox = threadIdx.x / TPV;
   const int local = threadIdx.x % TPV;
   const int prow = L::row_of(local);    // the thread's rows: prow + r * TPV
-  const i64 tiles = (a.n + VPB - 1) / VPB;
+  const i64 tps = (a.n + VPB - 1) / VPB;  // tiles per slice
+  const i64 tiles = STACK ? tps * a.slices : tps;
   const i64 ld = a.ld > 0 ? a.ld : a.n;  // plane / channel stride (a voxel range of a larger grid)
 
   // Tile loads.  TMA path: one thread issues nb boxes (hb plane rows x VPB
@@ -257,20 +270,45 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
   }
   __syncthreads();
   unsigned phase = 0;  // bit k: parity of bars[k]
+  // (a stack of slices: tile t = slice t / tps, tile t % tps of that slice; the
+  // slice's planes are rows [slice h, slice h + h) of the 2-D tensor)
   auto load_tile = [&](i64 t, float2* dst, const float2* src, const CUtensorMap* map, int bar) {
-    const i64 jj0 = t * VPB;
+    const i64 sl = STACK ? t / tps : 0;
+    const i64 jj0 = (t - sl * tps) * VPB;
     if (tt.use) {
       if (threadIdx.x == 0) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // prior generic writes to dst
         mbar_expect_tx(bars + bar, unsigned(tt.nb * tt.hb * VPB * sizeof(float2)));
-        for (int k = 0; k < tt.nb; ++k) tma_load_2d(dst + k * tt.hb * VPB, map, int(jj0), k * tt.hb, bars + bar);
+        for (int k = 0; k < tt.nb; ++k)
+          tma_load_2d(dst + k * tt.hb * VPB, map, int(jj0), int(sl) * h + k * tt.hb, bars + bar);
       }
       return;
     }
+    src += sl * i64(h) * ld;
     for (int e = threadIdx.x; e < h * VPB; e += blockDim.x) {
       const int pair = e / VPB, v = e % VPB;
       const bool ok = jj0 + v < a.n;
       cp_async8(dst + e, src + (ok ? i64(pair) * ld + jj0 + v : 0), ok ? 8 : 0);
+    }
+    cp_async_commit();
+  };
+  auto load_lo_tile = [&](i64 t) {  // the tile's lo planes into lbuf, completing on bars[2]
+    const i64 sl = STACK ? t / tps : 0;
+    const i64 jj0 = (t - sl * tps) * VPB;
+    if (tt.use) {
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_expect_tx(bars + 2, unsigned(tt.nb * tt.hb * VPB * sizeof(lo2)));
+        for (int k = 0; k < tt.nb; ++k)
+          tma_load_2d(lbuf + k * tt.hb * VPB, &tm_lo, int(jj0), int(sl) * h + k * tt.hb, bars + 2);
+      }
+      return;
+    }
+    const lo2* src = a.planes_lo + sl * i64(h) * ld;
+    for (int e = threadIdx.x; e < h * VPB; e += blockDim.x) {
+      const int pair = e / VPB, v = e % VPB;
+      const bool ok = jj0 + v < a.n;
+      cp_async4(lbuf + e, src + (ok ? i64(pair) * ld + jj0 + v : 0), ok ? 4 : 0);
     }
     cp_async_commit();
   };
@@ -295,9 +333,11 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
       __syncthreads();
     }
     float2* gs = gbuf + buf * tile_elems;
-    const i64 j0 = tile * VPB;
+    const i64 sl = STACK ? tile / tps : 0;  // slice of this tile
+    const i64 j0 = (tile - sl * tps) * VPB;
     const i64 j = j0 + vox;
     const bool live = j < a.n;
+    const i64 cbase = sl * i64(Q) * ld;  // the slice's first channel row in recon / maps
 
     // Unpack this thread's rows.
     float2 m[RPT][QP];
@@ -323,13 +363,13 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     }
     // Stream the lo residual planes of this tile while the iterations run
     // (its own buffer: the final Rayleigh quotient reads hi and lo packed).
-    if (a.planes_lo != nullptr) load_tile(tile, lbuf, a.planes_lo, &tm_lo, 2);
+    if (a.planes_lo != nullptr) load_lo_tile(tile);
     // recon values for the epilogue, loaded while the iterations run
     float2 rcv[RPT];
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
       const int p = prow + r * TPV;
-      rcv[r] = (a.recon != nullptr && p < Q && live) ? a.recon[i64(p) * ld + j] : make_float2(0.f, 0.f);
+      rcv[r] = (a.recon != nullptr && p < Q && live) ? a.recon[cbase + i64(p) * ld + j] : make_float2(0.f, 0.f);
     }
 
     // v is double-buffered in shared memory (buffers 0 and 1) together with
@@ -684,7 +724,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
         const float2 hv = gs[swz_at(e * VPB + vox, tt.swz)];
         double mx = double(hv.x), my = double(hv.y);
         if (a.planes_lo != nullptr) {
-          const float2 lv = lbuf[swz_at(e * VPB + vox, tt.swz)];
+          const float2 lv = lo_unpack(lbuf[swz_lo_at(e * VPB + vox, tt.swz_lo)]);
           mx += double(lv.x);
           my += double(lv.y);
         }
@@ -739,7 +779,7 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
 #pragma unroll
         for (int r = 0; r < RPT; ++r) vp[r] = make_float2(vp[r].x * inv, vp[r].y * inv);
       } else if (local == 0 && live && a.zeroed) {
-        atomicAdd(a.zeroed, 1ull);
+        atomicAdd(a.zeroed + sl, 1ull);
       }
       const float mag = sqrtf(ux * ux + uy * uy);
       if (mag > 0.f) {
@@ -758,13 +798,14 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
     __syncthreads();
     for (int e = threadIdx.x; e < Q * VPB; e += blockDim.x) {
       const int c = e / VPB, v = e % VPB;
-      if (j0 + v < a.n) a.maps[i64(c) * ld + j0 + v] = ms[c * VPB + v];
+      if (j0 + v < a.n) a.maps[cbase + i64(c) * ld + j0 + v] = ms[c * VPB + v];
     }
     if (local == 0 && live) {
       const float lam = float(mv * double(a.lam_scale));
-      if (a.lambda) a.lambda[j] = lam;
-      if (a.value) a.value[j] = float(double(a.alpha) * vn2 + double(a.beta) * mv);
-      if (a.mask) a.mask[j] = lam < a.mask_threshold ? 1 : 0;
+      const i64 js = sl * ld + j;
+      if (a.lambda) a.lambda[js] = lam;
+      if (a.value) a.value[js] = float(double(a.alpha) * vn2 + double(a.beta) * mv);
+      if (a.mask) a.mask[js] = lam < a.mask_threshold ? 1 : 0;
     }
     __syncthreads();  // the staging buffer is the prefetch target two tiles on
   }
@@ -772,7 +813,9 @@ __global__ void __launch_bounds__(L::kThreads, L::kMinBlocks)
 
 // 2-D tensor map over packed planes [h][n] (float2 as one 8-byte element):
 // box {VPB voxels, hb plane rows}.  Returns false when TMA cannot address it.
-bool encode_planes(CUtensorMap* m, const float2* base, i64 n, i64 ld, int h, int vpb, int hb, CUtensorMapSwizzle swz) {
+// elem: bytes per element (8: float2 hi planes, 4: bf16-pair lo planes).
+bool encode_planes(CUtensorMap* m, const void* base, int elem, i64 n, i64 ld, i64 h, int vpb, int hb,
+                   CUtensorMapSwizzle swz) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -781,14 +824,17 @@ bool encode_planes(CUtensorMap* m, const float2* base, i64 n, i64 ld, int h, int
       fn = nullptr;
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
-  if (!encode || base == nullptr || (ld * 8) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  if (!encode || base == nullptr || (ld * elem) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0 ||
+      (vpb * elem) % 16 != 0)
+    return false;
   const cuuint64_t dims[2] = {cuuint64_t(n), cuuint64_t(h)};
-  const cuuint64_t strides[1] = {cuuint64_t(ld) * 8};
+  const cuuint64_t strides[1] = {cuuint64_t(ld) * cuuint64_t(elem)};
   const cuuint32_t box[2] = {cuuint32_t(vpb), cuuint32_t(hb)};
   const cuuint32_t estr[2] = {1, 1};
   // L2 promotion of the 8*vpb-byte box rows: 256 B
   constexpr CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<float2*>(base), dims, strides, box, estr,
+  return encode(m, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2,
+                const_cast<void*>(base), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
@@ -813,25 +859,40 @@ void launch(sk_ctx* ctx, const PowerArgs& a) {
     if (tt.hb <= 256) break;
   }
   const i64 ld = a.ld > 0 ? a.ld : a.n;
-  tt.use = encode_planes(&tm_hi, a.planes, a.n, ld, h, L::kVPB, tt.hb, swz) &&
-           (a.planes_lo == nullptr || encode_planes(&tm_lo, a.planes_lo, a.n, ld, h, L::kVPB, tt.hb, swz));
+  // the lo tile's rows are half as long: the next smaller swizzle (dense below 32 B)
+  const CUtensorMapSwizzle swz_lo = swz == CU_TENSOR_MAP_SWIZZLE_128B  ? CU_TENSOR_MAP_SWIZZLE_64B
+                                    : swz == CU_TENSOR_MAP_SWIZZLE_64B ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                                       : CU_TENSOR_MAP_SWIZZLE_NONE;
+  const i64 rows = i64(h) * (a.slices > 1 ? a.slices : 1);  // a stack of slices: [slices][h] plane rows
+  tt.use = encode_planes(&tm_hi, a.planes, 8, a.n, ld, rows, L::kVPB, tt.hb, swz) &&
+           (a.planes_lo == nullptr || encode_planes(&tm_lo, a.planes_lo, 4, a.n, ld, rows, L::kVPB, tt.hb, swz_lo));
   if (a.planes_lo == nullptr) tm_lo = tm_hi;
   tt.swz = !tt.use ? 0 : swz == CU_TENSOR_MAP_SWIZZLE_32B ? 1 : swz == CU_TENSOR_MAP_SWIZZLE_64B ? 3
                                                           : swz == CU_TENSOR_MAP_SWIZZLE_128B ? 7 : 0;
+  tt.swz_lo = !tt.use ? 0 : swz_lo == CU_TENSOR_MAP_SWIZZLE_32B ? 1 : swz_lo == CU_TENSOR_MAP_SWIZZLE_64B ? 3 : 0;
   const int alt = tt.swz ? std::max(al, 1024 / row_bytes) : al;
   const int tile_rows = (std::max(std::max(h, L::QP), tt.use ? tt.nb * tt.hb : 0) + alt - 1) / alt * alt;
   const size_t tile = size_t(tile_rows) * L::kVPB * sizeof(float2);
-  // two hi tile buffers (double-buffered prefetch) + the lo tile
-  const size_t smem = 1024 + 128 + 3 * tile +
+  // two hi tile buffers (double-buffered prefetch) + the lo tile (half the bytes)
+  const size_t smem = 1024 + 128 + 2 * tile + tile / 2 +
                       2 * size_t(L::kVPB) * L::kStride * sizeof(float2) +
                       size_t(L::kVPB) * L::QP * sizeof(double2) +
                       size_t(L::kVPB) * L::kWPV * (sizeof(double) + 3 * sizeof(float)) + size_t(h) * sizeof(int);
-  set_smem_limit(reinterpret_cast<const void*>(power_kernel<L>), smem);
+  const bool stack = a.slices > 1;
+  auto* kern = stack ? power_kernel<L, true> : power_kernel<L, false>;
+  set_smem_limit(reinterpret_cast<const void*>(kern), smem);
   int per_sm = 0;
-  SKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_kernel<L>, L::kThreads, smem));
-  const i64 tiles = (a.n + L::kVPB - 1) / L::kVPB;
+  SKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::kThreads, smem));
+  const i64 tiles = (a.n + L::kVPB - 1) / L::kVPB * (a.slices > 1 ? a.slices : 1);
+  // a stack of slices runs beside the multislice producer's kernels: SKB_STACK_CTAS caps the
+  // persistent CTAs per SM it occupies (measured, DESIGN.md §4 multislice)
+  static const int stack_cap = [] {
+    const char* v = std::getenv("SKB_STACK_CTAS");
+    return v ? std::max(1, std::atoi(v)) : 0;
+  }();
+  if (stack && stack_cap > 0) per_sm = std::min(per_sm, stack_cap);
   const i64 blocks = std::min<i64>(tiles, i64(std::max(per_sm, 1)) * ctx->sm_count);
-  power_kernel<L><<<unsigned(blocks), L::kThreads, smem, ctx->stream>>>(a, tm_hi, tm_lo, tt, tile_rows);
+  kern<<<unsigned(blocks), L::kThreads, smem, ctx->stream>>>(a, tm_hi, tm_lo, tt, tile_rows);
   ++ctx->launches;
   SKB_LAUNCH("power_kernel");
 }
@@ -864,7 +925,7 @@ void power_iteration(sk_ctx* ctx, const PowerArgs& a) {
   else if (a.q <= 64)
     launch<Layout<64, 1, 256, 1>>(ctx, a);
   else
-    fail(9, "eig_power_field: more than 64 channels is outside the B200 path");
+    power_iteration_wide(ctx, a);  // any Q the shared memory holds (sk_power_wide.cu)
 }
 
 }  // namespace skb

@@ -293,7 +293,7 @@ double2* symdft_table64(sk_ctx* ctx, int N, int H, i64 j0, int sign) {
 // first; intermediates stay FP64.
 // slab0/slab1: optional axis-0 row range [slab0, slab1) of the grid (z-slab
 // sharding); the outputs then cover only those rows.
-void expand_lags(sk_ctx* ctx, const double2* lags, float2* hi, float2* lo, i64 h, int tau, const Dims& grid,
+void expand_lags(sk_ctx* ctx, const double2* lags, float2* hi, lo2* lo, i64 h, int tau, const Dims& grid,
                  i64 slab0 = 0, i64 slab1 = -1) {
   const int nd = int(grid.size()), lb = 4 * tau + 1, H = 2 * tau;
   Dims cur(static_cast<size_t>(nd), lb);
@@ -325,7 +325,7 @@ void expand_lags(sk_ctx* ctx, const double2* lags, float2* hi, float2* lo, i64 h
 
 struct Planes {
   float2* hi = nullptr;
-  float2* lo = nullptr;
+  lo2* lo = nullptr;
 };
 
 // Device index tables per (support, q), cached in the context (freed by sk_destroy).
@@ -1187,7 +1187,7 @@ Planes run_field(sk_ctx* ctx, const Eig& e, const Support& s, int q, const Dims&
     Planes p;
     const i64 nvox = slab1 >= 0 ? numel(grid) / grid[0] * (slab1 - slab0) : numel(grid);
     p.hi = ctx->arena.get<float2>("field:planes", i64(h) * nvox);
-    p.lo = ctx->arena.get<float2>("field:planes_lo", i64(h) * nvox);
+    p.lo = ctx->arena.get<lo2>("field:planes_lo", i64(h) * nvox);
     expand_lags(ctx, lags, p.hi, p.lo, h, s.tau, grid, slab0, slab1);
     return p;
   };
@@ -1219,7 +1219,7 @@ Planes run_field_from_w(sk_ctx* ctx, const float2* w, const Support& s, int q, c
   fold_lags_f32(ctx, w, n, h, int(s.count), t.nbox, t.pairs, t.lag_ptr, t.lag_st, lags);
   Planes p;
   p.hi = ctx->arena.get<float2>("field:planes", i64(h) * numel(grid));
-  p.lo = ctx->arena.get<float2>("field:planes_lo", i64(h) * numel(grid));
+  p.lo = ctx->arena.get<lo2>("field:planes_lo", i64(h) * numel(grid));
   expand_lags(ctx, lags, p.hi, p.lo, h, s.tau, grid);
   return p;
 }
@@ -1259,7 +1259,9 @@ bool interp_fft_ok(const Dims& low, const Dims& full) {
 // (maps.cpp:236-250).  When the innermost axis doubles and Q fits the fused
 // kernel, the outer axes run first and the innermost pass renormalises in
 // the same kernel; returns false when the caller still has to renormalise.
-bool run_interp_renorm(sk_ctx* ctx, const float2* low, float2* out, i64 q, const Dims& low_dims, const Dims& full) {
+// slices > 1: a stack [slices][Q][low] -> [slices][Q][full] (multislice groups).
+bool run_interp_renorm(sk_ctx* ctx, const float2* low, float2* out, i64 q, const Dims& low_dims, const Dims& full,
+                       i64 slices = 1) {
   const int nd = int(low_dims.size());
   const int n = int(low_dims[size_t(nd - 1)]), N = int(full[size_t(nd - 1)]);
   if (!interp_fft_ok(low_dims, full) || N != 2 * n || q > 32 || (q & (q - 1)) || q * n > 4096) return false;
@@ -1270,8 +1272,9 @@ bool run_interp_renorm(sk_ctx* ctx, const float2* low, float2* out, i64 q, const
     if (low_dims[size_t(a)] == full[size_t(a)]) continue;
     Dims next = cur;
     next[size_t(a)] = full[size_t(a)];
-    float2* dst = ctx->arena.get<float2>(std::string("interp:fft") + (pass++ % 2 ? ":b" : ":a"), q * numel(next));
-    i64 b = q, inner = 1;
+    float2* dst = ctx->arena.get<float2>(std::string("interp:fft") + (pass++ % 2 ? ":b" : ":a"),
+                                         slices * q * numel(next));
+    i64 b = slices * q, inner = 1;
     for (int k = 0; k < a; ++k) b *= cur[size_t(k)];
     for (int k = a + 1; k < nd; ++k) inner *= cur[size_t(k)];
     if (!interp_axis_fft(ctx, src, dst, b, int(low_dims[size_t(a)]), int(full[size_t(a)]), inner, false))
@@ -1280,7 +1283,7 @@ bool run_interp_renorm(sk_ctx* ctx, const float2* low, float2* out, i64 q, const
     src = dst;
   }
   const i64 positions = numel(cur) / cur[size_t(nd - 1)];
-  if (!interp_last_axis_sos(ctx, src, out, int(q), positions, n, N))
+  if (!interp_last_axis_sos(ctx, src, out, int(q), positions, n, N, int(slices)))
     fail(SK_ERR_UNSUPPORTED, "interpolate_maps: fused last pass refused its shape");
   return true;
 }
@@ -1314,19 +1317,21 @@ void run_interp(sk_ctx* ctx, const float2* low, float2* out, i64 batch, const Di
 
 // interpolate_real (maps.cpp:92-99) + support mask (maps.cpp:47-52): FP64
 // FFT path for power-of-two extents, the FP32 sinc-matrix path otherwise.
+// batch > 1 (FFT path only): a stack of [batch] maps.
 void run_interp_lambda(sk_ctx* ctx, const float* low, const Dims& low_dims, const Dims& full, float* lam_out,
-                       uint8_t* mask, float thr) {
+                       uint8_t* mask, float thr, i64 batch = 1) {
   const int nd = int(low_dims.size());
   const i64 nlow = numel(low_dims), nfull = numel(full);
   if (interp_fft_ok(low_dims, full)) {
-    double2* src = ctx->arena.get<double2>("interp:lam64", nlow);
-    real_to_c128(ctx, low, src, nlow);
+    double2* src = ctx->arena.get<double2>("interp:lam64", batch * nlow);
+    real_to_c128(ctx, low, src, batch * nlow);
     Dims cur = low_dims;
     for (int a = nd - 1; a >= 0; --a) {
       Dims next = cur;
       next[size_t(a)] = full[size_t(a)];
-      double2* dst = ctx->arena.get<double2>(std::string("interp:lam64") + (a % 2 ? ":a" : ":b"), numel(next));
-      i64 b = 1, inner = 1;
+      double2* dst = ctx->arena.get<double2>(std::string("interp:lam64") + (a % 2 ? ":a" : ":b"),
+                                             batch * numel(next));
+      i64 b = batch, inner = 1;
       for (int k = 0; k < a; ++k) b *= cur[size_t(k)];
       for (int k = a + 1; k < nd; ++k) inner *= cur[size_t(k)];
       if (!interp_axis_fft(ctx, src, dst, b, int(low_dims[size_t(a)]), int(full[size_t(a)]), inner, true))
@@ -1334,9 +1339,10 @@ void run_interp_lambda(sk_ctx* ctx, const float* low, const Dims& low_dims, cons
       cur = next;
       src = dst;
     }
-    lam64_to_f32_mask(ctx, src, nfull, lam_out, mask, thr);
+    lam64_to_f32_mask(ctx, src, batch * nfull, lam_out, mask, thr);
     return;
   }
+  if (batch != 1) fail(SK_ERR_UNSUPPORTED, "interpolate_real: stacks need the FFT path");
   float2* lam_c = ctx->arena.get<float2>("post:lam_c", nlow);
   real_to_c64(ctx, low, lam_c, nlow);
   float2* lam_full_c = ctx->arena.get<float2>("post:lam_full_c", nfull);
@@ -1408,7 +1414,8 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
     if (full[size_t(a)] < cdims[size_t(a)]) fail(SK_ERR_DIM, "full_dims must be at least the calibration extent");
   const Support s = make_support(cfg->kernel, cfg->tau, nd);
   check_calib(cdims, q, s);
-  if (q > 64) fail(SK_ERR_UNSUPPORTED, "more than 64 channels is outside the B200 path");
+  if (q > power_wide_max_q())
+    fail(SK_ERR_UNSUPPORTED, "more than " + std::to_string(power_wide_max_q()) + " channels is outside the B200 path");
   // grid_dims_for (maps.cpp:188-193) or the explicit grid.
   Dims grid(static_cast<size_t>(nd));
   bool explicit_grid = true;
@@ -1642,6 +1649,130 @@ void pipeline(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float
   }
 }
 
+
+// ---------------------------------------------------------------- multislice group tail
+// K3-K5 of a whole group of slices in one pass (sk_estimate_maps_batched with
+// the batched K2): the per-slice kernels of a 128 x 128 map grid are too small
+// to fill the GPU (C3: 15-40 us each, launch- and tail-bound even with twelve
+// concurrent lanes), so the group runs them with the slice as a batch axis:
+// the spectral fold with the slice on grid.y, the lag expansion over
+// slices x pairs, the recon over slices x channels, K4 over a stack of slices
+// (PowerArgs::slices), the interpolation passes over slices x channels and
+// the FP64 lambda interpolation over slices.  Arithmetic per slice is exactly
+// the single-slice pipeline's (same kernels, same order).
+// Eligible: power-iteration eigensolver, a reduced map grid whose
+// interpolation takes the FFT path with the fused SoS pass, a lag box that
+// fits the spectral fold.  grid: the map grid (out).
+bool group_tail_eligible(const sk_config* cfg, const Dims& cd, const Dims& fd, i64 q, const Support& s, Dims& grid) {
+  const int nd = int(cd.size());
+  if (!cfg || cfg->eig != 1 || cfg->field != 1 || q > 32 || (q & (q - 1))) return false;
+  grid.assign(size_t(nd), 0);
+  bool ex = true;
+  for (int a = 0; a < nd; ++a) ex = ex && cfg->grid_dims[a] > 0;
+  for (int a = 0; a < nd; ++a) {
+    grid[size_t(a)] = ex ? cfg->grid_dims[a]
+                         : (cfg->grid == 1 ? std::min(cd[size_t(a)] + cfg->grid_pad, fd[size_t(a)]) : fd[size_t(a)]);
+    if (grid[size_t(a)] < cd[size_t(a)] || fd[size_t(a)] < grid[size_t(a)]) return false;
+  }
+  if (grid == fd || !interp_fft_ok(grid, fd)) return false;
+  const i64 nl = grid[size_t(nd - 1)];
+  if (fd[size_t(nd - 1)] != 2 * nl || q * nl > 4096) return false;
+  return spectral_fold_smem(s.nd, s.tau, 64, int(q)) <= 200 * 1024;
+}
+
+void pipeline_group_tail(sk_ctx* ctx, const Dims& cdims, const Dims& co, i64 q, const float2* calib_dev, i64 gs,
+                         const PipelineOut::Basis* bases, const Dims& full, const Dims& grid, const sk_config* cfg,
+                         float2* maps, float* lambda, uint8_t* mask, sk_provenance* prov) {
+  const int nd = int(cdims.size());
+  const Support s = make_support(cfg->kernel, cfg->tau, nd);
+  const i64 lam = s.count, n = q * lam, ngrid = numel(grid), nfull = numel(full);
+  const int h = int(q * (q + 1) / 2);
+  SupportTables& t = tables_for(ctx, s, int(q));
+  cudaEvent_t* ev = ctx->ev;
+  SKB_CUDA(cudaEventRecord(ev[0], ctx->stream));
+  // K3: lags [gs][h][nbox] -> planes [gs][h][grid]
+  double2* lags = ctx->arena.get<double2>("field:lags64", gs * h * t.nbox);
+  const int* offs = support_offsets_dev(ctx, s);
+  for (i64 c0 = 0; c0 < gs; c0 += kFoldBatchMax) {
+    const int cnt = int(std::min<i64>(kFoldBatchMax, gs - c0));
+    FoldBatch fb{};
+    for (int i = 0; i < cnt; ++i) {
+      fb.u[i] = bases[c0 + i].usig;
+      fb.k[i] = int(bases[c0 + i].k);
+    }
+    fold_lags_spectral_batched(ctx, fb, cnt, n, int(q), int(lam), s.nd, s.tau, offs, lags + c0 * h * t.nbox);
+  }
+  Planes pl;
+  pl.hi = ctx->arena.get<float2>("field:planes", gs * h * ngrid);
+  pl.lo = ctx->arena.get<lo2>("field:planes_lo", gs * h * ngrid);
+  expand_lags(ctx, lags, pl.hi, pl.lo, gs * h, s.tau, grid);
+  SKB_CUDA(cudaEventRecord(ev[1], ctx->stream));
+  // post (part 1): recon [gs][Q][grid]
+  float2* recon = run_recon(ctx, cdims, co, gs * q, calib_dev, grid, cfg->apod_width);
+  SKB_CUDA(cudaEventRecord(ev[2], ctx->stream));
+  // K4 over the stack
+  unsigned long long* zeroed = ctx->arena.get<unsigned long long>("post:zeroed", gs);
+  SKB_CUDA(cudaMemsetAsync(zeroed, 0, size_t(gs) * sizeof(unsigned long long), ctx->stream));
+  float2* maps_grid = ctx->arena.get<float2>("post:maps_grid", gs * q * ngrid);
+  float* lam_grid = ctx->arena.get<float>("post:lam_grid", gs * ngrid);
+  PowerArgs pa{};
+  pa.planes = pl.hi;
+  pa.planes_lo = pl.lo;
+  pa.n = ngrid;
+  pa.q = int(q);
+  pa.iters = cfg->power_iters;
+  pa.alpha = 1.f;
+  pa.beta = -1.f / float(lam);
+  pa.lam_scale = 1.f / float(lam);
+  pa.recon = recon;
+  pa.maps = maps_grid;
+  pa.lambda = lam_grid;
+  pa.mask_threshold = float(cfg->mask_threshold);
+  pa.zeroed = zeroed;
+  pa.rq32_min = 0.f;  // an interpolation follows (see pipeline)
+  pa.slices = int(gs);
+  power_iteration(ctx, pa);
+  SKB_CUDA(cudaEventRecord(ev[3], ctx->stream));
+  // post (part 2): interpolation + renormalisation + mask
+  if (!run_interp_renorm(ctx, maps_grid, maps, q, grid, full, gs))
+    fail(SK_ERR_UNSUPPORTED, "multislice group: fused interpolation refused an eligible shape");
+  run_interp_lambda(ctx, lam_grid, grid, full, lambda, mask, float(cfg->mask_threshold), gs);
+  SKB_CUDA(cudaEventRecord(ev[4], ctx->stream));
+  const size_t need = size_t(gs) + 1;  // pinned staging in doubles (8 bytes each, as the counters)
+  if (ctx->hpin_cap < need) {
+    if (ctx->hpin) SKB_CUDA(cudaFreeHost(ctx->hpin));
+    SKB_CUDA(cudaMallocHost(&ctx->hpin, std::max<size_t>(need, 64) * sizeof(double)));
+    ctx->hpin_cap = std::max<size_t>(need, 64);
+  }
+  SKB_CUDA(cudaMemcpyAsync(ctx->hpin, zeroed, size_t(gs) * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (prov) {
+    float ms[4], total = 0;
+    for (int i = 0; i < 4; ++i) SKB_CUDA(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+    SKB_CUDA(cudaEventElapsedTime(&total, ev[0], ev[4]));
+    for (i64 i = 0; i < gs; ++i) {
+      sk_provenance* p = prov + i;
+      std::memset(p, 0, sizeof *p);
+      for (int a = 0; a < nd; ++a) p->grid_dims[a] = grid[size_t(a)];
+      p->support_size = lam;
+      p->valid_shifts = 1;
+      for (i64 d : cdims) p->valid_shifts *= std::max<i64>(0, d - 2 * cfg->tau);
+      p->nullspace_rank = n - bases[i].k;
+      unsigned long long z = 0;
+      std::memcpy(&z, reinterpret_cast<const unsigned char*>(ctx->hpin) + size_t(i) * sizeof z, sizeof z);
+      p->zeroed_voxels = i64(z);
+      p->sigma1 = bases[i].sigma1;
+      p->eig_solver_used = 2;
+      // the group's device time shared evenly over its slices (K1 + K2 ran batched on the producer)
+      p->stage_ms[2] = ms[0] / double(gs);
+      p->stage_ms[3] = ms[2] / double(gs);
+      p->stage_ms[4] = (ms[1] + ms[3]) / double(gs);
+      p->total_ms = total / double(gs);
+    }
+  }
+}
+
 template <typename Fn>
 int guarded(Fn&& fn) {
   try {
@@ -1719,6 +1850,7 @@ int sk_destroy(sk_ctx* ctx) {
       if (e) cudaEventDestroy(e);
     if (ctx->d2h_ready) cudaEventDestroy(ctx->d2h_ready);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->hp_stream) cudaStreamDestroy(ctx->hp_stream);
     cusolverDnDestroyParams(ctx->cusolver_params);
     cusolverDnDestroy(ctx->cusolver);
     cublasDestroy(ctx->cublas);
@@ -1917,7 +2049,8 @@ int sk_eig_power_field(sk_ctx* ctx, int64_t voxels, int64_t q, const sk_c64* b_f
                        float* values) {
   return guarded([&] {
     require_ctx(ctx);
-    if (q > 64) fail(SK_ERR_UNSUPPORTED, "more than 64 channels is outside the B200 path");
+    if (q > power_wide_max_q())
+      fail(SK_ERR_UNSUPPORTED, "more than " + std::to_string(power_wide_max_q()) + " channels is outside the B200 path");
     const float2* d_b = device_in(ctx, reinterpret_cast<const float2*>(b_field), voxels * q * q, "in:field");
     float2* planes = ctx->arena.get<float2>("field:planes", voxels * q * (q + 1) / 2);
     field_full_to_planes(ctx, d_b, voxels, int(q), planes);
@@ -2522,6 +2655,17 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
     gstart.push_back(slices);
   }
   const i64 groups = bk2 ? i64(gstart.size()) - 1 : 0;
+  // K3-K5 of each group in one batched pass on one consumer context
+  // (pipeline_group_tail) instead of slice by slice on the lanes: device
+  // outputs and an eligible configuration; SKB_GROUP_TAIL=0 keeps the lanes.
+  Dims grid_t;
+  static const bool tail_env = [] {
+    const char* v = std::getenv("SKB_GROUP_TAIL");
+    return !v || std::atoi(v) != 0;
+  }();
+  const bool tail = bk2 && tail_env && maps && lambda && mask && is_device_ptr(maps) && is_device_ptr(lambda) &&
+                    is_device_ptr(mask) && group_tail_eligible(cfg, cd, fd, q, sup, grid_t);
+  std::vector<const float2*> gcal(size_t(groups), nullptr);  // device calibration block of each group
   std::vector<PipelineOut::Basis> bases(size_t(bk2 ? slices : 0));
   std::vector<char> has_basis(size_t(bk2 ? slices : 0), 0);
   std::vector<cudaEvent_t> gev(size_t(groups), nullptr);
@@ -2574,10 +2718,65 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
       errs[size_t(lane)] = "multislice: deferred device-to-host copy failed";
     }
   };
+  const auto t_start = std::chrono::steady_clock::now();
+  // Group consumer (tail): one thread, one context, a whole group per pass.
+  auto consume = [&]() {
+    sk_ctx* sub = ctx->lanes[0];
+    cudaSetDevice(ctx->device);
+    sub->defer_d2h = 0;
+    const Dims cod = dims_of(ndim, center_offset);
+    for (i64 g = 0; g < groups; ++g) {
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return groups_ready > g || abort_k2; });
+        if (abort_k2) break;
+      }
+      if (cudaStreamWaitEvent(sub->stream, gev[size_t(g)], 0) != cudaSuccess) {
+        rcs[0] = SK_ERR_CUDA;
+        errs[0] = "multislice: waiting on the batched nullspace failed";
+        break;
+      }
+      const i64 s0 = gstart[size_t(g)], gs = group_size(g);
+      bool all = true;
+      for (i64 i = 0; i < gs; ++i) all = all && has_basis[size_t(s0 + i)];
+      int rc = SK_OK;
+      if (all) {
+        rc = guarded([&] {
+          pipeline_group_tail(sub, cd, cod, q, gcal[size_t(g)], gs, &bases[size_t(s0)], fd, grid_t, cfg,
+                              reinterpret_cast<float2*>(maps) + s0 * q * nfull, lambda + s0 * nfull, mask + s0 * nfull,
+                              prov ? prov + s0 : nullptr);
+        });
+      } else {  // a slice missed the batched convergence test: this group slice by slice
+        for (i64 i = 0; i < gs && rc == SK_OK; ++i) {
+          const i64 sl = s0 + i;
+          rc = estimate_impl(sub, ndim, calib_dims, center_offset, q, calib + sl * ncal, full_dims, cfg,
+                             maps + sl * q * nfull, lambda + sl * nfull, mask + sl * nfull, nullptr,
+                             prov ? prov + sl : nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                             has_basis[size_t(sl)] ? &bases[size_t(sl)] : nullptr);
+        }
+      }
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        done[size_t(g)] = gs;
+        cv.notify_all();
+      }
+      if (std::getenv("SKB_PROFILE_NS")) {
+        float tail_ms = 0.f;
+        cudaEventElapsedTime(&tail_ms, sub->ev[0], sub->ev[4]);
+        std::fprintf(stderr, "[bk2] group %lld tail done at %.3f ms (device %.3f ms, %s)\n", (long long)g,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(),
+                     tail_ms, all ? "batched" : "per slice");
+      }
+      if (rc != SK_OK) {
+        rcs[0] = rc;
+        errs[0] = sk_last_error();
+        break;
+      }
+    }
+  };
   // The batched K2 producer (calling thread): group g's Grams + bases into
   // buffer set g % 2, after the lanes finished group g - 2 with that set.
   std::string k2_err;
-  const auto t_start = std::chrono::steady_clock::now();
   auto produce = [&]() -> int {
     return guarded([&] {
       const Dims cdl = cd;
@@ -2598,6 +2797,7 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
           SKB_CUDA(cudaMemcpyAsync(cal_dev, calib + s0 * ncal, size_t(gs * ncal) * sizeof(float2),
                                    cudaMemcpyHostToDevice, ctx->stream));
         }
+        gcal[size_t(g)] = cal_on_dev ? reinterpret_cast<const float2*>(calib) + s0 * ncal : cal_dev;
         for (i64 i = 0; i < gs; ++i) {
           const float2* c = cal_on_dev ? reinterpret_cast<const float2*>(calib) + (s0 + i) * ncal : cal_dev + i * ncal;
           check_calib(cdl, q, sup);
@@ -2639,7 +2839,31 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
     work(0);
   } else {
     std::vector<std::thread> pool;
-    for (int l = 0; l < lanes; ++l) pool.emplace_back(work, l);
+    cudaStream_t saved = nullptr;
+    static const bool prio_env = [] {
+      const char* v = std::getenv("SKB_K2_PRIO");
+      return !v || std::atoi(v) != 0;
+    }();
+    if (tail && prio_env) {
+      // the producer on a highest-priority stream for the duration of the call
+      // (the caller's stream was synchronised above and is waited for below)
+      const int rcp = guarded([&] {
+        if (!ctx->hp_stream) {
+          int least = 0, greatest = 0;
+          SKB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+          SKB_CUDA(cudaStreamCreateWithPriority(&ctx->hp_stream, cudaStreamNonBlocking, greatest));
+        }
+        saved = ctx->stream;
+        ctx->stream = ctx->hp_stream;
+        check_cublas(cublasSetStream(ctx->cublas, ctx->stream), "cublasSetStream");
+        check_cusolver(cusolverDnSetStream(ctx->cusolver, ctx->stream), "cusolverDnSetStream");
+      });
+      if (rcp != SK_OK) return rcp;
+    }
+    if (tail)
+      pool.emplace_back(consume);
+    else
+      for (int l = 0; l < lanes; ++l) pool.emplace_back(work, l);
     if (bk2) {
       rc_k2 = produce();
       if (rc_k2 != SK_OK) {
@@ -2650,6 +2874,12 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
       }
     }
     for (auto& t : pool) t.join();
+    if (saved) {
+      cudaStreamSynchronize(ctx->stream);
+      ctx->stream = saved;
+      cublasSetStream(ctx->cublas, ctx->stream);
+      cusolverDnSetStream(ctx->cusolver, ctx->stream);
+    }
   }
   for (auto& e : gev)
     if (e) cudaEventDestroy(e);

@@ -130,6 +130,13 @@ class DeviceOps:
     def __init__(self, ctx, device):
         self.ctx, self.device = ctx, device
 
+    def _ready(self):
+        """The library runs on the context's own non-blocking stream: tensors
+        that torch kernels just produced (transposes, fills, slices made
+        contiguous) must be complete before a C-ABI call reads them."""
+        import torch
+        torch.cuda.current_stream(self.device).synchronize()
+
     def _cal(self, calib):
         import torch
         cal = calib.data if isinstance(calib.data, torch.Tensor) else torch.from_numpy(
@@ -146,6 +153,7 @@ class DeviceOps:
         cal = self._cal(calib)
         maps = torch.empty((q,) + shape, dtype=torch.complex64, device=self.device)
         lam = torch.empty(shape, dtype=torch.float32, device=self.device)
+        self._ready()
         api.estimate_raw_slab_device(self.ctx, cal.data_ptr(), calib.dims, calib.center_offset, q, full_dims, cfg,
                                      slab, maps.data_ptr(), lam.data_ptr())
         return maps, lam
@@ -160,6 +168,7 @@ class DeviceOps:
         kmax = min(n, 256)
         while True:
             u = torch.empty((kmax, n), dtype=torch.complex128, device=self.device)  # column-major n x kmax
+            self._ready()
             try:
                 info = api.signal_basis_device(self.ctx, cal.data_ptr(), calib.dims, calib.center_offset, q, cfg,
                                                u.data_ptr(), kmax)
@@ -182,6 +191,7 @@ class DeviceOps:
         u = basis["u"].transpose(0, 1).contiguous().to(self.device)  # (k, n) row-major = n x k column-major
         maps = torch.empty((q,) + shape, dtype=torch.complex64, device=self.device)
         lam = torch.empty(shape, dtype=torch.float32, device=self.device)
+        self._ready()
         api.estimate_raw_slab_basis_device(self.ctx, cal.data_ptr(), calib.dims, calib.center_offset, q, full_dims,
                                            cfg, u.data_ptr(), basis["k"], basis["sigma1"], slab, maps.data_ptr(),
                                            lam.data_ptr())
@@ -193,6 +203,7 @@ class DeviceOps:
         from . import api
         low = low.contiguous()
         out = torch.empty((low.shape[0],) + tuple(full_dims), dtype=torch.complex64, device=low.device)
+        self._ready()
         api._check(api.lib().sk_interpolate_maps(self.ctx.handle, low.dim() - 1, api._p(api._i64(low.shape[1:])),
                                                  low.shape[0], C.c_void_p(low.data_ptr()),
                                                  api._p(api._i64(full_dims)), C.c_void_p(out.data_ptr())))
@@ -204,6 +215,7 @@ class DeviceOps:
         from . import api
         low = low.contiguous()
         out = torch.empty(tuple(full_dims), dtype=torch.float32, device=low.device)
+        self._ready()
         api._check(api.lib().sk_interpolate_real(self.ctx.handle, low.dim(), api._p(api._i64(low.shape)),
                                                  C.c_void_p(low.data_ptr()), api._p(api._i64(full_dims)),
                                                  C.c_void_p(out.data_ptr())))
@@ -211,10 +223,12 @@ class DeviceOps:
 
     def sos_accumulate(self, maps, sos):
         from . import api
+        self._ready()
         return api.sos_accumulate(maps, sos, self.ctx)
 
     def renormalize(self, maps, sos):
         from . import api
+        self._ready()
         return api.renormalize_sos(maps, sos, self.ctx)
 
     def support_mask(self, lam, thr):
@@ -222,6 +236,7 @@ class DeviceOps:
         import torch
         from . import api
         out = torch.empty(lam.shape, dtype=torch.uint8, device=lam.device)
+        self._ready()
         api._check(api.lib().sk_support_mask(self.ctx.handle, lam.numel(), C.c_void_p(lam.data_ptr()), float(thr),
                                              C.c_void_p(out.data_ptr())))
         return out

@@ -248,6 +248,44 @@ def test_power_parity(K, O, q):
     assert err_v < 1e-3 and err_l < 1e-5
 
 
+@pytest.mark.parametrize("q", [65, 72, 96, 130])
+def test_power_parity_wide(K, O, q):
+    """More than 64 channels (eigensolve.cpp:40-74 is generic in Q): the
+    shared-memory K4 kernel (sk_power_wide.cu) against the oracle, including a
+    voxel whose all-ones start is annihilated (e_0 restart) and a zero voxel."""
+    n = 37
+    m = rnd((n, q, q), 12, np.complex128)
+    herm = (m + m.conj().transpose(0, 2, 1)) / 2
+    herm = herm + 2.5 * q ** 0.5 * np.eye(q)
+    ones = np.ones((q, 1)) / np.sqrt(q)
+    proj = np.eye(q) - ones @ ones.T
+    herm[3] = proj @ herm[3] @ proj  # B 1 = 0: restart from e_0 (eigensolve.cpp:56-63)
+    herm[5] = 0.0                    # B = 0: v stays e_0
+    herm = herm.astype(np.complex64)
+    vg, valg = K.eig_power_field(herm, 30)
+    vo, valo = O.eig_power_field(f32(herm), 30)
+    ph = np.sum(vo.conj() * vg, 0)
+    ph = ph / np.maximum(np.abs(ph), 1e-30)
+    keep = np.ones(n, bool)
+    keep[3] = False  # the annihilation is exact only in exact arithmetic: compared by value below
+    err_v = np.abs(vg - vo * ph[None])[:, keep].max()
+    err_l = PM.rel_fro(valg[keep], valo[keep])
+    report("power_wide", q=q, vec_max=float(err_v), value_rel=err_l)
+    assert err_v < 1e-3 and err_l < 1e-5
+    assert np.array_equal(vg[:, 5], np.eye(q, dtype=np.complex64)[:, 0]) and valg[5] == 0
+    assert abs(valg[3] - np.linalg.eigvalsh(herm[3].astype(np.complex128))[-1]) < 2e-2 * abs(valg[3])
+
+
+def test_estimate_maps_wide_channels(K, O):
+    """The whole pipeline at Q = 72 (> 64 channels takes the wide K4 kernel)."""
+    sc = O.simulate(72, (40, 36), 1, 7, noise_sigma=0.01, noise_seed=3)
+    cal = O.extract_calibration(sc["kspace"], (24, 22))
+    ck = K.PipelineConfig(kernel=K.ELLIPSOID, tau=1, grid_pad=8, power_iters=20)
+    co = O.PipelineConfig.pisco()
+    co.kernel, co.tau, co.grid_pad, co.power_iters = O.ELLIPSOID, 1, 8, 20
+    _pipeline_case(K, O, cal.data.astype(np.complex64), cal.center_offset, (40, 36), ck, co, name="wide-q72")
+
+
 def test_power_known_answers(K):  # test_eigensolve.cpp:67-83, eigensolve.cpp:56-66
     v, val = K.eig_power_field(np.diag([1.0, 0.1]).astype(np.complex64)[None], 10)
     assert abs(abs(v[0, 0]) - 1) < 1e-6 and abs(val[0] - 1) < 1e-6
@@ -660,6 +698,46 @@ def test_batched_multislice_batched_nullspace(K):
         assert d_maps < 1e-6, s
         assert np.allclose(lam[s], ref.lambda_min_map, rtol=1e-6, atol=1e-7), s
         assert (mask[s] == ref.support_mask).mean() > 0.9999, s
+
+
+def test_batched_multislice_group_tail(K):
+    """Device outputs: each group's K3-K5 run as one batched pass on one context
+    (pipeline_group_tail: the slice on the batch axis of the fold, expansion,
+    recon, K4 stack and interpolation kernels).  Against the lanes path (host
+    outputs) and per-slice calls; 37 slices = groups of 8 + 29 (one ragged)."""
+    import torch
+    from paper_2302_13431_b200 import phantom
+    case = phantom.generate("C3", slices=37)
+    spec = case.spec
+    cfg = K.PipelineConfig(kernel=spec.kernel, tau=spec.tau, nullspace_threshold=spec.nullspace_threshold,
+                           power_iters=spec.power_iters, grid=K.GRID_REDUCED,
+                           grid_pad=spec.grid_dims[0] - spec.calib[0])
+    ctx = K.Context(0)
+    s, q, full = case.calib.shape[0], spec.channels, spec.full_dims
+    cal = torch.from_numpy(case.calib).cuda()
+    d_maps = torch.full((s, q) + full, 3 + 3j, dtype=torch.complex64, device="cuda")
+    d_lam = torch.full((s,) + full, -1.0, dtype=torch.float32, device="cuda")
+    d_mask = torch.full((s,) + full, 7, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    for _ in range(2):  # the second call replays the settled step plan
+        pv = K.api.estimate_maps_batched_device(ctx, cal.data_ptr(), s, spec.calib, case.center_offset, q, full, cfg,
+                                                d_maps.data_ptr(), d_lam.data_ptr(), d_mask.data_ptr())
+    maps, lam, mask = d_maps.cpu().numpy(), d_lam.cpu().numpy(), d_mask.cpu().numpy()
+    assert not np.any(maps == 3 + 3j) and not np.any(lam == -1.0) and not np.any(mask == 7)
+    h_maps, h_lam, h_mask, h_info = K.api.estimate_maps_batched(case.calib, case.center_offset, full, cfg, ctx)
+    for sl in range(s):
+        assert int(pv[sl].nullspace_rank) == h_info[sl]["rank"], sl
+        assert int(pv[sl].zeroed_voxels) == 0
+    d_all = PM.rel_fro(maps, h_maps)
+    report("group_tail_vs_lanes", maps_rel=d_all, lam_abs=float(np.abs(lam - h_lam).max()))
+    assert d_all < 1e-6
+    assert np.allclose(lam, h_lam, rtol=1e-6, atol=1e-7)
+    assert (mask == h_mask).mean() > 0.9999
+    for sl in (0, 7, 8, 36):
+        ref = K.estimate_maps(K.Calib(case.calib[sl], case.center_offset), full, cfg, want_spectrum=False)
+        assert int(pv[sl].nullspace_rank) == ref.nullspace_rank
+        assert PM.rel_fro(maps[sl], ref.maps) < 1e-6, sl
+        assert np.allclose(lam[sl], ref.lambda_min_map, rtol=1e-6, atol=1e-7), sl
 
 
 # ------------------------------------------------- baseline preset (SURVEY §8f4)

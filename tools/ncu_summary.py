@@ -25,7 +25,10 @@ def read(rep, name=None):
     rows = list(csv.reader(out.splitlines()))
     hdr, units = rows[0], rows[1]
     k = hdr.index("Kernel Name")
-    vals = next(r for r in rows[2:] if name is None or name in r[k])
+    # the longest launch among the matching ones
+    t = hdr.index("gpu__time_duration.sum")
+    cand = [r for r in rows[2:] if len(r) == len(hdr) and (name is None or name in r[k])]
+    vals = max(cand, key=lambda r: float(r[t].replace(",", "")) * UNIT.get(units[t], 1))
     d = {"kernel": vals[hdr.index("Kernel Name")][:120]}
     for i, n in enumerate(hdr):
         if n in KEYS:
