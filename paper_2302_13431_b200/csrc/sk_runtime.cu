@@ -183,6 +183,17 @@ struct Out {
 
 Dims dims_of(int nd, const int64_t* d) { return Dims(d, d + nd); }
 
+// Host table -> device, ordered on the context's stream.  A synchronous
+// cudaMemcpy from pageable memory may return before the DMA has landed and
+// orders only the legacy default stream behind it; the kernels that read the
+// table run on the context's non-blocking stream, so the copy goes onto that
+// stream (found as a rare wrong-phase slice on a lane's first call:
+// normalize_maps read a recon built from a partly uploaded DFT matrix).
+void upload_table(sk_ctx* ctx, void* d, const void* h, size_t bytes) {
+  SKB_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 // Upload an N x L matrix (row-major) followed by its transpose (L x N).
 float2* upload_matrix(sk_ctx* ctx, const std::string& key, int N, int L, const std::vector<std::complex<double>>& m) {
   auto it = ctx->matrices.mats.find(key);
@@ -196,7 +207,7 @@ float2* upload_matrix(sk_ctx* ctx, const std::string& key, int N, int L, const s
     }
   float2* d = nullptr;
   SKB_CUDA(cudaMalloc(&d, h.size() * sizeof(float2)));
-  SKB_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  upload_table(ctx, d, h.data(), h.size() * sizeof(float2));
   ctx->matrices.mats[key] = d;
   return d;
 }
@@ -283,7 +294,7 @@ double2* symdft_table64(sk_ctx* ctx, int N, int H, i64 j0, int sign) {
     }
   double2* d = nullptr;
   SKB_CUDA(cudaMalloc(&d, h.size() * sizeof(double2)));
-  SKB_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  upload_table(ctx, d, h.data(), h.size() * sizeof(double2));
   ctx->matrices.mats[key] = reinterpret_cast<float2*>(d);
   return d;
 }
@@ -361,10 +372,10 @@ SupportTables& tables_for(sk_ctx* ctx, const Support& s, int q) {
   std::vector<int2> pairs;
   for (int p = 0; p < q; ++p)
     for (int c = p; c < q; ++c) pairs.push_back(make_int2(p, c));
-  auto up = [](const void* h, size_t bytes) {
+  auto up = [ctx](const void* h, size_t bytes) {
     void* d = nullptr;
     check_cuda(cudaMalloc(&d, std::max<size_t>(bytes, 16)), "cudaMalloc(table)");
-    check_cuda(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice), "upload table");
+    upload_table(ctx, d, h, bytes);
     return d;
   };
   t.pairs = static_cast<int2*>(up(pairs.data(), pairs.size() * sizeof(int2)));
@@ -432,7 +443,7 @@ const int* support_offsets_dev(sk_ctx* ctx, const Support& s) {
   if (it != ctx->tables.end()) return static_cast<const int*>(it->second);
   void* d = nullptr;
   SKB_CUDA(cudaMalloc(&d, std::max<size_t>(1, s.offsets.size()) * sizeof(int)));
-  SKB_CUDA(cudaMemcpy(d, s.offsets.data(), s.offsets.size() * sizeof(int), cudaMemcpyHostToDevice));
+  upload_table(ctx, d, s.offsets.data(), s.offsets.size() * sizeof(int));
   ctx->tables[key] = d;
   return static_cast<const int*>(d);
 }
