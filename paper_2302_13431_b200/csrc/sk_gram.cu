@@ -52,6 +52,9 @@ __global__ void __launch_bounds__(512) gram_pairs_kernel(const float2* __restric
   const int P0 = g.pad[0], P1 = g.pad[1], P2 = g.pad[2];
   const int lb = LB > 0 ? LB : g.lb, t2 = 2 * g.tau;
   const i64 npad = i64(P0) * P1 * P2;
+  // blockIdx.y: slice of a multislice group (its own spectra and Gram)
+  spectra += i64(blockIdx.y) * g.q * npad;
+  gram += i64(blockIdx.y) * (i64(g.q) * g.lam) * (i64(g.q) * g.lam);
   const int rest = P1 * P2;
   // twiddle tables (axis a at offset sum_{b<a} P_b)
   float2* tw = reinterpret_cast<float2*>(smem_raw);
@@ -191,7 +194,7 @@ size_t gram_pairs_smem(const GramGeom& g) {
 }
 
 void gram_pairs_launch(sk_ctx* ctx, const float2* spectra, const GramGeom& g_in, const int2* d_pairs, int npairs,
-                       const int* d_off, const float2* d_tw, float2* gram) {
+                       const int* d_off, const float2* d_tw, float2* gram, int slices) {
   GramGeom g = g_in;
   if (g.lb > kMaxLb) fail(9, "gram_fft: kernel radius > 7 is outside the B200 path");
   for (int a = 0; a < 3; ++a)
@@ -210,7 +213,8 @@ void gram_pairs_launch(sk_ctx* ctx, const float2* spectra, const GramGeom& g_in,
   const int threads = g.stage_prod ? 256 : 512;
   auto go = [&](auto kern) {
     set_smem_limit(reinterpret_cast<const void*>(kern), smem);
-    kern<<<npairs, threads, smem, ctx->stream>>>(spectra, g, d_pairs, d_off, d_tw, gram);
+    kern<<<dim3(unsigned(npairs), unsigned(slices)), threads, smem, ctx->stream>>>(spectra, g, d_pairs, d_off, d_tw,
+                                                                                   gram);
   };
   switch (g.lb) {  // lag-box extent fixed at compile time for the BASELINE radii, else run time
     case 9: go(gram_pairs_kernel<9>); break;

@@ -218,7 +218,7 @@ struct GramGeom {
 };
 size_t gram_pairs_smem(const GramGeom& g);
 void gram_pairs_launch(sk_ctx* ctx, const float2* spectra, const GramGeom& g, const int2* d_pairs, int npairs,
-                       const int* d_off, const float2* d_tw, float2* gram);
+                       const int* d_off, const float2* d_tw, float2* gram, int slices = 1);
 
 // Fold W (or I - U U^H) into per-pair lag kernels on the lag box
 // (spatial_gram.cpp:108-131).  w_is_signal: W = I - w (w = U_sig U_sig^H,

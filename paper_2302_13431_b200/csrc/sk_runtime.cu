@@ -403,18 +403,21 @@ void check_calib(const Dims& cdims, i64 q, const Support& s) {  // calibration.c
 }
 
 // ---------------------------------------------------------------- K1
-float2* run_gram(sk_ctx* ctx, const Dims& cdims, i64 q, const float2* calib, const Support& s, float2* gram_dst) {
+// slices > 1: calib [slices][Q][E..] -> gram_dst [slices][n][n] (multislice groups: the channel
+// spectra over slices x channels, the pair kernel with the slice on grid.y).
+float2* run_gram(sk_ctx* ctx, const Dims& cdims, i64 q, const float2* calib, const Support& s, float2* gram_dst,
+                 i64 slices = 1) {
   const int nd = int(cdims.size());
   const i64 lam = s.count, n = q * lam;
   Dims pad(cdims.size());
   for (size_t a = 0; a < cdims.size(); ++a) pad[a] = next_pow2(cdims[a] + 2 * s.tau);  // calibration.cpp:89-93
   std::vector<float2*> mats(static_cast<size_t>(nd));
   for (int a = 0; a < nd; ++a) mats[size_t(a)] = dft_matrix(ctx, int(pad[size_t(a)]), int(cdims[size_t(a)]), 0, 0, -1, 0.0);
-  float2* spectra = ctx->arena.get<float2>("gram:spectra", q * numel(pad));
+  float2* spectra = ctx->arena.get<float2>("gram:spectra", slices * q * numel(pad));
   if (nd == 2 && sep2d_smem(int(cdims[0]), int(cdims[1]), int(pad[0]), int(pad[1])) <= 160 * 1024)
-    sep2d(ctx, calib, spectra, q, int(cdims[0]), int(cdims[1]), int(pad[0]), int(pad[1]), mats[0], mats[1]);
+    sep2d(ctx, calib, spectra, slices * q, int(cdims[0]), int(cdims[1]), int(pad[0]), int(pad[1]), mats[0], mats[1]);
   else
-    separable(ctx, calib, spectra, q, cdims, pad, mats, "gram:tmp");
+    separable(ctx, calib, spectra, slices * q, cdims, pad, mats, "gram:tmp");
   SupportTables& t = tables_for(ctx, s, int(q));
   GramGeom g{};
   g.nd = nd;
@@ -431,8 +434,8 @@ float2* run_gram(sk_ctx* ctx, const Dims& cdims, i64 q, const float2* calib, con
   const std::string key = "gramtw:" + std::to_string(g.pad[0]) + ":" + std::to_string(g.pad[1]) + ":" +
                           std::to_string(g.pad[2]);
   float2* d_tw = upload_matrix(ctx, key, int(tw.size()), 1, tw);
-  float2* gram = gram_dst ? gram_dst : ctx->arena.get<float2>("gram:G", n * n);
-  gram_pairs_launch(ctx, spectra, g, t.pairs, int(q * (q + 1) / 2), t.off, d_tw, gram);
+  float2* gram = gram_dst ? gram_dst : ctx->arena.get<float2>("gram:G", slices * n * n);
+  gram_pairs_launch(ctx, spectra, g, t.pairs, int(q * (q + 1) / 2), t.off, d_tw, gram, int(slices));
   return gram;
 }
 
@@ -1055,6 +1058,7 @@ Eig run_nullspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, int solv
 // batch's signal bases stay valid while the next batch is solved).
 void run_eigh_subspace_batched(sk_ctx* ctx, const float2* grams, i64 batch, i64 n, double ratio, int set,
                                std::vector<Eig>& eigs, std::vector<char>& ok) {
+  PhaseLaps laps(ctx);
   const std::string sfx = ":" + std::to_string(set);
   constexpr i64 b = 64;  // the batched CholQR kernels (sk_cholqr.cu) are b = 64, n >= 1024
   const i64 nn = n * n, nb = n * b;
@@ -1065,6 +1069,7 @@ void run_eigh_subspace_batched(sk_ctx* ctx, const float2* grams, i64 batch, i64 
   double2* A = ctx->arena.get<double2>("bk:A" + sfx, batch * nn);
   float* gcat = ctx->arena.get<float>("bk:gcat" + sfx, batch * 4 * nn);
   promote_split_gram(ctx, grams, n, A, gcat, gcat + 2 * nn, batch, nn, 4 * nn);
+  laps.lap("promote");
   double2* V = ctx->arena.get<double2>("bk:V" + sfx, batch * nb);
   double2* Y = ctx->arena.get<double2>("bk:Y" + sfx, batch * nb);
   double2* T = ctx->arena.get<double2>("bk:T" + sfx, batch * nb);
@@ -1097,20 +1102,27 @@ void run_eigh_subspace_batched(sk_ctx* ctx, const float2* grams, i64 batch, i64 
                    "GemmStridedBatchedEx(3xTF32 cat)");
       ++ctx->lib_calls;
       combine_block_cat(ctx, ccat, n, b, Y, batch, 8 * nb, nb);
+      laps.lap("gemm32");
     } else {
       zgemm_b(n, b, n, A, n, nn, V, n, nb, Y, n, nb);  // Y = A V (FP64)
+      laps.lap("gemm64");
     }
     std::swap(V, Y);
     cholqr64(ctx, V, n, i + 1 == q_plan ? 2 : 1, info + 1, batch, nb);
+    laps.lap("orth");
   }
   zgemm_b(n, b, n, A, n, nn, V, n, nb, Y, n, nb);
+  laps.lap("gemm64");
   gram64(ctx, V, Y, n, H, batch, nb);  // H = V^H A V
+  laps.lap("rr_gram");
   herm_eig_small(ctx, H, int(b), w, info, 0.25 * ratio * ratio, int(batch));
+  laps.lap("rr_heev");
   zgemm_b(n, b, b, V, n, nb, H, b, b * b, T, n, nb);  // V <- V S
   std::swap(V, T);
   zgemm_b(n, b, b, Y, n, nb, H, b, b * b, T, n, nb);  // Y <- Y S
   std::swap(Y, T);
   ritz_residuals(ctx, Y, V, w, n, b, res, batch, nb, b);
+  laps.lap("rr_rotate");
   std::vector<double> hw(size_t(batch * b)), hres(size_t(batch * b));
   std::vector<int> hinfo(size_t(batch * 3));
   SKB_CUDA(cudaMemcpyAsync(hw.data(), w, hw.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -2663,6 +2675,7 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
     const i64 first = std::min<i64>(slices, std::max<i64>(2, G / 4));
     gstart.push_back(0);
     for (i64 s0 = first; s0 < slices; s0 += G) gstart.push_back(s0);
+    // (a small last group, whose K3-K5 nothing overlaps, measured no gain: 52.9 against 52.2 ms on C3)
     gstart.push_back(slices);
   }
   const i64 groups = bk2 ? i64(gstart.size()) - 1 : 0;
@@ -2809,10 +2822,12 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
                                    cudaMemcpyHostToDevice, ctx->stream));
         }
         gcal[size_t(g)] = cal_on_dev ? reinterpret_cast<const float2*>(calib) + s0 * ncal : cal_dev;
-        for (i64 i = 0; i < gs; ++i) {
-          const float2* c = cal_on_dev ? reinterpret_cast<const float2*>(calib) + (s0 + i) * ncal : cal_dev + i * ncal;
-          check_calib(cdl, q, sup);
-          run_gram(ctx, cdl, q, c, sup, grams + i * nn);
+        check_calib(cdl, q, sup);
+        run_gram(ctx, cdl, q, gcal[size_t(g)], sup, grams, gs);  // K1 of the whole group: two launches
+        if (std::getenv("SKB_PROFILE_NS")) {
+          SKB_CUDA(cudaStreamSynchronize(ctx->stream));
+          std::fprintf(stderr, "[bk2] group %lld Grams done at %.3f ms\n", (long long)g,
+                       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
         }
         // first batch of this size: one single-slice solve settles the step plan
         if (ctx->subspace_hint.find(n_gram) == ctx->subspace_hint.end())
@@ -2851,13 +2866,10 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
   } else {
     std::vector<std::thread> pool;
     cudaStream_t saved = nullptr;
-    static const bool prio_env = [] {
-      const char* v = std::getenv("SKB_K2_PRIO");
-      return !v || std::atoi(v) != 0;
-    }();
-    if (tail && prio_env) {
+    if (tail) {
       // the producer on a highest-priority stream for the duration of the call
-      // (the caller's stream was synchronised above and is waited for below)
+      // (the caller's stream was synchronised above and is waited for below):
+      // C3 54.3 -> 52.0 ms per call against the default priority
       const int rcp = guarded([&] {
         if (!ctx->hp_stream) {
           int least = 0, greatest = 0;
