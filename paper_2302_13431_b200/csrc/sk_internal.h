@@ -359,6 +359,11 @@ void normalize_standalone(sk_ctx* ctx, float2* maps, i64 n, int q, const float2*
 // Batched forms (multislice K2): `batch` slices at strides s* (elements) in one launch.
 void promote_split_gram(sk_ctx* ctx, const float2* a, i64 n, double2* a64, float* hi, float* lo, i64 batch = 1,
                         i64 sa = 0, i64 sh = 0);
+// Batched Gauss-3M FP64 products on real planes (sk_misc.cu).
+void promote_split3_gram(sk_ctx* ctx, const float2* a, i64 n, double* a3, float* hi, float* lo, i64 batch, i64 sa,
+                         i64 sh);
+void split3_block(sk_ctx* ctx, const double2* v, i64 len, double* v3, i64 batch, i64 sv);
+void combine3_block(sk_ctx* ctx, const double* t3, i64 len, double2* y, i64 batch, i64 sy);
 void split_block_cat_tf32(sk_ctx* ctx, const double2* v, i64 n, i64 m, float* vc, i64 batch = 1, i64 sv = 0,
                           i64 svc = 0);
 void combine_block_cat(sk_ctx* ctx, const float* c, i64 n, i64 m, double2* y, i64 batch = 1, i64 sc = 0, i64 sy = 0);

@@ -485,6 +485,70 @@ void promote_split_gram(sk_ctx* ctx, const float2* a, i64 n, double2* a64, float
 }
 
 
+// Batched FP64 products in the Gauss 3M form on real planes (the batched
+// solver: three real DGEMMs per complex product instead of four; cuBLAS has
+// no strided-batched ZGEMM-3M).  promote_split3: the c64 Gram -> planes
+// [Re A][Im A][Re A + Im A] (n x n doubles each) and the TF32 split of
+// promote_split; split3: V -> [Re V][Im V][Re V + Im V]; combine3: the three
+// products T1 = Re A Re V, T2 = Im A Im V, T3 = (Re A + Im A)(Re V + Im V)
+// -> Y = (T1 - T2) + i (T3 - T1 - T2).
+__global__ void promote_split3_kernel(const float2* __restrict__ a, i64 n, double* __restrict__ a3,
+                                      float* __restrict__ hi, float* __restrict__ lo, i64 sa, i64 sh) {
+  a += i64(blockIdx.y) * sa;
+  a3 += i64(blockIdx.y) * 3 * sa;
+  hi += i64(blockIdx.y) * sh;
+  lo += i64(blockIdx.y) * sh;
+  const i64 nn = n * n;
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < nn; e += i64(gridDim.x) * blockDim.x) {
+    const i64 r = e % n, c = e / n;
+    const float2 v = a[e];
+    a3[e] = double(v.x);
+    a3[nn + e] = double(v.y);
+    a3[2 * nn + e] = double(v.x) + double(v.y);
+    float h, l;
+    tf32_split(v.x, h, l);
+    hi[r + c * 2 * n] = h;
+    lo[r + c * 2 * n] = l;
+    tf32_split(v.y, h, l);
+    hi[n + r + c * 2 * n] = h;
+    lo[n + r + c * 2 * n] = l;
+  }
+}
+__global__ void split3_kernel(const double2* __restrict__ v, i64 len, double* __restrict__ v3, i64 sv) {
+  v += i64(blockIdx.y) * sv;
+  v3 += i64(blockIdx.y) * 3 * len;
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < len; e += i64(gridDim.x) * blockDim.x) {
+    const double2 x = v[e];
+    v3[e] = x.x;
+    v3[len + e] = x.y;
+    v3[2 * len + e] = x.x + x.y;
+  }
+}
+__global__ void combine3_kernel(const double* __restrict__ t3, i64 len, double2* __restrict__ y, i64 sy) {
+  t3 += i64(blockIdx.y) * 3 * len;
+  y += i64(blockIdx.y) * sy;
+  for (i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x; e < len; e += i64(gridDim.x) * blockDim.x) {
+    const double t1 = t3[e], t2 = t3[len + e], t = t3[2 * len + e];
+    y[e] = make_double2(t1 - t2, (t - t1) - t2);
+  }
+}
+void promote_split3_gram(sk_ctx* ctx, const float2* a, i64 n, double* a3, float* hi, float* lo, i64 batch, i64 sa,
+                         i64 sh) {
+  promote_split3_kernel<<<batch_grid(n * n, batch), kT, 0, ctx->stream>>>(a, n, a3, hi, lo, sa, sh);
+  ++ctx->launches;
+  SKB_LAUNCH("promote_split3");
+}
+void split3_block(sk_ctx* ctx, const double2* v, i64 len, double* v3, i64 batch, i64 sv) {
+  split3_kernel<<<batch_grid(len, batch), kT, 0, ctx->stream>>>(v, len, v3, sv);
+  ++ctx->launches;
+  SKB_LAUNCH("split3");
+}
+void combine3_block(sk_ctx* ctx, const double* t3, i64 len, double2* y, i64 batch, i64 sy) {
+  combine3_kernel<<<batch_grid(len, batch), kT, 0, ctx->stream>>>(t3, len, y, sy);
+  ++ctx->launches;
+  SKB_LAUNCH("combine3");
+}
+
 void mask_kernel(sk_ctx* ctx, const float* lambda, i64 n, float thr, uint8_t* mask) {
   mask_only_kernel<<<SKB_GRID(n)>>>(lambda, n, thr, mask);
   ++ctx->launches;

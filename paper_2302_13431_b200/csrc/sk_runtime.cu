@@ -1066,9 +1066,14 @@ void run_eigh_subspace_batched(sk_ctx* ctx, const float2* grams, i64 batch, i64 
   int q_plan = 3;
   auto it_h = hint.find(n);
   if (it_h != hint.end()) q_plan = it_h->second.plan;
-  double2* A = ctx->arena.get<double2>("bk:A" + sfx, batch * nn);
+  // FP64 products in the Gauss 3M form on real planes [Re A][Im A][Re A + Im A]
+  // (one strided-batched DGEMM over 3 x batch matrices per product; the
+  // strided-batched ZGEMM it replaces ran four real products' worth)
+  double* A3 = ctx->arena.get<double>("bk:A3" + sfx, batch * 3 * nn);
+  double* V3 = ctx->arena.get<double>("bk:V3" + sfx, batch * 3 * nb);
+  double* T3 = ctx->arena.get<double>("bk:T3" + sfx, batch * 3 * nb);
   float* gcat = ctx->arena.get<float>("bk:gcat" + sfx, batch * 4 * nn);
-  promote_split_gram(ctx, grams, n, A, gcat, gcat + 2 * nn, batch, nn, 4 * nn);
+  promote_split3_gram(ctx, grams, n, A3, gcat, gcat + 2 * nn, batch, nn, 4 * nn);
   laps.lap("promote");
   double2* V = ctx->arena.get<double2>("bk:V" + sfx, batch * nb);
   double2* Y = ctx->arena.get<double2>("bk:Y" + sfx, batch * nb);
@@ -1091,6 +1096,15 @@ void run_eigh_subspace_batched(sk_ctx* ctx, const float2* grams, i64 batch, i64 
                  "ZgemmStridedBatched");
     ++ctx->lib_calls;
   };
+  auto product64 = [&](const double2* v, double2* y) {  // y = A v for every slice
+    const double d1 = 1.0, d0 = 0.0;
+    split3_block(ctx, v, nb, V3, batch, nb);
+    check_cublas(cublasDgemmStridedBatched(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(n), int(b), int(n), &d1, A3,
+                                           int(n), nn, V3, int(n), nb, &d0, T3, int(n), nb, int(3 * batch)),
+                 "DgemmStridedBatched(3M)");
+    ++ctx->lib_calls;
+    combine3_block(ctx, T3, nb, y, batch, nb);
+  };
   for (int i = 0; i < q_plan; ++i) {
     if (i + 2 < q_plan) {  // 3xTF32 steering step over the K-concatenated split Gram
       const float f1 = 1.f, f0 = 0.f;
@@ -1104,14 +1118,14 @@ void run_eigh_subspace_batched(sk_ctx* ctx, const float2* grams, i64 batch, i64 
       combine_block_cat(ctx, ccat, n, b, Y, batch, 8 * nb, nb);
       laps.lap("gemm32");
     } else {
-      zgemm_b(n, b, n, A, n, nn, V, n, nb, Y, n, nb);  // Y = A V (FP64)
+      product64(V, Y);  // Y = A V (FP64)
       laps.lap("gemm64");
     }
     std::swap(V, Y);
     cholqr64(ctx, V, n, i + 1 == q_plan ? 2 : 1, info + 1, batch, nb);
     laps.lap("orth");
   }
-  zgemm_b(n, b, n, A, n, nn, V, n, nb, Y, n, nb);
+  product64(V, Y);
   laps.lap("gemm64");
   gram64(ctx, V, Y, n, H, batch, nb);  // H = V^H A V
   laps.lap("rr_gram");

@@ -945,6 +945,39 @@ def test_batched_multislice_pinned_outputs(K):
         assert (outs[kind][2] == outs["dev"][2]).mean() > 0.9999
 
 
+def test_cold_contexts_read_complete_tables(K):
+    """Regression: the DFT / support tables a fresh context uploads must be
+    complete before its first kernels read them on the context's non-blocking
+    stream (a synchronous cudaMemcpy from pageable memory orders only the
+    legacy default stream: 4 of 60 cold multislice calls had a wrong slice).
+    Fresh contexts, first call each, every slice against warm single calls."""
+    import torch
+    from paper_2302_13431_b200 import phantom
+    case = phantom.generate("C3", slices=14, full_dims=(64, 64), channels=8)
+    spec = case.spec
+    cfg = K.PipelineConfig(kernel=spec.kernel, tau=spec.tau, nullspace_threshold=spec.nullspace_threshold,
+                           power_iters=spec.power_iters, grid=K.GRID_REDUCED,
+                           grid_pad=spec.grid_dims[0] - spec.calib[0])
+    s, q, full = case.calib.shape[0], spec.channels, spec.full_dims
+    warm = K.Context(0)
+    ref = [K.estimate_maps(K.Calib(case.calib[i], case.center_offset), full, cfg, warm, want_spectrum=False)
+           for i in range(s)]
+    cal = torch.from_numpy(case.calib).cuda()
+    maps = torch.empty((s, q) + full, dtype=torch.complex64, device="cuda")
+    lam = torch.empty((s,) + full, dtype=torch.float32, device="cuda")
+    mask = torch.empty((s,) + full, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    for rep in range(25):
+        ctx = K.Context(0)
+        K.api.estimate_maps_batched_device(ctx, cal.data_ptr(), s, spec.calib, case.center_offset, q, full, cfg,
+                                           maps.data_ptr(), lam.data_ptr(), mask.data_ptr())
+        m, l = maps.cpu().numpy(), lam.cpu().numpy()
+        for i in range(s):
+            assert PM.rel_fro(m[i], ref[i].maps) < 1e-5, (rep, i)
+            assert np.allclose(l[i], ref[i].lambda_min_map, rtol=1e-5, atol=1e-6), (rep, i)
+        ctx.close()
+
+
 def test_estimate_maps_baseline_3d(K, O):
     """Baseline preset (explicit Gram, dense per-voxel eigensolve, nullspace method) on a 3-D explicit grid."""
     sc3 = O.simulate(4, (20, 18, 16), 1, 9, noise_sigma=0.01, noise_seed=2)
