@@ -724,6 +724,7 @@ def test_batched_multislice_group_tail(K):
                                                 d_maps.data_ptr(), d_lam.data_ptr(), d_mask.data_ptr())
     maps, lam, mask = d_maps.cpu().numpy(), d_lam.cpu().numpy(), d_mask.cpu().numpy()
     assert not np.any(maps == 3 + 3j) and not np.any(lam == -1.0) and not np.any(mask == 7)
+    assert pv[0].stage_ms[0] == 0.0 and pv[0].stage_ms[2] > 0.0, list(pv[0].stage_ms)  # the grouped pass ran
     h_maps, h_lam, h_mask, h_info = K.api.estimate_maps_batched(case.calib, case.center_offset, full, cfg, ctx)
     for sl in range(s):
         assert int(pv[sl].nullspace_rank) == h_info[sl]["rank"], sl
@@ -943,6 +944,36 @@ def test_batched_multislice_pinned_outputs(K):
         assert PM.rel_fro(outs[kind][0], outs["dev"][0]) < 1e-6
         assert np.allclose(outs[kind][1], outs["dev"][1], rtol=1e-6, atol=1e-7)
         assert (outs[kind][2] == outs["dev"][2]).mean() > 0.9999
+
+
+def test_batched_multislice_group_tail_q16(K):
+    """The grouped K3-K5 pass at Q = 16 (K4 stack on the dense, unswizzled lo
+    tile and the 128-byte swizzled hi tile), 128 x 128 full grid from a 64 x 64
+    map grid, tau = 5 (n = 1296): against the lanes path on host outputs."""
+    import torch
+    from paper_2302_13431_b200 import phantom
+    case = phantom.generate("C3", slices=11, full_dims=(128, 128), channels=16)
+    spec = case.spec
+    cfg = K.PipelineConfig(kernel=spec.kernel, tau=5, nullspace_threshold=spec.nullspace_threshold,
+                           power_iters=20, grid=K.GRID_REDUCED, grid_pad=64 - spec.calib[0])
+    ctx = K.Context(0)
+    s, q, full = case.calib.shape[0], 16, (128, 128)
+    cal = torch.from_numpy(case.calib).cuda()
+    d_maps = torch.empty((s, q) + full, dtype=torch.complex64, device="cuda")
+    d_lam = torch.empty((s,) + full, dtype=torch.float32, device="cuda")
+    d_mask = torch.empty((s,) + full, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    for _ in range(2):
+        pv = K.api.estimate_maps_batched_device(ctx, cal.data_ptr(), s, spec.calib, case.center_offset, q, full, cfg,
+                                                d_maps.data_ptr(), d_lam.data_ptr(), d_mask.data_ptr())
+    # the grouped pass reports no per-slice Gram / nullspace time (they ran batched on the producer)
+    assert pv[0].stage_ms[0] == 0.0 and pv[0].stage_ms[2] > 0.0, list(pv[0].stage_ms)
+    h_maps, h_lam, h_mask, h_info = K.api.estimate_maps_batched(case.calib, case.center_offset, full, cfg, ctx)
+    for sl in range(s):
+        assert int(pv[sl].nullspace_rank) == h_info[sl]["rank"], sl
+    assert PM.rel_fro(d_maps.cpu().numpy(), h_maps) < 1e-6
+    assert np.allclose(d_lam.cpu().numpy(), h_lam, rtol=1e-6, atol=1e-7)
+    assert (d_mask.cpu().numpy() == h_mask).mean() > 0.9999
 
 
 def test_cold_contexts_read_complete_tables(K):
