@@ -187,26 +187,29 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int byt
 }
 
 // Persistent form of the FULL expand_col: the (c, s) table is staged once per
-// CTA, and the next column block's 2H+1 input rows (32 columns each) are
-// prefetched into shared memory with cp.async while the current block is
-// expanded (no per-CTA load bubble, no table reloads).
-template <int H>
+// CTA, and the next column block's 2H+1 input rows are prefetched into shared
+// memory with cp.async while the current block is expanded (no per-CTA load
+// bubble, no table reloads).  CPT columns per thread (a block is 32 CPT
+// columns wide): every (c, s) tap is a warp-wide shared-memory broadcast
+// feeding 4 CPT DFMAs; two columns per thread pay only for long tap rows
+// (launch_stage).
+template <int H, int CPT>
 __global__ void __launch_bounds__(256) expand_col_persist_kernel(const double2* __restrict__ in, i64 inner, int N,
                                                                  int jc, int items, i64 nblocks,
                                                                  const double2* __restrict__ cs, double2* out64,
                                                                  float2* hi, lo2* lo) {
-  constexpr int L = 2 * H + 1;
+  constexpr int L = 2 * H + 1, W = 32 * CPT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* tab = reinterpret_cast<double2*>(smem_raw);  // [items][H] (items = P + S1, computed by the host)
-  double2* xin = tab + items * H;                       // [2][L][32]
+  double2* xin = tab + items * H;                       // [2][L][W]
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
-  const i64 nchunk = (inner + 31) / 32;
+  const i64 nchunk = (inner + W - 1) / W;
   auto issue = [&](i64 cb, int buf) {
-    const i64 b = cb / nchunk, ib = (cb % nchunk) * 32;
-    for (int e = tid; e < L * 32; e += 256) {
-      const int l = e >> 5, c = e & 31;
+    const i64 b = cb / nchunk, ib = (cb % nchunk) * W;
+    for (int e = tid; e < L * W; e += 256) {
+      const int l = e / W, c = e % W;
       const bool ok = ib + c < inner;
-      cp_async16(xin + (buf * L + l) * 32 + c, in + (b * L + l) * inner + (ok ? ib + c : 0), ok ? 16 : 0);
+      cp_async16(xin + (buf * L + l) * W + c, in + (b * L + l) * inner + (ok ? ib + c : 0), ok ? 16 : 0);
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
@@ -229,35 +232,50 @@ __global__ void __launch_bounds__(256) expand_col_persist_kernel(const double2* 
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();  // xin[buf] (and, on the first pass, the table) visible to all
-    const i64 b = cb / nchunk, i = (cb % nchunk) * 32 + tx;
-    const double2* xb = xin + buf * L * 32 + tx;
-    const double2 x0 = xb[H * 32];
-    double2 S[H > 0 ? H : 1], D[H > 0 ? H : 1];
+    const i64 b = cb / nchunk, i0 = (cb % nchunk) * W + tx;  // the thread's columns: i0 + 32 k
+    double2 x0[CPT], S[CPT][H > 0 ? H : 1], D[CPT][H > 0 ? H : 1];
 #pragma unroll
-    for (int l = 0; l < H; ++l) {
-      const double2 xp = xb[(H + 1 + l) * 32], xm = xb[(H - 1 - l) * 32];
-      S[l] = make_double2(xp.x + xm.x, xp.y + xm.y);
-      D[l] = make_double2(xp.x - xm.x, xp.y - xm.y);
+    for (int k = 0; k < CPT; ++k) {
+      const double2* xb = xin + buf * L * W + tx + 32 * k;
+      x0[k] = xb[H * W];
+#pragma unroll
+      for (int l = 0; l < H; ++l) {
+        const double2 xp = xb[(H + 1 + l) * W], xm = xb[(H - 1 - l) * W];
+        S[k][l] = make_double2(xp.x + xm.x, xp.y + xm.y);
+        D[k][l] = make_double2(xp.x - xm.x, xp.y - xm.y);
+      }
     }
-    __syncthreads();  // every thread has its column: xin[buf] may be refilled (issued next iteration)
-    if (i >= inner) continue;
+    __syncthreads();  // every thread has its columns: xin[buf] may be refilled (issued next iteration)
+    if (i0 >= inner) continue;
     for (int t = ty; t < P + S1; t += 8) {
       const bool single = t >= P;
       const int jp = single ? t - P : p0 + t;
       const int jm = single ? -1 : 2 * jc - jp;
       const double2* row = tab + t * H;
-      double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
+      double ax[CPT], ay[CPT], bx[CPT], by[CPT];
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) ax[k] = ay[k] = bx[k] = by[k] = 0.0;
 #pragma unroll
       for (int l = 0; l < H; ++l) {
         const double2 tcs = row[l];
-        ax = fma(tcs.x, S[l].x, ax);
-        ay = fma(tcs.x, S[l].y, ay);
-        bx = fma(-tcs.y, D[l].y, bx);
-        by = fma(tcs.y, D[l].x, by);
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+          ax[k] = fma(tcs.x, S[k][l].x, ax[k]);
+          ay[k] = fma(tcs.x, S[k][l].y, ay[k]);
+          bx[k] = fma(-tcs.y, D[k][l].y, bx[k]);
+          by[k] = fma(tcs.y, D[k][l].x, by[k]);
+        }
       }
-      store_out(make_double2(x0.x + (ax + bx), x0.y + (ay + by)), out64, hi, lo, (b * N + jp) * inner + i);
-      if (jm >= 0 && jm < N && jm != jp)
-        store_out(make_double2(x0.x + (ax - bx), x0.y + (ay - by)), out64, hi, lo, (b * N + jm) * inner + i);
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        const i64 i = i0 + 32 * k;
+        if (i >= inner) continue;
+        store_out(make_double2(x0[k].x + (ax[k] + bx[k]), x0[k].y + (ay[k] + by[k])), out64, hi, lo,
+                  (b * N + jp) * inner + i);
+        if (jm >= 0 && jm < N && jm != jp)
+          store_out(make_double2(x0[k].x + (ax[k] - bx[k]), x0[k].y + (ay[k] - by[k])), out64, hi, lo,
+                    (b * N + jm) * inner + i);
+      }
     }
   }
 }
@@ -274,14 +292,26 @@ void launch_stage(sk_ctx* ctx, const double2* in, i64 batch, i64 inner, int N, i
     const int p0 = std::max(jc, 0), P = std::max(0, N - p0);
     const int S1 = jc > 0 ? std::max(0, std::min(std::min(jc, N), 2 * jc - N + 1)) : 0;
     const int items = P + S1;
-    const size_t pbytes = size_t(items) * (H > 0 ? H : 1) * sizeof(double2) +
-                          size_t(2 * (2 * H + 1) * 32) * sizeof(double2);
-    if (H > 0 && pbytes <= 110 * 1024) {  // persistent, two CTAs per SM (C2 last stage 218 -> 146 us)
-      set_smem_limit(reinterpret_cast<const void*>(expand_col_persist_kernel<H>), pbytes);
+    const size_t tbytes = size_t(items) * (H > 0 ? H : 1) * sizeof(double2);
+    const size_t pbytes = tbytes + size_t(2 * (2 * H + 1) * 32) * sizeof(double2);
+    const size_t pbytes2 = tbytes + size_t(2 * (2 * H + 1) * 64) * sizeof(double2);
+    if (H >= 12 && inner % 64 == 0 && pbytes2 <= 200 * 1024) {
+      // two columns per thread, each (c, s) broadcast feeding eight DFMAs, for the long tap
+      // rows only: C5 (H = 12) field 3.19 -> 2.95 ms; with H <= 10 the halved occupancy costs
+      // more than the broadcasts saved (C2 0.241 -> 0.258 ms, C4 2.49 -> 2.61 ms, C3 +6%)
+      set_smem_limit(reinterpret_cast<const void*>(expand_col_persist_kernel<H, 2>), pbytes2);
+      const i64 nblocks = inner / 64 * batch;
+      int per_sm = 1;
+      SKB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expand_col_persist_kernel<H, 2>, 256, pbytes2));
+      const unsigned grid = unsigned(std::min<i64>(nblocks, i64(std::max(per_sm, 1)) * ctx->sm_count));
+      expand_col_persist_kernel<H, 2><<<grid, dim3{32, 8}, pbytes2, ctx->stream>>>(in, inner, N, jc, items, nblocks,
+                                                                                 cs, out64, hi, lo);
+    } else if (H > 0 && pbytes <= 110 * 1024) {  // persistent, two CTAs per SM (C2 last stage 218 -> 146 us)
+      set_smem_limit(reinterpret_cast<const void*>(expand_col_persist_kernel<H, 1>), pbytes);
       const i64 nblocks = gx;
       const unsigned grid = unsigned(std::min<i64>(nblocks, 2 * ctx->sm_count));
-      expand_col_persist_kernel<H><<<grid, dim3{32, 8}, pbytes, ctx->stream>>>(in, inner, N, jc, items, nblocks, cs,
-                                                                              out64, hi, lo);
+      expand_col_persist_kernel<H, 1><<<grid, dim3{32, 8}, pbytes, ctx->stream>>>(in, inner, N, jc, items, nblocks,
+                                                                                 cs, out64, hi, lo);
     } else if (full_bytes <= 110 * 1024) {  // two CTAs per SM still fit
       set_smem_limit(reinterpret_cast<const void*>(expand_col_kernel<H, true>), full_bytes);
       expand_col_kernel<H, true><<<dim3{unsigned(gx)}, dim3{32, 8}, full_bytes, ctx->stream>>>(in, inner, N, jc, cs,
