@@ -1714,6 +1714,9 @@ bool group_tail_eligible(const sk_config* cfg, const Dims& cd, const Dims& fd, i
   if (grid == fd || !interp_fft_ok(grid, fd)) return false;
   const i64 nl = grid[size_t(nd - 1)];
   if (fd[size_t(nd - 1)] != 2 * nl || q * nl > 4096) return false;
+  // a 32-slice group's planes (12 bytes per packed entry) stay within 16 GiB
+  const double group_bytes = 32.0 * double(q * (q + 1) / 2) * double(numel(grid)) * 12.0;
+  if (group_bytes > 16.0 * 1024 * 1024 * 1024) return false;
   return spectral_fold_smem(s.nd, s.tau, 64, int(q)) <= 200 * 1024;
 }
 
