@@ -2714,6 +2714,9 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
   std::condition_variable cv;
   i64 groups_ready = 0;
   bool abort_k2 = false;
+  // a lane or the group consumer stopped on an error: nobody may wait for its
+  // share of a group any more (the producer returns, the other workers stop)
+  bool worker_failed = false;
   std::vector<i64> done(size_t(groups), 0);
   auto group_size = [&](i64 g) { return gstart[size_t(g + 1)] - gstart[size_t(g)]; };
   auto group_of = [&](i64 s) { return i64(std::upper_bound(gstart.begin(), gstart.end(), s) - gstart.begin()) - 1; };
@@ -2727,12 +2730,15 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
       if (bk2) {
         g = group_of(s);
         std::unique_lock<std::mutex> lk(mu);
-        cv.wait(lk, [&] { return groups_ready > g || abort_k2; });
-        if (abort_k2) break;
+        cv.wait(lk, [&] { return groups_ready > g || abort_k2 || worker_failed; });
+        if (abort_k2 || worker_failed) break;
         lk.unlock();
         if (cudaStreamWaitEvent(sub->stream, gev[size_t(g)], 0) != cudaSuccess) {
           rcs[size_t(lane)] = SK_ERR_CUDA;
           errs[size_t(lane)] = "multislice: waiting on the batched nullspace failed";
+          std::lock_guard<std::mutex> lk2(mu);
+          worker_failed = true;
+          cv.notify_all();
           break;
         }
         if (has_basis[size_t(s)]) basis = &bases[size_t(s)];
@@ -2749,6 +2755,11 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
       if (rc != SK_OK) {
         rcs[size_t(lane)] = rc;
         errs[size_t(lane)] = sk_last_error();
+        if (bk2) {
+          std::lock_guard<std::mutex> lk(mu);
+          worker_failed = true;
+          cv.notify_all();
+        }
         break;
       }
     }
@@ -2769,12 +2780,15 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
     for (i64 g = 0; g < groups; ++g) {
       {
         std::unique_lock<std::mutex> lk(mu);
-        cv.wait(lk, [&] { return groups_ready > g || abort_k2; });
-        if (abort_k2) break;
+        cv.wait(lk, [&] { return groups_ready > g || abort_k2 || worker_failed; });
+        if (abort_k2 || worker_failed) break;
       }
       if (cudaStreamWaitEvent(sub->stream, gev[size_t(g)], 0) != cudaSuccess) {
         rcs[0] = SK_ERR_CUDA;
         errs[0] = "multislice: waiting on the batched nullspace failed";
+        std::lock_guard<std::mutex> lk2(mu);
+        worker_failed = true;
+        cv.notify_all();
         break;
       }
       const i64 s0 = gstart[size_t(g)], gs = group_size(g);
@@ -2811,6 +2825,9 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
       if (rc != SK_OK) {
         rcs[0] = rc;
         errs[0] = sk_last_error();
+        std::lock_guard<std::mutex> lk(mu);
+        worker_failed = true;
+        cv.notify_all();
         break;
       }
     }
@@ -2826,7 +2843,8 @@ int sk_estimate_maps_batched(sk_ctx* ctx, int64_t slices, int ndim, const int64_
       for (i64 g = 0; g < groups; ++g) {
         {
           std::unique_lock<std::mutex> lk(mu);
-          cv.wait(lk, [&] { return g < 2 || done[size_t(g - 2)] == group_size(g - 2); });
+          cv.wait(lk, [&] { return g < 2 || done[size_t(g - 2)] == group_size(g - 2) || worker_failed; });
+          if (worker_failed) return;  // its error is reported below
         }
         const int set = int(g % 2);
         const i64 gs = group_size(g), s0 = gstart[size_t(g)];

@@ -976,6 +976,43 @@ def test_batched_multislice_group_tail_q16(K):
     assert (d_mask.cpu().numpy() == h_mask).mean() > 0.9999
 
 
+@pytest.mark.timeout(300)
+def test_batched_multislice_failed_slice_returns(K):
+    """A slice that cannot be solved (all-zero calibration) inside a multislice
+    call: the call must return the slice's error on both consumers (grouped
+    pass on device outputs, lanes on host outputs) -- the producer and the
+    other workers stop instead of waiting for the failed worker's group."""
+    import torch
+    from paper_2302_13431_b200 import phantom
+    case = phantom.generate("C3", slices=40)
+    spec = case.spec
+    cfg = K.PipelineConfig(kernel=spec.kernel, tau=spec.tau, nullspace_threshold=spec.nullspace_threshold,
+                           power_iters=spec.power_iters, grid=K.GRID_REDUCED,
+                           grid_pad=spec.grid_dims[0] - spec.calib[0])
+    ctx = K.Context(0)
+    s, q, full = case.calib.shape[0], spec.channels, spec.full_dims
+    good = torch.from_numpy(case.calib).cuda()
+    d_maps = torch.empty((s, q) + full, dtype=torch.complex64, device="cuda")
+    d_lam = torch.empty((s,) + full, dtype=torch.float32, device="cuda")
+    d_mask = torch.empty((s,) + full, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+    # settle the step plan on good data first (the failure then happens inside a batched group)
+    K.api.estimate_maps_batched_device(ctx, good.data_ptr(), s, spec.calib, case.center_offset, q, full, cfg,
+                                       d_maps.data_ptr(), d_lam.data_ptr(), d_mask.data_ptr())
+    bad = case.calib.copy()
+    bad[20] = 0
+    cal = torch.from_numpy(bad).cuda()
+    torch.cuda.synchronize()
+    with pytest.raises(K.api.SensKitError):
+        K.api.estimate_maps_batched_device(ctx, cal.data_ptr(), s, spec.calib, case.center_offset, q, full, cfg,
+                                           d_maps.data_ptr(), d_lam.data_ptr(), d_mask.data_ptr())
+    with pytest.raises(K.api.SensKitError):
+        K.api.estimate_maps_batched(bad, case.center_offset, full, cfg, ctx)
+    # the context still works
+    K.api.estimate_maps_batched_device(ctx, good.data_ptr(), s, spec.calib, case.center_offset, q, full, cfg,
+                                       d_maps.data_ptr(), d_lam.data_ptr(), d_mask.data_ptr())
+
+
 def test_cold_contexts_read_complete_tables(K):
     """Regression: the DFT / support tables a fresh context uploads must be
     complete before its first kernels read them on the context's non-blocking
