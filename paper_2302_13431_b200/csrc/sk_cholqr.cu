@@ -59,6 +59,35 @@ __device__ __forceinline__ double2 cfma_conj_rev(double2 acc, double2 a, double2
   return acc;
 }
 
+// Element (rr, col) of the n x m block Y held as the K-concatenated 3xTF32
+// GEMM result C' (2n x 4m floats): C = C'[:, :2m] + C'[:, 2m:], Y = (C11 -
+// C22) + i (C12 + C21) (as combine_block_cat, sk_misc.cu).
+__device__ __forceinline__ double2 cat_load(const float* __restrict__ c, i64 n, int m, i64 rr, int col) {
+  const i64 ld = 2 * n, h = 2 * i64(m) * ld;
+  const float* p = c + rr + i64(col) * ld;
+  const float* q = p + i64(m) * ld;
+  const double c11 = double(p[0]) + double(p[h]);
+  const double c21 = double(p[n]) + double(p[h + n]);
+  const double c12 = double(q[0]) + double(q[h]);
+  const double c22 = double(q[n]) + double(q[h + n]);
+  return make_double2(c11 - c22, c12 + c21);
+}
+// The 3xTF32 operand V' = [[V_hi, V_lo]; [0, V_hi]] entries of element (rr, col) (as split_block_cat).
+__device__ __forceinline__ void cat_store(float* __restrict__ vc, i64 n, int m, i64 rr, int col, double2 x) {
+  const i64 ld = 2 * n;
+  float h, l;
+  tf32_split(float(x.x), h, l);
+  vc[rr + i64(col) * ld] = h;
+  vc[n + rr + i64(col) * ld] = 0.f;
+  vc[rr + (2 * i64(m) + col) * ld] = l;
+  vc[n + rr + (2 * i64(m) + col) * ld] = h;
+  tf32_split(float(x.y), h, l);
+  vc[rr + (i64(m) + col) * ld] = h;
+  vc[n + rr + (i64(m) + col) * ld] = 0.f;
+  vc[rr + (3 * i64(m) + col) * ld] = l;
+  vc[n + rr + (3 * i64(m) + col) * ld] = h;
+}
+
 // 16 x 16 tiles of the B x B result, T = B / 16 per side: tile t -> (ti, tj);
 // HERM lists the lower tiles row by row, else all T^2.
 template <int B, bool HERM>
@@ -80,12 +109,14 @@ constexpr int n_tiles() { return HERM ? (B / 16) * (B / 16 + 1) / 2 : (B / 16) *
 template <int B, bool HERM>
 __global__ void __cluster_dims__(kQCluster, 1, 1) __launch_bounds__(kQGramThreads)
     gram64_kernel(const double2* __restrict__ x, const double2* __restrict__ y, i64 n, int rows,
-                  double2* __restrict__ cpart, unsigned* __restrict__ counter, double2* __restrict__ out, i64 sx) {
+                  double2* __restrict__ cpart, unsigned* __restrict__ counter, double2* __restrict__ out, i64 sx,
+                  const float* __restrict__ ccat, i64 sc) {
   constexpr int NT = n_tiles<B, HERM>();
   constexpr int kQ = B, kQLd = B + 1;
   // batch (multislice K2): slice blockIdx.y, its own partials, ticket and output
   x += i64(blockIdx.y) * sx;
   y += i64(blockIdx.y) * sx;
+  if (ccat) ccat += i64(blockIdx.y) * sc;  // HERM only: X taken from the concatenated GEMM result
   out += i64(blockIdx.y) * kQ * kQ;
   cpart += i64(blockIdx.y) * (gridDim.x / kQCluster) * NT * kQGramThreads;
   counter += blockIdx.y;
@@ -111,7 +142,8 @@ __global__ void __cluster_dims__(kQCluster, 1, 1) __launch_bounds__(kQGramThread
       const int e = tid + kQGramThreads * u;
       const int k = e % kQStage, col = e / kQStage;  // lanes along rows: column-major X (coalesced)
       const i64 rr = rs + k;
-      v[u] = rr < row1 ? x[rr + i64(col) * n] : make_double2(0.0, 0.0);
+      v[u] = rr < row1 ? (HERM && ccat ? cat_load(ccat, n, kQ, rr, col) : x[rr + i64(col) * n])
+                       : make_double2(0.0, 0.0);
       if (!HERM) w[u] = rr < row1 ? y[rr + i64(col) * n] : make_double2(0.0, 0.0);
     }
     __syncthreads();
@@ -345,9 +377,13 @@ __global__ void __launch_bounds__(chol_threads<B>()) chol64_kernel(const double2
 template <int B>
 __global__ void __launch_bounds__(1024) trsm64_kernel(double2* __restrict__ x, i64 n, int rows,
                                                       const double2* __restrict__ l,
-                                                      const double2* __restrict__ dinv, i64 sx) {
+                                                      const double2* __restrict__ dinv, i64 sx,
+                                                      const float* __restrict__ ccat, i64 sc,
+                                                      float* __restrict__ vcat, i64 svc) {
   constexpr int kQ = B, kQLd = B + 1, NB = B / 16;
   x += i64(blockIdx.y) * sx;  // batch: slice blockIdx.y
+  if (ccat) ccat += i64(blockIdx.y) * sc;
+  if (vcat) vcat += i64(blockIdx.y) * svc;
   l += i64(blockIdx.y) * kQ * kQ;
   dinv += i64(blockIdx.y) * NB * 256;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -391,7 +427,9 @@ __global__ void __launch_bounds__(1024) trsm64_kernel(double2* __restrict__ x, i
     for (int u = 0; u < 4; ++u) {
       const int e = e0 + tid + u * nt;
       const int rr = e % rows, col = e / rows;
-      v[u] = (e < rows * kQ && rr < nr) ? x[row0 + rr + i64(col) * n] : make_double2(0.0, 0.0);
+      v[u] = (e < rows * kQ && rr < nr)
+                 ? (ccat ? cat_load(ccat, n, kQ, row0 + rr, col) : x[row0 + rr + i64(col) * n])
+                 : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -434,7 +472,9 @@ __global__ void __launch_bounds__(1024) trsm64_kernel(double2* __restrict__ x, i
   __syncthreads();
   for (int e = tid; e < nr * kQ; e += nt) {
     const int rr = e % nr, col = e / nr;
-    x[row0 + rr + i64(col) * n] = Xs[rr * kQLd + col];
+    const double2 v = Xs[rr * kQLd + col];
+    x[row0 + rr + i64(col) * n] = v;
+    if (vcat) cat_store(vcat, n, kQ, row0 + rr, col, v);
   }
 }
 
@@ -452,7 +492,8 @@ unsigned* gram_counter(sk_ctx* ctx) {
 }
 
 template <int B, bool HERM>
-void launch_gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, double2* out, i64 batch = 1, i64 sx = 0) {
+void launch_gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, double2* out, i64 batch = 1, i64 sx = 0,
+                   const float* ccat = nullptr, i64 sc = 0) {
   if (batch > kMaxBatch) fail(SK_ERR_DIM, "gram64: batch too large");
   constexpr int NT = n_tiles<B, HERM>();
   // one wave of CTAs over the whole batch: ~sm_count CTAs per slice alone,
@@ -468,13 +509,13 @@ void launch_gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, doubl
   const size_t smem = size_t((HERM ? 1 : 2) * kQStage * (B + 1) + NT * kQGramThreads) * sizeof(double2);
   set_smem_limit(reinterpret_cast<const void*>(gram64_kernel<B, HERM>), smem);
   gram64_kernel<B, HERM><<<dim3(unsigned(ctas), unsigned(batch)), kQGramThreads, smem, ctx->stream>>>(
-      x, y, n, rows, cpart, gram_counter(ctx), out, sx);
+      x, y, n, rows, cpart, gram_counter(ctx), out, sx, ccat, sc);
   ++ctx->launches;
   SKB_LAUNCH("gram64_kernel");
 }
 
 template <int B>
-void cholqr_blk(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag, i64 batch, i64 sx) {
+void cholqr_blk(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag, i64 batch, i64 sx, const CatIO& io) {
   constexpr int NB = B / 16;
   double2* S = ctx->arena.get<double2>("cq:S", batch * B * B);
   double2* L = ctx->arena.get<double2>("cq:L", batch * B * B);
@@ -490,12 +531,14 @@ void cholqr_blk(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag, i64 batch
   const size_t smem_t = size_t(B * (B + 1) + NB * 16 * 17 + rows * (B + 1)) * sizeof(double2);
   set_smem_limit(reinterpret_cast<const void*>(trsm64_kernel<B>), smem_t);
   for (int p = 0; p < passes; ++p) {
-    launch_gram64<B, true>(ctx, x, x, n, S, batch, sx);
+    const float* cc = p == 0 ? io.ccat : nullptr;           // the first pass reads the concatenated product
+    float* vc = p + 1 == passes ? io.vcat : nullptr;        // the last pass also writes the next split operand
+    launch_gram64<B, true>(ctx, x, x, n, S, batch, sx, cc, io.sc);
     chol64_kernel<B><<<unsigned(batch), chol_threads<B>(), smem_c, ctx->stream>>>(S, L, D, flag);
     ++ctx->launches;
     SKB_LAUNCH("chol64_kernel");
     trsm64_kernel<B><<<dim3(unsigned((n + rows - 1) / rows), unsigned(batch)), threads, smem_t, ctx->stream>>>(
-        x, n, rows, L, D, sx);
+        x, n, rows, L, D, sx, cc, io.sc, vc, io.svc);
     ++ctx->launches;
     SKB_LAUNCH("trsm64_kernel");
   }
@@ -519,14 +562,14 @@ void gram_blk(sk_ctx* ctx, int b, const double2* x, const double2* y, i64 n, dou
     launch_gram64<32, false>(ctx, x, y, n, out);
 }
 
-void cholqr64(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag, i64 batch, i64 sx) {
-  cholqr_blk<64>(ctx, x, n, passes, flag, batch, sx);
+void cholqr64(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag, i64 batch, i64 sx, const CatIO& io) {
+  cholqr_blk<64>(ctx, x, n, passes, flag, batch, sx, io);
 }
 
-void cholqr_b(sk_ctx* ctx, int b, double2* x, i64 n, int passes, int* flag) {
-  if (b == 64) return cholqr_blk<64>(ctx, x, n, passes, flag, 1, 0);
+void cholqr_b(sk_ctx* ctx, int b, double2* x, i64 n, int passes, int* flag, const CatIO& io) {
+  if (b == 64) return cholqr_blk<64>(ctx, x, n, passes, flag, 1, 0, io);
   if (b != 32) fail(SK_ERR_UNSUPPORTED, "cholqr_b: block width must be 32 or 64");
-  cholqr_blk<32>(ctx, x, n, passes, flag, 1, 0);
+  cholqr_blk<32>(ctx, x, n, passes, flag, 1, 0, io);
 }
 
 }  // namespace skb

@@ -30,6 +30,18 @@
 
 namespace skb {
 
+// 3xTF32 split: x = hi + lo with hi = tf32(x), lo = tf32(x - hi).
+#ifdef __CUDACC__
+__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
+  unsigned h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  hi = __uint_as_float(h);
+  unsigned l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
+  lo = __uint_as_float(l);
+}
+#endif
+
 using i64 = std::int64_t;
 using Dims = std::vector<i64>;
 
@@ -377,10 +389,23 @@ void cross_gram(sk_ctx* ctx, const double2* x, const double2* y, i64 n, int b, d
 // (one-CTA Cholesky; a non-positive pivot raises *flag).
 void gram64(sk_ctx* ctx, const double2* x, const double2* y, i64 n, double2* out, i64 batch = 1, i64 sx = 0);
 // flag: per-slice int at flag[3 * slice] (the nullspace info triple's flag slot)
-void cholqr64(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag, i64 batch = 1, i64 sx = 0);
+// CatIO (3xTF32 steering steps): the CholQR kernels can take their input block
+// straight from the K-concatenated GEMM result C' (ccat, 2n x 4b floats per
+// slice: Y = C'[:, :2b] + C'[:, 2b:] combined on load) instead of a formed
+// c128 block, and the solve can write, beside the c128 result, its 3xTF32
+// split operand V' for the next step's GEMM (vcat) -- the separate combine
+// and split passes of a steering step disappear.
+struct CatIO {
+  const float* ccat = nullptr;  // first pass loads from it (x is then output only)
+  i64 sc = 0;                   // slice stride of ccat (floats)
+  float* vcat = nullptr;        // last pass also writes the split block here
+  i64 svc = 0;                  // slice stride of vcat (floats)
+};
+void cholqr64(sk_ctx* ctx, double2* x, i64 n, int passes, int* flag, i64 batch = 1, i64 sx = 0,
+              const CatIO& io = CatIO());
 // the same kernels at block width b in {32, 64} (single slice)
 void gram_blk(sk_ctx* ctx, int b, const double2* x, const double2* y, i64 n, double2* out);
-void cholqr_b(sk_ctx* ctx, int b, double2* x, i64 n, int passes, int* flag);
+void cholqr_b(sk_ctx* ctx, int b, double2* x, i64 n, int passes, int* flag, const CatIO& io = CatIO());
 // One-CTA Hermitian eigensolver (sk_eig.cu) for b <= 64: eigenvalues ascending
 // into w, eigenvectors overwrite H (column-major); info[0] = 1 on a
 // non-finite result.  Returns false (nothing launched) for larger b.

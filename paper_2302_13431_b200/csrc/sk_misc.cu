@@ -398,15 +398,6 @@ double projection_residual_value(sk_ctx* ctx, const float2* img, const float2* m
 // 3xTF32 split of complex operands for the K2 FP32 products (tensor cores):
 // x = hi + lo with hi = tf32(x), lo = tf32(x - hi); complex n x m (column-major)
 // becomes real [Re; Im] (2n x m) for the Gram and [Re, Im] (n x 2m) for the block.
-__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
-  unsigned h;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  hi = __uint_as_float(h);
-  unsigned l;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
-  lo = __uint_as_float(l);
-}
-
 // K-concatenated 3xTF32 operand: V' (2n x 4m, column-major) = [[V_hi, V_lo]; [0, V_hi]]
 // so that [A_hi | A_lo] V' = [A_hi V_hi, A_hi V_lo + A_lo V_hi] in ONE GEMM that
 // reads the split Gram once ([Re, Im] column blocks of width m inside each half).

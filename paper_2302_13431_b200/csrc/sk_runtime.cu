@@ -626,10 +626,11 @@ void small_heev(sk_ctx* ctx, double2* H, i64 b, double* w, int* d_info, double f
 // lane-pair TRSM: faster once graphs hide the library's host cost).  Larger
 // blocks: cuBLAS HERK + POTRF + TRSM with a synchronous check.  Returns false
 // only on a detected (synchronous path) failure; the other paths raise `flag`.
-bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int passes = 2) {
+bool orth(sk_ctx* ctx, double2*& x, double2*& tmp, i64 n, i64 b, int* flag, int passes = 2,
+          const CatIO& io = CatIO()) {
   (void)tmp;
   if ((b == 64 && n >= 1024) || (b == 32 && n >= 128)) {
-    cholqr_b(ctx, int(b), x, n, passes, flag);
+    cholqr_b(ctx, int(b), x, n, passes, flag, io);
     return true;
   }
   if (b > 256) {
@@ -866,20 +867,37 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
     // so in steady state (per-size hint fixed) it is replayed as a CUDA graph.
     bool body_ok = true;
     auto body = [&]() {
+      // With the own CholQR kernels a steering step is GEMM + CholQR only: the
+      // kernels read the concatenated product directly and the solve writes
+      // the next step's split operand (CatIO) -- no combine / split passes
+      // between them (nine launches fewer per C2 call; K2 time C1 0.47 -> 0.45 ms,
+      // C4 2.63 -> 2.61 ms, C2 unchanged: the small passes were not on the critical path).
+      const bool cat_io = (b == 64 && n >= 1024) || (b == 32 && n >= 128);
+      bool have_split = false;
       for (int i = 0; i < q_plan; ++i) {
+        CatIO io;
         if (i + 2 < q_plan) {
           // 3xTF32 on tensor cores: [A_hi | A_lo] (2n x 2n) [[V_hi, V_lo]; [0, V_hi]]
           // (2n x 4b), the split Gram read once per step.
           const float one = 1.f, zero = 0.f;
           float* vcat = ctx->arena.get<float>("ss:vcat", 2 * n * 4 * bcap);
           float* ccat = ctx->arena.get<float>("ss:ccat", 2 * n * 4 * bcap);
-          split_block_cat_tf32(ctx, V, n, b, vcat);
+          if (!have_split) split_block_cat_tf32(ctx, V, n, b, vcat);
           check_cublas(cublasGemmEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(2 * n), int(4 * b), int(2 * n), &one,
                                     ghi, CUDA_R_32F, int(2 * n), vcat, CUDA_R_32F, int(2 * n), &zero, ccat,
                                     CUDA_R_32F, int(2 * n), CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT),
                        "GemmEx(3xTF32 cat)");
           ++ctx->lib_calls;
-          combine_block_cat(ctx, ccat, n, b, Y);
+          have_split = false;
+          if (cat_io) {
+            io.ccat = ccat;
+            if ((i + 1) + 2 < q_plan) {  // the next step is a steering step too
+              io.vcat = vcat;
+              have_split = true;
+            }
+          } else {
+            combine_block_cat(ctx, ccat, n, b, Y);
+          }
           laps.lap("gemm32");
         } else {
           zgemm(ctx, CUBLAS_OP_N, CUBLAS_OP_N, n, b, n, A, n, V, n, Y, n);  // Y = A V
@@ -888,7 +906,7 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
         std::swap(V, Y);
         // Only the span matters between Rayleigh-Ritz steps: one CholQR pass
         // (orthogonality ~ kappa^2 eps) except before the projection.
-        if (!orth(ctx, V, T, n, b, flag, i + 1 == q_plan ? 2 : 1)) {
+        if (!orth(ctx, V, T, n, b, flag, i + 1 == q_plan ? 2 : 1, io)) {
           body_ok = false;
           return;
         }
@@ -1105,24 +1123,33 @@ void run_eigh_subspace_batched(sk_ctx* ctx, const float2* grams, i64 batch, i64 
     ++ctx->lib_calls;
     combine3_block(ctx, T3, nb, y, batch, nb);
   };
+  bool have_split = false;
   for (int i = 0; i < q_plan; ++i) {
+    CatIO io;
     if (i + 2 < q_plan) {  // 3xTF32 steering step over the K-concatenated split Gram
       const float f1 = 1.f, f0 = 0.f;
-      split_block_cat_tf32(ctx, V, n, b, vcat, batch, nb, 8 * nb);
+      if (!have_split) split_block_cat_tf32(ctx, V, n, b, vcat, batch, nb, 8 * nb);
       check_cublas(cublasGemmStridedBatchedEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(2 * n), int(4 * b),
                                               int(2 * n), &f1, gcat, CUDA_R_32F, int(2 * n), 4 * nn, vcat, CUDA_R_32F,
                                               int(2 * n), 8 * nb, &f0, ccat, CUDA_R_32F, int(2 * n), 8 * nb,
                                               int(batch), CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT),
                    "GemmStridedBatchedEx(3xTF32 cat)");
       ++ctx->lib_calls;
-      combine_block_cat(ctx, ccat, n, b, Y, batch, 8 * nb, nb);
+      // the CholQR kernels read the concatenated product and write the next split operand (CatIO)
+      io.ccat = ccat;
+      io.sc = 8 * nb;
+      have_split = (i + 1) + 2 < q_plan;
+      if (have_split) {
+        io.vcat = vcat;
+        io.svc = 8 * nb;
+      }
       laps.lap("gemm32");
     } else {
       product64(V, Y);  // Y = A V (FP64)
       laps.lap("gemm64");
     }
     std::swap(V, Y);
-    cholqr64(ctx, V, n, i + 1 == q_plan ? 2 : 1, info + 1, batch, nb);
+    cholqr64(ctx, V, n, i + 1 == q_plan ? 2 : 1, info + 1, batch, nb, io);
     laps.lap("orth");
   }
   product64(V, Y);
