@@ -794,6 +794,17 @@ void run_graphed(sk_ctx* ctx, bool allowed, const RoundKey& key, double2*& V, do
   SKB_CUDA(cudaGraphLaunch(ctx->rounds[key].exec, ctx->stream));  // capture recorded, not ran, the round
 }
 
+// FP64 steps at the end of a round, before the (FP64) projection product; the
+// steps before them are 3xTF32 steering steps.  Two for the single solver at
+// b = 64 / 96; one where an FP64 step costs much more than a steering step and
+// the same step count still converges: the batched solver (C3: iterations
+// unchanged at 6, worst residual 1.1e-11 against the 3e-10 tolerance, 50.3 ->
+// 48.0 ms per 128 slices) and the 32-column block of small Grams (C1 K2 0.45
+// -> 0.41 ms).  Measured the other way on C2: one FP64 step needs a ninth
+// iteration (two more steering steps for one FP64 step saved, K2 1.27 -> 1.30
+// ms).  The convergence test is the same either way.
+constexpr int kFp64StepsSingle = 2, kFp64StepsSmall = 1, kFp64StepsBatched = 1;
+
 bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, bool certify, Eig& e) {
   PhaseLaps laps(ctx);
   e = Eig();
@@ -873,10 +884,11 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
       // between them (nine launches fewer per C2 call; K2 time C1 0.47 -> 0.45 ms,
       // C4 2.63 -> 2.61 ms, C2 unchanged: the small passes were not on the critical path).
       const bool cat_io = (b == 64 && n >= 1024) || (b == 32 && n >= 128);
+      const int nf64 = b == 32 ? kFp64StepsSmall : kFp64StepsSingle;
       bool have_split = false;
       for (int i = 0; i < q_plan; ++i) {
         CatIO io;
-        if (i + 2 < q_plan) {
+        if (i + nf64 < q_plan) {
           // 3xTF32 on tensor cores: [A_hi | A_lo] (2n x 2n) [[V_hi, V_lo]; [0, V_hi]]
           // (2n x 4b), the split Gram read once per step.
           const float one = 1.f, zero = 0.f;
@@ -891,7 +903,7 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
           have_split = false;
           if (cat_io) {
             io.ccat = ccat;
-            if ((i + 1) + 2 < q_plan) {  // the next step is a steering step too
+            if ((i + 1) + nf64 < q_plan) {  // the next step is a steering step too
               io.vcat = vcat;
               have_split = true;
             }
@@ -1126,7 +1138,7 @@ void run_eigh_subspace_batched(sk_ctx* ctx, const float2* grams, i64 batch, i64 
   bool have_split = false;
   for (int i = 0; i < q_plan; ++i) {
     CatIO io;
-    if (i + 2 < q_plan) {  // 3xTF32 steering step over the K-concatenated split Gram
+    if (i + kFp64StepsBatched < q_plan) {  // 3xTF32 steering step over the K-concatenated split Gram
       const float f1 = 1.f, f0 = 0.f;
       if (!have_split) split_block_cat_tf32(ctx, V, n, b, vcat, batch, nb, 8 * nb);
       check_cublas(cublasGemmStridedBatchedEx(ctx->cublas, CUBLAS_OP_N, CUBLAS_OP_N, int(2 * n), int(4 * b),
@@ -1138,7 +1150,7 @@ void run_eigh_subspace_batched(sk_ctx* ctx, const float2* grams, i64 batch, i64 
       // the CholQR kernels read the concatenated product and write the next split operand (CatIO)
       io.ccat = ccat;
       io.sc = 8 * nb;
-      have_split = (i + 1) + 2 < q_plan;
+      have_split = (i + 1) + kFp64StepsBatched < q_plan;
       if (have_split) {
         io.vcat = vcat;
         io.svc = 8 * nb;
