@@ -799,8 +799,8 @@ void run_graphed(sk_ctx* ctx, bool allowed, const RoundKey& key, double2*& V, do
 // b = 64 / 96; one where an FP64 step costs much more than a steering step and
 // the same step count still converges: the batched solver (C3: iterations
 // unchanged at 6, worst residual 1.1e-11 against the 3e-10 tolerance, 50.3 ->
-// 48.0 ms per 128 slices) and the 32-column block of small Grams (C1 K2 0.45
-// -> 0.41 ms).  Measured the other way on C2: one FP64 step needs a ninth
+// 48.0 ms per 128 slices), the 32-column block of small Grams (C1 K2 0.45
+// -> 0.41 ms) and the wide blocks of big Grams (C5, b = 96: K2 6.8 -> 6.5 ms).  Measured the other way on C2: one FP64 step needs a ninth
 // iteration (two more steering steps for one FP64 step saved, K2 1.27 -> 1.30
 // ms).  The convergence test is the same either way.
 constexpr int kFp64StepsSingle = 2, kFp64StepsSmall = 1, kFp64StepsBatched = 1;
@@ -884,7 +884,7 @@ bool run_eigh_subspace(sk_ctx* ctx, const float2* gram, i64 n, double ratio, boo
       // between them (nine launches fewer per C2 call; K2 time C1 0.47 -> 0.45 ms,
       // C4 2.63 -> 2.61 ms, C2 unchanged: the small passes were not on the critical path).
       const bool cat_io = (b == 64 && n >= 1024) || (b == 32 && n >= 128);
-      const int nf64 = b == 32 ? kFp64StepsSmall : kFp64StepsSingle;
+      const int nf64 = b == 64 ? kFp64StepsSingle : kFp64StepsSmall;  // (b = 32, and b >= 96: see above)
       bool have_split = false;
       for (int i = 0; i < q_plan; ++i) {
         CatIO io;
